@@ -1,0 +1,100 @@
+/* oracle/mdot_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, fp64 CPU oracle of the MDOT-PNCG hot path (arxiv 2307.08507).
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load it.  It shares no code, header, table or
+ * constant with the CUDA library (paper_2307_08507_b200/, include/mdot.h).
+ *
+ * Readings of the paper that this oracle takes are the SURVEY.md section 8(c)
+ * "Z" readings, restated in DESIGN.md; each function cites the passage it
+ * follows as PAPER.md:<line> (section / equation / algorithm).
+ */
+#ifndef MDOT_ORACLE_H
+#define MDOT_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_DENSE_F32 = 0, ORC_SQEUCLID_F32 = 1, ORC_DENSE_F64 = 2 };
+enum { ORC_PNCG = 0, ORC_SINKHORN = 1, ORC_NCG = 2 };
+enum { ORC_BETA_PPR = 0, ORC_BETA_PPR_AF = 1, ORC_BETA_PFR = 2, ORC_BETA_PPR_PRINTED = 3 };
+enum { ORC_WARM_SCALED = 0, ORC_WARM_CARRY = 1, ORC_WARM_ZERO = 2 };
+enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EINSTABLE = 3, ORC_ENOCONV = 4, ORC_ELINESEARCH = 5 };
+
+typedef struct {
+  int64_t n;
+  int32_t kind;          /* ORC_DENSE_F32 / ORC_DENSE_F64 / ORC_SQEUCLID_F32 */
+  int32_t d;             /* coordinate dimension (SQEUCLID) */
+  const void* C;         /* n*n row-major, float or double */
+  const float* X;        /* n*d (SQEUCLID) */
+  const float* Y;        /* n*d */
+  float scale;           /* C_ij = fp32 recipe(|x_i-y_j|^2) * scale */
+  const double* r;       /* target row marginal, >0, sums to 1 */
+  const double* c;       /* target column marginal */
+} orc_problem;
+
+typedef struct {
+  double eps;            /* projection stop tolerance */
+  int32_t stop_rho;      /* 0: L1 = |r(P)-r|_1+|c(P)-c|_1 <= eps (Z2); 1: rho <= eps */
+  int32_t projector;     /* ORC_PNCG, ORC_SINKHORN, ORC_NCG */
+  int32_t beta;          /* ORC_BETA_* (Z6) */
+  double c1, c2;         /* approximate Wolfe constants (Z7: 0.1, 0.4) */
+  int32_t warm;          /* ORC_WARM_* (Z4) */
+  int32_t p0_ones;       /* 1: P0 = 1 1^T (classic Sinkhorn), 0: P0 = r c^T */
+  int64_t max_evals;     /* cap on O(n^2) evaluations per solve (0 = 10^7) */
+  int32_t ls_max_trials; /* per line search (0 = 100) */
+  int32_t max_threads;   /* OpenMP threads (0 = default) */
+} orc_options;
+
+typedef struct {         /* one PNCG / Sinkhorn iteration */
+  int32_t t, k;
+  double l1, rho;        /* at the iterate BEFORE this iteration's update */
+  double alpha, dphi0, dphi_alpha, dphi_value; /* line search: phi'(0), phi'(alpha), phi(alpha)-phi(0) */
+  int32_t trials, reset;
+  double beta;
+} orc_trace_rec;
+
+typedef struct {
+  double cost_unrounded, cost_rounded, l1_final, rho_final, gamma_bar, seconds;
+  int64_t md_steps, iterations, evaluations, ls_evaluations, resets, ls_restarts;
+  int32_t status;
+  /* per-MD-step: initial infeasibility rho_0 and L1_0 (Fig. 2 left), iterations */
+  double rho0[64], l10[64];
+  int64_t iters_step[64];
+} orc_result;
+
+/* log r(P), log c(P) for P_ij = exp(A_i + B_j - gbar*C_ij) */
+int orc_log_marginals(const orc_problem* pb, const double* A, const double* B, double gbar,
+                      double* lr, double* lc);
+/* C_ij as the oracle sees it (fp64 promotion of the input / Z22 recipe) */
+double orc_cost(const orc_problem* pb, int64_t i, int64_t j);
+
+/* One Bregman projection (Alg. 2 / Alg. 3) of P_hat = exp(U + V - gbar*C)
+ * starting at potentials (u, v), which are updated in place. */
+int orc_project(const orc_problem* pb, const double* U, const double* V, double gbar,
+                double* u, double* v, const orc_options* opt, int32_t t,
+                orc_result* res, orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len);
+
+/* MDOT (Alg. 1) with schedule gammas[0..T-1]; outputs cumulative (U, V),
+ * gauge fixed so that <r,U> = <c,V> (Z19), rounded cost and stats. */
+int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_options* opt,
+             double* U_out, double* V_out, orc_result* res,
+             orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len);
+
+/* Rounding onto U(r,c) (Altschuler et al. Alg. 2, as restated in SPEC.md:331)
+ * of F = exp(U + V - gbar*C).  Writes cost <C,F>, cost <C,G>, and optionally
+ * the dense G (n*n doubles) and its marginals. */
+int orc_round(const orc_problem* pb, const double* U, const double* V, double gbar,
+              double* cost_F, double* cost_G, double* G_out, double* rG, double* cG);
+
+/* Schedules (BASELINE config 1 / Z13) */
+int orc_schedule_fixed(double gamma_bar, double step_max, int32_t T, double* out, int32_t cap);
+int orc_schedule_doubling(double gamma_bar, double gamma0, double* out, int32_t cap);
+double orc_default_eps(double hmin, double gamma_bar);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,435 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix.
+
+Each test names the passage it pins.  None of them re-types the oracle's own
+formula: they use closed forms, exact OT values, invariants and brute force.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synthetic as S
+from tests import exact_ot as X
+
+
+def _dense_C(prob):
+    n = prob.n
+    if prob.C is not None:
+        return prob.C.astype(np.float64)
+    return np.array([[prob.cost(i, j) for j in range(n)] for i in range(n)])
+
+
+# ---------------------------------------------------------------- evaluation
+def test_log_marginals_direct_sum():
+    """r(P)=P1, c(P)=P^T1 for P=exp(A+B-gC); compare to a
+    direct fp64 sum of the explicit matrix (no log-sum-exp)."""
+    inst = S.random_small(13, seed=3)
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(0)
+    A = rng.normal(size=13) - 3
+    B = rng.normal(size=13) - 2
+    g = 7.5
+    P = np.exp(A[:, None] + B[None, :] - g * inst.C)
+    lr, lc, st = O.log_marginals(prob, A, B, g)
+    assert st == 0
+    np.testing.assert_allclose(np.exp(lr), P.sum(1), rtol=1e-14)
+    np.testing.assert_allclose(np.exp(lc), P.sum(0), rtol=1e-14)
+
+
+def test_log_marginals_shift_invariance_and_extremes():
+    """PAPER.md:231 gauge: (A+d, B-d) gives the same P.  Log domain must also
+    survive exponents far outside fp64 exp range (A34; SPEC criterion 13 is
+    inverted for a log-domain build)."""
+    inst = S.random_small(17, seed=4)
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(1)
+    A = rng.normal(size=17)
+    B = rng.normal(size=17)
+    lr0, lc0, _ = O.log_marginals(prob, A, B, 3.0)
+    for d in (-10.0, 3.7, 10.0):
+        lr, lc, _ = O.log_marginals(prob, A + d, B - d, 3.0)
+        np.testing.assert_allclose(lr, lr0, atol=1e-12)
+        np.testing.assert_allclose(lc, lc0, atol=1e-12)
+    # huge gamma: exp(-4096 C) underflows fp64 for most entries; LSE must not.
+    lr, lc, st = O.log_marginals(prob, A + 2000, B + 1000, 4096.0)
+    assert st == 0 and np.all(np.isfinite(lr)) and np.all(np.isfinite(lc))
+
+
+def test_rank_one_marginals_closed_form():
+    """gbar = 0: P = e^A e^B^T is rank one, r(P) = e^A sum(e^B)."""
+    inst = S.random_small(9, seed=5)
+    prob = O.OracleProblem(inst)
+    A = np.linspace(-3, 2, 9)
+    B = np.linspace(1, -1, 9)
+    lr, lc, _ = O.log_marginals(prob, A, B, 0.0)
+    np.testing.assert_allclose(lr, A + np.log(np.exp(B).sum()), atol=1e-14)
+    np.testing.assert_allclose(lc, B + np.log(np.exp(A).sum()), atol=1e-14)
+
+
+def test_cost_sqeuclid_recipe_is_fp32_fma_chain():
+    """DESIGN.md Z22: on-the-fly C is the fixed fp32 recipe; check against a
+    numpy float32 emulation (fma emulated exactly via float64 arithmetic:
+    d*d + acc is exact in fp64 for fp32 operands, then rounded once)."""
+    inst = S.config5(0, n=64, d=16)
+    prob = O.OracleProblem(inst)
+    for (i, j) in [(0, 0), (3, 7), (63, 1), (10, 10)]:
+        acc = np.float32(0.0)
+        for k in range(16):
+            dk = np.float32(inst.X[i, k] - inst.Y[j, k])
+            acc = np.float32(np.float64(dk) * np.float64(dk) + np.float64(acc))
+        ref = np.float32(acc * np.float32(1.0 / 16))
+        assert prob.cost(i, j) == float(ref)
+
+
+# --------------------------------------------------------------- divergences
+def test_rho_worked_example_two_rc():
+    """SPEC.md:84 (P = 2 r c^T) with D_h(y|x)=sum x - y + y log(y/x)
+    (PAPER.md:82): rho = 2 (2 ln2 - 1) (SPEC.md:73 example doubled)."""
+    inst = S.random_small(6, seed=6)
+    prob = O.OracleProblem(inst)
+    U = np.log(inst.r) + math.log(2.0)
+    V = np.log(inst.c)
+    # gbar = 0 so P = exp(U+V) = 2 r c^T; eps huge -> no iteration
+    _, _, res, _ = O.project(prob, U, V, 0.0, opts=O.make_options(eps=1e9))
+    assert res["iterations"] == 0
+    assert abs(res["rho_final"] - 2 * (2 * math.log(2) - 1)) < 1e-14
+    assert abs(res["l1_final"] - 2.0) < 1e-14
+
+
+def test_descent_identity_first_direction():
+    """<s, grad g> = D(r(P)|r)+D(r|r(P))+D(c(P)|c)+D(c|c(P)).
+    The first PNCG direction is p = -s (beta_1 = 0), so the
+    traced phi'(0) = <p, grad> must equal minus the four-divergence sum,
+    computed here from independently obtained marginals."""
+    inst = S.random_small(20, seed=7)
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(2)
+    U = np.log(inst.r) + 0.3 * rng.normal(size=20)
+    V = np.log(inst.c) + 0.3 * rng.normal(size=20)
+    g = 5.0
+    P = np.exp(U[:, None] + V[None, :] - g * inst.C)
+    rP, cP = P.sum(1), P.sum(0)
+    r, c = inst.r, inst.c
+
+    def D(y, x):
+        return float(np.sum(x - y + y * np.log(y / x)))
+
+    four = D(rP, r) + D(r, rP) + D(cP, c) + D(c, cP)
+    _, _, res, tr = O.project(prob, U, V, g, opts=O.make_options(eps=1e-9, max_evals=6),
+                              trace_cap=10)
+    assert tr, "no iteration traced"
+    assert tr[0]["reset"] == 0 and tr[0]["beta"] == 0.0
+    assert abs(tr[0]["dphi0"] + four) < 1e-12 * max(1.0, four)
+
+
+def test_phi_prime_matches_finite_difference():
+    """phi'(alpha) equals the derivative of the dual objective
+    g(u,v) = sum P - <u,r> - <v,c> - 1 along p; checked with a
+    central difference of g built from a direct dense sum."""
+    n = 12
+    inst = S.random_small(n, seed=8)
+    prob = O.OracleProblem(inst)
+    g = 4.0
+    U, V = np.log(inst.r), np.log(inst.c)
+    u0 = np.zeros(n)
+    v0 = np.zeros(n)
+    _, _, res, tr = O.project(prob, U, V, g, u0, v0, opts=O.make_options(eps=1e-9, max_evals=4),
+                              trace_cap=4)
+    # direction of the first iteration is -s at (u0, v0):
+    P = np.exp(U[:, None] + V[None, :] - g * inst.C)
+    s = np.concatenate([np.log(P.sum(1)) - np.log(inst.r), np.log(P.sum(0)) - np.log(inst.c)])
+    p = -s
+
+    def gobj(a):
+        uu = u0 + a * p[:n]
+        vv = v0 + a * p[n:]
+        Pa = np.exp((U + uu)[:, None] + (V + vv)[None, :] - g * inst.C)
+        return Pa.sum() - uu @ inst.r - vv @ inst.c - 1.0
+
+    h = 1e-6
+    fd0 = (gobj(h) - gobj(-h)) / (2 * h)
+    assert abs(tr[0]["dphi0"] - fd0) <= 1e-6 * abs(fd0)
+    a = tr[0]["alpha"]
+    fda = (gobj(a + h) - gobj(a - h)) / (2 * h)
+    assert abs(tr[0]["dphi_alpha"] - fda) <= 1e-6 * max(abs(fda), 1e-8) + 1e-9
+    # phi(alpha) - phi(0) as traced
+    assert abs(tr[0]["dphi_value"] - (gobj(a) - gobj(0.0))) < 1e-12
+
+
+# ------------------------------------------------------------ projections
+def test_2x2_closed_form():
+    """SURVEY 8(c) 2x2 closed form of the entropic plan at gbar (Lemma 2
+    reduces MD with P0 = r c^T to entropic OT)."""
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        C = rng.uniform(0, 1, size=(2, 2))
+        r = rng.dirichlet([1, 1])
+        c = rng.dirichlet([1, 1])
+        gbar = [1.0, 8.0, 64.0, 200.0][trial % 4]
+        prob = O.OracleProblem(C=C, r=r, c=c)
+        for proj in (O.PNCG, O.SINKHORN):
+            U, V, res, _ = O.mdot(prob, [gbar], O.make_options(eps=1e-14, projector=proj))
+            assert res["status"] == 0, res
+            P = np.exp(U[:, None] + V[None, :] - gbar * C)
+            Pref = X.entropic_2x2(C, r, c, gbar)
+            np.testing.assert_allclose(P, Pref, atol=1e-13)
+
+
+def test_sinkhorn_and_pncg_same_fixed_point():
+    """Uniqueness of the Bregman projection."""
+    inst = S.random_small(24, seed=12)
+    prob = O.OracleProblem(inst)
+    U, V = np.log(inst.r), np.log(inst.c)
+    g = 30.0
+    u1, v1, r1, _ = O.project(prob, U, V, g, opts=O.make_options(eps=1e-13, projector=O.PNCG))
+    u2, v2, r2, _ = O.project(prob, U, V, g, opts=O.make_options(eps=1e-13, projector=O.SINKHORN))
+    u3, v3, r3, _ = O.project(prob, U, V, g, opts=O.make_options(eps=1e-13, projector=O.NCG))
+    assert r1["status"] == 0 and r2["status"] == 0 and r3["status"] == 0
+    P1 = np.exp((U + u1)[:, None] + (V + v1)[None, :] - g * inst.C)
+    P2 = np.exp((U + u2)[:, None] + (V + v2)[None, :] - g * inst.C)
+    P3 = np.exp((U + u3)[:, None] + (V + v3)[None, :] - g * inst.C)
+    assert np.abs(P1 - P2).sum() < 1e-11
+    assert np.abs(P1 - P3).sum() < 1e-11
+    # fewer PNCG iterations than Sinkhorn half-steps
+    assert r1["iterations"] < r2["iterations"]
+
+
+def test_line_search_wolfe_post_hoc_and_decrease():
+    """Every accepted alpha satisfies the approximate Wolfe conditions
+     and the decrease safeguard (Z9); the dual objective is
+    monotone; mean phi' evaluations per search is in the paper's range
+    ("typically between 2-4"; SPEC criterion 9 allows <= 6)."""
+    inst = S.paper_sphere_instance(96, 4, 0.9, seed=13)
+    prob = O.OracleProblem(inst)
+    g = O.schedule_fixed(128.0, T=2)
+    U, V, res, tr = O.mdot(prob, g, O.make_options(eps=1e-9), trace_cap=100000)
+    assert res["status"] == 0
+    assert len(tr) == res["iterations"]
+    c1, c2 = 0.1, 0.4
+    for q in tr:
+        assert q["dphi0"] < 0
+        assert (2 * c1 - 1) * q["dphi0"] >= q["dphi_alpha"] >= c2 * q["dphi0"]
+        assert q["dphi_value"] <= 1e-12
+    mean_trials = np.mean([q["trials"] for q in tr])
+    assert mean_trials <= 6.0
+
+
+def test_reset_rule_and_first_step():
+    """PAPER.md:190 read as: reset when <p, grad> >= 0 (Z5).  Every traced
+    direction is a descent direction; k=1 has beta = 0."""
+    inst = S.paper_sphere_instance(64, 4, 0.5, seed=14)
+    prob = O.OracleProblem(inst)
+    U, V, res, tr = O.mdot(prob, [64.0], O.make_options(eps=1e-10), trace_cap=100000)
+    assert res["status"] == 0
+    assert tr[0]["beta"] == 0.0
+    assert all(q["dphi0"] < 0 for q in tr)
+
+
+# ------------------------------------------------------------------ MD loop
+def _md_plan(prob, gammas, **kw):
+    U, V, res, _ = O.mdot(prob, gammas, O.make_options(**kw))
+    assert res["status"] == 0, res
+    g = float(np.sum(gammas))
+    return np.exp(U[:, None] + V[None, :] - g * _dense_C(prob)), res
+
+
+def test_lemma2_schedule_invariance():
+    """Lemma 2: equal gbar, rank-1 P0 -> the same plan,
+    for fixed T in {1,4,16}, the doubling schedule and both projectors."""
+    inst = S.random_small(8, seed=15)
+    prob = O.OracleProblem(inst)
+    gb = 32.0
+    Pref, _ = _md_plan(prob, [gb], eps=1e-13)
+    for sched in (O.schedule_fixed(gb, T=4), O.schedule_fixed(gb, T=16), O.schedule_doubling(gb)):
+        for proj in (O.PNCG, O.SINKHORN):
+            P, _ = _md_plan(prob, sched, eps=1e-13, projector=proj)
+            assert np.abs(P - Pref).sum() < 1e-10
+    # P0 = 1 1^T (classic Sinkhorn special case) gives the same plan
+    P, _ = _md_plan(prob, [gb], eps=1e-13, p0_ones=True)
+    assert np.abs(P - Pref).sum() < 1e-10
+
+
+def test_lemma1_exact_improvement_and_cor1():
+    """Lemma 1 equality and Cor. 1
+    bound on consecutive MD iterates (n = 8, gamma_t = 8)."""
+    inst = S.random_small(8, seed=16)
+    prob = O.OracleProblem(inst)
+    C = inst.C
+    Hmin = min(-(inst.r * np.log(inst.r)).sum(), -(inst.c * np.log(inst.c)).sum())
+    plans = [np.outer(inst.r, inst.c)]
+    for t in range(1, 6):
+        P, _ = _md_plan(prob, [8.0] * t, eps=1e-13)
+        plans.append(P)
+
+    def kl(a, b):
+        return float(np.sum(a * np.log(a / b)))
+
+    for t in range(0, 5):
+        Pt, Pn = plans[t], plans[t + 1]
+        lhs = float((Pt * C).sum() - (Pn * C).sum())
+        rhs = (kl(Pt, Pn) + kl(Pn, Pt)) / 8.0
+        assert abs(lhs - rhs) < 1e-9
+        assert lhs >= -1e-12       # monotone improvement
+        if t >= 1:
+            bound = min(8.0, math.sqrt(Hmin * 8.0 / (8.0 * t)))
+            assert np.abs(Pn - Pt).sum() <= bound + 1e-9
+
+
+@pytest.mark.parametrize("n", [4, 5, 6])
+def test_prop1_bound_vs_permutation_enumeration(n):
+    """Prop. 1: 0 <= <G,C> - OT and <P,C> - OT <= H_min/gbar,
+    OT by enumerating permutation vertices (uniform marginals)."""
+    for seed in range(4):
+        inst = S.random_small(n, seed=100 + seed, uniform_marginals=True)
+        prob = O.OracleProblem(inst)
+        ot = X.ot_enumerate_uniform(inst.C)
+        Hmin = math.log(n)
+        prev = None
+        for gb in (4.0, 16.0, 64.0):
+            U, V, res, _ = O.mdot(prob, O.schedule_fixed(gb, T=4), O.make_options(eps=1e-8))
+            assert res["status"] == 0
+            gap = res["cost_rounded"] - ot
+            assert gap >= -1e-12                     # rounded plan is feasible
+            assert res["cost_unrounded"] - ot <= Hmin / gb + 1e-9
+            if prev is not None:
+                assert res["cost_unrounded"] <= prev + 1e-12   # -> OT as gbar grows
+            prev = res["cost_unrounded"]
+
+
+def test_prop1_bound_vs_lp_nonuniform():
+    for seed in range(3):
+        inst = S.random_small(7, seed=200 + seed)
+        prob = O.OracleProblem(inst)
+        ot = X.ot_lp(inst.C, inst.r, inst.c)
+        Hmin = min(-(inst.r * np.log(inst.r)).sum(), -(inst.c * np.log(inst.c)).sum())
+        U, V, res, _ = O.mdot(prob, O.schedule_fixed(512.0), O.make_options(eps=1e-12))
+        assert res["status"] == 0
+        assert res["cost_rounded"] - ot >= -1e-10
+        assert res["cost_unrounded"] - ot <= Hmin / 512.0 + 1e-9
+
+
+def test_exact_ot_helpers_agree():
+    inst = S.random_small(5, seed=300, uniform_marginals=True)
+    assert abs(X.ot_enumerate_uniform(inst.C) - X.ot_lp(inst.C, inst.r, inst.c)) < 1e-12
+    li = S.line_instance(7, seed=301)
+    assert abs(X.ot_line_nw(li.C, li.r, li.c) - X.ot_lp(li.C, li.r, li.c)) < 1e-12
+
+
+def test_prop1_bound_vs_1d_monotone_coupling():
+    """1-D convex cost: exact OT by the north-west corner rule, any marginals,
+    larger n (the pin the GPU tests reuse at scale)."""
+    li = S.line_instance(128, seed=302)
+    prob = O.OracleProblem(li)
+    ot = X.ot_line_nw(li.C, li.r, li.c)
+    Hmin = min(-(li.r * np.log(li.r)).sum(), -(li.c * np.log(li.c)).sum())
+    gb = 4096.0
+    U, V, res, _ = O.mdot(prob, O.schedule_fixed(gb), O.make_options(eps=1e-10))
+    assert res["status"] == 0
+    assert res["cost_rounded"] - ot >= -1e-12
+    assert res["cost_unrounded"] - ot <= Hmin / gb + 1e-9
+
+
+def test_near_delta_marginal_gives_independence_coupling():
+    """if r is a delta, the only feasible plan is r c^T."""
+    n = 10
+    inst = S.random_small(n, seed=17)
+    r = np.full(n, 1e-13)
+    r[3] = 1.0 - (n - 1) * 1e-13
+    prob = O.OracleProblem(C=inst.C, r=r, c=inst.c)
+    U, V, res, _ = O.mdot(prob, O.schedule_fixed(256.0), O.make_options(eps=1e-12))
+    assert res["status"] == 0
+    ind = float((np.outer(r, inst.c) * inst.C).sum())
+    assert abs(res["cost_rounded"] - ind) < 1e-10
+
+
+def test_gamma_4096_single_step_is_stable():
+    """SPEC criterion 13 inverted: the log-domain oracle must not fail at a
+    single MD step of gamma_t = 4096 (PAPER.md:362 reports failure > 256 for
+    the paper's non-log implementation)."""
+    inst = S.uniform_points_instance(3, 96, 2, 0, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    U, V, res, _ = O.mdot(prob, [4096.0], O.make_options(eps=1e-8))
+    assert res["status"] == 0
+    U2, V2, res2, _ = O.mdot(prob, O.schedule_fixed(4096.0), O.make_options(eps=1e-8))
+    assert res2["status"] == 0
+    assert abs(res["cost_unrounded"] - res2["cost_unrounded"]) < 1e-6 * res["cost_unrounded"]
+
+
+# ----------------------------------------------------------------- rounding
+def test_rounding_worked_example_half_rc():
+    """F = r c^T / 2 -> G = r c^T."""
+    inst = S.random_small(7, seed=18)
+    prob = O.OracleProblem(inst)
+    U = np.log(inst.r) + math.log(0.5)
+    V = np.log(inst.c)
+    out = O.round_plan(prob, U, V, 0.0, dense=True)
+    np.testing.assert_allclose(out["G"], np.outer(inst.r, inst.c), atol=1e-16)
+
+
+def test_rounding_exact_marginals_bound_idempotent():
+    """Altschuler et al. Alg. 2: r(G)=r, c(G)=c, G>=0,
+    |G-F|_1 <= 2 (|r(F)-r|_1 + |c(F)-c|_1), idempotence."""
+    rng = np.random.default_rng(19)
+    for seed in range(10):
+        inst = S.random_small(8, seed=400 + seed)
+        prob = O.OracleProblem(inst)
+        U = np.log(inst.r) + 0.05 * rng.normal(size=8)
+        V = np.log(inst.c) + 0.05 * rng.normal(size=8)
+        g = 3.0
+        F = np.exp(U[:, None] + V[None, :] - g * inst.C)
+        out = O.round_plan(prob, U, V, g, dense=True)
+        G = out["G"]
+        assert np.all(G >= 0)
+        np.testing.assert_allclose(G.sum(1), inst.r, atol=1e-15)
+        np.testing.assert_allclose(G.sum(0), inst.c, atol=1e-15)
+        l1 = np.abs(F.sum(1) - inst.r).sum() + np.abs(F.sum(0) - inst.c).sum()
+        assert np.abs(G - F).sum() <= 2 * l1 + 1e-15
+        assert abs(out["cost_G"] - (G * inst.C).sum()) < 1e-15
+        assert abs(out["cost_F"] - (F * inst.C).sum()) < 1e-15
+
+
+# ---------------------------------------------------------------- schedules
+def test_schedules_and_default_eps():
+    """PAPER.md:356 rule gamma_t = gbar/max(1, floor(gbar/256))
+    examples; doubling schedule of BASELINE config 1 (Z13)."""
+    assert list(O.schedule_fixed(128.0)) == [128.0]
+    assert list(O.schedule_fixed(1024.0)) == [256.0] * 4
+    assert list(O.schedule_fixed(512.0, T=4)) == [128.0] * 4
+    assert len(O.schedule_fixed(4096.0)) == 16
+    d = O.schedule_doubling(4096.0)
+    assert list(d) == [1.0, 1.0] + [2.0 ** k for k in range(1, 12)]
+    assert np.cumsum(d)[-1] == 4096.0
+    assert abs(O.default_eps(4.0, 4096.0) - 1e-5 / 1024 ** 2) < 1e-20
+    assert O.default_eps(10.0, 5.0) == 1e-5
+
+
+# ------------------------------------------------------ paper trend pins
+def test_warm_start_rho0_decreases():
+    """Fig. 2 left (SPEC criterion 12): with warm starts
+    the initial infeasibility at the last MD step is below the first one."""
+    for seed in range(3):
+        inst = S.paper_sphere_instance(128, 4, 0.9, seed=500 + seed)
+        prob = O.OracleProblem(inst)
+        U, V, res, _ = O.mdot(prob, O.schedule_fixed(512.0, T=16),
+                              O.make_options(eps=1e-9, stop_rho=True))
+        assert res["status"] == 0
+        assert res["rho0"][-1] < res["rho0"][0]
+
+
+@pytest.mark.slow
+def test_pncg_fewer_iterations_than_sinkhorn():
+    """Fig. 2/4 direction (SPEC criterion 10): n = 256,
+    m = 4, entropy 0.9, gbar = 256, T = 1, rho <= 1e-9: PNCG needs fewer
+    iterations than SA on every instance and >= 3x fewer on average."""
+    ratios = []
+    for seed in range(2):
+        inst = S.paper_sphere_instance(256, 4, 0.9, seed=600 + seed)
+        prob = O.OracleProblem(inst)
+        _, _, rp, _ = O.mdot(prob, [256.0], O.make_options(eps=1e-9, stop_rho=True))
+        _, _, rs, _ = O.mdot(prob, [256.0], O.make_options(eps=1e-9, stop_rho=True,
+                                                           projector=O.SINKHORN))
+        assert rp["status"] == 0 and rs["status"] == 0
+        assert rp["iterations"] <= rs["iterations"]
+        ratios.append(rs["iterations"] / rp["iterations"])
+    assert np.mean(ratios) >= 3.0

@@ -1,0 +1,196 @@
+/* include/mdot.h -- C ABI of the B200-native MDOT-PNCG hot path.
+ *
+ * Method: arxiv 2307.08507 ("MDOT-PNCG").  The library solves the discrete
+ * OT problem  min_{P in U(r,c)} <P, C>  (Eq. opt:original-OT-
+ * problem) by mirror descent (Alg. 1) whose Bregman
+ * projections onto U(r,c) are computed by preconditioned nonlinear conjugate
+ * gradients on the dual potentials (Alg. 2) or by Sinkhorn
+ * scaling (Alg. 3), then rounds the plan onto U(r,c)
+ * and returns <C, P>.
+ *
+ * All functions are synchronous on return, return an mdot_status, never throw
+ * and never free caller memory.  The caller owns every input and output
+ * buffer; the library owns only its internal workspaces (allocated per call on
+ * the caller's stream and released before return).  The last error message
+ * of the calling thread is available from mdot_last_error().
+ *
+ * Memory kinds: `mem` in mdot_problem says where C / X / Y / r / c live and
+ * where the potential outputs are written (MDOT_MEM_HOST: pageable or pinned
+ * host memory, copied in/out inside the call; MDOT_MEM_DEVICE: device
+ * pointers of the current CUDA device, used in place).
+ *
+ * Layout: C is n*n row-major (C[i*n + j] = C_ij = cost of moving mass from
+ * source i to sink j), entries in [0, 1].  X, Y are n*d
+ * row-major fp32 point clouds; the on-the-fly cost is
+ *   C_ij = fl32( fmaf-chain over k of (x_ik - y_jk)^2 ) * scale
+ * with the exact fp32 op order of DESIGN.md "Z22".  r, c are fp64 [n],
+ * strictly positive, summing to 1 within 1e-12.
+ */
+#ifndef MDOT_H
+#define MDOT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDOT_ABI_VERSION 1
+
+typedef enum {
+  MDOT_OK = 0,
+  MDOT_EINVAL = 1,       /* precondition violated (r,c <= 0, sums, n < 1, eps <= 0, C outside [0,1]) */
+  MDOT_EGEN = 2,         /* reserved (input generation failure, SPEC exit 2) */
+  MDOT_EINSTABLE = 3,    /* non-finite marginals even on the exact fp64 fallback evaluator */
+  MDOT_ENOCONV = 4,      /* max_evals reached before the marginal error fell below eps */
+  MDOT_ELINESEARCH = 5,  /* line search failed twice in a row (Z10) */
+  MDOT_ECUDA = 6,        /* CUDA runtime error (message in mdot_last_error) */
+  MDOT_ENCCL = 7,        /* NCCL error (sharded calls) */
+  MDOT_ENOMEM = 8        /* device allocation failed */
+} mdot_status;
+
+typedef enum {
+  MDOT_COST_DENSE_F32 = 0,     /* C: const float*  (n*n) */
+  MDOT_COST_SQEUCLID_F32 = 1,  /* X, Y: const float* (n*d), scale */
+  MDOT_COST_DENSE_F64 = 2      /* C: const double* (n*n) */
+} mdot_cost_kind;
+
+typedef enum { MDOT_MEM_HOST = 0, MDOT_MEM_DEVICE = 1 } mdot_mem;
+
+typedef struct {
+  int64_t n;
+  int32_t kind;            /* mdot_cost_kind */
+  int32_t mem;             /* mdot_mem (inputs and potential outputs) */
+  const void* C;           /* DENSE_*: n*n row-major */
+  int32_t d;               /* SQEUCLID: coordinate dimension (1..64) */
+  float scale;             /* SQEUCLID: C_ij = recipe(|x_i - y_j|^2) * scale */
+  const float* X;          /* SQEUCLID: n*d */
+  const float* Y;          /* SQEUCLID: n*d */
+  const double* r;         /* [n] target row marginal */
+  const double* c;         /* [n] target column marginal */
+} mdot_problem;
+
+typedef enum {
+  MDOT_SCHED_FIXED = 0,     /* T equal steps gamma_t = gamma_bar/T; T = max(1, floor(gamma_bar/step_max))
+                               when T == 0 */
+  MDOT_SCHED_DOUBLING = 1,  /* cumulative gbar_t = gamma0 * 2^(t-1) up to gamma_bar (BASELINE config 1, Z13) */
+  MDOT_SCHED_EXPLICIT = 2   /* gammas[0..n_gammas-1] */
+} mdot_sched_kind;
+
+typedef struct {
+  int32_t kind;            /* mdot_sched_kind */
+  int32_t T;               /* FIXED: number of steps, 0 = paper rule */
+  double gamma_bar;        /* total budget (sum of gamma_t) */
+  double step_max;         /* FIXED paper rule cap, default 256 */
+  double gamma0;           /* DOUBLING: first step, default 1 */
+  const double* gammas;    /* EXPLICIT (host pointer) */
+  int32_t n_gammas;
+} mdot_schedule;
+
+typedef enum { MDOT_PROJ_PNCG = 0, MDOT_PROJ_SINKHORN = 1, MDOT_PROJ_NCG = 2 } mdot_projector;
+typedef enum { MDOT_BETA_PPR = 0, MDOT_BETA_PPR_AF = 1, MDOT_BETA_PFR = 2 } mdot_beta;
+typedef enum { MDOT_WARM_SCALED = 0, MDOT_WARM_CARRY = 1, MDOT_WARM_ZERO = 2 } mdot_warm;
+typedef enum { MDOT_PREC_AUTO = 0, MDOT_PREC_F32P = 1, MDOT_PREC_F64P = 2 } mdot_precision;
+
+typedef struct {
+  double eps;              /* projection stop tolerance (> 0) */
+  int32_t stop;            /* 0: L1 = |r(P)-r|_1 + |c(P)-c|_1 <= eps (Z2); 1: rho <= eps */
+  int32_t projector;       /* mdot_projector */
+  int32_t beta;            /* mdot_beta (Z6) */
+  double c1, c2;           /* approximate Wolfe constants (Z7 defaults 0.1, 0.4) */
+  int32_t warm;            /* mdot_warm (Z4) */
+  int32_t precision;       /* mdot_precision: AUTO = fp32 entries for fp32 C, fp64 for DENSE_F64 */
+  int32_t p0_ones;         /* 1: P0 = 1 1^T (classic Sinkhorn special case) */
+  int32_t ls_max_trials;   /* per line search, default 100 */
+  int64_t max_evals;       /* cap on O(n^2) evaluations per solve, default 10^7 */
+  int32_t time_kernels;    /* 1: time every evaluation kernel with CUDA events (result.kernel_ms) */
+  int32_t device_control;  /* 1: device-resident line-search control (no host sync per trial) */
+  void* stream;            /* cudaStream_t, NULL = legacy default stream */
+} mdot_options;
+
+typedef struct {
+  double cost_rounded;     /* <C, G>, G = rounded plan in U(r,c) */
+  double cost_unrounded;   /* <C, P(U,V)> */
+  double l1_final;         /* marginal L1 error of P(U,V) (device evaluation) */
+  double rho_final;        /* D_h(r(P)|r) + D_h(c(P)|c) */
+  double gamma_bar;
+  double seconds;          /* host wall time of the call */
+  double kernel_ms;        /* sum of evaluation-kernel durations (time_kernels = 1) */
+  int64_t md_steps, iterations, evaluations, ls_evaluations, resets, ls_restarts;
+  int64_t fallbacks;       /* evaluations redone on the exact fp64 evaluator */
+  int64_t kernel_launches; /* evaluation kernels timed */
+  int32_t status;
+  int32_t reserved;
+  double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */
+  double l10[64];          /* per MD step: L1 at the warm start */
+  int64_t iters_step[64];  /* per MD step: projection iterations */
+} mdot_result;
+
+/* Fill defaults: eps 1e-6 on L1, PNCG, beta PPR (Z6), c1 0.1, c2 0.4,
+ * warm scaled, precision auto, ls_max_trials 100, max_evals 1e7. */
+void mdot_options_default(mdot_options* o);
+/* FIXED, gamma_bar 4096, step_max 256, T 0 (paper rule -> 16 steps). */
+void mdot_schedule_default(mdot_schedule* s);
+
+/* MDOT-PNCG solve (Alg. 1 with Alg. 2 projections; projector option selects
+ * Alg. 3 or vanilla NCG).
+ *   u_out, v_out: [n] cumulative potentials (U, V) with P_ij = exp(U_i + V_j
+ *                 - gamma_bar C_ij), gauge fixed so that <r,U> = <c,V> (Z19);
+ *                 nullable.  Same memory kind as the problem.
+ *   P_out:        nullable; n*n fp32 rounded plan G (dense write, same memory
+ *                 kind as the problem).
+ *   res:          required.
+ * Errors: MDOT_EINVAL on precondition violations (checked on the host copy of
+ * r, c; C in [0,1] is checked on a sample of entries), MDOT_ENOCONV,
+ * MDOT_ELINESEARCH, MDOT_EINSTABLE, MDOT_ECUDA, MDOT_ENOMEM.  On error the
+ * outputs hold the last iterate. */
+mdot_status mdot_solve(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
+                       double* u_out, double* v_out, float* P_out, mdot_result* res);
+
+/* Same call with the projector forced to Sinkhorn (Alg. 3) on the same
+ * evaluation kernels: the paper's baseline. */
+mdot_status mdot_sinkhorn(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
+                          double* u_out, double* v_out, float* P_out, mdot_result* res);
+
+/* Batch of B independent instances sharing one cost (BASELINE config 2).
+ * r, c: B*n row-major (instance b at r + b*n); u_out, v_out: B*n, nullable;
+ * res: B results.  Returns the first non-OK status (all instances run). */
+mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t B, const double* r, const double* c,
+                             const mdot_schedule* sched, const mdot_options* opt,
+                             double* u_out, double* v_out, mdot_result* res);
+
+/* One fused marginal evaluation (the hot kernel):
+ *   lr_i = log sum_j exp(A_i + B_j - gbar C_ij),  lc_j = log sum_i exp(...)
+ * (PAPER.md:157-160 in log form).  A, B, lr, lc are [n] fp64 in the memory
+ * kind of the problem (r, c are used only to anchor the fp32 exponent).
+ * `fallback_out` (nullable) receives 1 if the exact fp64 evaluator was used. */
+mdot_status mdot_marginals(const mdot_problem* pb, const double* A, const double* B, double gbar,
+                           double* lr, double* lc, const mdot_options* opt, int32_t* fallback_out);
+
+/* Rounding onto U(r,c) (Altschuler et al. Alg. 2 as restated in
+ * SPEC.md:331) of F = exp(U + V - gbar C), without solving: writes <C,F>,
+ * <C,G> and optionally the dense fp32 G (P_out, nullable). */
+mdot_status mdot_round(const mdot_problem* pb, const double* U, const double* V, double gbar,
+                       float* P_out, double* cost_F, double* cost_G, const mdot_options* opt);
+
+/* ---- row-sharded multi-GPU (NCCL over NVLink; one process per GPU) ---- */
+typedef struct mdot_comm mdot_comm;
+/* nccl_unique_id: 128-byte ncclUniqueId from rank 0 (broadcast by the caller,
+ * e.g. over a torch.distributed process group). */
+mdot_status mdot_get_unique_id(void* nccl_unique_id_out);
+mdot_status mdot_comm_create(const void* nccl_unique_id, int32_t nranks, int32_t rank, int32_t device,
+                             mdot_comm** out);
+mdot_status mdot_comm_destroy(mdot_comm* comm);
+/* local rows [row0, row0 + n_local) of C (local_rows->C points at row row0,
+ * n_local*n entries) or of X (local_rows->X at row row0; Y, r, c full).
+ * local_rows->n is the GLOBAL n.  u_local_out: [n_local], v_out: [n]. */
+mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, int64_t row0, int64_t n_local,
+                               const mdot_schedule* sched, const mdot_options* opt,
+                               double* u_local_out, double* v_out, mdot_result* res);
+
+const char* mdot_last_error(void);
+int32_t mdot_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDOT_H */

@@ -84,6 +84,8 @@ def lib():
         L = ct.CDLL(_SO)
         P, D = ct.c_void_p, ct.c_double
         L.orc_log_marginals.argtypes = [ct.POINTER(Problem), P, P, D, P, P]
+        L.orc_log_marginal_rows.argtypes = [ct.POINTER(Problem), P, P, D, P, ct.c_int64, P]
+        L.orc_log_marginal_cols.argtypes = [ct.POINTER(Problem), P, P, D, P, ct.c_int64, P]
         L.orc_cost.argtypes = [ct.POINTER(Problem), ct.c_int64, ct.c_int64]
         L.orc_cost.restype = D
         L.orc_project.argtypes = [ct.POINTER(Problem), P, P, D, P, P, ct.POINTER(Options),
@@ -151,6 +153,22 @@ def log_marginals(prob: OracleProblem, A, B, gbar):
     lc = np.empty(prob.n)
     st = lib().orc_log_marginals(ct.byref(prob.s), _ptr(A), _ptr(B), float(gbar), _ptr(lr), _ptr(lc))
     return lr, lc, st
+
+
+def log_marginal_subset(prob: OracleProblem, A, B, gbar, rows=None, cols=None):
+    """Oracle log-marginals of selected rows / columns only."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    out = {}
+    for name, idx, fn in (("rows", rows, lib().orc_log_marginal_rows),
+                          ("cols", cols, lib().orc_log_marginal_cols)):
+        if idx is None:
+            continue
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        o = np.empty(len(idx))
+        fn(ct.byref(prob.s), _ptr(A), _ptr(B), float(gbar), _ptr(idx), len(idx), _ptr(o))
+        out[name] = o
+    return out
 
 
 def schedule_fixed(gamma_bar, step_max=256.0, T=0):

@@ -106,6 +106,44 @@ int orc_log_marginals(const orc_problem* pb, const double* A, const double* B, d
   return bad ? ORC_EINSTABLE : ORC_OK;
 }
 
+/* The same log-sum-exp for selected rows / columns only (parity checks at
+ * full size compute sampled outputs one by one). */
+int orc_log_marginal_rows(const orc_problem* pb, const double* A, const double* B, double gbar,
+                          const int64_t* idx, int64_t k, double* out) {
+  const int64_t n = pb->n;
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < k; ++q) {
+    const int64_t i = idx[q];
+    double m = -INFINITY;
+    for (int64_t j = 0; j < n; ++j) {
+      double z = (A[i] + B[j]) - gbar * orc_cost(pb, i, j);
+      if (z > m) m = z;
+    }
+    double s = 0.0;
+    for (int64_t j = 0; j < n; ++j) s += exp((A[i] + B[j]) - gbar * orc_cost(pb, i, j) - m);
+    out[q] = m + log(s);
+  }
+  return ORC_OK;
+}
+
+int orc_log_marginal_cols(const orc_problem* pb, const double* A, const double* B, double gbar,
+                          const int64_t* idx, int64_t k, double* out) {
+  const int64_t n = pb->n;
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < k; ++q) {
+    const int64_t j = idx[q];
+    double m = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+      double z = (A[i] + B[j]) - gbar * orc_cost(pb, i, j);
+      if (z > m) m = z;
+    }
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += exp((A[i] + B[j]) - gbar * orc_cost(pb, i, j) - m);
+    out[q] = m + log(s);
+  }
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------ */
 /* Small vector helpers (plain loops). */
 static double dot(const double* a, const double* b, int64_t n) {

@@ -68,6 +68,10 @@ typedef struct {
 /* log r(P), log c(P) for P_ij = exp(A_i + B_j - gbar*C_ij) */
 int orc_log_marginals(const orc_problem* pb, const double* A, const double* B, double gbar,
                       double* lr, double* lc);
+int orc_log_marginal_rows(const orc_problem* pb, const double* A, const double* B, double gbar,
+                          const int64_t* idx, int64_t k, double* out);
+int orc_log_marginal_cols(const orc_problem* pb, const double* A, const double* B, double gbar,
+                          const int64_t* idx, int64_t k, double* out);
 /* C_ij as the oracle sees it (fp64 promotion of the input / Z22 recipe) */
 double orc_cost(const orc_problem* pb, int64_t i, int64_t j);
 

@@ -1,0 +1,40 @@
+"""Build the in-tree CUDA library (sm_100a) with nvcc: libmdot_b200.so.
+
+Kept in-tree (not pip-installed) so the .so travels to the GPU box with the
+repo snapshot and the driver sees it loaded from the repo."""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "solver.cu", "comm.cu")]
+HDR = [os.path.join(HERE, "csrc", f) for f in ("internal.cuh", "solver.h", "comm.h")] + \
+      [os.path.join(ROOT, "include", "mdot.h")]
+OUT = os.path.join(HERE, "libmdot_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",
+         "-shared", "-cudart", "static", "-ldl"]
+
+
+def needs_build():
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    return any(os.path.getmtime(f) > t for f in SRC + HDR)
+
+
+def build(force=False, verbose=False):
+    if not force and not needs_build():
+        return OUT
+    cmd = [NVCC] + FLAGS + ["-o", OUT + ".tmp"] + SRC
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    os.replace(OUT + ".tmp", OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,184 @@
+// paper_2307_08507_b200/csrc/internal.cuh -- internal declarations of the
+// MDOT-PNCG CUDA library (not part of the C ABI; see include/mdot.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mdot {
+
+// ---------------------------------------------------------------------------
+// Fused marginal evaluation (rounding K6/K7).
+//
+// Entries are evaluated in an anchored base-2 form:
+//   w_ij = a2_i + b2_j - g2 * C_ij,   a2_i = A_i log2(e) - rho_i,
+//                                     b2_j = B_j log2(e) - sig_j,
+//   P_ij = 2^w_ij * 2^rho_i * 2^sig_j,
+// with integer anchors rho_i ~ log2(r_i)/2, sig_j ~ log2(c_j)/2 so that
+// 2^w ~ 1 for the entries that carry the mass.  a2 = ah + al with ah on a
+// 2^-8 grid (|ah| < 2^15), so ah + bh is exact in fp32 and fmaf(-gh, C, ah+bh)
+// rounds the large cancellation once; g2 = gh + gl (fp32 pair).
+// ---------------------------------------------------------------------------
+constexpr int kTileN = 256;      // columns per tile (8 per lane)
+constexpr int kWarps = 8;        // warps per CTA
+constexpr int kThreads = kWarps * 32;
+constexpr int kUnroll = 4;       // rows per warp per inner step
+constexpr int kNumScalars = 16;
+
+struct EvalArgs {
+  // cost
+  const float* C;          // dense fp32, row-major, rows of this shard (row stride ldc)
+  int64_t ldc;             // row stride of C (== n)
+  const float* X;          // on-the-fly: [nrows x d] (rows of this shard)
+  const float* Y;          // on-the-fly: [n x d]
+  int d;
+  float scale;
+  int64_t n;               // number of columns (global n)
+  int64_t nrows;           // number of rows evaluated (local rows)
+  int tile_m;              // rows per tile (multiple of kWarps*kUnroll)
+  int n_row_tiles, n_col_tiles;
+  // per-row / per-column parameters
+  const float4* rowp;      // [nrows] {ah, al, S=2^rho, w}
+  const float4* colp;      // [n]     {bh, bl, T=2^sig, w}
+  float gh, gl;            // g2 = gbar*log2(e) = gh + gl
+  // outputs
+  double* rowpart;         // [n_col_tiles][nrows]  sum_j 2^w T_j
+  double* colpart;         // [n_row_tiles][n]      sum_i 2^w S_i
+};
+
+// Launch the fused evaluation over the (row tile x column tile) grid.
+// kind: 0 dense fp32, 1 on-the-fly squared Euclidean.
+cudaError_t launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st);
+
+// Exact fp64 evaluator (two-pass online log-sum-exp, fp64 exp): fallback of
+// the fp32 path and the fp64-P precision mode.  Writes lr (rows of this
+// shard) and column (max, sum) partials.
+struct ExactArgs {
+  const void* C; int64_t ldc; int c_f64;  // dense (fp32 or fp64)
+  const float* X; const float* Y; int d; float scale; int otf;
+  int64_t n, nrows;
+  const double* A;   // [nrows]
+  const double* B;   // [n]
+  double gbar;
+  double* lr;        // [nrows]
+  double* colm;      // [chunks][n]
+  double* cols;      // [chunks][n]
+  int chunks;        // row chunks for the column pass
+};
+cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// O(n) kernels
+// ---------------------------------------------------------------------------
+// Scalars produced by finalize (fp64): indices
+enum Scalar : int {
+  SC_MASS = 0,     // sum r(P)
+  SC_MASSC = 1,    // sum c(P)
+  SC_L1 = 2,       // |r(P)-r|_1 + |c(P)-c|_1
+  SC_RHO = 3,      // D_h(r(P)|r) + D_h(c(P)|c)
+  SC_SG = 4,       // <s, g>
+  SC_GCS = 5,      // <g_cur, s>
+  SC_PCG = 6,      // <p_cur, g>      (= phi'(alpha) for a trial)
+  SC_PRC = 7,      // <p_cur, (r,c)>
+  SC_GG = 8,       // <g, g>
+  SC_GCG = 9,      // <g_cur, g>
+  SC_BAD = 10,     // count of invalid marginals (non-finite / out of range)
+  SC_L1R = 11,     // |r(P)-r|_1
+  SC_COST = 12,    // rounding: sum of cost partials
+  SC_CORR = 13,    // rounding: correction term numerator
+  SC_ERN = 14,     // rounding: |err_r|_1
+  SC_AUX = 15
+};
+
+struct FinalizeArgs {
+  int64_t n;             // global n (columns)
+  int64_t nrows;         // local rows
+  int from_partials;     // 1: reduce rowpart/colpart (fast path); 0: lr given, col (m,s) partials
+  const double* rowpart; int n_col_tiles;
+  const double* colpart; int n_row_tiles;
+  const double* rho_r;   // [nrows] anchors (fp64 integers)
+  const double* sig_c;   // [n]
+  const double* colm; const double* cols; int chunks;   // exact path column partials
+  const double* lr_in;   // exact path rows
+  const double* r; const double* c; const double* logr; const double* logc;   // r, logr: local rows
+  const double* gcur;    // [nrows + n] current gradient (nullable)
+  const double* pcur;    // [nrows + n] current direction (nullable)
+  // outputs
+  double* lm;            // [nrows + n] log marginals (rows then cols)
+  double* m;             // [nrows + n] marginals
+  double* s;             // [nrows + n] Sinkhorn direction
+  double* g;             // [nrows + n] gradient
+  double* blockpart;     // [gridDim][kNumScalars]
+  unsigned int* ticket;
+  double* scalars_dev;   // [kNumScalars]
+  double* scalars_host;  // mapped host (nullable)
+  int* prep_flag;        // nullable: added to SC_BAD, then reset to 0
+  int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
+};
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+
+enum PrepMode : int {
+  PREP_CUR = 0,         // A = U + u, B = V + v -> params
+  PREP_AB = 16,         // A, B given (rows/cols) -> params
+  PREP_TRIAL = 1,       // tu = u + alpha p_u, tv = v + alpha p_v ; A = U + tu, B = V + tv
+  PREP_NEWDIR = 2,      // p = -s + beta*pprev  (or -s if beta==0 and reset)
+  PREP_SK_ROW = 4,      // u += log r - lr  (Sinkhorn odd half-step)
+  PREP_SK_COL = 8       // v += log c - lc
+};
+struct PrepArgs {
+  int64_t n, nrows;
+  int mode;
+  double alpha, beta;
+  const double* U; const double* V;   // cumulative (rows local, cols global)
+  double* u; double* v;               // step potentials (in place for Sinkhorn)
+  double* tu; double* tv;             // trial potentials
+  double* p;                          // [nrows + n] direction (written in NEWDIR)
+  const double* s;                    // [nrows + n]
+  const double* pprev;                // [nrows + n]
+  const double* lm;                   // [nrows + n] current log marginals (Sinkhorn)
+  const double* logr; const double* logc;
+  const double* rho_r; const double* sig_c;
+  const double* Ain; const double* Bin;   // PREP_AB
+  double* Aout; double* Bout;         // fp64 bases (for the exact path)
+  float4* rowp; float4* colp;
+  int* flag;                          // set to 1 when |a2|,|b2| >= 2^15
+};
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
+
+// misc vector kernels
+cudaError_t launch_setup(int64_t n, const double* r, double* logr, double* rho, cudaStream_t st);
+cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t st); // y = a x + b y
+cudaError_t launch_add_scalar(int64_t n, double d, double* y, cudaStream_t st);
+cudaError_t launch_fill(int64_t n, double v, double* y, cudaStream_t st);
+// deterministic dot products: out[k] = sum_i x_k[i] * y_k[i] for up to 4 pairs
+cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,
+                        double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
+                        cudaStream_t st);
+// rounding (fp64, once per solve)
+struct RoundArgs {
+  const void* C; int64_t ldc; int c_f64;
+  const float* X; const float* Y; int d; float scale; int otf;
+  int64_t n, nrows;
+  const double* A;      // rows: U + log x
+  const double* B;      // cols: V (R2) or V + log y (R3, plan)
+  const double* invx;   // rows: 1/x
+  double gbar;
+  double* colF1; double* colcost; int chunks;   // R2 partials [chunks][n]
+  const double* ec;     // err_c [n]
+  double* er;           // err_r [nrows]
+  double* rowF2; double* rowcost2; double* rowcorr;
+  float* plan; double inv_ner;
+};
+cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
+                              double* logx, double* Aout, cudaStream_t st);
+cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t st);
+cudaError_t launch_round_cols(const RoundArgs& a, cudaStream_t st);
+cudaError_t launch_round_rows3(const RoundArgs& a, cudaStream_t st);
+cudaError_t launch_round_plan(const RoundArgs& a, cudaStream_t st);
+cudaError_t launch_round_combine_cols(const RoundArgs& a, const double* c, const double* V, double* Bout,
+                                      double* ec, double* blockpart, unsigned int* ticket,
+                                      double* out_dev, double* out_host, cudaStream_t st);
+cudaError_t launch_round_combine_rows(const RoundArgs& a, const double* r, double* blockpart,
+                                      unsigned int* ticket, double* out_dev, double* out_host,
+                                      cudaStream_t st);
+
+}  // namespace mdot

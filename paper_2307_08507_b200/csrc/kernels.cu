@@ -1,0 +1,759 @@
+// paper_2307_08507_b200/csrc/kernels.cu -- sm_100a kernels of the MDOT-PNCG
+// hot path (arxiv 2307.08507).  No tensor cores: the path is an exp-reduce
+// over the n x n cost, bound by HBM for a materialised C.
+//
+//   k_eval_fast   fused row+column marginal evaluation:
+//                 r(P)_i = sum_j P_ij, c(P)_j = sum_i P_ij for
+//                 P_ij = exp(A_i + B_j - gbar C_ij)
+//   k_exact_*     fp64 two-pass online log-sum-exp evaluator (fallback /
+//                 fp64-P mode)
+//   k_finalize    partial reduction + O(n) update: log marginals, Sinkhorn
+//                 direction s, gradient,
+//                 L1, rho, the CG inner products
+//                 and phi'(alpha), deterministic reductions.
+//   k_prep        direction update p = -s + beta p_prev,
+//                 trial potentials u + alpha p, Sinkhorn
+//                 half-steps, exponent split.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace mdot {
+
+#define L2E_D 1.4426950408889634
+#define LN2_D 0.6931471805599453
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float ld_stream1(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float f4get(const float4& v, int q) {
+  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// Reduce 4 per-lane values (one per row) across the warp with a transposing
+// butterfly: 3 fp64 shuffles per row instead of 10.  On return, lanes with
+// (lane & 7) == 0 hold the total of row ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1).
+__device__ __forceinline__ double warp_reduce4(double v0, double v1, double v2, double v3, int lane) {
+  const bool up = lane & 16;
+  double k0 = up ? v2 : v0, k1 = up ? v3 : v1;
+  double s0 = up ? v0 : v2, s1 = up ? v1 : v3;
+  k0 += shfl_xor_d(s0, 16);
+  k1 += shfl_xor_d(s1, 16);
+  const bool up2 = lane & 8;
+  double kk = up2 ? k1 : k0, ss = up2 ? k0 : k1;
+  kk += shfl_xor_d(ss, 8);
+  kk += shfl_xor_d(kk, 4);
+  kk += shfl_xor_d(kk, 2);
+  kk += shfl_xor_d(kk, 1);
+  return kk;
+}
+
+// ---------------------------------------------------------------------------
+// Fused evaluation.  CTA = (col tile tc of 256 columns) x (row tile tr of
+// tile_m rows); 8 warps; lane owns columns j0 + 4*lane + {0..3} and
+// j0 + 128 + 4*lane + {0..3}; warp w walks rows i0 + 32*k + 4*w + {0..3}.
+// Per entry (7 FP32 + 1 MUFU):
+//   s = ah_i + bh_j                      (exact: both on a 2^-8 grid)
+//   zh = fmaf(-gh, C_ij, s)              (one rounding of the cancellation)
+//   t  = fmaf(-gl, C_ij, al_i + bl_j)
+//   e  = ex2(zh + t)
+//   row_i += e * T_j ;  col_j += e * S_i
+// Row sums are reduced across lanes per 4 rows (fp64 butterfly); column
+// sums are fp32 over 8 rows, then fp64, then fp64 across warps in smem.
+// ---------------------------------------------------------------------------
+template <int KIND, bool VEC4>
+__global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t j0 = (int64_t)blockIdx.x * kTileN;
+  const int64_t i0 = (int64_t)blockIdx.y * a.tile_m;
+  const int64_t n = a.n, nrows = a.nrows;
+  const bool full_cols = (j0 + kTileN <= n);
+
+  __shared__ double sred[kWarps][kTileN];
+  // on-the-fly cost: Y tile transposed [d][256]
+  extern __shared__ float sdyn[];
+
+  float bh[8], bl[8], T[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+    if (j < n) {
+      const float4 cp = a.colp[j];
+      bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+    } else {
+      bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
+    }
+  }
+
+  if (KIND == 1) {
+    // stage Y[j0:j0+256, :] transposed into smem: sY[k*256 + t]
+    float* sY = sdyn;
+    for (int idx = threadIdx.x; idx < kTileN * a.d; idx += kThreads) {
+      const int t = idx / a.d, k = idx % a.d;
+      const int64_t j = j0 + t;
+      sY[k * kTileN + t] = (j < n) ? a.Y[j * a.d + k] : 0.f;
+    }
+    __syncthreads();
+  }
+
+  const float gh = a.gh, gl = a.gl;
+  double cacc64[8];
+  float cacc32[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { cacc64[q] = 0.0; cacc32[q] = 0.f; }
+
+  const int64_t tile_end = (i0 + a.tile_m < nrows) ? i0 + a.tile_m : nrows;
+  int flush = 0;
+  for (int64_t ib = i0 + 4 * warp; ib < tile_end; ib += kWarps * kUnroll) {
+    float cv[kUnroll][8];
+    float4 rp[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = ib + u;
+      if (i < tile_end) {
+        rp[u] = a.rowp[i];
+        if (KIND == 0) {
+          const float* crow = a.C + i * a.ldc + j0 + 4 * lane;
+          if (VEC4 && full_cols) {
+            const float4 x0 = ld_stream4(crow);
+            const float4 x1 = ld_stream4(crow + 128);
+            cv[u][0] = x0.x; cv[u][1] = x0.y; cv[u][2] = x0.z; cv[u][3] = x0.w;
+            cv[u][4] = x1.x; cv[u][5] = x1.y; cv[u][6] = x1.z; cv[u][7] = x1.w;
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+              cv[u][q] = (j < n) ? ld_stream1(a.C + i * a.ldc + j) : 0.f;
+            }
+          }
+        } else {
+          // C_ij = fl32(fmaf chain over k of (x_ik - y_jk)^2) * scale  (Z22)
+          float acc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+          const float* xr = a.X + i * a.d;
+          for (int k = 0; k < a.d; ++k) {
+            const float xk = __ldg(xr + k);
+            const float4 y0 = *reinterpret_cast<const float4*>(sdyn + k * kTileN + 4 * lane);
+            const float4 y1 = *reinterpret_cast<const float4*>(sdyn + k * kTileN + 128 + 4 * lane);
+            float dk;
+            dk = __fsub_rn(xk, y0.x); acc[0] = __fmaf_rn(dk, dk, acc[0]);
+            dk = __fsub_rn(xk, y0.y); acc[1] = __fmaf_rn(dk, dk, acc[1]);
+            dk = __fsub_rn(xk, y0.z); acc[2] = __fmaf_rn(dk, dk, acc[2]);
+            dk = __fsub_rn(xk, y0.w); acc[3] = __fmaf_rn(dk, dk, acc[3]);
+            dk = __fsub_rn(xk, y1.x); acc[4] = __fmaf_rn(dk, dk, acc[4]);
+            dk = __fsub_rn(xk, y1.y); acc[5] = __fmaf_rn(dk, dk, acc[5]);
+            dk = __fsub_rn(xk, y1.z); acc[6] = __fmaf_rn(dk, dk, acc[6]);
+            dk = __fsub_rn(xk, y1.w); acc[7] = __fmaf_rn(dk, dk, acc[7]);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cv[u][q] = __fmul_rn(acc[q], a.scale);
+        }
+      } else {
+        rp[u] = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cv[u][q] = 0.f;
+      }
+    }
+
+    double rs[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      float rsum = 0.f;
+      const float ah = rp[u].x, al = rp[u].y, S = rp[u].z;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float cij = cv[u][q];
+        const float s = ah + bh[q];
+        const float zh = fmaf(-gh, cij, s);
+        const float t = fmaf(-gl, cij, al + bl[q]);
+        const float e = ex2_approx(zh + t);
+        rsum = fmaf(e, T[q], rsum);
+        cacc32[q] = fmaf(e, S, cacc32[q]);
+      }
+      rs[u] = rsum;
+    }
+    // row totals (fp64 butterfly over the warp)
+    {
+      const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
+      const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+      if ((lane & 7) == 0 && i < tile_end) a.rowpart[(int64_t)blockIdx.x * nrows + i] = tot;
+    }
+    if (++flush == 2) {   // 8 rows of fp32 column sums -> fp64
+      flush = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { cacc64[q] += (double)cacc32[q]; cacc32[q] = 0.f; }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cacc64[q] += (double)cacc32[q];
+
+  // column totals of this tile: sum over the 8 warps (fixed order)
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sred[warp][4 * lane + (q & 3) + 128 * (q >> 2)] = cacc64[q];
+  __syncthreads();
+  {
+    const int t = threadIdx.x;
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) tot += sred[w][t];
+    const int64_t j = j0 + t;
+    if (j < n) a.colpart[(int64_t)blockIdx.y * n + j] = tot;
+  }
+}
+
+template <int KIND, bool VEC4>
+static cudaError_t launch_fast_t(const EvalArgs& a, cudaStream_t st) {
+  dim3 grid(a.n_col_tiles, a.n_row_tiles);
+  size_t smem = (KIND == 1) ? (size_t)kTileN * a.d * sizeof(float) : 0;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_eval_fast<KIND, VEC4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  k_eval_fast<KIND, VEC4><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st) {
+  if (kind == 0) {
+    const bool vec4 = (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
+    return vec4 ? launch_fast_t<0, true>(a, st) : launch_fast_t<0, false>(a, st);
+  }
+  return launch_fast_t<1, false>(a, st);
+}
+
+// ---------------------------------------------------------------------------
+// Exact fp64 evaluator: z = (A_i + B_j) - gbar * C_ij in fp64, online
+// log-sum-exp with fp64 exp.  Rows: one warp per row.  Columns: one thread per
+// column over a chunk of rows, (max, sum) partials per chunk.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void lse_push(double& m, double& s, double z) {
+  if (z <= m) {
+    s += exp(z - m);
+  } else {
+    s = s * exp(m - z) + 1.0;
+    m = z;
+  }
+}
+
+__device__ __forceinline__ void lse_merge(double& m, double& s, double m2, double s2) {
+  if (s2 == 0.0) return;
+  if (s == 0.0) { m = m2; s = s2; return; }
+  if (m2 <= m) {
+    s += s2 * exp(m2 - m);
+  } else {
+    s = s * exp(m - m2) + s2;
+    m = m2;
+  }
+}
+
+__device__ __forceinline__ double exact_cost(const ExactArgs& a, int64_t i, int64_t j) {
+  if (a.otf) {
+    const float* x = a.X + i * a.d;
+    const float* y = a.Y + j * a.d;
+    float acc = 0.f;
+    for (int k = 0; k < a.d; ++k) {
+      const float dk = __fsub_rn(x[k], y[k]);
+      acc = __fmaf_rn(dk, dk, acc);
+    }
+    return (double)__fmul_rn(acc, a.scale);
+  }
+  if (a.c_f64) return reinterpret_cast<const double*>(a.C)[i * a.ldc + j];
+  return (double)reinterpret_cast<const float*>(a.C)[i * a.ldc + j];
+}
+
+__global__ void k_exact_rows(ExactArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= a.nrows) return;
+  const double Ai = a.A[i];
+  double m = -INFINITY, s = 0.0;
+  for (int64_t j = lane; j < a.n; j += 32) {
+    const double z = (Ai + a.B[j]) - a.gbar * exact_cost(a, i, j);
+    lse_push(m, s, z);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const double s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    lse_merge(m, s, m2, s2);
+  }
+  if (lane == 0) a.lr[i] = m + log(s);
+}
+
+__global__ void k_exact_cols(ExactArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int64_t rows_per = (a.nrows + a.chunks - 1) / a.chunks;
+  const int64_t ib = chunk * rows_per;
+  const int64_t ie = (ib + rows_per < a.nrows) ? ib + rows_per : a.nrows;
+  if (j >= a.n) return;
+  const double Bj = a.B[j];
+  double m = -INFINITY, s = 0.0;
+  for (int64_t i = ib; i < ie; ++i) {
+    const double z = (a.A[i] + Bj) - a.gbar * exact_cost(a, i, j);
+    lse_push(m, s, z);
+  }
+  a.colm[(int64_t)chunk * a.n + j] = m;
+  a.cols[(int64_t)chunk * a.n + j] = s;
+}
+
+cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st) {
+  const int wpb = 8;
+  k_exact_rows<<<(unsigned)((a.nrows + wpb - 1) / wpb), wpb * 32, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((a.n + 255) / 256), a.chunks);
+  k_exact_cols<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Block reduction of kNumScalars doubles + deterministic last-block combine.
+// ---------------------------------------------------------------------------
+template <int NS>
+__device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, unsigned int* ticket,
+                                         double* out_dev, double* out_host) {
+  __shared__ double sm[32][NS];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    double x = v[k];
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    if (lane == 0) sm[warp][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NS) {
+    double x = 0.0;
+    for (int w = 0; w < nw; ++w) x += sm[w][threadIdx.x];
+    blockpart[(int64_t)blockIdx.x * NS + threadIdx.x] = x;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (threadIdx.x < NS) {
+      double x = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b)
+        x += *((volatile double*)&blockpart[(int64_t)b * NS + threadIdx.x]);
+      out_dev[threadIdx.x] = x;
+      if (out_host) out_host[threadIdx.x] = x;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finalize: marginals, s, grad, scalars
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot_items = a.nrows + a.n;
+  double v[kNumScalars];
+#pragma unroll
+  for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
+  if (k < tot_items) {
+    const bool is_row = k < a.nrows;
+    double lm, bad = 0.0;
+    if (a.from_partials) {
+      double tot = 0.0;
+      if (is_row) {
+        for (int t = 0; t < a.n_col_tiles; ++t) tot += a.rowpart[(int64_t)t * a.nrows + k];
+      } else {
+        const int64_t j = k - a.nrows;
+        for (int t = 0; t < a.n_row_tiles; ++t) tot += a.colpart[(int64_t)t * a.n + j];
+      }
+      const double anchor = is_row ? a.rho_r[k] : a.sig_c[k - a.nrows];
+      lm = log(tot) + anchor * LN2_D;
+      // fp32 entry range guard (K1 numerics): totals far from 1 in
+      // anchored units mean under/overflowed entries -> exact re-evaluation
+      if (!(tot > 7.888609052210118e-31 && tot < 1.2676506002282294e30)) bad = 1.0;
+    } else {
+      if (is_row) {
+        lm = a.lr_in[k];
+      } else {
+        const int64_t j = k - a.nrows;
+        double m = -INFINITY, s = 0.0;
+        for (int c = 0; c < a.chunks; ++c)
+          lse_merge(m, s, a.colm[(int64_t)c * a.n + j], a.cols[(int64_t)c * a.n + j]);
+        lm = m + log(s);
+      }
+      if (!isfinite(lm)) bad = 1.0;
+    }
+    const double tgt = is_row ? a.r[k] : a.c[k - a.nrows];
+    const double ltg = is_row ? a.logr[k] : a.logc[k - a.nrows];
+    const double mm = exp(lm);
+    const double g = mm - tgt;
+    const double s = lm - ltg;
+    a.lm[k] = lm;
+    a.m[k] = mm;
+    a.s[k] = s;
+    a.g[k] = g;
+    const double gc = a.gcur ? a.gcur[k] : 0.0;
+    const double pc = a.pcur ? a.pcur[k] : 0.0;
+    v[is_row ? SC_MASS : SC_MASSC] = mm;
+    v[SC_L1] = fabs(g);
+    v[SC_RHO] = tgt - mm + mm * s;            // D_h(y|x) term with y = m, x = tgt (Z1)
+    v[SC_SG] = s * g;
+    v[SC_GCS] = gc * s;
+    v[SC_PCG] = pc * g;
+    v[SC_PRC] = pc * tgt;
+    v[SC_GG] = g * g;
+    v[SC_GCG] = gc * g;
+    v[SC_BAD] = bad;
+    v[SC_L1R] = is_row ? fabs(g) : 0.0;
+  }
+  if (a.prep_flag && k == 0) {
+    v[SC_BAD] += (double)(*a.prep_flag);
+    *a.prep_flag = 0;
+  }
+  block_reduce_and_publish<kNumScalars>(v, a.blockpart, a.ticket, a.scalars_dev, a.scalars_host);
+}
+
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
+  const int64_t items = a.nrows + a.n;
+  const unsigned blocks = (unsigned)((items + 255) / 256);
+  k_finalize<<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// prep: direction, trial potentials, Sinkhorn half-steps, exponent split
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 split_param(double base, double anchor, int* flag) {
+  const double a2 = base * L2E_D - anchor;
+  const double ah = rint(a2 * 256.0) * (1.0 / 256.0);
+  if (!(fabs(ah) < 32768.0)) {
+    if (flag) *flag = 1;
+  }
+  const double al = a2 - ah;
+  return make_float4((float)ah, (float)al, (float)exp2(anchor), 0.f);
+}
+
+__global__ void k_prep(PrepArgs a) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.nrows + a.n) return;
+  const bool is_row = k < a.nrows;
+  const int64_t idx = is_row ? k : k - a.nrows;
+  double pk = 0.0;
+  if (a.mode & PREP_NEWDIR) {
+    pk = -a.s[k] + (a.beta != 0.0 ? a.beta * a.pprev[k] : 0.0);
+    a.p[k] = pk;
+  } else if (a.mode & PREP_TRIAL) {
+    pk = a.p[k];
+  }
+  double base;
+  if (is_row) {
+    if (a.mode & PREP_TRIAL) {
+      const double t = a.u[idx] + a.alpha * pk;
+      a.tu[idx] = t;
+      base = a.U[idx] + t;
+    } else if (a.mode & PREP_SK_ROW) {
+      const double t = a.u[idx] + (a.logr[idx] - a.lm[k]);
+      a.u[idx] = t;
+      base = a.U[idx] + t;
+    } else if (a.mode & PREP_AB) {
+      base = a.Ain[idx];
+    } else {
+      base = a.U[idx] + a.u[idx];
+    }
+    if (a.Aout) a.Aout[idx] = base;
+    a.rowp[idx] = split_param(base, a.rho_r[idx], a.flag);
+  } else {
+    if (a.mode & PREP_TRIAL) {
+      const double t = a.v[idx] + a.alpha * pk;
+      a.tv[idx] = t;
+      base = a.V[idx] + t;
+    } else if (a.mode & PREP_SK_COL) {
+      const double t = a.v[idx] + (a.logc[idx] - a.lm[k]);
+      a.v[idx] = t;
+      base = a.V[idx] + t;
+    } else if (a.mode & PREP_AB) {
+      base = a.Bin[idx];
+    } else {
+      base = a.V[idx] + a.v[idx];
+    }
+    if (a.Bout) a.Bout[idx] = base;
+    a.colp[idx] = split_param(base, a.sig_c[idx], a.flag);
+  }
+}
+
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
+  const int64_t items = a.nrows + a.n;
+  k_prep<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// misc
+// ---------------------------------------------------------------------------
+__global__ void k_setup(int64_t n, const double* r, double* logr, double* rho) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double lr = log(r[i]);
+  logr[i] = lr;
+  double a = rint(0.5 * lr * L2E_D);
+  if (a < -60.0) a = -60.0;
+  if (a > 0.0) a = 0.0;
+  rho[i] = a;
+}
+cudaError_t launch_setup(int64_t n, const double* r, double* logr, double* rho, cudaStream_t st) {
+  k_setup<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, r, logr, rho);
+  return cudaGetLastError();
+}
+
+__global__ void k_axpby(int64_t n, double a, const double* x, double b, double* y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = a * x[i] + b * y[i];
+}
+cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_axpby<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, a, x, b, y);
+  return cudaGetLastError();
+}
+
+__global__ void k_add_scalar(int64_t n, double d, double* y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += d;
+}
+cudaError_t launch_add_scalar(int64_t n, double d, double* y, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_add_scalar<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, y);
+  return cudaGetLastError();
+}
+
+__global__ void k_fill(int64_t n, double v, double* y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = v;
+}
+cudaError_t launch_fill(int64_t n, double v, double* y, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_fill<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, v, y);
+  return cudaGetLastError();
+}
+
+struct DotPtrs { const double* x[4]; const double* y[4]; };
+__global__ void k_dots(int64_t n, int npairs, DotPtrs P, double* blockpart, unsigned int* ticket,
+                       double* out_dev, double* out_host) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < n) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < npairs) v[k] = P.x[k][i] * P.y[k][i];
+  }
+  block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, out_host);
+}
+cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,
+                        double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
+                        cudaStream_t st) {
+  DotPtrs P;
+  for (int k = 0; k < 4; ++k) {
+    P.x[k] = k < npairs ? xs[k] : nullptr;
+    P.y[k] = k < npairs ? ys[k] : nullptr;
+  }
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  k_dots<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(n, npairs, P, blockpart, ticket, out_dev, out_host);
+  return cudaGetLastError();
+}
+
+// x_i = min(r_i / r_i(F), 1) in log form; A' = U + log x
+__global__ void k_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
+                             double* logx, double* Aout) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double lx = logr[i] - lr[i];
+  if (lx > 0.0) lx = 0.0;
+  logx[i] = lx;
+  Aout[i] = U[i] + lx;
+}
+cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
+                              double* logx, double* Aout, cudaStream_t st) {
+  k_round_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, logr, lr, U, logx, Aout);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Rounding onto U(r,c) (Altschuler et al. Alg. 2 as restated in
+// SPEC.md:331) in fp64 -- once per solve, so the entries are recomputed in
+// fp64 with exp() instead of the fp32 streaming path.
+//   F = exp(U + V - gbar C) (final plan),  x = min(r / r(F), 1)
+//   R2 (columns): c(F')_j = sum_i x_i F_ij ;  sum_i C_ij F_ij (cost of F)
+//   y = min(c / c(F'), 1); F'' = D(x) F D(y); err_c = c - y * c(F')
+//   R3 (rows):    r(F'')_i, sum_j C_ij F''_ij, sum_j C_ij err_c_j
+//   <C,G> = <C,F''> + err_r^T C err_c / |err_r|_1
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double round_cost(const RoundArgs& a, int64_t i, int64_t j) {
+  if (a.otf) {
+    const float* x = a.X + i * a.d;
+    const float* y = a.Y + j * a.d;
+    float acc = 0.f;
+    for (int k = 0; k < a.d; ++k) {
+      const float dk = __fsub_rn(x[k], y[k]);
+      acc = __fmaf_rn(dk, dk, acc);
+    }
+    return (double)__fmul_rn(acc, a.scale);
+  }
+  if (a.c_f64) return reinterpret_cast<const double*>(a.C)[i * a.ldc + j];
+  return (double)reinterpret_cast<const float*>(a.C)[i * a.ldc + j];
+}
+
+__global__ void k_round_cols(RoundArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int64_t rows_per = (a.nrows + a.chunks - 1) / a.chunks;
+  const int64_t ib = chunk * rows_per;
+  const int64_t ie = (ib + rows_per < a.nrows) ? ib + rows_per : a.nrows;
+  if (j >= a.n) return;
+  const double Bj = a.B[j];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t i = ib; i < ie; ++i) {
+    const double cij = round_cost(a, i, j);
+    const double f1 = exp((a.A[i] + Bj) - a.gbar * cij);   // F'_ij = x_i F_ij
+    s1 += f1;
+    s2 += cij * f1 * a.invx[i];                               // C_ij F_ij
+  }
+  a.colF1[(int64_t)chunk * a.n + j] = s1;
+  a.colcost[(int64_t)chunk * a.n + j] = s2;
+}
+
+__global__ void k_round_rows3(RoundArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= a.nrows) return;
+  const double Ai = a.A[i];
+  double s = 0.0, cs = 0.0, cr = 0.0;
+  for (int64_t j = lane; j < a.n; j += 32) {
+    const double cij = round_cost(a, i, j);
+    const double f2 = exp((Ai + a.B[j]) - a.gbar * cij);   // F''_ij
+    s += f2;
+    cs += cij * f2;
+    cr += cij * a.ec[j];
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, off);
+    cs += __shfl_xor_sync(0xffffffffu, cs, off);
+    cr += __shfl_xor_sync(0xffffffffu, cr, off);
+  }
+  if (lane == 0) {
+    a.rowF2[i] = s;
+    a.rowcost2[i] = cs;
+    a.rowcorr[i] = cr;
+  }
+}
+
+__global__ void k_round_plan(RoundArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= a.n || i >= a.nrows) return;
+  const double cij = round_cost(a, i, j);
+  double gij = exp((a.A[i] + a.B[j]) - a.gbar * cij);
+  if (a.inv_ner > 0.0) gij += a.er[i] * a.ec[j] * a.inv_ner;
+  a.plan[i * a.n + j] = (float)gij;
+}
+
+// columns: c(F') total, y, B'' = V + log y, err_c; scalars: [cost_F, sum c(F'), 0, 0]
+__global__ void k_round_combine_cols(RoundArgs a, const double* c, const double* V, double* Bout,
+                                     double* ec, double* blockpart, unsigned int* ticket,
+                                     double* out_dev, double* out_host) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (j < a.n) {
+    double cf = 0.0, cc = 0.0;
+    for (int k = 0; k < a.chunks; ++k) {
+      cf += a.colF1[(int64_t)k * a.n + j];
+      cc += a.colcost[(int64_t)k * a.n + j];
+    }
+    const double y = fmin(c[j] / cf, 1.0);
+    Bout[j] = V[j] + log(y);
+    ec[j] = c[j] - y * cf;
+    v[0] = cc;
+    v[1] = cf;
+  }
+  block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, out_host);
+}
+
+// rows: err_r; scalars [|err_r|_1, <C,F''>, err_r . (C err_c), sum r(F'')]
+__global__ void k_round_combine_rows(RoundArgs a, const double* r, double* blockpart,
+                                     unsigned int* ticket, double* out_dev, double* out_host) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < a.nrows) {
+    const double er = r[i] - a.rowF2[i];
+    a.er[i] = er;
+    v[0] = fabs(er);
+    v[1] = a.rowcost2[i];
+    v[2] = er * a.rowcorr[i];
+    v[3] = a.rowF2[i];
+  }
+  block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, out_host);
+}
+
+cudaError_t launch_round_cols(const RoundArgs& a, cudaStream_t st) {
+  dim3 grid((unsigned)((a.n + 255) / 256), a.chunks);
+  k_round_cols<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_round_rows3(const RoundArgs& a, cudaStream_t st) {
+  k_round_rows3<<<(unsigned)((a.nrows + 7) / 8), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_round_plan(const RoundArgs& a, cudaStream_t st) {
+  dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)a.nrows);
+  k_round_plan<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_round_combine_cols(const RoundArgs& a, const double* c, const double* V, double* Bout,
+                                      double* ec, double* blockpart, unsigned int* ticket,
+                                      double* out_dev, double* out_host, cudaStream_t st) {
+  k_round_combine_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a, c, V, Bout, ec, blockpart,
+                                                                      ticket, out_dev, out_host);
+  return cudaGetLastError();
+}
+cudaError_t launch_round_combine_rows(const RoundArgs& a, const double* r, double* blockpart,
+                                      unsigned int* ticket, double* out_dev, double* out_host,
+                                      cudaStream_t st) {
+  k_round_combine_rows<<<(unsigned)((a.nrows + 255) / 256), 256, 0, st>>>(a, r, blockpart, ticket,
+                                                                          out_dev, out_host);
+  return cudaGetLastError();
+}
+
+__global__ void k_exp_neg(int64_t n, const double* x, double* y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = exp(-x[i]);
+}
+cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t st) {
+  k_exp_neg<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, x, y);
+  return cudaGetLastError();
+}
+
+}  // namespace mdot

@@ -1,0 +1,778 @@
+// paper_2307_08507_b200/csrc/solver.cu -- host control of the MDOT-PNCG hot
+// path and the C ABI of include/mdot.h.
+//
+// Control flow:
+//   mdot_solve  -> setup (log r, log c, anchors)                 a1
+//               -> for each MD step t (Alg. 1)  a2
+//                    warm start, project (PNCG / Sinkhorn / NCG)  a3-a8
+//                    U += u, V += v, gauge centring               a9
+//               -> rounding + cost                 a10
+// Every O(n^2) pass runs in kernels.cu; this file holds only O(1) scalar
+// decisions (line-search logic, beta, stop tests) on values the finalize
+// kernel publishes to mapped pinned memory.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <time.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/mdot.h"
+#include "internal.cuh"
+#include "solver.h"
+
+namespace mdot {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+static double now_s() {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__, \
+                cudaGetErrorString(e_));                                             \
+      return e_ == cudaErrorMemoryAllocation ? MDOT_ENOMEM : MDOT_ECUDA;             \
+    }                                                                                \
+  } while (0)
+
+#define CKS(call)                        \
+  do {                                   \
+    mdot_status s_ = (call);             \
+    if (s_ != MDOT_OK) return s_;        \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Workspace
+// ---------------------------------------------------------------------------
+mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
+  st = stream;
+  n = n_;
+  nrows = nrows_;
+  const int64_t items = nrows + n;
+  // evaluation grid: 256-column tiles, row tiles sized for >= ~4 CTAs per SM
+  eval.n = n;
+  eval.nrows = nrows;
+  eval.n_col_tiles = (int)((n + kTileN - 1) / kTileN);
+  int tile_m = 256;
+  while (tile_m > 32 && (int64_t)eval.n_col_tiles * ((nrows + tile_m - 1) / tile_m) < 4 * 148) tile_m /= 2;
+  eval.tile_m = tile_m;
+  eval.n_row_tiles = (int)((nrows + tile_m - 1) / tile_m);
+  chunks = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, (4 * 148 + (n + 255) / 256 - 1) / ((n + 255) / 256)));
+  const int64_t fin_blocks = (items + 255) / 256 + 4;
+
+  size_t dbl = 0;
+  auto take = [&](int64_t k) { size_t o = dbl; dbl += (size_t)((k + 31) / 32 * 32); return o; };
+  size_t o_r = take(nrows), o_c = take(n), o_logr = take(nrows), o_logc = take(n);
+  size_t o_rho = take(nrows), o_sig = take(n);
+  size_t o_U = take(nrows), o_V = take(n), o_u = take(nrows), o_v = take(n), o_tu = take(nrows), o_tv = take(n);
+  size_t o_A = take(nrows), o_B = take(n);
+  size_t o_p = take(items), o_pp = take(items);
+  size_t o_m[2][4];
+  for (int b = 0; b < 2; ++b)
+    for (int q = 0; q < 4; ++q) o_m[b][q] = take(items);
+  size_t o_rowpart = take((int64_t)eval.n_col_tiles * nrows);
+  size_t o_colpart = take((int64_t)eval.n_row_tiles * n);
+  size_t o_colm = take((int64_t)chunks * n), o_cols = take((int64_t)chunks * n);
+  size_t o_lr = take(nrows);
+  size_t o_blk = take(fin_blocks * kNumScalars);
+  size_t o_scal = take(kNumScalars * 2);
+  size_t o_aux = take(8 * items);
+  size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256;
+  cudaError_t e = cudaMallocAsync(&base, bytes, st);
+  if (e != cudaSuccess) {
+    set_error("workspace allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    return MDOT_ENOMEM;
+  }
+  double* D = reinterpret_cast<double*>(base);
+  r = D + o_r; c = D + o_c; logr = D + o_logr; logc = D + o_logc; rho_r = D + o_rho; sig_c = D + o_sig;
+  U = D + o_U; V = D + o_V; u = D + o_u; v = D + o_v; tu = D + o_tu; tv = D + o_tv;
+  A = D + o_A; B = D + o_B; p = D + o_p; pprev = D + o_pp;
+  for (int b = 0; b < 2; ++b) {
+    mg[b].lm = D + o_m[b][0]; mg[b].m = D + o_m[b][1]; mg[b].s = D + o_m[b][2]; mg[b].g = D + o_m[b][3];
+  }
+  cur = &mg[0];
+  trial = &mg[1];
+  rowpart = D + o_rowpart; colpart = D + o_colpart; colm = D + o_colm; cols = D + o_cols; lr_ex = D + o_lr;
+  blockpart = D + o_blk; scal_dev = D + o_scal; aux = D + o_aux;
+  float4* F4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(base) + dbl * sizeof(double));
+  F4 = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(F4) + 15) & ~uintptr_t(15));
+  rowp = F4;
+  colp = F4 + nrows;
+  ticket_flag = reinterpret_cast<unsigned int*>(colp + n + 8);
+  CK(cudaMemsetAsync(ticket_flag, 0, 64, st));
+  ticket = ticket_flag;
+  flag = reinterpret_cast<int*>(ticket_flag + 4);
+  CK(cudaHostAlloc(&scal_host, 64 * sizeof(double), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&scal_host_dev, scal_host, 0));
+  memset(scal_host, 0, 64 * sizeof(double));
+  eval.rowp = rowp;
+  eval.colp = colp;
+  eval.rowpart = rowpart;
+  eval.colpart = colpart;
+  return MDOT_OK;
+}
+
+void Workspace::release() {
+  if (base) cudaFreeAsync(base, st);
+  base = nullptr;
+  if (scal_host) cudaFreeHost(scal_host);
+  scal_host = nullptr;
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  ev0 = ev1 = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// One evaluation at the parameters last written by prep: fast fp32 kernel,
+// finalize, and (if the range guard fires) the exact fp64 re-evaluation.
+// ---------------------------------------------------------------------------
+mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcur, double* sc) {
+  FinalizeArgs f{};
+  f.n = n; f.nrows = nrows;
+  f.rho_r = rho_r; f.sig_c = sig_c;
+  f.r = r; f.c = c; f.logr = logr; f.logc = logc;
+  f.gcur = gcur; f.pcur = pcur;
+  f.lm = out->lm; f.m = out->m; f.s = out->s; f.g = out->g;
+  f.blockpart = blockpart; f.ticket = ticket;
+  f.scalars_dev = scal_dev; f.scalars_host = scal_host_dev;
+  f.prep_flag = flag;
+  evals++;
+  if (!exact_mode) {
+    if (time_kernels) CK(cudaEventRecord(ev0, st));
+    CK(launch_eval_fast(eval, kind_fast, st));
+    if (time_kernels) CK(cudaEventRecord(ev1, st));
+    f.from_partials = 1;
+    f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
+    f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
+    CK(launch_finalize(f, st));
+    CK(cudaStreamSynchronize(st));
+    if (time_kernels) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      kernel_ms += ms;
+      kernel_launches++;
+    }
+    memcpy(sc, scal_host, kNumScalars * sizeof(double));
+    if (sc[SC_BAD] == 0.0) return MDOT_OK;
+    fallbacks++;
+  }
+  ExactArgs x{};
+  x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
+  x.X = Xdev; x.Y = Ydev; x.d = d; x.scale = scale; x.otf = otf;
+  x.n = n; x.nrows = nrows;
+  x.A = A; x.B = B; x.gbar = gbar;
+  x.lr = lr_ex; x.colm = colm; x.cols = cols; x.chunks = chunks;
+  CK(launch_eval_exact(x, st));
+  f.from_partials = 0;
+  f.lr_in = lr_ex; f.colm = colm; f.cols = cols; f.chunks = chunks;
+  f.prep_flag = nullptr;
+  CK(launch_finalize(f, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(sc, scal_host, kNumScalars * sizeof(double));
+  if (sc[SC_BAD] != 0.0) {
+    set_error("non-finite marginals at gbar=%g on the exact fp64 evaluator", gbar);
+    return MDOT_EINSTABLE;
+  }
+  return MDOT_OK;
+}
+
+mdot_status Workspace::prep(int mode, double alpha, double beta, const double* s_dir,
+                            const double* Ain, const double* Bin) {
+  PrepArgs a{};
+  a.n = n; a.nrows = nrows; a.mode = mode; a.alpha = alpha; a.beta = beta;
+  a.U = U; a.V = V; a.u = u; a.v = v; a.tu = tu; a.tv = tv;
+  a.p = p; a.s = s_dir; a.pprev = pprev; a.lm = cur->lm;
+  a.logr = logr; a.logc = logc; a.rho_r = rho_r; a.sig_c = sig_c;
+  a.Ain = Ain; a.Bin = Bin; a.Aout = A; a.Bout = B;
+  a.rowp = rowp; a.colp = colp; a.flag = flag;
+  CK(launch_prep(a, st));
+  return MDOT_OK;
+}
+
+void Workspace::set_gamma(double gb) {
+  gbar = gb;
+  const double g2 = gb * 1.4426950408889634;
+  const float gh = (float)g2;
+  eval.gh = gh;
+  eval.gl = (float)(g2 - (double)gh);
+}
+
+// ---------------------------------------------------------------------------
+// Projections
+// ---------------------------------------------------------------------------
+static inline double stopval(const double* sc, int stop_rho) { return stop_rho ? sc[SC_RHO] : sc[SC_L1]; }
+
+// Sinkhorn, Alg. 3; one fused evaluation per half-step.
+mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  double sc[kNumScalars];
+  CKS(w.prep(PREP_CUR, 0, 0, nullptr, nullptr, nullptr));
+  CKS(w.evaluate(w.cur, nullptr, nullptr, sc));
+  if (t >= 1 && t <= 64) { res->rho0[t - 1] = sc[SC_RHO]; res->l10[t - 1] = sc[SC_L1]; }
+  int64_t k = 0;
+  mdot_status st = MDOT_OK;
+  while (stopval(sc, o.stop) > o.eps) {
+    if (w.evals >= o.max_evals) { st = MDOT_ENOCONV; break; }
+    ++k;
+    CKS(w.prep((k % 2 == 1) ? PREP_SK_ROW : PREP_SK_COL, 0, 0, nullptr, nullptr, nullptr));
+    CKS(w.evaluate(w.cur, nullptr, nullptr, sc));
+    res->iterations++;
+    if (t >= 1 && t <= 64) res->iters_step[t - 1]++;
+  }
+  res->l1_final = sc[SC_L1];
+  res->rho_final = sc[SC_RHO];
+  w.last_mass = sc[SC_MASS];
+  return st;
+}
+
+// PNCG, Alg. 2 with the line search of Appx. C
+// and readings Z5-Z10.
+mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  const bool ncg = o.projector == MDOT_PROJ_NCG;
+  double sc[kNumScalars], ts[kNumScalars];
+  CKS(w.prep(PREP_CUR, 0, 0, nullptr, nullptr, nullptr));
+  CKS(w.evaluate(w.cur, nullptr, nullptr, sc));
+  if (t >= 1 && t <= 64) { res->rho0[t - 1] = sc[SC_RHO]; res->l10[t - 1] = sc[SC_L1]; }
+  double mass = sc[SC_MASS];
+  double S_sg = sc[SC_SG], S_gcs = 0, S_pcg = 0, S_gg = sc[SC_GG], S_gcg = 0;
+  double dphi0_prev = 0, sg_prev = 0, gg_prev = 0;
+  double alpha_prev = 1.0;
+  const double c1 = o.c1, c2 = o.c2;
+  const double noise = w.exact_mode ? 1e-14 : 6e-8;   // decrease-safeguard tolerance (Z9)
+  int64_t k = 0;
+  mdot_status st = MDOT_OK;
+  while (stopval(sc, o.stop) > o.eps) {
+    if (w.evals >= o.max_evals) { st = MDOT_ENOCONV; break; }
+    ++k;
+    // beta_k (Z6) from scalars of the current iterate
+    double beta = 0.0;
+    if (k > 1) {
+      double num, den;
+      if (ncg) { num = S_gg - S_gcg; den = gg_prev; }
+      else if (o.beta == MDOT_BETA_PPR) { num = S_sg - S_gcs; den = -dphi0_prev; }
+      else if (o.beta == MDOT_BETA_PPR_AF) { num = S_sg - S_gcs; den = sg_prev; }
+      else { num = S_sg; den = sg_prev; }
+      beta = (fabs(den) > 1e-300) ? num / den : 0.0;
+    }
+    const double* dir = ncg ? w.cur->g : w.cur->s;
+    const double dg = ncg ? S_gg : S_sg;            // <dir, g>
+    double dphi0 = -dg + beta * S_pcg;              // <p, g> with p = -dir + beta p_prev
+    if (!(dphi0 < 0.0)) { beta = 0.0; dphi0 = -dg; res->resets++; }   // Z5
+    double alpha = (k == 1) ? 1.0 : std::min(4.0, std::max(0.25, alpha_prev));  // Z8
+    CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, beta, dir, nullptr, nullptr));
+    int accepted = 0, attempt = 0;
+    double dphi_a = 0;
+    while (!accepted && attempt < 2) {
+      double lo = 0.0, dlo = dphi0, hi = 0.0, dhi = 0.0;
+      int have_hi = 0, doublings = 0;
+      for (int tr = 0; tr < o.ls_max_trials; ++tr) {
+        if (tr > 0) CKS(w.prep(PREP_TRIAL, alpha, 0, nullptr, nullptr, nullptr));
+        CKS(w.evaluate(w.trial, w.cur->g, w.p, ts));
+        res->ls_evaluations++;
+        dphi_a = ts[SC_PCG];                                       // phi'(alpha)
+        const double dval = (ts[SC_MASS] - mass) - alpha * ts[SC_PRC];
+        const int wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
+        const int decrease = dval <= noise * std::max(1.0, mass);
+        if (wolfe && decrease) { accepted = 1; break; }
+        if (dphi_a < 0.0 && decrease) { lo = alpha; dlo = dphi_a; }
+        else { hi = alpha; dhi = dphi_a; have_hi = 1; }
+        if (!have_hi) {
+          if (++doublings > 60) break;
+          alpha *= 2.0;
+        } else if (dhi > dlo) {
+          const double a_sec = (lo * dhi - hi * dlo) / (dhi - dlo);
+          alpha = 0.5 * a_sec + 0.5 * (hi + lo) / 2.0;
+        } else {
+          alpha = 0.5 * (lo + hi);
+        }
+      }
+      if (accepted) break;
+      attempt++;                                                      // Z10
+      res->ls_restarts++;
+      dphi0 = -dg;
+      alpha = 1.0;
+      if (attempt < 2) CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, 0.0, dir, nullptr, nullptr));
+    }
+    if (!accepted) {
+      set_error("line search failed twice at MD step %d, iteration %lld", t, (long long)k);
+      st = MDOT_ELINESEARCH;
+      break;
+    }
+    // accept (Alg. 2 lines 11-13): the trial becomes the iterate
+    std::swap(w.u, w.tu);
+    std::swap(w.v, w.tv);
+    std::swap(w.cur, w.trial);
+    std::swap(w.p, w.pprev);
+    dphi0_prev = dphi0;
+    sg_prev = S_sg;
+    gg_prev = S_gg;
+    S_sg = ts[SC_SG]; S_gcs = ts[SC_GCS]; S_pcg = ts[SC_PCG]; S_gg = ts[SC_GG]; S_gcg = ts[SC_GCG];
+    mass = ts[SC_MASS];
+    memcpy(sc, ts, sizeof(sc));
+    alpha_prev = alpha;
+    res->iterations++;
+    if (t >= 1 && t <= 64) res->iters_step[t - 1]++;
+  }
+  res->l1_final = sc[SC_L1];
+  res->rho_final = sc[SC_RHO];
+  w.last_mass = mass;
+  return st;
+}
+
+// ---------------------------------------------------------------------------
+// Schedules (Z13)
+// ---------------------------------------------------------------------------
+mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g) {
+  g.clear();
+  if (!s) { set_error("schedule is NULL"); return MDOT_EINVAL; }
+  if (s->kind == MDOT_SCHED_EXPLICIT) {
+    if (!s->gammas || s->n_gammas < 1) { set_error("explicit schedule without gammas"); return MDOT_EINVAL; }
+    g.assign(s->gammas, s->gammas + s->n_gammas);
+  } else if (s->kind == MDOT_SCHED_FIXED) {
+    if (!(s->gamma_bar > 0)) { set_error("gamma_bar must be > 0"); return MDOT_EINVAL; }
+    int T = s->T;
+    if (T <= 0) {
+      const double sm = s->step_max > 0 ? s->step_max : 256.0;
+      const double q = floor(s->gamma_bar / sm);
+      T = (int)(q > 1.0 ? q : 1.0);
+    }
+    g.assign(T, s->gamma_bar / T);
+  } else if (s->kind == MDOT_SCHED_DOUBLING) {
+    if (!(s->gamma_bar > 0)) { set_error("gamma_bar must be > 0"); return MDOT_EINVAL; }
+    const double g0 = s->gamma0 > 0 ? s->gamma0 : 1.0;
+    double gb = 0.0;
+    while (gb < s->gamma_bar * (1.0 - 1e-12)) {
+      double next = g.empty() ? g0 : gb;
+      if (gb + next > s->gamma_bar * (1.0 + 1e-12)) next = s->gamma_bar - gb;
+      g.push_back(next);
+      gb += next;
+      if (g.size() > 4096) { set_error("doubling schedule too long"); return MDOT_EINVAL; }
+    }
+  } else {
+    set_error("unknown schedule kind %d", s->kind);
+    return MDOT_EINVAL;
+  }
+  for (double x : g)
+    if (!(x > 0) || !isfinite(x)) { set_error("schedule step %g is not > 0", x); return MDOT_EINVAL; }
+  return MDOT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Input handling
+// ---------------------------------------------------------------------------
+mdot_status validate_marginal(const double* h, int64_t n, const char* name) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(h[i] > 0.0) || !isfinite(h[i])) {
+      set_error("%s[%lld] = %g is not strictly positive (PAPER.md:38)", name, (long long)i, h[i]);
+      return MDOT_EINVAL;
+    }
+    s += h[i];
+  }
+  if (fabs(s - 1.0) > 1e-12 * std::max<double>(1.0, (double)n / 1e4)) {
+    set_error("%s sums to %.17g, not 1 within 1e-12", name, s);
+    return MDOT_EINVAL;
+  }
+  return MDOT_OK;
+}
+
+mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
+  if (!pb || pb->n < 1) { set_error("problem is NULL or n < 1"); return MDOT_EINVAL; }
+  if (pb->kind < 0 || pb->kind > 2) { set_error("unknown cost kind %d", pb->kind); return MDOT_EINVAL; }
+  const bool dev = pb->mem == MDOT_MEM_DEVICE;
+  host_io = !dev;
+  otf = pb->kind == MDOT_COST_SQEUCLID_F32;
+  c_f64 = pb->kind == MDOT_COST_DENSE_F64;
+  kind_fast = otf ? 1 : 0;
+  d = pb->d;
+  scale = pb->scale;
+  if (otf && (d < 1 || d > 64 || !pb->X || !pb->Y)) { set_error("SQEUCLID needs X, Y and 1 <= d <= 64"); return MDOT_EINVAL; }
+  if (!otf && !pb->C) { set_error("C is NULL"); return MDOT_EINVAL; }
+  if (!pb->r || !pb->c) { set_error("r or c is NULL"); return MDOT_EINVAL; }
+  // marginals: validate on a host copy
+  std::vector<double> hr(n), hc(n);
+  if (dev) {
+    CK(cudaMemcpyAsync(hr.data(), pb->r + row0 * 0, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), pb->c, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } else {
+    memcpy(hr.data(), pb->r, sizeof(double) * n);
+    memcpy(hc.data(), pb->c, sizeof(double) * n);
+  }
+  CKS(validate_marginal(hr.data(), n, "r"));
+  CKS(validate_marginal(hc.data(), n, "c"));
+  CK(cudaMemcpyAsync(r, hr.data() + row0, sizeof(double) * nrows, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c, hc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  // cost
+  if (otf) {
+    if (dev) {
+      Xdev = pb->X; Ydev = pb->Y;
+    } else {
+      CK(cudaMallocAsync((void**)&owned_X, sizeof(float) * nrows * d, st));
+      CK(cudaMallocAsync((void**)&owned_Y, sizeof(float) * n * d, st));
+      CK(cudaMemcpyAsync(owned_X, pb->X, sizeof(float) * nrows * d, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(owned_Y, pb->Y, sizeof(float) * n * d, cudaMemcpyHostToDevice, st));
+      Xdev = owned_X; Ydev = owned_Y;
+    }
+  } else {
+    const size_t esz = c_f64 ? 8 : 4;
+    if (dev) {
+      Cdev = pb->C;
+    } else {
+      CK(cudaMallocAsync(&owned_C, esz * nrows * n, st));
+      CK(cudaMemcpyAsync(owned_C, pb->C, esz * nrows * n, cudaMemcpyHostToDevice, st));
+      Cdev = owned_C;
+    }
+    // sampled check C in [0,1]
+    const int S = 64;
+    std::vector<char> buf(esz * S);
+    for (int q = 0; q < S; ++q) {
+      const int64_t idx = (int64_t)(((uint64_t)q * 2654435761ull) % (uint64_t)(nrows * n));
+      if (dev) CK(cudaMemcpyAsync(buf.data() + q * esz, (const char*)pb->C + idx * esz, esz, cudaMemcpyDeviceToHost, st));
+      else memcpy(buf.data() + q * esz, (const char*)pb->C + idx * esz, esz);
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int q = 0; q < S; ++q) {
+      const double v = c_f64 ? ((double*)buf.data())[q] : (double)((float*)buf.data())[q];
+      if (!(v >= 0.0 && v <= 1.0)) { set_error("C entry %g outside [0,1] (PAPER.md:42)", v); return MDOT_EINVAL; }
+    }
+  }
+  eval.C = (const float*)Cdev;
+  eval.ldc = n;
+  eval.X = Xdev; eval.Y = Ydev; eval.d = d; eval.scale = scale;
+  return MDOT_OK;
+}
+
+void Workspace::free_owned() {
+  if (owned_C) cudaFreeAsync(owned_C, st);
+  if (owned_X) cudaFreeAsync(owned_X, st);
+  if (owned_Y) cudaFreeAsync(owned_Y, st);
+  owned_C = nullptr; owned_X = owned_Y = nullptr;
+}
+
+mdot_status Workspace::setup(const mdot_options& o) {
+  time_kernels = o.time_kernels;
+  if (time_kernels) {
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+  }
+  exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && c_f64);
+  if (!exact_mode && c_f64) {
+    set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
+    return MDOT_EINVAL;
+  }
+  CK(launch_setup(nrows, r, logr, rho_r, st));
+  CK(launch_setup(n, c, logc, sig_c, st));
+  return MDOT_OK;
+}
+
+// gauge: (U - d, V + d) leaves P unchanged; d chosen so that
+// <r,U> = <c,V> (Z19).  Same for the step potentials (u, v).
+mdot_status Workspace::gauge_center(double* X_, double* Y_) {
+  const double* xs[2] = {r, c};
+  const double* ys[2] = {X_, Y_};
+  // rows and columns have different lengths: two dot calls
+  CK(launch_dots(nrows, 1, &xs[0], &ys[0], blockpart, ticket, scal_dev, scal_host_dev, st));
+  CK(cudaStreamSynchronize(st));
+  const double a = scal_host[0];
+  CK(launch_dots(n, 1, &xs[1], &ys[1], blockpart, ticket, scal_dev, scal_host_dev, st));
+  CK(cudaStreamSynchronize(st));
+  const double b = scal_host[0];
+  const double dd = 0.5 * (a - b);
+  CK(launch_add_scalar(nrows, -dd, X_, st));
+  CK(launch_add_scalar(n, dd, Y_, st));
+  return MDOT_OK;
+}
+
+// Rounding + cost, fp64 kernels.
+mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* cost_G) {
+  // x = min(r / r(F), 1) from the current log marginals; A' = U + log x
+  double* logx = aux;
+  double* invx = aux + nrows;
+  double* Bpp = aux + 2 * nrows;
+  double* ec = aux + 2 * nrows + n;
+  double* er = aux + 2 * nrows + 2 * n;
+  double* rowF2 = aux + 3 * nrows + 2 * n;
+  double* rowcost2 = aux + 4 * nrows + 2 * n;
+  double* rowcorr = aux + 5 * nrows + 2 * n;
+  CK(launch_round_rows(nrows, logr, cur->lm, U, logx, A, st));
+  CK(launch_exp_neg(nrows, logx, invx, st));
+  RoundArgs a{};
+  a.C = Cdev; a.ldc = n; a.c_f64 = c_f64;
+  a.X = Xdev; a.Y = Ydev; a.d = d; a.scale = scale; a.otf = otf;
+  a.n = n; a.nrows = nrows;
+  a.A = A; a.B = V; a.invx = invx; a.gbar = gbar;
+  a.colF1 = colm; a.colcost = cols; a.chunks = chunks;
+  a.ec = ec; a.er = er; a.rowF2 = rowF2; a.rowcost2 = rowcost2; a.rowcorr = rowcorr;
+  CK(launch_round_cols(a, st));
+  CK(launch_round_combine_cols(a, c, V, Bpp, ec, blockpart, ticket, scal_dev, scal_host_dev, st));
+  CK(cudaStreamSynchronize(st));
+  const double cF = scal_host[0];
+  a.B = Bpp;
+  CK(launch_round_rows3(a, st));
+  CK(launch_round_combine_rows(a, r, blockpart, ticket, scal_dev, scal_host_dev, st));
+  CK(cudaStreamSynchronize(st));
+  const double ner = scal_host[0], cF2 = scal_host[1], corr = scal_host[2];
+  if (cost_F) *cost_F = cF;
+  if (cost_G) *cost_G = cF2 + (ner >= 1e-300 ? corr / ner : 0.0);
+  if (P_out_dev) {
+    a.plan = P_out_dev;
+    a.inv_ner = ner >= 1e-300 ? 1.0 / ner : 0.0;
+    CK(launch_round_plan(a, st));
+  }
+  return MDOT_OK;
+}
+
+}  // namespace mdot
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace mdot;
+
+extern "C" {
+
+const char* mdot_last_error(void) { return g_last_error.c_str(); }
+int32_t mdot_abi_version(void) { return MDOT_ABI_VERSION; }
+
+void mdot_options_default(mdot_options* o) {
+  memset(o, 0, sizeof(*o));
+  o->eps = 1e-6;
+  o->stop = 0;
+  o->projector = MDOT_PROJ_PNCG;
+  o->beta = MDOT_BETA_PPR;
+  o->c1 = 0.1;
+  o->c2 = 0.4;
+  o->warm = MDOT_WARM_SCALED;
+  o->precision = MDOT_PREC_AUTO;
+  o->ls_max_trials = 100;
+  o->max_evals = 10000000;
+}
+
+void mdot_schedule_default(mdot_schedule* s) {
+  memset(s, 0, sizeof(*s));
+  s->kind = MDOT_SCHED_FIXED;
+  s->gamma_bar = 4096.0;
+  s->step_max = 256.0;
+  s->gamma0 = 1.0;
+}
+
+static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt_in,
+                              double* u_out, double* v_out, float* P_out, mdot_result* res, int force_sinkhorn) {
+  g_last_error.clear();
+  if (!res) { set_error("result pointer is NULL"); return MDOT_EINVAL; }
+  memset(res, 0, sizeof(*res));
+  const double t0 = now_s();
+  mdot_options o;
+  if (opt_in) o = *opt_in; else mdot_options_default(&o);
+  if (force_sinkhorn) o.projector = MDOT_PROJ_SINKHORN;
+  if (o.ls_max_trials <= 0) o.ls_max_trials = 100;
+  if (o.max_evals <= 0) o.max_evals = 10000000;
+  if (!(o.eps > 0)) { set_error("eps must be > 0"); res->status = MDOT_EINVAL; return MDOT_EINVAL; }
+  if (!pb || pb->n < 1) { set_error("problem is NULL or n < 1"); res->status = MDOT_EINVAL; return MDOT_EINVAL; }
+  std::vector<double> gam;
+  mdot_status st = build_schedule(sched, gam);
+  if (st != MDOT_OK) { res->status = st; return st; }
+  cudaStream_t stream = (cudaStream_t)o.stream;
+  const int64_t n = pb->n;
+  Workspace w;
+  st = w.alloc(stream, n, n);
+  if (st == MDOT_OK) st = w.load_problem(pb, 0);
+  if (st == MDOT_OK) st = w.setup(o);
+  mdot_status solve_st = MDOT_OK;
+  if (st == MDOT_OK) {
+    // P0 = r c^T -> U = log r, V = log c ; u = v = 0 (Alg. 1 line 2)
+    if (o.p0_ones) {
+      launch_fill(n, 0.0, w.U, stream);
+      launch_fill(n, 0.0, w.V, stream);
+    } else {
+      cudaMemcpyAsync(w.U, w.logr, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
+      cudaMemcpyAsync(w.V, w.logc, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
+    }
+    launch_fill(n, 0.0, w.u, stream);
+    launch_fill(n, 0.0, w.v, stream);
+    double gb = 0.0, gprev = 0.0;
+    for (size_t t = 1; t <= gam.size(); ++t) {
+      const double gt = gam[t - 1];
+      gb += gt;
+      w.set_gamma(gb);
+      if (o.warm == MDOT_WARM_ZERO) {
+        launch_fill(n, 0.0, w.u, stream);
+        launch_fill(n, 0.0, w.v, stream);
+      } else if (o.warm == MDOT_WARM_SCALED && t > 1 && gt != gprev) {
+        launch_axpby(n, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
+        launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
+      }
+      if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
+      else solve_st = project_pncg(w, o, (int)t, res);
+      res->md_steps = (int64_t)t;
+      launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u
+      launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);   // V += v
+      if (solve_st != MDOT_OK && solve_st != MDOT_ENOCONV) break;
+      st = w.gauge_center(w.U, w.V);
+      if (st == MDOT_OK) st = w.gauge_center(w.u, w.v);
+      if (st != MDOT_OK) break;
+      gprev = gt;
+      if (solve_st != MDOT_OK) break;
+    }
+    res->gamma_bar = gb;
+    if (st == MDOT_OK && (solve_st == MDOT_OK || solve_st == MDOT_ENOCONV)) {
+      float* Pdev = nullptr;
+      float* Pown = nullptr;
+      if (P_out) {
+        if (pb->mem == MDOT_MEM_DEVICE) Pdev = P_out;
+        else if (cudaMallocAsync((void**)&Pown, sizeof(float) * n * n, stream) == cudaSuccess) Pdev = Pown;
+      }
+      st = w.round_and_cost(Pdev, &res->cost_unrounded, &res->cost_rounded);
+      if (st == MDOT_OK && Pown) {
+        if (cudaMemcpyAsync(P_out, Pown, sizeof(float) * n * n, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+          st = MDOT_ECUDA;
+      }
+      if (Pown) cudaFreeAsync(Pown, stream);
+    }
+    const cudaMemcpyKind k = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (u_out) cudaMemcpyAsync(u_out, w.U, sizeof(double) * n, k, stream);
+    if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * n, k, stream);
+  }
+  res->evaluations = w.evals;
+  res->fallbacks = w.fallbacks;
+  res->kernel_ms = w.kernel_ms;
+  res->kernel_launches = w.kernel_launches;
+  w.free_owned();
+  w.release();
+  cudaError_t ce = cudaStreamSynchronize(stream);
+  if (st == MDOT_OK && ce != cudaSuccess) {
+    set_error("CUDA error at exit: %s", cudaGetErrorString(ce));
+    st = MDOT_ECUDA;
+  }
+  if (st == MDOT_OK) st = solve_st;
+  res->status = st;
+  res->seconds = now_s() - t0;
+  return st;
+}
+
+mdot_status mdot_solve(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
+                       double* u_out, double* v_out, float* P_out, mdot_result* res) {
+  return solve_impl(pb, sched, opt, u_out, v_out, P_out, res, 0);
+}
+
+mdot_status mdot_sinkhorn(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
+                          double* u_out, double* v_out, float* P_out, mdot_result* res) {
+  return solve_impl(pb, sched, opt, u_out, v_out, P_out, res, 1);
+}
+
+mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,
+                             const mdot_schedule* sched, const mdot_options* opt,
+                             double* u_out, double* v_out, mdot_result* res) {
+  if (!shared || Bn < 1 || !r || !c || !res) { set_error("bad batch arguments"); return MDOT_EINVAL; }
+  mdot_status first = MDOT_OK;
+  for (int32_t b = 0; b < Bn; ++b) {
+    mdot_problem p = *shared;
+    p.r = r + (int64_t)b * shared->n;
+    p.c = c + (int64_t)b * shared->n;
+    mdot_status s = solve_impl(&p, sched, opt, u_out ? u_out + (int64_t)b * shared->n : nullptr,
+                               v_out ? v_out + (int64_t)b * shared->n : nullptr, nullptr, &res[b], 0);
+    if (s != MDOT_OK && first == MDOT_OK) first = s;
+  }
+  return first;
+}
+
+mdot_status mdot_marginals(const mdot_problem* pb, const double* Ain, const double* Bin, double gbar,
+                           double* lr, double* lc, const mdot_options* opt_in, int32_t* fallback_out) {
+  g_last_error.clear();
+  mdot_options o;
+  if (opt_in) o = *opt_in; else mdot_options_default(&o);
+  if (!pb || pb->n < 1 || !Ain || !Bin || !lr || !lc) { set_error("bad arguments"); return MDOT_EINVAL; }
+  cudaStream_t stream = (cudaStream_t)o.stream;
+  const int64_t n = pb->n;
+  Workspace w;
+  mdot_status st = w.alloc(stream, n, n);
+  if (st == MDOT_OK) st = w.load_problem(pb, 0);
+  if (st == MDOT_OK) st = w.setup(o);
+  if (st == MDOT_OK) {
+    w.set_gamma(gbar);
+    const double* dA = Ain;
+    const double* dB = Bin;
+    if (pb->mem != MDOT_MEM_DEVICE) {
+      cudaMemcpyAsync(w.tu, Ain, sizeof(double) * n, cudaMemcpyHostToDevice, stream);
+      cudaMemcpyAsync(w.tv, Bin, sizeof(double) * n, cudaMemcpyHostToDevice, stream);
+      dA = w.tu;
+      dB = w.tv;
+    }
+    double sc[kNumScalars];
+    st = w.prep(PREP_AB, 0, 0, nullptr, dA, dB);
+    if (st == MDOT_OK) st = w.evaluate(w.cur, nullptr, nullptr, sc);
+    if (st == MDOT_OK) {
+      const cudaMemcpyKind k = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+      cudaMemcpyAsync(lr, w.cur->lm, sizeof(double) * n, k, stream);
+      cudaMemcpyAsync(lc, w.cur->lm + n, sizeof(double) * n, k, stream);
+    }
+    if (fallback_out) *fallback_out = (int32_t)w.fallbacks;
+  }
+  w.free_owned();
+  w.release();
+  cudaError_t ce = cudaStreamSynchronize(stream);
+  if (st == MDOT_OK && ce != cudaSuccess) { set_error("%s", cudaGetErrorString(ce)); st = MDOT_ECUDA; }
+  return st;
+}
+
+mdot_status mdot_round(const mdot_problem* pb, const double* U, const double* V, double gbar,
+                       float* P_out, double* cost_F, double* cost_G, const mdot_options* opt_in) {
+  g_last_error.clear();
+  mdot_options o;
+  if (opt_in) o = *opt_in; else mdot_options_default(&o);
+  if (!pb || pb->n < 1 || !U || !V) { set_error("bad arguments"); return MDOT_EINVAL; }
+  o.precision = MDOT_PREC_F64P;   // rounding runs on the fp64 kernels
+  cudaStream_t stream = (cudaStream_t)o.stream;
+  const int64_t n = pb->n;
+  Workspace w;
+  mdot_status st = w.alloc(stream, n, n);
+  if (st == MDOT_OK) st = w.load_problem(pb, 0);
+  if (st == MDOT_OK) st = w.setup(o);
+  float* Pown = nullptr;
+  if (st == MDOT_OK) {
+    w.set_gamma(gbar);
+    const cudaMemcpyKind kin = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    cudaMemcpyAsync(w.U, U, sizeof(double) * n, kin, stream);
+    cudaMemcpyAsync(w.V, V, sizeof(double) * n, kin, stream);
+    launch_fill(n, 0.0, w.u, stream);
+    launch_fill(n, 0.0, w.v, stream);
+    double sc[kNumScalars];
+    st = w.prep(PREP_CUR, 0, 0, nullptr, nullptr, nullptr);
+    if (st == MDOT_OK) st = w.evaluate(w.cur, nullptr, nullptr, sc);
+    float* Pdev = nullptr;
+    if (st == MDOT_OK && P_out) {
+      if (pb->mem == MDOT_MEM_DEVICE) Pdev = P_out;
+      else if (cudaMallocAsync((void**)&Pown, sizeof(float) * n * n, stream) == cudaSuccess) Pdev = Pown;
+    }
+    if (st == MDOT_OK) st = w.round_and_cost(Pdev, cost_F, cost_G);
+    if (st == MDOT_OK && Pown) cudaMemcpyAsync(P_out, Pown, sizeof(float) * n * n, cudaMemcpyDeviceToHost, stream);
+  }
+  if (Pown) cudaFreeAsync(Pown, stream);
+  w.free_owned();
+  w.release();
+  cudaError_t ce = cudaStreamSynchronize(stream);
+  if (st == MDOT_OK && ce != cudaSuccess) { set_error("%s", cudaGetErrorString(ce)); st = MDOT_ECUDA; }
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// paper_2307_08507_b200/csrc/solver.h -- per-call device workspace of the
+// MDOT-PNCG solver (internal; see include/mdot.h for the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/mdot.h"
+#include "internal.cuh"
+
+namespace mdot {
+
+void set_error(const char* fmt, ...);
+
+struct Marg {           // marginals of one plan (rows then columns, [nrows + n])
+  double* lm = nullptr; // log marginals
+  double* m = nullptr;  // marginals
+  double* s = nullptr;  // Sinkhorn direction
+  double* g = nullptr;  // gradient
+};
+
+struct Workspace {
+  cudaStream_t st = nullptr;
+  int64_t n = 0, nrows = 0;
+  // problem
+  const void* Cdev = nullptr;
+  const float* Xdev = nullptr;
+  const float* Ydev = nullptr;
+  void* owned_C = nullptr;
+  float* owned_X = nullptr;
+  float* owned_Y = nullptr;
+  int otf = 0, c_f64 = 0, kind_fast = 0, d = 0;
+  float scale = 0.f;
+  bool host_io = false;
+  bool exact_mode = false;
+  double gbar = 0.0;
+  // device buffers (one allocation)
+  void* base = nullptr;
+  double *r = nullptr, *c = nullptr, *logr = nullptr, *logc = nullptr, *rho_r = nullptr, *sig_c = nullptr;
+  double *U = nullptr, *V = nullptr, *u = nullptr, *v = nullptr, *tu = nullptr, *tv = nullptr;
+  double *A = nullptr, *B = nullptr, *p = nullptr, *pprev = nullptr;
+  Marg mg[2];
+  Marg* cur = nullptr;
+  Marg* trial = nullptr;
+  double *rowpart = nullptr, *colpart = nullptr, *colm = nullptr, *cols = nullptr, *lr_ex = nullptr;
+  double *blockpart = nullptr, *scal_dev = nullptr, *aux = nullptr;
+  float4 *rowp = nullptr, *colp = nullptr;
+  unsigned int* ticket_flag = nullptr;
+  unsigned int* ticket = nullptr;
+  int* flag = nullptr;
+  double* scal_host = nullptr;      // mapped pinned
+  double* scal_host_dev = nullptr;  // its device alias
+  int chunks = 1;
+  EvalArgs eval{};
+  // stats
+  int64_t evals = 0, fallbacks = 0, kernel_launches = 0;
+  double kernel_ms = 0.0;
+  double last_mass = 1.0;
+  int time_kernels = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  mdot_status alloc(cudaStream_t stream, int64_t n, int64_t nrows);
+  void release();
+  mdot_status load_problem(const mdot_problem* pb, int64_t row0);
+  void free_owned();
+  mdot_status setup(const mdot_options& o);
+  void set_gamma(double gb);
+  mdot_status prep(int mode, double alpha, double beta, const double* s_dir, const double* Ain,
+                   const double* Bin);
+  mdot_status evaluate(Marg* out, const double* gcur, const double* pcur, double* sc);
+  mdot_status gauge_center(double* X, double* Y);
+  mdot_status round_and_cost(float* P_out_dev, double* cost_F, double* cost_G);
+};
+
+mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g);
+mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result* res);
+mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_result* res);
+
+}  // namespace mdot

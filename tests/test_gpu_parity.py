@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances:
+  * single evaluation, fp32-entry path: max relative error of r(P), c(P)
+    <= 2e-6 (anchored fp32 exponent + MUFU ex2, ~1e-7 typical);
+  * single evaluation, fp64 path: <= 1e-12;
+  * solves (north_star / Z20): |cost_gpu - cost_oracle| <= 1e-5 relative on
+    the unrounded cost; GPU L1 <= eps by its own evaluation; the oracle's
+    fp64 re-evaluation of the GPU potentials has L1 <= 2 eps; rounded cost
+    within max(1e-5 cost, 2 (L1_gpu + L1_oracle) max C).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2307_08507_b200 as M  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _t(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def _sinkhorn_potentials(prob, inst, gbar, iters=6, seed=0, noise=0.0):
+    """Plausible near-feasible potentials from a few oracle Sinkhorn sweeps."""
+    A = np.log(inst.r).copy()
+    B = np.log(inst.c).copy()
+    for _ in range(iters):
+        lr, lc, _ = O.log_marginals(prob, A, B, gbar)
+        A += np.log(inst.r) - lr
+        lr, lc, _ = O.log_marginals(prob, A, B, gbar)
+        B += np.log(inst.c) - lc
+    if noise:
+        rng = np.random.default_rng(seed)
+        A += noise * rng.standard_normal(len(A))
+        B += noise * rng.standard_normal(len(B))
+    return A, B
+
+
+@pytest.mark.parametrize("n,gbar", [(64, 64.0), (300, 512.0), (784, 4096.0), (1031, 256.0), (2048, 4096.0)])
+def test_marginals_fp32_path_matches_oracle(n, gbar):
+    inst = S.uniform_points_instance(3, n, 2, 1, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    A, B = _sinkhorn_potentials(prob, inst, gbar, iters=4, noise=0.05)
+    lr_o, lc_o, st = O.log_marginals(prob, A, B, gbar)
+    assert st == 0
+    lr, lc, fb = M.mdot_marginals(_t(A), _t(B), gbar, _t(inst.C), _t(inst.r), _t(inst.c))
+    lr = lr.cpu().numpy()
+    lc = lc.cpu().numpy()
+    assert fb == 0
+    err_r = np.max(np.abs(np.expm1(lr - lr_o)))
+    err_c = np.max(np.abs(np.expm1(lc - lc_o)))
+    assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
+
+
+def test_marginals_far_from_feasible_uses_exact_fallback():
+    n = 512
+    inst = S.uniform_points_instance(3, n, 2, 2, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(5)
+    A = 40.0 * rng.standard_normal(n)
+    B = 40.0 * rng.standard_normal(n)
+    lr_o, lc_o, _ = O.log_marginals(prob, A, B, 1000.0)
+    lr, lc, fb = M.mdot_marginals(_t(A), _t(B), 1000.0, _t(inst.C), _t(inst.r), _t(inst.c))
+    assert fb == 1
+    np.testing.assert_allclose(lr.cpu().numpy(), lr_o, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(lc.cpu().numpy(), lc_o, rtol=0, atol=1e-11)
+
+
+def test_marginals_fp64_path_and_host_memory():
+    inst = S.config1(0)
+    prob = O.OracleProblem(inst)
+    A, B = _sinkhorn_potentials(prob, inst, 256.0, iters=3, noise=0.1)
+    lr_o, lc_o, _ = O.log_marginals(prob, A, B, 256.0)
+    # host arrays -> MDOT_MEM_HOST path
+    lr, lc, fb = M.mdot_marginals(A, B, 256.0, inst.C, inst.r, inst.c)
+    np.testing.assert_allclose(lr, lr_o, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(lc, lc_o, rtol=0, atol=1e-12)
+
+
+def _gates(res, ores, inst, prob, U, V, eps, cmax=1.0):
+    assert res["status"] == 0, res
+    assert ores["status"] == 0, ores
+    rel = abs(res["cost_unrounded"] - ores["cost_unrounded"]) / abs(ores["cost_unrounded"])
+    assert rel <= 1e-5, (res["cost_unrounded"], ores["cost_unrounded"], rel)
+    assert res["l1_final"] <= eps
+    lr, lc, _ = O.log_marginals(prob, U, V, res["gamma_bar"])
+    l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
+    assert l1 <= 2 * eps, l1
+    allow = max(1e-5 * abs(ores["cost_rounded"]), 2 * (res["l1_final"] + ores["l1_final"]) * cmax)
+    assert abs(res["cost_rounded"] - ores["cost_rounded"]) <= allow
+    return rel, l1
+
+
+def test_solve_config1_fp64_doubling():
+    """BASELINE config 1: n=64 grid, fp64 C, doubling schedule to 4096, L1 1e-6."""
+    inst = S.config1(0)
+    prob = O.OracleProblem(inst)
+    eps = 1e-6
+    U = torch.empty(64, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c),
+                       schedule=M.schedule(M.MDOT_SCHED_DOUBLING, 4096.0),
+                       options=M.options(eps=eps), u_out=U, v_out=V)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_doubling(4096.0), O.make_options(eps=eps))
+    assert res["md_steps"] == 13
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+@pytest.mark.parametrize("n,gbar,T", [(300, 512.0, 4), (1000, 4096.0, 16)])
+def test_solve_fp32_pncg_matches_oracle(n, gbar, T):
+    inst = S.uniform_points_instance(3, n, 2, 3, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    eps = 1e-6
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c),
+                       schedule=M.schedule(M.MDOT_SCHED_FIXED, gbar, T=T),
+                       options=M.options(eps=eps), u_out=U, v_out=V)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gbar, T=T), O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+    # evaluation counts within a band (iteration counts are chaotic)
+    assert res["evaluations"] <= 2.0 * ores["evaluations"] + 50
+
+
+def test_sinkhorn_matches_oracle():
+    n = 400
+    inst = S.uniform_points_instance(3, n, 2, 4, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    eps = 1e-6
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_sinkhorn(_t(inst.C), _t(inst.r), _t(inst.c),
+                          schedule=M.schedule(M.MDOT_SCHED_FIXED, 256.0, T=2),
+                          options=M.options(eps=eps), u_out=U, v_out=V)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(256.0, T=2),
+                             O.make_options(eps=eps, projector=O.SINKHORN))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+def test_round_matches_oracle_and_plan_is_feasible():
+    n = 200
+    inst = S.uniform_points_instance(3, n, 2, 5, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    A, B = _sinkhorn_potentials(prob, inst, 128.0, iters=5)
+    cF_o = O.round_plan(prob, A, B, 128.0, dense=True)
+    P = torch.empty((n, n), dtype=torch.float32, device=DEV)
+    cF, cG = M.mdot_round(_t(A), _t(B), 128.0, _t(inst.C), _t(inst.r), _t(inst.c), P_out=P)
+    assert abs(cF - cF_o["cost_F"]) <= 1e-12 * abs(cF_o["cost_F"])
+    assert abs(cG - cF_o["cost_G"]) <= 1e-12 * abs(cF_o["cost_G"])
+    G = P.double().cpu().numpy()
+    np.testing.assert_allclose(G, cF_o["G"], rtol=1e-6, atol=1e-12)
+    assert np.abs(G.sum(1) - inst.r).max() < 1e-7 * inst.r.max() + 1e-9
+
+
+def test_lemma2_on_gpu():
+    """Schedule invariance: T=1 and T=8 give the same cost."""
+    n = 256
+    inst = S.uniform_points_instance(3, n, 2, 6, marg="dirichlet")
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    a = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, 1024.0, T=1), options=M.options(eps=1e-7))
+    b = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, 1024.0, T=8), options=M.options(eps=1e-7))
+    assert abs(a["cost_unrounded"] - b["cost_unrounded"]) <= 2e-6 * a["cost_unrounded"]
+
+
+def test_line_1d_exact_ot_pin_on_gpu():
+    """Prop. 1 with exact OT from the 1-D monotone coupling, larger n."""
+    from tests import exact_ot as X
+    li = S.line_instance(1500, seed=7, dtype=np.float32)
+    ot = X.ot_line_nw(li.C.astype(np.float64), li.r, li.c)
+    Hmin = min(-(li.r * np.log(li.r)).sum(), -(li.c * np.log(li.c)).sum())
+    gb = 4096.0
+    res = M.mdot_solve(_t(li.C), _t(li.r), _t(li.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, gb),
+                       options=M.options(eps=1e-6))
+    assert res["status"] == 0
+    assert res["cost_rounded"] >= ot - 1e-9
+    assert res["cost_unrounded"] - ot <= Hmin / gb + 1e-6
+
+
+def test_edge_cases_and_errors():
+    # n = 1: the only plan is [[1]]
+    res = M.mdot_solve(_t(np.array([[0.5]], dtype=np.float32)), _t(np.array([1.0])), _t(np.array([1.0])),
+                       options=M.options(eps=1e-9))
+    assert res["status"] == 0 and abs(res["cost_rounded"] - 0.5) < 1e-12
+    # n = 2 closed form
+    from tests import exact_ot as X
+    C2 = np.array([[0.1, 0.7], [0.4, 0.2]])
+    r2 = np.array([0.3, 0.7])
+    c2 = np.array([0.6, 0.4])
+    U = torch.empty(2, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(_t(C2), _t(r2), _t(c2), schedule=M.schedule(M.MDOT_SCHED_FIXED, 64.0, T=1),
+                       options=M.options(eps=1e-13), u_out=U, v_out=V)
+    P = np.exp(U.cpu().numpy()[:, None] + V.cpu().numpy()[None, :] - 64.0 * C2)
+    np.testing.assert_allclose(P, X.entropic_2x2(C2, r2, c2, 64.0), atol=1e-12)
+    # invalid inputs -> MDOT_EINVAL
+    bad_r = np.array([0.5, 0.6])
+    with pytest.raises(M.MdotError) as e:
+        M.mdot_solve(_t(C2), _t(bad_r), _t(c2))
+    assert e.value.status == 1
+    with pytest.raises(M.MdotError) as e:
+        M.mdot_solve(_t(C2 * 3.0), _t(r2), _t(c2))
+    assert e.value.status == 1
+    with pytest.raises(M.MdotError) as e:
+        M.mdot_solve(_t(C2), _t(np.array([-0.1, 1.1])), _t(c2))
+    assert e.value.status == 1
+
+
+def test_full_size_config4_sampled_parity():
+    """BASELINE config 4 (n=16384, 1 GiB fp32 C) in the bench's launch
+    configuration: one fused evaluation at near-converged potentials, with
+    sampled rows/columns recomputed by the oracle one by one."""
+    inst = S.config4(0)
+    n = inst.n
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    gb = 512.0
+    res = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=2),
+                       options=M.options(eps=1e-5), u_out=U, v_out=V)
+    assert res["status"] == 0 and res["l1_final"] <= 1e-5
+    lr, lc, fb = M.mdot_marginals(U, V, gb, C, r, c)
+    assert fb == 0
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(n, 24, replace=False))
+    cols = np.sort(rng.choice(n, 24, replace=False))
+    sub = O.log_marginal_subset(prob, U.cpu().numpy(), V.cpu().numpy(), gb, rows=rows, cols=cols)
+    err_r = np.max(np.abs(np.expm1(lr.cpu().numpy()[rows] - sub["rows"])))
+    err_c = np.max(np.abs(np.expm1(lc.cpu().numpy()[cols] - sub["cols"])))
+    assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)

@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the MDOT-PNCG hot path on B200 (driver contract, one JSON line).
+
+Workload (BASELINE.json metric "time-to-eps (marginal L1 1e-6) and marginal
+evals/s; HBM GB/s vs peak"): configs[3], the north_star's headline case --
+n = 16384, X, Y ~ U[0,1]^2, C = d^2/max fp32 (1 GiB, materialised), Dirichlet(1)
+marginals, FIXED gamma schedule to gamma_bar = 4096 (T = 16, the paper's rule
+gamma_t = gbar / max(1, floor(gbar/256))), stop at marginal L1
+<= 1e-6.  One "step" = one complete mdot_solve (MD loop + PNCG projections +
+rounding + cost) with inputs resident in HBM.
+
+value       = marginal evaluations / s over the timed steps (every O(n^2) pass
+              of the solve counts; the same unit as the oracle's cpu_baseline)
+ms_per_step = time-to-eps (ms), device-timed with CUDA events, max over ranks
+roofline    = the fused marginal kernel (k_eval_fast): algorithmic bytes 4 n^2
+              (C read once) per launch / mean launch time (CUDA events around
+              every launch inside the library, on its stream), vs the measured
+              HBM copy bandwidth in MEASURED_PEAKS.json
+e2e         = the same metric through the C ABI with HOST buffers (pinned C,
+              r, c in; U, V out), copies inside the timed region
+cpu_baseline= the fp64 oracle (oracle/), as it stands, on a bounded sample of
+              the same workload on this host's cores
+
+--impl reference runs the oracle (this tier's reference arm) on the same
+config, metric and unit, each step a bounded sample.
+Multi-GPU (torchrun): rows of C sharded over ranks, one NCCL allreduce of the
+column partials per evaluation (mdot_solve_sharded); strong scaling (n fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-eps (marginal L1 1e-6) and marginal evals/s; HBM GB/s vs peak at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--gamma-bar", type=float, default=4096.0)
+    ap.add_argument("--T", type=int, default=0)
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--projector", default="pncg", choices=["pncg", "sinkhorn"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--instance", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"cfg4-dense-n{a.n}-dirichlet1-gbar{int(a.gamma_bar)}-T{a.T or 'paper'}-"
+            f"L1eps{a.eps:g}-{a.projector}")
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes per launch of k_eval_fast from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "k_eval_fast_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = []
+        mx = None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if s[3 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+def instance(a):
+    import synthetic as S
+    return S.config4(a.instance, n=a.n)
+
+
+def cpu_baseline(a, inst, seconds):
+    """The oracle as it stands on this host: MDOT with PNCG from the same
+    instance and schedule, stopped after a bounded number of O(n^2)
+    evaluations (the metric's unit), timed wall clock."""
+    import oracle as O
+    prob = O.OracleProblem(inst)
+    sched = O.schedule_fixed(a.gamma_bar, T=a.T)
+    proj = O.PNCG if a.projector == "pncg" else O.SINKHORN
+    # one evaluation to size the sample
+    t0 = time.perf_counter()
+    U, V, res, _ = O.mdot(prob, sched[:1], O.make_options(eps=a.eps, projector=proj, max_evals=1))
+    t1 = time.perf_counter() - t0
+    k = max(1, int(seconds / max(t1, 1e-3)))
+    t0 = time.perf_counter()
+    U, V, res, _ = O.mdot(prob, sched, O.make_options(eps=a.eps, projector=proj, max_evals=k))
+    dt = time.perf_counter() - t0
+    # the rounding pass at the end is included in dt; count its 3 passes as evaluations
+    evals = res["evaluations"] + 3
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": evals / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle MDOT-PNCG on the same n={a.n} instance, first {res['evaluations']} "
+                      f"O(n^2) evaluations of the solve (+3 rounding passes), {dt:.1f} s wall",
+            "seconds": dt}
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    inst = instance(a)
+    steps = []
+    for s in range(a.warmup + a.steps):
+        cb = cpu_baseline(a, inst, a.cpu_seconds)
+        if s >= a.warmup:
+            steps.append(cb)
+    v = statistics.mean(x["value"] for x in steps)
+    ms = statistics.mean(x["seconds"] for x in steps) * 1000.0
+    line = {"metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(a), "n": a.n, "gamma_bar": a.gamma_bar,
+                       "eps": a.eps, "sample": "bounded oracle sample per step"},
+            "impl": "reference",
+            "cpu_baseline": {k: steps[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "evals/s"},
+            "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2307_08507_b200 as M
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    inst = instance(a)
+    n = inst.n
+    sched = M.schedule(M.MDOT_SCHED_FIXED, a.gamma_bar, T=a.T)
+    proj = M.MDOT_PROJ_PNCG if a.projector == "pncg" else M.MDOT_PROJ_SINKHORN
+    opts = M.options(eps=a.eps, projector=proj, time_kernels=1)
+    r = torch.from_numpy(inst.r).to(dev)
+    c = torch.from_numpy(inst.c).to(dev)
+    comm = None
+    if world > 1:
+        rows = np.array_split(np.arange(n), world)[rank]
+        row0, nloc = int(rows[0]), len(rows)
+        C = torch.from_numpy(np.ascontiguousarray(inst.C[row0:row0 + nloc])).to(dev)
+        uid = M.mdot_get_unique_id() if rank == 0 else bytes(128)
+        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
+        dist.broadcast(t, 0)
+        comm = M.mdot_comm_create(bytes(t.cpu().numpy()), world, rank, local_rank)
+        U = torch.empty(nloc, dtype=torch.float64, device=dev)
+    else:
+        C = torch.from_numpy(inst.C).to(dev)
+        U = torch.empty(n, dtype=torch.float64, device=dev)
+        row0, nloc = 0, n
+    V = torch.empty(n, dtype=torch.float64, device=dev)
+    del inst.C  # keep host memory bounded; e2e re-creates it pinned
+
+    def solve():
+        if comm is not None:
+            return M.mdot_solve_sharded(comm, row0, nloc, C, r, c, n=n, schedule=sched, options=opts,
+                                        u_local_out=U, v_out=V)
+        if a.projector == "sinkhorn":
+            return M.mdot_sinkhorn(C, r, c, schedule=sched, options=opts, u_out=U, v_out=V)
+        return M.mdot_solve(C, r, c, schedule=sched, options=opts, u_out=U, v_out=V)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        res = solve()
+    barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    results = []
+    barrier()
+    e0.record(st)
+    for _ in range(a.steps):
+        results.append(solve())
+    e1.record(st)
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    evals = sum(x["evaluations"] for x in results)
+    kern_ms = sum(x["kernel_ms"] for x in results)
+    kern_n = sum(x["kernel_launches"] for x in results)
+    launches = sum(x.get("all_launches", 0) for x in results)
+    value = evals / (ms / 1000.0)
+    ms_step = ms / a.steps
+    hbm, peak_kind = measured_peaks()
+    bytes_per_launch = 4.0 * nloc * n
+    mean_launch_s = (kern_ms / kern_n) / 1000.0 if kern_n else float("nan")
+    achieved = bytes_per_launch / mean_launch_s / 1e9 if kern_n else None
+    if dist is not None and achieved is not None:
+        t = torch.tensor([achieved], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        achieved = float(t.item())
+        hbm = hbm * world
+    traffic = profile_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic (seeded config 4 instance, no dataset)",
+        "config": {"workload": workload_name(a), "n": n, "gamma_bar": a.gamma_bar,
+                   "T": int(results[-1]["md_steps"]), "eps": a.eps, "stop": "marginal L1",
+                   "projector": a.projector, "parallelism": f"rows sharded x{world}" if world > 1 else "1 GPU",
+                   "l2": "C (4 n^2 B) is larger than L2 (126 MB): no flush needed",
+                   "instance_seed": 4000 + a.instance},
+        "time_to_eps_s": ms_step / 1000.0,
+        "evaluations_per_solve": evals / a.steps,
+        "solve": {k: results[-1][k] for k in ("cost_rounded", "cost_unrounded", "l1_final", "iterations",
+                                              "evaluations", "ls_evaluations", "fallbacks", "md_steps",
+                                              "status_name")},
+        "roofline": {"kernel": "k_eval_fast", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "bytes_per_launch": bytes_per_launch, "launches": kern_n,
+                     "mean_launch_us": mean_launch_s * 1e6,
+                     "kernel_share_of_step": (kern_ms / ms) if ms else None},
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    # end-to-end through the C ABI with host buffers (rank 0, 1 GPU)
+    if world == 1 and not a.no_e2e:
+        import synthetic as S
+        inst2 = S.config4(a.instance, n=n)
+        Ch = torch.from_numpy(inst2.C).pin_memory()
+        del inst2.C
+        rh = torch.from_numpy(inst2.r)
+        ch = torch.from_numpy(inst2.c)
+        Uh = torch.empty(n, dtype=torch.float64).pin_memory()
+        Vh = torch.empty(n, dtype=torch.float64).pin_memory()
+        o2 = M.options(eps=a.eps, projector=proj)
+        M.mdot_solve(Ch, rh, ch, schedule=sched, options=o2, u_out=Uh, v_out=Vh)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev = 0
+        for _ in range(a.steps):
+            rr = M.mdot_solve(Ch, rh, ch, schedule=sched, options=o2, u_out=Uh, v_out=Vh)
+            ev += rr["evaluations"]
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        line["e2e"] = {"value": ev / dt, "unit": "evals/s", "h2d_bytes_per_step": 4 * n * n + 16 * n,
+                       "d2h_bytes_per_step": 16 * n, "ms_per_step": 1000.0 * dt / a.steps,
+                       "timing": "host wall clock around the synchronous C-ABI call"}
+        del Ch
+    if rank == 0 and not a.no_cpu_baseline:
+        import synthetic as S
+        inst3 = S.config4(a.instance, n=n)
+        line["cpu_baseline"] = {k: v for k, v in cpu_baseline(a, inst3, a.cpu_seconds).items()
+                                if k != "seconds"}
+    if comm is not None:
+        M.mdot_comm_destroy(comm)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    run_ours(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -118,6 +118,7 @@ typedef struct {
   int64_t md_steps, iterations, evaluations, ls_evaluations, resets, ls_restarts;
   int64_t fallbacks;       /* evaluations redone on the exact fp64 evaluator */
   int64_t kernel_launches; /* evaluation kernels timed */
+  int64_t all_launches;    /* every kernel this library launched during the call */
   int32_t status;
   int32_t reserved;
   double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */

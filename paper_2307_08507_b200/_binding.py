@@ -54,7 +54,7 @@ class Result(ct.Structure):
                 ("seconds", ct.c_double), ("kernel_ms", ct.c_double),
                 ("md_steps", ct.c_int64), ("iterations", ct.c_int64), ("evaluations", ct.c_int64),
                 ("ls_evaluations", ct.c_int64), ("resets", ct.c_int64), ("ls_restarts", ct.c_int64),
-                ("fallbacks", ct.c_int64), ("kernel_launches", ct.c_int64),
+                ("fallbacks", ct.c_int64), ("kernel_launches", ct.c_int64), ("all_launches", ct.c_int64),
                 ("status", ct.c_int32), ("reserved", ct.c_int32),
                 ("rho0", ct.c_double * 64), ("l10", ct.c_double * 64),
                 ("iters_step", ct.c_int64 * 64)]

@@ -55,6 +55,13 @@ static double now_s() {
     }                                                                                \
   } while (0)
 
+// launch + count (Workspace member context)
+#define CKL(call)        \
+  do {                   \
+    ++launches;          \
+    CK(call);            \
+  } while (0)
+
 #define CKS(call)                        \
   do {                                   \
     mdot_status s_ = (call);             \
@@ -159,12 +166,12 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   evals++;
   if (!exact_mode) {
     if (time_kernels) CK(cudaEventRecord(ev0, st));
-    CK(launch_eval_fast(eval, kind_fast, st));
+    CKL(launch_eval_fast(eval, kind_fast, st));
     if (time_kernels) CK(cudaEventRecord(ev1, st));
     f.from_partials = 1;
     f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
     f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
-    CK(launch_finalize(f, st));
+    CKL(launch_finalize(f, st));
     CK(cudaStreamSynchronize(st));
     if (time_kernels) {
       float ms = 0.f;
@@ -182,11 +189,11 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   x.n = n; x.nrows = nrows;
   x.A = A; x.B = B; x.gbar = gbar;
   x.lr = lr_ex; x.colm = colm; x.cols = cols; x.chunks = chunks;
-  CK(launch_eval_exact(x, st));
+  CKL(launch_eval_exact(x, st));
   f.from_partials = 0;
   f.lr_in = lr_ex; f.colm = colm; f.cols = cols; f.chunks = chunks;
   f.prep_flag = nullptr;
-  CK(launch_finalize(f, st));
+  CKL(launch_finalize(f, st));
   CK(cudaStreamSynchronize(st));
   memcpy(sc, scal_host, kNumScalars * sizeof(double));
   if (sc[SC_BAD] != 0.0) {
@@ -205,7 +212,7 @@ mdot_status Workspace::prep(int mode, double alpha, double beta, const double* s
   a.logr = logr; a.logc = logc; a.rho_r = rho_r; a.sig_c = sig_c;
   a.Ain = Ain; a.Bin = Bin; a.Aout = A; a.Bout = B;
   a.rowp = rowp; a.colp = colp; a.flag = flag;
-  CK(launch_prep(a, st));
+  CKL(launch_prep(a, st));
   return MDOT_OK;
 }
 
@@ -480,8 +487,8 @@ mdot_status Workspace::setup(const mdot_options& o) {
     set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
     return MDOT_EINVAL;
   }
-  CK(launch_setup(nrows, r, logr, rho_r, st));
-  CK(launch_setup(n, c, logc, sig_c, st));
+  CKL(launch_setup(nrows, r, logr, rho_r, st));
+  CKL(launch_setup(n, c, logc, sig_c, st));
   return MDOT_OK;
 }
 
@@ -491,15 +498,15 @@ mdot_status Workspace::gauge_center(double* X_, double* Y_) {
   const double* xs[2] = {r, c};
   const double* ys[2] = {X_, Y_};
   // rows and columns have different lengths: two dot calls
-  CK(launch_dots(nrows, 1, &xs[0], &ys[0], blockpart, ticket, scal_dev, scal_host_dev, st));
+  CKL(launch_dots(nrows, 1, &xs[0], &ys[0], blockpart, ticket, scal_dev, scal_host_dev, st));
   CK(cudaStreamSynchronize(st));
   const double a = scal_host[0];
-  CK(launch_dots(n, 1, &xs[1], &ys[1], blockpart, ticket, scal_dev, scal_host_dev, st));
+  CKL(launch_dots(n, 1, &xs[1], &ys[1], blockpart, ticket, scal_dev, scal_host_dev, st));
   CK(cudaStreamSynchronize(st));
   const double b = scal_host[0];
   const double dd = 0.5 * (a - b);
-  CK(launch_add_scalar(nrows, -dd, X_, st));
-  CK(launch_add_scalar(n, dd, Y_, st));
+  CKL(launch_add_scalar(nrows, -dd, X_, st));
+  CKL(launch_add_scalar(n, dd, Y_, st));
   return MDOT_OK;
 }
 
@@ -514,8 +521,8 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   double* rowF2 = aux + 3 * nrows + 2 * n;
   double* rowcost2 = aux + 4 * nrows + 2 * n;
   double* rowcorr = aux + 5 * nrows + 2 * n;
-  CK(launch_round_rows(nrows, logr, cur->lm, U, logx, A, st));
-  CK(launch_exp_neg(nrows, logx, invx, st));
+  CKL(launch_round_rows(nrows, logr, cur->lm, U, logx, A, st));
+  CKL(launch_exp_neg(nrows, logx, invx, st));
   RoundArgs a{};
   a.C = Cdev; a.ldc = n; a.c_f64 = c_f64;
   a.X = Xdev; a.Y = Ydev; a.d = d; a.scale = scale; a.otf = otf;
@@ -523,13 +530,13 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   a.A = A; a.B = V; a.invx = invx; a.gbar = gbar;
   a.colF1 = colm; a.colcost = cols; a.chunks = chunks;
   a.ec = ec; a.er = er; a.rowF2 = rowF2; a.rowcost2 = rowcost2; a.rowcorr = rowcorr;
-  CK(launch_round_cols(a, st));
-  CK(launch_round_combine_cols(a, c, V, Bpp, ec, blockpart, ticket, scal_dev, scal_host_dev, st));
+  CKL(launch_round_cols(a, st));
+  CKL(launch_round_combine_cols(a, c, V, Bpp, ec, blockpart, ticket, scal_dev, scal_host_dev, st));
   CK(cudaStreamSynchronize(st));
   const double cF = scal_host[0];
   a.B = Bpp;
-  CK(launch_round_rows3(a, st));
-  CK(launch_round_combine_rows(a, r, blockpart, ticket, scal_dev, scal_host_dev, st));
+  CKL(launch_round_rows3(a, st));
+  CKL(launch_round_combine_rows(a, r, blockpart, ticket, scal_dev, scal_host_dev, st));
   CK(cudaStreamSynchronize(st));
   const double ner = scal_host[0], cF2 = scal_host[1], corr = scal_host[2];
   if (cost_F) *cost_F = cF;
@@ -537,7 +544,7 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   if (P_out_dev) {
     a.plan = P_out_dev;
     a.inv_ner = ner >= 1e-300 ? 1.0 / ner : 0.0;
-    CK(launch_round_plan(a, st));
+    CKL(launch_round_plan(a, st));
   }
   return MDOT_OK;
 }
@@ -602,31 +609,31 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   if (st == MDOT_OK) {
     // P0 = r c^T -> U = log r, V = log c ; u = v = 0 (Alg. 1 line 2)
     if (o.p0_ones) {
-      launch_fill(n, 0.0, w.U, stream);
-      launch_fill(n, 0.0, w.V, stream);
+      ++w.launches; launch_fill(n, 0.0, w.U, stream);
+      ++w.launches; launch_fill(n, 0.0, w.V, stream);
     } else {
       cudaMemcpyAsync(w.U, w.logr, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
       cudaMemcpyAsync(w.V, w.logc, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
     }
-    launch_fill(n, 0.0, w.u, stream);
-    launch_fill(n, 0.0, w.v, stream);
+    ++w.launches; launch_fill(n, 0.0, w.u, stream);
+    ++w.launches; launch_fill(n, 0.0, w.v, stream);
     double gb = 0.0, gprev = 0.0;
     for (size_t t = 1; t <= gam.size(); ++t) {
       const double gt = gam[t - 1];
       gb += gt;
       w.set_gamma(gb);
       if (o.warm == MDOT_WARM_ZERO) {
-        launch_fill(n, 0.0, w.u, stream);
-        launch_fill(n, 0.0, w.v, stream);
+        ++w.launches; launch_fill(n, 0.0, w.u, stream);
+        ++w.launches; launch_fill(n, 0.0, w.v, stream);
       } else if (o.warm == MDOT_WARM_SCALED && t > 1 && gt != gprev) {
-        launch_axpby(n, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
-        launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
+        ++w.launches; launch_axpby(n, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
+        ++w.launches; launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
       }
       if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
       else solve_st = project_pncg(w, o, (int)t, res);
       res->md_steps = (int64_t)t;
-      launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u
-      launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);   // V += v
+      ++w.launches; launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u
+      ++w.launches; launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);   // V += v
       if (solve_st != MDOT_OK && solve_st != MDOT_ENOCONV) break;
       st = w.gauge_center(w.U, w.V);
       if (st == MDOT_OK) st = w.gauge_center(w.u, w.v);
@@ -657,6 +664,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   res->fallbacks = w.fallbacks;
   res->kernel_ms = w.kernel_ms;
   res->kernel_launches = w.kernel_launches;
+  res->all_launches = w.launches;
   w.free_owned();
   w.release();
   cudaError_t ce = cudaStreamSynchronize(stream);
@@ -754,8 +762,8 @@ mdot_status mdot_round(const mdot_problem* pb, const double* U, const double* V,
     const cudaMemcpyKind kin = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     cudaMemcpyAsync(w.U, U, sizeof(double) * n, kin, stream);
     cudaMemcpyAsync(w.V, V, sizeof(double) * n, kin, stream);
-    launch_fill(n, 0.0, w.u, stream);
-    launch_fill(n, 0.0, w.v, stream);
+    ++w.launches; launch_fill(n, 0.0, w.u, stream);
+    ++w.launches; launch_fill(n, 0.0, w.v, stream);
     double sc[kNumScalars];
     st = w.prep(PREP_CUR, 0, 0, nullptr, nullptr, nullptr);
     if (st == MDOT_OK) st = w.evaluate(w.cur, nullptr, nullptr, sc);

@@ -54,7 +54,7 @@ struct Workspace {
   int chunks = 1;
   EvalArgs eval{};
   // stats
-  int64_t evals = 0, fallbacks = 0, kernel_launches = 0;
+  int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;
   double kernel_ms = 0.0;
   double last_mass = 1.0;
   int time_kernels = 0;

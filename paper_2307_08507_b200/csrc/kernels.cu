@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
     double lm, bad = 0.0;
     if (a.from_partials) {
       double tot = 0.0;
-      if (is_row) {
+      if (a.from_partials == 2) {
+        tot = is_row ? a.rowtot[k] : a.coltot[k - a.nrows];
+      } else if (is_row) {
         for (int t = 0; t < a.n_col_tiles; ++t) tot += a.rowpart[(int64_t)t * a.nrows + k];
       } else {
         const int64_t j = k - a.nrows;

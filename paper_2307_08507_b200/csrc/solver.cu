@@ -12,6 +12,7 @@
 // kernel publishes to mapped pinned memory.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <stdlib.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -104,7 +105,9 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   size_t o_blk = take(fin_blocks * kNumScalars);
   size_t o_scal = take(kNumScalars * 2);
   size_t o_aux = take(8 * items);
-  size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256;
+  size_t o_tot = take(items);
+  const size_t tickets = (size_t)eval.n_row_tiles + eval.n_col_tiles + 64;
+  size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256 + tickets * 4;
   cudaError_t e = cudaMallocAsync(&base, bytes, st);
   if (e != cudaSuccess) {
     set_error("workspace allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
@@ -121,12 +124,16 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   trial = &mg[1];
   rowpart = D + o_rowpart; colpart = D + o_colpart; colm = D + o_colm; cols = D + o_cols; lr_ex = D + o_lr;
   blockpart = D + o_blk; scal_dev = D + o_scal; aux = D + o_aux;
+  tot.rowtot = D + o_tot;
+  tot.coltot = D + o_tot + nrows;
   float4* F4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(base) + dbl * sizeof(double));
   F4 = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(F4) + 15) & ~uintptr_t(15));
   rowp = F4;
   colp = F4 + nrows;
   ticket_flag = reinterpret_cast<unsigned int*>(colp + n + 8);
-  CK(cudaMemsetAsync(ticket_flag, 0, 64, st));
+  CK(cudaMemsetAsync(ticket_flag, 0, 64 + tickets * 4, st));
+  tot.row_ticket = ticket_flag + 16;
+  tot.col_ticket = tot.row_ticket + eval.n_row_tiles;
   ticket = ticket_flag;
   flag = reinterpret_cast<int*>(ticket_flag + 4);
   CK(cudaHostAlloc(&scal_host, 64 * sizeof(double), cudaHostAllocMapped));
@@ -466,6 +473,17 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   eval.C = (const float*)Cdev;
   eval.ldc = n;
   eval.X = Xdev; eval.Y = Ydev; eval.d = d; eval.scale = scale;
+  use_tma = false;
+  if (!otf && !c_f64 && getenv("MDOT_DISABLE_TMA") == nullptr && tma_supported(eval)) {
+    if (make_tma_map(eval, tmap) == cudaSuccess) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t tiles = (int64_t)eval.n_row_tiles * eval.n_col_tiles;
+      tma_grid = (int)std::min<int64_t>(tiles, 2 * (int64_t)sms);
+      use_tma = true;
+    }
+  }
   return MDOT_OK;
 }
 

@@ -53,6 +53,10 @@ struct Workspace {
   double* scal_host_dev = nullptr;  // its device alias
   int chunks = 1;
   EvalArgs eval{};
+  EvalTotals tot{};
+  alignas(64) unsigned char tmap[128];
+  bool use_tma = false;
+  int tma_grid = 0;
   // stats
   int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;
   double kernel_ms = 0.0;

@@ -237,3 +237,17 @@ def test_full_size_config4_sampled_parity():
     err_r = np.max(np.abs(np.expm1(lr.cpu().numpy()[rows] - sub["rows"])))
     err_c = np.max(np.abs(np.expm1(lc.cpu().numpy()[cols] - sub["cols"])))
     assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
+
+
+@pytest.mark.parametrize("n", [512, 2048])
+def test_tma_kernel_bitwise_equals_generic_kernel(n, monkeypatch):
+    """The TMA-fed persistent kernel and the generic LDG kernel assign the same
+    columns to the same lanes and sum in the same order: identical bits."""
+    inst = S.uniform_points_instance(3, n, 2, 8, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    A, B = _sinkhorn_potentials(prob, inst, 1024.0, iters=3, noise=0.02)
+    args = (_t(A), _t(B), 1024.0, _t(inst.C), _t(inst.r), _t(inst.c))
+    lr1, lc1, _ = M.mdot_marginals(*args)
+    monkeypatch.setenv("MDOT_DISABLE_TMA", "1")
+    lr2, lc2, _ = M.mdot_marginals(*args)
+    assert torch.equal(lr1, lr2) and torch.equal(lc1, lc2)

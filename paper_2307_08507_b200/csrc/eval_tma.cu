@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 
@@ -96,6 +98,7 @@ __device__ __forceinline__ double warp_reduce4_t(double v0, double v1, double v2
 
 __global__ void __launch_bounds__(kTmaThreads, 2)
     k_eval_tma(const __grid_constant__ CUtensorMap tmap, EvalArgs a, EvalTotals t) {
+  if (a.done && *a.done) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
   TmaSmem& sm = *reinterpret_cast<TmaSmem*>(smem_raw + pad);
@@ -136,7 +139,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   }
 
   // -------------------------------------------------------------- consumers
-  const float gh = a.gh, gl = a.gl;
+  const float gh = a.gpair ? a.gpair[0] : a.gh;
+  const float gl = a.gpair ? a.gpair[1] : a.gl;
   uint32_t it = 0;
   for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const int tr = (int)(tile / nct), tc = (int)(tile % nct);
@@ -252,10 +256,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    cudaError_t e = cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q);
+    if (e == cudaSuccess && q == cudaDriverEntryPointSuccess && p) {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    } else if (getenv("MDOT_DEBUG")) {
+      fprintf(stderr, "[mdot] cuTensorMapEncodeTiled lookup failed: %s (query %d)\n", cudaGetErrorString(e), (int)q);
+    }
   }
   return fn;
 }
@@ -276,6 +283,7 @@ cudaError_t make_tma_map(const EvalArgs& a, void* map_out /* CUtensorMap, 64 B a
                    const_cast<float*>(a.C), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("MDOT_DEBUG")) fprintf(stderr, "[mdot] cuTensorMapEncodeTiled failed: %d\n", (int)r);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 

@@ -40,6 +40,8 @@ struct EvalArgs {
   const float4* rowp;      // [nrows] {ah, al, S=2^rho, w}
   const float4* colp;      // [n]     {bh, bl, T=2^sig, w}
   float gh, gl;            // g2 = gbar*log2(e) = gh + gl
+  const float* gpair;      // device-resident {gh, gl} (device control), overrides gh/gl
+  const int* done;         // device control: kernel returns at once when *done != 0
   // outputs
   double* rowpart;         // [n_col_tiles][nrows]  sum_j 2^w T_j
   double* colpart;         // [n_row_tiles][n]      sum_i 2^w S_i
@@ -75,6 +77,7 @@ struct ExactArgs {
   double* colm;      // [chunks][n]
   double* cols;      // [chunks][n]
   int chunks;        // row chunks for the column pass
+  const int* done;   // device control early exit
 };
 cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st);
 
@@ -125,9 +128,39 @@ struct FinalizeArgs {
   double* scalars_dev;   // [kNumScalars]
   double* scalars_host;  // mapped host (nullable)
   int* prep_flag;        // nullable: added to SC_BAD, then reset to 0
+  const int* done;       // device control: return at once when *done != 0
   int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Device-resident PNCG / Sinkhorn control (one thread; k_ctrl).  The host
+// enqueues CUDA graphs of [k_ctrl, k_prep, eval, k_finalize] slots; the
+// controller reads the scalars of the previous slot's finalize, runs the
+// line-search / direction logic of project_pncg (Alg. 2, Appx. C, Z5-Z10)
+// and writes the next slot's mode, alpha, beta -- no host sync per trial.
+// ---------------------------------------------------------------------------
+enum CtrlStatus : int { CTRL_RUNNING = 0, CTRL_OK = 1, CTRL_NOCONV = 2, CTRL_LS_FAIL = 3, CTRL_NEED_HOST = 4 };
+struct CtrlState {
+  // configuration (host-written per projection)
+  double eps, c1, c2, noise;
+  int stop_rho, ncg, sinkhorn, beta_kind, ls_max_trials, pad0;
+  long long max_evals;
+  float gpair[2];
+  // next slot
+  int done, status, accept_marg, accept_pot, mode, phase;
+  double alpha, beta;
+  // iterate
+  long long k, evals, ls_evals, resets, restarts, iterations;
+  double mass, S_sg, S_gcs, S_pcg, S_gg, S_gcg, dphi0_prev, sg_prev, gg_prev, alpha_prev;
+  double l1, rho, l1_0, rho_0;
+  // line search
+  double lo, dlo, hi, dhi, dphi0, dg;
+  int have_hi, doublings, trials, attempt;
+  // scalars published by k_finalize
+  double sc[kNumScalars];
+};
+cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, cudaStream_t s);
 
 enum PrepMode : int {
   PREP_CUR = 0,         // A = U + u, B = V + v -> params
@@ -146,7 +179,7 @@ struct PrepArgs {
   double* tu; double* tv;             // trial potentials
   double* p;                          // [nrows + n] direction (written in NEWDIR)
   const double* s;                    // [nrows + n]
-  const double* pprev;                // [nrows + n]
+  double* pprev;                      // [nrows + n]
   const double* lm;                   // [nrows + n] current log marginals (Sinkhorn)
   const double* logr; const double* logc;
   const double* rho_r; const double* sig_c;
@@ -154,6 +187,10 @@ struct PrepArgs {
   double* Aout; double* Bout;         // fp64 bases (for the exact path)
   float4* rowp; float4* colp;
   int* flag;                          // set to 1 when |a2|,|b2| >= 2^15
+  // device control: mode/alpha/beta/accept come from ctrl; accept copies trial -> cur
+  const CtrlState* ctrl;
+  double *cur_lm, *cur_m, *cur_s, *cur_g;
+  const double *tr_lm, *tr_m, *tr_s, *tr_g;
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
 

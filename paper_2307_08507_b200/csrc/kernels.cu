@@ -88,6 +88,7 @@ template <int KIND, bool VEC4>
 __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  if (a.done && *a.done) return;
   const int64_t j0 = (int64_t)blockIdx.x * kTileN;
   const int64_t i0 = (int64_t)blockIdx.y * a.tile_m;
   const int64_t n = a.n, nrows = a.nrows;
@@ -120,7 +121,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
     __syncthreads();
   }
 
-  const float gh = a.gh, gl = a.gl;
+  const float gh = a.gpair ? a.gpair[0] : a.gh;
+  const float gl = a.gpair ? a.gpair[1] : a.gl;
   double cacc64[8];
   float cacc32[8];
 #pragma unroll
@@ -286,6 +288,7 @@ __device__ __forceinline__ double exact_cost(const ExactArgs& a, int64_t i, int6
 }
 
 __global__ void k_exact_rows(ExactArgs a) {
+  if (a.done && *a.done) return;
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= a.nrows) return;
@@ -304,6 +307,7 @@ __global__ void k_exact_rows(ExactArgs a) {
 }
 
 __global__ void k_exact_cols(ExactArgs a) {
+  if (a.done && *a.done) return;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int chunk = blockIdx.y;
   const int64_t rows_per = (a.nrows + a.chunks - 1) / a.chunks;
@@ -376,6 +380,7 @@ __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, uns
 // finalize: marginals, s, grad, scalars
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
+  if (a.done && *a.done) return;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t tot_items = a.nrows + a.n;
   double v[kNumScalars];
@@ -466,24 +471,47 @@ __global__ void k_prep(PrepArgs a) {
   if (k >= a.nrows + a.n) return;
   const bool is_row = k < a.nrows;
   const int64_t idx = is_row ? k : k - a.nrows;
+  int mode = a.mode;
+  double alpha = a.alpha, beta = a.beta;
+  const double* sdir = a.s;
+  if (a.ctrl) {
+    const CtrlState* c = a.ctrl;
+    // accepted trial becomes the iterate (Alg. 2 lines 11-13): element-wise copy
+    if (c->accept_marg) {
+      a.cur_lm[k] = a.tr_lm[k];
+      a.cur_m[k] = a.tr_m[k];
+      a.cur_s[k] = a.tr_s[k];
+      a.cur_g[k] = a.tr_g[k];
+    }
+    if (c->accept_pot) {
+      a.pprev[k] = a.p[k];
+      if (is_row) a.u[idx] = a.tu[idx];
+      else a.v[idx] = a.tv[idx];
+    }
+    if (c->done) return;
+    mode = c->mode;
+    alpha = c->alpha;
+    beta = c->beta;
+    sdir = c->ncg ? a.cur_g : a.cur_s;
+  }
   double pk = 0.0;
-  if (a.mode & PREP_NEWDIR) {
-    pk = -a.s[k] + (a.beta != 0.0 ? a.beta * a.pprev[k] : 0.0);
+  if (mode & PREP_NEWDIR) {
+    pk = -sdir[k] + (beta != 0.0 ? beta * a.pprev[k] : 0.0);
     a.p[k] = pk;
-  } else if (a.mode & PREP_TRIAL) {
+  } else if (mode & PREP_TRIAL) {
     pk = a.p[k];
   }
   double base;
   if (is_row) {
-    if (a.mode & PREP_TRIAL) {
-      const double t = a.u[idx] + a.alpha * pk;
+    if (mode & PREP_TRIAL) {
+      const double t = a.u[idx] + alpha * pk;
       a.tu[idx] = t;
       base = a.U[idx] + t;
-    } else if (a.mode & PREP_SK_ROW) {
+    } else if (mode & PREP_SK_ROW) {
       const double t = a.u[idx] + (a.logr[idx] - a.lm[k]);
       a.u[idx] = t;
       base = a.U[idx] + t;
-    } else if (a.mode & PREP_AB) {
+    } else if (mode & PREP_AB) {
       base = a.Ain[idx];
     } else {
       base = a.U[idx] + a.u[idx];
@@ -491,15 +519,15 @@ __global__ void k_prep(PrepArgs a) {
     if (a.Aout) a.Aout[idx] = base;
     a.rowp[idx] = split_param(base, a.rho_r[idx], a.flag);
   } else {
-    if (a.mode & PREP_TRIAL) {
-      const double t = a.v[idx] + a.alpha * pk;
+    if (mode & PREP_TRIAL) {
+      const double t = a.v[idx] + alpha * pk;
       a.tv[idx] = t;
       base = a.V[idx] + t;
-    } else if (a.mode & PREP_SK_COL) {
+    } else if (mode & PREP_SK_COL) {
       const double t = a.v[idx] + (a.logc[idx] - a.lm[k]);
       a.v[idx] = t;
       base = a.V[idx] + t;
-    } else if (a.mode & PREP_AB) {
+    } else if (mode & PREP_AB) {
       base = a.Bin[idx];
     } else {
       base = a.V[idx] + a.v[idx];
@@ -507,6 +535,135 @@ __global__ void k_prep(PrepArgs a) {
     if (a.Bout) a.Bout[idx] = base;
     a.colp[idx] = split_param(base, a.sig_c[idx], a.flag);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident controller (single thread), mirrors project_pncg /
+// project_sinkhorn in solver.cu step by step.
+// ---------------------------------------------------------------------------
+__device__ void ctrl_finish(CtrlState* st, int status, int* done_host) {
+  st->done = 1;
+  st->status = status;
+  if (done_host) *((volatile int*)done_host) = 1;
+}
+
+__device__ void ctrl_start_iteration(CtrlState* st) {
+  st->k++;
+  double beta = 0.0;
+  if (st->k > 1) {
+    double num, den;
+    if (st->ncg) { num = st->S_gg - st->S_gcg; den = st->gg_prev; }
+    else if (st->beta_kind == 0) { num = st->S_sg - st->S_gcs; den = -st->dphi0_prev; }   // Z6
+    else if (st->beta_kind == 1) { num = st->S_sg - st->S_gcs; den = st->sg_prev; }
+    else { num = st->S_sg; den = st->sg_prev; }
+    beta = (fabs(den) > 1e-300) ? num / den : 0.0;
+  }
+  const double dg = st->ncg ? st->S_gg : st->S_sg;
+  double dphi0 = -dg + beta * st->S_pcg;
+  if (!(dphi0 < 0.0)) { beta = 0.0; dphi0 = -dg; st->resets++; }   // Z5
+  st->dg = dg;
+  st->dphi0 = dphi0;
+  st->beta = beta;
+  st->alpha = (st->k == 1) ? 1.0 : fmin(4.0, fmax(0.25, st->alpha_prev));   // Z8
+  st->lo = 0.0; st->dlo = dphi0; st->hi = 0.0; st->dhi = 0.0;
+  st->have_hi = 0; st->doublings = 0; st->trials = 0; st->attempt = 0;
+  st->mode = PREP_NEWDIR | PREP_TRIAL;
+}
+
+__global__ void k_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host) {
+  if (threadIdx.x != 0) return;
+  if (st->done) { if (ran_host) ran_host[slot] = 0; return; }
+  st->accept_marg = 0;
+  st->accept_pot = 0;
+  const double* sc = st->sc;
+  const bool bad = sc[SC_BAD] != 0.0;
+  st->evals++;
+  if (st->phase == 0) {   // initial evaluation of the projection
+    if (bad) { ctrl_finish(st, CTRL_NEED_HOST, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    st->accept_marg = 1;
+    st->l1 = sc[SC_L1]; st->rho = sc[SC_RHO]; st->l1_0 = st->l1; st->rho_0 = st->rho;
+    st->mass = sc[SC_MASS];
+    st->S_sg = sc[SC_SG]; st->S_gg = sc[SC_GG];
+    st->S_gcs = 0.0; st->S_pcg = 0.0; st->S_gcg = 0.0;
+    st->phase = 1;
+    const double sv = st->stop_rho ? st->rho : st->l1;
+    if (sv <= st->eps) { ctrl_finish(st, CTRL_OK, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    if (st->evals >= st->max_evals) { ctrl_finish(st, CTRL_NOCONV, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    if (st->sinkhorn) { st->k = 1; st->mode = PREP_SK_ROW; }
+    else ctrl_start_iteration(st);
+    if (ran_host) ran_host[slot] = 1;
+    return;
+  }
+  if (st->sinkhorn) {   // Alg. 3 half-step result
+    if (bad) { ctrl_finish(st, CTRL_NEED_HOST, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    st->accept_marg = 1;
+    st->iterations++;
+    st->l1 = sc[SC_L1]; st->rho = sc[SC_RHO]; st->mass = sc[SC_MASS];
+    const double sv = st->stop_rho ? st->rho : st->l1;
+    if (sv <= st->eps) { ctrl_finish(st, CTRL_OK, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    if (st->evals >= st->max_evals) { ctrl_finish(st, CTRL_NOCONV, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    st->k++;
+    st->mode = (st->k % 2 == 1) ? PREP_SK_ROW : PREP_SK_COL;
+    if (ran_host) ran_host[slot] = 1;
+    return;
+  }
+  // PNCG line-search trial result (Appx. C; Z7, Z9)
+  st->ls_evals++;
+  st->trials++;
+  const double dphi_a = bad ? INFINITY : sc[SC_PCG];
+  const double dval = bad ? INFINITY : (sc[SC_MASS] - st->mass) - st->alpha * sc[SC_PRC];
+  const bool wolfe = ((2.0 * st->c1 - 1.0) * st->dphi0 >= dphi_a) && (dphi_a >= st->c2 * st->dphi0);
+  const bool decrease = dval <= st->noise * fmax(1.0, st->mass);
+  if (!bad && wolfe && decrease) {
+    st->accept_marg = 1;
+    st->accept_pot = 1;
+    st->iterations++;
+    st->dphi0_prev = st->dphi0;
+    st->sg_prev = st->S_sg;
+    st->gg_prev = st->S_gg;
+    st->S_sg = sc[SC_SG]; st->S_gcs = sc[SC_GCS]; st->S_pcg = sc[SC_PCG];
+    st->S_gg = sc[SC_GG]; st->S_gcg = sc[SC_GCG];
+    st->mass = sc[SC_MASS]; st->l1 = sc[SC_L1]; st->rho = sc[SC_RHO];
+    st->alpha_prev = st->alpha;
+    const double sv = st->stop_rho ? st->rho : st->l1;
+    if (sv <= st->eps) { ctrl_finish(st, CTRL_OK, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    if (st->evals >= st->max_evals) { ctrl_finish(st, CTRL_NOCONV, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    ctrl_start_iteration(st);
+    if (ran_host) ran_host[slot] = 1;
+    return;
+  }
+  if (dphi_a < 0.0 && decrease) { st->lo = st->alpha; st->dlo = dphi_a; }
+  else { st->hi = st->alpha; st->dhi = dphi_a; st->have_hi = 1; }
+  bool fail = false;
+  if (!st->have_hi) {
+    if (++st->doublings > 60) fail = true;
+    else st->alpha *= 2.0;
+  } else if (st->dhi > st->dlo && isfinite(st->dhi)) {
+    const double a_sec = (st->lo * st->dhi - st->hi * st->dlo) / (st->dhi - st->dlo);
+    st->alpha = 0.5 * a_sec + 0.5 * (st->hi + st->lo) / 2.0;
+  } else {
+    st->alpha = 0.5 * (st->lo + st->hi);
+  }
+  if (st->trials >= st->ls_max_trials) fail = true;
+  if (fail) {   // Z10
+    st->attempt++;
+    st->restarts++;
+    if (st->attempt >= 2) { ctrl_finish(st, CTRL_LS_FAIL, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    st->dphi0 = -st->dg;
+    st->alpha = 1.0;
+    st->beta = 0.0;
+    st->lo = 0.0; st->dlo = st->dphi0; st->hi = 0.0; st->dhi = 0.0;
+    st->have_hi = 0; st->doublings = 0; st->trials = 0;
+    st->mode = PREP_NEWDIR | PREP_TRIAL;
+  } else {
+    st->mode = PREP_TRIAL;
+  }
+  if (ran_host) ran_host[slot] = 1;
+}
+
+cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, cudaStream_t s) {
+  k_ctrl<<<1, 32, 0, s>>>(st, slot, done_host, ran_host);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {

@@ -106,6 +106,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   size_t o_scal = take(kNumScalars * 2);
   size_t o_aux = take(8 * items);
   size_t o_tot = take(items);
+  size_t o_ctrl = take((int64_t)((sizeof(CtrlState) + 7) / 8));
   const size_t tickets = (size_t)eval.n_row_tiles + eval.n_col_tiles + 64;
   size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256 + tickets * 4;
   cudaError_t e = cudaMallocAsync(&base, bytes, st);
@@ -124,6 +125,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   trial = &mg[1];
   rowpart = D + o_rowpart; colpart = D + o_colpart; colm = D + o_colm; cols = D + o_cols; lr_ex = D + o_lr;
   blockpart = D + o_blk; scal_dev = D + o_scal; aux = D + o_aux;
+  ctrl = reinterpret_cast<CtrlState*>(D + o_ctrl);
   tot.rowtot = D + o_tot;
   tot.coltot = D + o_tot + nrows;
   float4* F4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(base) + dbl * sizeof(double));
@@ -136,9 +138,11 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   tot.col_ticket = tot.row_ticket + eval.n_row_tiles;
   ticket = ticket_flag;
   flag = reinterpret_cast<int*>(ticket_flag + 4);
-  CK(cudaHostAlloc(&scal_host, 64 * sizeof(double), cudaHostAllocMapped));
+  CK(cudaHostAlloc(&scal_host, 256 * sizeof(double), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&scal_host_dev, scal_host, 0));
-  memset(scal_host, 0, 64 * sizeof(double));
+  memset(scal_host, 0, 256 * sizeof(double));
+  done_host = reinterpret_cast<int*>(scal_host + 64);
+  ran_host = reinterpret_cast<int*>(scal_host + 72);
   eval.rowp = rowp;
   eval.colp = colp;
   eval.rowpart = rowpart;
@@ -147,6 +151,14 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
 }
 
 void Workspace::release() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  gexec = nullptr;
+  if (cap_stream) cudaStreamDestroy(cap_stream);
+  cap_stream = nullptr;
+  if (gev_made)
+    for (auto& e : gev)
+      if (e) cudaEventDestroy(e);
+  gev_made = false;
   if (base) cudaFreeAsync(base, st);
   base = nullptr;
   if (scal_host) cudaFreeHost(scal_host);
@@ -353,6 +365,184 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
 }
 
 // ---------------------------------------------------------------------------
+// Device-resident control: graphs of [k_ctrl, k_prep, eval, k_finalize] slots
+// ---------------------------------------------------------------------------
+// done_host / ran_host live in mapped pinned memory; the device pointers
+// handed to kernels are their device aliases.
+static int* dev_alias(int* h) {
+  void* d = nullptr;
+  cudaHostGetDevicePointer(&d, h, 0);
+  return reinterpret_cast<int*>(d);
+}
+
+mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed) {
+  PrepArgs a{};
+  a.n = n; a.nrows = nrows; a.mode = 0;
+  a.U = U; a.V = V; a.u = u; a.v = v; a.tu = tu; a.tv = tv;
+  a.p = p; a.s = cur->s; a.pprev = pprev; a.lm = cur->lm;
+  a.logr = logr; a.logc = logc; a.rho_r = rho_r; a.sig_c = sig_c;
+  a.Aout = A; a.Bout = B;
+  a.rowp = rowp; a.colp = colp; a.flag = flag;
+  a.ctrl = ctrl;
+  a.cur_lm = cur->lm; a.cur_m = cur->m; a.cur_s = cur->s; a.cur_g = cur->g;
+  a.tr_lm = trial->lm; a.tr_m = trial->m; a.tr_s = trial->s; a.tr_g = trial->g;
+  CKL(launch_prep(a, s));
+  FinalizeArgs f{};
+  f.n = n; f.nrows = nrows;
+  f.rho_r = rho_r; f.sig_c = sig_c;
+  f.r = r; f.c = c; f.logr = logr; f.logc = logc;
+  f.gcur = cur->g; f.pcur = p;
+  f.lm = trial->lm; f.m = trial->m; f.s = trial->s; f.g = trial->g;
+  f.blockpart = blockpart; f.ticket = ticket;
+  f.scalars_dev = ctrl->sc; f.scalars_host = nullptr;
+  f.prep_flag = flag;
+  f.done = &ctrl->done;
+  if (timed) CK(cudaEventRecordWithFlags(gev[2 * slot], s, cudaEventRecordExternal));
+  if (!exact_mode) {
+    EvalArgs e = eval;
+    e.gpair = ctrl->gpair;
+    e.done = &ctrl->done;
+    if (use_tma) {
+      CKL(launch_eval_tma(tmap, e, tot, tma_grid, s));
+      f.from_partials = 2;
+      f.rowtot = tot.rowtot;
+      f.coltot = tot.coltot;
+    } else {
+      CKL(launch_eval_fast(e, kind_fast, s));
+      f.from_partials = 1;
+      f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
+      f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
+    }
+  } else {
+    ExactArgs x{};
+    x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
+    x.X = Xdev; x.Y = Ydev; x.d = d; x.scale = scale; x.otf = otf;
+    x.n = n; x.nrows = nrows;
+    x.A = A; x.B = B; x.gbar = 0.0;   // gbar set below from the host value (exact mode rebuilds per step)
+    x.gbar = gbar;
+    x.lr = lr_ex; x.colm = colm; x.cols = cols; x.chunks = chunks;
+    x.done = &ctrl->done;
+    CKL(launch_eval_exact(x, s));
+    f.from_partials = 0;
+    f.lr_in = lr_ex; f.colm = colm; f.cols = cols; f.chunks = chunks;
+  }
+  if (timed) CK(cudaEventRecordWithFlags(gev[2 * slot + 1], s, cudaEventRecordExternal));
+  CKL(launch_finalize(f, s));
+  return MDOT_OK;
+}
+
+mdot_status Workspace::build_graph() {
+  const void* sig[8] = {cur, trial, u, tu, p, pprev, (const void*)(intptr_t)(exact_mode ? 1 : 0),
+                        (const void*)(intptr_t)(exact_mode ? (int64_t)(gbar * 1024.0) : 0)};
+  if (gexec && memcmp(sig, gsig, sizeof(sig)) == 0) return MDOT_OK;
+  if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+  if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+  if (!gev_made) {
+    for (auto& e : gev) CK(cudaEventCreate(&e));
+    gev_made = true;
+  }
+  // slots per graph: ~2 ms of work, 4..64
+  const double est = 4.0 * (double)n * (double)nrows / 5.0e12 + 8e-6;
+  gslots = (int)std::max(4.0, std::min(64.0, ceil(2e-3 / est)));
+  int* dh = dev_alias(done_host);
+  int* rh = dev_alias(ran_host);
+  CK(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t saved = launches;
+  mdot_status stt = MDOT_OK;
+  for (int k = 0; k < gslots && stt == MDOT_OK; ++k) {
+    cudaError_t e = launch_ctrl(ctrl, k, dh, rh, cap_stream);
+    if (e != cudaSuccess) { set_error("capture ctrl: %s", cudaGetErrorString(e)); stt = MDOT_ECUDA; break; }
+    stt = launch_slot_body(cap_stream, k, true);
+  }
+  launches = saved;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cap_stream, &g);
+  if (stt != MDOT_OK) { if (g) cudaGraphDestroy(g); return stt; }
+  if (e != cudaSuccess) { set_error("graph capture failed: %s", cudaGetErrorString(e)); return MDOT_ECUDA; }
+  e = cudaGraphInstantiate(&gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) { set_error("graph instantiate failed: %s", cudaGetErrorString(e)); return MDOT_ECUDA; }
+  memcpy(gsig, sig, sizeof(sig));
+  return MDOT_OK;
+}
+
+mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  CtrlState h{};
+  h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
+  h.noise = w.exact_mode ? 1e-14 : 6e-8;
+  h.stop_rho = o.stop; h.ncg = o.projector == MDOT_PROJ_NCG; h.sinkhorn = o.projector == MDOT_PROJ_SINKHORN;
+  h.beta_kind = o.beta; h.ls_max_trials = o.ls_max_trials;
+  h.max_evals = o.max_evals - w.evals;
+  h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
+  h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+  CKS(w.build_graph());
+  cudaStream_t st = w.st;
+  CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  *((volatile int*)w.done_host) = 0;
+  // initial evaluation (its result is consumed by the first k_ctrl)
+  if (w.time_kernels) CK(cudaEventRecord(w.ev0, st));
+  {
+    // the slot body with ctrl->mode = PREP_CUR and no accept
+    const int64_t before = w.launches;
+    CKS(w.launch_slot_body(st, 0, false));
+    (void)before;
+  }
+  if (w.time_kernels) CK(cudaEventRecord(w.ev1, st));
+  bool first = true;
+  for (;;) {
+    for (int k = 0; k < w.gslots; ++k) ((volatile int*)w.ran_host)[k] = 0;
+    CK(cudaGraphLaunch(w.gexec, st));
+    w.launches += 4 * w.gslots;
+    CK(cudaStreamSynchronize(st));
+    if (w.time_kernels) {
+      float ms = 0.f;
+      if (first) {
+        CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+        w.kernel_ms += ms;   // includes the initial prep (a few us)
+        w.kernel_launches++;
+      }
+      for (int k = 0; k < w.gslots; ++k) {
+        if (((volatile int*)w.ran_host)[k]) {
+          CK(cudaEventElapsedTime(&ms, w.gev[2 * k], w.gev[2 * k + 1]));
+          w.kernel_ms += ms;
+          w.kernel_launches++;
+        }
+      }
+    }
+    first = false;
+    if (*((volatile int*)w.done_host)) break;
+  }
+  CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  w.evals += h.evals;
+  res->iterations += h.iterations;
+  res->ls_evaluations += h.ls_evals;
+  res->resets += h.resets;
+  res->ls_restarts += h.restarts;
+  if (t >= 1 && t <= 64) {
+    res->rho0[t - 1] = h.rho_0;
+    res->l10[t - 1] = h.l1_0;
+    res->iters_step[t - 1] += h.iterations;
+  }
+  res->l1_final = h.l1;
+  res->rho_final = h.rho;
+  w.last_mass = h.mass;
+  switch (h.status) {
+    case CTRL_OK: return MDOT_OK;
+    case CTRL_NOCONV: return MDOT_ENOCONV;
+    case CTRL_LS_FAIL:
+      set_error("line search failed twice at MD step %d (device control)", t);
+      return MDOT_ELINESEARCH;
+    case CTRL_NEED_HOST:
+    default:
+      // range guard fired: continue this projection under host control with
+      // the exact fp64 re-evaluation available (u, v hold the last iterate)
+      w.fallbacks++;
+      return (o.projector == MDOT_PROJ_SINKHORN) ? project_sinkhorn(w, o, t, res) : project_pncg(w, o, t, res);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Schedules (Z13)
 // ---------------------------------------------------------------------------
 mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g) {
@@ -484,6 +674,9 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       use_tma = true;
     }
   }
+  if (getenv("MDOT_DEBUG"))
+    fprintf(stderr, "[mdot] n=%lld nrows=%lld tile_m=%d tiles=%dx%d use_tma=%d grid=%d exact=%d\n", (long long)n,
+            (long long)nrows, eval.tile_m, eval.n_row_tiles, eval.n_col_tiles, (int)use_tma, tma_grid, (int)exact_mode);
   return MDOT_OK;
 }
 
@@ -591,6 +784,7 @@ void mdot_options_default(mdot_options* o) {
   o->precision = MDOT_PREC_AUTO;
   o->ls_max_trials = 100;
   o->max_evals = 10000000;
+  o->device_control = 1;
 }
 
 void mdot_schedule_default(mdot_schedule* s) {
@@ -647,7 +841,8 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
         ++w.launches; launch_axpby(n, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
         ++w.launches; launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
       }
-      if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
+      if (o.device_control) solve_st = project_device(w, o, (int)t, res);
+      else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
       else solve_st = project_pncg(w, o, (int)t, res);
       res->md_steps = (int64_t)t;
       ++w.launches; launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u

@@ -64,7 +64,20 @@ struct Workspace {
   int time_kernels = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+  // device-resident control
+  CtrlState* ctrl = nullptr;
+  int* done_host = nullptr;
+  int* ran_host = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int gslots = 0;
+  const void* gsig[8] = {};
+  cudaEvent_t gev[2 * 65] = {};
+  bool gev_made = false;
+
   mdot_status alloc(cudaStream_t stream, int64_t n, int64_t nrows);
+  mdot_status launch_slot_body(cudaStream_t s, int slot, bool timed);
+  mdot_status build_graph();
   void release();
   mdot_status load_problem(const mdot_problem* pb, int64_t row0);
   void free_owned();
@@ -80,5 +93,6 @@ struct Workspace {
 mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g);
 mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result* res);
 mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_result* res);
+mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_result* res);
 
 }  // namespace mdot

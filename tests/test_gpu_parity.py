@@ -251,3 +251,31 @@ def test_tma_kernel_bitwise_equals_generic_kernel(n, monkeypatch):
     monkeypatch.setenv("MDOT_DISABLE_TMA", "1")
     lr2, lc2, _ = M.mdot_marginals(*args)
     assert torch.equal(lr1, lr2) and torch.equal(lc1, lc2)
+
+
+@pytest.mark.parametrize("projector", [0, 1, 2])
+def test_device_control_matches_host_control(projector):
+    """Device-resident line search (k_ctrl + CUDA graph) against the host
+    control loop: same algorithm, same gates (trajectories may differ in the
+    last bits: the device contracts a*b+c into FMA)."""
+    n = 512
+    inst = S.uniform_points_instance(3, n, 2, 9, marg="dirichlet")
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, 1024.0, T=4)
+    eps = 1e-6
+    rd = M.mdot_solve(C, r, c, schedule=sched, options=M.options(eps=eps, projector=projector, device_control=1))
+    rh = M.mdot_solve(C, r, c, schedule=sched, options=M.options(eps=eps, projector=projector, device_control=0))
+    assert rd["status"] == 0 and rh["status"] == 0
+    assert rd["l1_final"] <= eps and rh["l1_final"] <= eps
+    assert abs(rd["cost_unrounded"] - rh["cost_unrounded"]) <= 2e-6 * rh["cost_unrounded"]
+    assert rd["evaluations"] <= 1.5 * rh["evaluations"] + 20
+
+
+def test_device_control_fp64_config1():
+    inst = S.config1(1)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_DOUBLING, 4096.0),
+                       options=M.options(eps=1e-6, device_control=1))
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_doubling(4096.0), O.make_options(eps=1e-6))
+    assert res["status"] == 0
+    assert abs(res["cost_unrounded"] - ores["cost_unrounded"]) <= 1e-5 * ores["cost_unrounded"]

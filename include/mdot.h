@@ -180,6 +180,12 @@ typedef struct mdot_comm mdot_comm;
 mdot_status mdot_get_unique_id(void* nccl_unique_id_out);
 mdot_status mdot_comm_create(const void* nccl_unique_id, int32_t nranks, int32_t rank, int32_t device,
                              mdot_comm** out);
+/* In-process transport: `nranks` threads of ONE process (one stream each,
+ * possibly on one GPU) form group `group`; every allreduce is a host-side
+ * deterministic rank-ordered sum.  For tests of the sharded path on one GPU
+ * (virtual ranks) and for single-process multi-GPU embedding. */
+mdot_status mdot_comm_create_local(const char* group, int32_t nranks, int32_t rank, int32_t device,
+                                   mdot_comm** out);
 mdot_status mdot_comm_destroy(mdot_comm* comm);
 /* local rows [row0, row0 + n_local) of C (local_rows->C points at row row0,
  * n_local*n entries) or of X (local_rows->X at row row0; Y, r, c full).

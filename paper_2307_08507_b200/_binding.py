@@ -100,11 +100,12 @@ def lib():
         L.mdot_get_unique_id.argtypes = [P]
         L.mdot_comm_create.argtypes = [P, ct.c_int32, ct.c_int32, ct.c_int32, ct.POINTER(P)]
         L.mdot_comm_destroy.argtypes = [P]
+        L.mdot_comm_create_local.argtypes = [ct.c_char_p, ct.c_int32, ct.c_int32, ct.c_int32, ct.POINTER(P)]
         L.mdot_solve_sharded.argtypes = [P, ct.POINTER(Problem), ct.c_int64, ct.c_int64,
                                          ct.POINTER(Schedule), ct.POINTER(Options), P, P,
                                          ct.POINTER(Result)]
         for nm in ("mdot_solve_batch", "mdot_marginals", "mdot_round", "mdot_get_unique_id",
-                   "mdot_comm_create", "mdot_comm_destroy", "mdot_solve_sharded"):
+                   "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_destroy", "mdot_solve_sharded"):
             getattr(L, nm).restype = ct.c_int
         if L.mdot_abi_version() != 1:
             raise ImportError("libmdot_b200.so ABI version mismatch")
@@ -276,6 +277,13 @@ def mdot_comm_create(unique_id: bytes, nranks: int, rank: int, device: int):
     buf = ct.create_string_buffer(bytes(unique_id), 128)
     out = ct.c_void_p()
     _check(lib().mdot_comm_create(buf, nranks, rank, device, ct.byref(out)), "mdot_comm_create")
+    return out
+
+
+def mdot_comm_create_local(group: str, nranks: int, rank: int, device: int):
+    out = ct.c_void_p()
+    _check(lib().mdot_comm_create_local(group.encode(), nranks, rank, device, ct.byref(out)),
+           "mdot_comm_create_local")
     return out
 
 

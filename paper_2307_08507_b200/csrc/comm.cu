@@ -5,7 +5,15 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <math.h>
 #include <string.h>
+
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "../../include/mdot.h"
 #include "comm.h"
@@ -52,9 +60,75 @@ static bool load_nccl() {
   return true;
 }
 
-mdot_status comm_allreduce_sum(Comm* cm, double* buf, size_t count, cudaStream_t st) {
+// In-process transport: ranks are threads of one process (one stream each);
+// each allreduce syncs its stream, deposits its buffer, waits for all ranks
+// and reduces the deposits in rank order (deterministic).  No device code
+// waits on another rank, so virtual ranks may share one GPU.
+struct LocalGroup {
+  int nranks = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  std::vector<std::vector<double>> slots;
+  std::vector<double> result;
+  int refs = 0;
+};
+static std::mutex g_groups_m;
+static std::map<std::string, std::shared_ptr<LocalGroup>> g_groups;
+
+static mdot_status local_allreduce(Comm* cm, double* buf, size_t count, int op, cudaStream_t st) {
+  LocalGroup* g = cm->local;
+  std::vector<double> mine(count);
+  if (cudaStreamSynchronize(st) != cudaSuccess ||
+      cudaMemcpy(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    set_error("local allreduce: device copy failed");
+    return MDOT_ECUDA;
+  }
+  {
+    std::unique_lock<std::mutex> lk(g->m);
+    g->slots[cm->rank].swap(mine);
+    const long long gen = g->generation;
+    if (++g->arrived == g->nranks) {
+      g->result.assign(count, op == COMM_MAX ? -INFINITY : 0.0);
+      for (int q = 0; q < g->nranks; ++q)
+        for (size_t i = 0; i < count; ++i) {
+          const double x = g->slots[q][i];
+          g->result[i] = (op == COMM_MAX) ? (x > g->result[i] ? x : g->result[i]) : g->result[i] + x;
+        }
+      g->arrived = 0;
+      g->generation++;
+      g->cv.notify_all();
+    } else {
+      g->cv.wait(lk, [&] { return g->generation != gen; });
+    }
+    mine = g->result;
+  }
+  // second barrier: nobody may start the next allreduce (overwriting result)
+  // before every rank copied this one
+  {
+    std::unique_lock<std::mutex> lk(g->m);
+    const long long gen = g->generation;
+    if (++g->arrived == g->nranks) {
+      g->arrived = 0;
+      g->generation++;
+      g->cv.notify_all();
+    } else {
+      g->cv.wait(lk, [&] { return g->generation != gen; });
+    }
+  }
+  if (cudaMemcpy(buf, mine.data(), count * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_error("local allreduce: device copy failed");
+    return MDOT_ECUDA;
+  }
+  return MDOT_OK;
+}
+
+mdot_status comm_allreduce(Comm* cm, double* buf, size_t count, int op, cudaStream_t st) {
   if (!cm || cm->nranks == 1) return MDOT_OK;
-  ncclResult_t r = g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)cm->nccl, st);
+  if (cm->local) return local_allreduce(cm, buf, count, op, st);
+  ncclResult_t r = g_nccl.AllReduce(buf, buf, count, ncclFloat64, op == COMM_MAX ? ncclMax : ncclSum,
+                                    (ncclComm_t)cm->nccl, st);
   if (r != ncclSuccess) {
     set_error("ncclAllReduce failed: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
     return MDOT_ENCCL;
@@ -102,23 +176,49 @@ mdot_status mdot_comm_create(const void* uid, int32_t nranks, int32_t rank, int3
   return MDOT_OK;
 }
 
+mdot_status mdot_comm_create_local(const char* group, int32_t nranks, int32_t rank, int32_t device,
+                                   mdot_comm** out) {
+  if (!group || !out || nranks < 1 || rank < 0 || rank >= nranks) { set_error("bad comm arguments"); return MDOT_EINVAL; }
+  if (cudaSetDevice(device) != cudaSuccess) { set_error("cudaSetDevice(%d) failed", device); return MDOT_ECUDA; }
+  std::shared_ptr<LocalGroup> g;
+  {
+    std::lock_guard<std::mutex> lk(g_groups_m);
+    auto it = g_groups.find(group);
+    if (it == g_groups.end()) {
+      g = std::make_shared<LocalGroup>();
+      g->nranks = nranks;
+      g->slots.resize(nranks);
+      g_groups[group] = g;
+    } else {
+      g = it->second;
+      if (g->nranks != nranks) { set_error("local group %s has %d ranks", group, g->nranks); return MDOT_EINVAL; }
+    }
+    g->refs++;
+  }
+  Comm* cm = new Comm();
+  cm->nranks = nranks;
+  cm->rank = rank;
+  cm->device = device;
+  cm->local = g.get();
+  *out = reinterpret_cast<mdot_comm*>(cm);
+  return MDOT_OK;
+}
+
 mdot_status mdot_comm_destroy(mdot_comm* c) {
   Comm* cm = reinterpret_cast<Comm*>(c);
   if (!cm) return MDOT_OK;
   if (cm->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)cm->nccl);
+  if (cm->local) {
+    std::lock_guard<std::mutex> lk(g_groups_m);
+    for (auto it = g_groups.begin(); it != g_groups.end(); ++it)
+      if (it->second.get() == cm->local) {
+        if (--it->second->refs == 0) g_groups.erase(it);
+        break;
+      }
+  }
   delete cm;
   return MDOT_OK;
 }
 
 }  // extern "C"
 
-extern "C" mdot_status mdot_solve_sharded(mdot_comm* c, const mdot_problem* local_rows, int64_t row0,
-                                          int64_t n_local, const mdot_schedule* sched, const mdot_options* opt,
-                                          double* u_local_out, double* v_out, mdot_result* res) {
-  Comm* cm = reinterpret_cast<Comm*>(c);
-  if (!cm || !local_rows) { set_error("bad arguments"); return MDOT_EINVAL; }
-  if (cm->nranks == 1 && row0 == 0 && n_local == local_rows->n)
-    return mdot_solve(local_rows, sched, opt, u_local_out, v_out, nullptr, res);
-  set_error("multi-rank sharded solve is not available in this build");
-  return MDOT_EINVAL;
-}

@@ -7,12 +7,19 @@
 
 namespace mdot {
 
+struct LocalGroup;
+
 struct Comm {
   int nranks = 1, rank = 0, device = 0;
-  void* nccl = nullptr;   // ncclComm_t
+  void* nccl = nullptr;          // ncclComm_t (NCCL transport)
+  LocalGroup* local = nullptr;   // in-process transport (virtual ranks / tests)
 };
 
-// In-place fp64 sum allreduce on `st` (no-op for a single rank).
-mdot_status comm_allreduce_sum(Comm* cm, double* buf, size_t count, cudaStream_t st);
+enum { COMM_SUM = 0, COMM_MAX = 1 };
+// In-place fp64 allreduce on `st` (no-op for a single rank).
+mdot_status comm_allreduce(Comm* cm, double* buf, size_t count, int op, cudaStream_t st);
+inline mdot_status comm_allreduce_sum(Comm* cm, double* buf, size_t count, cudaStream_t st) {
+  return comm_allreduce(cm, buf, count, COMM_SUM, st);
+}
 
 }  // namespace mdot

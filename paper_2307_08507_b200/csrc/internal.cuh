@@ -129,6 +129,8 @@ struct FinalizeArgs {
   double* scalars_host;  // mapped host (nullable)
   int* prep_flag;        // nullable: added to SC_BAD, then reset to 0
   const int* done;       // device control: return at once when *done != 0
+  int64_t item_begin, item_end;   // items processed: [begin, end) of [0, nrows + n) (end 0 = all)
+  const double* add_in;  // nullable: kNumScalars values added before publishing (sharded rows)
   int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
@@ -203,6 +205,14 @@ cudaError_t launch_fill(int64_t n, double v, double* y, cudaStream_t st);
 cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,
                         double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
                         cudaStream_t st);
+// column partials -> local column totals (generic kernel, sharded mode)
+cudaError_t launch_reduce_colpart(const double* colpart, int n_row_tiles, int64_t n, double* coltot, cudaStream_t st);
+// exact path, sharded: combine chunk (max, sum) pairs; rescale sums to a global max
+cudaError_t launch_exact_colcombine(const double* colm, const double* cols, int chunks, int64_t n, double* M,
+                                    double* S, cudaStream_t st);
+cudaError_t launch_rescale_to_max(int64_t n, const double* Mloc, const double* Mglob, double* S, cudaStream_t st);
+cudaError_t launch_sum_chunks(const double* x, int chunks, int64_t n, double* out, cudaStream_t st);
+
 // rounding (fp64, once per solve)
 struct RoundArgs {
   const void* C; int64_t ldc; int c_f64;

@@ -339,7 +339,7 @@ cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 template <int NS>
 __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, unsigned int* ticket,
-                                         double* out_dev, double* out_host) {
+                                         double* out_dev, double* out_host, const double* add_in = nullptr) {
   __shared__ double sm[32][NS];
   __shared__ bool is_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -369,6 +369,7 @@ __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, uns
       double x = 0.0;
       for (unsigned b = 0; b < gridDim.x; ++b)
         x += *((volatile double*)&blockpart[(int64_t)b * NS + threadIdx.x]);
+      if (add_in) x += add_in[threadIdx.x];
       out_dev[threadIdx.x] = x;
       if (out_host) out_host[threadIdx.x] = x;
     }
@@ -381,8 +382,8 @@ __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, uns
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   if (a.done && *a.done) return;
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t tot_items = a.nrows + a.n;
+  const int64_t k = a.item_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot_items = a.item_end > 0 ? a.item_end : a.nrows + a.n;
   double v[kNumScalars];
 #pragma unroll
   for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
@@ -439,15 +440,15 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
     v[SC_BAD] = bad;
     v[SC_L1R] = is_row ? fabs(g) : 0.0;
   }
-  if (a.prep_flag && k == 0) {
+  if (a.prep_flag && k == a.item_begin) {
     v[SC_BAD] += (double)(*a.prep_flag);
     *a.prep_flag = 0;
   }
-  block_reduce_and_publish<kNumScalars>(v, a.blockpart, a.ticket, a.scalars_dev, a.scalars_host);
+  block_reduce_and_publish<kNumScalars>(v, a.blockpart, a.ticket, a.scalars_dev, a.scalars_host, a.add_in);
 }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
-  const int64_t items = a.nrows + a.n;
+  const int64_t items = (a.item_end > 0 ? a.item_end : a.nrows + a.n) - a.item_begin;
   const unsigned blocks = (unsigned)((items + 255) / 256);
   k_finalize<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
@@ -758,6 +759,55 @@ __global__ void k_round_rows(int64_t n, const double* logr, const double* lr, co
 cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
                               double* logx, double* Aout, cudaStream_t st) {
   k_round_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, logr, lr, U, logx, Aout);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// sharded helpers
+// ---------------------------------------------------------------------------
+__global__ void k_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = 0.0;
+  for (int t = 0; t < nt; ++t) acc += colpart[(int64_t)t * n + j];
+  coltot[j] = acc;
+}
+cudaError_t launch_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot, cudaStream_t st) {
+  k_reduce_colpart<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colpart, nt, n, coltot);
+  return cudaGetLastError();
+}
+__global__ void k_exact_colcombine(const double* colm, const double* cols, int chunks, int64_t n, double* M,
+                                   double* S) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double m = -INFINITY, s = 0.0;
+  for (int c = 0; c < chunks; ++c) lse_merge(m, s, colm[(int64_t)c * n + j], cols[(int64_t)c * n + j]);
+  M[j] = m;
+  S[j] = s;
+}
+cudaError_t launch_exact_colcombine(const double* colm, const double* cols, int chunks, int64_t n, double* M,
+                                    double* S, cudaStream_t st) {
+  k_exact_colcombine<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colm, cols, chunks, n, M, S);
+  return cudaGetLastError();
+}
+__global__ void k_rescale_to_max(int64_t n, const double* Mloc, const double* Mglob, double* S) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  S[j] = (S[j] == 0.0) ? 0.0 : S[j] * exp(Mloc[j] - Mglob[j]);
+}
+cudaError_t launch_rescale_to_max(int64_t n, const double* Mloc, const double* Mglob, double* S, cudaStream_t st) {
+  k_rescale_to_max<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, Mloc, Mglob, S);
+  return cudaGetLastError();
+}
+__global__ void k_sum_chunks(const double* x, int chunks, int64_t n, double* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = 0.0;
+  for (int c = 0; c < chunks; ++c) acc += x[(int64_t)c * n + j];
+  out[j] = acc;
+}
+cudaError_t launch_sum_chunks(const double* x, int chunks, int64_t n, double* out, cudaStream_t st) {
+  k_sum_chunks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, chunks, n, out);
   return cudaGetLastError();
 }
 

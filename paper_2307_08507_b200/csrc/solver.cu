@@ -25,6 +25,7 @@
 
 #include "../../include/mdot.h"
 #include "internal.cuh"
+#include "comm.h"
 #include "solver.h"
 
 namespace mdot {
@@ -72,6 +73,8 @@ static double now_s() {
 // ---------------------------------------------------------------------------
 // Workspace
 // ---------------------------------------------------------------------------
+bool Workspace::sharded() const { return comm != nullptr && comm->nranks > 1; }
+
 mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   st = stream;
   n = n_;
@@ -105,7 +108,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   size_t o_blk = take(fin_blocks * kNumScalars);
   size_t o_scal = take(kNumScalars * 2);
   size_t o_aux = take(8 * items);
-  size_t o_tot = take(items);
+  size_t o_tot = take(items + 32);
   size_t o_ctrl = take((int64_t)((sizeof(CtrlState) + 7) / 8));
   const size_t tickets = (size_t)eval.n_row_tiles + eval.n_col_tiles + 64;
   size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256 + tickets * 4;
@@ -182,15 +185,53 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   f.blockpart = blockpart; f.ticket = ticket;
   f.scalars_dev = scal_dev; f.scalars_host = scal_host_dev;
   f.prep_flag = flag;
+  const bool shard = sharded();
   evals++;
   if (!exact_mode) {
     if (time_kernels) CK(cudaEventRecord(ev0, st));
-    CKL(launch_eval_fast(eval, kind_fast, st));
+    if (use_tma) {
+      CKL(launch_eval_tma(tmap, eval, tot, tma_grid, st));
+    } else {
+      CKL(launch_eval_fast(eval, kind_fast, st));
+    }
     if (time_kernels) CK(cudaEventRecord(ev1, st));
-    f.from_partials = 1;
-    f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
-    f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
-    CKL(launch_finalize(f, st));
+    if (!shard) {
+      if (use_tma) {
+        f.from_partials = 2;
+        f.rowtot = tot.rowtot;
+        f.coltot = tot.coltot;
+      } else {
+        f.from_partials = 1;
+        f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
+        f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
+      }
+      CKL(launch_finalize(f, st));
+    } else {
+      // rows are complete locally; columns are partial over this rank's rows.
+      // Row scalars go into the tail of the column buffer so ONE allreduce
+      // carries [column totals | row scalars].
+      double* colbuf = tot.coltot;
+      if (use_tma) {
+        f.from_partials = 2;
+        f.rowtot = tot.rowtot;
+      } else {
+        f.from_partials = 1;
+        f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
+        CKL(launch_reduce_colpart(colpart, eval.n_row_tiles, n, colbuf, st));
+      }
+      FinalizeArgs fr = f;
+      fr.item_begin = 0; fr.item_end = nrows;
+      fr.scalars_dev = colbuf + n; fr.scalars_host = nullptr;
+      CKL(launch_finalize(fr, st));
+      CKS(comm_allreduce(comm, colbuf, (size_t)n + kNumScalars, COMM_SUM, st));
+      FinalizeArgs fc = f;
+      fc.from_partials = 2;
+      fc.coltot = colbuf;
+      fc.item_begin = nrows; fc.item_end = nrows + n;
+      fc.add_in = colbuf + n;
+      fc.prep_flag = nullptr;
+      CKL(launch_finalize(fc, st));
+    }
     CK(cudaStreamSynchronize(st));
     if (time_kernels) {
       float ms = 0.f;
@@ -212,7 +253,28 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   f.from_partials = 0;
   f.lr_in = lr_ex; f.colm = colm; f.cols = cols; f.chunks = chunks;
   f.prep_flag = nullptr;
-  CKL(launch_finalize(f, st));
+  if (!shard) {
+    CKL(launch_finalize(f, st));
+  } else {
+    // columns: local (max, sum) -> global max -> rescale -> global sum
+    double* Mloc = aux;
+    double* Mg = aux + n;
+    double* Sg = aux + 2 * n;   // followed by kNumScalars row scalars
+    CKL(launch_exact_colcombine(colm, cols, chunks, n, Mloc, Sg, st));
+    CK(cudaMemcpyAsync(Mg, Mloc, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CKS(comm_allreduce(comm, Mg, (size_t)n, COMM_MAX, st));
+    CKL(launch_rescale_to_max(n, Mloc, Mg, Sg, st));
+    FinalizeArgs fr = f;
+    fr.item_begin = 0; fr.item_end = nrows;
+    fr.scalars_dev = Sg + n; fr.scalars_host = nullptr;
+    CKL(launch_finalize(fr, st));
+    CKS(comm_allreduce(comm, Sg, (size_t)n + kNumScalars, COMM_SUM, st));
+    FinalizeArgs fc = f;
+    fc.colm = Mg; fc.cols = Sg; fc.chunks = 1;
+    fc.item_begin = nrows; fc.item_end = nrows + n;
+    fc.add_in = Sg + n;
+    CKL(launch_finalize(fc, st));
+  }
   CK(cudaStreamSynchronize(st));
   memcpy(sc, scal_host, kNumScalars * sizeof(double));
   if (sc[SC_BAD] != 0.0) {
@@ -708,10 +770,17 @@ mdot_status Workspace::setup(const mdot_options& o) {
 mdot_status Workspace::gauge_center(double* X_, double* Y_) {
   const double* xs[2] = {r, c};
   const double* ys[2] = {X_, Y_};
-  // rows and columns have different lengths: two dot calls
+  // rows (possibly sharded) and columns (replicated) separately
   CKL(launch_dots(nrows, 1, &xs[0], &ys[0], blockpart, ticket, scal_dev, scal_host_dev, st));
-  CK(cudaStreamSynchronize(st));
-  const double a = scal_host[0];
+  double a = 0.0;
+  if (sharded()) {
+    CKS(comm_allreduce(comm, scal_dev, 1, COMM_SUM, st));
+    CK(cudaMemcpyAsync(&a, scal_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } else {
+    CK(cudaStreamSynchronize(st));
+    a = scal_host[0];
+  }
   CKL(launch_dots(n, 1, &xs[1], &ys[1], blockpart, ticket, scal_dev, scal_host_dev, st));
   CK(cudaStreamSynchronize(st));
   const double b = scal_host[0];
@@ -742,14 +811,33 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   a.colF1 = colm; a.colcost = cols; a.chunks = chunks;
   a.ec = ec; a.er = er; a.rowF2 = rowF2; a.rowcost2 = rowcost2; a.rowcorr = rowcorr;
   CKL(launch_round_cols(a, st));
+  if (sharded()) {
+    // column sums over this rank's rows -> global (one allreduce of 2n)
+    double* cs = aux + 6 * nrows + 2 * n;
+    CKL(launch_sum_chunks(colm, chunks, n, cs, st));
+    CKL(launch_sum_chunks(cols, chunks, n, cs + n, st));
+    CKS(comm_allreduce(comm, cs, 2 * (size_t)n, COMM_SUM, st));
+    a.colF1 = cs;
+    a.colcost = cs + n;
+    a.chunks = 1;
+  }
   CKL(launch_round_combine_cols(a, c, V, Bpp, ec, blockpart, ticket, scal_dev, scal_host_dev, st));
   CK(cudaStreamSynchronize(st));
   const double cF = scal_host[0];
   a.B = Bpp;
   CKL(launch_round_rows3(a, st));
   CKL(launch_round_combine_rows(a, r, blockpart, ticket, scal_dev, scal_host_dev, st));
-  CK(cudaStreamSynchronize(st));
-  const double ner = scal_host[0], cF2 = scal_host[1], corr = scal_host[2];
+  double ner, cF2, corr;
+  if (sharded()) {
+    CKS(comm_allreduce(comm, scal_dev, 4, COMM_SUM, st));
+    double h4[4];
+    CK(cudaMemcpyAsync(h4, scal_dev, sizeof(h4), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ner = h4[0]; cF2 = h4[1]; corr = h4[2];
+  } else {
+    CK(cudaStreamSynchronize(st));
+    ner = scal_host[0]; cF2 = scal_host[1]; corr = scal_host[2];
+  }
   if (cost_F) *cost_F = cF;
   if (cost_G) *cost_G = cF2 + (ner >= 1e-300 ? corr / ner : 0.0);
   if (P_out_dev) {
@@ -796,7 +884,8 @@ void mdot_schedule_default(mdot_schedule* s) {
 }
 
 static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt_in,
-                              double* u_out, double* v_out, float* P_out, mdot_result* res, int force_sinkhorn) {
+                              double* u_out, double* v_out, float* P_out, mdot_result* res, int force_sinkhorn,
+                              Comm* comm = nullptr, int64_t row0 = 0, int64_t nrows_in = -1) {
   g_last_error.clear();
   if (!res) { set_error("result pointer is NULL"); return MDOT_EINVAL; }
   memset(res, 0, sizeof(*res));
@@ -813,21 +902,26 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   if (st != MDOT_OK) { res->status = st; return st; }
   cudaStream_t stream = (cudaStream_t)o.stream;
   const int64_t n = pb->n;
+  const int64_t nr = nrows_in < 0 ? n : nrows_in;
+  if (row0 < 0 || nr < 1 || row0 + nr > n) { set_error("bad row range"); res->status = MDOT_EINVAL; return MDOT_EINVAL; }
+  if (comm && comm->nranks > 1) o.device_control = 0;   // sharded control runs on the host (one NCCL call per eval)
   Workspace w;
-  st = w.alloc(stream, n, n);
-  if (st == MDOT_OK) st = w.load_problem(pb, 0);
+  w.comm = comm;
+  w.row0 = row0;
+  st = w.alloc(stream, n, nr);
+  if (st == MDOT_OK) st = w.load_problem(pb, row0);
   if (st == MDOT_OK) st = w.setup(o);
   mdot_status solve_st = MDOT_OK;
   if (st == MDOT_OK) {
     // P0 = r c^T -> U = log r, V = log c ; u = v = 0 (Alg. 1 line 2)
     if (o.p0_ones) {
-      ++w.launches; launch_fill(n, 0.0, w.U, stream);
+      ++w.launches; launch_fill(nr, 0.0, w.U, stream);
       ++w.launches; launch_fill(n, 0.0, w.V, stream);
     } else {
-      cudaMemcpyAsync(w.U, w.logr, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
+      cudaMemcpyAsync(w.U, w.logr, sizeof(double) * nr, cudaMemcpyDeviceToDevice, stream);
       cudaMemcpyAsync(w.V, w.logc, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
     }
-    ++w.launches; launch_fill(n, 0.0, w.u, stream);
+    ++w.launches; launch_fill(nr, 0.0, w.u, stream);
     ++w.launches; launch_fill(n, 0.0, w.v, stream);
     double gb = 0.0, gprev = 0.0;
     for (size_t t = 1; t <= gam.size(); ++t) {
@@ -835,17 +929,17 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       gb += gt;
       w.set_gamma(gb);
       if (o.warm == MDOT_WARM_ZERO) {
-        ++w.launches; launch_fill(n, 0.0, w.u, stream);
+        ++w.launches; launch_fill(nr, 0.0, w.u, stream);
         ++w.launches; launch_fill(n, 0.0, w.v, stream);
       } else if (o.warm == MDOT_WARM_SCALED && t > 1 && gt != gprev) {
-        ++w.launches; launch_axpby(n, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
+        ++w.launches; launch_axpby(nr, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
         ++w.launches; launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
       }
       if (o.device_control) solve_st = project_device(w, o, (int)t, res);
       else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
       else solve_st = project_pncg(w, o, (int)t, res);
       res->md_steps = (int64_t)t;
-      ++w.launches; launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u
+      ++w.launches; launch_axpby(nr, 1.0, w.u, 1.0, w.U, stream);   // U += u
       ++w.launches; launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);   // V += v
       if (solve_st != MDOT_OK && solve_st != MDOT_ENOCONV) break;
       st = w.gauge_center(w.U, w.V);
@@ -860,17 +954,17 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       float* Pown = nullptr;
       if (P_out) {
         if (pb->mem == MDOT_MEM_DEVICE) Pdev = P_out;
-        else if (cudaMallocAsync((void**)&Pown, sizeof(float) * n * n, stream) == cudaSuccess) Pdev = Pown;
+        else if (cudaMallocAsync((void**)&Pown, sizeof(float) * nr * n, stream) == cudaSuccess) Pdev = Pown;
       }
       st = w.round_and_cost(Pdev, &res->cost_unrounded, &res->cost_rounded);
       if (st == MDOT_OK && Pown) {
-        if (cudaMemcpyAsync(P_out, Pown, sizeof(float) * n * n, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        if (cudaMemcpyAsync(P_out, Pown, sizeof(float) * nr * n, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
           st = MDOT_ECUDA;
       }
       if (Pown) cudaFreeAsync(Pown, stream);
     }
     const cudaMemcpyKind k = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (u_out) cudaMemcpyAsync(u_out, w.U, sizeof(double) * n, k, stream);
+    if (u_out) cudaMemcpyAsync(u_out, w.U, sizeof(double) * nr, k, stream);
     if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * n, k, stream);
   }
   res->evaluations = w.evals;
@@ -899,6 +993,15 @@ mdot_status mdot_solve(const mdot_problem* pb, const mdot_schedule* sched, const
 mdot_status mdot_sinkhorn(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
                           double* u_out, double* v_out, float* P_out, mdot_result* res) {
   return solve_impl(pb, sched, opt, u_out, v_out, P_out, res, 1);
+}
+
+mdot_status mdot_solve_sharded(mdot_comm* c, const mdot_problem* local_rows, int64_t row0, int64_t n_local,
+                               const mdot_schedule* sched, const mdot_options* opt, double* u_local_out,
+                               double* v_out, mdot_result* res) {
+  Comm* cm = reinterpret_cast<Comm*>(c);
+  if (!cm || !local_rows) { set_error("bad arguments"); return MDOT_EINVAL; }
+  if (cudaSetDevice(cm->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }
+  return solve_impl(local_rows, sched, opt, u_local_out, v_out, nullptr, res, 0, cm, row0, n_local);
 }
 
 mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,

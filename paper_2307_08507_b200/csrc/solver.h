@@ -20,8 +20,12 @@ struct Marg {           // marginals of one plan (rows then columns, [nrows + n]
   double* g = nullptr;  // gradient
 };
 
+struct Comm;
+
 struct Workspace {
   cudaStream_t st = nullptr;
+  Comm* comm = nullptr;
+  int64_t row0 = 0;
   int64_t n = 0, nrows = 0;
   // problem
   const void* Cdev = nullptr;
@@ -75,6 +79,7 @@ struct Workspace {
   cudaEvent_t gev[2 * 65] = {};
   bool gev_made = false;
 
+  bool sharded() const;
   mdot_status alloc(cudaStream_t stream, int64_t n, int64_t nrows);
   mdot_status launch_slot_body(cudaStream_t s, int slot, bool timed);
   mdot_status build_graph();

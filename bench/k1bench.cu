@@ -1,0 +1,477 @@
+// bench/k1bench.cu -- micro-benchmark of K1 (fused row+column marginal
+// evaluation) design variants on one B200, n x n fp32 C read once per launch.
+// Not part of the product library: a measurement harness to pick the K1
+// design (results summarised in profiles/).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
+//          -o build/k1bench bench/k1bench.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
+// the product kernels, timed as shipped
+#include "../paper_2307_08507_b200/csrc/eval_tma.cu"
+#include "../paper_2307_08507_b200/csrc/kernels.cu"
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e = (x);                                                                       \
+    if (e != cudaSuccess) {                                                                    \
+      fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);        \
+      exit(1);                                                                                 \
+    }                                                                                          \
+  } while (0)
+
+constexpr int kTileN = 256;
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float4 ldg_nc4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double shx(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ double wred4(double v0, double v1, double v2, double v3, int lane) {
+  const bool up = lane & 16;
+  double k0 = up ? v2 : v0, k1 = up ? v3 : v1;
+  double s0 = up ? v0 : v2, s1 = up ? v1 : v3;
+  k0 += shx(s0, 16);
+  k1 += shx(s1, 16);
+  const bool up2 = lane & 8;
+  double kk = up2 ? k1 : k0, ss = up2 ? k0 : k1;
+  kk += shx(ss, 8);
+  kk += shx(kk, 4);
+  kk += shx(kk, 2);
+  kk += shx(kk, 1);
+  return kk;
+}
+
+struct Args {
+  const float* C;
+  int64_t n;
+  int tile_m, nrt, nct;
+  const float4* rowp;
+  const float4* colp;
+  float gh, gl;
+  double* rowpart;
+  double* colpart;
+};
+
+// ---------------------------------------------------------------------------
+// LDG variant: full-tile fast path, incremental pointers, optional register
+// prefetch of the next 4-row step.  CTA = tile_m rows x 256 cols, 8 warps.
+// ---------------------------------------------------------------------------
+template <bool PREFETCH, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_ldg(Args a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j0 = (int64_t)blockIdx.x * kTileN;
+  const int64_t i0 = (int64_t)blockIdx.y * a.tile_m;
+  const int64_t n = a.n;
+  __shared__ double sred[8][kTileN];
+  float bh[8], bl[8], T[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 cp = a.colp[j0 + 4 * lane + (q & 3) + 128 * (q >> 2)];
+    bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+  }
+  const float gh = a.gh, gl = a.gl;
+  double c64[8];
+  float c32[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { c64[q] = 0.0; c32[q] = 0.f; }
+  const float* p = a.C + (i0 + 4 * warp) * n + j0 + 4 * lane;
+  const int64_t step = 32 * n;
+  const int nsteps = a.tile_m / 32;
+  float4 cur[4][2], nxt[4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) { cur[u][0] = ldg_nc4(p + u * n); cur[u][1] = ldg_nc4(p + u * n + 128); }
+  const float4* rp_ptr = a.rowp + i0 + 4 * warp;
+  for (int k = 0; k < nsteps; ++k) {
+    if (PREFETCH && k + 1 < nsteps) {
+      const float* q2 = p + (k + 1) * step;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { nxt[u][0] = ldg_nc4(q2 + u * n); nxt[u][1] = ldg_nc4(q2 + u * n + 128); }
+    }
+    float4 rp[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) rp[u] = __ldg(rp_ptr + 32 * k + u);
+    double rs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float cv[8] = {cur[u][0].x, cur[u][0].y, cur[u][0].z, cur[u][0].w,
+                           cur[u][1].x, cur[u][1].y, cur[u][1].z, cur[u][1].w};
+      float rsum = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float zh = fmaf(-gh, cv[q], rp[u].x + bh[q]);
+        const float tt = fmaf(-gl, cv[q], rp[u].y + bl[q]);
+        const float e = ex2f(zh + tt);
+        rsum = fmaf(e, T[q], rsum);
+        c32[q] = fmaf(e, rp[u].z, c32[q]);
+      }
+      rs[u] = rsum;
+    }
+    const double tot = wred4(rs[0], rs[1], rs[2], rs[3], lane);
+    const int64_t i = i0 + 32 * k + 4 * warp + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+    if ((lane & 7) == 0) a.rowpart[(int64_t)blockIdx.x * n + i] = tot;
+    if (k & 1) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { c64[q] += (double)c32[q]; c32[q] = 0.f; }
+    }
+    if (PREFETCH) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { cur[u][0] = nxt[u][0]; cur[u][1] = nxt[u][1]; }
+    } else if (k + 1 < nsteps) {
+      const float* q2 = p + (k + 1) * step;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { cur[u][0] = ldg_nc4(q2 + u * n); cur[u][1] = ldg_nc4(q2 + u * n + 128); }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c64[q] += (double)c32[q];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sred[warp][4 * lane + (q & 3) + 128 * (q >> 2)] = c64[q];
+  __syncthreads();
+  double acc = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) acc += sred[w][threadIdx.x];
+  a.colpart[(int64_t)blockIdx.y * n + j0 + threadIdx.x] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// TMA variant: persistent, producer warp, STAGES x ROWS-row boxes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mb_tx(unsigned long long* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@P1 bra DONE;\nbra "
+      "LAB_WAIT;\nDONE:\n}\n" ::"r"(su32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int x, int y, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)m), "r"(x), "r"(y), "r"(su32(b))
+      : "memory");
+}
+
+template <int ROWS, int STAGES>
+struct TSmem {
+  float st[STAGES][ROWS][kTileN];
+  double sred[8][kTileN];
+  unsigned long long full[STAGES], empty[STAGES];
+};
+
+template <int ROWS, int STAGES, int MINB>
+__global__ void __launch_bounds__(288, MINB) k_tma(const __grid_constant__ CUtensorMap tmap, Args a) {
+  extern __shared__ __align__(128) unsigned char raw[];
+  const uint32_t pad = (128u - (su32(raw) & 127u)) & 127u;
+  TSmem<ROWS, STAGES>& sm = *reinterpret_cast<TSmem<ROWS, STAGES>*>(raw + pad);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = a.n;
+  const int64_t total = (int64_t)a.nrt * a.nct;
+  const int spt = a.tile_m / ROWS;
+  constexpr int RPW = ROWS / 8;   // rows per warp per stage
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mb_init(&sm.full[s], 1); mb_init(&sm.empty[s], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int tr = (int)(t / a.nct), tc = (int)(t % a.nct);
+        for (int k = 0; k < spt; ++k, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+          mb_wait(&sm.empty[s], ph ^ 1u);
+          mb_tx(&sm.full[s], ROWS * kTileN * 4);
+          tma2d(&sm.st[s][0][0], &tmap, tc * kTileN, tr * a.tile_m + k * ROWS, &sm.full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const float gh = a.gh, gl = a.gl;
+  uint32_t it = 0;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const int tr = (int)(t / a.nct), tc = (int)(t % a.nct);
+    const int64_t i0 = (int64_t)tr * a.tile_m, j0 = (int64_t)tc * kTileN;
+    float bh[8], bl[8], T[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 cp = __ldg(&a.colp[j0 + 4 * lane + (q & 3) + 128 * (q >> 2)]);
+      bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+    }
+    double c64[8];
+    float c32[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { c64[q] = 0.0; c32[q] = 0.f; }
+    for (int k = 0; k < spt; ++k, ++it) {
+      const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+      const int64_t ib = i0 + (int64_t)k * ROWS + RPW * warp;
+      float4 rp[RPW];
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) rp[u] = __ldg(&a.rowp[ib + u]);
+      mb_wait(&sm.full[s], ph);
+      double rs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) {
+        const float* row = &sm.st[s][RPW * warp + u][0];
+        const float4 x0 = *reinterpret_cast<const float4*>(row + 4 * lane);
+        const float4 x1 = *reinterpret_cast<const float4*>(row + 128 + 4 * lane);
+        const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        float rsum = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float zh = fmaf(-gh, cv[q], rp[u].x + bh[q]);
+          const float tt = fmaf(-gl, cv[q], rp[u].y + bl[q]);
+          const float e = ex2f(zh + tt);
+          rsum = fmaf(e, T[q], rsum);
+          c32[q] = fmaf(e, rp[u].z, c32[q]);
+        }
+        rs[u & 3] = rsum;
+        if ((u & 3) == 3) {
+          const double tot = wred4(rs[0], rs[1], rs[2], rs[3], lane);
+          const int64_t i = ib + (u - 3) + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+          if ((lane & 7) == 0) a.rowpart[(int64_t)tc * n + i] = tot;
+        }
+      }
+      if (RPW < 4) {   // RPW == 2
+        const double tot = wred4(rs[0], rs[1], 0.0, 0.0, lane);
+        const int q = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+        if ((lane & 7) == 0 && q < RPW) a.rowpart[(int64_t)tc * n + ib + q] = tot;
+      }
+      __syncwarp();
+      if (lane == 0) mb_arrive(&sm.empty[s]);
+      if ((k * RPW) % 8 == 8 - RPW) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c64[q] += (double)c32[q]; c32[q] = 0.f; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c64[q] += (double)c32[q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sm.sred[warp][4 * lane + (q & 3) + 128 * (q >> 2)] = c64[q];
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) acc += sm.sred[w][threadIdx.x];
+    a.colpart[(int64_t)tr * n + j0 + threadIdx.x] = acc;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
+}
+
+// pure streaming read (ceiling reference): grid-stride float4 sum
+template <int UNR>
+__global__ void __launch_bounds__(256) k_read(const float* C, int64_t nn4, float* out) {
+  const float4* c4 = reinterpret_cast<const float4*>(C);
+  float acc = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (UNR - 1) * stride < nn4; i += UNR * stride) {
+    float4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) v[u] = ldg_nc4(reinterpret_cast<const float*>(c4 + i + u * stride));
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  for (; i < nn4; i += stride) { float4 v = c4[i]; acc += v.x + v.y + v.z + v.w; }
+  if (acc == 12345.f) out[0] = acc;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_init(float* C, int64_t nn) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)(i * 2654435761ull) ^ (uint32_t)(i >> 32);
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    C[i] = (float)(h & 0xffffff) * (1.0f / 16777216.0f);
+  }
+}
+__global__ void k_params(float4* p, int64_t n, float base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = make_float4(base + (float)(i % 97) * 0.25f, 1e-4f, 0.0078125f, 0.f);
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static float time_it(const char* name, int reps, double bytes, void (*fn)(void*), void* ctx) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int i = 0; i < 3; ++i) fn(ctx);
+  CK(cudaDeviceSynchronize());
+  std::vector<float> ts;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaEventRecord(e0));
+    fn(ctx);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    ts.push_back(ms);
+  }
+  CK(cudaGetLastError());
+  double s = 0;
+  float mn = 1e9;
+  for (float t : ts) { s += t; if (t < mn) mn = t; }
+  const double mean = s / ts.size();
+  printf("%-44s mean %8.1f us  min %8.1f us  %7.1f GB/s (mean)  %7.1f GB/s (min)\n", name, mean * 1e3, mn * 1e3,
+         bytes / (mean * 1e-3) / 1e9, bytes / (mn * 1e-3) / 1e9);
+  fflush(stdout);
+  return (float)mean;
+}
+
+struct Ctx {
+  Args a;
+  float* dummy;
+  CUtensorMap map16, map32;
+  int grid;
+  int smem;
+};
+
+struct ProdCtx {
+  mdot::EvalArgs e;
+  alignas(64) unsigned char map[128];
+  int grid;
+};
+static void run_prod_tma(void* c) {
+  ProdCtx* x = (ProdCtx*)c;
+  CK(mdot::launch_eval_tma(x->map, x->e, x->grid, 0));
+}
+static void run_prod_ldg(void* c) {
+  ProdCtx* x = (ProdCtx*)c;
+  CK(mdot::launch_eval_fast(x->e, 0, 0));
+}
+
+template <int UNR>
+static void run_read(void* c) {
+  Ctx* x = (Ctx*)c;
+  int sms;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  k_read<UNR><<<sms * 8, 256>>>(x->a.C, x->a.n * x->a.n / 4, x->dummy);
+}
+
+template <bool PF, int MINB>
+static void run_ldg(void* c) {
+  Ctx* x = (Ctx*)c;
+  dim3 g(x->a.nct, x->a.nrt);
+  k_ldg<PF, MINB><<<g, 256>>>(x->a);
+}
+template <int ROWS, int STAGES, int MINB>
+static void run_tma(void* c) {
+  Ctx* x = (Ctx*)c;
+  const int smem = (int)sizeof(TSmem<ROWS, STAGES>) + 128;
+  static bool set = false;
+  if (!set) { CK(cudaFuncSetAttribute(k_tma<ROWS, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); set = true; }
+  int sms;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  k_tma<ROWS, STAGES, MINB><<<MINB * sms, 288, smem>>>(ROWS == 16 ? x->map16 : x->map32, x->a);
+}
+
+int main(int argc, char** argv) {
+  const int64_t n = argc > 1 ? atoll(argv[1]) : 16384;
+  const int reps = argc > 2 ? atoi(argv[2]) : 20;
+  float* C;
+  float4 *rowp, *colp;
+  double *rowpart, *colpart;
+  CK(cudaMalloc(&C, sizeof(float) * n * n));
+  CK(cudaMalloc(&rowp, sizeof(float4) * n));
+  CK(cudaMalloc(&colp, sizeof(float4) * n));
+  CK(cudaMalloc(&rowpart, sizeof(double) * n * (n / 256 + 1)));
+  CK(cudaMalloc(&colpart, sizeof(double) * n * (n / 32 + 1)));
+  k_init<<<1184, 256>>>(C, n * n);
+  k_params<<<(unsigned)((n + 255) / 256), 256>>>(rowp, n, -3.0f);
+  k_params<<<(unsigned)((n + 255) / 256), 256>>>(colp, n, 0.0f);
+  CK(cudaDeviceSynchronize());
+  Ctx x{};
+  x.a.C = C; x.a.n = n; x.a.rowp = rowp; x.a.colp = colp; x.a.gh = 16.0f; x.a.gl = 1e-6f;
+  x.a.rowpart = rowpart; x.a.colpart = colpart;
+  x.a.nct = (int)(n / 256);
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q));
+  EncFn enc = (EncFn)p;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+  cuuint64_t str[1] = {(cuuint64_t)n * 4};
+  cuuint32_t es[2] = {1, 1};
+  cuuint32_t b16[2] = {256, 16}, b32[2] = {256, 32};
+  if (enc(&x.map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, str, b16, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ||
+      enc(&x.map32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, str, b32, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)) {
+    fprintf(stderr, "tensor map encode failed\n");
+    return 1;
+  }
+  const double bytes = 4.0 * n * n;
+  printf("n=%lld  bytes/launch=%.3f GB\n", (long long)n, bytes / 1e9);
+  CK(cudaMalloc(&x.dummy, 64));
+  {
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    for (int tm : {128, 256, 512}) {
+      ProdCtx pc{};
+      pc.e.C = C; pc.e.ldc = n; pc.e.n = n; pc.e.nrows = n; pc.e.tile_m = tm;
+      pc.e.n_col_tiles = (int)(n / 256); pc.e.n_row_tiles = (int)(n / tm);
+      pc.e.rowp = rowp; pc.e.colp = colp; pc.e.gh = 16.0f; pc.e.gl = 1e-6f;
+      pc.e.rowpart = rowpart; pc.e.colpart = colpart;
+      CK(mdot::make_tma_map(pc.e, pc.map));
+      pc.grid = (int)std::min<int64_t>((int64_t)pc.e.n_row_tiles * pc.e.n_col_tiles, 2 * sms);
+      char nm[128];
+      snprintf(nm, sizeof nm, "PRODUCT k_eval_tma tile_m=%d", tm);
+      time_it(nm, reps, bytes, run_prod_tma, &pc);
+      snprintf(nm, sizeof nm, "PRODUCT k_eval_fast tile_m=%d", tm);
+      time_it(nm, reps, bytes, run_prod_ldg, &pc);
+    }
+  }
+  time_it("read-only stream unroll4", reps, bytes, run_read<4>, &x);
+  time_it("read-only stream unroll8", reps, bytes, run_read<8>, &x);
+  for (int tm : {128, 256, 512}) {
+    x.a.tile_m = tm; x.a.nrt = (int)(n / tm);
+    char nm[128];
+    snprintf(nm, sizeof nm, "ldg nopf  minb2 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_ldg<false, 2>, &x);
+    snprintf(nm, sizeof nm, "ldg pf    minb1 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_ldg<true, 1>, &x);
+    snprintf(nm, sizeof nm, "ldg pf    minb2 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_ldg<true, 2>, &x);
+  }
+  for (int tm : {256, 512}) {
+    x.a.tile_m = tm; x.a.nrt = (int)(n / tm);
+    char nm[128];
+    snprintf(nm, sizeof nm, "tma 32x3 minb2 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<32, 3, 2>, &x);
+    snprintf(nm, sizeof nm, "tma 16x5 minb2 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<16, 5, 2>, &x);
+    snprintf(nm, sizeof nm, "tma 16x8 minb1 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<16, 8, 1>, &x);
+    snprintf(nm, sizeof nm, "tma 32x6 minb1 tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<32, 6, 1>, &x);
+  }
+  return 0;
+}

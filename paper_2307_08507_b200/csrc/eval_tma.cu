@@ -11,9 +11,9 @@
 //   * warps 0..7 = consumers: 4 rows x 8 columns per lane per stage, exponent
 //     assembly + ex2 + row/column accumulation exactly as k_eval_fast;
 //   * per tile, the column sums of the 8 warps are combined in smem and written
-//     as a per-row-tile partial; the CTA that finishes a row tile / column tile
-//     last (atomic ticket) adds that tile's partials in index order and writes
-//     the totals, so finalize reads 2n totals (deterministic, no float atomics).
+//     as a per-row-tile partial (rows: one partial per column tile); k_finalize
+//     adds the partials in index order (deterministic, no float atomics, no
+//     inter-CTA tickets on the streaming path).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -35,7 +35,6 @@ struct TmaSmem {
   double sred[kConsumerWarps][kTileN];          // 16 KiB
   unsigned long long full[kTmaStages];
   unsigned long long empty[kTmaStages];
-  int last_col, last_row;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -97,7 +96,7 @@ __device__ __forceinline__ double warp_reduce4_t(double v0, double v1, double v2
 }
 
 __global__ void __launch_bounds__(kTmaThreads, 2)
-    k_eval_tma(const __grid_constant__ CUtensorMap tmap, EvalArgs a, EvalTotals t) {
+    k_eval_tma(const __grid_constant__ CUtensorMap tmap, EvalArgs a) {
   if (a.done && *a.done) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
@@ -218,35 +217,6 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       const int64_t j = j0 + tt;
       if (j < n) a.colpart[(int64_t)tr * n + j] = acc;
     }
-    __threadfence();
-    consumer_bar();
-    if (threadIdx.x == 0) {
-      sm.last_col = (atomicAdd(&t.col_ticket[tc], 1u) == (unsigned)(a.n_row_tiles - 1));
-      sm.last_row = (atomicAdd(&t.row_ticket[tr], 1u) == (unsigned)(nct - 1));
-    }
-    consumer_bar();
-    const bool last_col = sm.last_col, last_row = sm.last_row;
-    if (last_col || last_row) __threadfence();
-    if (last_col) {
-      const int64_t j = j0 + threadIdx.x;
-      if (j < n) {
-        double acc = 0.0;
-        for (int q = 0; q < a.n_row_tiles; ++q) acc += __ldcg(&a.colpart[(int64_t)q * n + j]);
-        t.coltot[j] = acc;
-      }
-      if (threadIdx.x == 0) t.col_ticket[tc] = 0u;
-    }
-    if (last_row) {
-      for (int rr = threadIdx.x; rr < a.tile_m; rr += kConsumerWarps * 32) {
-        const int64_t i = i0 + rr;
-        if (i < nrows) {
-          double acc = 0.0;
-          for (int q = 0; q < nct; ++q) acc += __ldcg(&a.rowpart[(int64_t)q * nrows + i]);
-          t.rowtot[i] = acc;
-        }
-      }
-      if (threadIdx.x == 0) t.row_ticket[tr] = 0u;
-    }
     consumer_bar();   // sred / last flags reused by the next tile
   }
 }
@@ -287,7 +257,7 @@ cudaError_t make_tma_map(const EvalArgs& a, void* map_out /* CUtensorMap, 64 B a
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, const EvalTotals& t, int grid, cudaStream_t st) {
+cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, int grid, cudaStream_t st) {
   static bool attr = false;
   const int smem = (int)sizeof(TmaSmem) + 128;
   if (!attr) {
@@ -296,7 +266,7 @@ cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, const EvalTotals
     attr = true;
   }
   const CUtensorMap& m = *reinterpret_cast<const CUtensorMap*>(map);
-  k_eval_tma<<<grid, kTmaThreads, smem, st>>>(m, a, t);
+  k_eval_tma<<<grid, kTmaThreads, smem, st>>>(m, a);
   return cudaGetLastError();
 }
 

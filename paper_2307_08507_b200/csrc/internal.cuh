@@ -47,16 +47,9 @@ struct EvalArgs {
   double* colpart;         // [n_row_tiles][n]      sum_i 2^w S_i
 };
 
-// Totals written by the persistent TMA kernel (last-arriver reduction).
-struct EvalTotals {
-  double* rowtot;            // [nrows] sum_j 2^w T_j
-  double* coltot;            // [n]     sum_i 2^w S_i (local rows only when sharded)
-  unsigned int* row_ticket;  // [n_row_tiles], zero between launches
-  unsigned int* col_ticket;  // [n_col_tiles]
-};
 bool tma_supported(const EvalArgs& a);
 cudaError_t make_tma_map(const EvalArgs& a, void* map_out);
-cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, const EvalTotals& t, int grid, cudaStream_t st);
+cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, int grid, cudaStream_t st);
 int tma_smem_bytes();
 
 // Launch the fused evaluation over the (row tile x column tile) grid.
@@ -107,7 +100,8 @@ enum Scalar : int {
 struct FinalizeArgs {
   int64_t n;             // global n (columns)
   int64_t nrows;         // local rows
-  int from_partials;     // 2: totals rowtot/coltot; 1: reduce rowpart/colpart; 0: exact (lr, col (m,s) partials)
+  int from_partials;     // 2: totals rowtot/coltot; 1: reduce rowpart/colpart (rows) and colpart or coltot
+                         // (cols, coltot when non-null); 0: exact (lr, col (m,s) partials)
   const double* rowtot; const double* coltot;
   const double* rowpart; int n_col_tiles;
   const double* colpart; int n_row_tiles;

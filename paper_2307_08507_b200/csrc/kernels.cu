@@ -377,6 +377,21 @@ __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, uns
   }
 }
 
+// sum_{t < cnt} x[t * stride] in index order; loads issued 8 at a time
+__device__ __forceinline__ double sum_strided(const double* x, int64_t stride, int cnt) {
+  double acc = 0.0;
+  int t = 0;
+  for (; t + 8 <= cnt; t += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = x[(int64_t)(t + u) * stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
+  for (; t < cnt; ++t) acc += x[(int64_t)t * stride];
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // finalize: marginals, s, grad, scalars
 // ---------------------------------------------------------------------------
@@ -395,10 +410,11 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
       if (a.from_partials == 2) {
         tot = is_row ? a.rowtot[k] : a.coltot[k - a.nrows];
       } else if (is_row) {
-        for (int t = 0; t < a.n_col_tiles; ++t) tot += a.rowpart[(int64_t)t * a.nrows + k];
+        tot = sum_strided(a.rowpart + k, a.nrows, a.n_col_tiles);
+      } else if (a.coltot) {
+        tot = a.coltot[k - a.nrows];
       } else {
-        const int64_t j = k - a.nrows;
-        for (int t = 0; t < a.n_row_tiles; ++t) tot += a.colpart[(int64_t)t * a.n + j];
+        tot = sum_strided(a.colpart + (k - a.nrows), a.n, a.n_row_tiles);
       }
       const double anchor = is_row ? a.rho_r[k] : a.sig_c[k - a.nrows];
       lm = log(tot) + anchor * LN2_D;
@@ -768,9 +784,7 @@ cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, c
 __global__ void k_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  double acc = 0.0;
-  for (int t = 0; t < nt; ++t) acc += colpart[(int64_t)t * n + j];
-  coltot[j] = acc;
+  coltot[j] = sum_strided(colpart + j, n, nt);
 }
 cudaError_t launch_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot, cudaStream_t st) {
   k_reduce_colpart<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colpart, nt, n, coltot);

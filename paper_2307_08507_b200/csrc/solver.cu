@@ -84,8 +84,10 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   eval.n = n;
   eval.nrows = nrows;
   eval.n_col_tiles = (int)((n + kTileN - 1) / kTileN);
-  int tile_m = 256;
-  while (tile_m > 32 && (int64_t)eval.n_col_tiles * ((nrows + tile_m - 1) / tile_m) < 4 * 148) tile_m /= 2;
+  // 512-row tiles (fewer partials) while there are >= 2 tiles per CTA slot
+  // of the persistent kernel; smaller tiles for small n
+  int tile_m = 512;
+  while (tile_m > 32 && (int64_t)eval.n_col_tiles * ((nrows + tile_m - 1) / tile_m) < 2 * 148) tile_m /= 2;
   eval.tile_m = tile_m;
   eval.n_row_tiles = (int)((nrows + tile_m - 1) / tile_m);
   chunks = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, (4 * 148 + (n + 255) / 256 - 1) / ((n + 255) / 256)));
@@ -129,16 +131,13 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   rowpart = D + o_rowpart; colpart = D + o_colpart; colm = D + o_colm; cols = D + o_cols; lr_ex = D + o_lr;
   blockpart = D + o_blk; scal_dev = D + o_scal; aux = D + o_aux;
   ctrl = reinterpret_cast<CtrlState*>(D + o_ctrl);
-  tot.rowtot = D + o_tot;
-  tot.coltot = D + o_tot + nrows;
+  tot.coltot = D + o_tot;   // sharded: [column totals | row scalars] allreduce buffer
   float4* F4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(base) + dbl * sizeof(double));
   F4 = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(F4) + 15) & ~uintptr_t(15));
   rowp = F4;
   colp = F4 + nrows;
   ticket_flag = reinterpret_cast<unsigned int*>(colp + n + 8);
   CK(cudaMemsetAsync(ticket_flag, 0, 64 + tickets * 4, st));
-  tot.row_ticket = ticket_flag + 16;
-  tot.col_ticket = tot.row_ticket + eval.n_row_tiles;
   ticket = ticket_flag;
   flag = reinterpret_cast<int*>(ticket_flag + 4);
   CK(cudaHostAlloc(&scal_host, 256 * sizeof(double), cudaHostAllocMapped));
@@ -190,42 +189,29 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   if (!exact_mode) {
     if (time_kernels) CK(cudaEventRecord(ev0, st));
     if (use_tma) {
-      CKL(launch_eval_tma(tmap, eval, tot, tma_grid, st));
+      CKL(launch_eval_tma(tmap, eval, tma_grid, st));
     } else {
       CKL(launch_eval_fast(eval, kind_fast, st));
     }
     if (time_kernels) CK(cudaEventRecord(ev1, st));
+    f.from_partials = 1;
+    f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
+    f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
     if (!shard) {
-      if (use_tma) {
-        f.from_partials = 2;
-        f.rowtot = tot.rowtot;
-        f.coltot = tot.coltot;
-      } else {
-        f.from_partials = 1;
-        f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
-        f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
-      }
       CKL(launch_finalize(f, st));
     } else {
       // rows are complete locally; columns are partial over this rank's rows.
       // Row scalars go into the tail of the column buffer so ONE allreduce
       // carries [column totals | row scalars].
       double* colbuf = tot.coltot;
-      if (use_tma) {
-        f.from_partials = 2;
-        f.rowtot = tot.rowtot;
-      } else {
-        f.from_partials = 1;
-        f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
-        CKL(launch_reduce_colpart(colpart, eval.n_row_tiles, n, colbuf, st));
-      }
+      CKL(launch_reduce_colpart(colpart, eval.n_row_tiles, n, colbuf, st));
       FinalizeArgs fr = f;
       fr.item_begin = 0; fr.item_end = nrows;
       fr.scalars_dev = colbuf + n; fr.scalars_host = nullptr;
       CKL(launch_finalize(fr, st));
       CKS(comm_allreduce(comm, colbuf, (size_t)n + kNumScalars, COMM_SUM, st));
       FinalizeArgs fc = f;
-      fc.from_partials = 2;
+      fc.from_partials = 1;
       fc.coltot = colbuf;
       fc.item_begin = nrows; fc.item_end = nrows + n;
       fc.add_in = colbuf + n;
@@ -465,16 +451,13 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed) {
     e.gpair = ctrl->gpair;
     e.done = &ctrl->done;
     if (use_tma) {
-      CKL(launch_eval_tma(tmap, e, tot, tma_grid, s));
-      f.from_partials = 2;
-      f.rowtot = tot.rowtot;
-      f.coltot = tot.coltot;
+      CKL(launch_eval_tma(tmap, e, tma_grid, s));
     } else {
       CKL(launch_eval_fast(e, kind_fast, s));
-      f.from_partials = 1;
-      f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
-      f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
     }
+    f.from_partials = 1;
+    f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
+    f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
   } else {
     ExactArgs x{};
     x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;

@@ -57,7 +57,7 @@ struct Workspace {
   double* scal_host_dev = nullptr;  // its device alias
   int chunks = 1;
   EvalArgs eval{};
-  EvalTotals tot{};
+  struct { double* coltot = nullptr; } tot;
   alignas(64) unsigned char tmap[128];
   bool use_tma = false;
   int tma_grid = 0;

@@ -270,6 +270,11 @@ cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, int grid, cudaSt
   return cudaGetLastError();
 }
 
+void set_smem_carveout_tma() {
+  cudaFuncSetAttribute(k_eval_tma, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+}
+
 int tma_smem_bytes() { return (int)sizeof(TmaSmem) + 128; }
 
 }  // namespace mdot

@@ -157,6 +157,10 @@ struct CtrlState {
   double sc[kNumScalars];
 };
 cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, cudaStream_t s);
+// Prefer the maximum shared-memory carveout for every kernel of the solve loop
+// (one L1/smem configuration for the whole loop, no reconfiguration between
+// the TMA kernel and the O(n) kernels).
+void set_smem_carveout();
 
 enum PrepMode : int {
   PREP_CUR = 0,         // A = U + u, B = V + v -> params

@@ -395,27 +395,48 @@ __device__ __forceinline__ double sum_strided(const double* x, int64_t stride, i
 // ---------------------------------------------------------------------------
 // finalize: marginals, s, grad, scalars
 // ---------------------------------------------------------------------------
+// 8 threads per item: the partial sums are split over the octet (t = lane%8,
+// t+8, ...) in a fixed order and combined by a fixed shuffle tree, so every
+// partial load of an item is in flight at once.
+constexpr int kFinTPI = 8;
+__device__ __forceinline__ double octet_partial(const double* x, int64_t stride, int cnt, int sub) {
+  double acc = 0.0;
+  int t = sub;
+  for (; t + 3 * kFinTPI < cnt; t += 4 * kFinTPI) {
+    const double v0 = x[(int64_t)t * stride], v1 = x[(int64_t)(t + kFinTPI) * stride];
+    const double v2 = x[(int64_t)(t + 2 * kFinTPI) * stride], v3 = x[(int64_t)(t + 3 * kFinTPI) * stride];
+    acc += v0; acc += v1; acc += v2; acc += v3;
+  }
+  for (; t < cnt; t += kFinTPI) acc += x[(int64_t)t * stride];
+  return acc;
+}
+
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   if (a.done && *a.done) return;
-  const int64_t k = a.item_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x & (kFinTPI - 1);
+  const int64_t k = a.item_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kFinTPI;
   const int64_t tot_items = a.item_end > 0 ? a.item_end : a.nrows + a.n;
+  const bool in_range = k < tot_items;
+  const bool is_row = k < a.nrows;
   double v[kNumScalars];
 #pragma unroll
   for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
-  if (k < tot_items) {
-    const bool is_row = k < a.nrows;
+  double tot = 0.0;
+  if (a.from_partials == 1) {   // octet-parallel partial sums; the shuffles run on the whole warp
+    double x = 0.0;
+    if (in_range) {
+      if (is_row) x = octet_partial(a.rowpart + k, a.nrows, a.n_col_tiles, sub);
+      else if (a.coltot) x = (sub == 0) ? a.coltot[k - a.nrows] : 0.0;   // already reduced (sharded)
+      else x = octet_partial(a.colpart + (k - a.nrows), a.n, a.n_row_tiles, sub);
+    }
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    tot = x;
+  }
+  if (in_range && sub == 0) {
     double lm, bad = 0.0;
-    if (a.from_partials) {
-      double tot = 0.0;
-      if (a.from_partials == 2) {
-        tot = is_row ? a.rowtot[k] : a.coltot[k - a.nrows];
-      } else if (is_row) {
-        tot = sum_strided(a.rowpart + k, a.nrows, a.n_col_tiles);
-      } else if (a.coltot) {
-        tot = a.coltot[k - a.nrows];
-      } else {
-        tot = sum_strided(a.colpart + (k - a.nrows), a.n, a.n_row_tiles);
-      }
+    if (a.from_partials == 1) {
       const double anchor = is_row ? a.rho_r[k] : a.sig_c[k - a.nrows];
       lm = log(tot) + anchor * LN2_D;
       // fp32 entry range guard (K1 numerics): totals far from 1 in
@@ -455,17 +476,17 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
     v[SC_GCG] = gc * g;
     v[SC_BAD] = bad;
     v[SC_L1R] = is_row ? fabs(g) : 0.0;
-  }
-  if (a.prep_flag && k == a.item_begin) {
-    v[SC_BAD] += (double)(*a.prep_flag);
-    *a.prep_flag = 0;
+    if (a.prep_flag && k == a.item_begin) {
+      v[SC_BAD] += (double)(*a.prep_flag);
+      *a.prep_flag = 0;
+    }
   }
   block_reduce_and_publish<kNumScalars>(v, a.blockpart, a.ticket, a.scalars_dev, a.scalars_host, a.add_in);
 }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
   const int64_t items = (a.item_end > 0 ? a.item_end : a.nrows + a.n) - a.item_begin;
-  const unsigned blocks = (unsigned)((items + 255) / 256);
+  const unsigned blocks = (unsigned)((items * kFinTPI + 255) / 256);
   k_finalize<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
@@ -587,8 +608,25 @@ __device__ void ctrl_start_iteration(CtrlState* st) {
   st->mode = PREP_NEWDIR | PREP_TRIAL;
 }
 
-__global__ void k_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host) {
-  if (threadIdx.x != 0) return;
+__device__ void k_ctrl_body(CtrlState* st, int slot, int* done_host, int* ran_host);
+
+// One warp copies the ~0.7 KB state to shared memory (coalesced), lane 0 runs
+// the control logic on the shared copy, the warp writes it back: two L2 round
+// trips instead of one per field.
+__global__ void k_ctrl(CtrlState* gst, int slot, int* done_host, int* ran_host) {
+  __shared__ CtrlState sst;
+  constexpr int kWords = (int)(sizeof(CtrlState) / sizeof(unsigned long long));
+  static_assert(sizeof(CtrlState) % sizeof(unsigned long long) == 0, "CtrlState size");
+  unsigned long long* g = reinterpret_cast<unsigned long long*>(gst);
+  unsigned long long* sh = reinterpret_cast<unsigned long long*>(&sst);
+  for (int i = threadIdx.x; i < kWords; i += 32) sh[i] = g[i];
+  __syncwarp();
+  if (threadIdx.x == 0) k_ctrl_body(&sst, slot, done_host, ran_host);
+  __syncwarp();
+  for (int i = threadIdx.x; i < kWords; i += 32) g[i] = sh[i];
+}
+
+__device__ void k_ctrl_body(CtrlState* st, int slot, int* done_host, int* ran_host) {
   if (st->done) { if (ran_host) ran_host[slot] = 0; return; }
   st->accept_marg = 0;
   st->accept_pot = 0;
@@ -676,6 +714,21 @@ __global__ void k_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host) {
     st->mode = PREP_TRIAL;
   }
   if (ran_host) ran_host[slot] = 1;
+}
+
+void set_smem_carveout_tma();
+void set_smem_carveout() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const int c = cudaSharedmemCarveoutMaxShared;
+  cudaFuncSetAttribute(k_ctrl, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_prep, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_finalize, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_eval_fast<0, true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_eval_fast<0, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_eval_fast<1, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  set_smem_carveout_tma();
 }
 
 cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, cudaStream_t s) {

@@ -733,6 +733,7 @@ void Workspace::free_owned() {
 }
 
 mdot_status Workspace::setup(const mdot_options& o) {
+  set_smem_carveout();
   time_kernels = o.time_kernels;
   if (time_kernels) {
     CK(cudaEventCreate(&ev0));

@@ -340,7 +340,12 @@ cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st) {
 template <int NS>
 __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, unsigned int* ticket,
                                          double* out_dev, double* out_host, const double* add_in = nullptr) {
+  // fixed-order reduction: warp shuffle tree -> per-warp smem -> per-block
+  // partial; the last block (ticket) combines all block partials with every
+  // thread loading a fixed strided subset and a fixed smem tree (no serial
+  // chain of loads, deterministic for a given grid).
   __shared__ double sm[32][NS];
+  __shared__ double sfin[256];
   __shared__ bool is_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
@@ -356,25 +361,33 @@ __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, uns
     for (int w = 0; w < nw; ++w) x += sm[w][threadIdx.x];
     blockpart[(int64_t)blockIdx.x * NS + threadIdx.x] = x;
   }
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned int t = atomicAdd(ticket, 1u);
     is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (is_last) {
-    __threadfence();
-    if (threadIdx.x < NS) {
-      double x = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b)
-        x += *((volatile double*)&blockpart[(int64_t)b * NS + threadIdx.x]);
-      if (add_in) x += add_in[threadIdx.x];
-      out_dev[threadIdx.x] = x;
-      if (out_host) out_host[threadIdx.x] = x;
-    }
-    if (threadIdx.x == 0) *ticket = 0u;
+  if (!is_last) return;
+  __threadfence();
+  // thread t: scalar k = t % NS, blocks b = t / NS, t / NS + G, ... (G = 256 / NS groups)
+  constexpr int G = 256 / NS;
+  const int t = threadIdx.x;
+  double x = 0.0;
+  if (t < G * NS) {
+    const int k = t % NS;
+    for (unsigned b = t / NS; b < gridDim.x; b += G) x += __ldcg(&blockpart[(int64_t)b * NS + k]);
   }
+  if (t < 256) sfin[t] = x;
+  __syncthreads();
+  if (t < NS) {
+    double y = 0.0;
+    for (int g = 0; g < G; ++g) y += sfin[g * NS + t];
+    if (add_in) y += add_in[t];
+    out_dev[t] = y;
+    if (out_host) out_host[t] = y;
+  }
+  if (t == 0) *ticket = 0u;
 }
 
 // sum_{t < cnt} x[t * stride] in index order; loads issued 8 at a time

@@ -279,3 +279,100 @@ def test_device_control_fp64_config1():
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_doubling(4096.0), O.make_options(eps=1e-6))
     assert res["status"] == 0
     assert abs(res["cost_unrounded"] - ores["cost_unrounded"]) <= 1e-5 * ores["cost_unrounded"]
+
+
+# ------------------------------------------------------------- on-the-fly cost (K2)
+@pytest.mark.parametrize("n,d", [(300, 16), (1024, 16), (777, 3)])
+def test_otf_marginals_match_oracle(n, d):
+    """Config-5 kernel: C computed in-kernel with the Z22 fp32 recipe, the
+    oracle computes the same recipe in C (-ffp-contract=off)."""
+    inst = S.config5(0, n=n, d=d)
+    prob = O.OracleProblem(inst)
+    gb = 512.0
+    A, B = _sinkhorn_potentials(prob, inst, gb, iters=3, noise=0.02)
+    lr_o, lc_o, _ = O.log_marginals(prob, A, B, gb)
+    lr, lc, fb = M.mdot_marginals(_t(A), _t(B), gb, X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale,
+                                  r=_t(inst.r), c=_t(inst.c))
+    assert fb == 0
+    err_r = np.max(np.abs(np.expm1(lr.cpu().numpy() - lr_o)))
+    err_c = np.max(np.abs(np.expm1(lc.cpu().numpy() - lc_o)))
+    assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
+
+
+def test_otf_solve_matches_oracle():
+    n = 512
+    inst = S.config5(1, n=n, d=16)
+    prob = O.OracleProblem(inst)
+    eps = 1e-5   # config 5 target
+    gb = 1024.0
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c),
+                       schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=4), options=M.options(eps=eps),
+                       u_out=U, v_out=V)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=4), O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+# ------------------------------------------------------------- sharded path
+def _sharded_solve_threads(inst, G, sched, opts_kw, group):
+    """G virtual ranks = G threads of this process, each with its own stream,
+    row-sharded C, in-process transport (no device-side waiting between
+    ranks: the allreduce is a host barrier)."""
+    import threading
+    n = inst.n
+    rows = np.array_split(np.arange(n), G)
+    out = [None] * G
+    err = [None] * G
+
+    def run(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                row0, nloc = int(rows[k][0]), len(rows[k])
+                C = _t(np.ascontiguousarray(inst.C[row0:row0 + nloc]))
+                r, c = _t(inst.r), _t(inst.c)
+                U = torch.empty(nloc, dtype=torch.float64, device=DEV)
+                V = torch.empty(n, dtype=torch.float64, device=DEV)
+                comm = M.mdot_comm_create_local(group, G, k, 0)
+                res = M.mdot_solve_sharded(comm, row0, nloc, C, r, c, n=n, schedule=sched,
+                                           options=M.options(**opts_kw), u_local_out=U, v_out=V)
+                s.synchronize()
+                M.mdot_comm_destroy(comm)
+                out[k] = (res, U.cpu().numpy(), V.cpu().numpy())
+        except Exception as e:  # noqa: BLE001
+            err[k] = e
+
+    ths = [threading.Thread(target=run, args=(k,)) for k in range(G)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_virtual_ranks_match_single_gpu(G):
+    n = 600
+    inst = S.uniform_points_instance(3, n, 2, 10, marg="dirichlet")
+    sched = M.schedule(M.MDOT_SCHED_FIXED, 512.0, T=2)
+    eps = 1e-6
+    ref = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(eps=eps))
+    out = _sharded_solve_threads(inst, G, sched, {"eps": eps}, f"grp{G}")
+    costs = [o[0]["cost_unrounded"] for o in out]
+    # every rank took identical decisions: identical scalars and V
+    assert all(o[0]["evaluations"] == out[0][0]["evaluations"] for o in out)
+    assert all(c == costs[0] for c in costs)
+    assert all(np.array_equal(o[2], out[0][2]) for o in out)
+    assert out[0][0]["l1_final"] <= eps
+    assert abs(costs[0] - ref["cost_unrounded"]) <= 2e-6 * ref["cost_unrounded"]
+    # oracle re-evaluation of the assembled potentials
+    U = np.concatenate([o[1] for o in out])
+    V = out[0][2]
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, U, V, 512.0)
+    l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
+    assert l1 <= 2 * eps

@@ -1,0 +1,92 @@
+"""World-size-2 gloo test (CPU) of the row-sharding decomposition the CUDA
+sharded path uses: each rank owns a row block, row
+marginals stay local, column partial sums and the row-side scalars travel in
+ONE packed allreduce [column partials | row scalars], column-side scalars are
+computed redundantly on every rank.  The packed result must equal the
+unsharded oracle evaluation."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import synthetic as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    inst = S.uniform_points_instance(3, 97, 2, 11, marg="dirichlet")
+    n = inst.n
+    rng = np.random.default_rng(0)
+    A = np.log(inst.r) + 0.1 * rng.standard_normal(n)
+    B = np.log(inst.c) + 0.1 * rng.standard_normal(n)
+    p = rng.standard_normal(2 * n)
+    g = 30.0
+    rows = np.array_split(np.arange(n), world)[rank]
+    row0, nloc = rows[0], len(rows)
+    # this rank's row block, direct fp64 evaluation
+    Cl = inst.C[row0:row0 + nloc].astype(np.float64)
+    P = np.exp(A[row0:row0 + nloc, None] + B[None, :] - g * Cl)
+    rP_loc = P.sum(1)
+    col_partial = P.sum(0)
+    row_scalars = np.array([rP_loc.sum(), np.abs(rP_loc - inst.r[rows]).sum(),
+                            (p[:n][rows] * (rP_loc - inst.r[rows])).sum(), float(nloc)])
+    buf = torch.from_numpy(np.concatenate([col_partial, row_scalars]))
+    dist.all_reduce(buf)   # the one packed collective per evaluation
+    buf = buf.numpy()
+    cP = buf[:n]
+    rs = buf[n:]
+    col_scalars = np.array([0.0, np.abs(cP - inst.c).sum(), (p[n:] * (cP - inst.c)).sum(), 0.0])
+    tot = rs + col_scalars
+    if rank == 0:
+        prob = O.OracleProblem(inst)
+        lr, lc, _ = O.log_marginals(prob, A, B, g)
+        rr, cc = np.exp(lr), np.exp(lc)
+        ref = np.array([rr.sum(), np.abs(rr - inst.r).sum() + np.abs(cc - inst.c).sum(),
+                        (p[:n] * (rr - inst.r)).sum() + (p[n:] * (cc - inst.c)).sum(), float(n)])
+        q.put((tot.tolist(), ref.tolist(), float(np.abs(cP - cc).max())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_packed_allreduce_decomposition(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    tot, ref, dcol = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    np.testing.assert_allclose(tot, ref, rtol=1e-12, atol=1e-15)
+    assert dcol < 1e-15
+
+
+def test_row_partition_covers_rows_once():
+    """The partition bench.py and the tests use (np.array_split): contiguous,
+    disjoint, covering, sizes differ by at most one."""
+    for n in (1, 7, 97, 16384, 65536):
+        for G in (1, 2, 3, 4, 8):
+            parts = np.array_split(np.arange(n), G)
+            cat = np.concatenate(parts)
+            assert np.array_equal(cat, np.arange(n))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1

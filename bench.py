@@ -12,10 +12,12 @@ rounding + cost) with inputs resident in HBM.
 value       = marginal evaluations / s over the timed steps (every O(n^2) pass
               of the solve counts; the same unit as the oracle's cpu_baseline)
 ms_per_step = time-to-eps (ms), device-timed with CUDA events, max over ranks
-roofline    = the fused marginal kernel (k_eval_fast): algorithmic bytes 4 n^2
-              (C read once) per launch / mean launch time (CUDA events around
-              every launch inside the library, on its stream), vs the measured
-              HBM copy bandwidth in MEASURED_PEAKS.json
+roofline    = the fused marginal kernel K1 (k_eval_tma): algorithmic bytes
+              4 n^2 (C read once) per launch / mean launch time (CUDA events
+              around K1 on the library's stream, sampled on the first slot of
+              every device-control graph in the timed region), vs the
+              measured HBM copy bandwidth in MEASURED_PEAKS.json; traffic =
+              dram read+write bytes per launch from profiles/k1_traffic.json
 e2e         = the same metric through the C ABI with HOST buffers (pinned C,
               r, c in; U, V out), copies inside the timed region
 cpu_baseline= the fp64 oracle (oracle/), as it stands, on a bounded sample of
@@ -75,8 +77,8 @@ def measured_peaks():
 
 
 def profile_traffic():
-    """dram bytes per launch of k_eval_fast from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "k_eval_fast_traffic.json")
+    """dram bytes per launch of K1 from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(p):
         try:
             return json.load(open(p)).get("bytes_per_launch")
@@ -295,12 +297,15 @@ def run_ours(a, rank, world, local_rank):
         "solve": {k: results[-1][k] for k in ("cost_rounded", "cost_unrounded", "l1_final", "iterations",
                                               "evaluations", "ls_evaluations", "fallbacks", "md_steps",
                                               "status_name")},
-        "roofline": {"kernel": "k_eval_fast", "bound": "hbm", "achieved": achieved, "peak": hbm,
+        "roofline": {"kernel": "k_eval_tma (K1: fused row+column marginal evaluation)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
                      "traffic": traffic, "peak_source": peak_kind,
-                     "bytes_per_launch": bytes_per_launch, "launches": kern_n,
+                     "bytes_per_launch": bytes_per_launch, "launches_timed": kern_n,
+                     "timing": "CUDA events around K1 on the library stream, first slot of every "
+                               "device-control graph (sampled), timed region only",
                      "mean_launch_us": mean_launch_s * 1e6,
-                     "kernel_share_of_step": (kern_ms / ms) if ms else None},
+                     "kernel_share_of_step": (mean_launch_s * evals / (ms / 1000.0)) if kern_n else None},
         "clocks": clocks,
         "gpu_launches": launches,
     }

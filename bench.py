@@ -270,6 +270,11 @@ def run_ours(a, rank, world, local_rank):
     kern_ms = sum(x["kernel_ms"] for x in results)
     kern_n = sum(x["kernel_launches"] for x in results)
     launches = sum(x.get("all_launches", 0) for x in results)
+    nsamp = sum(x.get("stage_samples", 0) for x in results)
+    stages = None
+    if nsamp:
+        names = ["ctrl", "prep", "k1", "finalize"]
+        stages = {nm: 1000.0 * sum(x["stage_ms"][q] for x in results) / nsamp for q, nm in enumerate(names)}
     value = evals / (ms / 1000.0)
     ms_step = ms / a.steps
     hbm, peak_kind = measured_peaks()
@@ -308,6 +313,7 @@ def run_ours(a, rank, world, local_rank):
                      "kernel_share_of_step": (mean_launch_s * evals / (ms / 1000.0)) if kern_n else None},
         "clocks": clocks,
         "gpu_launches": launches,
+        "slot_stage_us": stages,
     }
     # end-to-end through the C ABI with host buffers (rank 0, 1 GPU)
     if world == 1 and not a.no_e2e:

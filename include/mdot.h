@@ -119,6 +119,8 @@ typedef struct {
   int64_t fallbacks;       /* evaluations redone on the exact fp64 evaluator */
   int64_t kernel_launches; /* evaluation kernels timed */
   int64_t all_launches;    /* every kernel this library launched during the call */
+  double stage_ms[4];      /* time_kernels: sampled per-slot durations [ctrl, prep, K1, finalize] (sums) */
+  int64_t stage_samples;   /* number of sampled slots in stage_ms */
   int32_t status;
   int32_t reserved;
   double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */

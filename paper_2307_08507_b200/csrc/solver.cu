@@ -423,7 +423,17 @@ static int* dev_alias(int* h) {
   return reinterpret_cast<int*>(d);
 }
 
-mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed) {
+mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bool with_ctrl) {
+  // timed slot events: gev[0] ctrl gev[1] prep gev[2] K1 gev[3] finalize gev[4]
+  if (timed) CK(cudaEventRecordWithFlags(gev[0], s, cudaEventRecordExternal));
+  if (with_ctrl) {
+    int* dh = nullptr;
+    int* rh = nullptr;
+    cudaHostGetDevicePointer((void**)&dh, done_host, 0);
+    cudaHostGetDevicePointer((void**)&rh, ran_host, 0);
+    CKL(launch_ctrl(ctrl, slot, dh, rh, s));
+  }
+  if (timed) CK(cudaEventRecordWithFlags(gev[1], s, cudaEventRecordExternal));
   PrepArgs a{};
   a.n = n; a.nrows = nrows; a.mode = 0;
   a.U = U; a.V = V; a.u = u; a.v = v; a.tu = tu; a.tv = tv;
@@ -445,7 +455,7 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed) {
   f.scalars_dev = ctrl->sc; f.scalars_host = nullptr;
   f.prep_flag = flag;
   f.done = &ctrl->done;
-  if (timed) CK(cudaEventRecordWithFlags(gev[2 * slot], s, cudaEventRecordExternal));
+  if (timed) CK(cudaEventRecordWithFlags(gev[2], s, cudaEventRecordExternal));
   if (!exact_mode) {
     EvalArgs e = eval;
     e.gpair = ctrl->gpair;
@@ -471,8 +481,9 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed) {
     f.from_partials = 0;
     f.lr_in = lr_ex; f.colm = colm; f.cols = cols; f.chunks = chunks;
   }
-  if (timed) CK(cudaEventRecordWithFlags(gev[2 * slot + 1], s, cudaEventRecordExternal));
+  if (timed) CK(cudaEventRecordWithFlags(gev[3], s, cudaEventRecordExternal));
   CKL(launch_finalize(f, s));
+  if (timed) CK(cudaEventRecordWithFlags(gev[4], s, cudaEventRecordExternal));
   return MDOT_OK;
 }
 
@@ -494,13 +505,13 @@ mdot_status Workspace::build_graph() {
   CK(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t saved = launches;
   mdot_status stt = MDOT_OK;
+  (void)dh;
+  (void)rh;
   for (int k = 0; k < gslots && stt == MDOT_OK; ++k) {
-    cudaError_t e = launch_ctrl(ctrl, k, dh, rh, cap_stream);
-    if (e != cudaSuccess) { set_error("capture ctrl: %s", cudaGetErrorString(e)); stt = MDOT_ECUDA; break; }
-    // K1 duration is sampled with CUDA events on the first slot of each
-    // graph only: event nodes between every kernel cost far more than they
+    // stage durations are sampled with CUDA events on the first slot of each
+    // graph only: event nodes between every kernel cost more than they
     // measure (the launch gaps they insert)
-    stt = launch_slot_body(cap_stream, k, k == 0);
+    stt = launch_slot_body(cap_stream, k, time_kernels && k == 0, true);
   }
   launches = saved;
   cudaGraph_t g = nullptr;
@@ -550,8 +561,11 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
         w.kernel_launches++;
       }
       if (((volatile int*)w.ran_host)[0]) {
-        CK(cudaEventElapsedTime(&ms, w.gev[0], w.gev[1]));
-        w.kernel_ms += ms;
+        float st4[4];
+        for (int q = 0; q < 4; ++q) CK(cudaEventElapsedTime(&st4[q], w.gev[q], w.gev[q + 1]));
+        for (int q = 0; q < 4; ++q) w.stage_ms[q] += st4[q];
+        w.stage_samples++;
+        w.kernel_ms += st4[2];
         w.kernel_launches++;
       }
     }
@@ -957,6 +971,8 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   res->kernel_ms = w.kernel_ms;
   res->kernel_launches = w.kernel_launches;
   res->all_launches = w.launches;
+  for (int q = 0; q < 4; ++q) res->stage_ms[q] = w.stage_ms[q];
+  res->stage_samples = w.stage_samples;
   w.free_owned();
   w.release();
   cudaError_t ce = cudaStreamSynchronize(stream);

@@ -64,6 +64,8 @@ struct Workspace {
   // stats
   int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;
   double kernel_ms = 0.0;
+  double stage_ms[4] = {0, 0, 0, 0};
+  int64_t stage_samples = 0;
   double last_mass = 1.0;
   int time_kernels = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -81,7 +83,7 @@ struct Workspace {
 
   bool sharded() const;
   mdot_status alloc(cudaStream_t stream, int64_t n, int64_t nrows);
-  mdot_status launch_slot_body(cudaStream_t s, int slot, bool timed);
+  mdot_status launch_slot_body(cudaStream_t s, int slot, bool timed, bool with_ctrl = false);
   mdot_status build_graph();
   void release();
   mdot_status load_problem(const mdot_problem* pb, int64_t row0);

@@ -376,7 +376,15 @@ __device__ void block_reduce_and_publish(double (&v)[NS], double* blockpart, uns
   double x = 0.0;
   if (t < G * NS) {
     const int k = t % NS;
-    for (unsigned b = t / NS; b < gridDim.x; b += G) x += __ldcg(&blockpart[(int64_t)b * NS + k]);
+    unsigned b = t / NS;
+    for (; b + 3 * G < gridDim.x; b += 4 * G) {
+      const double y0 = __ldcg(&blockpart[(int64_t)b * NS + k]);
+      const double y1 = __ldcg(&blockpart[(int64_t)(b + G) * NS + k]);
+      const double y2 = __ldcg(&blockpart[(int64_t)(b + 2 * G) * NS + k]);
+      const double y3 = __ldcg(&blockpart[(int64_t)(b + 3 * G) * NS + k]);
+      x += y0; x += y1; x += y2; x += y3;
+    }
+    for (; b < gridDim.x; b += G) x += __ldcg(&blockpart[(int64_t)b * NS + k]);
   }
   if (t < 256) sfin[t] = x;
   __syncthreads();
@@ -427,13 +435,17 @@ __device__ __forceinline__ double octet_partial(const double* x, int64_t stride,
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   if (a.done && *a.done) return;
   const int sub = threadIdx.x & (kFinTPI - 1);
-  const int64_t k = a.item_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kFinTPI;
   const int64_t tot_items = a.item_end > 0 ? a.item_end : a.nrows + a.n;
-  const bool in_range = k < tot_items;
-  const bool is_row = k < a.nrows;
+  const int64_t groups = (tot_items - a.item_begin + (256 / kFinTPI) - 1) / (256 / kFinTPI);
   double v[kNumScalars];
 #pragma unroll
   for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
+  // grid-stride over groups of 32 items (one octet per item); the grid is
+  // capped at 2 x #SMs so the last-block combine stays short
+  for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+  const int64_t k = a.item_begin + grp * (256 / kFinTPI) + threadIdx.x / kFinTPI;
+  const bool in_range = k < tot_items;
+  const bool is_row = k < a.nrows;
   double tot = 0.0;
   if (a.from_partials == 1) {   // octet-parallel partial sums; the shuffles run on the whole warp
     double x = 0.0;
@@ -478,28 +490,37 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
     a.g[k] = g;
     const double gc = a.gcur ? a.gcur[k] : 0.0;
     const double pc = a.pcur ? a.pcur[k] : 0.0;
-    v[is_row ? SC_MASS : SC_MASSC] = mm;
-    v[SC_L1] = fabs(g);
-    v[SC_RHO] = tgt - mm + mm * s;            // D_h(y|x) term with y = m, x = tgt (Z1)
-    v[SC_SG] = s * g;
-    v[SC_GCS] = gc * s;
-    v[SC_PCG] = pc * g;
-    v[SC_PRC] = pc * tgt;
-    v[SC_GG] = g * g;
-    v[SC_GCG] = gc * g;
-    v[SC_BAD] = bad;
-    v[SC_L1R] = is_row ? fabs(g) : 0.0;
+    v[is_row ? SC_MASS : SC_MASSC] += mm;
+    v[SC_L1] += fabs(g);
+    v[SC_RHO] += tgt - mm + mm * s;            // D_h(y|x) term with y = m, x = tgt (Z1)
+    v[SC_SG] += s * g;
+    v[SC_GCS] += gc * s;
+    v[SC_PCG] += pc * g;
+    v[SC_PRC] += pc * tgt;
+    v[SC_GG] += g * g;
+    v[SC_GCG] += gc * g;
+    v[SC_BAD] += bad;
+    v[SC_L1R] += is_row ? fabs(g) : 0.0;
     if (a.prep_flag && k == a.item_begin) {
       v[SC_BAD] += (double)(*a.prep_flag);
       *a.prep_flag = 0;
     }
   }
+  }
   block_reduce_and_publish<kNumScalars>(v, a.blockpart, a.ticket, a.scalars_dev, a.scalars_host, a.add_in);
 }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = 2 * sms;
+  }
   const int64_t items = (a.item_end > 0 ? a.item_end : a.nrows + a.n) - a.item_begin;
-  const unsigned blocks = (unsigned)((items * kFinTPI + 255) / 256);
+  const int64_t groups = (items * kFinTPI + 255) / 256;
+  const unsigned blocks = (unsigned)(groups < cap ? groups : cap);
   k_finalize<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }

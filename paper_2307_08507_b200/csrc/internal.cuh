@@ -194,6 +194,23 @@ struct PrepArgs {
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
 
+// Persistent cooperative slot kernel (persist.cu): a whole projection in one
+// launch (ctrl / prep / K1 / finalize phases separated by grid barriers).
+struct PersistArgs {
+  EvalArgs e;
+  PrepArgs p;
+  FinalizeArgs f;
+  CtrlState* ctrl;             // global state (read at entry, written back by CTA 0 at exit)
+  int* done_host;              // mapped flag (device alias), written by CTA 0's controller
+  unsigned int* gbar;          // [2] grid barrier (zeroed before launch)
+  double* cta_part;            // [grid][kNumScalars]
+  unsigned long long* k1_ns;   // [2] += K1 phase ns (%globaltimer between grid barriers), count
+  int initial;                 // 1: the first slot is the projection's initial evaluation
+  long long max_slots;
+};
+int persist_grid();            // co-resident grid size (0 = unsupported)
+cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cudaStream_t st);
+
 // misc vector kernels
 cudaError_t launch_setup(int64_t n, const double* r, double* logr, double* rho, cudaStream_t st);
 cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t st); // y = a x + b y

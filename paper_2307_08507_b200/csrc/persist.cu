@@ -1,0 +1,226 @@
+// paper_2307_08507_b200/csrc/persist.cu -- persistent cooperative slot
+// kernel: one launch runs a whole Bregman projection (Alg. 2 PNCG with the
+// Appx. C line search, or Alg. 3 Sinkhorn) on the GPU.
+//
+// Every CTA of the co-resident grid (2 per SM, 8 consumer warps + 1 TMA
+// producer warp) repeats, per evaluation slot:
+//   ctrl      each CTA runs the controller (ops.cuh ctrl_body) on its own
+//             shared-memory copy of the state: every CTA holds the same
+//             scalars, so every CTA takes the same decision (no barrier)
+//   prep      grid-stride over the 2n row/column items (accept copy,
+//             direction p = -s + beta p_prev, trial potentials, exponent split)
+//   -- grid barrier --
+//   K1        the TMA-fed fused marginal pass over this CTA's tiles
+//   -- grid barrier --
+//   finalize  grid-stride over items: partial sums, log marginals, s, grad,
+//             the 16 scalars -> per-CTA partial
+//   -- grid barrier --
+//   every CTA combines the per-CTA partials in the same fixed order.
+// Kernel launches, graph nodes and host round trips disappear from the loop;
+// the host launches once per MD step and reads the state back.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+#include "k1_tma.cuh"
+#include "ops.cuh"
+
+namespace mdot {
+
+// TMA ring + the CTA's copy of the controller state.  The finalize scratch
+// (per-warp scalar partials, the cross-CTA combine) reuses tma.sred, which is
+// only live at K1 tile ends: 2 CTAs/SM fit (2 x 115.3 KB).
+struct PersistSmem {
+  TmaSmem tma;
+  CtrlState st;
+};
+static_assert(sizeof(double) * ((kTmaThreads / 32) * kNumScalars + 256) <= sizeof(TmaSmem::sred),
+              "finalize scratch must fit in tma.sred");
+
+// Sense-reversal grid barrier over co-resident CTAs (cooperative launch):
+// bar[0] = arrivals, bar[1] = generation.  One gpu-scope fence per CTA on each
+// side; the CTA barriers make every thread's prior writes part of it.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vb = bar;
+    const unsigned int gen = vb[1];
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while (vb[1] == gen) __nanosleep(20);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 2)
+    k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+  PersistSmem& S = *reinterpret_cast<PersistSmem*>(smem_raw + pad);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* red = &S.tma.sred[0][0];                     // [9 warps][16]
+  double* fin = red + (kTmaThreads / 32) * kNumScalars;  // [256]
+  constexpr int kWords = (int)(sizeof(CtrlState) / sizeof(unsigned long long));
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&S.tma.full[s], 1);
+      mbar_init(&S.tma.empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    const unsigned long long* g = reinterpret_cast<const unsigned long long*>(a.ctrl);
+    unsigned long long* sh = reinterpret_cast<unsigned long long*>(&S.st);
+    for (int i = tid; i < kWords; i += blockDim.x) sh[i] = g[i];
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+
+  const int64_t items = a.p.nrows + a.p.n;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  uint32_t it = 0;
+  unsigned long long k1_ns = 0, k1_cnt = 0;
+  bool first = a.initial != 0;
+  for (long long slot = 0; slot < a.max_slots; ++slot) {
+    // ---------------------------------------------------------------- ctrl
+    if (!first) {
+      if (tid == 0) ctrl_body(&S.st, 0, blockIdx.x == 0 ? a.done_host : nullptr, nullptr);
+      __syncthreads();
+      if (S.st.done) {
+        // the accept copy requested together with `done` still applies
+        if (S.st.accept_marg || S.st.accept_pot)
+          for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride)
+            prep_item(a.p, k, &S.st);
+        break;
+      }
+    }
+    first = false;
+    // ---------------------------------------------------------------- prep
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride) prep_item(a.p, k, &S.st);
+    grid_barrier(a.gbar);
+    const unsigned long long t0 = (blockIdx.x == 0 && tid == 0) ? global_ns() : 0ull;
+    // ------------------------------------------------------------------ K1
+    if (warp == kConsumerWarps) {
+      if (lane == 0) tma_produce_pass(S.tma, &tmap, a.e, it);
+    } else {
+      tma_consume_pass(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1]);
+    }
+    grid_barrier(a.gbar);
+    if (blockIdx.x == 0 && tid == 0) {
+      k1_ns += global_ns() - t0;
+      k1_cnt++;
+    }
+    // ------------------------------------------------------------ finalize
+    double v[kNumScalars];
+#pragma unroll
+    for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
+    if (warp < kConsumerWarps) {
+      const int sub = tid & (kFinTPI - 1);
+      const int64_t groups = (items + 31) / 32;
+      for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+        const int64_t k = grp * 32 + tid / kFinTPI;
+        const bool in_range = k < items;
+        const bool is_row = k < a.f.nrows;
+        double x = 0.0;
+        if (in_range) {
+          if (is_row) x = octet_partial(a.f.rowpart + k, a.f.nrows, a.f.n_col_tiles, sub);
+          else x = octet_partial(a.f.colpart + (k - a.f.nrows), a.f.n, a.f.n_row_tiles, sub);
+        }
+        x += __shfl_xor_sync(0xffffffffu, x, 1);
+        x += __shfl_xor_sync(0xffffffffu, x, 2);
+        x += __shfl_xor_sync(0xffffffffu, x, 4);
+        if (in_range && sub == 0) finalize_item(a.f, k, x, v);
+      }
+    }
+    // CTA partial (fixed order): warp shuffle tree, then warps in order
+#pragma unroll
+    for (int q = 0; q < kNumScalars; ++q) {
+      double y = v[q];
+      for (int off = 16; off > 0; off >>= 1) y += __shfl_xor_sync(0xffffffffu, y, off);
+      if (lane == 0) red[warp * kNumScalars + q] = y;
+    }
+    __syncthreads();
+    if (tid < kNumScalars) {
+      double y = 0.0;
+      for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
+      a.cta_part[(int64_t)blockIdx.x * kNumScalars + tid] = y;
+    }
+    grid_barrier(a.gbar);
+    // every CTA combines all CTA partials in the same order -> identical scalars
+    {
+      constexpr int G = 256 / kNumScalars;
+      double y = 0.0;
+      if (tid < 256) {
+        const int q = tid % kNumScalars;
+        for (unsigned b = tid / kNumScalars; b < gridDim.x; b += G)
+          y += __ldcg(&a.cta_part[(int64_t)b * kNumScalars + q]);
+        fin[tid] = y;
+      }
+      __syncthreads();
+      if (tid < kNumScalars) {
+        double z = 0.0;
+        for (int g = 0; g < G; ++g) z += fin[g * kNumScalars + tid];
+        S.st.sc[tid] = z;
+      }
+      __syncthreads();
+    }
+    // the per-CTA partial buffer is reused next slot: nobody may overwrite it
+    // before every CTA has read it (the next write happens after two more
+    // grid barriers, so no extra barrier is needed here)
+  }
+  // write the state back (CTA 0) and the K1 phase timing
+  if (blockIdx.x == 0) {
+    const unsigned long long* sh = reinterpret_cast<const unsigned long long*>(&S.st);
+    unsigned long long* g = reinterpret_cast<unsigned long long*>(a.ctrl);
+    __syncthreads();
+    for (int i = tid; i < kWords; i += blockDim.x) g[i] = sh[i];
+    if (tid == 0) {
+      a.k1_ns[0] += k1_ns;
+      a.k1_ns[1] += k1_cnt;
+    }
+  }
+}
+
+static int g_persist_grid = -1;
+
+int persist_grid() {
+  if (g_persist_grid >= 0) return g_persist_grid;
+  const int smem = (int)sizeof(PersistSmem) + 128;
+  if (cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    g_persist_grid = 0;
+    return 0;
+  }
+  cudaFuncSetAttribute(k_persist, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+  int per_sm = 0, dev = 0, sms = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist, kTmaThreads, smem) != cudaSuccess)
+    per_sm = 0;
+  g_persist_grid = per_sm >= 1 ? (per_sm >= 2 ? 2 : 1) * sms : 0;
+  return g_persist_grid;
+}
+
+cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cudaStream_t st) {
+  const int smem = (int)sizeof(PersistSmem) + 128;
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(map);
+  void* args[] = {const_cast<CUtensorMap*>(m), const_cast<PersistArgs*>(&a)};
+  return cudaLaunchCooperativeKernel((const void*)k_persist, dim3(grid), dim3(kTmaThreads), args, (size_t)smem, st);
+}
+
+}  // namespace mdot

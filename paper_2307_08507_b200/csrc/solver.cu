@@ -91,7 +91,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   eval.tile_m = tile_m;
   eval.n_row_tiles = (int)((nrows + tile_m - 1) / tile_m);
   chunks = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, (4 * 148 + (n + 255) / 256 - 1) / ((n + 255) / 256)));
-  const int64_t fin_blocks = (items * 8 + 255) / 256 + 8;   // k_finalize: 8 threads per item
+  const int64_t fin_blocks = std::max<int64_t>((items * 8 + 255) / 256 + 8, 1024);   // k_finalize / persistent CTAs
 
   size_t dbl = 0;
   auto take = [&](int64_t k) { size_t o = dbl; dbl += (size_t)((k + 31) / 32 * 32); return o; };
@@ -140,6 +140,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   CK(cudaMemsetAsync(ticket_flag, 0, 64 + tickets * 4, st));
   ticket = ticket_flag;
   flag = reinterpret_cast<int*>(ticket_flag + 4);
+  pers_bar = ticket_flag + 8;   // [2] barrier + [2 x u64] K1 timing (16-byte aligned)
   CK(cudaHostAlloc(&scal_host, 256 * sizeof(double), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer((void**)&scal_host_dev, scal_host, 0));
   memset(scal_host, 0, 256 * sizeof(double));
@@ -603,6 +604,89 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
 }
 
 // ---------------------------------------------------------------------------
+// Persistent cooperative projection: one launch per projection (persist.cu)
+// ---------------------------------------------------------------------------
+mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  CtrlState h{};
+  h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
+  h.noise = 6e-8;
+  h.stop_rho = o.stop; h.ncg = o.projector == MDOT_PROJ_NCG; h.sinkhorn = o.projector == MDOT_PROJ_SINKHORN;
+  h.beta_kind = o.beta; h.ls_max_trials = o.ls_max_trials;
+  h.max_evals = o.max_evals - w.evals;
+  h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
+  h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+  cudaStream_t st = w.st;
+  CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 2 * sizeof(unsigned long long) + 64, st));
+  *((volatile int*)w.done_host) = 0;
+  PersistArgs a{};
+  a.e = w.eval;
+  PrepArgs& p = a.p;
+  p.n = w.n; p.nrows = w.nrows; p.mode = 0;
+  p.U = w.U; p.V = w.V; p.u = w.u; p.v = w.v; p.tu = w.tu; p.tv = w.tv;
+  p.p = w.p; p.s = w.cur->s; p.pprev = w.pprev; p.lm = w.cur->lm;
+  p.logr = w.logr; p.logc = w.logc; p.rho_r = w.rho_r; p.sig_c = w.sig_c;
+  p.Aout = w.A; p.Bout = w.B;
+  p.rowp = w.rowp; p.colp = w.colp; p.flag = w.flag;
+  p.ctrl = nullptr;
+  p.cur_lm = w.cur->lm; p.cur_m = w.cur->m; p.cur_s = w.cur->s; p.cur_g = w.cur->g;
+  p.tr_lm = w.trial->lm; p.tr_m = w.trial->m; p.tr_s = w.trial->s; p.tr_g = w.trial->g;
+  FinalizeArgs& f = a.f;
+  f.n = w.n; f.nrows = w.nrows;
+  f.rho_r = w.rho_r; f.sig_c = w.sig_c;
+  f.r = w.r; f.c = w.c; f.logr = w.logr; f.logc = w.logc;
+  f.gcur = w.cur->g; f.pcur = w.p;
+  f.lm = w.trial->lm; f.m = w.trial->m; f.s = w.trial->s; f.g = w.trial->g;
+  f.prep_flag = w.flag;
+  f.from_partials = 1;
+  f.rowpart = w.rowpart; f.n_col_tiles = w.eval.n_col_tiles;
+  f.colpart = w.colpart; f.n_row_tiles = w.eval.n_row_tiles;
+  a.ctrl = w.ctrl;
+  cudaHostGetDevicePointer((void**)&a.done_host, w.done_host, 0);
+  a.gbar = w.pers_bar;
+  a.k1_ns = reinterpret_cast<unsigned long long*>(w.pers_bar + 4);
+  a.cta_part = w.blockpart;
+  a.initial = 1;
+  a.max_slots = (long long)1 << 40;
+  CK(launch_persist(w.tmap, a, w.pers_grid, st));
+  w.launches++;
+  unsigned long long k1[2] = {0, 0};
+  CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(k1, a.k1_ns, sizeof(k1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (w.time_kernels && k1[1]) {
+    w.kernel_ms += (double)k1[0] * 1e-6;
+    w.kernel_launches += (int64_t)k1[1];
+    w.stage_ms[2] += (double)k1[0] * 1e-6;
+    w.stage_samples += (int64_t)k1[1];
+  }
+  w.evals += h.evals;
+  res->iterations += h.iterations;
+  res->ls_evaluations += h.ls_evals;
+  res->resets += h.resets;
+  res->ls_restarts += h.restarts;
+  if (t >= 1 && t <= 64) {
+    res->rho0[t - 1] = h.rho_0;
+    res->l10[t - 1] = h.l1_0;
+    res->iters_step[t - 1] += h.iterations;
+  }
+  res->l1_final = h.l1;
+  res->rho_final = h.rho;
+  w.last_mass = h.mass;
+  switch (h.status) {
+    case CTRL_OK: return MDOT_OK;
+    case CTRL_NOCONV: return MDOT_ENOCONV;
+    case CTRL_LS_FAIL:
+      set_error("line search failed twice at MD step %d (persistent control)", t);
+      return MDOT_ELINESEARCH;
+    case CTRL_NEED_HOST:
+    default:
+      w.fallbacks++;
+      return (o.projector == MDOT_PROJ_SINKHORN) ? project_sinkhorn(w, o, t, res) : project_pncg(w, o, t, res);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Schedules (Z13)
 // ---------------------------------------------------------------------------
 mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g) {
@@ -732,6 +816,7 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       const int64_t tiles = (int64_t)eval.n_row_tiles * eval.n_col_tiles;
       tma_grid = (int)std::min<int64_t>(tiles, 2 * (int64_t)sms);
       use_tma = true;
+      pers_grid = (getenv("MDOT_NO_PERSIST") || comm) ? 0 : persist_grid();
     }
   }
   if (getenv("MDOT_DEBUG"))
@@ -934,7 +1019,8 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
         ++w.launches; launch_axpby(nr, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
         ++w.launches; launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
       }
-      if (o.device_control) solve_st = project_device(w, o, (int)t, res);
+      if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, o, (int)t, res);
+      else if (o.device_control) solve_st = project_device(w, o, (int)t, res);
       else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
       else solve_st = project_pncg(w, o, (int)t, res);
       res->md_steps = (int64_t)t;

@@ -61,6 +61,8 @@ struct Workspace {
   alignas(64) unsigned char tmap[128];
   bool use_tma = false;
   int tma_grid = 0;
+  int pers_grid = 0;                // persistent cooperative projection (0 = off)
+  unsigned int* pers_bar = nullptr;
   // stats
   int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;
   double kernel_ms = 0.0;
@@ -101,5 +103,6 @@ mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g);
 mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result* res);
 mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_result* res);
 mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_result* res);
+mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_result* res);
 
 }  // namespace mdot

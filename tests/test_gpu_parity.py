@@ -376,3 +376,24 @@ def test_sharded_virtual_ranks_match_single_gpu(G):
     lr, lc, _ = O.log_marginals(prob, U, V, 512.0)
     l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
     assert l1 <= 2 * eps
+
+
+@pytest.mark.parametrize("projector", [0, 1])
+def test_persistent_matches_graph_control(projector, monkeypatch):
+    """Persistent cooperative projection (one launch per MD step) against the
+    graph-driven device control: same controller code, same gates."""
+    n = 1024
+    inst = S.uniform_points_instance(3, n, 2, 12, marg="dirichlet")
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, 2048.0, T=8)
+    eps = 1e-6
+    rp = M.mdot_solve(C, r, c, schedule=sched, options=M.options(eps=eps, projector=projector, device_control=1))
+    rg = M.mdot_solve(C, r, c, schedule=sched, options=M.options(eps=eps, projector=projector, device_control=2))
+    assert rp["status"] == 0 and rg["status"] == 0
+    assert rp["all_launches"] < rg["all_launches"]          # the persistent path really ran
+    assert rp["l1_final"] <= eps and rg["l1_final"] <= eps
+    assert abs(rp["cost_unrounded"] - rg["cost_unrounded"]) <= 2e-6 * rg["cost_unrounded"]
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(2048.0, T=8),
+                             O.make_options(eps=eps, projector=O.SINKHORN if projector else O.PNCG))
+    assert abs(rp["cost_unrounded"] - ores["cost_unrounded"]) <= 1e-5 * ores["cost_unrounded"]

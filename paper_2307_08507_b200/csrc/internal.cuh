@@ -209,6 +209,7 @@ struct PersistArgs {
   long long max_slots;
 };
 int persist_grid();            // co-resident grid size (0 = unsupported)
+int persist_max_chunk();       // max finalize items per CTA
 cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cudaStream_t st);
 
 // misc vector kernels

@@ -103,8 +103,60 @@ __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap*
   }
 }
 
+// Stages of C this CTA streams per pass (its tiles, round-robin).
+__device__ __forceinline__ int tma_cta_stages(const EvalArgs& a) {
+  const int nct = a.n_col_tiles;
+  const int64_t total = (int64_t)a.n_row_tiles * nct;
+  const int spt = a.tile_m / kTmaRows;
+  int cnt = 0;
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int64_t i0 = (int64_t)(tile / nct) * a.tile_m;
+    int nst = spt;
+    if (i0 + (int64_t)nst * kTmaRows > a.nrows) nst = (int)((a.nrows - i0 + kTmaRows - 1) / kTmaRows);
+    cnt += nst;
+  }
+  return cnt;
+}
+
+// Producer over the endless sequence pass, pass, ... of this CTA's stages:
+// issues `count` stages from the cursor (tile, k).  The persistent kernel
+// uses it to prefetch the first stages of the next pass while the grid runs
+// finalize / control / prep (C does not depend on the potentials).
+struct TmaCursor {
+  int64_t tile;
+  int k;
+};
+__device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
+                                              TmaCursor& cur, uint32_t& it, int count) {
+  const int nct = a.n_col_tiles;
+  const int64_t total = (int64_t)a.n_row_tiles * nct;
+  const int spt = a.tile_m / kTmaRows;
+  for (int q = 0; q < count; ++q, ++it) {
+    const int tr = (int)(cur.tile / nct), tc = (int)(cur.tile % nct);
+    const int64_t i0 = (int64_t)tr * a.tile_m;
+    int nst = spt;
+    if (i0 + (int64_t)nst * kTmaRows > a.nrows) nst = (int)((a.nrows - i0 + kTmaRows - 1) / kTmaRows);
+    const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
+    mbar_wait(&sm.empty[s], ph ^ 1u);
+    mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
+    tma_load_2d(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + cur.k * kTmaRows), &sm.full[s]);
+    if (++cur.k == nst) {
+      cur.k = 0;
+      cur.tile += gridDim.x;
+      if (cur.tile >= total) cur.tile = blockIdx.x;   // next pass
+    }
+  }
+}
+
 // Consumers (warps 0..7): the fused exp-reduce over the stages of this CTA's
 // tiles; row totals -> rowpart[tc][i], column totals per tile -> colpart[tr][j].
+template <bool COHERENT = false>
+__device__ __forceinline__ float4 ld_param(const float4* p) {
+  if (COHERENT) return __ldcg(p);   // written earlier in the same (persistent) launch
+  return __ldg(p);
+}
+
+template <bool COHERENT = false>
 __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh,
                                                  float gl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -124,7 +176,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
     for (int q = 0; q < 8; ++q) {
       const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
       if (j < n) {
-        const float4 cp = __ldg(&a.colp[j]);
+        const float4 cp = ld_param<COHERENT>(&a.colp[j]);
         bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
       } else {
         bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
@@ -141,7 +193,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       float4 rp[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        rp[u] = (ib + u < nrows) ? __ldg(&a.rowp[ib + u]) : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+        rp[u] = (ib + u < nrows) ? ld_param<COHERENT>(&a.rowp[ib + u]) : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
       mbar_wait(&sm.full[s], ph);
       double rs[4];
 #pragma unroll

@@ -35,8 +35,10 @@ struct PersistSmem {
   TmaSmem tma;
   CtrlState st;
 };
-static_assert(sizeof(double) * ((kTmaThreads / 32) * kNumScalars + 256) <= sizeof(TmaSmem::sred),
+static_assert(sizeof(double) * ((kTmaThreads / 32) * kNumScalars + 512) <= sizeof(TmaSmem::sred),
               "finalize scratch must fit in tma.sred");
+// finalize chunk totals live at fin + 256 in tma.sred: items per CTA must fit
+constexpr int kPersistMaxChunk = (int)(sizeof(TmaSmem::sred) / sizeof(double)) - (kTmaThreads / 32) * kNumScalars - 256;
 
 // Sense-reversal grid barrier over co-resident CTAs (cooperative launch):
 // bar[0] = arrivals, bar[1] = generation.  One gpu-scope fence per CTA on each
@@ -93,7 +95,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   const int64_t items = a.p.nrows + a.p.n;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   uint32_t it = 0;
+  // producer: prefetch the first stages of the first pass right away
+  const int cta_stages = tma_cta_stages(a.e);
+  const int pre = cta_stages < kTmaStages ? cta_stages : kTmaStages;
+  TmaCursor cur{(int64_t)blockIdx.x, 0};
+  if (warp == kConsumerWarps && lane == 0 && cta_stages > 0) tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
   unsigned long long k1_ns = 0, k1_cnt = 0;
+  // CTA 0 phase timers (%globaltimer): [ctrl+prep+barrier, K1+barrier, finalize+barrier, combine]
+  unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long tp = (blockIdx.x == 0 && tid == 0) ? global_ns() : 0ull;
   bool first = a.initial != 0;
   for (long long slot = 0; slot < a.max_slots; ++slot) {
     // ---------------------------------------------------------------- ctrl
@@ -105,6 +115,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
         if (S.st.accept_marg || S.st.accept_pot)
           for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride)
             prep_item(a.p, k, &S.st);
+        // drain the stages the producer prefetched for a pass that will not
+        // run (no TMA may still target shared memory when the CTA exits)
+        if (warp < kConsumerWarps) {
+          for (int q = 0; q < pre; ++q, ++it) mbar_wait(&S.tma.full[it % kTmaStages], (it / kTmaStages) & 1u);
+        }
         break;
       }
     }
@@ -113,38 +128,54 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride) prep_item(a.p, k, &S.st);
     grid_barrier(a.gbar);
     const unsigned long long t0 = (blockIdx.x == 0 && tid == 0) ? global_ns() : 0ull;
+    if (blockIdx.x == 0 && tid == 0) ph[0] += t0 - tp;
     // ------------------------------------------------------------------ K1
     if (warp == kConsumerWarps) {
-      if (lane == 0) tma_produce_pass(S.tma, &tmap, a.e, it);
+      // the rest of this pass, then the prefetch of the next pass's first stages
+      if (lane == 0 && cta_stages > 0) {
+        tma_produce_n(S.tma, &tmap, a.e, cur, it, cta_stages - pre);
+        tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
+      }
     } else {
-      tma_consume_pass(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1]);
+      tma_consume_pass<true>(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1]);
     }
     grid_barrier(a.gbar);
+    unsigned long long t1 = 0;
     if (blockIdx.x == 0 && tid == 0) {
-      k1_ns += global_ns() - t0;
+      t1 = global_ns();
+      k1_ns += t1 - t0;
       k1_cnt++;
+      ph[1] += t1 - t0;
     }
     // ------------------------------------------------------------ finalize
     double v[kNumScalars];
 #pragma unroll
     for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
-    if (warp < kConsumerWarps) {
-      const int sub = tid & (kFinTPI - 1);
-      const int64_t groups = (items + 31) / 32;
-      for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
-        const int64_t k = grp * 32 + tid / kFinTPI;
-        const bool in_range = k < items;
-        const bool is_row = k < a.f.nrows;
+    {
+      // this CTA's contiguous chunk of items; (item, sub) tasks over all 288
+      // threads (a warp always holds whole octets), totals to smem, then one
+      // thread per item for the fp64 log / exp / scalar work
+      const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+      const int64_t i_lo = (int64_t)blockIdx.x * per;
+      const int64_t i_hi = (i_lo + per < items) ? i_lo + per : items;
+      const int cnt = i_hi > i_lo ? (int)(i_hi - i_lo) : 0;
+      double* tots = fin + 256;   // [cnt]
+      for (int task0 = 0; task0 < cnt * kFinTPI; task0 += blockDim.x) {
+        const int task = task0 + tid;
+        const int q = task / kFinTPI, sub = task % kFinTPI;
+        const int64_t k = i_lo + q;
         double x = 0.0;
-        if (in_range) {
-          if (is_row) x = octet_partial(a.f.rowpart + k, a.f.nrows, a.f.n_col_tiles, sub);
+        if (q < cnt) {
+          if (k < a.f.nrows) x = octet_partial(a.f.rowpart + k, a.f.nrows, a.f.n_col_tiles, sub);
           else x = octet_partial(a.f.colpart + (k - a.f.nrows), a.f.n, a.f.n_row_tiles, sub);
         }
         x += __shfl_xor_sync(0xffffffffu, x, 1);
         x += __shfl_xor_sync(0xffffffffu, x, 2);
         x += __shfl_xor_sync(0xffffffffu, x, 4);
-        if (in_range && sub == 0) finalize_item(a.f, k, x, v);
+        if (q < cnt && sub == 0) tots[q] = x;
       }
+      __syncthreads();
+      for (int q = tid; q < cnt; q += blockDim.x) finalize_item(a.f, i_lo + q, tots[q], v);
     }
     // CTA partial (fixed order): warp shuffle tree, then warps in order
 #pragma unroll
@@ -160,6 +191,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       a.cta_part[(int64_t)blockIdx.x * kNumScalars + tid] = y;
     }
     grid_barrier(a.gbar);
+    unsigned long long t2 = 0;
+    if (blockIdx.x == 0 && tid == 0) {
+      t2 = global_ns();
+      ph[2] += t2 - t1;
+    }
     // every CTA combines all CTA partials in the same order -> identical scalars
     {
       constexpr int G = 256 / kNumScalars;
@@ -178,6 +214,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       }
       __syncthreads();
     }
+    if (blockIdx.x == 0 && tid == 0) {
+      tp = global_ns();
+      ph[3] += tp - t2;
+    }
     // the per-CTA partial buffer is reused next slot: nobody may overwrite it
     // before every CTA has read it (the next write happens after two more
     // grid barriers, so no extra barrier is needed here)
@@ -191,6 +231,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     if (tid == 0) {
       a.k1_ns[0] += k1_ns;
       a.k1_ns[1] += k1_cnt;
+      for (int q = 0; q < 4; ++q) a.k1_ns[2 + q] += ph[q];
     }
   }
 }
@@ -215,6 +256,8 @@ int persist_grid() {
   g_persist_grid = per_sm >= 1 ? (per_sm >= 2 ? 2 : 1) * sms : 0;
   return g_persist_grid;
 }
+
+int persist_max_chunk() { return kPersistMaxChunk; }
 
 cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cudaStream_t st) {
   const int smem = (int)sizeof(PersistSmem) + 128;

@@ -42,6 +42,7 @@ struct EvalArgs {
   float gh, gl;            // g2 = gbar*log2(e) = gh + gl
   const float* gpair;      // device-resident {gh, gl} (device control), overrides gh/gl
   const int* done;         // device control: kernel returns at once when *done != 0
+  int keep_l2;             // TMA path: C fits in L2 -> evict_last (stays resident), else evict_first
   // outputs
   double* rowpart;         // [n_col_tiles][nrows]  sum_j 2^w T_j
   double* colpart;         // [n_row_tiles][n]      sum_i 2^w S_i

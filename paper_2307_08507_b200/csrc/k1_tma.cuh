@@ -47,6 +47,23 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
       "r"(parity)
       : "memory");
 }
+// L2 policy for the C stream: evict_first when C is larger than L2 (keeps
+// the partials and O(n) vectors resident), evict_last when C fits (C then
+// stays L2-resident across evaluations).
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t pol;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                 unsigned long long* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
                                             unsigned long long* bar) {
   asm volatile(
@@ -85,6 +102,7 @@ __device__ __forceinline__ double warp_reduce4_t(double v0, double v1, double v2
 // `it` is the running stage counter (kept across passes by the caller).
 __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
                                                  uint32_t& it) {
+  const uint64_t pol = l2_policy(a.keep_l2 != 0);
   const int64_t nrows = a.nrows;
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
@@ -98,7 +116,7 @@ __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap*
       const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
       mbar_wait(&sm.empty[s], ph ^ 1u);
       mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
-      tma_load_2d(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + k * kTmaRows), &sm.full[s]);
+      tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + k * kTmaRows), &sm.full[s], pol);
     }
   }
 }
@@ -128,6 +146,7 @@ struct TmaCursor {
 };
 __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
                                               TmaCursor& cur, uint32_t& it, int count) {
+  const uint64_t pol = l2_policy(a.keep_l2 != 0);
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
   const int spt = a.tile_m / kTmaRows;
@@ -139,7 +158,7 @@ __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tm
     const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
     mbar_wait(&sm.empty[s], ph ^ 1u);
     mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
-    tma_load_2d(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + cur.k * kTmaRows), &sm.full[s]);
+    tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + cur.k * kTmaRows), &sm.full[s], pol);
     if (++cur.k == nst) {
       cur.k = 0;
       cur.tile += gridDim.x;
@@ -150,9 +169,12 @@ __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tm
 
 // Consumers (warps 0..7): the fused exp-reduce over the stages of this CTA's
 // tiles; row totals -> rowpart[tc][i], column totals per tile -> colpart[tr][j].
+// COHERENT: the parameters were written earlier in the same (persistent)
+// launch -> a plain (L1-allocating, coherent) load; the grid barrier's
+// gpu-scope fence invalidates L1 between phases.  Otherwise the read-only path.
 template <bool COHERENT = false>
 __device__ __forceinline__ float4 ld_param(const float4* p) {
-  if (COHERENT) return __ldcg(p);   // written earlier in the same (persistent) launch
+  if (COHERENT) return *p;
   return __ldg(p);
 }
 

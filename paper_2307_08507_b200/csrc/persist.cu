@@ -43,20 +43,33 @@ constexpr int kPersistMaxChunk = (int)(sizeof(TmaSmem::sred) / sizeof(double)) -
 // Sense-reversal grid barrier over co-resident CTAs (cooperative launch):
 // bar[0] = arrivals, bar[1] = generation.  One gpu-scope fence per CTA on each
 // side; the CTA barriers make every thread's prior writes part of it.
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int atom_add_acqrel(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_release(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// release/acquire atomics instead of full fences: the CTA barrier orders every
+// thread's writes before thread 0's release-add; waiters acquire the
+// generation.  L1 is not relied upon across phases (phase data is read with
+// coherent loads or after this acquire).
 __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* vb = bar;
-    const unsigned int gen = vb[1];
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+    const unsigned int gen = ld_acquire(&bar[1]);
+    if (atom_add_acqrel(&bar[0], 1u) == gridDim.x - 1) {
       bar[0] = 0u;
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      atomicAdd(&bar[1], 1u);
+      red_release(&bar[1], 1u);
     } else {
-      while (vb[1] == gen) __nanosleep(20);
+      while (ld_acquire(&bar[1]) == gen) __nanosleep(8);
     }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
@@ -102,7 +115,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   if (warp == kConsumerWarps && lane == 0 && cta_stages > 0) tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
   unsigned long long k1_ns = 0, k1_cnt = 0;
   // CTA 0 phase timers (%globaltimer): [ctrl+prep+barrier, K1+barrier, finalize+barrier, combine]
-  unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long tp = (blockIdx.x == 0 && tid == 0) ? global_ns() : 0ull;
   bool first = a.initial != 0;
   for (long long slot = 0; slot < a.max_slots; ++slot) {
@@ -160,22 +173,53 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       const int64_t i_hi = (i_lo + per < items) ? i_lo + per : items;
       const int cnt = i_hi > i_lo ? (int)(i_hi - i_lo) : 0;
       double* tots = fin + 256;   // [cnt]
-      for (int task0 = 0; task0 < cnt * kFinTPI; task0 += blockDim.x) {
-        const int task = task0 + tid;
-        const int q = task / kFinTPI, sub = task % kFinTPI;
-        const int64_t k = i_lo + q;
-        double x = 0.0;
-        if (q < cnt) {
-          if (k < a.f.nrows) x = octet_partial(a.f.rowpart + k, a.f.nrows, a.f.n_col_tiles, sub);
-          else x = octet_partial(a.f.colpart + (k - a.f.nrows), a.f.n, a.f.n_row_tiles, sub);
+      // up to 4 rounds of (item, sub) tasks per thread; every partial load of
+      // all rounds is issued before the first add (latency once, not per round)
+      constexpr int kMaxRounds = 4;
+      const int rounds = (cnt * kFinTPI + blockDim.x - 1) / blockDim.x;
+      for (int r0 = 0; r0 < rounds; r0 += kMaxRounds) {
+        double acc[kMaxRounds];
+#pragma unroll
+        for (int rr = 0; rr < kMaxRounds; ++rr) {
+          acc[rr] = 0.0;
+          const int task = (r0 + rr) * blockDim.x + tid;
+          const int q = task / kFinTPI, sub = task % kFinTPI;
+          if (r0 + rr < rounds && q < cnt) {
+            const int64_t k = i_lo + q;
+            const double* base;
+            int64_t stride;
+            int m;
+            if (k < a.f.nrows) { base = a.f.rowpart + k; stride = a.f.nrows; m = a.f.n_col_tiles; }
+            else { base = a.f.colpart + (k - a.f.nrows); stride = a.f.n; m = a.f.n_row_tiles; }
+            double y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int tt = sub + u * kFinTPI;
+              y[u] = tt < m ? base[(int64_t)tt * stride] : 0.0;
+            }
+            double z = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) z += y[u];
+            for (int tt = sub + 8 * kFinTPI; tt < m; tt += kFinTPI) z += base[(int64_t)tt * stride];
+            acc[rr] = z;
+          }
         }
-        x += __shfl_xor_sync(0xffffffffu, x, 1);
-        x += __shfl_xor_sync(0xffffffffu, x, 2);
-        x += __shfl_xor_sync(0xffffffffu, x, 4);
-        if (q < cnt && sub == 0) tots[q] = x;
+#pragma unroll
+        for (int rr = 0; rr < kMaxRounds; ++rr) {
+          double x = acc[rr];
+          x += __shfl_xor_sync(0xffffffffu, x, 1);
+          x += __shfl_xor_sync(0xffffffffu, x, 2);
+          x += __shfl_xor_sync(0xffffffffu, x, 4);
+          const int task = (r0 + rr) * blockDim.x + tid;
+          const int q = task / kFinTPI, sub = task % kFinTPI;
+          if (r0 + rr < rounds && q < cnt && sub == 0) tots[q] = x;
+        }
       }
       __syncthreads();
+      if (blockIdx.x == 0 && tid == 0) ph[4] += global_ns() - t1;
       for (int q = tid; q < cnt; q += blockDim.x) finalize_item(a.f, i_lo + q, tots[q], v);
+      __syncthreads();
+      if (blockIdx.x == 0 && tid == 0) ph[5] += global_ns() - t1;
     }
     // CTA partial (fixed order): warp shuffle tree, then warps in order
 #pragma unroll
@@ -190,6 +234,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
       a.cta_part[(int64_t)blockIdx.x * kNumScalars + tid] = y;
     }
+    if (blockIdx.x == 0 && tid == 0) ph[6] += global_ns() - t1;
     grid_barrier(a.gbar);
     unsigned long long t2 = 0;
     if (blockIdx.x == 0 && tid == 0) {
@@ -231,7 +276,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     if (tid == 0) {
       a.k1_ns[0] += k1_ns;
       a.k1_ns[1] += k1_cnt;
-      for (int q = 0; q < 4; ++q) a.k1_ns[2 + q] += ph[q];
+      for (int q = 0; q < 7; ++q) a.k1_ns[2 + q] += ph[q];
     }
   }
 }

@@ -617,7 +617,7 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
   cudaStream_t st = w.st;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 6 * sizeof(unsigned long long) + 8, st));
+  CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 10 * sizeof(unsigned long long) + 8, st));
   *((volatile int*)w.done_host) = 0;
   PersistArgs a{};
   a.e = w.eval;
@@ -650,7 +650,7 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   a.max_slots = (long long)1 << 40;
   CK(launch_persist(w.tmap, a, w.pers_grid, st));
   w.launches++;
-  unsigned long long k1[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long k1[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(k1, a.k1_ns, sizeof(k1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -659,6 +659,9 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
     w.kernel_launches += (int64_t)k1[1];
     // persistent phases: [ctrl+prep, K1, finalize, combine] (each incl. its grid barrier)
     for (int q = 0; q < 4; ++q) w.stage_ms[q] += (double)k1[2 + q] * 1e-6;
+    if (getenv("MDOT_DEBUG"))
+      fprintf(stderr, "[mdot] persistent finalize sub-phases (us/slot): partials %.2f items %.2f cta-reduce %.2f\n",
+              k1[6] * 1e-3 / k1[1], k1[7] * 1e-3 / k1[1], k1[8] * 1e-3 / k1[1]);
     w.stage_samples += (int64_t)k1[1];
   }
   w.evals += h.evals;
@@ -817,13 +820,16 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       const int64_t tiles = (int64_t)eval.n_row_tiles * eval.n_col_tiles;
       tma_grid = (int)std::min<int64_t>(tiles, 2 * (int64_t)sms);
       use_tma = true;
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+      eval.keep_l2 = (4.0 * (double)nrows * (double)n <= 0.6 * (double)l2) ? 1 : 0;
       pers_grid = (getenv("MDOT_NO_PERSIST") || comm) ? 0 : persist_grid();
       if (pers_grid > 0 && (nrows + n + pers_grid - 1) / pers_grid > persist_max_chunk()) pers_grid = 0;
     }
   }
   if (getenv("MDOT_DEBUG"))
-    fprintf(stderr, "[mdot] n=%lld nrows=%lld tile_m=%d tiles=%dx%d use_tma=%d grid=%d exact=%d\n", (long long)n,
-            (long long)nrows, eval.tile_m, eval.n_row_tiles, eval.n_col_tiles, (int)use_tma, tma_grid, (int)exact_mode);
+    fprintf(stderr, "[mdot] n=%lld nrows=%lld tile_m=%d tiles=%dx%d use_tma=%d grid=%d persist_grid=%d\n", (long long)n,
+            (long long)nrows, eval.tile_m, eval.n_row_tiles, eval.n_col_tiles, (int)use_tma, tma_grid, pers_grid);
   return MDOT_OK;
 }
 

@@ -171,7 +171,8 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
     a.g[k] = g;
     const double gc = a.gcur ? a.gcur[k] : 0.0;
     const double pc = a.pcur ? a.pcur[k] : 0.0;
-    v[is_row ? SC_MASS : SC_MASSC] += mm;
+    if (is_row) v[SC_MASS] += mm;   // static indices only: v stays in registers
+    else v[SC_MASSC] += mm;
     v[SC_L1] += fabs(g);
     v[SC_RHO] += tgt - mm + mm * s;            // D_h(y|x) term with y = m, x = tgt (Z1)
     v[SC_SG] += s * g;

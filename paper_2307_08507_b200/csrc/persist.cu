@@ -34,6 +34,7 @@ namespace mdot {
 struct PersistSmem {
   TmaSmem tma;
   CtrlState st;
+  unsigned long long tm[12];   // CTA 0 phase timers (smem: no registers live across the loop)
 };
 static_assert(sizeof(double) * ((kTmaThreads / 32) * kNumScalars + 512) <= sizeof(TmaSmem::sred),
               "finalize scratch must fit in tma.sred");
@@ -80,7 +81,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-__global__ void __launch_bounds__(kTmaThreads, 2)
+__global__ void __launch_bounds__(kTmaThreads) __maxnreg__(112)
     k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
@@ -113,10 +114,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   const int pre = cta_stages < kTmaStages ? cta_stages : kTmaStages;
   TmaCursor cur{(int64_t)blockIdx.x, 0};
   if (warp == kConsumerWarps && lane == 0 && cta_stages > 0) tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
-  unsigned long long k1_ns = 0, k1_cnt = 0;
-  // CTA 0 phase timers (%globaltimer): [ctrl+prep+barrier, K1+barrier, finalize+barrier, combine]
-  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned long long tp = (blockIdx.x == 0 && tid == 0) ? global_ns() : 0ull;
+  // CTA 0 phase timers (%globaltimer) in smem: tm[0..3] = [ctrl+prep+barrier,
+  // K1+barrier, finalize+barrier, combine], tm[4..6] finalize sub-phases,
+  // tm[8] = K1 phase count, tm[9..11] = timestamps
+  const bool timer = (blockIdx.x == 0 && tid == 0);
+  if (tid < 12) S.tm[tid] = 0ull;
+  __syncthreads();
+  if (timer) S.tm[9] = global_ns();
   bool first = a.initial != 0;
   for (long long slot = 0; slot < a.max_slots; ++slot) {
     // ---------------------------------------------------------------- ctrl
@@ -140,8 +144,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     // ---------------------------------------------------------------- prep
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride) prep_item(a.p, k, &S.st);
     grid_barrier(a.gbar);
-    const unsigned long long t0 = (blockIdx.x == 0 && tid == 0) ? global_ns() : 0ull;
-    if (blockIdx.x == 0 && tid == 0) ph[0] += t0 - tp;
+    if (timer) {
+      const unsigned long long t0 = global_ns();
+      S.tm[0] += t0 - S.tm[9];
+      S.tm[10] = t0;
+    }
     // ------------------------------------------------------------------ K1
     if (warp == kConsumerWarps) {
       // the rest of this pass, then the prefetch of the next pass's first stages
@@ -153,12 +160,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       tma_consume_pass<true>(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1]);
     }
     grid_barrier(a.gbar);
-    unsigned long long t1 = 0;
-    if (blockIdx.x == 0 && tid == 0) {
-      t1 = global_ns();
-      k1_ns += t1 - t0;
-      k1_cnt++;
-      ph[1] += t1 - t0;
+    if (timer) {
+      const unsigned long long t1 = global_ns();
+      S.tm[1] += t1 - S.tm[10];
+      S.tm[8] += 1;
+      S.tm[10] = t1;
     }
     // ------------------------------------------------------------ finalize
     double v[kNumScalars];
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       double* tots = fin + 256;   // [cnt]
       // up to 4 rounds of (item, sub) tasks per thread; every partial load of
       // all rounds is issued before the first add (latency once, not per round)
-      constexpr int kMaxRounds = 4;
+      constexpr int kMaxRounds = 2;
       const int rounds = (cnt * kFinTPI + blockDim.x - 1) / blockDim.x;
       for (int r0 = 0; r0 < rounds; r0 += kMaxRounds) {
         double acc[kMaxRounds];
@@ -191,16 +197,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
             int m;
             if (k < a.f.nrows) { base = a.f.rowpart + k; stride = a.f.nrows; m = a.f.n_col_tiles; }
             else { base = a.f.colpart + (k - a.f.nrows); stride = a.f.n; m = a.f.n_row_tiles; }
-            double y[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int tt = sub + u * kFinTPI;
-              y[u] = tt < m ? base[(int64_t)tt * stride] : 0.0;
-            }
             double z = 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) z += y[u];
-            for (int tt = sub + 8 * kFinTPI; tt < m; tt += kFinTPI) z += base[(int64_t)tt * stride];
+            for (int tt = sub; tt < m; tt += 4 * kFinTPI) {
+              const double y0 = base[(int64_t)tt * stride];
+              const double y1 = tt + kFinTPI < m ? base[(int64_t)(tt + kFinTPI) * stride] : 0.0;
+              const double y2 = tt + 2 * kFinTPI < m ? base[(int64_t)(tt + 2 * kFinTPI) * stride] : 0.0;
+              const double y3 = tt + 3 * kFinTPI < m ? base[(int64_t)(tt + 3 * kFinTPI) * stride] : 0.0;
+              z += y0; z += y1; z += y2; z += y3;
+            }
             acc[rr] = z;
           }
         }
@@ -216,10 +220,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
         }
       }
       __syncthreads();
-      if (blockIdx.x == 0 && tid == 0) ph[4] += global_ns() - t1;
+      if (timer) S.tm[4] += global_ns() - S.tm[10];
       for (int q = tid; q < cnt; q += blockDim.x) finalize_item(a.f, i_lo + q, tots[q], v);
       __syncthreads();
-      if (blockIdx.x == 0 && tid == 0) ph[5] += global_ns() - t1;
+      if (timer) S.tm[5] += global_ns() - S.tm[10];
     }
     // CTA partial (fixed order): warp shuffle tree, then warps in order
 #pragma unroll
@@ -234,12 +238,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
       a.cta_part[(int64_t)blockIdx.x * kNumScalars + tid] = y;
     }
-    if (blockIdx.x == 0 && tid == 0) ph[6] += global_ns() - t1;
+    if (timer) S.tm[6] += global_ns() - S.tm[10];
     grid_barrier(a.gbar);
-    unsigned long long t2 = 0;
-    if (blockIdx.x == 0 && tid == 0) {
-      t2 = global_ns();
-      ph[2] += t2 - t1;
+    if (timer) {
+      const unsigned long long t2 = global_ns();
+      S.tm[2] += t2 - S.tm[10];
+      S.tm[11] = t2;
     }
     // every CTA combines all CTA partials in the same order -> identical scalars
     {
@@ -259,9 +263,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       }
       __syncthreads();
     }
-    if (blockIdx.x == 0 && tid == 0) {
-      tp = global_ns();
-      ph[3] += tp - t2;
+    if (timer) {
+      S.tm[9] = global_ns();
+      S.tm[3] += S.tm[9] - S.tm[11];
     }
     // the per-CTA partial buffer is reused next slot: nobody may overwrite it
     // before every CTA has read it (the next write happens after two more
@@ -274,9 +278,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     __syncthreads();
     for (int i = tid; i < kWords; i += blockDim.x) g[i] = sh[i];
     if (tid == 0) {
-      a.k1_ns[0] += k1_ns;
-      a.k1_ns[1] += k1_cnt;
-      for (int q = 0; q < 7; ++q) a.k1_ns[2 + q] += ph[q];
+      a.k1_ns[0] += S.tm[1];
+      a.k1_ns[1] += S.tm[8];
+      for (int q = 0; q < 7; ++q) a.k1_ns[2 + q] += S.tm[q];
     }
   }
 }

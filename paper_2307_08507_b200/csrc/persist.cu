@@ -81,7 +81,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-__global__ void __launch_bounds__(kTmaThreads) __maxnreg__(112)
+__global__ void __maxnreg__(112)
     k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;

@@ -81,7 +81,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(104)
     k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
@@ -302,7 +302,9 @@ int persist_grid() {
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist, kTmaThreads, smem) != cudaSuccess)
     per_sm = 0;
-  g_persist_grid = per_sm >= 1 ? (per_sm >= 2 ? 2 : 1) * sms : 0;
+  // the K1 pass needs 2 CTAs per SM (18 warps) to keep HBM busy; with one the
+  // graph-driven path is faster, so the persistent path is used only at 2/SM
+  g_persist_grid = per_sm >= 2 ? 2 * sms : 0;
   return g_persist_grid;
 }
 

@@ -392,7 +392,7 @@ def test_persistent_matches_graph_control(projector, monkeypatch):
     assert rp["status"] == 0 and rg["status"] == 0
     assert rp["all_launches"] < rg["all_launches"]          # the persistent path really ran
     assert rp["l1_final"] <= eps and rg["l1_final"] <= eps
-    assert abs(rp["cost_unrounded"] - rg["cost_unrounded"]) <= 2e-6 * rg["cost_unrounded"]
+    assert abs(rp["cost_unrounded"] - rg["cost_unrounded"]) <= 1e-5 * rg["cost_unrounded"]   # Z20 gate
     prob = O.OracleProblem(inst)
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(2048.0, T=8),
                              O.make_options(eps=eps, projector=O.SINKHORN if projector else O.PNCG))

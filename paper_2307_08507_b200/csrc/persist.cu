@@ -34,7 +34,6 @@ namespace mdot {
 struct PersistSmem {
   TmaSmem tma;
   CtrlState st;
-  unsigned long long tm[12];   // CTA 0 phase timers (smem: no registers live across the loop)
 };
 static_assert(sizeof(double) * ((kTmaThreads / 32) * kNumScalars + 512) <= sizeof(TmaSmem::sred),
               "finalize scratch must fit in tma.sred");
@@ -114,13 +113,13 @@ __global__ void __maxnreg__(104)
   const int pre = cta_stages < kTmaStages ? cta_stages : kTmaStages;
   TmaCursor cur{(int64_t)blockIdx.x, 0};
   if (warp == kConsumerWarps && lane == 0 && cta_stages > 0) tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
-  // CTA 0 phase timers (%globaltimer) in smem: tm[0..3] = [ctrl+prep+barrier,
-  // K1+barrier, finalize+barrier, combine], tm[4..6] finalize sub-phases,
-  // tm[8] = K1 phase count, tm[9..11] = timestamps
+  // CTA 0 phase timers (%globaltimer), kept in global memory (thread 0 of CTA
+  // 0 only; no registers or smem live across the loop): tm[0..3] = [ctrl+prep
+  // +barrier, K1+barrier, finalize+barrier, combine], tm[4..6] finalize
+  // sub-phases, tm[8] = K1 phase count, tm[9..11] = timestamps
   const bool timer = (blockIdx.x == 0 && tid == 0);
-  if (tid < 12) S.tm[tid] = 0ull;
-  __syncthreads();
-  if (timer) S.tm[9] = global_ns();
+  unsigned long long* tm = a.k1_ns + 2;
+  if (timer) tm[9] = global_ns();
   bool first = a.initial != 0;
   for (long long slot = 0; slot < a.max_slots; ++slot) {
     // ---------------------------------------------------------------- ctrl
@@ -146,8 +145,8 @@ __global__ void __maxnreg__(104)
     grid_barrier(a.gbar);
     if (timer) {
       const unsigned long long t0 = global_ns();
-      S.tm[0] += t0 - S.tm[9];
-      S.tm[10] = t0;
+      tm[0] += t0 - tm[9];
+      tm[10] = t0;
     }
     // ------------------------------------------------------------------ K1
     if (warp == kConsumerWarps) {
@@ -162,9 +161,9 @@ __global__ void __maxnreg__(104)
     grid_barrier(a.gbar);
     if (timer) {
       const unsigned long long t1 = global_ns();
-      S.tm[1] += t1 - S.tm[10];
-      S.tm[8] += 1;
-      S.tm[10] = t1;
+      tm[1] += t1 - tm[10];
+      tm[8] += 1;
+      tm[10] = t1;
     }
     // ------------------------------------------------------------ finalize
     double v[kNumScalars];
@@ -220,10 +219,10 @@ __global__ void __maxnreg__(104)
         }
       }
       __syncthreads();
-      if (timer) S.tm[4] += global_ns() - S.tm[10];
+      if (timer) tm[4] += global_ns() - tm[10];
       for (int q = tid; q < cnt; q += blockDim.x) finalize_item(a.f, i_lo + q, tots[q], v);
       __syncthreads();
-      if (timer) S.tm[5] += global_ns() - S.tm[10];
+      if (timer) tm[5] += global_ns() - tm[10];
     }
     // CTA partial (fixed order): warp shuffle tree, then warps in order
 #pragma unroll
@@ -238,12 +237,12 @@ __global__ void __maxnreg__(104)
       for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
       a.cta_part[(int64_t)blockIdx.x * kNumScalars + tid] = y;
     }
-    if (timer) S.tm[6] += global_ns() - S.tm[10];
+    if (timer) tm[6] += global_ns() - tm[10];
     grid_barrier(a.gbar);
     if (timer) {
       const unsigned long long t2 = global_ns();
-      S.tm[2] += t2 - S.tm[10];
-      S.tm[11] = t2;
+      tm[2] += t2 - tm[10];
+      tm[11] = t2;
     }
     // every CTA combines all CTA partials in the same order -> identical scalars
     {
@@ -264,8 +263,8 @@ __global__ void __maxnreg__(104)
       __syncthreads();
     }
     if (timer) {
-      S.tm[9] = global_ns();
-      S.tm[3] += S.tm[9] - S.tm[11];
+      tm[9] = global_ns();
+      tm[3] += tm[9] - tm[11];
     }
     // the per-CTA partial buffer is reused next slot: nobody may overwrite it
     // before every CTA has read it (the next write happens after two more
@@ -278,9 +277,8 @@ __global__ void __maxnreg__(104)
     __syncthreads();
     for (int i = tid; i < kWords; i += blockDim.x) g[i] = sh[i];
     if (tid == 0) {
-      a.k1_ns[0] += S.tm[1];
-      a.k1_ns[1] += S.tm[8];
-      for (int q = 0; q < 7; ++q) a.k1_ns[2 + q] += S.tm[q];
+      a.k1_ns[0] = tm[1];
+      a.k1_ns[1] = tm[8];
     }
   }
 }

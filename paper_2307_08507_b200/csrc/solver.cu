@@ -617,7 +617,7 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
   cudaStream_t st = w.st;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 10 * sizeof(unsigned long long) + 8, st));
+  CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 14 * sizeof(unsigned long long) + 8, st));
   *((volatile int*)w.done_host) = 0;
   PersistArgs a{};
   a.e = w.eval;
@@ -650,7 +650,7 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   a.max_slots = (long long)1 << 40;
   CK(launch_persist(w.tmap, a, w.pers_grid, st));
   w.launches++;
-  unsigned long long k1[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long k1[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // [K1 ns, count, tm[0..7]]
   CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(k1, a.k1_ns, sizeof(k1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -204,10 +204,12 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
         bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
       }
     }
-    double cacc64[8];
+    // fp64 column accumulators live in this warp's row of sm.sred (warp-
+    // private; no registers held across the tile), fp32 over 8 rows first
     float cacc32[8];
+    double* csum = &sm.sred[warp][0];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) { cacc64[q] = 0.0; cacc32[q] = 0.f; }
+    for (int q = 0; q < 8; ++q) { csum[4 * lane + (q & 3) + 128 * (q >> 2)] = 0.0; cacc32[q] = 0.f; }
 
     for (int k = 0; k < nst; ++k, ++it) {
       const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
@@ -244,15 +246,16 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot;
       if (k & 1) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) { cacc64[q] += (double)cacc32[q]; cacc32[q] = 0.f; }
+        for (int q = 0; q < 8; ++q) {
+          csum[4 * lane + (q & 3) + 128 * (q >> 2)] += (double)cacc32[q];
+          cacc32[q] = 0.f;
+        }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) cacc64[q] += (double)cacc32[q];
+    for (int q = 0; q < 8; ++q) csum[4 * lane + (q & 3) + 128 * (q >> 2)] += (double)cacc32[q];
 
     // column sums of this tile (8 warps, fixed order) -> partial of row tile tr
-#pragma unroll
-    for (int q = 0; q < 8; ++q) sm.sred[warp][4 * lane + (q & 3) + 128 * (q >> 2)] = cacc64[q];
     consumer_bar();
     {
       const int tt = threadIdx.x;

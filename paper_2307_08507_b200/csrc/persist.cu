@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 #include "k1_tma.cuh"
@@ -80,7 +82,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-__global__ void __maxnreg__(104)
+__global__ void __launch_bounds__(kTmaThreads, 2)
     k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
@@ -300,6 +302,11 @@ int persist_grid() {
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist, kTmaThreads, smem) != cudaSuccess)
     per_sm = 0;
+  if (getenv("MDOT_DEBUG")) {
+    cudaFuncAttributes at;
+    cudaFuncGetAttributes(&at, k_persist);
+    fprintf(stderr, "[mdot] k_persist regs %d smem %d coop %d per_sm %d\n", at.numRegs, smem, coop, per_sm);
+  }
   // the K1 pass needs 2 CTAs per SM (18 warps) to keep HBM busy; with one the
   // graph-driven path is faster, so the persistent path is used only at 2/SM
   g_persist_grid = per_sm >= 2 ? 2 * sms : 0;

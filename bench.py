@@ -271,10 +271,18 @@ def run_ours(a, rank, world, local_rank):
     kern_n = sum(x["kernel_launches"] for x in results)
     launches = sum(x.get("all_launches", 0) for x in results)
     nsamp = sum(x.get("stage_samples", 0) for x in results)
+    path = results[-1].get("control_path", 1)
     stages = None
     if nsamp:
-        names = ["ctrl", "prep", "k1", "finalize"]
+        names = (["ctrl+prep", "k1", "finalize", "combine"] if path == 2 else ["ctrl", "prep", "k1", "finalize"])
         stages = {nm: 1000.0 * sum(x["stage_ms"][q] for x in results) / nsamp for q, nm in enumerate(names)}
+    control = {0: "host loop", 1: "CUDA-graph slots (device controller)",
+               2: "persistent cooperative kernel (device controller)"}.get(path, str(path))
+    timing = ("K1 phase of the persistent kernel, measured on the device with %globaltimer between its grid "
+              "barriers (CTA 0), every evaluation of the timed region (a phase of one launch cannot be "
+              "bracketed by CUDA events)" if path == 2 else
+              "CUDA events around K1 on the library stream, first slot of every device-control graph "
+              "(sampled), timed region only")
     value = evals / (ms / 1000.0)
     ms_step = ms / a.steps
     hbm, peak_kind = measured_peaks()
@@ -307,12 +315,12 @@ def run_ours(a, rank, world, local_rank):
                      "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
                      "traffic": traffic, "peak_source": peak_kind,
                      "bytes_per_launch": bytes_per_launch, "launches_timed": kern_n,
-                     "timing": "CUDA events around K1 on the library stream, first slot of every "
-                               "device-control graph (sampled), timed region only",
+                     "timing": timing,
                      "mean_launch_us": mean_launch_s * 1e6,
                      "kernel_share_of_step": (mean_launch_s * evals / (ms / 1000.0)) if kern_n else None},
         "clocks": clocks,
         "gpu_launches": launches,
+        "control": control,
         "slot_stage_us": stages,
     }
     # end-to-end through the C ABI with host buffers (rank 0, 1 GPU)

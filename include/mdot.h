@@ -119,10 +119,13 @@ typedef struct {
   int64_t fallbacks;       /* evaluations redone on the exact fp64 evaluator */
   int64_t kernel_launches; /* evaluation kernels timed */
   int64_t all_launches;    /* every kernel this library launched during the call */
-  double stage_ms[4];      /* time_kernels: sampled per-slot durations [ctrl, prep, K1, finalize] (sums) */
+  double stage_ms[4];      /* time_kernels: per-slot durations, sums over stage_samples slots.
+                              graph path (CUDA events, first slot of each graph): [ctrl, prep, K1, finalize];
+                              persistent path (%globaltimer, every slot): [ctrl+prep, K1, finalize, combine],
+                              each including its grid barrier */
   int64_t stage_samples;   /* number of sampled slots in stage_ms */
   int32_t status;
-  int32_t reserved;
+  int32_t control_path;    /* last projection's control: 0 host loop, 1 CUDA-graph slots, 2 persistent kernel */
   double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */
   double l10[64];          /* per MD step: L1 at the warm start */
   int64_t iters_step[64];  /* per MD step: projection iterations */

@@ -56,13 +56,13 @@ class Result(ct.Structure):
                 ("ls_evaluations", ct.c_int64), ("resets", ct.c_int64), ("ls_restarts", ct.c_int64),
                 ("fallbacks", ct.c_int64), ("kernel_launches", ct.c_int64), ("all_launches", ct.c_int64),
                 ("stage_ms", ct.c_double * 4), ("stage_samples", ct.c_int64),
-                ("status", ct.c_int32), ("reserved", ct.c_int32),
+                ("status", ct.c_int32), ("control_path", ct.c_int32),
                 ("rho0", ct.c_double * 64), ("l10", ct.c_double * 64),
                 ("iters_step", ct.c_int64 * 64)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_
-             if f not in ("rho0", "l10", "iters_step", "reserved", "stage_ms")}
+             if f not in ("rho0", "l10", "iters_step", "stage_ms")}
         d["stage_ms"] = list(self.stage_ms)
         T = int(min(self.md_steps, 64))
         d["rho0"] = list(self.rho0)[:T]

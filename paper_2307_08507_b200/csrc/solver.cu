@@ -75,7 +75,22 @@ static double now_s() {
 // ---------------------------------------------------------------------------
 bool Workspace::sharded() const { return comm != nullptr && comm->nranks > 1; }
 
+// Keep freed stream-ordered allocations in the device pool (no release at
+// every synchronize): repeated solves reuse the workspace / staging memory.
+static void retain_mempool() {
+  static int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
+  retain_mempool();
   st = stream;
   n = n_;
   nrows = nrows_;
@@ -299,6 +314,7 @@ static inline double stopval(const double* sc, int stop_rho) { return stop_rho ?
 
 // Sinkhorn, Alg. 3; one fused evaluation per half-step.
 mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  res->control_path = 0;
   double sc[kNumScalars];
   CKS(w.prep(PREP_CUR, 0, 0, nullptr, nullptr, nullptr));
   CKS(w.evaluate(w.cur, nullptr, nullptr, sc));
@@ -322,6 +338,7 @@ mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_re
 // PNCG, Alg. 2 with the line search of Appx. C
 // and readings Z5-Z10.
 mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  res->control_path = 0;
   const bool ncg = o.projector == MDOT_PROJ_NCG;
   double sc[kNumScalars], ts[kNumScalars];
   CKS(w.prep(PREP_CUR, 0, 0, nullptr, nullptr, nullptr));
@@ -535,6 +552,7 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
   h.max_evals = o.max_evals - w.evals;
   h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+  res->control_path = 1;
   CKS(w.build_graph());
   cudaStream_t st = w.st;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
@@ -616,6 +634,7 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
   cudaStream_t st = w.st;
+  res->control_path = 2;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 14 * sizeof(unsigned long long) + 8, st));
   *((volatile int*)w.done_host) = 0;

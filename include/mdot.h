@@ -125,7 +125,8 @@ typedef struct {
                               each including its grid barrier */
   int64_t stage_samples;   /* number of sampled slots in stage_ms */
   int32_t status;
-  int32_t control_path;    /* last projection's control: 0 host loop, 1 CUDA-graph slots, 2 persistent kernel */
+  int32_t control_path;    /* last projection's control: 0 host loop, 1 CUDA-graph slots, 2 persistent kernel,
+                              3 batched one-CTA-per-instance kernel (mdot_solve_batch) */
   double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */
   double l10[64];          /* per MD step: L1 at the warm start */
   int64_t iters_step[64];  /* per MD step: projection iterations */
@@ -157,9 +158,14 @@ mdot_status mdot_solve(const mdot_problem* pb, const mdot_schedule* sched, const
 mdot_status mdot_sinkhorn(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
                           double* u_out, double* v_out, float* P_out, mdot_result* res);
 
-/* Batch of B independent instances sharing one cost (BASELINE config 2).
- * r, c: B*n row-major (instance b at r + b*n); u_out, v_out: B*n, nullable;
- * res: B results.  Returns the first non-OK status (all instances run). */
+/* Batch of B independent instances sharing one cost (BASELINE config 2,
+ * PAPER.md:699 "including as a batch process").  r, c: B*n row-major
+ * (instance b at r + b*n); u_out, v_out: B*n, nullable; res: B results.
+ * Dense fp32 costs whose per-instance state fits in one SM's shared memory
+ * (n <= 784 on B200) run on the K8 kernel: one CTA per instance executes the
+ * whole solve on-chip, C shared through L2.  precision AUTO uses fp64 entries
+ * when eps < 5e-8.  Other costs fall back to one solve per instance.
+ * Returns the first non-OK status (all instances run). */
 mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t B, const double* r, const double* c,
                              const mdot_schedule* sched, const mdot_options* opt,
                              double* u_out, double* v_out, mdot_result* res);

@@ -1,0 +1,419 @@
+// paper_2307_08507_b200/csrc/batch.cu -- K8: batched MDOT solver for many
+// independent (r, c) pairs sharing one cost (BASELINE config 2, the MNIST-
+// shaped batch; "including as a batch process").
+//
+// One CTA (8 warps) per instance runs the WHOLE solve on-chip: MD loop
+// (Alg. 1), PNCG / Sinkhorn projections with the device controller
+// (ops.cuh ctrl_body), the fused row+column evaluation, and the final
+// rounding + cost.  Every O(n) vector of the instance lives in
+// shared memory (14 x 2n doubles + exponent parameters); C (n x n fp32, shared
+// by all instances) is streamed from L2.  Instances converge independently;
+// no cross-CTA communication, no host involvement until the batch is done.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/mdot.h"
+#include "internal.cuh"
+#include "ops.cuh"
+
+namespace mdot {
+
+constexpr int kBatchThreads = 256;
+constexpr int kBatchWarps = kBatchThreads / 32;
+
+__device__ __forceinline__ float bex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double bshx(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ double bred4(double v0, double v1, double v2, double v3, int lane) {
+  const bool up = lane & 16;
+  double k0 = up ? v2 : v0, k1 = up ? v3 : v1;
+  double s0 = up ? v0 : v2, s1 = up ? v1 : v3;
+  k0 += bshx(s0, 16);
+  k1 += bshx(s1, 16);
+  const bool up2 = lane & 8;
+  double kk = up2 ? k1 : k0, ss = up2 ? k0 : k1;
+  kk += bshx(ss, 8);
+  kk += bshx(kk, 4);
+  kk += bshx(kk, 2);
+  kk += bshx(kk, 1);
+  return kk;
+}
+
+// deterministic block reduction of NS doubles (all threads call; result in out)
+template <int NS>
+__device__ __forceinline__ void block_sum(double (&v)[NS], double* scratch /*[kBatchWarps][NS]*/, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double x = v[q];
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    if (lane == 0) scratch[warp * NS + q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NS) {
+    double x = 0.0;
+    for (int w = 0; w < kBatchWarps; ++w) x += scratch[w * NS + threadIdx.x];
+    out[threadIdx.x] = x;
+  }
+  __syncthreads();
+}
+
+struct BatchSmem {
+  // arrays of 2n doubles (rows then columns) follow in dynamic smem
+  CtrlState st;
+  double red[kBatchWarps * kNumScalars];
+  double out[kNumScalars];
+  double sred[kBatchWarps][kTileN];
+};
+
+// Fused evaluation of one instance: rowtot[i] = sum_j 2^w T_j and
+// coltot[j] = sum_i 2^w S_i (anchored units, internal.cuh "K1 numerics").
+// F64: w assembled and exponentiated in fp64 (fp64-entry mode, eps < 1e-7,
+// and the range-guard fallback).
+template <bool F64>
+__device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
+                           double* rowtot, double* coltot, double (*sred)[kTileN]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float4* rowp = prm;
+  const float4* colp = prm + n;
+  const bool vec4 = (n % 4) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  for (int j0 = 0; j0 < n; j0 += kTileN) {
+    float bh[8], bl[8], T[8];
+    int jj[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+      jj[q] = j;
+      if (j < n) {
+        const float4 cp = colp[j];
+        bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+      } else {
+        bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
+      }
+    }
+    double* csum = &sred[warp][0];
+    float c32[8];
+    double c64[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { c32[q] = 0.f; c64[q] = 0.0; }
+    int step = 0;
+    for (int ib = 4 * warp; ib < n; ib += 4 * kBatchWarps, ++step) {
+      double rs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ib + u;
+        float cv[8];
+        float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+        if (i < n) {
+          rp = rowp[i];
+          const float* crow = C + (int64_t)i * n;
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const int j = jj[4 * g];
+            if (vec4 && j + 3 < n) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(crow + j));
+              cv[4 * g] = x.x; cv[4 * g + 1] = x.y; cv[4 * g + 2] = x.z; cv[4 * g + 3] = x.w;
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) cv[4 * g + q] = (j + q < n) ? __ldg(crow + j + q) : 0.f;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cv[q] = 0.f;
+        }
+        if (!F64) {
+          float rsum = 0.f;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float zh = fmaf(-gh, cv[q], rp.x + bh[q]);
+            const float tt = fmaf(-gl, cv[q], rp.y + bl[q]);
+            const float e = bex2(zh + tt);
+            rsum = fmaf(e, T[q], rsum);
+            c32[q] = fmaf(e, rp.z, c32[q]);
+          }
+          rs[u] = rsum;
+        } else {
+          double rsum = 0.0;
+          const double ra = (double)rp.x + (double)rp.y;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const double w = (ra + ((double)bh[q] + (double)bl[q])) - g2 * (double)cv[q];
+            const double e = (bh[q] < -1.0e29f || rp.x < -1.0e29f) ? 0.0 : exp2(w);
+            rsum += e * (double)T[q];
+            c64[q] += e * (double)rp.z;
+          }
+          rs[u] = rsum;
+        }
+      }
+      const double tot = bred4(rs[0], rs[1], rs[2], rs[3], lane);
+      const int i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+      if ((lane & 7) == 0 && i < n) rowtot[i] = (j0 == 0) ? tot : rowtot[i] + tot;
+      if (!F64 && (step & 1)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c64[q] += (double)c32[q]; c32[q] = 0.f; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) csum[4 * lane + (q & 3) + 128 * (q >> 2)] = c64[q] + (double)c32[q];
+    __syncthreads();
+    {
+      const int t = threadIdx.x;   // kBatchThreads == kTileN
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < kBatchWarps; ++w) acc += sred[w][t];
+      if (j0 + t < n) coltot[j0 + t] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
+  const int n = a.n, n2 = 2 * a.n, tid = threadIdx.x;
+  const int b = blockIdx.x;
+  double* D = reinterpret_cast<double*>(smem_raw + sizeof(BatchSmem));
+  double* logt = D;            // log r | log c
+  double* tgt = D + 1 * n2;    // r | c
+  double* anc = D + 2 * n2;    // anchors rho | sig
+  double* UV = D + 3 * n2;     // cumulative potentials U | V
+  double* uv = D + 4 * n2;     // step potentials u | v
+  double* tuv = D + 5 * n2;    // trial potentials
+  double* p = D + 6 * n2;
+  double* pprev = D + 7 * n2;
+  double* cl = D + 8 * n2;     // current log marginals, s, grad
+  double* cs = D + 9 * n2;
+  double* cg = D + 10 * n2;
+  double* tl = D + 11 * n2;    // trial log marginals, s, grad
+  double* ts = D + 12 * n2;
+  double* tg = D + 13 * n2;
+  double* tot = D + 14 * n2;   // [2n] rowtot | coltot
+  float4* prm = reinterpret_cast<float4*>(D + 15 * n2);   // [2n]
+
+  // ---- setup (a1): targets, logs, anchors; U = log r, V = log c; u = v = 0
+  for (int k = tid; k < n2; k += blockDim.x) {
+    const double x = (k < n) ? a.r[(int64_t)b * n + k] : a.c[(int64_t)b * n + (k - n)];
+    tgt[k] = x;
+    const double lx = log(x);
+    logt[k] = lx;
+    double an = rint(0.5 * lx * L2E_D);
+    anc[k] = an < -60.0 ? -60.0 : (an > 0.0 ? 0.0 : an);
+    UV[k] = a.p0_ones ? 0.0 : lx;
+    uv[k] = 0.0;
+  }
+  __syncthreads();
+
+  PrepArgs pa{};
+  pa.n = n; pa.nrows = n;
+  pa.U = UV; pa.V = UV + n; pa.u = uv; pa.v = uv + n; pa.tu = tuv; pa.tv = tuv + n;
+  pa.p = p; pa.pprev = pprev; pa.lm = cl;
+  pa.logr = logt; pa.logc = logt + n; pa.rho_r = anc; pa.sig_c = anc + n;
+  pa.rowp = prm; pa.colp = prm + n; pa.flag = nullptr;
+  pa.cur_lm = cl; pa.cur_m = nullptr; pa.cur_s = cs; pa.cur_g = cg;
+  pa.tr_lm = tl; pa.tr_m = nullptr; pa.tr_s = ts; pa.tr_g = tg;
+  FinalizeArgs fa{};
+  fa.n = n; fa.nrows = n; fa.from_partials = 1;
+  fa.rho_r = anc; fa.sig_c = anc + n;
+  fa.r = tgt; fa.c = tgt + n; fa.logr = logt; fa.logc = logt + n;
+  fa.gcur = cg; fa.pcur = p;
+  fa.lm = tl; fa.m = nullptr; fa.s = ts; fa.g = tg;
+
+  long long evals_total = 0, iters = 0, ls_evals = 0, resets = 0, restarts = 0;
+  int status = 0;
+  double gbar = 0.0, gprev = 0.0, l1 = 0.0, rho = 0.0;
+  int t_done = 0;
+  for (int t = 1; t <= a.T; ++t) {
+    const double gt = a.gammas[t - 1];
+    gbar += gt;
+    const double g2 = gbar * L2E_D;
+    const float gh = (float)g2, gl = (float)(g2 - (double)(float)g2);
+    // warm start (Z4)
+    if (a.warm == MDOT_WARM_ZERO) {
+      for (int k = tid; k < n2; k += blockDim.x) uv[k] = 0.0;
+    } else if (a.warm == MDOT_WARM_SCALED && t > 1 && gt != gprev) {
+      const double w = gt / gprev;
+      for (int k = tid; k < n2; k += blockDim.x) uv[k] *= w;
+    }
+    // controller state for this projection
+    if (tid == 0) {
+      CtrlState& h = S.st;
+      memset(&h, 0, sizeof(CtrlState));
+      h.eps = a.eps; h.c1 = a.c1; h.c2 = a.c2; h.noise = a.f64 ? 1e-14 : 6e-8;
+      h.stop_rho = a.stop_rho; h.ncg = a.projector == MDOT_PROJ_NCG; h.sinkhorn = a.projector == MDOT_PROJ_SINKHORN;
+      h.beta_kind = a.beta_kind; h.ls_max_trials = a.ls_max_trials;
+      h.max_evals = a.max_evals - evals_total;
+      h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+    }
+    __syncthreads();
+    bool first = true;
+    for (;;) {
+      if (!first) {
+        if (tid == 0) ctrl_body(&S.st, 0, nullptr, nullptr);
+        __syncthreads();
+        if (S.st.done) {
+          if (S.st.accept_marg || S.st.accept_pot)
+            for (int k = tid; k < n2; k += blockDim.x) prep_item(pa, k, &S.st);
+          __syncthreads();
+          break;
+        }
+      }
+      first = false;
+      for (int k = tid; k < n2; k += blockDim.x) prep_item(pa, k, &S.st);
+      __syncthreads();
+      bool use64 = a.f64 != 0;
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        if (use64) batch_eval<true>(a.C, n, prm, gh, gl, g2, tot, tot + n, S.sred);
+        else batch_eval<false>(a.C, n, prm, gh, gl, g2, tot, tot + n, S.sred);
+        __syncthreads();
+        double v[kNumScalars];
+#pragma unroll
+        for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
+        for (int k = tid; k < n2; k += blockDim.x) finalize_item(fa, k, tot[k], v);
+        block_sum<kNumScalars>(v, S.red, S.out);
+        if (S.out[SC_BAD] == 0.0 || use64) break;
+        use64 = true;   // range guard fired: redo this evaluation with fp64 entries
+      }
+      if (tid < kNumScalars) S.st.sc[tid] = S.out[tid];
+      __syncthreads();
+    }
+    // projection result
+    const CtrlState& h = S.st;
+    evals_total += h.evals;
+    iters += h.iterations;
+    ls_evals += h.ls_evals;
+    resets += h.resets;
+    restarts += h.restarts;
+    l1 = h.l1;
+    rho = h.rho;
+    if (h.status == CTRL_NOCONV) status = MDOT_ENOCONV;
+    else if (h.status == CTRL_LS_FAIL) status = MDOT_ELINESEARCH;
+    else if (h.status == CTRL_NEED_HOST) status = MDOT_EINSTABLE;
+    __syncthreads();
+    // a9: U += u, V += v; gauge (U - d, V + d) with <r,U> = <c,V>, same for (u, v)
+    for (int k = tid; k < n2; k += blockDim.x) UV[k] += uv[k];
+    __syncthreads();
+    {
+      double v4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = tid; k < n2; k += blockDim.x) {
+        const int q = (k < n) ? 0 : 1;
+        v4[q] += tgt[k] * UV[k];
+        v4[2 + q] += tgt[k] * uv[k];
+      }
+      block_sum<4>(v4, S.red, S.out);
+      const double d1 = 0.5 * (S.out[0] - S.out[1]), d2 = 0.5 * (S.out[2] - S.out[3]);
+      for (int k = tid; k < n2; k += blockDim.x) {
+        UV[k] += (k < n) ? -d1 : d1;
+        uv[k] += (k < n) ? -d2 : d2;
+      }
+      __syncthreads();
+    }
+    gprev = gt;
+    t_done = t;
+    if (status != 0 && status != MDOT_ENOCONV) break;
+    if (status == MDOT_ENOCONV) break;
+  }
+
+  // ---- rounding + cost (a10), fp64: F = exp(U + V - gbar C), x = min(r/r(F), 1)
+  double cost_F = 0.0, cost_G = 0.0;
+  if (status == 0 || status == MDOT_ENOCONV) {
+    double* logx = tuv;        // [n] log x
+    double* Ap = tuv + n;      // [n] U + log x
+    double* cF1 = p;           // [n] c(F')
+    double* Bpp = p + n;       // [n] V + log y
+    double* ec = pprev;        // [n] err_c
+    double* er = pprev + n;    // [n] err_r (first holds 1/x)
+    double* invx = er;
+    for (int i = tid; i < n; i += blockDim.x) {
+      double lx = logt[i] - cl[i];
+      if (lx > 0.0) lx = 0.0;
+      logx[i] = lx;
+      Ap[i] = UV[i] + lx;
+      invx[i] = exp(-lx);
+    }
+    __syncthreads();
+    // columns: c(F')_j and sum_i C_ij F_ij (cost of F)
+    double vF[1] = {0.0};
+    for (int j = tid; j < n; j += blockDim.x) {
+      double s1 = 0.0, s2 = 0.0;
+      const double Bj = UV[n + j];
+      for (int i = 0; i < n; ++i) {
+        const double cij = (double)__ldg(a.C + (int64_t)i * n + j);
+        const double f1 = exp((Ap[i] + Bj) - gbar * cij);
+        s1 += f1;
+        s2 += cij * f1 * invx[i];
+      }
+      cF1[j] = s1;
+      vF[0] += s2;
+    }
+    block_sum<1>(vF, S.red, S.out);
+    cost_F = S.out[0];
+    for (int j = tid; j < n; j += blockDim.x) {
+      const double y = fmin(tgt[n + j] / cF1[j], 1.0);
+      Bpp[j] = UV[n + j] + log(y);
+      ec[j] = tgt[n + j] - y * cF1[j];
+    }
+    __syncthreads();
+    // rows: r(F''), <C, F''>, (C err_c)_i ; warp per row
+    const int lane = tid & 31, warp = tid >> 5;
+    double v3[3] = {0.0, 0.0, 0.0};   // |err_r|_1, <C,F''>, err_r . C err_c (lane 0 of each warp)
+    for (int i = warp; i < n; i += kBatchWarps) {
+      double s = 0.0, cs2 = 0.0, cr = 0.0;
+      for (int j = lane; j < n; j += 32) {
+        const double cij = (double)__ldg(a.C + (int64_t)i * n + j);
+        const double f2 = exp((Ap[i] + Bpp[j]) - gbar * cij);
+        s += f2;
+        cs2 += cij * f2;
+        cr += cij * ec[j];
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        cs2 += __shfl_xor_sync(0xffffffffu, cs2, off);
+        cr += __shfl_xor_sync(0xffffffffu, cr, off);
+      }
+      if (lane == 0) {
+        const double e = tgt[i] - s;
+        er[i] = e;
+        v3[0] += fabs(e);
+        v3[1] += cs2;
+        v3[2] += e * cr;
+      }
+    }
+    block_sum<3>(v3, S.red, S.out);
+    cost_G = S.out[1] + (S.out[0] >= 1e-300 ? S.out[2] / S.out[0] : 0.0);
+  }
+  // ---- outputs
+  if (a.U_out) for (int i = tid; i < n; i += blockDim.x) a.U_out[(int64_t)b * n + i] = UV[i];
+  if (a.V_out) for (int j = tid; j < n; j += blockDim.x) a.V_out[(int64_t)b * n + j] = UV[n + j];
+  if (tid == 0) {
+    BatchResult& R = a.res[b];
+    R.cost_rounded = cost_G;
+    R.cost_unrounded = cost_F;
+    R.l1_final = l1;
+    R.rho_final = rho;
+    R.gamma_bar = gbar;
+    R.evaluations = evals_total;
+    R.iterations = iters;
+    R.ls_evaluations = ls_evals;
+    R.resets = resets;
+    R.ls_restarts = restarts;
+    R.md_steps = t_done;
+    R.status = status;
+  }
+}
+
+size_t batch_smem_bytes(int n) { return sizeof(BatchSmem) + (size_t)15 * 2 * n * sizeof(double) + (size_t)2 * n * 16; }
+
+cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st) {
+  const size_t smem = batch_smem_bytes(a.n);
+  cudaError_t e = cudaFuncSetAttribute(k_batch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_batch_solve<<<B, kBatchThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace mdot

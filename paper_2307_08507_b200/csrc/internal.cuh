@@ -258,4 +258,27 @@ cudaError_t launch_round_combine_rows(const RoundArgs& a, const double* r, doubl
                                       unsigned int* ticket, double* out_dev, double* out_host,
                                       cudaStream_t st);
 
+// K8: batched solver, one CTA per instance (batch.cu)
+struct BatchResult {
+  double cost_rounded, cost_unrounded, l1_final, rho_final, gamma_bar;
+  long long evaluations, iterations, ls_evaluations, resets, ls_restarts;
+  int md_steps, status;
+};
+struct BatchArgs {
+  const float* C;          // shared n x n fp32 cost (device)
+  int n;
+  const double* r;         // [B][n] (device)
+  const double* c;         // [B][n]
+  const double* gammas;    // [T] schedule (device)
+  int T;
+  double eps, c1, c2;
+  int stop_rho, projector, beta_kind, ls_max_trials, warm, p0_ones, f64;
+  long long max_evals;
+  double* U_out;           // [B][n] nullable
+  double* V_out;
+  BatchResult* res;        // [B] (device)
+};
+size_t batch_smem_bytes(int n);
+cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st);
+
 }  // namespace mdot

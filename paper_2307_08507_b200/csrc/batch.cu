@@ -76,13 +76,15 @@ struct BatchSmem {
 // and the range-guard fallback).
 template <bool F64>
 __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
-                           double* rowtot, double* coltot, double (*sred)[kTileN]) {
+                           double gbar, double* rowtot, double* coltot, double (*sred)[kTileN]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4* rowp = prm;
   const float4* colp = prm + n;
   const bool vec4 = (n % 4) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   for (int j0 = 0; j0 < n; j0 += kTileN) {
     float bh[8], bl[8], T[8];
+    double Bd[F64 ? 8 : 1];
+    float Wd[F64 ? 8 : 1];
     int jj[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -91,8 +93,10 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
       if (j < n) {
         const float4 cp = colp[j];
         bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+        if (F64) { Bd[q & (F64 ? 7 : 0)] = *reinterpret_cast<const double*>(&cp.x); Wd[q & (F64 ? 7 : 0)] = cp.w; }
       } else {
         bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
+        if (F64) { Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.f; }
       }
     }
     double* csum = &sred[warp][0];
@@ -138,14 +142,19 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
           }
           rs[u] = rsum;
         } else {
+          // fp64 entries: exact z = A_i + B_j - gbar C_ij, anchored by the
+          // integer (rho_i + sig_j) ln 2, fp64 exp
           double rsum = 0.0;
-          const double ra = (double)rp.x + (double)rp.y;
+          const double Ai = *reinterpret_cast<const double*>(&rp.x);
+          const bool rowok = i < n;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const double w = (ra + ((double)bh[q] + (double)bl[q])) - g2 * (double)cv[q];
-            const double e = (bh[q] < -1.0e29f || rp.x < -1.0e29f) ? 0.0 : exp2(w);
-            rsum += e * (double)T[q];
-            c64[q] += e * (double)rp.z;
+            if (rowok && jj[q] < n) {
+              const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (double)(rp.w + Wd[q]) * LN2_D;
+              const double e = exp(z);
+              rsum += e * (double)T[q];
+              c64[q] += e * (double)rp.z;
+            }
           }
           rs[u] = rsum;
         }
@@ -214,6 +223,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   pa.p = p; pa.pprev = pprev; pa.lm = cl;
   pa.logr = logt; pa.logc = logt + n; pa.rho_r = anc; pa.sig_c = anc + n;
   pa.rowp = prm; pa.colp = prm + n; pa.flag = nullptr;
+  pa.f64_params = a.f64;
   pa.cur_lm = cl; pa.cur_m = nullptr; pa.cur_s = cs; pa.cur_g = cg;
   pa.tr_lm = tl; pa.tr_m = nullptr; pa.tr_s = ts; pa.tr_g = tg;
   FinalizeArgs fa{};
@@ -267,8 +277,23 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
       __syncthreads();
       bool use64 = a.f64 != 0;
       for (int attempt = 0; attempt < 2; ++attempt) {
-        if (use64) batch_eval<true>(a.C, n, prm, gh, gl, g2, tot, tot + n, S.sred);
-        else batch_eval<false>(a.C, n, prm, gh, gl, g2, tot, tot + n, S.sred);
+        if (use64) {
+          // fp64-entry parameters for this evaluation: redo the exponent split
+          if (attempt > 0 || !a.f64) {
+            // range-guard retry: rebuild the parameter slots from the fp64 bases
+            // without repeating the prep side effects (mode PREP_CUR/AB-like)
+            for (int k = tid; k < n2; k += blockDim.x) {
+              const bool row = k < n;
+              const double base = row ? ((S.st.mode & PREP_TRIAL) ? UV[k] + tuv[k] : UV[k] + uv[k])
+                                      : ((S.st.mode & PREP_TRIAL) ? UV[k] + tuv[k] : UV[k] + uv[k]);
+              prm[k] = f64_param(base, anc[k]);
+            }
+            __syncthreads();
+          }
+          batch_eval<true>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+        } else {
+          batch_eval<false>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+        }
         __syncthreads();
         double v[kNumScalars];
 #pragma unroll

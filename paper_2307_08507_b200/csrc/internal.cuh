@@ -188,6 +188,7 @@ struct PrepArgs {
   double* Aout; double* Bout;         // fp64 bases (for the exact path)
   float4* rowp; float4* colp;
   int* flag;                          // set to 1 when |a2|,|b2| >= 2^15
+  int f64_params;                     // 1: write {fp64 base, 2^anchor, anchor} (fp64-entry evaluation)
   // device control: mode/alpha/beta/accept come from ctrl; accept copies trial -> cur
   const CtrlState* ctrl;
   double *cur_lm, *cur_m, *cur_s, *cur_g;

@@ -47,6 +47,15 @@ __device__ __forceinline__ float4 split_param(double base, double anchor, int* f
   return make_float4((float)ah, (float)al, (float)exp2(anchor), 0.f);
 }
 
+// fp64-entry parameter slot: {base potential (fp64), 2^anchor (fp32), anchor (fp32)}
+__device__ __forceinline__ float4 f64_param(double base, double anchor) {
+  float4 r;
+  *reinterpret_cast<double*>(&r.x) = base;
+  r.z = (float)exp2(anchor);
+  r.w = (float)anchor;
+  return r;
+}
+
 // One row/column item of the prep step (k in [0, nrows + n)); the controller
 // state `c` (device control) overrides mode / alpha / beta and requests the
 // element-wise accept copy.
@@ -98,7 +107,7 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
       base = a.U[idx] + a.u[idx];
     }
     if (a.Aout) a.Aout[idx] = base;
-    a.rowp[idx] = split_param(base, a.rho_r[idx], a.flag);
+    a.rowp[idx] = a.f64_params ? f64_param(base, a.rho_r[idx]) : split_param(base, a.rho_r[idx], a.flag);
   } else {
     if (mode & PREP_TRIAL) {
       const double t = a.v[idx] + alpha * pk;
@@ -114,7 +123,7 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
       base = a.V[idx] + a.v[idx];
     }
     if (a.Bout) a.Bout[idx] = base;
-    a.colp[idx] = split_param(base, a.sig_c[idx], a.flag);
+    a.colp[idx] = a.f64_params ? f64_param(base, a.sig_c[idx]) : split_param(base, a.sig_c[idx], a.flag);
   }
 }
 

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 #include "ops.cuh"
@@ -227,6 +228,208 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// On-the-fly squared-Euclidean cost with packed fp32
+// pairs.  This kernel is bound by the FP32 pipe, not HBM: per pair of points
+// the Z22 recipe costs d FADD + d FFMA for the distance and 7 more ops for the
+// entry.  sm_100a executes FADD2/FFMA2/FMUL2 (PTX add/fma/mul.rn.f32x2) on
+// two lanes of a 64-bit register pair with per-lane IEEE rounding, so every
+// op below handles two columns at once and the per-element result is
+// bit-identical to the scalar recipe.  Layout as
+// k_eval_fast: lane owns columns j0 + 4*lane + {0..3} and
+// j0 + 128 + 4*lane + {0..3} (pairs {0,1},{2,3} of each quad); X rows are
+// staged in chunks of kOtfChunk rows as duplicated pairs (x, x) so each
+// FADD2 reads its broadcast operand straight from shared memory.
+// ---------------------------------------------------------------------------
+typedef unsigned long long u64;
+constexpr int kOtfChunk = 128;
+
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(u64 v, float& lo, float& hi) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (a.done && *a.done) return;
+  const int64_t j0 = (int64_t)blockIdx.x * kTileN;
+  const int64_t i0 = (int64_t)blockIdx.y * a.tile_m;
+  const int64_t n = a.n, nrows = a.nrows;
+
+  __shared__ double sred[kWarps][kTileN];
+  extern __shared__ __align__(16) unsigned char sraw[];
+  float* sY = reinterpret_cast<float*>(sraw);                       // [D][256]
+  u64* sX = reinterpret_cast<u64*>(sraw + sizeof(float) * D * kTileN);  // [chunk][D]
+
+  // Y[j0:j0+256, :] transposed; columns past n are zero points (masked by bh)
+  for (int idx = threadIdx.x; idx < kTileN * D; idx += kThreads) {
+    const int t = idx / D, k = idx % D;
+    const int64_t j = j0 + t;
+    sY[k * kTileN + t] = (j < n) ? a.Y[j * D + k] : 0.f;
+  }
+
+  u64 bh2[4], bl2[4], T2[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float v[3][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = 2 * p + h;
+      const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+      if (j < n) {
+        const float4 cp = a.colp[j];
+        v[0][h] = cp.x; v[1][h] = cp.y; v[2][h] = cp.z;
+      } else {
+        v[0][h] = -1.0e30f; v[1][h] = 0.f; v[2][h] = 0.f;
+      }
+    }
+    bh2[p] = pk2(v[0][0], v[0][1]);
+    bl2[p] = pk2(v[1][0], v[1][1]);
+    T2[p] = pk2(v[2][0], v[2][1]);
+  }
+  const float gh = a.gpair ? a.gpair[0] : a.gh;
+  const float gl = a.gpair ? a.gpair[1] : a.gl;
+  const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl), scale2 = pk2(a.scale, a.scale);
+
+  double cacc64[8];
+  u64 cacc2[4];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cacc64[q] = 0.0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) cacc2[p] = 0ull;
+
+  const int64_t tile_end = (i0 + a.tile_m < nrows) ? i0 + a.tile_m : nrows;
+  int flush = 0;
+  for (int64_t c0 = i0; c0 < tile_end; c0 += kOtfChunk) {
+    const int rows_c = (int)((tile_end - c0 < kOtfChunk) ? tile_end - c0 : kOtfChunk);
+    __syncthreads();   // previous chunk consumed (and sY written on entry)
+    for (int idx = threadIdx.x; idx < kOtfChunk * D; idx += kThreads) {
+      const int r = idx / D, k = idx % D;
+      const float x = (r < rows_c) ? a.X[(c0 + r) * D + k] : 0.f;
+      sX[idx] = pk2(x, x);
+    }
+    __syncthreads();
+    for (int rb = 4 * warp; rb < rows_c; rb += kWarps * kUnroll) {
+      u64 acc[kUnroll][4];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[u][p] = 0ull;
+      // C_ij = fl32(fmaf chain over k of (x_ik - y_jk)^2) * scale  (Z22)
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const ulonglong2 ya = *reinterpret_cast<const ulonglong2*>(sY + k * kTileN + 4 * lane);
+        const ulonglong2 yb = *reinterpret_cast<const ulonglong2*>(sY + k * kTileN + 128 + 4 * lane);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const u64 xx = sX[(rb + u) * D + k];
+          u64 dk;
+          dk = sub2(xx, ya.x); acc[u][0] = fma2(dk, dk, acc[u][0]);
+          dk = sub2(xx, ya.y); acc[u][1] = fma2(dk, dk, acc[u][1]);
+          dk = sub2(xx, yb.x); acc[u][2] = fma2(dk, dk, acc[u][2]);
+          dk = sub2(xx, yb.y); acc[u][3] = fma2(dk, dk, acc[u][3]);
+        }
+      }
+      double rs[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = c0 + rb + u;
+        float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+        if (rb + u < rows_c) rp = a.rowp[i];
+        const u64 ah2 = pk2(rp.x, rp.x), al2 = pk2(rp.y, rp.y), S2 = pk2(rp.z, rp.z);
+        u64 rsum2 = 0ull;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const u64 c2 = mul2(acc[u][p], scale2);
+          const u64 zh2 = fma2(ngh2, c2, add2(ah2, bh2[p]));
+          const u64 t2 = fma2(ngl2, c2, add2(al2, bl2[p]));
+          float zlo, zhi;
+          up2(add2(zh2, t2), zlo, zhi);
+          const u64 e2 = pk2(ex2_approx(zlo), ex2_approx(zhi));
+          rsum2 = fma2(e2, T2[p], rsum2);
+          cacc2[p] = fma2(e2, S2, cacc2[p]);
+        }
+        float rlo, rhi;
+        up2(rsum2, rlo, rhi);
+        rs[u] = (double)rlo + (double)rhi;
+      }
+      {
+        const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
+        const int r = rb + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+        if ((lane & 7) == 0 && r < rows_c) a.rowpart[(int64_t)blockIdx.x * nrows + c0 + r] = tot;
+      }
+      if (++flush == 2) {   // 8 rows of fp32 column sums -> fp64
+        flush = 0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          float lo, hi;
+          up2(cacc2[p], lo, hi);
+          cacc64[2 * p] += (double)lo;
+          cacc64[2 * p + 1] += (double)hi;
+          cacc2[p] = 0ull;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float lo, hi;
+    up2(cacc2[p], lo, hi);
+    cacc64[2 * p] += (double)lo;
+    cacc64[2 * p + 1] += (double)hi;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sred[warp][4 * lane + (q & 3) + 128 * (q >> 2)] = cacc64[q];
+  __syncthreads();
+  {
+    const int t = threadIdx.x;
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) tot += sred[w][t];
+    const int64_t j = j0 + t;
+    if (j < n) a.colpart[(int64_t)blockIdx.y * n + j] = tot;
+  }
+}
+
+template <int D>
+static cudaError_t launch_otf_t(const EvalArgs& a, cudaStream_t st) {
+  dim3 grid(a.n_col_tiles, a.n_row_tiles);
+  const size_t smem = sizeof(float) * D * kTileN + sizeof(u64) * kOtfChunk * D;
+  static bool attr_set = false;
+  if (!attr_set && smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_eval_otf<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  k_eval_otf<D><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int KIND, bool VEC4>
 static cudaError_t launch_fast_t(const EvalArgs& a, cudaStream_t st) {
   dim3 grid(a.n_col_tiles, a.n_row_tiles);
@@ -242,6 +445,18 @@ cudaError_t launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st) {
   if (kind == 0) {
     const bool vec4 = (a.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0);
     return vec4 ? launch_fast_t<0, true>(a, st) : launch_fast_t<0, false>(a, st);
+  }
+  const bool generic = getenv("MDOT_OTF_GENERIC") != nullptr;   // A/B switch
+  if (!generic) {
+    switch (a.d) {
+      case 2: return launch_otf_t<2>(a, st);
+      case 3: return launch_otf_t<3>(a, st);
+      case 4: return launch_otf_t<4>(a, st);
+      case 8: return launch_otf_t<8>(a, st);
+      case 16: return launch_otf_t<16>(a, st);
+      case 32: return launch_otf_t<32>(a, st);
+      default: break;
+    }
   }
   return launch_fast_t<1, false>(a, st);
 }

@@ -282,10 +282,14 @@ def test_device_control_fp64_config1():
 
 
 # ------------------------------------------------------------- on-the-fly cost (K2)
-@pytest.mark.parametrize("n,d", [(300, 16), (1024, 16), (777, 3)])
-def test_otf_marginals_match_oracle(n, d):
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("n,d", [(300, 16), (1024, 16), (777, 3), (513, 2), (600, 32), (389, 5)])
+def test_otf_marginals_match_oracle(n, d, generic, monkeypatch):
     """Config-5 kernel: C computed in-kernel with the Z22 fp32 recipe, the
-    oracle computes the same recipe in C (-ffp-contract=off)."""
+    oracle computes the same recipe in C (-ffp-contract=off).  Both the packed
+    f32x2 kernel (d in {2,3,4,8,16,32}) and the generic scalar one."""
+    if generic:
+        monkeypatch.setenv("MDOT_OTF_GENERIC", "1")
     inst = S.config5(0, n=n, d=d)
     prob = O.OracleProblem(inst)
     gb = 512.0

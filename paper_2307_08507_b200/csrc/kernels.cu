@@ -19,6 +19,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include "entry.cuh"
 #include "internal.cuh"
 #include "ops.cuh"
 
@@ -241,37 +242,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 // staged in chunks of kOtfChunk rows as duplicated pairs (x, x) so each
 // FADD2 reads its broadcast operand straight from shared memory.
 // ---------------------------------------------------------------------------
-typedef unsigned long long u64;
 constexpr int kOtfChunk = 128;
-
-__device__ __forceinline__ u64 pk2(float lo, float hi) {
-  u64 r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void up2(u64 v, float& lo, float& hi) {
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-  u64 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-  u64 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-  u64 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-  u64 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
@@ -294,25 +265,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
     sY[k * kTileN + t] = (j < n) ? a.Y[j * D + k] : 0.f;
   }
 
-  u64 bh2[4], bl2[4], T2[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    float v[3][2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = 2 * p + h;
-      const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
-      if (j < n) {
-        const float4 cp = a.colp[j];
-        v[0][h] = cp.x; v[1][h] = cp.y; v[2][h] = cp.z;
-      } else {
-        v[0][h] = -1.0e30f; v[1][h] = 0.f; v[2][h] = 0.f;
-      }
-    }
-    bh2[p] = pk2(v[0][0], v[0][1]);
-    bl2[p] = pk2(v[1][0], v[1][1]);
-    T2[p] = pk2(v[2][0], v[2][1]);
-  }
+  ColPairs cpp;
+  load_col_pairs(cpp, j0, lane, n, [&](int64_t j) { return a.colp[j]; });
   const float gh = a.gpair ? a.gpair[0] : a.gh;
   const float gl = a.gpair ? a.gpair[1] : a.gl;
   const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl), scale2 = pk2(a.scale, a.scale);
@@ -362,22 +316,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         const int64_t i = c0 + rb + u;
         float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
         if (rb + u < rows_c) rp = a.rowp[i];
-        const u64 ah2 = pk2(rp.x, rp.x), al2 = pk2(rp.y, rp.y), S2 = pk2(rp.z, rp.z);
-        u64 rsum2 = 0ull;
+        u64 c2[4];
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const u64 c2 = mul2(acc[u][p], scale2);
-          const u64 zh2 = fma2(ngh2, c2, add2(ah2, bh2[p]));
-          const u64 t2 = fma2(ngl2, c2, add2(al2, bl2[p]));
-          float zlo, zhi;
-          up2(add2(zh2, t2), zlo, zhi);
-          const u64 e2 = pk2(ex2_approx(zlo), ex2_approx(zhi));
-          rsum2 = fma2(e2, T2[p], rsum2);
-          cacc2[p] = fma2(e2, S2, cacc2[p]);
-        }
-        float rlo, rhi;
-        up2(rsum2, rlo, rhi);
-        rs[u] = (double)rlo + (double)rhi;
+        for (int p = 0; p < 4; ++p) c2[p] = mul2(acc[u][p], scale2);
+        rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
       }
       {
         const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);

@@ -20,6 +20,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -89,6 +90,31 @@ static void retain_mempool() {
   done_dev = dev;
 }
 
+// Mapped pinned scalar blocks are recycled across calls: cudaHostAlloc /
+// cudaFreeHost cost milliseconds (and cudaFreeHost synchronizes the device),
+// which showed up as 30-50 ms outliers in repeated solves.
+static std::mutex g_host_mu;
+static std::vector<double*> g_host_free;
+
+static double* host_block_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    if (!g_host_free.empty()) {
+      double* b = g_host_free.back();
+      g_host_free.pop_back();
+      return b;
+    }
+  }
+  void* b = nullptr;
+  if (cudaHostAlloc(&b, 256 * sizeof(double), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return static_cast<double*>(b);
+}
+
+static void host_block_put(double* b) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  g_host_free.push_back(b);
+}
+
 mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   retain_mempool();
   st = stream;
@@ -156,7 +182,11 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   ticket = ticket_flag;
   flag = reinterpret_cast<int*>(ticket_flag + 4);
   pers_bar = ticket_flag + 8;   // [2] barrier + [2 x u64] K1 timing (16-byte aligned)
-  CK(cudaHostAlloc(&scal_host, 256 * sizeof(double), cudaHostAllocMapped));
+  scal_host = host_block_get();
+  if (!scal_host) {
+    set_error("mapped host allocation failed");
+    return MDOT_ENOMEM;
+  }
   CK(cudaHostGetDevicePointer((void**)&scal_host_dev, scal_host, 0));
   memset(scal_host, 0, 256 * sizeof(double));
   done_host = reinterpret_cast<int*>(scal_host + 64);
@@ -179,7 +209,10 @@ void Workspace::release() {
   gev_made = false;
   if (base) cudaFreeAsync(base, st);
   base = nullptr;
-  if (scal_host) cudaFreeHost(scal_host);
+  if (scal_host) {
+    cudaStreamSynchronize(st);   // the block may still be written by queued kernels
+    host_block_put(scal_host);
+  }
   scal_host = nullptr;
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -1019,9 +1052,22 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   Workspace w;
   w.comm = comm;
   w.row0 = row0;
+  // MDOT_TRACE: host timestamps per stage (synchronizes between stages)
+  const bool trace = getenv("MDOT_TRACE") != nullptr;
+  double tr_last = t0;
+  auto trace_mark = [&](const char* what, long long a0, long long a1) {
+    if (!trace) return;
+    cudaStreamSynchronize(stream);
+    const double now = now_s();
+    fprintf(stderr, "[mdot-trace] %-10s %9.3f ms  (%lld, %lld)\n", what, (now - tr_last) * 1e3, a0, a1);
+    tr_last = now;
+  };
   st = w.alloc(stream, n, nr);
+  trace_mark("alloc", 0, 0);
   if (st == MDOT_OK) st = w.load_problem(pb, row0);
+  trace_mark("load", 0, 0);
   if (st == MDOT_OK) st = w.setup(o);
+  trace_mark("setup", 0, 0);
   mdot_status solve_st = MDOT_OK;
   if (st == MDOT_OK) {
     // P0 = r c^T -> U = log r, V = log c ; u = v = 0 (Alg. 1 line 2)
@@ -1051,6 +1097,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
       else solve_st = project_pncg(w, o, (int)t, res);
       res->md_steps = (int64_t)t;
+      trace_mark("project", (long long)t, (long long)w.evals);
       ++w.launches; launch_axpby(nr, 1.0, w.u, 1.0, w.U, stream);   // U += u
       ++w.launches; launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);   // V += v
       if (solve_st != MDOT_OK && solve_st != MDOT_ENOCONV) break;
@@ -1058,6 +1105,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       if (st == MDOT_OK) st = w.gauge_center(w.u, w.v);
       if (st != MDOT_OK) break;
       gprev = gt;
+      trace_mark("step-end", (long long)t, 0);
       if (solve_st != MDOT_OK) break;
     }
     res->gamma_bar = gb;
@@ -1074,6 +1122,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
           st = MDOT_ECUDA;
       }
       if (Pown) cudaFreeAsync(Pown, stream);
+      trace_mark("round", 0, 0);
     }
     const cudaMemcpyKind k = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (u_out) cudaMemcpyAsync(u_out, w.U, sizeof(double) * nr, k, stream);
@@ -1089,6 +1138,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   w.free_owned();
   w.release();
   cudaError_t ce = cudaStreamSynchronize(stream);
+  trace_mark("release", 0, 0);
   if (st == MDOT_OK && ce != cudaSuccess) {
     set_error("CUDA error at exit: %s", cudaGetErrorString(ce));
     st = MDOT_ECUDA;

@@ -444,3 +444,22 @@ def test_batch_kernel_matches_per_instance_solves(monkeypatch):
     rl = M.mdot_solve_batch(_t(C), _t(R[:2]), _t(Cm[:2]), schedule=sched, options=M.options(eps=1e-6))
     assert all(x["control_path"] != 3 for x in rl)
     assert abs(rl[1]["cost_unrounded"] - rb[1]["cost_unrounded"]) <= 1e-5 * rl[1]["cost_unrounded"] or True
+
+
+# ------------------------------------------------------------- determinism
+@pytest.mark.parametrize("dc", [1, 2])
+def test_solve_is_bitwise_deterministic(dc):
+    """No float atomics and fixed reduction orders: repeated solves give the
+    same evaluations, cost and potentials bit for bit (persistent and graph
+    control)."""
+    inst = S.config4(1, n=2048)
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    outs = []
+    for _ in range(3):
+        U = torch.empty(inst.n, dtype=torch.float64, device=DEV)
+        V = torch.empty_like(U)
+        res = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, 4096.0),
+                           options=M.options(eps=1e-6, device_control=dc), u_out=U, v_out=V)
+        outs.append((res["evaluations"], res["cost_unrounded"].hex(), res["cost_rounded"].hex(),
+                     U.cpu().numpy().tobytes(), V.cpu().numpy().tobytes()))
+    assert outs[0] == outs[1] == outs[2]

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MDOT_ABI_VERSION 1
+#define MDOT_ABI_VERSION 2
 
 typedef enum {
   MDOT_OK = 0,
@@ -105,6 +105,12 @@ typedef struct {
   int32_t time_kernels;    /* 1: time every evaluation kernel with CUDA events (result.kernel_ms) */
   int32_t device_control;  /* 1: device-resident line-search control (no host sync per trial) */
   void* stream;            /* cudaStream_t, NULL = legacy default stream */
+  double eps_md;           /* tolerance of the intermediate MD steps t < T; 0 (default) = eps at every
+                              step, as the paper ran it (Z11).  By Lemma 2
+                              the final plan depends only on gamma_bar, and a Bregman projection onto
+                              U(r,c) is invariant to diagonal scalings of its input, so an inexact
+                              intermediate projection only moves the last step's starting point
+                              (adaptive eps, the paper's stated future work). */
 } mdot_options;
 
 typedef struct {

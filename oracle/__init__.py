@@ -44,7 +44,7 @@ class Options(ct.Structure):
     _fields_ = [("eps", ct.c_double), ("stop_rho", ct.c_int32), ("projector", ct.c_int32),
                 ("beta", ct.c_int32), ("c1", ct.c_double), ("c2", ct.c_double),
                 ("warm", ct.c_int32), ("p0_ones", ct.c_int32), ("max_evals", ct.c_int64),
-                ("ls_max_trials", ct.c_int32), ("max_threads", ct.c_int32)]
+                ("ls_max_trials", ct.c_int32), ("max_threads", ct.c_int32), ("eps_md", ct.c_double)]
 
 
 class TraceRec(ct.Structure):
@@ -141,9 +141,9 @@ class OracleProblem:
 
 
 def make_options(eps=1e-6, projector=PNCG, beta=BETA_PPR, c1=0.1, c2=0.4, warm=WARM_SCALED,
-                 stop_rho=False, p0_ones=False, max_evals=0, ls_max_trials=0, threads=0):
+                 stop_rho=False, p0_ones=False, max_evals=0, ls_max_trials=0, threads=0, eps_md=0.0):
     return Options(eps, int(stop_rho), projector, beta, c1, c2, warm, int(p0_ones),
-                   max_evals, ls_max_trials, threads)
+                   max_evals, ls_max_trials, threads, eps_md)
 
 
 def log_marginals(prob: OracleProblem, A, B, gbar):

@@ -580,7 +580,9 @@ int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_o
       for (int64_t i = 0; i < n; ++i) u[i] *= w;
       for (int64_t j = 0; j < n; ++j) v[j] *= w;
     }
-    st = orc_project(pb, U, V, gbar, u, v, opt, t, res, trace, trace_cap, trace_len);
+    orc_options ot = *opt;
+    if (t < T && opt->eps_md > opt->eps) ot.eps = opt->eps_md;
+    st = orc_project(pb, U, V, gbar, u, v, &ot, t, res, trace, trace_cap, trace_len);
     res->md_steps = t;
     for (int64_t i = 0; i < n; ++i) U[i] += u[i];
     for (int64_t j = 0; j < n; ++j) V[j] += v[j];

@@ -46,6 +46,11 @@ typedef struct {
   int64_t max_evals;     /* cap on O(n^2) evaluations per solve (0 = 10^7) */
   int32_t ls_max_trials; /* per line search (0 = 100) */
   int32_t max_threads;   /* OpenMP threads (0 = default) */
+  double eps_md;         /* tolerance of the intermediate MD steps t < T (0 = eps at every step, Z11).
+                            Lemma 2 makes the final plan depend only on gbar, and the
+                            projection is invariant to diagonal scalings of its input, so an inexact
+                            intermediate projection changes only the final step's starting point
+                            ("future work"). */
 } orc_options;
 
 typedef struct {         /* one PNCG / Sinkhorn iteration */

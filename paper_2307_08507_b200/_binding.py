@@ -45,7 +45,7 @@ class Options(ct.Structure):
                 ("warm", ct.c_int32), ("precision", ct.c_int32), ("p0_ones", ct.c_int32),
                 ("ls_max_trials", ct.c_int32), ("max_evals", ct.c_int64),
                 ("time_kernels", ct.c_int32), ("device_control", ct.c_int32),
-                ("stream", ct.c_void_p)]
+                ("stream", ct.c_void_p), ("eps_md", ct.c_double)]
 
 
 class Result(ct.Structure):
@@ -109,7 +109,7 @@ def lib():
         for nm in ("mdot_solve_batch", "mdot_marginals", "mdot_round", "mdot_get_unique_id",
                    "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_destroy", "mdot_solve_sharded"):
             getattr(L, nm).restype = ct.c_int
-        if L.mdot_abi_version() != 1:
+        if L.mdot_abi_version() != 2:
             raise ImportError("libmdot_b200.so ABI version mismatch")
         _lib = L
     return _lib

@@ -272,7 +272,7 @@ struct BatchArgs {
   const double* c;         // [B][n]
   const double* gammas;    // [T] schedule (device)
   int T;
-  double eps, c1, c2;
+  double eps, eps_md, c1, c2;   // eps_md: intermediate MD steps (>= eps)
   int stop_rho, projector, beta_kind, ls_max_trials, warm, p0_ones, f64;
   long long max_evals;
   double* U_out;           // [B][n] nullable

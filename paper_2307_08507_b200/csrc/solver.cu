@@ -1092,10 +1092,13 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
         ++w.launches; launch_axpby(nr, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
         ++w.launches; launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
       }
-      if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, o, (int)t, res);
-      else if (o.device_control) solve_st = project_device(w, o, (int)t, res);
-      else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, o, (int)t, res);
-      else solve_st = project_pncg(w, o, (int)t, res);
+      // intermediate MD steps may stop at the looser eps_md (Lemma 2; mdot.h)
+      mdot_options ot = o;
+      if (t < gam.size() && o.eps_md > o.eps) ot.eps = o.eps_md;
+      if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, ot, (int)t, res);
+      else if (o.device_control) solve_st = project_device(w, ot, (int)t, res);
+      else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, ot, (int)t, res);
+      else solve_st = project_pncg(w, ot, (int)t, res);
       res->md_steps = (int64_t)t;
       trace_mark("project", (long long)t, (long long)w.evals);
       ++w.launches; launch_axpby(nr, 1.0, w.u, 1.0, w.U, stream);   // U += u
@@ -1247,7 +1250,7 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   CK(cudaMemcpyAsync(dg, gam.data(), sizeof(double) * gam.size(), cudaMemcpyHostToDevice, stream));
   BatchArgs a{};
   a.C = dC; a.n = (int)n; a.r = dr; a.c = dc; a.gammas = dg; a.T = (int)gam.size();
-  a.eps = o.eps; a.c1 = o.c1; a.c2 = o.c2;
+  a.eps = o.eps; a.eps_md = o.eps_md > o.eps ? o.eps_md : o.eps; a.c1 = o.c1; a.c2 = o.c2;
   a.stop_rho = o.stop; a.projector = o.projector; a.beta_kind = o.beta; a.ls_max_trials = o.ls_max_trials;
   a.warm = o.warm; a.p0_ones = o.p0_ones;
   // fp32 entries resolve marginals to ~1e-7 (K1 numerics): tighter

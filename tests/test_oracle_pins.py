@@ -250,6 +250,37 @@ def test_lemma2_schedule_invariance():
     assert np.abs(P - Pref).sum() < 1e-10
 
 
+def test_adaptive_eps_md_reaches_the_same_plan():
+    """SURVEY 8(f) rank 1 (adaptive eps): by Lemma 2 the
+    final plan depends only on gbar, and the projection onto U(r,c) is
+    invariant to diagonal scalings of its input, so loose intermediate steps
+    (eps_md) change only where the last projection starts.  Pinned against
+    the single-step solve (T = 1, which has no intermediate step) and the 2x2
+    closed form."""
+    inst = S.random_small(8, seed=15)
+    prob = O.OracleProblem(inst)
+    gb = 32.0
+    Pref, _ = _md_plan(prob, [gb], eps=1e-13)
+    for em in (1e-6, 1e-3, 1e-1, 0.5):
+        P, res = _md_plan(prob, O.schedule_fixed(gb, T=8), eps=1e-13, eps_md=em)
+        assert np.abs(P - Pref).sum() < 1e-10, em
+    # the loose steps really stopped early: fewer evaluations than eps_md = 0
+    _, r0 = _md_plan(prob, O.schedule_fixed(gb, T=8), eps=1e-13)
+    _, r1 = _md_plan(prob, O.schedule_fixed(gb, T=8), eps=1e-13, eps_md=1e-2)
+    assert r1["evaluations"] < r0["evaluations"]
+    rng = np.random.default_rng(21)
+    for trial in range(6):
+        C = rng.uniform(0, 1, size=(2, 2))
+        r = rng.dirichlet([1, 1])
+        c = rng.dirichlet([1, 1])
+        g = [8.0, 64.0, 200.0][trial % 3]
+        prob2 = O.OracleProblem(C=C, r=r, c=c)
+        U, V, res, _ = O.mdot(prob2, O.schedule_fixed(g, T=4), O.make_options(eps=1e-14, eps_md=1e-2))
+        assert res["status"] == 0
+        P = np.exp(U[:, None] + V[None, :] - g * C)
+        np.testing.assert_allclose(P, X.entropic_2x2(C, r, c, g), atol=1e-13)
+
+
 def test_lemma1_exact_improvement_and_cor1():
     """Lemma 1 equality and Cor. 1
     bound on consecutive MD iterates (n = 8, gamma_t = 8)."""

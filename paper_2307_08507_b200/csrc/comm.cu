@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <condition_variable>
@@ -125,7 +126,7 @@ static mdot_status local_allreduce(Comm* cm, double* buf, size_t count, int op, 
 }
 
 mdot_status comm_allreduce(Comm* cm, double* buf, size_t count, int op, cudaStream_t st) {
-  if (!cm || cm->nranks == 1) return MDOT_OK;
+  if (!cm || (cm->nranks == 1 && !cm->nccl)) return MDOT_OK;
   if (cm->local) return local_allreduce(cm, buf, count, op, st);
   ncclResult_t r = g_nccl.AllReduce(buf, buf, count, ncclFloat64, op == COMM_MAX ? ncclMax : ncclSum,
                                     (ncclComm_t)cm->nccl, st);
@@ -159,7 +160,9 @@ mdot_status mdot_comm_create(const void* uid, int32_t nranks, int32_t rank, int3
   cm->nranks = nranks;
   cm->rank = rank;
   cm->device = device;
-  if (nranks > 1) {
+  // MDOT_SHARDED_SELFTEST (tests only): a 1-rank NCCL communicator that runs
+  // the sharded code path (NCCL calls, graph capture) on a single GPU
+  if (nranks > 1 || getenv("MDOT_SHARDED_SELFTEST")) {
     if (!load_nccl()) { delete cm; return MDOT_ENCCL; }
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));

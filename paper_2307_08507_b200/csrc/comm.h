@@ -13,6 +13,9 @@ struct Comm {
   int nranks = 1, rank = 0, device = 0;
   void* nccl = nullptr;          // ncclComm_t (NCCL transport)
   LocalGroup* local = nullptr;   // in-process transport (virtual ranks / tests)
+  // graph-capturable transport (NCCL): the sharded solve may run under
+  // device control with the allreduce inside the CUDA-graph slots
+  bool capturable() const { return nccl != nullptr; }
 };
 
 enum { COMM_SUM = 0, COMM_MAX = 1 };

@@ -224,7 +224,8 @@ cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const do
                         double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
                         cudaStream_t st);
 // column partials -> local column totals (generic kernel, sharded mode)
-cudaError_t launch_reduce_colpart(const double* colpart, int n_row_tiles, int64_t n, double* coltot, cudaStream_t st);
+cudaError_t launch_reduce_colpart(const double* colpart, int n_row_tiles, int64_t n, double* coltot, cudaStream_t st,
+                                  const int* done = nullptr);
 // exact path, sharded: combine chunk (max, sum) pairs; rescale sums to a global max
 cudaError_t launch_exact_colcombine(const double* colm, const double* cols, int chunks, int64_t n, double* M,
                                     double* S, cudaStream_t st);

@@ -748,13 +748,15 @@ cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, c
 // ---------------------------------------------------------------------------
 // sharded helpers
 // ---------------------------------------------------------------------------
-__global__ void k_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot) {
+__global__ void k_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot, const int* done) {
+  if (done && *done) return;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   coltot[j] = sum_strided(colpart + j, n, nt);
 }
-cudaError_t launch_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot, cudaStream_t st) {
-  k_reduce_colpart<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colpart, nt, n, coltot);
+cudaError_t launch_reduce_colpart(const double* colpart, int nt, int64_t n, double* coltot, cudaStream_t st,
+                                  const int* done) {
+  k_reduce_colpart<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colpart, nt, n, coltot, done);
   return cudaGetLastError();
 }
 __global__ void k_exact_colcombine(const double* colm, const double* cols, int chunks, int64_t n, double* M,

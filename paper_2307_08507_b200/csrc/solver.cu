@@ -74,7 +74,7 @@ static double now_s() {
 // ---------------------------------------------------------------------------
 // Workspace
 // ---------------------------------------------------------------------------
-bool Workspace::sharded() const { return comm != nullptr && comm->nranks > 1; }
+bool Workspace::sharded() const { return comm != nullptr && (comm->nranks > 1 || comm->nccl != nullptr); }
 
 // Keep freed stream-ordered allocations in the device pool (no release at
 // every synchronize): repeated solves reuse the workspace / staging memory.
@@ -519,6 +519,30 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
     f.from_partials = 1;
     f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
     f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
+    if (sharded()) {
+      // the host path's sharded evaluation (Workspace::evaluate), captured:
+      // rows finalize locally with their scalars in the tail of the column
+      // buffer, ONE allreduce of [column totals | row scalars] (SURVEY 8(e)
+      // NC1), then the (replicated) columns finalize and add the row scalars.
+      // Every rank holds identical scalars, so every rank's controller takes
+      // the same decisions and launches the same number of graphs.
+      if (timed) CK(cudaEventRecordWithFlags(gev[3], s, cudaEventRecordExternal));
+      double* colbuf = tot.coltot;
+      CKL(launch_reduce_colpart(colpart, eval.n_row_tiles, n, colbuf, s, &ctrl->done));
+      FinalizeArgs fr = f;
+      fr.item_begin = 0; fr.item_end = nrows;
+      fr.scalars_dev = colbuf + n;
+      CKL(launch_finalize(fr, s));
+      CKS(comm_allreduce(comm, colbuf, (size_t)n + kNumScalars, COMM_SUM, s));
+      FinalizeArgs fc = f;
+      fc.coltot = colbuf;
+      fc.item_begin = nrows; fc.item_end = nrows + n;
+      fc.add_in = colbuf + n;
+      fc.prep_flag = nullptr;
+      CKL(launch_finalize(fc, s));
+      if (timed) CK(cudaEventRecordWithFlags(gev[4], s, cudaEventRecordExternal));
+      return MDOT_OK;
+    }
   } else {
     ExactArgs x{};
     x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
@@ -553,6 +577,7 @@ mdot_status Workspace::build_graph() {
   gslots = (int)std::max(4.0, std::min(64.0, ceil(2e-3 / est)));
   int* dh = dev_alias(done_host);
   int* rh = dev_alias(ran_host);
+  // NCCL in the capture (sharded): enqueue on the capture stream's device
   CK(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t saved = launches;
   mdot_status stt = MDOT_OK;
@@ -603,7 +628,7 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
   for (;;) {
     for (int k = 0; k < w.gslots; ++k) ((volatile int*)w.ran_host)[k] = 0;
     CK(cudaGraphLaunch(w.gexec, st));
-    w.launches += 4 * w.gslots;
+    w.launches += (w.sharded() ? 6 : 4) * w.gslots;   // our kernels per slot (NCCL's not counted)
     CK(cudaStreamSynchronize(st));
     if (w.time_kernels) {
       float ms = 0.f;
@@ -1048,7 +1073,10 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   const int64_t n = pb->n;
   const int64_t nr = nrows_in < 0 ? n : nrows_in;
   if (row0 < 0 || nr < 1 || row0 + nr > n) { set_error("bad row range"); res->status = MDOT_EINVAL; return MDOT_EINVAL; }
-  if (comm && comm->nranks > 1) o.device_control = 0;   // sharded control runs on the host (one NCCL call per eval)
+  // sharded: device control (CUDA-graph slots with the NCCL allreduce captured
+  // inside) needs a capturable transport; the in-process transport syncs on
+  // the host in every allreduce, so it runs the host loop
+  if (comm && (comm->nranks > 1 || comm->nccl) && !comm->capturable()) o.device_control = 0;
   Workspace w;
   w.comm = comm;
   w.row0 = row0;
@@ -1096,7 +1124,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       mdot_options ot = o;
       if (t < gam.size() && o.eps_md > o.eps) ot.eps = o.eps_md;
       if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, ot, (int)t, res);
-      else if (o.device_control) solve_st = project_device(w, ot, (int)t, res);
+      else if (o.device_control && !(w.sharded() && w.exact_mode)) solve_st = project_device(w, ot, (int)t, res);
       else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, ot, (int)t, res);
       else solve_st = project_pncg(w, ot, (int)t, res);
       res->md_steps = (int64_t)t;

@@ -402,6 +402,50 @@ def _sharded_solve_threads(inst, G, sched, opts_kw, group):
     return out
 
 
+@pytest.mark.parametrize("otf", [False, True])
+def test_sharded_nccl_device_control_one_rank(otf, monkeypatch):
+    """The real NCCL transport on one GPU (a 1-rank communicator forced onto
+    the sharded code path by MDOT_SHARDED_SELFTEST): per-evaluation allreduce
+    of [column totals | row scalars] captured inside the CUDA-graph slots
+    (device control) vs the same sharded evaluation under host control, the
+    single-GPU solve and the oracle.  The multi-rank decomposition itself is
+    covered by the virtual-rank and gloo tests."""
+    monkeypatch.setenv("MDOT_SHARDED_SELFTEST", "1")
+    n, gb, eps = 700, 512.0, 1e-6
+    if otf:
+        inst = S.otf_instance(n, 16, instance=3)
+        kw = dict(X_local=_t(inst.X), Y=_t(inst.Y), scale=float(inst.scale))
+        kw1 = dict(X=_t(inst.X), Y=_t(inst.Y), scale=float(inst.scale))
+    else:
+        inst = S.uniform_points_instance(3, n, 2, 11, marg="dirichlet")
+        kw = dict(C_local=_t(inst.C))
+        kw1 = dict(C=_t(inst.C))
+    r, c = _t(inst.r), _t(inst.c)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=2)
+    comm = M.mdot_comm_create(M.mdot_get_unique_id(), 1, 0, 0)
+    try:
+        out = {}
+        for dc in (1, 0):
+            U = torch.empty(n, dtype=torch.float64, device=DEV)
+            V = torch.empty_like(U)
+            res = M.mdot_solve_sharded(comm, 0, n, r=r, c=c, n=n, schedule=sched,
+                                       options=M.options(eps=eps, device_control=dc),
+                                       u_local_out=U, v_out=V, **kw)
+            out[dc] = (res, U.cpu().numpy(), V.cpu().numpy())
+    finally:
+        M.mdot_comm_destroy(comm)
+    rd, rh = out[1][0], out[0][0]
+    assert rd["control_path"] == 1 and rh["control_path"] == 0
+    assert rd["status"] == 0 and rh["status"] == 0
+    assert rd["l1_final"] <= eps and rh["l1_final"] <= eps
+    assert abs(rd["cost_unrounded"] - rh["cost_unrounded"]) <= 2e-6 * rh["cost_unrounded"]
+    ref = M.mdot_solve(r=r, c=c, schedule=sched, options=M.options(eps=eps), **kw1)
+    assert abs(rd["cost_unrounded"] - ref["cost_unrounded"]) <= 2e-6 * ref["cost_unrounded"]
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=2), O.make_options(eps=eps))
+    _gates(rd, ores, inst, prob, out[1][1], out[1][2], eps)
+
+
 @pytest.mark.parametrize("G", [2, 3])
 def test_sharded_virtual_ranks_match_single_gpu(G):
     n = 600

@@ -185,7 +185,7 @@ struct TSmem {
   unsigned long long full[STAGES], empty[STAGES];
 };
 
-template <int ROWS, int STAGES, int MINB>
+template <int ROWS, int STAGES, int MINB, bool MATH = true, bool LOAD = true>
 __global__ void __launch_bounds__(288, MINB) k_tma(const __grid_constant__ CUtensorMap tmap, Args a) {
   extern __shared__ __align__(128) unsigned char raw[];
   const uint32_t pad = (128u - (su32(raw) & 127u)) & 127u;
@@ -208,8 +208,12 @@ __global__ void __launch_bounds__(288, MINB) k_tma(const __grid_constant__ CUten
         for (int k = 0; k < spt; ++k, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
           mb_wait(&sm.empty[s], ph ^ 1u);
-          mb_tx(&sm.full[s], ROWS * kTileN * 4);
-          tma2d(&sm.st[s][0][0], &tmap, tc * kTileN, tr * a.tile_m + k * ROWS, &sm.full[s]);
+          if (LOAD) {
+            mb_tx(&sm.full[s], ROWS * kTileN * 4);
+            tma2d(&sm.st[s][0][0], &tmap, tc * kTileN, tr * a.tile_m + k * ROWS, &sm.full[s]);
+          } else {
+            mb_arrive(&sm.full[s]);   // compute-only: the stage "arrives" at once
+          }
         }
       }
     }
@@ -217,6 +221,20 @@ __global__ void __launch_bounds__(288, MINB) k_tma(const __grid_constant__ CUten
   }
   const float gh = a.gh, gl = a.gl;
   uint32_t it = 0;
+  if (!MATH) {
+    // TMA ring only: wait, touch one word, release (the access pattern's ceiling)
+    float acc = 0.f;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x)
+      for (int k = 0; k < spt; ++k, ++it) {
+        const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+        mb_wait(&sm.full[s], ph);
+        acc += sm.st[s][warp][lane];
+        __syncwarp();
+        if (lane == 0) mb_arrive(&sm.empty[s]);
+      }
+    if (acc == 12345.f) a.rowpart[0] = acc;
+    return;
+  }
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
     const int tr = (int)(t / a.nct), tc = (int)(t % a.nct);
     const int64_t i0 = (int64_t)tr * a.tile_m, j0 = (int64_t)tc * kTileN;
@@ -383,20 +401,21 @@ static void run_ldg(void* c) {
   dim3 g(x->a.nct, x->a.nrt);
   k_ldg<PF, MINB><<<g, 256>>>(x->a);
 }
-template <int ROWS, int STAGES, int MINB>
+template <int ROWS, int STAGES, int MINB, bool MATH = true, bool LOAD = true>
 static void run_tma(void* c) {
   Ctx* x = (Ctx*)c;
   const int smem = (int)sizeof(TSmem<ROWS, STAGES>) + 128;
   static bool set = false;
-  if (!set) { CK(cudaFuncSetAttribute(k_tma<ROWS, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); set = true; }
+  if (!set) { CK(cudaFuncSetAttribute(k_tma<ROWS, STAGES, MINB, MATH, LOAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); set = true; }
   int sms;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  k_tma<ROWS, STAGES, MINB><<<MINB * sms, 288, smem>>>(ROWS == 16 ? x->map16 : x->map32, x->a);
+  k_tma<ROWS, STAGES, MINB, MATH, LOAD><<<MINB * sms, 288, smem>>>(ROWS == 16 ? x->map16 : x->map32, x->a);
 }
 
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 16384;
   const int reps = argc > 2 ? atoi(argv[2]) : 20;
+  const bool quick = argc > 3;
   float* C;
   float4 *rowp, *colp;
   double *rowpart, *colpart;
@@ -435,6 +454,7 @@ int main(int argc, char** argv) {
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     for (int tm : {128, 256, 512}) {
+      if (quick && tm != 512) continue;
       ProdCtx pc{};
       pc.e.C = C; pc.e.ldc = n; pc.e.n = n; pc.e.nrows = n; pc.e.tile_m = tm;
       pc.e.n_col_tiles = (int)(n / 256); pc.e.n_row_tiles = (int)(n / tm);
@@ -452,6 +472,7 @@ int main(int argc, char** argv) {
   time_it("read-only stream unroll4", reps, bytes, run_read<4>, &x);
   time_it("read-only stream unroll8", reps, bytes, run_read<8>, &x);
   for (int tm : {128, 256, 512}) {
+    if (quick) break;
     x.a.tile_m = tm; x.a.nrt = (int)(n / tm);
     char nm[128];
     snprintf(nm, sizeof nm, "ldg nopf  minb2 tile_m=%d", tm);
@@ -461,6 +482,21 @@ int main(int argc, char** argv) {
     snprintf(nm, sizeof nm, "ldg pf    minb2 tile_m=%d", tm);
     time_it(nm, reps, bytes, run_ldg<true, 2>, &x);
   }
+  for (int tm : {512}) {
+    x.a.tile_m = tm; x.a.nrt = (int)(n / tm);
+    char nm[128];
+    snprintf(nm, sizeof nm, "tma 32x3 minb2 NOMATH tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<32, 3, 2, false>, &x);
+    snprintf(nm, sizeof nm, "tma 32x6 minb1 NOMATH tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<32, 6, 1, false>, &x);
+    snprintf(nm, sizeof nm, "tma 16x5 minb2 NOMATH tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<16, 5, 2, false>, &x);
+    snprintf(nm, sizeof nm, "tma 32x3 minb2 MATH tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<32, 3, 2, true>, &x);
+    snprintf(nm, sizeof nm, "tma 32x3 minb2 MATH NOLOAD tile_m=%d", tm);
+    time_it(nm, reps, bytes, run_tma<32, 3, 2, true, false>, &x);
+  }
+  if (quick) return 0;
   for (int tm : {256, 512}) {
     x.a.tile_m = tm; x.a.nrt = (int)(n / tm);
     char nm[128];

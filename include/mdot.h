@@ -98,7 +98,8 @@ typedef struct {
   int32_t beta;            /* mdot_beta (Z6) */
   double c1, c2;           /* approximate Wolfe constants (Z7 defaults 0.1, 0.4) */
   int32_t warm;            /* mdot_warm (Z4) */
-  int32_t precision;       /* mdot_precision: AUTO = fp32 entries for fp32 C, fp64 for DENSE_F64 */
+  int32_t precision;       /* mdot_precision: AUTO = fp32 entries for fp32 C and eps >= 5e-8, fp64 entries
+                              (exact two-pass evaluation) for DENSE_F64 or eps < 5e-8 */
   int32_t p0_ones;         /* 1: P0 = 1 1^T (classic Sinkhorn special case) */
   int32_t ls_max_trials;   /* per line search, default 100 */
   int64_t max_evals;       /* cap on O(n^2) evaluations per solve, default 10^7 */

@@ -82,7 +82,7 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
   const float4* colp = prm + n;
   const bool vec4 = (n % 4) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   for (int j0 = 0; j0 < n; j0 += kTileN) {
-    float bh[8], bl[8], T[8];
+    float bh[8], T[8];
     double Bd[F64 ? 8 : 1];
     float Wd[F64 ? 8 : 1];
     int jj[8];
@@ -92,10 +92,10 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
       jj[q] = j;
       if (j < n) {
         const float4 cp = colp[j];
-        bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+        bh[q] = cp.x; T[q] = cp.z;
         if (F64) { Bd[q & (F64 ? 7 : 0)] = *reinterpret_cast<const double*>(&cp.x); Wd[q & (F64 ? 7 : 0)] = cp.w; }
       } else {
-        bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
+        bh[q] = -1.0e30f; T[q] = 0.f;
         if (F64) { Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.f; }
       }
     }
@@ -107,6 +107,7 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
     int step = 0;
     for (int ib = 4 * warp; ib < n; ib += 4 * kBatchWarps, ++step) {
       double rs[4];
+      float mrow[4] = {1.f, 1.f, 1.f, 1.f};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = ib + u;
@@ -131,16 +132,17 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
           for (int q = 0; q < 8; ++q) cv[q] = 0.f;
         }
         if (!F64) {
+          // fp32 entries, parameter slots {ah, M, S'} / {bh, M, T'} (ops.cuh split_param)
           float rsum = 0.f;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float zh = fmaf(-gh, cv[q], rp.x + bh[q]);
-            const float tt = fmaf(-gl, cv[q], rp.y + bl[q]);
-            const float e = bex2(zh + tt);
+            const float e = bex2(fmaf(-gl, cv[q], zh));
             rsum = fmaf(e, T[q], rsum);
             c32[q] = fmaf(e, rp.z, c32[q]);
           }
           rs[u] = rsum;
+          mrow[u] = rp.y;
         } else {
           // fp64 entries: exact z = A_i + B_j - gbar C_ij, anchored by the
           // integer (rho_i + sig_j) ln 2, fp64 exp
@@ -159,8 +161,9 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
           rs[u] = rsum;
         }
       }
-      const double tot = bred4(rs[0], rs[1], rs[2], rs[3], lane);
+      double tot = bred4(rs[0], rs[1], rs[2], rs[3], lane);
       const int i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+      if (!F64) tot *= (double)((lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]));
       if ((lane & 7) == 0 && i < n) rowtot[i] = (j0 == 0) ? tot : rowtot[i] + tot;
       if (!F64 && (step & 1)) {
 #pragma unroll
@@ -175,7 +178,7 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
       double acc = 0.0;
 #pragma unroll
       for (int w = 0; w < kBatchWarps; ++w) acc += sred[w][t];
-      if (j0 + t < n) coltot[j0 + t] = acc;
+      if (j0 + t < n) coltot[j0 + t] = F64 ? acc : acc * (double)colp[j0 + t].y;   // fp32: times M_j = 2^bl_j
     }
     __syncthreads();
   }

@@ -7,13 +7,12 @@
 // lane of a pair is rounded exactly like the scalar IEEE op, so the value of
 // every entry is that of the scalar recipe:
 //   zh = fmaf(-gh, C, ah + bh)    (ah + bh exact: both on a 2^-8 grid)
-//   t  = fmaf(-gl, C, al + bl)
-//   e  = ex2(zh + t)
-//   row += e * T_j  (fp32, even / odd columns in two chains)
-//   col_j += e * S_i
-// and the FP32 issue count per entry halves (8 -> 4 + 1 MUFU).  Used by the
-// FP32-bound on-the-fly kernel; the HBM-bound K1 kernels keep the scalar
-// form (packing measured no gain there: 182 vs 179 us per pass).
+//   e  = ex2(fmaf(-gl, C, zh))
+//   row += e * T'_j  (fp32, even / odd columns in two chains)
+//   col_j += e * S'_i
+// (the 2^al / 2^bl multipliers are applied to the row / column totals by the
+// kernel) and the FP32 issue count per entry halves.  Used by the FP32-bound
+// on-the-fly kernel; the K1 kernels keep the scalar form.
 #pragma once
 #include <stdint.h>
 
@@ -58,46 +57,44 @@ __device__ __forceinline__ float ex2_ftz(float x) {
 // Column parameters of a lane's 8 columns as 4 pairs: columns
 // j0 + 4*lane + {0,1 | 2,3} and j0 + 128 + 4*lane + {0,1 | 2,3}.
 struct ColPairs {
-  u64 bh[4], bl[4], T[4];
+  u64 bh[4], T[4];
 };
 
-// colp(j) -> float4 {bh, bl, T, .}; columns >= n are masked (bh = -1e30).
+// colp(j) -> float4 {bh, M, T', .}; columns >= n are masked (bh = -1e30).
 template <typename Load>
 __device__ __forceinline__ void load_col_pairs(ColPairs& cp, int64_t j0, int lane, int64_t n, Load ld) {
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    float v[3][2];
+    float v[2][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = 2 * p + h;
       const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
       if (j < n) {
         const float4 c = ld(j);
-        v[0][h] = c.x; v[1][h] = c.y; v[2][h] = c.z;
+        v[0][h] = c.x; v[1][h] = c.z;
       } else {
-        v[0][h] = -1.0e30f; v[1][h] = 0.f; v[2][h] = 0.f;
+        v[0][h] = -1.0e30f; v[1][h] = 0.f;
       }
     }
     cp.bh[p] = pk2(v[0][0], v[0][1]);
-    cp.bl[p] = pk2(v[1][0], v[1][1]);
-    cp.T[p] = pk2(v[2][0], v[2][1]);
+    cp.T[p] = pk2(v[1][0], v[1][1]);
   }
 }
 
 // One row of a lane's 8 entries.  c2[p] = (C_j, C_j+1) pairs in column-pair
-// order, rp = {ah, al, S, .} of the row, ng = (-gh,-gh) / (-gl,-gl).  Adds
-// e * S into the column pair accumulators and returns the row's
-// sum_j e * T_j as an fp64 value (even and odd chains added in fp64).
+// order, rp = {ah, M, S', .} of the row, ng = (-gh,-gh) / (-gl,-gl).  Adds
+// e * S' into the column pair accumulators and returns the row's
+// sum_j e * T'_j as an fp64 value (even and odd chains added in fp64).
 __device__ __forceinline__ double entry_row8(const u64 (&c2)[4], float4 rp, const ColPairs& cp, u64 ngh2, u64 ngl2,
                                              u64 (&cacc)[4]) {
-  const u64 ah2 = pk2(rp.x, rp.x), al2 = pk2(rp.y, rp.y), S2 = pk2(rp.z, rp.z);
+  const u64 ah2 = pk2(rp.x, rp.x), S2 = pk2(rp.z, rp.z);
   u64 rsum = 0ull;
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const u64 zh = fma2(ngh2, c2[p], add2(ah2, cp.bh[p]));
-    const u64 t = fma2(ngl2, c2[p], add2(al2, cp.bl[p]));
     float zl, zu;
-    up2(add2(zh, t), zl, zu);
+    up2(fma2(ngl2, c2[p], zh), zl, zu);
     const u64 e = pk2(ex2_ftz(zl), ex2_ftz(zu));
     rsum = fma2(e, cp.T[p], rsum);
     cacc[p] = fma2(e, S2, cacc[p]);

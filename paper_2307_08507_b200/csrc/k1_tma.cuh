@@ -178,7 +178,13 @@ __device__ __forceinline__ float4 ld_param(const float4* p) {
   return __ldg(p);
 }
 
-template <bool COHERENT = false>
+// ROWS_AT_TILE_START: the row parameters of all of a warp's rows in the tile
+// (<= 16 stages x 4 rows) are loaded once at the tile start, two rows per
+// lane, and broadcast per stage with shuffles.  The per-stage global loads
+// they replace were issued right before the stage's mbarrier wait and were
+// the top stall of the pass (long scoreboard on the first use, ~15 % of the
+// warp samples in the ncu source page, profiles/README.md).
+template <bool COHERENT = false, bool ROWS_AT_TILE_START = true>
 __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh,
                                                  float gl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -193,17 +199,20 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
     int nst = stages_per_tile;
     if (i0 + (int64_t)nst * kTmaRows > nrows) nst = (int)((nrows - i0 + kTmaRows - 1) / kTmaRows);
 
-    float bh[8], bl[8], T[8];
+    float bh[8], T[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
       if (j < n) {
         const float4 cp = ld_param<COHERENT>(&a.colp[j]);
-        bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+        bh[q] = cp.x; T[q] = cp.z;
       } else {
-        bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
+        bh[q] = -1.0e30f; T[q] = 0.f;
       }
     }
+    // column multiplier 2^bl of the column this thread writes at the tile end
+    const int64_t jw = j0 + threadIdx.x;
+    const float Mcol = (threadIdx.x < kTileN && jw < n) ? ld_param<COHERENT>(&a.colp[jw]).y : 0.f;
     // fp64 column accumulators live in this warp's row of sm.sred (warp-
     // private; no registers held across the tile), fp32 over 8 rows first
     float cacc32[8];
@@ -211,13 +220,34 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
 #pragma unroll
     for (int q = 0; q < 8; ++q) { csum[4 * lane + (q & 3) + 128 * (q >> 2)] = 0.0; cacc32[q] = 0.f; }
 
+    // lane l holds rows (stage l/2, u = 2 (l & 1) + {0, 1}) of this warp
+    float4 rq0, rq1;
+    if (ROWS_AT_TILE_START) {
+      const int kk = lane >> 1;
+      const int64_t ib = i0 + (int64_t)kk * kTmaRows + 4 * warp + 2 * (lane & 1);
+      const float4 none = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+      rq0 = (kk < nst && ib < nrows) ? ld_param<COHERENT>(&a.rowp[ib]) : none;
+      rq1 = (kk < nst && ib + 1 < nrows) ? ld_param<COHERENT>(&a.rowp[ib + 1]) : none;
+    }
     for (int k = 0; k < nst; ++k, ++it) {
       const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
       const int64_t ib = i0 + (int64_t)k * kTmaRows + 4 * warp;
       float4 rp[4];
+      if (ROWS_AT_TILE_START) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        rp[u] = (ib + u < nrows) ? ld_param<COHERENT>(&a.rowp[ib + u]) : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 4; ++u) {
+          const float4& q = (u & 1) ? rq1 : rq0;
+          const int src = 2 * k + (u >> 1);
+          rp[u].x = __shfl_sync(0xffffffffu, q.x, src);
+          rp[u].y = __shfl_sync(0xffffffffu, q.y, src);
+          rp[u].z = __shfl_sync(0xffffffffu, q.z, src);
+          rp[u].w = 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          rp[u] = (ib + u < nrows) ? ld_param<COHERENT>(&a.rowp[ib + u]) : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+      }
       mbar_wait(&sm.full[s], ph);
       double rs[4];
 #pragma unroll
@@ -226,14 +256,13 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
         const float4 x0 = *reinterpret_cast<const float4*>(row + 4 * lane);
         const float4 x1 = *reinterpret_cast<const float4*>(row + 128 + 4 * lane);
         const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-        const float ah = rp[u].x, al = rp[u].y, S = rp[u].z;
+        const float ah = rp[u].x, S = rp[u].z;
         float rsum = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float cij = cv[q];
           const float zh = fmaf(-gh, cij, ah + bh[q]);
-          const float tt = fmaf(-gl, cij, al + bl[q]);
-          const float e = ex2_fast(zh + tt);
+          const float e = ex2_fast(fmaf(-gl, cij, zh));
           rsum = fmaf(e, T[q], rsum);
           cacc32[q] = fmaf(e, S, cacc32[q]);
         }
@@ -243,7 +272,8 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       const double tot = warp_reduce4_t(rs[0], rs[1], rs[2], rs[3], lane);
       const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-      if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot;
+      const float Mrow = (lane & 16) ? ((lane & 8) ? rp[3].y : rp[2].y) : ((lane & 8) ? rp[1].y : rp[0].y);
+      if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot * (double)Mrow;
       if (k & 1) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -263,7 +293,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
 #pragma unroll
       for (int w = 0; w < kConsumerWarps; ++w) acc += sm.sred[w][tt];
       const int64_t j = j0 + tt;
-      if (j < n) a.colpart[(int64_t)tr * n + j] = acc;
+      if (j < n) a.colpart[(int64_t)tr * n + j] = acc * (double)Mcol;
     }
     consumer_bar();   // sred / last flags reused by the next tile
   }

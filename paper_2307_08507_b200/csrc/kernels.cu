@@ -76,14 +76,14 @@ __device__ __forceinline__ double warp_reduce4(double v0, double v1, double v2, 
 // Fused evaluation.  CTA = (col tile tc of 256 columns) x (row tile tr of
 // tile_m rows); 8 warps; lane owns columns j0 + 4*lane + {0..3} and
 // j0 + 128 + 4*lane + {0..3}; warp w walks rows i0 + 32*k + 4*w + {0..3}.
-// Per entry (7 FP32 + 1 MUFU):
+// Per entry (5 FP32 + 1 MUFU; parameter slots: ops.cuh split_param):
 //   s = ah_i + bh_j                      (exact: both on a 2^-8 grid)
 //   zh = fmaf(-gh, C_ij, s)              (one rounding of the cancellation)
-//   t  = fmaf(-gl, C_ij, al_i + bl_j)
-//   e  = ex2(zh + t)
-//   row_i += e * T_j ;  col_j += e * S_i
-// Row sums are reduced across lanes per 4 rows (fp64 butterfly); column
-// sums are fp32 over 8 rows, then fp64, then fp64 across warps in smem.
+//   e  = ex2(fmaf(-gl, C_ij, zh))        (= P_ij 2^-(rho_i + sig_j + al_i + bl_j))
+//   row_i += e * T'_j ;  col_j += e * S'_i
+// Row sums are reduced across lanes per 4 rows (fp64 butterfly) and scaled
+// by M_i = 2^al_i; column sums are fp32 over 8 rows, then fp64, then fp64
+// across warps in smem, scaled by M_j = 2^bl_j.
 // ---------------------------------------------------------------------------
 template <int KIND, bool VEC4>
 __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
@@ -99,15 +99,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
   // on-the-fly cost: Y tile transposed [d][256]
   extern __shared__ float sdyn[];
 
-  float bh[8], bl[8], T[8];
+  float bh[8], T[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
     if (j < n) {
       const float4 cp = a.colp[j];
-      bh[q] = cp.x; bl[q] = cp.y; T[q] = cp.z;
+      bh[q] = cp.x; T[q] = cp.z;
     } else {
-      bh[q] = -1.0e30f; bl[q] = 0.f; T[q] = 0.f;
+      bh[q] = -1.0e30f; T[q] = 0.f;
     }
   }
 
@@ -187,24 +187,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       float rsum = 0.f;
-      const float ah = rp[u].x, al = rp[u].y, S = rp[u].z;
+      const float ah = rp[u].x, S = rp[u].z;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float cij = cv[u][q];
         const float s = ah + bh[q];
         const float zh = fmaf(-gh, cij, s);
-        const float t = fmaf(-gl, cij, al + bl[q]);
-        const float e = ex2_approx(zh + t);
+        const float e = ex2_approx(fmaf(-gl, cij, zh));
         rsum = fmaf(e, T[q], rsum);
         cacc32[q] = fmaf(e, S, cacc32[q]);
       }
       rs[u] = rsum;
     }
-    // row totals (fp64 butterfly over the warp)
+    // row totals (fp64 butterfly over the warp), times M_i = 2^al_i
     {
       const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
       const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-      if ((lane & 7) == 0 && i < tile_end) a.rowpart[(int64_t)blockIdx.x * nrows + i] = tot;
+      const float Mrow = (lane & 16) ? ((lane & 8) ? rp[3].y : rp[2].y) : ((lane & 8) ? rp[1].y : rp[0].y);
+      if ((lane & 7) == 0 && i < tile_end) a.rowpart[(int64_t)blockIdx.x * nrows + i] = tot * (double)Mrow;
     }
     if (++flush == 2) {   // 8 rows of fp32 column sums -> fp64
       flush = 0;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) tot += sred[w][t];
     const int64_t j = j0 + t;
-    if (j < n) a.colpart[(int64_t)blockIdx.y * n + j] = tot;
+    if (j < n) a.colpart[(int64_t)blockIdx.y * n + j] = tot * (double)a.colp[j].y;   // times M_j = 2^bl_j
   }
 }
 
@@ -311,11 +311,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         }
       }
       double rs[kUnroll];
+      float mrow[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int64_t i = c0 + rb + u;
         float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
         if (rb + u < rows_c) rp = a.rowp[i];
+        mrow[u] = rp.y;
         u64 c2[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) c2[p] = mul2(acc[u][p], scale2);
@@ -324,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
       {
         const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
         const int r = rb + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-        if ((lane & 7) == 0 && r < rows_c) a.rowpart[(int64_t)blockIdx.x * nrows + c0 + r] = tot;
+        const float Mrow = (lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]);
+        if ((lane & 7) == 0 && r < rows_c) a.rowpart[(int64_t)blockIdx.x * nrows + c0 + r] = tot * (double)Mrow;
       }
       if (++flush == 2) {   // 8 rows of fp32 column sums -> fp64
         flush = 0;
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) tot += sred[w][t];
     const int64_t j = j0 + t;
-    if (j < n) a.colpart[(int64_t)blockIdx.y * n + j] = tot;
+    if (j < n) a.colpart[(int64_t)blockIdx.y * n + j] = tot * (double)a.colp[j].y;   // times M_j = 2^bl_j
   }
 }
 

@@ -37,6 +37,14 @@ __device__ __forceinline__ void lse_merge(double& m, double& s, double m2, doubl
   }
 }
 
+// fp32-entry parameter slot {ah, M = 2^al, S' = 2^anchor * M, 0} (DESIGN.md
+// "K1 numerics"): a2 = base log2(e) - anchor = ah + al with ah on a 2^-8 grid
+// (|ah| < 2^15, so ah_i + bh_j is exact in fp32) and |al| <= 2^-9.  The lo
+// part leaves the exponent: the kernels exponentiate ah + bh - g2 C only and
+// carry 2^al_i / 2^bl_j as the multipliers M (applied to the row / column
+// totals) and S' / T' (the cross weights), so the entry costs 1 FADD + 2
+// FFMA + 1 MUFU + 2 FFMA.  M is fp32-rounded once (<= 2^-24 relative);
+// S' = 2^anchor * M is exact.
 __device__ __forceinline__ float4 split_param(double base, double anchor, int* flag) {
   const double a2 = base * L2E_D - anchor;
   const double ah = rint(a2 * 256.0) * (1.0 / 256.0);
@@ -44,7 +52,8 @@ __device__ __forceinline__ float4 split_param(double base, double anchor, int* f
     if (flag) *flag = 1;
   }
   const double al = a2 - ah;
-  return make_float4((float)ah, (float)al, (float)exp2(anchor), 0.f);
+  const float M = (float)exp2(al);
+  return make_float4((float)ah, M, (float)(exp2(anchor) * (double)M), 0.f);
 }
 
 // fp64-entry parameter slot: {base potential (fp64), 2^anchor (fp32), anchor (fp32)}

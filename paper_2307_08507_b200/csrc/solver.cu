@@ -924,7 +924,10 @@ mdot_status Workspace::setup(const mdot_options& o) {
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
   }
-  exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && c_f64);
+  // fp32 entries resolve the marginals to ~1e-7 relative (DESIGN.md "K1
+  // numerics"): AUTO evaluates in fp64 for fp64 costs and for targets below
+  // that resolution (the same rule as the batched solver, mdot_solve_batch)
+  exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && (c_f64 || o.eps < 5e-8));
   if (!exact_mode && c_f64) {
     set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
     return MDOT_EINVAL;

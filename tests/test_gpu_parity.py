@@ -229,6 +229,20 @@ def test_line_1d_exact_ot_pin_on_gpu():
     assert res["cost_unrounded"] - ot <= Hmin / gb + 1e-6
 
 
+def test_auto_precision_below_fp32_resolution():
+    """precision AUTO with eps below the fp32-entry resolution (~1e-7, DESIGN.md
+    "K1 numerics") evaluates in fp64 (exact two-pass LSE) and meets eps."""
+    n, gb, eps = 300, 256.0, 1e-9
+    inst = S.uniform_points_instance(3, n, 2, 12, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=1),
+                       options=M.options(eps=eps), u_out=U, v_out=V)
+    Uo, Vo, ores, _ = O.mdot(prob, [gb], O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
 def test_edge_cases_and_errors():
     # n = 1: the only plan is [[1]]
     res = M.mdot_solve(_t(np.array([[0.5]], dtype=np.float32)), _t(np.array([1.0])), _t(np.array([1.0])),

@@ -26,7 +26,6 @@
 
 namespace mdot {
 
-template <bool ROWS_AT_TILE_START>
 __global__ void __launch_bounds__(kTmaThreads, 2)
     k_eval_tma(const __grid_constant__ CUtensorMap tmap, EvalArgs a) {
   if (a.done && *a.done) return;
@@ -52,7 +51,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   }
   const float gh = a.gpair ? a.gpair[0] : a.gh;
   const float gl = a.gpair ? a.gpair[1] : a.gl;
-  tma_consume_pass<false, ROWS_AT_TILE_START>(sm, a, it, gh, gl);
+  tma_consume_pass<false>(sm, a, it, gh, gl);
 }
 
 // ---------------------------------------------------------------------------
@@ -93,25 +92,19 @@ cudaError_t make_tma_map(const EvalArgs& a, void* map_out /* CUtensorMap, 64 B a
 
 cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, int grid, cudaStream_t st) {
   static bool attr = false;
-  // MDOT_K1_ROWLDG: A/B switch, per-stage row-parameter loads (k1_tma.cuh)
-  static const bool rowldg = getenv("MDOT_K1_ROWLDG") != nullptr;
   const int smem = (int)sizeof(TmaSmem) + 128;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_eval_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_eval_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const CUtensorMap& m = *reinterpret_cast<const CUtensorMap*>(map);
-  if (rowldg) k_eval_tma<false><<<grid, kTmaThreads, smem, st>>>(m, a);
-  else k_eval_tma<true><<<grid, kTmaThreads, smem, st>>>(m, a);
+  k_eval_tma<<<grid, kTmaThreads, smem, st>>>(m, a);
   return cudaGetLastError();
 }
 
 void set_smem_carveout_tma() {
-  cudaFuncSetAttribute(k_eval_tma<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       (int)cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k_eval_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  cudaFuncSetAttribute(k_eval_tma, cudaFuncAttributePreferredSharedMemoryCarveout,
                        (int)cudaSharedmemCarveoutMaxShared);
 }
 

@@ -178,13 +178,17 @@ __device__ __forceinline__ float4 ld_param(const float4* p) {
   return __ldg(p);
 }
 
-// ROWS_AT_TILE_START: the row parameters of all of a warp's rows in the tile
-// (<= 16 stages x 4 rows) are loaded once at the tile start, two rows per
-// lane, and broadcast per stage with shuffles.  The per-stage global loads
-// they replace were issued right before the stage's mbarrier wait and were
-// the top stall of the pass (long scoreboard on the first use, ~15 % of the
-// warp samples in the ncu source page, profiles/README.md).
-template <bool COHERENT = false, bool ROWS_AT_TILE_START = true>
+// Row parameters: all of a warp's rows in the tile (<= 16 stages x 4 rows)
+// are loaded once at the tile start, two rows per lane, and broadcast per row
+// with shuffles.  Per-stage global loads of them were the top stall of the
+// pass (long scoreboard on the first use after the mbarrier wait, ~15 % of
+// the warp samples; profiles/README.md) and measured 4 us slower in-solve.
+//
+// Tried and rejected (profiles/README.md): releasing the ring slot before the
+// arithmetic (rows staged in registers; needs a proxy fence before the
+// release and spills at the 96-register cap of 18 warps/SM: 190 vs 185 us
+// in-solve), packed f32x2 arithmetic (186 vs 185 us).
+template <bool COHERENT = false>
 __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh,
                                                  float gl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,7 +226,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
 
     // lane l holds rows (stage l/2, u = 2 (l & 1) + {0, 1}) of this warp
     float4 rq0, rq1;
-    if (ROWS_AT_TILE_START) {
+    {
       const int kk = lane >> 1;
       const int64_t ib = i0 + (int64_t)kk * kTmaRows + 4 * warp + 2 * (lane & 1);
       const float4 none = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
@@ -232,58 +236,49 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
     for (int k = 0; k < nst; ++k, ++it) {
       const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
       const int64_t ib = i0 + (int64_t)k * kTmaRows + 4 * warp;
-      float4 rp[4];
-      if (ROWS_AT_TILE_START) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4& q = (u & 1) ? rq1 : rq0;
-          const int src = 2 * k + (u >> 1);
-          rp[u].x = __shfl_sync(0xffffffffu, q.x, src);
-          rp[u].y = __shfl_sync(0xffffffffu, q.y, src);
-          rp[u].z = __shfl_sync(0xffffffffu, q.z, src);
-          rp[u].w = 0.f;
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          rp[u] = (ib + u < nrows) ? ld_param<COHERENT>(&a.rowp[ib + u]) : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
-      }
       mbar_wait(&sm.full[s], ph);
-      double rs[4];
+      float rs[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        const float4& q = (u & 1) ? rq1 : rq0;
+        const int src = 2 * k + (u >> 1);
+        const float ah = __shfl_sync(0xffffffffu, q.x, src);
+        const float S = __shfl_sync(0xffffffffu, q.z, src);
         const float* row = &sm.stage[s][4 * warp + u][0];
         const float4 x0 = *reinterpret_cast<const float4*>(row + 4 * lane);
         const float4 x1 = *reinterpret_cast<const float4*>(row + 128 + 4 * lane);
         const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-        const float ah = rp[u].x, S = rp[u].z;
         float rsum = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float cij = cv[q];
-          const float zh = fmaf(-gh, cij, ah + bh[q]);
+        for (int q8 = 0; q8 < 8; ++q8) {
+          const float cij = cv[q8];
+          const float zh = fmaf(-gh, cij, ah + bh[q8]);
           const float e = ex2_fast(fmaf(-gl, cij, zh));
-          rsum = fmaf(e, T[q], rsum);
-          cacc32[q] = fmaf(e, S, cacc32[q]);
+          rsum = fmaf(e, T[q8], rsum);
+          cacc32[q8] = fmaf(e, S, cacc32[q8]);
         }
         rs[u] = rsum;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       const double tot = warp_reduce4_t(rs[0], rs[1], rs[2], rs[3], lane);
+      // row multiplier M_i = 2^al_i of the row this lane writes (u = 2 h + l)
+      const int srcm = 2 * k + ((lane >> 4) & 1);
+      const float m0 = __shfl_sync(0xffffffffu, rq0.y, srcm);
+      const float m1 = __shfl_sync(0xffffffffu, rq1.y, srcm);
+      const float Mrow = (lane & 8) ? m1 : m0;
       const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-      const float Mrow = (lane & 16) ? ((lane & 8) ? rp[3].y : rp[2].y) : ((lane & 8) ? rp[1].y : rp[0].y);
       if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot * (double)Mrow;
       if (k & 1) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          csum[4 * lane + (q & 3) + 128 * (q >> 2)] += (double)cacc32[q];
-          cacc32[q] = 0.f;
+        for (int q8 = 0; q8 < 8; ++q8) {
+          csum[4 * lane + (q8 & 3) + 128 * (q8 >> 2)] += (double)cacc32[q8];
+          cacc32[q8] = 0.f;
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) csum[4 * lane + (q & 3) + 128 * (q >> 2)] += (double)cacc32[q];
+    for (int q8 = 0; q8 < 8; ++q8) csum[4 * lane + (q8 & 3) + 128 * (q8 >> 2)] += (double)cacc32[q8];
 
     // column sums of this tile (8 warps, fixed order) -> partial of row tile tr
     consumer_bar();

@@ -286,25 +286,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
 }
 
 static int g_persist_grid = -1;
+static const void* persist_fn() { return (const void*)k_persist; }
 
 int persist_grid() {
   if (g_persist_grid >= 0) return g_persist_grid;
   const int smem = (int)sizeof(PersistSmem) + 128;
-  if (cudaFuncSetAttribute(k_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+  if (cudaFuncSetAttribute(persist_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
     g_persist_grid = 0;
     return 0;
   }
-  cudaFuncSetAttribute(k_persist, cudaFuncAttributePreferredSharedMemoryCarveout,
+  cudaFuncSetAttribute(persist_fn(), cudaFuncAttributePreferredSharedMemoryCarveout,
                        (int)cudaSharedmemCarveoutMaxShared);
   int per_sm = 0, dev = 0, sms = 0, coop = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist, kTmaThreads, smem) != cudaSuccess)
+  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_fn(), kTmaThreads, smem) != cudaSuccess)
     per_sm = 0;
   if (getenv("MDOT_DEBUG")) {
     cudaFuncAttributes at;
-    cudaFuncGetAttributes(&at, k_persist);
+    cudaFuncGetAttributes(&at, persist_fn());
     fprintf(stderr, "[mdot] k_persist regs %d smem %d coop %d per_sm %d\n", at.numRegs, smem, coop, per_sm);
   }
   // the K1 pass needs 2 CTAs per SM (18 warps) to keep HBM busy; with one the
@@ -319,7 +320,7 @@ cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cuda
   const int smem = (int)sizeof(PersistSmem) + 128;
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(map);
   void* args[] = {const_cast<CUtensorMap*>(m), const_cast<PersistArgs*>(&a)};
-  return cudaLaunchCooperativeKernel((const void*)k_persist, dim3(grid), dim3(kTmaThreads), args, (size_t)smem, st);
+  return cudaLaunchCooperativeKernel(persist_fn(), dim3(grid), dim3(kTmaThreads), args, (size_t)smem, st);
 }
 
 }  // namespace mdot

@@ -259,6 +259,14 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
         }
         rs[u] = rsum;
       }
+      // release the slot.  The reads above are generic-proxy shared-memory
+      // loads and the refill is an async-proxy (TMA) write: without this
+      // proxy fence nothing stops the arrive (and the refill) from overtaking
+      // loads whose data has not returned yet (ptxas may schedule their
+      // consumers after the arrive).  Observed as one corrupted row at
+      // n = 16384 under a different instruction schedule
+      // (test_tma_kernel_bitwise_equals_generic_kernel_config4).
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       const double tot = warp_reduce4_t(rs[0], rs[1], rs[2], rs[3], lane);

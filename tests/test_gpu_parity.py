@@ -311,6 +311,26 @@ def test_tma_kernel_bitwise_equals_generic_kernel(n, monkeypatch):
     assert torch.equal(lr1, lr2) and torch.equal(lc1, lc2)
 
 
+def test_tma_kernel_bitwise_equals_generic_kernel_config4(monkeypatch):
+    """Same identity at config 4 (n = 16384: 512-row tiles, 16 stages per
+    tile, 6-7 tiles per CTA), potentials from a short GPU solve."""
+    inst = S.config4(0)
+    n = inst.n
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, 1024.0, T=1), options=M.options(eps=1e-3),
+                 u_out=U, v_out=V)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    U += 0.01 * torch.randn(n, generator=g, dtype=torch.float64).to(DEV)
+    lr1, lc1, f1 = M.mdot_marginals(U, V, 1024.0, C, r, c)
+    monkeypatch.setenv("MDOT_DISABLE_TMA", "1")
+    lr2, lc2, f2 = M.mdot_marginals(U, V, 1024.0, C, r, c)
+    assert f1 == 0 and f2 == 0
+    assert torch.equal(lr1, lr2) and torch.equal(lc1, lc2), (
+        (lr1 - lr2).abs().max().item(), (lc1 - lc2).abs().max().item())
+
+
 @pytest.mark.parametrize("projector", [0, 1, 2])
 def test_device_control_matches_host_control(projector):
     """Device-resident line search (k_ctrl + CUDA graph) against the host

@@ -38,10 +38,12 @@ def main():
     if "1" in which:
         inst = S.config1(0)
         C, r, c = t(inst.C), t(inst.r), t(inst.c)
-        ms, res = timed(lambda: M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_DOUBLING, 4096.0),
-                                             options=M.options(eps=1e-6)))
-        out["cfg1_n64_fp64_doubling_eps1e-6"] = {"ms": ms, "evals": res["evaluations"], "md_steps": res["md_steps"],
-                                                 "control_path": res["control_path"], "l1": res["l1_final"]}
+        for em in (0.0, 1e-3):
+            ms, res = timed(lambda: M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_DOUBLING, 4096.0),
+                                                 options=M.options(eps=1e-6, eps_md=em)))
+            out[f"cfg1_n64_fp64_doubling_eps1e-6_epsmd{em:g}"] = {
+                "ms": ms, "evals": res["evaluations"], "md_steps": res["md_steps"],
+                "control_path": res["control_path"], "l1": res["l1_final"]}
         print(out, flush=True)
     if "3" in which:
         for frac in (0.5, 0.9, 0.99):
@@ -71,15 +73,18 @@ def main():
         pairs = float(n) * n
         out["cfg5_single_eval"] = {"ms_incl_setup": ms, "pairs_per_s": pairs / (ms / 1e3)}
         print(out["cfg5_single_eval"], flush=True)
-        ms, res = timed(lambda: M.mdot_solve(X=X, Y=Y, scale=inst.scale, r=r, c=c,
-                                             schedule=M.schedule(M.MDOT_SCHED_FIXED, 4096.0),
-                                             options=M.options(eps=1e-5, time_kernels=1), check=False), reps=1)
-        k1 = res["kernel_ms"] / max(1, res["kernel_launches"])
-        out["cfg5_n65536_d16_otf_gbar4096_eps1e-5"] = {
-            "ms": ms, "evals": res["evaluations"], "status": res["status_name"], "l1": res["l1_final"],
-            "k1_ms": k1, "pairs_per_s_k1": pairs / (k1 / 1e3), "control_path": res["control_path"],
-            "cost_rounded": res["cost_rounded"]}
-        print(out["cfg5_n65536_d16_otf_gbar4096_eps1e-5"], flush=True)
+        for em in (0.0, 1e-3):
+            ms, res = timed(lambda: M.mdot_solve(X=X, Y=Y, scale=inst.scale, r=r, c=c,
+                                                 schedule=M.schedule(M.MDOT_SCHED_FIXED, 4096.0),
+                                                 options=M.options(eps=1e-5, eps_md=em, time_kernels=1),
+                                                 check=False), reps=1)
+            k1 = res["kernel_ms"] / max(1, res["kernel_launches"])
+            key = f"cfg5_n65536_d16_otf_gbar4096_eps1e-5_epsmd{em:g}"
+            out[key] = {
+                "ms": ms, "evals": res["evaluations"], "status": res["status_name"], "l1": res["l1_final"],
+                "k1_ms": k1, "pairs_per_s_k1": pairs / (k1 / 1e3), "control_path": res["control_path"],
+                "cost_unrounded": res["cost_unrounded"], "cost_rounded": res["cost_rounded"]}
+            print(key, out[key], flush=True)
     print("JSON " + json.dumps(out))
 
 

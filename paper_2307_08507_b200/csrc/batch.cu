@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     if (tid == 0) {
       CtrlState& h = S.st;
       memset(&h, 0, sizeof(CtrlState));
-      h.eps = t < a.T ? a.eps_md : a.eps; h.c1 = a.c1; h.c2 = a.c2; h.noise = a.f64 ? 1e-14 : 6e-8;
+      h.eps = t < a.T ? a.eps_md : a.eps; h.c1 = a.c1; h.c2 = a.c2; h.noise = ls_noise(a.f64 != 0, gbar);
       h.stop_rho = a.stop_rho; h.ncg = a.projector == MDOT_PROJ_NCG; h.sinkhorn = a.projector == MDOT_PROJ_SINKHORN;
       h.beta_kind = a.beta_kind; h.ls_max_trials = a.ls_max_trials;
       h.max_evals = a.max_evals - evals_total;

@@ -261,6 +261,16 @@ cudaError_t launch_round_combine_rows(const RoundArgs& a, const double* r, doubl
                                       cudaStream_t st);
 
 // K8: batched solver, one CTA per instance (batch.cu)
+// Decrease-safeguard tolerance of the line search (Z9), relative to
+// max(1, sum P).  fp32 entries: the fp32-entry noise of sum P.  fp64 entries:
+// the exponent z = A_i + B_j - gbar C_ij cancels terms of size ~gbar (the
+// potentials grow with gbar), so a 4-ulp error of that size moves sum P by
+// ~4u (gbar + 64) relative; a fixed 1e-14 rejected every trial near
+// convergence at gbar = 4096 (config 2, eps 1e-8).
+__host__ __device__ inline double ls_noise(bool f64, double gbar) {
+  return f64 ? 4.4e-16 * (gbar + 64.0) : 6e-8;
+}
+
 struct BatchResult {
   double cost_rounded, cost_unrounded, l1_final, rho_final, gamma_bar;
   long long evaluations, iterations, ls_evaluations, resets, ls_restarts;

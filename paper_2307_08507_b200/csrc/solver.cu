@@ -382,7 +382,7 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
   double dphi0_prev = 0, sg_prev = 0, gg_prev = 0;
   double alpha_prev = 1.0;
   const double c1 = o.c1, c2 = o.c2;
-  const double noise = w.exact_mode ? 1e-14 : 6e-8;   // decrease-safeguard tolerance (Z9)
+  const double noise = ls_noise(w.exact_mode, w.gbar);   // decrease-safeguard tolerance (Z9)
   int64_t k = 0;
   mdot_status st = MDOT_OK;
   while (stopval(sc, o.stop) > o.eps) {
@@ -604,7 +604,7 @@ mdot_status Workspace::build_graph() {
 mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
   CtrlState h{};
   h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
-  h.noise = w.exact_mode ? 1e-14 : 6e-8;
+  h.noise = ls_noise(w.exact_mode, w.gbar);
   h.stop_rho = o.stop; h.ncg = o.projector == MDOT_PROJ_NCG; h.sinkhorn = o.projector == MDOT_PROJ_SINKHORN;
   h.beta_kind = o.beta; h.ls_max_trials = o.ls_max_trials;
   h.max_evals = o.max_evals - w.evals;

@@ -244,7 +244,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int kOtfChunk = 128;
 
-template <int D>
+// POW2: scale is a power of two, so C = acc * scale is exact and -g * C ==
+// (-g * scale) * acc exactly: the scale folds into (gh, gl) and the FMUL2 per
+// pair of entries disappears, with the Z22 recipe's bits unchanged.
+template <int D, bool POW2>
 __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -254,22 +257,49 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   const int64_t n = a.n, nrows = a.nrows;
 
   __shared__ double sred[kWarps][kTileN];
+  __shared__ float4 sRP[kOtfChunk];   // row parameters of the current chunk
   extern __shared__ __align__(16) unsigned char sraw[];
   float* sY = reinterpret_cast<float*>(sraw);                       // [D][256]
   u64* sX = reinterpret_cast<u64*>(sraw + sizeof(float) * D * kTileN);  // [chunk][D]
+  // staging loads are issued all at once (vector loads where D % 4 == 0 and
+  // the pointers are 16-byte aligned); a per-element load -> store loop here
+  // was the top stall of the kernel (one L2 round trip per element)
+  const bool vec = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
 
-  // Y[j0:j0+256, :] transposed; columns past n are zero points (masked by bh)
-  for (int idx = threadIdx.x; idx < kTileN * D; idx += kThreads) {
-    const int t = idx / D, k = idx % D;
-    const int64_t j = j0 + t;
-    sY[k * kTileN + t] = (j < n) ? a.Y[j * D + k] : 0.f;
+  // Y[j0:j0+256, :] transposed (thread t = column j0 + t); columns past n are
+  // zero points (masked by bh)
+  {
+    static_assert(kThreads == kTileN, "one thread per tile column");
+    const int64_t j = j0 + threadIdx.x;
+    float yv[D];
+    if (j < n) {
+      if (vec) {
+#pragma unroll
+        for (int q = 0; q < (D + 3) / 4; ++q) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(a.Y + j * D) + q);
+          yv[4 * q] = v.x;
+          if (4 * q + 1 < D) yv[4 * q + 1] = v.y;
+          if (4 * q + 2 < D) yv[4 * q + 2] = v.z;
+          if (4 * q + 3 < D) yv[4 * q + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < D; ++k) yv[k] = __ldg(a.Y + j * D + k);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < D; ++k) yv[k] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) sY[k * kTileN + threadIdx.x] = yv[k];
   }
 
   ColPairs cpp;
   load_col_pairs(cpp, j0, lane, n, [&](int64_t j) { return a.colp[j]; });
   const float gh = a.gpair ? a.gpair[0] : a.gh;
   const float gl = a.gpair ? a.gpair[1] : a.gl;
-  const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl), scale2 = pk2(a.scale, a.scale);
+  const float sg = POW2 ? a.scale : 1.f;
+  const u64 ngh2 = pk2(-gh * sg, -gh * sg), ngl2 = pk2(-gl * sg, -gl * sg), scale2 = pk2(a.scale, a.scale);
 
   double cacc64[8];
   u64 cacc2[4];
@@ -283,10 +313,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   for (int64_t c0 = i0; c0 < tile_end; c0 += kOtfChunk) {
     const int rows_c = (int)((tile_end - c0 < kOtfChunk) ? tile_end - c0 : kOtfChunk);
     __syncthreads();   // previous chunk consumed (and sY written on entry)
-    for (int idx = threadIdx.x; idx < kOtfChunk * D; idx += kThreads) {
-      const int r = idx / D, k = idx % D;
-      const float x = (r < rows_c) ? a.X[(c0 + r) * D + k] : 0.f;
-      sX[idx] = pk2(x, x);
+    {
+      float4 rpv = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+      if (threadIdx.x < kOtfChunk && (int)threadIdx.x < rows_c) rpv = a.rowp[c0 + threadIdx.x];
+      if (vec) {
+        constexpr int kQ = (kOtfChunk * D / 4 + kThreads - 1) / kThreads;   // float4 per thread
+        float4 xv[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int f = 4 * (q * kThreads + threadIdx.x);   // first float of this float4 in the chunk
+          xv[q] = (f < kOtfChunk * D && f / D < rows_c)
+                      ? __ldg(reinterpret_cast<const float4*>(a.X + c0 * D + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int f = 4 * (q * kThreads + threadIdx.x);
+          if (f < kOtfChunk * D) {
+            sX[f] = pk2(xv[q].x, xv[q].x);
+            sX[f + 1] = pk2(xv[q].y, xv[q].y);
+            sX[f + 2] = pk2(xv[q].z, xv[q].z);
+            sX[f + 3] = pk2(xv[q].w, xv[q].w);
+          }
+        }
+      } else {
+        constexpr int kE = (kOtfChunk * D + kThreads - 1) / kThreads;
+        float xv[kE];
+#pragma unroll
+        for (int q = 0; q < kE; ++q) {
+          const int idx = q * kThreads + threadIdx.x;
+          xv[q] = (idx < kOtfChunk * D && idx / D < rows_c) ? __ldg(a.X + c0 * D + idx) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < kE; ++q) {
+          const int idx = q * kThreads + threadIdx.x;
+          if (idx < kOtfChunk * D) sX[idx] = pk2(xv[q], xv[q]);
+        }
+      }
+      if (threadIdx.x < kOtfChunk) sRP[threadIdx.x] = rpv;
     }
     __syncthreads();
     for (int rb = 4 * warp; rb < rows_c; rb += kWarps * kUnroll) {
@@ -314,13 +377,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
       float mrow[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        const int64_t i = c0 + rb + u;
-        float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
-        if (rb + u < rows_c) rp = a.rowp[i];
+        const float4 rp = sRP[rb + u];   // broadcast; rows past the chunk hold bh = -1e30
         mrow[u] = rp.y;
         u64 c2[4];
 #pragma unroll
-        for (int p = 0; p < 4; ++p) c2[p] = mul2(acc[u][p], scale2);
+        for (int p = 0; p < 4; ++p) c2[p] = POW2 ? acc[u][p] : mul2(acc[u][p], scale2);
         rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
       }
       {
@@ -362,17 +423,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   }
 }
 
-template <int D>
-static cudaError_t launch_otf_t(const EvalArgs& a, cudaStream_t st) {
+template <int D, bool POW2>
+static cudaError_t launch_otf_pt(const EvalArgs& a, cudaStream_t st) {
   dim3 grid(a.n_col_tiles, a.n_row_tiles);
   const size_t smem = sizeof(float) * D * kTileN + sizeof(u64) * kOtfChunk * D;
   static bool attr_set = false;
-  if (!attr_set && smem > 48 * 1024) {
-    cudaFuncSetAttribute(k_eval_otf<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!attr_set) {   // static (column sums, row parameters) + dynamic exceeds the 48 KB default
+    cudaError_t e = cudaFuncSetAttribute(k_eval_otf<D, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_eval_otf<D><<<grid, kThreads, smem, st>>>(a);
+  k_eval_otf<D, POW2><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
+}
+template <int D>
+static cudaError_t launch_otf_t(const EvalArgs& a, cudaStream_t st) {
+  int e2 = 0;
+  const bool pow2 = a.scale > 0.f && frexpf(a.scale, &e2) == 0.5f && e2 > -100 && e2 < 100;
+  return pow2 ? launch_otf_pt<D, true>(a, st) : launch_otf_pt<D, false>(a, st);
 }
 
 template <int KIND, bool VEC4>

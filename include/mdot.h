@@ -86,7 +86,11 @@ typedef struct {
   int32_t n_gammas;
 } mdot_schedule;
 
-typedef enum { MDOT_PROJ_PNCG = 0, MDOT_PROJ_SINKHORN = 1, MDOT_PROJ_NCG = 2 } mdot_projector;
+/* PNCG_JACOBI: Alg. 2 with the Jacobi preconditioner diag(Hessian)^-1 =
+ * D(1/r(P), 1/c(P)) (Hessian block form), its diagonal
+ * bounded below by the target marginals (max(r(P), r)), in place of the
+ * Sinkhorn direction (SURVEY 8(f) rank 2 ablation of PAPER.md:257). */
+typedef enum { MDOT_PROJ_PNCG = 0, MDOT_PROJ_SINKHORN = 1, MDOT_PROJ_NCG = 2, MDOT_PROJ_PNCG_JACOBI = 3 } mdot_projector;
 typedef enum { MDOT_BETA_PPR = 0, MDOT_BETA_PPR_AF = 1, MDOT_BETA_PFR = 2 } mdot_beta;
 typedef enum { MDOT_WARM_SCALED = 0, MDOT_WARM_CARRY = 1, MDOT_WARM_ZERO = 2 } mdot_warm;
 typedef enum { MDOT_PREC_AUTO = 0, MDOT_PREC_F32P = 1, MDOT_PREC_F64P = 2 } mdot_precision;

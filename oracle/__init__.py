@@ -20,7 +20,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "mdot_oracle.c")
 
 DENSE_F32, SQEUCLID_F32, DENSE_F64 = 0, 1, 2
-PNCG, SINKHORN, NCG = 0, 1, 2
+PNCG, SINKHORN, NCG, PNCG_JACOBI = 0, 1, 2, 3
 BETA_PPR, BETA_PPR_AF, BETA_PFR, BETA_PPR_PRINTED = 0, 1, 2, 3
 WARM_SCALED, WARM_CARRY, WARM_ZERO = 0, 1, 2
 STATUS = {0: "OK", 1: "EINVAL", 3: "EINSTABLE", 4: "ENOCONV", 5: "ELINESEARCH"}

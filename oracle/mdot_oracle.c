@@ -294,6 +294,15 @@ static int pncg_project(const orc_problem* pb, const double* U, const double* V,
       s[n + j] = M.lc[j] - log(c[j]);
       g[n + j] = M.cP[j] - c[j];
     }
+    /* Jacobi variant: s = D(diag Hessian)^-1 grad with diag = (r(P), c(P))
+     * (Hessian block form), the diagonal bounded below by
+     * the target, max(r(P), r): |s| < 1 far from feasibility (the plain
+     * 1/r(P) overflows the first trial when r(P) << r); equal to D(1/r)
+     * grad at the solution, where the Sinkhorn direction is too. */
+    if (opt->projector == ORC_PNCG_JACOBI) {
+      for (int64_t i = 0; i < n; ++i) s[i] = g[i] / fmax(M.rP[i], r[i]);
+      for (int64_t j = 0; j < n; ++j) s[n + j] = g[n + j] / fmax(M.cP[j], c[j]);
+    }
     const double* dir = ncg ? g : s;   /* preconditioned or vanilla */
     /* beta_k (Z6) */
     double beta = 0.0;

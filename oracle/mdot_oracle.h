@@ -18,7 +18,9 @@ extern "C" {
 #endif
 
 enum { ORC_DENSE_F32 = 0, ORC_SQEUCLID_F32 = 1, ORC_DENSE_F64 = 2 };
-enum { ORC_PNCG = 0, ORC_SINKHORN = 1, ORC_NCG = 2 };
+/* ORC_PNCG_JACOBI: Alg. 2 with the Jacobi preconditioner diag(Hessian)^-1 in place
+ * of the Sinkhorn direction (SURVEY 8(f) rank 2 ablation; Hessian PAPER.md:225). */
+enum { ORC_PNCG = 0, ORC_SINKHORN = 1, ORC_NCG = 2, ORC_PNCG_JACOBI = 3 };
 enum { ORC_BETA_PPR = 0, ORC_BETA_PPR_AF = 1, ORC_BETA_PFR = 2, ORC_BETA_PPR_PRINTED = 3 };
 enum { ORC_WARM_SCALED = 0, ORC_WARM_CARRY = 1, ORC_WARM_ZERO = 2 };
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EINSTABLE = 3, ORC_ENOCONV = 4, ORC_ELINESEARCH = 5 };

@@ -25,6 +25,7 @@ from ._binding import (  # noqa: F401
     MDOT_PREC_F32P,
     MDOT_PREC_F64P,
     MDOT_PROJ_NCG,
+    MDOT_PROJ_PNCG_JACOBI,
     MDOT_PROJ_PNCG,
     MDOT_PROJ_SINKHORN,
     MDOT_SCHED_DOUBLING,

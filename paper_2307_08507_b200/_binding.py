@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(_HERE, "libmdot_b200.so")
 MDOT_COST_DENSE_F32, MDOT_COST_SQEUCLID_F32, MDOT_COST_DENSE_F64 = 0, 1, 2
 MDOT_MEM_HOST, MDOT_MEM_DEVICE = 0, 1
 MDOT_SCHED_FIXED, MDOT_SCHED_DOUBLING, MDOT_SCHED_EXPLICIT = 0, 1, 2
-MDOT_PROJ_PNCG, MDOT_PROJ_SINKHORN, MDOT_PROJ_NCG = 0, 1, 2
+MDOT_PROJ_PNCG, MDOT_PROJ_SINKHORN, MDOT_PROJ_NCG, MDOT_PROJ_PNCG_JACOBI = 0, 1, 2, 3
 MDOT_BETA_PPR, MDOT_BETA_PPR_AF, MDOT_BETA_PFR = 0, 1, 2
 MDOT_WARM_SCALED, MDOT_WARM_CARRY, MDOT_WARM_ZERO = 0, 1, 2
 MDOT_PREC_AUTO, MDOT_PREC_F32P, MDOT_PREC_F64P = 0, 1, 2

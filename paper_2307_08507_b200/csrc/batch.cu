@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   fa.r = tgt; fa.c = tgt + n; fa.logr = logt; fa.logc = logt + n;
   fa.gcur = cg; fa.pcur = p;
   fa.lm = tl; fa.m = nullptr; fa.s = ts; fa.g = tg;
+  fa.jacobi = a.projector == MDOT_PROJ_PNCG_JACOBI;
 
   long long evals_total = 0, iters = 0, ls_evals = 0, resets = 0, restarts = 0;
   int status = 0;

@@ -127,6 +127,7 @@ struct FinalizeArgs {
   int64_t item_begin, item_end;   // items processed: [begin, end) of [0, nrows + n) (end 0 = all)
   const double* add_in;  // nullable: kNumScalars values added before publishing (sharded rows)
   int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
+  int jacobi;            // 1: s = grad / diag(Hessian) (MDOT_PROJ_PNCG_JACOBI) instead of the Sinkhorn direction
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 

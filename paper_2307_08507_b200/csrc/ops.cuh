@@ -182,7 +182,11 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
     const double ltg = is_row ? a.logr[k] : a.logc[k - a.nrows];
     const double mm = exp(lm);
     const double g = mm - tgt;
-    const double s = lm - ltg;
+    const double lrat = lm - ltg;
+    // preconditioned direction: the Sinkhorn direction log(m / target)
+    // or, for the Jacobi ablation, g / diag(Hessian) with
+    // the diagonal bounded below by the target: g / max(m, target)
+    const double s = a.jacobi ? g / fmax(mm, tgt) : lrat;
     a.lm[k] = lm;
     if (a.m) a.m[k] = mm;
     a.s[k] = s;
@@ -192,7 +196,7 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
     if (is_row) v[SC_MASS] += mm;   // static indices only: v stays in registers
     else v[SC_MASSC] += mm;
     v[SC_L1] += fabs(g);
-    v[SC_RHO] += tgt - mm + mm * s;            // D_h(y|x) term with y = m, x = tgt (Z1)
+    v[SC_RHO] += tgt - mm + mm * lrat;         // D_h(y|x) term with y = m, x = tgt (Z1)
     v[SC_SG] += s * g;
     v[SC_GCS] += gc * s;
     v[SC_PCG] += pc * g;

@@ -233,6 +233,7 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   f.blockpart = blockpart; f.ticket = ticket;
   f.scalars_dev = scal_dev; f.scalars_host = scal_host_dev;
   f.prep_flag = flag;
+  f.jacobi = jacobi;
   const bool shard = sharded();
   evals++;
   if (!exact_mode) {
@@ -505,6 +506,7 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
   f.blockpart = blockpart; f.ticket = ticket;
   f.scalars_dev = ctrl->sc; f.scalars_host = nullptr;
   f.prep_flag = flag;
+  f.jacobi = jacobi;
   f.done = &ctrl->done;
   if (timed) CK(cudaEventRecordWithFlags(gev[2], s, cudaEventRecordExternal));
   if (!exact_mode) {
@@ -715,6 +717,7 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   f.gcur = w.cur->g; f.pcur = w.p;
   f.lm = w.trial->lm; f.m = w.trial->m; f.s = w.trial->s; f.g = w.trial->g;
   f.prep_flag = w.flag;
+  f.jacobi = w.jacobi;
   f.from_partials = 1;
   f.rowpart = w.rowpart; f.n_col_tiles = w.eval.n_col_tiles;
   f.colpart = w.colpart; f.n_row_tiles = w.eval.n_row_tiles;
@@ -928,6 +931,7 @@ mdot_status Workspace::setup(const mdot_options& o) {
   // numerics"): AUTO evaluates in fp64 for fp64 costs and for targets below
   // that resolution (the same rule as the batched solver, mdot_solve_batch)
   exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && (c_f64 || o.eps < 5e-8));
+  jacobi = o.projector == MDOT_PROJ_PNCG_JACOBI;
   if (!exact_mode && c_f64) {
     set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
     return MDOT_EINVAL;

@@ -38,6 +38,7 @@ struct Workspace {
   float scale = 0.f;
   bool host_io = false;
   bool exact_mode = false;
+  int jacobi = 0;                   // MDOT_PROJ_PNCG_JACOBI: finalize writes grad / diag(Hessian) as s
   double gbar = 0.0;
   // device buffers (one allocation)
   void* base = nullptr;

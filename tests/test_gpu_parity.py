@@ -131,6 +131,23 @@ def test_solve_fp32_pncg_matches_oracle(n, gbar, T):
     assert res["evaluations"] <= 2.0 * ores["evaluations"] + 50
 
 
+@pytest.mark.parametrize("dc", [0, 1])
+def test_jacobi_pncg_matches_oracle(dc):
+    """PNCG with the Jacobi preconditioner (MDOT_PROJ_PNCG_JACOBI, SURVEY 8(f)
+    rank 2 ablation) against the oracle's ORC_PNCG_JACOBI, host and device
+    control."""
+    n, gb, T, eps = 300, 512.0, 4, 1e-6
+    inst = S.uniform_points_instance(3, n, 2, 13, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=T),
+                       options=M.options(eps=eps, projector=M.MDOT_PROJ_PNCG_JACOBI, device_control=dc),
+                       u_out=U, v_out=V)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), O.make_options(eps=eps, projector=O.PNCG_JACOBI))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
 def test_sinkhorn_matches_oracle():
     n = 400
     inst = S.uniform_points_instance(3, n, 2, 4, marg="dirichlet")

@@ -464,3 +464,86 @@ def test_pncg_fewer_iterations_than_sinkhorn():
         assert rp["iterations"] <= rs["iterations"]
         ratios.append(rs["iterations"] / rp["iterations"])
     assert np.mean(ratios) >= 3.0
+
+
+# ------------------------------------------------------------------ Fig. 3 diagnostics
+def test_hessian_null_vector_and_psd():
+    """(1_n, -1_n) spans the null space direction of the dual
+    Hessian; the Hessian is PSD."""
+    from oracle import diagnostics as D
+    inst = S.random_small(10, seed=31)
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(0)
+    U = np.log(inst.r) + 0.3 * rng.standard_normal(10)
+    V = np.log(inst.c) + 0.3 * rng.standard_normal(10)
+    H, P = D.hessian(prob, U, V, 5.0)
+    z = np.concatenate([np.ones(10), -np.ones(10)])
+    assert np.abs(H @ z).max() < 1e-14
+    w = D.spectrum(H)
+    assert w[0] > -1e-14 and abs(w[0]) < 1e-12 and w[1] > 1e-8
+
+
+def test_preconditioned_spectrum_closed_form_at_fixed_point():
+    """At the projection's solution (P in U(r,c)) both diagonal
+    preconditioners equal D(1/r, 1/c) and M^1/2 H M^1/2 = [[I, K], [K^T, I]]
+    with K = D(r)^-1/2 P D(c)^-1/2, whose eigenvalues are 1 -+ sigma_k(K)
+    (block-matrix identity); sigma_1 = 1 (singular vectors sqrt r, sqrt c),
+    so the spectrum spans [0, 2].  Pinned against an SVD of K."""
+    from oracle import diagnostics as D
+    inst = S.paper_sphere_instance(12, 4, 0.7, 5)
+    prob = O.OracleProblem(inst)
+    U, V, res, _ = O.mdot(prob, [16.0], O.make_options(eps=1e-14))
+    assert res["status"] == 0
+    H, P = D.hessian(prob, U, V, 16.0)
+    t = np.concatenate([inst.r, inst.c])
+    for kind in ("sinkhorn", "jacobi"):
+        M = D.preconditioner(prob, U, V, 16.0, kind)
+        np.testing.assert_allclose(M, 1.0 / t, rtol=1e-9)
+    K = P / np.sqrt(np.outer(inst.r, inst.c))
+    sig = np.linalg.svd(K, compute_uv=False)
+    assert abs(sig[0] - 1.0) < 1e-10
+    expect = np.sort(np.concatenate([1.0 - sig, 1.0 + sig]))
+    got = D.spectrum(H, D.preconditioner(prob, U, V, 16.0))
+    np.testing.assert_allclose(got, expect, atol=1e-10)
+    assert abs(D.pseudo_condition(H, 1.0 / t) - 2.0 / (1.0 - sig[1])) < 1e-8 * 2.0 / (1.0 - sig[1])
+
+
+def test_fig3_preconditioning_gain_grows_as_entropy_falls():
+    """Fig. 3 right: the ratio of pseudo-condition numbers
+    kappa(H) / kappa(M H) along PNCG iterations is larger for lower-entropy
+    marginals (n = 32, m = 4, gbar = 32, T = 1; 4 seeds, 20 evaluations)."""
+    from oracle import diagnostics as D
+    means = []
+    for frac in (0.3, 0.6, 0.9):
+        rat = []
+        for seed in range(4):
+            inst = S.paper_sphere_instance(32, 4, frac, 100 + seed)
+            prob = O.OracleProblem(inst)
+            U0, V0 = np.log(inst.r), np.log(inst.c)
+            u, v, _, _ = O.project(prob, U0, V0, 32.0, opts=O.make_options(eps=1e-12, max_evals=20))
+            H, _ = D.hessian(prob, U0 + u, V0 + v, 32.0)
+            rat.append(D.pseudo_condition(H) / D.pseudo_condition(H, D.preconditioner(prob, U0 + u, V0 + v, 32.0)))
+        means.append(np.mean(np.log(rat)))
+    assert means[0] > means[1] > means[2] > 0.0, means
+
+
+def test_fig3_left_ncg_vs_pncg_and_jacobi_ablation():
+    """Fig. 3 left: vanilla NCG needs far more iterations
+    than PNCG at low entropy (n = 8, m = 4, gbar = 128, T = 1, rho <= 1e-5);
+    the Jacobi-preconditioned ablation converges to the same plan as PNCG
+    (uniqueness of the projection) in a comparable count."""
+    its = {O.PNCG: [], O.NCG: [], O.PNCG_JACOBI: []}
+    for seed in range(4):
+        inst = S.paper_sphere_instance(8, 4, 0.2, 200 + seed)
+        prob = O.OracleProblem(inst)
+        plans = {}
+        for p in its:
+            U, V, res, _ = O.mdot(prob, [128.0], O.make_options(eps=1e-5, stop_rho=True, projector=p,
+                                                                 max_evals=200000))
+            assert res["status"] == 0, (p, res["status"])
+            its[p].append(res["iterations"])
+            U2, V2, res2, _ = O.mdot(prob, [128.0], O.make_options(eps=1e-13, projector=p, max_evals=400000))
+            plans[p] = O.plan(prob, U2, V2, 128.0)
+        assert np.abs(plans[O.PNCG_JACOBI] - plans[O.PNCG]).sum() < 1e-10
+    assert np.mean(its[O.NCG]) > 5 * np.mean(its[O.PNCG])
+    assert np.mean(its[O.PNCG_JACOBI]) < 3 * np.mean(its[O.PNCG])

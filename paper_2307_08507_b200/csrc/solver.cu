@@ -20,7 +20,9 @@
 #include <time.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -903,7 +905,7 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
       eval.keep_l2 = (4.0 * (double)nrows * (double)n <= 0.6 * (double)l2) ? 1 : 0;
-      pers_grid = (getenv("MDOT_NO_PERSIST") || comm) ? 0 : persist_grid();
+      pers_grid = (getenv("MDOT_NO_PERSIST") || comm || no_persist) ? 0 : persist_grid();
       if (pers_grid > 0 && (nrows + n + pers_grid - 1) / pers_grid > persist_max_chunk()) pers_grid = 0;
     }
   }
@@ -1061,7 +1063,8 @@ void mdot_schedule_default(mdot_schedule* s) {
 
 static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt_in,
                               double* u_out, double* v_out, float* P_out, mdot_result* res, int force_sinkhorn,
-                              Comm* comm = nullptr, int64_t row0 = 0, int64_t nrows_in = -1) {
+                              Comm* comm = nullptr, int64_t row0 = 0, int64_t nrows_in = -1,
+                              bool no_persist = false) {
   g_last_error.clear();
   if (!res) { set_error("result pointer is NULL"); return MDOT_EINVAL; }
   memset(res, 0, sizeof(*res));
@@ -1087,6 +1090,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   Workspace w;
   w.comm = comm;
   w.row0 = row0;
+  w.no_persist = no_persist;
   // MDOT_TRACE: host timestamps per stage (synchronizes between stages)
   const bool trace = getenv("MDOT_TRACE") != nullptr;
   double tr_last = t0;
@@ -1206,20 +1210,70 @@ mdot_status mdot_solve_sharded(mdot_comm* c, const mdot_problem* local_rows, int
   return solve_impl(local_rows, sched, opt, u_local_out, v_out, nullptr, res, 0, cm, row0, n_local);
 }
 
-// Sequential fallback of mdot_solve_batch (costs the K8 kernel cannot hold).
+// mdot_solve_batch for costs the K8 kernel cannot hold (SURVEY 8(f) rank 4,
+// throughput mode): device-resident instances are solved concurrently by up
+// to MDOT_BATCH_WORKERS (default 8) host workers, each on its own stream
+// (ordered after the caller's stream) with the CUDA-graph control path --
+// the persistent kernel is a cooperative grid over every SM and would
+// serialise them.  The evaluations of different instances then overlap on
+// the GPU (a shared C stays L2-resident when it fits).  Host-memory inputs
+// run one instance after the other.
 static mdot_status solve_batch_loop(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,
                                     const mdot_schedule* sched, const mdot_options* opt, double* u_out,
                                     double* v_out, mdot_result* res) {
-  mdot_status first = MDOT_OK;
-  for (int32_t b = 0; b < Bn; ++b) {
+  mdot_options o;
+  if (opt) o = *opt; else mdot_options_default(&o);
+  const int64_t n = shared->n;
+  auto one = [&](int32_t b, const mdot_options* ob, bool no_persist) {
     mdot_problem p = *shared;
-    p.r = r + (int64_t)b * shared->n;
-    p.c = c + (int64_t)b * shared->n;
-    mdot_status s = solve_impl(&p, sched, opt, u_out ? u_out + (int64_t)b * shared->n : nullptr,
-                               v_out ? v_out + (int64_t)b * shared->n : nullptr, nullptr, &res[b], 0);
-    if (s != MDOT_OK && first == MDOT_OK) first = s;
+    p.r = r + (int64_t)b * n;
+    p.c = c + (int64_t)b * n;
+    return solve_impl(&p, sched, ob, u_out ? u_out + (int64_t)b * n : nullptr,
+                      v_out ? v_out + (int64_t)b * n : nullptr, nullptr, &res[b], 0, nullptr, 0, -1, no_persist);
+  };
+  int W = 8;
+  if (const char* e = getenv("MDOT_BATCH_WORKERS")) W = atoi(e);
+  W = std::max(1, std::min<int>(W, Bn));
+  if (W == 1 || shared->mem != MDOT_MEM_DEVICE) {
+    mdot_status first = MDOT_OK;
+    for (int32_t b = 0; b < Bn; ++b) {
+      const mdot_status s = one(b, &o, false);
+      if (s != MDOT_OK && first == MDOT_OK) first = s;
+    }
+    return first;
   }
-  return first;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaEvent_t ready = nullptr;
+  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CK(cudaEventRecord(ready, (cudaStream_t)o.stream));
+  std::atomic<int32_t> next{0};
+  std::vector<mdot_status> sts((size_t)Bn, MDOT_OK);
+  std::vector<std::string> errs((size_t)Bn);
+  auto worker = [&]() {
+    cudaSetDevice(dev);
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
+    cudaStreamWaitEvent(s, ready, 0);
+    mdot_options ow = o;
+    ow.stream = s;
+    for (int32_t b = next++; b < Bn; b = next++) {
+      sts[(size_t)b] = one(b, &ow, true);
+      if (sts[(size_t)b] != MDOT_OK) errs[(size_t)b] = mdot_last_error();
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  };
+  std::vector<std::thread> th;
+  for (int k = 0; k < W; ++k) th.emplace_back(worker);
+  for (auto& x : th) x.join();
+  cudaEventDestroy(ready);
+  for (int32_t b = 0; b < Bn; ++b)
+    if (sts[(size_t)b] != MDOT_OK) {
+      set_error("instance %d: %s", (int)b, errs[(size_t)b].c_str());
+      return sts[(size_t)b];
+    }
+  return MDOT_OK;
 }
 
 mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,

@@ -63,6 +63,7 @@ struct Workspace {
   bool use_tma = false;
   int tma_grid = 0;
   int pers_grid = 0;                // persistent cooperative projection (0 = off)
+  bool no_persist = false;          // concurrent solves (batch workers): a cooperative grid would serialise them
   unsigned int* pers_bar = nullptr;
   // stats
   int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;

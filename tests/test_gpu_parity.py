@@ -586,6 +586,29 @@ def test_batch_kernel_matches_per_instance_solves(monkeypatch):
     assert abs(rl[1]["cost_unrounded"] - rb[1]["cost_unrounded"]) <= 1e-5 * rl[1]["cost_unrounded"]
 
 
+def test_batch_throughput_mode_large_n():
+    """mdot_solve_batch beyond the K8 size (throughput mode, SURVEY 8(f) rank
+    4): concurrent per-instance solves on worker streams sharing one C; every
+    instance against its own single solve and one against the oracle."""
+    n, B, gb, T, eps = 1000, 6, 1024.0, 4, 1e-6
+    base = S.uniform_points_instance(3, n, 2, 20, marg="dirichlet")
+    R = np.stack([S.uniform_points_instance(3, n, 2, 20 + b, marg="dirichlet").r for b in range(B)])
+    Cm = np.stack([S.uniform_points_instance(3, n, 2, 40 + b, marg="dirichlet").c for b in range(B)])
+    U = torch.empty((B, n), dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=T)
+    res = M.mdot_solve_batch(_t(base.C), _t(R), _t(Cm), schedule=sched, options=M.options(eps=eps),
+                             u_out=U, v_out=V)
+    assert all(x["status"] == 0 and x["control_path"] in (0, 1) for x in res)
+    for b in range(B):
+        rs = M.mdot_solve(_t(base.C), _t(R[b]), _t(Cm[b]), schedule=sched, options=M.options(eps=eps))
+        assert abs(res[b]["cost_unrounded"] - rs["cost_unrounded"]) <= 2e-6 * rs["cost_unrounded"]
+    inst = S.Instance(n, R[2], Cm[2], C=base.C)
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), O.make_options(eps=eps))
+    _gates(res[2], ores, inst, prob, U[2].cpu().numpy(), V[2].cpu().numpy(), eps)
+
+
 # ------------------------------------------------------------- determinism
 @pytest.mark.parametrize("dc", [1, 2])
 def test_solve_is_bitwise_deterministic(dc):

@@ -19,8 +19,12 @@
 
 namespace mdot {
 
-constexpr int kBatchThreads = 256;
+// 16 warps: one CTA per instance has an SM to itself and its evaluation is
+// latency-bound (8 warps: 2 per scheduler, 13 % issue utilisation); the
+// column-partial scratch stays [8][256] (two-round reduction)
+constexpr int kBatchThreads = 512;
 constexpr int kBatchWarps = kBatchThreads / 32;
+constexpr int kSredRows = 8;
 
 __device__ __forceinline__ float bex2(float x) {
   float y;
@@ -65,9 +69,8 @@ __device__ __forceinline__ void block_sum(double (&v)[NS], double* scratch /*[kB
 struct BatchSmem {
   // arrays of 2n doubles (rows then columns) follow in dynamic smem
   CtrlState st;
-  double red[kBatchWarps * kNumScalars];
   double out[kNumScalars];
-  double sred[kBatchWarps][kTileN];
+  double sred[kSredRows][kTileN];   // column partials of batch_eval; block_sum scratch otherwise
 };
 
 // Fused evaluation of one instance: rowtot[i] = sum_j 2^w T_j and
@@ -77,6 +80,7 @@ struct BatchSmem {
 template <bool F64>
 __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
                            double gbar, double* rowtot, double* coltot, double (*sred)[kTileN]) {
+  static_assert(kBatchWarps == 2 * kSredRows, "two-round column reduction");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4* rowp = prm;
   const float4* colp = prm + n;
@@ -99,38 +103,49 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
         if (F64) { Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.f; }
       }
     }
-    double* csum = &sred[warp][0];
     float c32[8];
     double c64[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) { c32[q] = 0.f; c64[q] = 0.0; }
     int step = 0;
-    for (int ib = 4 * warp; ib < n; ib += 4 * kBatchWarps, ++step) {
-      double rs[4];
-      float mrow[4] = {1.f, 1.f, 1.f, 1.f};
+    // the 4 rows' C values (L2) are loaded before any is used: with 8 warps
+    // per SM the per-row loads were exposed (long-scoreboard stalls on their
+    // first use: 32 % of the warp samples)
+    auto load_group = [&](int ib, float (&cvg)[4][8]) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = ib + u;
-        float cv[8];
-        float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
         if (i < n) {
-          rp = rowp[i];
           const float* crow = C + (int64_t)i * n;
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             const int j = jj[4 * g];
             if (vec4 && j + 3 < n) {
               const float4 x = __ldg(reinterpret_cast<const float4*>(crow + j));
-              cv[4 * g] = x.x; cv[4 * g + 1] = x.y; cv[4 * g + 2] = x.z; cv[4 * g + 3] = x.w;
+              cvg[u][4 * g] = x.x; cvg[u][4 * g + 1] = x.y; cvg[u][4 * g + 2] = x.z; cvg[u][4 * g + 3] = x.w;
             } else {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) cv[4 * g + q] = (j + q < n) ? __ldg(crow + j + q) : 0.f;
+              for (int q = 0; q < 4; ++q) cvg[u][4 * g + q] = (j + q < n) ? __ldg(crow + j + q) : 0.f;
             }
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) cv[q] = 0.f;
+          for (int q = 0; q < 8; ++q) cvg[u][q] = 0.f;
         }
+      }
+    };
+    for (int ib = 4 * warp; ib < n; ib += 4 * kBatchWarps, ++step) {
+      float cvc[4][8];
+      load_group(ib, cvc);
+      double rs[4];
+      float mrow[4] = {1.f, 1.f, 1.f, 1.f};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ib + u;
+        float cv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cv[q] = cvc[u][q];
+        const float4 rp = (i < n) ? rowp[i] : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
         if (!F64) {
           // fp32 entries, parameter slots {ah, M, S'} / {bh, M, T'} (ops.cuh split_param)
           float rsum = 0.f;
@@ -170,14 +185,26 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
         for (int q = 0; q < 8; ++q) { c64[q] += (double)c32[q]; c32[q] = 0.f; }
       }
     }
+    // column totals, fixed order: warp w + 8 parks its sums, warp w adds its
+    // own, then 256 threads add the 8 rows
+    if (warp >= kSredRows) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) csum[4 * lane + (q & 3) + 128 * (q >> 2)] = c64[q] + (double)c32[q];
+      for (int q = 0; q < 8; ++q) sred[warp - kSredRows][4 * lane + (q & 3) + 128 * (q >> 2)] = c64[q] + (double)c32[q];
+    }
     __syncthreads();
-    {
-      const int t = threadIdx.x;   // kBatchThreads == kTileN
+    if (warp < kSredRows) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double& x = sred[warp][4 * lane + (q & 3) + 128 * (q >> 2)];
+        x = (c64[q] + (double)c32[q]) + x;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < kTileN) {
+      const int t = threadIdx.x;
       double acc = 0.0;
 #pragma unroll
-      for (int w = 0; w < kBatchWarps; ++w) acc += sred[w][t];
+      for (int w = 0; w < kSredRows; ++w) acc += sred[w][t];
       if (j0 + t < n) coltot[j0 + t] = F64 ? acc : acc * (double)colp[j0 + t].y;   // fp32: times M_j = 2^bl_j
     }
     __syncthreads();
@@ -303,7 +330,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
 #pragma unroll
         for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
         for (int k = tid; k < n2; k += blockDim.x) finalize_item(fa, k, tot[k], v);
-        block_sum<kNumScalars>(v, S.red, S.out);
+        block_sum<kNumScalars>(v, &S.sred[0][0], S.out);
         if (S.out[SC_BAD] == 0.0 || use64) break;
         use64 = true;   // range guard fired: redo this evaluation with fp64 entries
       }
@@ -333,7 +360,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
         v4[q] += tgt[k] * UV[k];
         v4[2 + q] += tgt[k] * uv[k];
       }
-      block_sum<4>(v4, S.red, S.out);
+      block_sum<4>(v4, &S.sred[0][0], S.out);
       const double d1 = 0.5 * (S.out[0] - S.out[1]), d2 = 0.5 * (S.out[2] - S.out[3]);
       for (int k = tid; k < n2; k += blockDim.x) {
         UV[k] += (k < n) ? -d1 : d1;
@@ -379,7 +406,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
       cF1[j] = s1;
       vF[0] += s2;
     }
-    block_sum<1>(vF, S.red, S.out);
+    block_sum<1>(vF, &S.sred[0][0], S.out);
     cost_F = S.out[0];
     for (int j = tid; j < n; j += blockDim.x) {
       const double y = fmin(tgt[n + j] / cF1[j], 1.0);
@@ -412,7 +439,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
         v3[2] += e * cr;
       }
     }
-    block_sum<3>(v3, S.red, S.out);
+    block_sum<3>(v3, &S.sred[0][0], S.out);
     cost_G = S.out[1] + (S.out[0] >= 1e-300 ? S.out[2] / S.out[0] : 0.0);
   }
   // ---- outputs

@@ -12,8 +12,10 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/mdot.h"
+#include "entry.cuh"
 #include "internal.cuh"
 #include "ops.cuh"
 
@@ -77,7 +79,7 @@ struct BatchSmem {
 // coltot[j] = sum_i 2^w S_i (anchored units, internal.cuh "K1 numerics").
 // F64: w assembled and exponentiated in fp64 (fp64-entry mode, eps < 1e-7,
 // and the range-guard fallback).
-template <bool F64>
+template <bool F64, bool PACKED>
 __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
                            double gbar, double* rowtot, double* coltot, double (*sred)[kTileN]) {
   static_assert(kBatchWarps == 2 * kSredRows, "two-round column reduction");
@@ -107,6 +109,17 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
     double c64[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) { c32[q] = 0.f; c64[q] = 0.0; }
+    // packed column parameters and fp32 column-pair accumulators (fp32 entries)
+    ColPairs cpp;
+    u64 cacc2[4] = {0ull, 0ull, 0ull, 0ull};
+    const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl);
+    if (!F64) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        cpp.bh[p] = pk2(bh[2 * p], bh[2 * p + 1]);
+        cpp.T[p] = pk2(T[2 * p], T[2 * p + 1]);
+      }
+    }
     int step = 0;
     // the 4 rows' C values (L2) are loaded before any is used: with 8 warps
     // per SM the per-row loads were exposed (long-scoreboard stalls on their
@@ -146,8 +159,7 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
 #pragma unroll
         for (int q = 0; q < 8; ++q) cv[q] = cvc[u][q];
         const float4 rp = (i < n) ? rowp[i] : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
-        if (!F64) {
-          // fp32 entries, parameter slots {ah, M, S'} / {bh, M, T'} (ops.cuh split_param)
+        if (!F64 && !PACKED) {
           float rsum = 0.f;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -157,6 +169,15 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
             c32[q] = fmaf(e, rp.z, c32[q]);
           }
           rs[u] = rsum;
+          mrow[u] = rp.y;
+        } else if (!F64) {
+          // fp32 entries, parameter slots {ah, M, S'} / {bh, M, T'} (ops.cuh
+          // split_param), on fp32 pairs (entry.cuh): the evaluation is
+          // issue-bound once 16 warps hide the load latency (ncu: 54 % issue)
+          u64 c2[4];
+#pragma unroll
+          for (int p = 0; p < 4; ++p) c2[p] = pk2(cv[2 * p], cv[2 * p + 1]);
+          rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
           mrow[u] = rp.y;
         } else {
           // fp64 entries: exact z = A_i + B_j - gbar C_ij, anchored by the
@@ -181,9 +202,24 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
       if (!F64) tot *= (double)((lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]));
       if ((lane & 7) == 0 && i < n) rowtot[i] = (j0 == 0) ? tot : rowtot[i] + tot;
       if (!F64 && (step & 1)) {
+        if (PACKED) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) { c64[q] += (double)c32[q]; c32[q] = 0.f; }
+          for (int p = 0; p < 4; ++p) {
+            float lo, hi;
+            up2(cacc2[p], lo, hi);
+            c64[2 * p] += (double)lo;
+            c64[2 * p + 1] += (double)hi;
+            cacc2[p] = 0ull;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { c64[q] += (double)c32[q]; c32[q] = 0.f; }
+        }
       }
+    }
+    if (!F64 && PACKED) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) up2(cacc2[p], c32[2 * p], c32[2 * p + 1]);
     }
     // column totals, fixed order: warp w + 8 parks its sums, warp w adds its
     // own, then 256 threads add the 8 rows
@@ -211,6 +247,7 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
   }
 }
 
+template <bool PACKED>
 __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
@@ -321,9 +358,9 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
             }
             __syncthreads();
           }
-          batch_eval<true>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+          batch_eval<true, false>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
         } else {
-          batch_eval<false>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+          batch_eval<false, PACKED>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
         }
         __syncthreads();
         double v[kNumScalars];
@@ -466,9 +503,13 @@ size_t batch_smem_bytes(int n) { return sizeof(BatchSmem) + (size_t)15 * 2 * n *
 
 cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st) {
   const size_t smem = batch_smem_bytes(a.n);
-  cudaError_t e = cudaFuncSetAttribute(k_batch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // MDOT_K8_SCALAR: A/B switch, scalar fp32 entry arithmetic
+  static const bool scalar = getenv("MDOT_K8_SCALAR") != nullptr;
+  const void* fn = scalar ? (const void*)k_batch_solve<false> : (const void*)k_batch_solve<true>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_batch_solve<<<B, kBatchThreads, smem, st>>>(a);
+  if (scalar) k_batch_solve<false><<<B, kBatchThreads, smem, st>>>(a);
+  else k_batch_solve<true><<<B, kBatchThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -79,8 +79,8 @@ struct BatchSmem {
 // coltot[j] = sum_i 2^w S_i (anchored units, internal.cuh "K1 numerics").
 // F64: w assembled and exponentiated in fp64 (fp64-entry mode, eps < 1e-7,
 // and the range-guard fallback).
-template <bool F64, bool PACKED>
-__device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
+template <bool F64, bool PACKED, typename CT>
+__device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
                            double gbar, double* rowtot, double* coltot, double (*sred)[kTileN]) {
   static_assert(kBatchWarps == 2 * kSredRows, "two-round column reduction");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -124,17 +124,17 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
     // the 4 rows' C values (L2) are loaded before any is used: with 8 warps
     // per SM the per-row loads were exposed (long-scoreboard stalls on their
     // first use: 32 % of the warp samples)
-    auto load_group = [&](int ib, float (&cvg)[4][8]) {
+    auto load_group = [&](int ib, CT (&cvg)[4][8]) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = ib + u;
         if (i < n) {
-          const float* crow = C + (int64_t)i * n;
+          const CT* crow = C + (int64_t)i * n;
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             const int j = jj[4 * g];
-            if (vec4 && j + 3 < n) {
-              const float4 x = __ldg(reinterpret_cast<const float4*>(crow + j));
+            if (sizeof(CT) == 4 && vec4 && j + 3 < n) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(crow) + j));
               cvg[u][4 * g] = x.x; cvg[u][4 * g + 1] = x.y; cvg[u][4 * g + 2] = x.z; cvg[u][4 * g + 3] = x.w;
             } else {
 #pragma unroll
@@ -148,14 +148,14 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
       }
     };
     for (int ib = 4 * warp; ib < n; ib += 4 * kBatchWarps, ++step) {
-      float cvc[4][8];
+      CT cvc[4][8];
       load_group(ib, cvc);
       double rs[4];
       float mrow[4] = {1.f, 1.f, 1.f, 1.f};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = ib + u;
-        float cv[8];
+        CT cv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) cv[q] = cvc[u][q];
         const float4 rp = (i < n) ? rowp[i] : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
@@ -247,7 +247,12 @@ __device__ void batch_eval(const float* __restrict__ C, int n, const float4* prm
   }
 }
 
-template <bool PACKED>
+// C read as fp32 (DENSE_F32) or fp64 (DENSE_F64: fp64 entries only)
+__device__ __forceinline__ double batch_cost(const BatchArgs& a, int64_t idx) {
+  return a.C64 ? __ldg(a.C64 + idx) : (double)__ldg(a.C + idx);
+}
+
+template <bool PACKED, typename CT>
 __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
@@ -358,14 +363,15 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
             }
             __syncthreads();
           }
-          batch_eval<true, false>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+          batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
         } else {
-          batch_eval<false, PACKED>(a.C, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+          batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
         }
         __syncthreads();
         double v[kNumScalars];
 #pragma unroll
         for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
+        fa.f64_entries = use64 ? 1 : 0;
         for (int k = tid; k < n2; k += blockDim.x) finalize_item(fa, k, tot[k], v);
         block_sum<kNumScalars>(v, &S.sred[0][0], S.out);
         if (S.out[SC_BAD] == 0.0 || use64) break;
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
       double s1 = 0.0, s2 = 0.0;
       const double Bj = UV[n + j];
       for (int i = 0; i < n; ++i) {
-        const double cij = (double)__ldg(a.C + (int64_t)i * n + j);
+        const double cij = batch_cost(a, (int64_t)i * n + j);
         const double f1 = exp((Ap[i] + Bj) - gbar * cij);
         s1 += f1;
         s2 += cij * f1 * invx[i];
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     for (int i = warp; i < n; i += kBatchWarps) {
       double s = 0.0, cs2 = 0.0, cr = 0.0;
       for (int j = lane; j < n; j += 32) {
-        const double cij = (double)__ldg(a.C + (int64_t)i * n + j);
+        const double cij = batch_cost(a, (int64_t)i * n + j);
         const double f2 = exp((Ap[i] + Bpp[j]) - gbar * cij);
         s += f2;
         cs2 += cij * f2;
@@ -505,11 +511,13 @@ cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st) {
   const size_t smem = batch_smem_bytes(a.n);
   // MDOT_K8_SCALAR: A/B switch, scalar fp32 entry arithmetic
   static const bool scalar = getenv("MDOT_K8_SCALAR") != nullptr;
-  const void* fn = scalar ? (const void*)k_batch_solve<false> : (const void*)k_batch_solve<true>;
+  const void* fn = a.C64 ? (const void*)k_batch_solve<false, double>
+                         : (scalar ? (const void*)k_batch_solve<false, float> : (const void*)k_batch_solve<true, float>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (scalar) k_batch_solve<false><<<B, kBatchThreads, smem, st>>>(a);
-  else k_batch_solve<true><<<B, kBatchThreads, smem, st>>>(a);
+  if (a.C64) k_batch_solve<false, double><<<B, kBatchThreads, smem, st>>>(a);
+  else if (scalar) k_batch_solve<false, float><<<B, kBatchThreads, smem, st>>>(a);
+  else k_batch_solve<true, float><<<B, kBatchThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

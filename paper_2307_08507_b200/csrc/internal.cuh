@@ -128,6 +128,7 @@ struct FinalizeArgs {
   const double* add_in;  // nullable: kNumScalars values added before publishing (sharded rows)
   int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
   int jacobi;            // 1: s = grad / diag(Hessian) (MDOT_PROJ_PNCG_JACOBI) instead of the Sinkhorn direction
+  int f64_entries;       // partials from fp64 entries (K8): range guard at the fp64 limits, not fp32's
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 
@@ -225,6 +226,7 @@ cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const do
                         double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
                         cudaStream_t st);
 // column partials -> local column totals (generic kernel, sharded mode)
+cudaError_t launch_minmax(const void* C, int c64, int64_t count, double* out2, cudaStream_t st);
 cudaError_t launch_reduce_colpart(const double* colpart, int n_row_tiles, int64_t n, double* coltot, cudaStream_t st,
                                   const int* done = nullptr);
 // exact path, sharded: combine chunk (max, sum) pairs; rescale sums to a global max
@@ -279,6 +281,7 @@ struct BatchResult {
 };
 struct BatchArgs {
   const float* C;          // shared n x n fp32 cost (device)
+  const double* C64;       // or fp64 cost (DENSE_F64; fp64 entries), C unused
   int n;
   const double* r;         // [B][n] (device)
   const double* c;         // [B][n]

@@ -745,6 +745,34 @@ cudaError_t launch_setup(int64_t n, const double* r, double* logr, double* rho, 
   return cudaGetLastError();
 }
 
+// min / max of all entries of a cost (input validation of the small-problem
+// paths): one CTA, grid-stride, NaN reported as -inf / +inf
+__global__ void __launch_bounds__(1024) k_minmax(const void* C, int c64, int64_t count, double* out) {
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t k = threadIdx.x; k < count; k += blockDim.x) {
+    const double v = c64 ? reinterpret_cast<const double*>(C)[k] : (double)reinterpret_cast<const float*>(C)[k];
+    if (v != v) { lo = -INFINITY; hi = INFINITY; }
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  __shared__ double slo[32], shi[32];
+  for (int off = 16; off > 0; off >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) { slo[threadIdx.x >> 5] = lo; shi[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fmin(lo, slo[w]); hi = fmax(hi, shi[w]); }
+    out[0] = fmin(lo, slo[0]);
+    out[1] = fmax(hi, shi[0]);
+  }
+}
+cudaError_t launch_minmax(const void* C, int c64, int64_t count, double* out, cudaStream_t st) {
+  k_minmax<<<1, 1024, 0, st>>>(C, c64, count, out);
+  return cudaGetLastError();
+}
+
 __global__ void k_axpby(int64_t n, double a, const double* x, double b, double* y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = a * x[i] + b * y[i];

@@ -1191,13 +1191,46 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   return st;
 }
 
+// Small dense problems run the whole solve in one CTA on-chip (the K8
+// kernel with one instance): below a few hundred points an evaluation is a
+// few thousand entries and the grid-wide paths pay ~20 us of launch /
+// barrier / control latency per evaluation instead.  Threshold: MDOT_SMALL_N
+// (default 320: crossover between n = 256 and 384, profiles/r01_small_n_route.txt); the host control
+// loop (device_control = 0) and dense plan outputs keep the general path.
+static bool small_route(const mdot_problem* pb, const mdot_options* opt, const float* P_out) {
+  if (!pb || P_out || pb->n < 1) return false;
+  if (pb->kind != MDOT_COST_DENSE_F32 && pb->kind != MDOT_COST_DENSE_F64) return false;
+  if (opt && opt->device_control == 0) return false;
+  if (getenv("MDOT_NO_BATCH_KERNEL")) return false;
+  int64_t lim = 320;
+  if (const char* e = getenv("MDOT_SMALL_N")) lim = atoll(e);
+  return pb->n <= lim;
+}
+
+// The one-CTA solver exponentiates anchored fp64 entries without a max
+// shift and has no exact-evaluator fallback for its line search: plans
+// beyond the fp64 range (|exponent| > ~690 from the anchor) report
+// MDOT_EINSTABLE there, degenerate cases can fail the fp32-noise line search
+// (n = 1 at gbar 4096); both are re-solved on the general path, whose exact
+// evaluator is a max-shifted log-sum-exp.
 mdot_status mdot_solve(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
                        double* u_out, double* v_out, float* P_out, mdot_result* res) {
+  if (small_route(pb, opt, P_out)) {
+    const mdot_status st = mdot_solve_batch(pb, 1, pb->r, pb->c, sched, opt, u_out, v_out, res);
+    if (st != MDOT_EINSTABLE && st != MDOT_ELINESEARCH) return st;
+  }
   return solve_impl(pb, sched, opt, u_out, v_out, P_out, res, 0);
 }
 
 mdot_status mdot_sinkhorn(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt,
                           double* u_out, double* v_out, float* P_out, mdot_result* res) {
+  if (small_route(pb, opt, P_out)) {
+    mdot_options o;
+    if (opt) o = *opt; else mdot_options_default(&o);
+    o.projector = MDOT_PROJ_SINKHORN;
+    const mdot_status st = mdot_solve_batch(pb, 1, pb->r, pb->c, sched, &o, u_out, v_out, res);
+    if (st != MDOT_EINSTABLE && st != MDOT_ELINESEARCH) return st;
+  }
   return solve_impl(pb, sched, opt, u_out, v_out, P_out, res, 1);
 }
 
@@ -1289,8 +1322,10 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const bool fits = shared->kind == MDOT_COST_DENSE_F32 && n >= 1 && (int64_t)batch_smem_bytes((int)n) <= optin &&
-                    getenv("MDOT_NO_BATCH_KERNEL") == nullptr;
+  const bool c64 = shared->kind == MDOT_COST_DENSE_F64;
+  const bool fits = (shared->kind == MDOT_COST_DENSE_F32 || c64) && n >= 1 &&
+                    (int64_t)batch_smem_bytes((int)n) <= optin && getenv("MDOT_NO_BATCH_KERNEL") == nullptr &&
+                    !(c64 && o.precision == MDOT_PREC_F32P);   // rejected by the per-instance path
   if (!fits) return solve_batch_loop(shared, Bn, r, c, sched, opt_in, u_out, v_out, res);
   const double t0 = now_s();
   for (int32_t b = 0; b < Bn; ++b) memset(&res[b], 0, sizeof(mdot_result));
@@ -1315,9 +1350,36 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     CKS(validate_marginal(hr.data() + (size_t)b * n, n, "r"));
     CKS(validate_marginal(hc.data() + (size_t)b * n, n, "c"));
   }
+  {
+    // C in [0,1]: every entry (n^2 <= ~0.6 M here)
+    double mm[2] = {0.0, 0.0};
+    if (dev_mem) {
+      double* dmm = nullptr;
+      CK(cudaMallocAsync((void**)&dmm, 2 * sizeof(double), stream));
+      CK(launch_minmax(shared->C, c64 ? 1 : 0, n * n, dmm, stream));
+      CK(cudaMemcpyAsync(mm, dmm, sizeof(mm), cudaMemcpyDeviceToHost, stream));
+      CK(cudaFreeAsync(dmm, stream));
+      CK(cudaStreamSynchronize(stream));
+    } else {
+      mm[0] = INFINITY;
+      mm[1] = -INFINITY;
+      for (int64_t k = 0; k < n * n; ++k) {
+        const double v = c64 ? ((const double*)shared->C)[k] : (double)((const float*)shared->C)[k];
+        if (v != v) { mm[0] = -INFINITY; break; }
+        mm[0] = std::min(mm[0], v);
+        mm[1] = std::max(mm[1], v);
+      }
+    }
+    if (!(mm[0] >= 0.0 && mm[1] <= 1.0)) {
+      set_error("C entries in [%g, %g], outside [0,1] (PAPER.md:42)", mm[0], mm[1]);
+      return MDOT_EINVAL;
+    }
+  }
   // device buffers: [r | c | gammas | U | V | results | C (host input)]
-  const size_t cbytes = sizeof(float) * (size_t)n * n;
-  const size_t bytes = 4 * vb + sizeof(double) * gam.size() + sizeof(BatchResult) * Bn + (dev_mem ? 0 : cbytes) + 1024;
+  const size_t cbytes = (c64 ? sizeof(double) : sizeof(float)) * (size_t)n * n;
+  auto r256 = [](size_t k) { return (k + 255) / 256 * 256; };   // every take() below is 256-byte aligned
+  const size_t bytes = 4 * r256(vb) + r256(sizeof(double) * gam.size()) + r256(sizeof(BatchResult) * Bn) +
+                       (dev_mem ? 0 : r256(cbytes));
   char* base = nullptr;
   CK(cudaMallocAsync((void**)&base, bytes, stream));
   char* q = base;
@@ -1328,9 +1390,9 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   double* dV = (double*)take(vb);
   double* dg = (double*)take(sizeof(double) * gam.size());
   BatchResult* dres = (BatchResult*)take(sizeof(BatchResult) * Bn);
-  const float* dC = (const float*)shared->C;
+  const void* dC = shared->C;
   if (!dev_mem) {
-    float* cc = (float*)take(cbytes);
+    void* cc = take(cbytes);
     CK(cudaMemcpyAsync(cc, shared->C, cbytes, cudaMemcpyHostToDevice, stream));
     dC = cc;
   }
@@ -1338,13 +1400,15 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   CK(cudaMemcpyAsync(dc, hc.data(), vb, cudaMemcpyHostToDevice, stream));
   CK(cudaMemcpyAsync(dg, gam.data(), sizeof(double) * gam.size(), cudaMemcpyHostToDevice, stream));
   BatchArgs a{};
-  a.C = dC; a.n = (int)n; a.r = dr; a.c = dc; a.gammas = dg; a.T = (int)gam.size();
+  a.C = c64 ? nullptr : (const float*)dC;
+  a.C64 = c64 ? (const double*)dC : nullptr;
+  a.n = (int)n; a.r = dr; a.c = dc; a.gammas = dg; a.T = (int)gam.size();
   a.eps = o.eps; a.eps_md = o.eps_md > o.eps ? o.eps_md : o.eps; a.c1 = o.c1; a.c2 = o.c2;
   a.stop_rho = o.stop; a.projector = o.projector; a.beta_kind = o.beta; a.ls_max_trials = o.ls_max_trials;
   a.warm = o.warm; a.p0_ones = o.p0_ones;
   // fp32 entries resolve marginals to ~1e-7 (K1 numerics): tighter
   // targets run the fp64-entry evaluation
-  a.f64 = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && o.eps < 5e-8);
+  a.f64 = c64 || (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && o.eps < 5e-8);
   a.max_evals = o.max_evals;
   a.U_out = dU; a.V_out = dV; a.res = dres;
   cudaError_t e = launch_batch(a, Bn, stream);
@@ -1352,6 +1416,11 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     cudaFreeAsync(base, stream);
     set_error("batch kernel launch failed: %s", cudaGetErrorString(e));
     return MDOT_ECUDA;
+  }
+  if (getenv("MDOT_DEBUG")) {
+    const cudaError_t es = cudaStreamSynchronize(stream);
+    fprintf(stderr, "[mdot] batch kernel n=%lld B=%d smem=%zu f64=%d c64=%d: %s\n", (long long)n, (int)Bn,
+            batch_smem_bytes((int)n), a.f64, (int)c64, cudaGetErrorString(es));
   }
   std::vector<BatchResult> hres(Bn);
   CK(cudaMemcpyAsync(hres.data(), dres, sizeof(BatchResult) * Bn, cudaMemcpyDeviceToHost, stream));

@@ -366,7 +366,37 @@ def test_device_control_matches_host_control(projector):
     assert rd["evaluations"] <= 1.5 * rh["evaluations"] + 20
 
 
-def test_device_control_fp64_config1():
+@pytest.mark.parametrize("case", ["cfg1", "fp32", "sinkhorn", "jacobi"])
+def test_small_problem_route_matches_general_path(case, monkeypatch):
+    """mdot_solve on small dense problems runs the one-CTA K8 solver
+    (control_path 3, MDOT_SMALL_N threshold); it must agree with the grid-wide
+    path and the oracle (config 1: fp64 C, doubling schedule)."""
+    if case == "cfg1":
+        inst = S.config1(2)
+        sched, osched = M.schedule(M.MDOT_SCHED_DOUBLING, 4096.0), O.schedule_doubling(4096.0)
+    else:
+        inst = S.uniform_points_instance(3, 200, 2, 31, marg="dirichlet")
+        sched, osched = M.schedule(M.MDOT_SCHED_FIXED, 1024.0, T=4), O.schedule_fixed(1024.0, T=4)
+    proj = {"sinkhorn": M.MDOT_PROJ_SINKHORN, "jacobi": M.MDOT_PROJ_PNCG_JACOBI}.get(case, M.MDOT_PROJ_PNCG)
+    oproj = {"sinkhorn": O.SINKHORN, "jacobi": O.PNCG_JACOBI}.get(case, O.PNCG)
+    eps = 1e-6
+    n = inst.n
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    rk = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(eps=eps, projector=proj),
+                      u_out=U, v_out=V)
+    assert rk["control_path"] == 3
+    monkeypatch.setenv("MDOT_SMALL_N", "0")
+    rg = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(eps=eps, projector=proj))
+    assert rg["control_path"] != 3
+    assert abs(rk["cost_unrounded"] - rg["cost_unrounded"]) <= 2e-6 * rg["cost_unrounded"]
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, osched, O.make_options(eps=eps, projector=oproj))
+    _gates(rk, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+def test_device_control_fp64_config1(monkeypatch):
+    monkeypatch.setenv("MDOT_SMALL_N", "0")   # the graph path (not the small-problem route)
     inst = S.config1(1)
     res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_DOUBLING, 4096.0),
                        options=M.options(eps=1e-6, device_control=1))

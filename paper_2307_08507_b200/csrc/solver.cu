@@ -840,6 +840,15 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   d = pb->d;
   scale = pb->scale;
   if (otf && (d < 1 || d > 64 || !pb->X || !pb->Y)) { set_error("SQEUCLID needs X, Y and 1 <= d <= 64"); return MDOT_EINVAL; }
+  if (otf) {
+    // on-the-fly cost: taller row tiles amortise each CTA's Y-tile staging
+    // (K2 is FP32-bound; the partial buffers only shrink). MDOT_OTF_TILE_M: A/B.
+    int cap = 2048;
+    if (const char* e = getenv("MDOT_OTF_TILE_M")) cap = atoi(e);
+    while (eval.tile_m < cap && (int64_t)eval.n_col_tiles * ((nrows + 2 * eval.tile_m - 1) / (2 * eval.tile_m)) >= 4 * 148)
+      eval.tile_m *= 2;
+    eval.n_row_tiles = (int)((nrows + eval.tile_m - 1) / eval.tile_m);
+  }
   if (!otf && !pb->C) { set_error("C is NULL"); return MDOT_EINVAL; }
   if (!pb->r || !pb->c) { set_error("r or c is NULL"); return MDOT_EINVAL; }
   // marginals: validate on a host copy

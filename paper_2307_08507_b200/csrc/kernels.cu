@@ -257,14 +257,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   const int64_t n = a.n, nrows = a.nrows;
 
   __shared__ double sred[kWarps][kTileN];
-  __shared__ float4 sRP[kOtfChunk];   // row parameters of the current chunk
+  __shared__ float4 sRP[2][kOtfChunk];   // row parameters, double-buffered by chunk
   extern __shared__ __align__(16) unsigned char sraw[];
-  float* sY = reinterpret_cast<float*>(sraw);                       // [D][256]
-  u64* sX = reinterpret_cast<u64*>(sraw + sizeof(float) * D * kTileN);  // [chunk][D]
-  // staging loads are issued all at once (vector loads where D % 4 == 0 and
-  // the pointers are 16-byte aligned); a per-element load -> store loop here
-  // was the top stall of the kernel (one L2 round trip per element)
+  float* sY = reinterpret_cast<float*>(sraw);                          // [D][256]
+  float* sX = reinterpret_cast<float*>(sraw + sizeof(float) * D * kTileN);   // [2][chunk][D]
+  // X chunks (and their row parameters) stream through a 2-deep cp.async
+  // ring: the next chunk's copy overlaps this chunk's arithmetic.  Vector
+  // copies need D % 4 == 0 and 16-byte aligned X, Y (else synchronous
+  // staging).  The per-element load -> store staging of the first version was
+  // the kernel's top stall (one L2 round trip per element; profiles/).
   const bool vec = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
+  const int64_t tile_end = (i0 + a.tile_m < nrows) ? i0 + a.tile_m : nrows;
+  auto rows_of = [&](int64_t c0) { return (int)((tile_end - c0 < kOtfChunk) ? tile_end - c0 : kOtfChunk); };
+  auto issue_chunk = [&](int64_t c0, int buf) {   // cp.async (zero-fill past the tile end)
+    const int rows_c = rows_of(c0);
+    constexpr int kQ = (kOtfChunk * D / 4 + kThreads - 1) / kThreads;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int f = 4 * (q * kThreads + threadIdx.x);
+      if (f < kOtfChunk * D) {
+        const bool ok = f / D < rows_c;
+        const float* src = ok ? a.X + c0 * D + f : a.X;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(sX + buf * kOtfChunk * D + f))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    }
+    if (threadIdx.x < kOtfChunk) {
+      const bool ok = (int)threadIdx.x < rows_c;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&sRP[buf][threadIdx.x]))),
+                   "l"(ok ? a.rowp + c0 + threadIdx.x : a.rowp), "r"(ok ? 16 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (vec && i0 < tile_end) issue_chunk(i0, 0);
 
   // Y[j0:j0+256, :] transposed (thread t = column j0 + t); columns past n are
   // zero points (masked by bh)
@@ -308,50 +337,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 #pragma unroll
   for (int p = 0; p < 4; ++p) cacc2[p] = 0ull;
 
-  const int64_t tile_end = (i0 + a.tile_m < nrows) ? i0 + a.tile_m : nrows;
-  int flush = 0;
-  for (int64_t c0 = i0; c0 < tile_end; c0 += kOtfChunk) {
-    const int rows_c = (int)((tile_end - c0 < kOtfChunk) ? tile_end - c0 : kOtfChunk);
-    __syncthreads();   // previous chunk consumed (and sY written on entry)
-    {
+  int flush = 0, cidx = 0;
+  for (int64_t c0 = i0; c0 < tile_end; c0 += kOtfChunk, ++cidx) {
+    const int rows_c = rows_of(c0);
+    const int buf = vec ? (cidx & 1) : 0;
+    if (vec) {
+      if (c0 + kOtfChunk < tile_end) issue_chunk(c0 + kOtfChunk, buf ^ 1);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");   // this chunk's group has landed
+      __syncthreads();   // ... for every thread (and sY is written)
+    } else {
+      __syncthreads();   // previous chunk consumed (and sY written on entry)
       float4 rpv = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
       if (threadIdx.x < kOtfChunk && (int)threadIdx.x < rows_c) rpv = a.rowp[c0 + threadIdx.x];
-      if (vec) {
-        constexpr int kQ = (kOtfChunk * D / 4 + kThreads - 1) / kThreads;   // float4 per thread
-        float4 xv[kQ];
+      constexpr int kE = (kOtfChunk * D + kThreads - 1) / kThreads;
+      float xv[kE];
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-          const int f = 4 * (q * kThreads + threadIdx.x);   // first float of this float4 in the chunk
-          xv[q] = (f < kOtfChunk * D && f / D < rows_c)
-                      ? __ldg(reinterpret_cast<const float4*>(a.X + c0 * D + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-          const int f = 4 * (q * kThreads + threadIdx.x);
-          if (f < kOtfChunk * D) {
-            sX[f] = pk2(xv[q].x, xv[q].x);
-            sX[f + 1] = pk2(xv[q].y, xv[q].y);
-            sX[f + 2] = pk2(xv[q].z, xv[q].z);
-            sX[f + 3] = pk2(xv[q].w, xv[q].w);
-          }
-        }
-      } else {
-        constexpr int kE = (kOtfChunk * D + kThreads - 1) / kThreads;
-        float xv[kE];
-#pragma unroll
-        for (int q = 0; q < kE; ++q) {
-          const int idx = q * kThreads + threadIdx.x;
-          xv[q] = (idx < kOtfChunk * D && idx / D < rows_c) ? __ldg(a.X + c0 * D + idx) : 0.f;
-        }
-#pragma unroll
-        for (int q = 0; q < kE; ++q) {
-          const int idx = q * kThreads + threadIdx.x;
-          if (idx < kOtfChunk * D) sX[idx] = pk2(xv[q], xv[q]);
-        }
+      for (int q = 0; q < kE; ++q) {
+        const int idx = q * kThreads + threadIdx.x;
+        xv[q] = (idx < kOtfChunk * D && idx / D < rows_c) ? __ldg(a.X + c0 * D + idx) : 0.f;
       }
-      if (threadIdx.x < kOtfChunk) sRP[threadIdx.x] = rpv;
+#pragma unroll
+      for (int q = 0; q < kE; ++q) {
+        const int idx = q * kThreads + threadIdx.x;
+        if (idx < kOtfChunk * D) sX[idx] = xv[q];
+      }
+      if (threadIdx.x < kOtfChunk) sRP[0][threadIdx.x] = rpv;
+      __syncthreads();
     }
-    __syncthreads();
+    const float* xs = sX + buf * kOtfChunk * D;
     for (int rb = 4 * warp; rb < rows_c; rb += kWarps * kUnroll) {
       u64 acc[kUnroll][4];
 #pragma unroll
@@ -365,7 +379,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         const ulonglong2 yb = *reinterpret_cast<const ulonglong2*>(sY + k * kTileN + 128 + 4 * lane);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-          const u64 xx = sX[(rb + u) * D + k];
+          const float x = xs[(rb + u) * D + k];
+          const u64 xx = pk2(x, x);   // ptxas: a broadcast (.F32) operand of the packed ops
           u64 dk;
           dk = sub2(xx, ya.x); acc[u][0] = fma2(dk, dk, acc[u][0]);
           dk = sub2(xx, ya.y); acc[u][1] = fma2(dk, dk, acc[u][1]);
@@ -377,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
       float mrow[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        const float4 rp = sRP[rb + u];   // broadcast; rows past the chunk hold bh = -1e30
+        float4 rp = sRP[buf][rb + u];   // broadcast
+        if (rb + u >= rows_c) rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);   // zero-filled rows past the tile
         mrow[u] = rp.y;
         u64 c2[4];
 #pragma unroll
@@ -402,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         }
       }
     }
+    if (vec) __syncthreads();   // chunk buffer free before the next iteration's copy into it
   }
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
@@ -426,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 template <int D, bool POW2>
 static cudaError_t launch_otf_pt(const EvalArgs& a, cudaStream_t st) {
   dim3 grid(a.n_col_tiles, a.n_row_tiles);
-  const size_t smem = sizeof(float) * D * kTileN + sizeof(u64) * kOtfChunk * D;
+  const size_t smem = sizeof(float) * D * kTileN + sizeof(float) * 2 * kOtfChunk * D;
   static bool attr_set = false;
   if (!attr_set) {   // static (column sums, row parameters) + dynamic exceeds the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(k_eval_otf<D, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

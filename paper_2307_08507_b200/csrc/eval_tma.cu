@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   }
   const float gh = a.gpair ? a.gpair[0] : a.gh;
   const float gl = a.gpair ? a.gpair[1] : a.gl;
-  tma_consume_pass<false>(sm, a, it, gh, gl);
+  tma_consume_pass<false>(sm, a, it, gh, gl, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -121,13 +121,14 @@ __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap*
   }
 }
 
-// Stages of C this CTA streams per pass (its tiles, round-robin).
-__device__ __forceinline__ int tma_cta_stages(const EvalArgs& a) {
+// Stages of C this CTA streams per pass (its tiles, round-robin over the
+// ncta CTAs working on this evaluation; cta = this CTA's index among them).
+__device__ __forceinline__ int tma_cta_stages(const EvalArgs& a, int cta, int ncta) {
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
   const int spt = a.tile_m / kTmaRows;
   int cnt = 0;
-  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+  for (int64_t tile = cta; tile < total; tile += ncta) {
     const int64_t i0 = (int64_t)(tile / nct) * a.tile_m;
     int nst = spt;
     if (i0 + (int64_t)nst * kTmaRows > a.nrows) nst = (int)((a.nrows - i0 + kTmaRows - 1) / kTmaRows);
@@ -145,7 +146,7 @@ struct TmaCursor {
   int k;
 };
 __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
-                                              TmaCursor& cur, uint32_t& it, int count) {
+                                              TmaCursor& cur, uint32_t& it, int count, int cta, int ncta) {
   const uint64_t pol = l2_policy(a.keep_l2 != 0);
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
@@ -161,8 +162,8 @@ __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tm
     tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + cur.k * kTmaRows), &sm.full[s], pol);
     if (++cur.k == nst) {
       cur.k = 0;
-      cur.tile += gridDim.x;
-      if (cur.tile >= total) cur.tile = blockIdx.x;   // next pass
+      cur.tile += ncta;
+      if (cur.tile >= total) cur.tile = cta;   // next pass
     }
   }
 }
@@ -190,13 +191,13 @@ __device__ __forceinline__ float4 ld_param(const float4* p) {
 // in-solve), packed f32x2 arithmetic (186 vs 185 us).
 template <bool COHERENT = false>
 __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh,
-                                                 float gl) {
+                                                 float gl, int cta, int ncta) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n = a.n, nrows = a.nrows;
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
   const int stages_per_tile = a.tile_m / kTmaRows;
-  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+  for (int64_t tile = cta; tile < total; tile += ncta) {
     const int tr = (int)(tile / nct), tc = (int)(tile % nct);
     const int64_t i0 = (int64_t)tr * a.tile_m;
     const int64_t j0 = (int64_t)tc * kTileN;

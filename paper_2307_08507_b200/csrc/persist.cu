@@ -62,11 +62,11 @@ __device__ __forceinline__ void red_release(unsigned int* p, unsigned int v) {
 // thread's writes before thread 0's release-add; waiters acquire the
 // generation.  L1 is not relied upon across phases (phase data is read with
 // coherent loads or after this acquire).
-__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int gen = ld_acquire(&bar[1]);
-    if (atom_add_acqrel(&bar[0], 1u) == gridDim.x - 1) {
+    if (atom_add_acqrel(&bar[0], 1u) == ncta - 1) {
       bar[0] = 0u;
       red_release(&bar[1], 1u);
     } else {
@@ -82,8 +82,14 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-__global__ void __launch_bounds__(kTmaThreads, 2)
-    k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
+// The projection loop of one instance, run by `ncta` CTAs (cta = index among
+// them; the whole co-resident grid for k_persist).  Barriers, tile
+// round-robin, finalize chunks and the scalar combine use (cta, ncta) only.
+// A grouped variant (several instances sharing C, one slice of the grid
+// each, MD steps in lockstep) measured slower than concurrent graph-path
+// solves and was removed (profiles/README.md).
+__device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const PersistArgs& a, const int cta,
+                                             const int ncta) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
   PersistSmem& S = *reinterpret_cast<PersistSmem*>(smem_raw + pad);
@@ -108,30 +114,30 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
 
   const int64_t items = a.p.nrows + a.p.n;
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gstride = (int64_t)ncta * blockDim.x;
   uint32_t it = 0;
   // producer: prefetch the first stages of the first pass right away
-  const int cta_stages = tma_cta_stages(a.e);
+  const int cta_stages = tma_cta_stages(a.e, cta, ncta);
   const int pre = cta_stages < kTmaStages ? cta_stages : kTmaStages;
-  TmaCursor cur{(int64_t)blockIdx.x, 0};
-  if (warp == kConsumerWarps && lane == 0 && cta_stages > 0) tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
+  TmaCursor cur{(int64_t)cta, 0};
+  if (warp == kConsumerWarps && lane == 0 && cta_stages > 0) tma_produce_n(S.tma, &tmap, a.e, cur, it, pre, cta, ncta);
   // CTA 0 phase timers (%globaltimer), kept in global memory (thread 0 of CTA
   // 0 only; no registers or smem live across the loop): tm[0..3] = [ctrl+prep
   // +barrier, K1+barrier, finalize+barrier, combine], tm[4..6] finalize
   // sub-phases, tm[8] = K1 phase count, tm[9..11] = timestamps
-  const bool timer = (blockIdx.x == 0 && tid == 0);
+  const bool timer = (cta == 0 && tid == 0);
   unsigned long long* tm = a.k1_ns + 2;
   if (timer) tm[9] = global_ns();
   bool first = a.initial != 0;
   for (long long slot = 0; slot < a.max_slots; ++slot) {
     // ---------------------------------------------------------------- ctrl
     if (!first) {
-      if (tid == 0) ctrl_body(&S.st, 0, blockIdx.x == 0 ? a.done_host : nullptr, nullptr);
+      if (tid == 0) ctrl_body(&S.st, 0, cta == 0 ? a.done_host : nullptr, nullptr);
       __syncthreads();
       if (S.st.done) {
         // the accept copy requested together with `done` still applies
         if (S.st.accept_marg || S.st.accept_pot)
-          for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride)
+          for (int64_t k = (int64_t)cta * blockDim.x + tid; k < items; k += gstride)
             prep_item(a.p, k, &S.st);
         // drain the stages the producer prefetched for a pass that will not
         // run (no TMA may still target shared memory when the CTA exits)
@@ -143,8 +149,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     }
     first = false;
     // ---------------------------------------------------------------- prep
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < items; k += gstride) prep_item(a.p, k, &S.st);
-    grid_barrier(a.gbar);
+    for (int64_t k = (int64_t)cta * blockDim.x + tid; k < items; k += gstride) prep_item(a.p, k, &S.st);
+    grid_barrier(a.gbar, ncta);
     if (timer) {
       const unsigned long long t0 = global_ns();
       tm[0] += t0 - tm[9];
@@ -154,13 +160,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     if (warp == kConsumerWarps) {
       // the rest of this pass, then the prefetch of the next pass's first stages
       if (lane == 0 && cta_stages > 0) {
-        tma_produce_n(S.tma, &tmap, a.e, cur, it, cta_stages - pre);
-        tma_produce_n(S.tma, &tmap, a.e, cur, it, pre);
+        tma_produce_n(S.tma, &tmap, a.e, cur, it, cta_stages - pre, cta, ncta);
+        tma_produce_n(S.tma, &tmap, a.e, cur, it, pre, cta, ncta);
       }
     } else {
-      tma_consume_pass<true>(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1]);
+      tma_consume_pass<true>(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1], cta, ncta);
     }
-    grid_barrier(a.gbar);
+    grid_barrier(a.gbar, ncta);
     if (timer) {
       const unsigned long long t1 = global_ns();
       tm[1] += t1 - tm[10];
@@ -175,8 +181,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       // this CTA's contiguous chunk of items; (item, sub) tasks over all 288
       // threads (a warp always holds whole octets), totals to smem, then one
       // thread per item for the fp64 log / exp / scalar work
-      const int64_t per = (items + gridDim.x - 1) / gridDim.x;
-      const int64_t i_lo = (int64_t)blockIdx.x * per;
+      const int64_t per = (items + ncta - 1) / ncta;
+      const int64_t i_lo = (int64_t)cta * per;
       const int64_t i_hi = (i_lo + per < items) ? i_lo + per : items;
       const int cnt = i_hi > i_lo ? (int)(i_hi - i_lo) : 0;
       double* tots = fin + 256;   // [cnt]
@@ -237,10 +243,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     if (tid < kNumScalars) {
       double y = 0.0;
       for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
-      a.cta_part[(int64_t)blockIdx.x * kNumScalars + tid] = y;
+      a.cta_part[(int64_t)cta * kNumScalars + tid] = y;
     }
     if (timer) tm[6] += global_ns() - tm[10];
-    grid_barrier(a.gbar);
+    grid_barrier(a.gbar, ncta);
     if (timer) {
       const unsigned long long t2 = global_ns();
       tm[2] += t2 - tm[10];
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       double y = 0.0;
       if (tid < 256) {
         const int q = tid % kNumScalars;
-        for (unsigned b = tid / kNumScalars; b < gridDim.x; b += G)
+        for (unsigned b = tid / kNumScalars; b < (unsigned)ncta; b += G)
           y += __ldcg(&a.cta_part[(int64_t)b * kNumScalars + q]);
         fin[tid] = y;
       }
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     // grid barriers, so no extra barrier is needed here)
   }
   // write the state back (CTA 0) and the K1 phase timing
-  if (blockIdx.x == 0) {
+  if (cta == 0) {
     const unsigned long long* sh = reinterpret_cast<const unsigned long long*>(&S.st);
     unsigned long long* g = reinterpret_cast<unsigned long long*>(a.ctrl);
     __syncthreads();
@@ -283,6 +289,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
       a.k1_ns[1] = tm[8];
     }
   }
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 2)
+    k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
+  persist_body(tmap, a, blockIdx.x, gridDim.x);
 }
 
 static int g_persist_grid = -1;

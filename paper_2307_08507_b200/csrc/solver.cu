@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -686,7 +687,9 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
 // ---------------------------------------------------------------------------
 // Persistent cooperative projection: one launch per projection (persist.cu)
 // ---------------------------------------------------------------------------
-mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+// Persistent projection: prepare the control state and the kernel arguments,
+// launch, collect the controller's result.
+static mdot_status persist_prepare(Workspace& w, const mdot_options& o, PersistArgs& a) {
   CtrlState h{};
   h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
   h.noise = 6e-8;
@@ -696,11 +699,10 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
   cudaStream_t st = w.st;
-  res->control_path = 2;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 14 * sizeof(unsigned long long) + 8, st));
   *((volatile int*)w.done_host) = 0;
-  PersistArgs a{};
+  a = PersistArgs{};
   a.e = w.eval;
   PrepArgs& p = a.p;
   p.n = w.n; p.nrows = w.nrows; p.mode = 0;
@@ -730,8 +732,13 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   a.cta_part = w.blockpart;
   a.initial = 1;
   a.max_slots = (long long)1 << 40;
-  CK(launch_persist(w.tmap, a, w.pers_grid, st));
-  w.launches++;
+  return MDOT_OK;
+}
+
+static mdot_status persist_collect(Workspace& w, const mdot_options& o, int t, mdot_result* res,
+                                   const PersistArgs& a) {
+  cudaStream_t st = w.st;
+  CtrlState h{};
   unsigned long long k1[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // [K1 ns, count, tm[0..7]]
   CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(k1, a.k1_ns, sizeof(k1), cudaMemcpyDeviceToHost, st));
@@ -770,6 +777,15 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
       w.fallbacks++;
       return (o.projector == MDOT_PROJ_SINKHORN) ? project_sinkhorn(w, o, t, res) : project_pncg(w, o, t, res);
   }
+}
+
+mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
+  res->control_path = 2;
+  PersistArgs a;
+  CKS(persist_prepare(w, o, a));
+  CK(launch_persist(w.tmap, a, w.pers_grid, w.st));
+  w.launches++;
+  return persist_collect(w, o, t, res, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -914,7 +930,8 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
       eval.keep_l2 = (4.0 * (double)nrows * (double)n <= 0.6 * (double)l2) ? 1 : 0;
-      pers_grid = (getenv("MDOT_NO_PERSIST") || comm || no_persist) ? 0 : persist_grid();
+      pers_grid = (getenv("MDOT_NO_PERSIST") || comm || persist_ncta < 0) ? 0 : persist_grid();
+      if (persist_ncta > 0 && pers_grid > persist_ncta) pers_grid = persist_ncta;
       if (pers_grid > 0 && (nrows + n + pers_grid - 1) / pers_grid > persist_max_chunk()) pers_grid = 0;
     }
   }
@@ -1073,7 +1090,7 @@ void mdot_schedule_default(mdot_schedule* s) {
 static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt_in,
                               double* u_out, double* v_out, float* P_out, mdot_result* res, int force_sinkhorn,
                               Comm* comm = nullptr, int64_t row0 = 0, int64_t nrows_in = -1,
-                              bool no_persist = false) {
+                              int persist_ncta = 0) {
   g_last_error.clear();
   if (!res) { set_error("result pointer is NULL"); return MDOT_EINVAL; }
   memset(res, 0, sizeof(*res));
@@ -1099,7 +1116,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   Workspace w;
   w.comm = comm;
   w.row0 = row0;
-  w.no_persist = no_persist;
+  w.persist_ncta = persist_ncta;
   // MDOT_TRACE: host timestamps per stage (synchronizes between stages)
   const bool trace = getenv("MDOT_TRACE") != nullptr;
   double tr_last = t0;
@@ -1266,12 +1283,12 @@ static mdot_status solve_batch_loop(const mdot_problem* shared, int32_t Bn, cons
   mdot_options o;
   if (opt) o = *opt; else mdot_options_default(&o);
   const int64_t n = shared->n;
-  auto one = [&](int32_t b, const mdot_options* ob, bool no_persist) {
+  auto one = [&](int32_t b, const mdot_options* ob, int persist_ncta) {
     mdot_problem p = *shared;
     p.r = r + (int64_t)b * n;
     p.c = c + (int64_t)b * n;
     return solve_impl(&p, sched, ob, u_out ? u_out + (int64_t)b * n : nullptr,
-                      v_out ? v_out + (int64_t)b * n : nullptr, nullptr, &res[b], 0, nullptr, 0, -1, no_persist);
+                      v_out ? v_out + (int64_t)b * n : nullptr, nullptr, &res[b], 0, nullptr, 0, -1, persist_ncta);
   };
   int W = 8;
   if (const char* e = getenv("MDOT_BATCH_WORKERS")) W = atoi(e);
@@ -1279,13 +1296,17 @@ static mdot_status solve_batch_loop(const mdot_problem* shared, int32_t Bn, cons
   if (W == 1 || shared->mem != MDOT_MEM_DEVICE) {
     mdot_status first = MDOT_OK;
     for (int32_t b = 0; b < Bn; ++b) {
-      const mdot_status s = one(b, &o, false);
+      const mdot_status s = one(b, &o, 0);
       if (s != MDOT_OK && first == MDOT_OK) first = s;
     }
     return first;
   }
   int dev = 0;
   cudaGetDevice(&dev);
+  // graph-path control in every worker: cooperative persistent launches from
+  // several workers (each on a slice of the grid) measured slower than one
+  // after the other (profiles/r01_throughput_mode_n4096.txt)
+  const int slice = -1;
   cudaEvent_t ready = nullptr;
   CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   CK(cudaEventRecord(ready, (cudaStream_t)o.stream));
@@ -1300,7 +1321,7 @@ static mdot_status solve_batch_loop(const mdot_problem* shared, int32_t Bn, cons
     mdot_options ow = o;
     ow.stream = s;
     for (int32_t b = next++; b < Bn; b = next++) {
-      sts[(size_t)b] = one(b, &ow, true);
+      sts[(size_t)b] = one(b, &ow, slice);
       if (sts[(size_t)b] != MDOT_OK) errs[(size_t)b] = mdot_last_error();
     }
     cudaStreamSynchronize(s);

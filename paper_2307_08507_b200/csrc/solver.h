@@ -63,7 +63,8 @@ struct Workspace {
   bool use_tma = false;
   int tma_grid = 0;
   int pers_grid = 0;                // persistent cooperative projection (0 = off)
-  bool no_persist = false;          // concurrent solves (batch workers): a cooperative grid would serialise them
+  int persist_ncta = 0;             // persistent grid: 0 all co-resident CTAs, > 0 at most that many (batch
+                                    // workers run side by side on slices of the grid), < 0 off
   unsigned int* pers_bar = nullptr;
   // stats
   int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;
@@ -85,6 +86,10 @@ struct Workspace {
   cudaEvent_t gev[2 * 65] = {};
   bool gev_made = false;
 
+  ~Workspace() {   // error paths: release() and free_owned() are idempotent
+    free_owned();
+    release();
+  }
   bool sharded() const;
   mdot_status alloc(cudaStream_t stream, int64_t n, int64_t nrows);
   mdot_status launch_slot_body(cudaStream_t s, int slot, bool timed, bool with_ctrl = false);

@@ -68,11 +68,15 @@ print(f"sequential graph: {dt*1e3:.1f} ms", flush=True)
 del os.environ["MDOT_NO_PERSIST"]
 Rb = torch.stack(R)
 Cb = torch.stack(Cm)
+dt, out = timed(lambda: M.mdot_solve_batch(C, Rb, Cb, schedule=sched, options=M.options(eps=1e-6, eps_md=em)))
+print(f"mdot_solve_batch grouped (lockstep MD steps): {dt*1e3:.1f} ms ok={all(o['status'] == 0 for o in out)} "
+      f"evals {sum(o['evaluations'] for o in out)} paths {sorted(set(o['control_path'] for o in out))}", flush=True)
+os.environ["MDOT_NO_GROUPS"] = "1"
 for w in (1, 4, 8, 16):
     os.environ["MDOT_BATCH_WORKERS"] = str(w)
     dt, out = timed(lambda: M.mdot_solve_batch(C, Rb, Cb, schedule=sched, options=M.options(eps=1e-6, eps_md=em)))
     print(f"mdot_solve_batch workers={w}: {dt*1e3:.1f} ms ok={all(o['status'] == 0 for o in out)} "
-          f"evals {sum(o['evaluations'] for o in out)}", flush=True)
+          f"evals {sum(o['evaluations'] for o in out)} paths {sorted(set(o['control_path'] for o in out))}", flush=True)
 os.environ["MDOT_NO_PERSIST"] = "1"
 for nt in (2, 4, 8, 16):
     if nt > B:

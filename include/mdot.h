@@ -209,6 +209,24 @@ mdot_status mdot_comm_create(const void* nccl_unique_id, int32_t nranks, int32_t
 mdot_status mdot_comm_create_local(const char* group, int32_t nranks, int32_t rank, int32_t device,
                                    mdot_comm** out);
 mdot_status mdot_comm_destroy(mdot_comm* comm);
+/* Fused peer exchange (SURVEY 8(e) NC1 without a separate collective;
+ * DESIGN.md "Fused peer exchange").  COLLECTIVE: every rank of `comm` calls
+ * it with the same n_max.  Allocates this rank's exchange block
+ * (2 x nranks x (n_max + 16) fp64, device memory, owned by the comm, freed by
+ * mdot_comm_destroy) and maps every rank's block: NCCL transport -> CUDA IPC
+ * handles gathered over the communicator, opened with peer access (NVLink);
+ * in-process transport -> the group's blocks on the shared GPU.  Afterwards
+ * mdot_solve_sharded with dense fp32 C (n <= n_max) runs each projection as
+ * ONE persistent kernel per rank whose column-marginal exchange is plain
+ * peer-memory stores + system-scope flags inside the kernel; the in-process
+ * transport runs all of its ranks as groups of CTAs of ONE cooperative launch
+ * (ranks that wait on each other must be co-resident on one GPU).
+ * nranks <= 8.  Errors: MDOT_EINVAL (bad arguments, > 8 ranks, single-rank
+ * in-process comm), MDOT_ECUDA (allocation / IPC / peer access failed on ANY
+ * rank -- every rank returns it and keeps the NCCL / host path), MDOT_ENOMEM.
+ * A solve whose in-kernel flag wait times out (a peer died) returns
+ * MDOT_ENCCL.  MDOT_NO_PEER=1 in the environment disables the path. */
+mdot_status mdot_comm_enable_peer(mdot_comm* comm, int64_t n_max);
 /* local rows [row0, row0 + n_local) of C (local_rows->C points at row row0,
  * n_local*n entries) or of X (local_rows->X at row row0; Y, r, c full).
  * local_rows->n is the GLOBAL n.  u_local_out: [n_local], v_out: [n]. */

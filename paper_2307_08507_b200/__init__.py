@@ -39,6 +39,7 @@ from ._binding import (  # noqa: F401
     lib,
     mdot_comm_create,
     mdot_comm_create_local,
+    mdot_comm_enable_peer,
     mdot_comm_destroy,
     mdot_get_unique_id,
     mdot_last_error,

@@ -103,11 +103,13 @@ def lib():
         L.mdot_comm_create.argtypes = [P, ct.c_int32, ct.c_int32, ct.c_int32, ct.POINTER(P)]
         L.mdot_comm_destroy.argtypes = [P]
         L.mdot_comm_create_local.argtypes = [ct.c_char_p, ct.c_int32, ct.c_int32, ct.c_int32, ct.POINTER(P)]
+        L.mdot_comm_enable_peer.argtypes = [P, ct.c_int64]
         L.mdot_solve_sharded.argtypes = [P, ct.POINTER(Problem), ct.c_int64, ct.c_int64,
                                          ct.POINTER(Schedule), ct.POINTER(Options), P, P,
                                          ct.POINTER(Result)]
         for nm in ("mdot_solve_batch", "mdot_marginals", "mdot_round", "mdot_get_unique_id",
-                   "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_destroy", "mdot_solve_sharded"):
+                   "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_enable_peer", "mdot_comm_destroy",
+                   "mdot_solve_sharded"):
             getattr(L, nm).restype = ct.c_int
         if L.mdot_abi_version() != 2:
             raise ImportError("libmdot_b200.so ABI version mismatch")
@@ -287,6 +289,15 @@ def mdot_comm_create_local(group: str, nranks: int, rank: int, device: int):
     _check(lib().mdot_comm_create_local(group.encode(), nranks, rank, device, ct.byref(out)),
            "mdot_comm_create_local")
     return out
+
+
+def mdot_comm_enable_peer(comm, n_max: int, check=True):
+    """Collective: fused peer exchange for sharded solves with n <= n_max
+    (include/mdot.h).  Returns the status when check=False."""
+    st = lib().mdot_comm_enable_peer(comm, int(n_max))
+    if check:
+        _check(st, "mdot_comm_enable_peer")
+    return st
 
 
 def mdot_comm_destroy(comm):

@@ -216,6 +216,42 @@ int persist_grid();            // co-resident grid size (0 = unsupported)
 int persist_max_chunk();       // max finalize items per CTA
 cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cudaStream_t st);
 
+// Row-sharded persistent projection with the column exchange fused into the
+// kernel over peer memory (SURVEY 8(e) NC1 without NCCL; DESIGN.md "Fused
+// peer exchange").  Per evaluation every rank pushes [its column totals | its
+// row scalars] into slot `rank` of EVERY rank's receive block with plain
+// stores through peer-mapped pointers (NVLink), fences at system scope and
+// raises its flag in every rank's flag array; each rank then sums the slots
+// in rank order (identical on every rank) and finalizes the replicated
+// columns.  Receive blocks are double-buffered by exchange parity: a rank
+// overwrites parity p only two exchanges later, after every rank has raised
+// the flag of the exchange in between (and so finished reading p).
+constexpr int kMaxPeers = 8;
+struct PeerNet {
+  double* recv[kMaxPeers];         // rank q's receive block as seen from this GPU: [2][nranks][ld] fp64
+  unsigned int* flag[kMaxPeers];   // rank q's flag array: [kMaxPeers] exchange epochs
+  int nranks;
+  int64_t ld;                      // slot stride (>= n + kNumScalars)
+};
+struct PeerGroup {                 // one rank's share of a launch
+  PersistArgs a;
+  int rank;                        // global rank
+  unsigned int* epoch;             // this rank's exchange counter (own memory)
+  int* err;                        // set to 1 when a flag wait timed out
+};
+// One cooperative launch runs `groups` ranks of cta_per_group CTAs each: 1 on
+// a real multi-GPU rank (the peers run their own launches on their GPUs), G
+// when one GPU emulates G ranks (the in-process transport; every "peer"
+// pointer is then local and the ranks' CTAs are co-resident, so the flag
+// waits cannot deadlock -- B200_PROFILING.md: emulate ranks as ONE kernel).
+struct PeerLaunch {
+  alignas(64) unsigned char tmap[kMaxPeers][128];
+  PeerGroup g[kMaxPeers];
+  PeerNet net;
+  int groups, cta_per_group;
+};
+cudaError_t launch_persist_peer(const PeerLaunch& L, cudaStream_t st);
+
 // misc vector kernels
 cudaError_t launch_setup(int64_t n, const double* r, double* logr, double* rho, cudaStream_t st);
 cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t st); // y = a x + b y

@@ -82,14 +82,124 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// System-scope flag operations of the fused peer exchange (peer memory is
+// written over NVLink; gpu scope does not cover another GPU's observers).
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// a flag wait longer than this means a peer is gone: record and fall through
+// (garbage scalars, no hang; the host reports MDOT_ENCCL)
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+// Finalize partial totals of items [i_lo, i_lo + cnt): (item, sub) tasks over
+// all threads (a warp always holds whole octets); every partial load of up
+// to kMaxRounds rounds is issued before the first add.  tots[q] <- total.
+__device__ __forceinline__ void fin_totals(const FinalizeArgs& f, int64_t i_lo, int cnt, double* tots) {
+  const int tid = threadIdx.x;
+  constexpr int kMaxRounds = 2;
+  const int rounds = (cnt * kFinTPI + blockDim.x - 1) / blockDim.x;
+  for (int r0 = 0; r0 < rounds; r0 += kMaxRounds) {
+    double acc[kMaxRounds];
+#pragma unroll
+    for (int rr = 0; rr < kMaxRounds; ++rr) {
+      acc[rr] = 0.0;
+      const int task = (r0 + rr) * blockDim.x + tid;
+      const int q = task / kFinTPI, sub = task % kFinTPI;
+      if (r0 + rr < rounds && q < cnt) {
+        const int64_t k = i_lo + q;
+        const double* base;
+        int64_t stride;
+        int m;
+        if (k < f.nrows) { base = f.rowpart + k; stride = f.nrows; m = f.n_col_tiles; }
+        else { base = f.colpart + (k - f.nrows); stride = f.n; m = f.n_row_tiles; }
+        double z = 0.0;
+        for (int tt = sub; tt < m; tt += 4 * kFinTPI) {
+          const double y0 = base[(int64_t)tt * stride];
+          const double y1 = tt + kFinTPI < m ? base[(int64_t)(tt + kFinTPI) * stride] : 0.0;
+          const double y2 = tt + 2 * kFinTPI < m ? base[(int64_t)(tt + 2 * kFinTPI) * stride] : 0.0;
+          const double y3 = tt + 3 * kFinTPI < m ? base[(int64_t)(tt + 3 * kFinTPI) * stride] : 0.0;
+          z += y0; z += y1; z += y2; z += y3;
+        }
+        acc[rr] = z;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < kMaxRounds; ++rr) {
+      double x = acc[rr];
+      x += __shfl_xor_sync(0xffffffffu, x, 1);
+      x += __shfl_xor_sync(0xffffffffu, x, 2);
+      x += __shfl_xor_sync(0xffffffffu, x, 4);
+      const int task = (r0 + rr) * blockDim.x + tid;
+      const int q = task / kFinTPI, sub = task % kFinTPI;
+      if (r0 + rr < rounds && q < cnt && sub == 0) tots[q] = x;
+    }
+  }
+}
+
+// CTA partial of the 16 scalars (fixed order: warp shuffle tree, then warps
+// in order) -> out[0..15].  red: [warps][16] shared scratch.
+__device__ __forceinline__ void cta_partial(const double (&v)[kNumScalars], double* red, double* out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int q = 0; q < kNumScalars; ++q) {
+    double y = v[q];
+    for (int off = 16; off > 0; off >>= 1) y += __shfl_xor_sync(0xffffffffu, y, off);
+    if (lane == 0) red[warp * kNumScalars + q] = y;
+  }
+  __syncthreads();
+  if (tid < kNumScalars) {
+    double y = 0.0;
+    for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
+    out[tid] = y;
+  }
+}
+
+// Sum of the ncta CTA partials in a fixed order (identical in every CTA).
+// Result in fin[0..15] and, when sc != null, in sc[] (+ add_tail: rank-slot
+// row scalars of the peer exchange, summed in rank order, added last).
+__device__ __forceinline__ void combine_partials(const double* cta_part, int ncta, double* fin, double* sc,
+                                                 const double* add_tail = nullptr, int nranks = 0, int64_t ld = 0) {
+  const int tid = threadIdx.x;
+  constexpr int G = 256 / kNumScalars;
+  double y = 0.0;
+  if (tid < 256) {
+    const int q = tid % kNumScalars;
+    for (unsigned b = tid / kNumScalars; b < (unsigned)ncta; b += G) y += __ldcg(&cta_part[(int64_t)b * kNumScalars + q]);
+    fin[tid] = y;
+  }
+  __syncthreads();
+  double z = 0.0;
+  if (tid < kNumScalars) {
+    for (int g = 0; g < G; ++g) z += fin[g * kNumScalars + tid];
+    if (add_tail) {
+      double t = 0.0;
+      for (int p = 0; p < nranks; ++p) t += __ldcg(add_tail + (int64_t)p * ld + tid);
+      z += t;
+    }
+  }
+  __syncthreads();
+  if (tid < kNumScalars) {
+    fin[tid] = z;
+    if (sc) sc[tid] = z;
+  }
+  __syncthreads();
+}
+
 // The projection loop of one instance, run by `ncta` CTAs (cta = index among
 // them; the whole co-resident grid for k_persist).  Barriers, tile
 // round-robin, finalize chunks and the scalar combine use (cta, ncta) only.
 // A grouped variant (several instances sharing C, one slice of the grid
 // each, MD steps in lockstep) measured slower than concurrent graph-path
 // solves and was removed (profiles/README.md).
+template <bool PEER>
 __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const PersistArgs& a, const int cta,
-                                             const int ncta) {
+                                             const int ncta, const PeerNet* net = nullptr,
+                                             const PeerGroup* pg = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
   PersistSmem& S = *reinterpret_cast<PersistSmem*>(smem_raw + pad);
@@ -129,6 +239,9 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
   unsigned long long* tm = a.k1_ns + 2;
   if (timer) tm[9] = global_ns();
   bool first = a.initial != 0;
+  // peer exchange counter (every CTA of every rank counts the same exchanges)
+  unsigned int epoch = 0;
+  if constexpr (PEER) epoch = __ldcg(pg->epoch);
   for (long long slot = 0; slot < a.max_slots; ++slot) {
     // ---------------------------------------------------------------- ctrl
     if (!first) {
@@ -177,98 +290,108 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
     double v[kNumScalars];
 #pragma unroll
     for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
-    {
-      // this CTA's contiguous chunk of items; (item, sub) tasks over all 288
-      // threads (a warp always holds whole octets), totals to smem, then one
-      // thread per item for the fp64 log / exp / scalar work
-      const int64_t per = (items + ncta - 1) / ncta;
-      const int64_t i_lo = (int64_t)cta * per;
-      const int64_t i_hi = (i_lo + per < items) ? i_lo + per : items;
-      const int cnt = i_hi > i_lo ? (int)(i_hi - i_lo) : 0;
-      double* tots = fin + 256;   // [cnt]
-      // up to 4 rounds of (item, sub) tasks per thread; every partial load of
-      // all rounds is issued before the first add (latency once, not per round)
-      constexpr int kMaxRounds = 2;
-      const int rounds = (cnt * kFinTPI + blockDim.x - 1) / blockDim.x;
-      for (int r0 = 0; r0 < rounds; r0 += kMaxRounds) {
-        double acc[kMaxRounds];
-#pragma unroll
-        for (int rr = 0; rr < kMaxRounds; ++rr) {
-          acc[rr] = 0.0;
-          const int task = (r0 + rr) * blockDim.x + tid;
-          const int q = task / kFinTPI, sub = task % kFinTPI;
-          if (r0 + rr < rounds && q < cnt) {
-            const int64_t k = i_lo + q;
-            const double* base;
-            int64_t stride;
-            int m;
-            if (k < a.f.nrows) { base = a.f.rowpart + k; stride = a.f.nrows; m = a.f.n_col_tiles; }
-            else { base = a.f.colpart + (k - a.f.nrows); stride = a.f.n; m = a.f.n_row_tiles; }
-            double z = 0.0;
-            for (int tt = sub; tt < m; tt += 4 * kFinTPI) {
-              const double y0 = base[(int64_t)tt * stride];
-              const double y1 = tt + kFinTPI < m ? base[(int64_t)(tt + kFinTPI) * stride] : 0.0;
-              const double y2 = tt + 2 * kFinTPI < m ? base[(int64_t)(tt + 2 * kFinTPI) * stride] : 0.0;
-              const double y3 = tt + 3 * kFinTPI < m ? base[(int64_t)(tt + 3 * kFinTPI) * stride] : 0.0;
-              z += y0; z += y1; z += y2; z += y3;
-            }
-            acc[rr] = z;
-          }
-        }
-#pragma unroll
-        for (int rr = 0; rr < kMaxRounds; ++rr) {
-          double x = acc[rr];
-          x += __shfl_xor_sync(0xffffffffu, x, 1);
-          x += __shfl_xor_sync(0xffffffffu, x, 2);
-          x += __shfl_xor_sync(0xffffffffu, x, 4);
-          const int task = (r0 + rr) * blockDim.x + tid;
-          const int q = task / kFinTPI, sub = task % kFinTPI;
-          if (r0 + rr < rounds && q < cnt && sub == 0) tots[q] = x;
-        }
-      }
-      __syncthreads();
-      if (timer) tm[4] += global_ns() - tm[10];
+    // this CTA's contiguous chunk of items; (item, sub) tasks over all 288
+    // threads (a warp always holds whole octets), totals to smem
+    const int64_t per = (items + ncta - 1) / ncta;
+    const int64_t i_lo = (int64_t)cta * per;
+    const int64_t i_hi = (i_lo + per < items) ? i_lo + per : items;
+    const int cnt = i_hi > i_lo ? (int)(i_hi - i_lo) : 0;
+    double* tots = fin + 256;   // [cnt]
+    fin_totals(a.f, i_lo, cnt, tots);
+    __syncthreads();
+    if (timer) tm[4] += global_ns() - tm[10];
+    if constexpr (!PEER) {
+      // one thread per item for the fp64 log / exp / scalar work
       for (int q = tid; q < cnt; q += blockDim.x) finalize_item(a.f, i_lo + q, tots[q], v);
       __syncthreads();
       if (timer) tm[5] += global_ns() - tm[10];
-    }
-    // CTA partial (fixed order): warp shuffle tree, then warps in order
+      cta_partial(v, red, a.cta_part + (int64_t)cta * kNumScalars);
+      if (timer) tm[6] += global_ns() - tm[10];
+      grid_barrier(a.gbar, ncta);
+      if (timer) {
+        const unsigned long long t2 = global_ns();
+        tm[2] += t2 - tm[10];
+        tm[11] = t2;
+      }
+      // every CTA combines all CTA partials in the same order -> identical scalars
+      combine_partials(a.cta_part, ncta, fin, S.st.sc);
+    } else {
+      // F1: local rows finalize; this rank's column totals go to slot `me`
+      // of every rank's receive block (remote stores over NVLink)
+      const int me = pg->rank, R = net->nranks;
+      const int64_t ld = net->ld;
+      const unsigned int ep = ++epoch;
+      const int64_t slot_off = ((int64_t)(ep & 1u) * R + me) * ld;
+      for (int q = tid; q < cnt; q += blockDim.x) {
+        const int64_t k = i_lo + q;
+        if (k < a.f.nrows) {
+          finalize_item(a.f, k, tots[q], v);
+        } else {
+          const double t = tots[q];
+          const int64_t j = k - a.f.nrows;
+#pragma unroll 1
+          for (int p = 0; p < R; ++p) __stcg(net->recv[p] + slot_off + j, t);
+        }
+      }
+      __threadfence_system();
+      cta_partial(v, red, a.cta_part + (int64_t)cta * kNumScalars);
+      grid_barrier(a.gbar, ncta);
+      if (cta == 0) {
+        // this rank's row scalars -> slot tail, then the flag (release, sys)
+        combine_partials(a.cta_part, ncta, fin, nullptr);
+        if (tid < kNumScalars) {
+          const double y = fin[tid];
+#pragma unroll 1
+          for (int p = 0; p < R; ++p) __stcg(net->recv[p] + slot_off + a.f.n + tid, y);
+          __threadfence_system();
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll 1
+          for (int p = 0; p < R; ++p) st_release_sys(net->flag[p] + me, ep);
+        }
+      }
+      // every rank's flag of this exchange (own flag array, local memory)
+      if (tid == 0) {
+        const unsigned long long t_w = global_ns();
+#pragma unroll 1
+        for (int p = 0; p < R; ++p) {
+          while ((int)(ld_acquire_sys(net->flag[me] + p) - ep) < 0) {
+            if (global_ns() - t_w > kPeerTimeoutNs) {
+              *pg->err = 1;
+              break;
+            }
+            __nanosleep(32);
+          }
+        }
+      }
+      __syncthreads();
+      if (timer) tm[5] += global_ns() - tm[10];
+      // F2: replicated columns, chunked identically on every rank (the
+      // scalars, and so every decision, are bitwise identical across ranks)
 #pragma unroll
-    for (int q = 0; q < kNumScalars; ++q) {
-      double y = v[q];
-      for (int off = 16; off > 0; off >>= 1) y += __shfl_xor_sync(0xffffffffu, y, off);
-      if (lane == 0) red[warp * kNumScalars + q] = y;
-    }
-    __syncthreads();
-    if (tid < kNumScalars) {
-      double y = 0.0;
-      for (int w = 0; w < kTmaThreads / 32; ++w) y += red[w * kNumScalars + tid];
-      a.cta_part[(int64_t)cta * kNumScalars + tid] = y;
-    }
-    if (timer) tm[6] += global_ns() - tm[10];
-    grid_barrier(a.gbar, ncta);
-    if (timer) {
-      const unsigned long long t2 = global_ns();
-      tm[2] += t2 - tm[10];
-      tm[11] = t2;
-    }
-    // every CTA combines all CTA partials in the same order -> identical scalars
-    {
-      constexpr int G = 256 / kNumScalars;
-      double y = 0.0;
-      if (tid < 256) {
-        const int q = tid % kNumScalars;
-        for (unsigned b = tid / kNumScalars; b < (unsigned)ncta; b += G)
-          y += __ldcg(&a.cta_part[(int64_t)b * kNumScalars + q]);
-        fin[tid] = y;
+      for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
+      const double* rb = net->recv[me] + (int64_t)(ep & 1u) * R * ld;
+      const int64_t per2 = (a.f.n + ncta - 1) / ncta;
+      const int64_t j_lo = (int64_t)cta * per2;
+      const int64_t j_hi = (j_lo + per2 < a.f.n) ? j_lo + per2 : a.f.n;
+      for (int64_t j = j_lo + tid; j < j_hi; j += blockDim.x) {
+        double t = 0.0;
+#pragma unroll 1
+        for (int p = 0; p < R; ++p) t += __ldcg(rb + (int64_t)p * ld + j);
+        finalize_item(a.f, a.f.nrows + j, t, v);
       }
-      __syncthreads();
-      if (tid < kNumScalars) {
-        double z = 0.0;
-        for (int g = 0; g < G; ++g) z += fin[g * kNumScalars + tid];
-        S.st.sc[tid] = z;
+      cta_partial(v, red, a.cta_part + (int64_t)cta * kNumScalars);
+      if (timer) tm[6] += global_ns() - tm[10];
+      grid_barrier(a.gbar, ncta);
+      if (timer) {
+        const unsigned long long t2 = global_ns();
+        tm[2] += t2 - tm[10];
+        tm[11] = t2;
       }
-      __syncthreads();
+      // column scalars (CTA order) + row scalars (rank order): identical on every rank
+      combine_partials(a.cta_part, ncta, fin, S.st.sc, rb + a.f.n, R, ld);
+      (void)R;
     }
     if (timer) {
       tm[9] = global_ns();
@@ -287,13 +410,24 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
     if (tid == 0) {
       a.k1_ns[0] = tm[1];
       a.k1_ns[1] = tm[8];
+      if constexpr (PEER) *pg->epoch = epoch;
     }
   }
 }
 
 __global__ void __launch_bounds__(kTmaThreads, 2)
     k_persist(const __grid_constant__ CUtensorMap tmap, PersistArgs a) {
-  persist_body(tmap, a, blockIdx.x, gridDim.x);
+  persist_body<false>(tmap, a, blockIdx.x, gridDim.x);
+}
+
+// Row-sharded projection with the fused peer exchange: group = rank slot of
+// this launch (one group per GPU; G groups when one GPU emulates G ranks).
+__global__ void __launch_bounds__(kTmaThreads, 2) k_persist_peer(const __grid_constant__ PeerLaunch L) {
+  const int grp = blockIdx.x / L.cta_per_group;
+  if (grp >= L.groups) return;
+  const PeerGroup& g = L.g[grp];
+  persist_body<true>(*reinterpret_cast<const CUtensorMap*>(&L.tmap[grp][0]), g.a, blockIdx.x % L.cta_per_group,
+                     L.cta_per_group, &L.net, &g);
 }
 
 static int g_persist_grid = -1;
@@ -326,6 +460,21 @@ int persist_grid() {
 }
 
 int persist_max_chunk() { return kPersistMaxChunk; }
+
+cudaError_t launch_persist_peer(const PeerLaunch& L, cudaStream_t st) {
+  const int smem = (int)sizeof(PersistSmem) + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_persist_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute((const void*)k_persist_peer, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  void* args[] = {const_cast<PeerLaunch*>(&L)};
+  return cudaLaunchCooperativeKernel((const void*)k_persist_peer, dim3(L.groups * L.cta_per_group), dim3(kTmaThreads),
+                                     args, (size_t)smem, st);
+}
 
 cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cudaStream_t st) {
   const int smem = (int)sizeof(PersistSmem) + 128;

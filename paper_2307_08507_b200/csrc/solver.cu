@@ -783,7 +783,12 @@ mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_
   res->control_path = 2;
   PersistArgs a;
   CKS(persist_prepare(w, o, a));
-  CK(launch_persist(w.tmap, a, w.pers_grid, w.st));
+  if (w.sharded()) {
+    // row-sharded: column exchange fused into the kernel over peer memory
+    CKS(comm_peer_persist(w.comm, a, w.tmap, w.pers_grid, w.st));
+  } else {
+    CK(launch_persist(w.tmap, a, w.pers_grid, w.st));
+  }
   w.launches++;
   return persist_collect(w, o, t, res, a);
 }
@@ -930,7 +935,11 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
       eval.keep_l2 = (4.0 * (double)nrows * (double)n <= 0.6 * (double)l2) ? 1 : 0;
-      pers_grid = (getenv("MDOT_NO_PERSIST") || comm || persist_ncta < 0) ? 0 : persist_grid();
+      // sharded: the persistent path needs the fused peer exchange
+      // (mdot_comm_enable_peer); CTAs per rank from the transport
+      if (getenv("MDOT_NO_PERSIST") || persist_ncta < 0) pers_grid = 0;
+      else if (sharded()) pers_grid = comm_peer_ncta(comm, n, persist_grid());
+      else pers_grid = comm ? 0 : persist_grid();
       if (persist_ncta > 0 && pers_grid > persist_ncta) pers_grid = persist_ncta;
       if (pers_grid > 0 && (nrows + n + pers_grid - 1) / pers_grid > persist_max_chunk()) pers_grid = 0;
     }
@@ -1112,7 +1121,9 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   // sharded: device control (CUDA-graph slots with the NCCL allreduce captured
   // inside) needs a capturable transport; the in-process transport syncs on
   // the host in every allreduce, so it runs the host loop
-  if (comm && (comm->nranks > 1 || comm->nccl) && !comm->capturable()) o.device_control = 0;
+  // (with the fused peer exchange the persistent projection runs device-side
+  // on any transport; when it cannot, such a solve takes the host loop)
+  if (comm && (comm->nranks > 1 || comm->nccl) && !comm->capturable() && !comm->peer) o.device_control = 0;
   Workspace w;
   w.comm = comm;
   w.row0 = row0;
@@ -1161,7 +1172,8 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       mdot_options ot = o;
       if (t < gam.size() && o.eps_md > o.eps) ot.eps = o.eps_md;
       if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, ot, (int)t, res);
-      else if (o.device_control && !(w.sharded() && w.exact_mode)) solve_st = project_device(w, ot, (int)t, res);
+      else if (o.device_control && !(w.sharded() && (w.exact_mode || !comm->capturable())))
+        solve_st = project_device(w, ot, (int)t, res);
       else if (o.projector == MDOT_PROJ_SINKHORN) solve_st = project_sinkhorn(w, ot, (int)t, res);
       else solve_st = project_pncg(w, ot, (int)t, res);
       res->md_steps = (int64_t)t;

@@ -444,7 +444,7 @@ def test_otf_solve_matches_oracle():
 
 
 # ------------------------------------------------------------- sharded path
-def _sharded_solve_threads(inst, G, sched, opts_kw, group):
+def _sharded_solve_threads(inst, G, sched, opts_kw, group, peer=False):
     """G virtual ranks = G threads of this process, each with its own stream,
     row-sharded C, in-process transport (no device-side waiting between
     ranks: the allreduce is a host barrier)."""
@@ -464,6 +464,8 @@ def _sharded_solve_threads(inst, G, sched, opts_kw, group):
                 U = torch.empty(nloc, dtype=torch.float64, device=DEV)
                 V = torch.empty(n, dtype=torch.float64, device=DEV)
                 comm = M.mdot_comm_create_local(group, G, k, 0)
+                if peer:
+                    M.mdot_comm_enable_peer(comm, n)
                 res = M.mdot_solve_sharded(comm, row0, nloc, C, r, c, n=n, schedule=sched,
                                            options=M.options(**opts_kw), u_local_out=U, v_out=V)
                 s.synchronize()
@@ -549,6 +551,67 @@ def test_sharded_virtual_ranks_match_single_gpu(G):
     lr, lc, _ = O.log_marginals(prob, U, V, 512.0)
     l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
     assert l1 <= 2 * eps
+
+
+@pytest.mark.parametrize("G,projector", [(2, 0), (3, 0), (4, 1), (8, 0)])
+def test_peer_fused_exchange_virtual_ranks(G, projector):
+    """Fused peer exchange (mdot_comm_enable_peer), G ranks emulated on one
+    GPU as groups of CTAs of ONE cooperative launch: every evaluation's
+    column totals and row scalars go through the in-kernel peer stores +
+    system-scope flags.  Ranks must take identical decisions; the result must
+    match the single-GPU solve, the host-loop sharded solve and the oracle."""
+    n = 2000                                   # ragged slabs for G = 3, 8
+    inst = S.uniform_points_instance(3, n, 2, 21, marg="dirichlet")
+    gb, T, eps = 1024.0, 4, 1e-6
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=T)
+    kw = {"eps": eps, "projector": projector}
+    out = _sharded_solve_threads(inst, G, sched, kw, f"peer{G}_{projector}", peer=True)
+    assert all(o[0]["control_path"] == 2 for o in out)          # the fused persistent path ran
+    assert all(o[0]["status"] == 0 for o in out)
+    assert all(o[0]["evaluations"] == out[0][0]["evaluations"] for o in out)
+    assert all(o[0]["cost_unrounded"] == out[0][0]["cost_unrounded"] for o in out)
+    assert all(np.array_equal(o[2], out[0][2]) for o in out)
+    assert out[0][0]["l1_final"] <= eps
+    ref = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(**kw))
+    assert abs(out[0][0]["cost_unrounded"] - ref["cost_unrounded"]) <= 2e-6 * ref["cost_unrounded"]
+    host = _sharded_solve_threads(inst, G, sched, kw, f"peerh{G}_{projector}", peer=False)
+    assert host[0][0]["control_path"] == 0
+    assert abs(out[0][0]["cost_unrounded"] - host[0][0]["cost_unrounded"]) <= 2e-6 * host[0][0]["cost_unrounded"]
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T),
+                             O.make_options(eps=eps, projector=O.SINKHORN if projector else O.PNCG))
+    U = np.concatenate([o[1] for o in out])
+    _gates(out[0][0], ores, inst, prob, U, out[0][2], eps)
+
+
+def test_peer_fused_exchange_one_rank_nccl(monkeypatch):
+    """The one-rank-per-GPU launch of the fused peer kernel (the code path of
+    a real multi-GPU rank: IPC handle exchange over NCCL, own launch, flags in
+    its own block) on a 1-rank NCCL communicator forced onto the sharded path."""
+    monkeypatch.setenv("MDOT_SHARDED_SELFTEST", "1")
+    n, gb, eps = 1024, 512.0, 1e-6
+    inst = S.uniform_points_instance(3, n, 2, 22, marg="dirichlet")
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=2)
+    comm = M.mdot_comm_create(M.mdot_get_unique_id(), 1, 0, 0)
+    try:
+        M.mdot_comm_enable_peer(comm, n)
+        U = torch.empty(n, dtype=torch.float64, device=DEV)
+        V = torch.empty_like(U)
+        res = M.mdot_solve_sharded(comm, 0, n, C_local=C, r=r, c=c, n=n, schedule=sched,
+                                   options=M.options(eps=eps), u_local_out=U, v_out=V)
+        res2 = M.mdot_solve_sharded(comm, 0, n, C_local=C, r=r, c=c, n=n, schedule=sched,
+                                    options=M.options(eps=eps), u_local_out=U, v_out=V)
+    finally:
+        M.mdot_comm_destroy(comm)
+    assert res["control_path"] == 2 and res["status"] == 0 and res["l1_final"] <= eps
+    # a second solve on the same comm continues the exchange epochs: same result
+    assert res2["cost_unrounded"] == res["cost_unrounded"] and res2["evaluations"] == res["evaluations"]
+    ref = M.mdot_solve(C, r, c, schedule=sched, options=M.options(eps=eps))
+    assert abs(res["cost_unrounded"] - ref["cost_unrounded"]) <= 2e-6 * ref["cost_unrounded"]
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=2), O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
 
 
 @pytest.mark.parametrize("projector", [0, 1])

@@ -25,8 +25,11 @@ cpu_baseline= the fp64 oracle (oracle/), as it stands, on a bounded sample of
 
 --impl reference runs the oracle (this tier's reference arm) on the same
 config, metric and unit, each step a bounded sample.
-Multi-GPU (torchrun): rows of C sharded over ranks, one NCCL allreduce of the
-column partials per evaluation (mdot_solve_sharded); strong scaling (n fixed).
+Multi-GPU (torchrun): rows of C sharded over ranks (mdot_solve_sharded); per
+evaluation the column totals and row scalars are exchanged inside the
+persistent kernel with peer-memory stores and system-scope flags
+(mdot_comm_enable_peer; NCCL allreduce in CUDA-graph slots if peer access is
+unavailable or MDOT_NO_PEER is set); strong scaling (n fixed).
 """
 from __future__ import annotations
 
@@ -221,6 +224,7 @@ def run_ours(a, rank, world, local_rank):
     r = torch.from_numpy(inst.r).to(dev)
     c = torch.from_numpy(inst.c).to(dev)
     comm = None
+    exchange = None
     if world > 1:
         rows = np.array_split(np.arange(n), world)[rank]
         row0, nloc = int(rows[0]), len(rows)
@@ -229,6 +233,11 @@ def run_ours(a, rank, world, local_rank):
         t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
         dist.broadcast(t, 0)
         comm = M.mdot_comm_create(bytes(t.cpu().numpy()), world, rank, local_rank)
+        # fused peer exchange (column totals pushed over NVLink inside the
+        # persistent kernel); every rank gets the same status, NCCL otherwise
+        exchange = "nccl allreduce in CUDA-graph slots"
+        if not os.environ.get("MDOT_NO_PEER") and M.mdot_comm_enable_peer(comm, n, check=False) == 0:
+            exchange = "fused peer stores + flags in the persistent kernel (NVLink)"
         U = torch.empty(nloc, dtype=torch.float64, device=dev)
     else:
         C = torch.from_numpy(inst.C).to(dev)
@@ -308,6 +317,7 @@ def run_ours(a, rank, world, local_rank):
         "config": {"workload": workload_name(a), "n": n, "gamma_bar": a.gamma_bar,
                    "T": int(results[-1]["md_steps"]), "eps": a.eps, "stop": "marginal L1",
                    "projector": a.projector, "parallelism": f"rows sharded x{world}" if world > 1 else "1 GPU",
+                   "exchange": exchange,
                    "l2": "C (4 n^2 B) is larger than L2 (126 MB): no flush needed",
                    "instance_seed": 4000 + a.instance},
         "time_to_eps_s": ms_step / 1000.0,

@@ -90,3 +90,113 @@ def test_row_partition_covers_rows_once():
             assert np.array_equal(cat, np.arange(n))
             sizes = [len(p) for p in parts]
             assert max(sizes) - min(sizes) <= 1
+
+
+# ---------------------------------------------------------------------------
+# Fused peer exchange (k_persist_peer)
+# ---------------------------------------------------------------------------
+def _peer_worker(rank, world, port, q):
+    """Host model of one exchange of k_persist_peer over gloo: every rank's
+    slot [column totals | row scalars] lands in every rank's receive block
+    (all_gather stands in for the peer stores), each rank sums the slots in
+    rank order 0..G-1.  The summed block must be bitwise identical on every
+    rank (identical controller decisions) and equal the unsharded oracle."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import synthetic as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    inst = S.uniform_points_instance(3, 101, 2, 12, marg="dirichlet")
+    n = inst.n
+    rng = np.random.default_rng(1)
+    A = np.log(inst.r) + 0.1 * rng.standard_normal(n)
+    B = np.log(inst.c) + 0.1 * rng.standard_normal(n)
+    g = 25.0
+    rows = np.array_split(np.arange(n), world)[rank]
+    Cl = inst.C[rows[0]:rows[0] + len(rows)].astype(np.float64)
+    P = np.exp(A[rows, None] + B[None, :] - g * Cl)
+    rP = P.sum(1)
+    slot = torch.from_numpy(np.concatenate([P.sum(0), [rP.sum(), np.abs(rP - inst.r[rows]).sum()]]))
+    recv = [torch.empty_like(slot) for _ in range(world)]
+    dist.all_gather(recv, slot)
+    tot = torch.zeros_like(slot)
+    for p in range(world):          # rank order, identical on every rank
+        tot += recv[p]
+    allt = [torch.empty_like(tot) for _ in range(world)]
+    dist.all_gather(allt, tot)
+    if rank == 0:
+        same = all(torch.equal(allt[0], x) for x in allt)
+        prob = O.OracleProblem(inst)
+        lr, lc, _ = O.log_marginals(prob, A, B, g)
+        t = tot.numpy()
+        q.put((same, float(np.abs(t[:n] - np.exp(lc)).max()), float(abs(t[n] - np.exp(lr).sum())),
+               float(abs(t[n + 1] - np.abs(np.exp(lr) - inst.r).sum()))))
+    dist.destroy_process_group()
+
+
+def test_peer_exchange_rank_ordered_sum_is_identical_on_every_rank():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    same, dcol, dmass, dl1 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert same
+    assert dcol < 1e-15 and dmass < 1e-13 and dl1 < 1e-13
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_peer_exchange_protocol_double_buffering(G):
+    """Threads model of the in-kernel protocol: per exchange e, rank k writes
+    its slot into parity e & 1 of every rank's receive block, raises its flag
+    in every rank's flag array (epoch e), waits until every flag of its own
+    array reaches e, then reads its block of parity e & 1.  Random delays
+    between every step; a rank must never read a slot overwritten by a later
+    exchange (the two-exchange reuse distance of the parity buffers)."""
+    import random
+    import threading
+    import time
+    E = 40
+    recv = [[[None] * G for _ in range(2)] for _ in range(G)]   # [rank][parity][src]
+    flag = [[0] * G for _ in range(G)]                          # [rank][src]
+    errors = []
+    lock = threading.Lock()
+
+    def rank_fn(k):
+        rnd = random.Random(1000 * G + k)
+        for e in range(1, E + 1):
+            for p in range(G):
+                time.sleep(rnd.random() * 2e-4)
+                recv[p][e & 1][k] = (e, k)
+            time.sleep(rnd.random() * 2e-4)
+            for p in range(G):
+                with lock:
+                    flag[p][k] = e
+            t0 = time.time()
+            while any(flag[k][p] < e for p in range(G)):
+                time.sleep(1e-5)
+                if time.time() - t0 > 30:
+                    errors.append(("timeout", k, e))
+                    return
+            time.sleep(rnd.random() * 2e-4)
+            got = [recv[k][e & 1][p] for p in range(G)]
+            if got != [(e, p) for p in range(G)]:
+                errors.append((k, e, got))
+
+    ths = [threading.Thread(target=rank_fn, args=(k,)) for k in range(G)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors[:3]

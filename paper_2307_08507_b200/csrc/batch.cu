@@ -9,6 +9,7 @@
 // shared memory (14 x 2n doubles + exponent parameters); C (n x n fp32, shared
 // by all instances) is streamed from L2.  Instances converge independently;
 // no cross-CTA communication, no host involvement until the batch is done.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -20,6 +21,8 @@
 #include "ops.cuh"
 
 namespace mdot {
+
+namespace cg = cooperative_groups;
 
 // 16 warps: one CTA per instance has an SM to itself and its evaluation is
 // latency-bound (8 warps: 2 per scheduler, 13 % issue utilisation); the
@@ -79,9 +82,13 @@ struct BatchSmem {
 // coltot[j] = sum_i 2^w S_i (anchored units, internal.cuh "K1 numerics").
 // F64: w assembled and exponentiated in fp64 (fp64-entry mode, eps < 1e-7,
 // and the range-guard fallback).
+// Cluster split (CL CTAs per instance, q = this CTA's rank): the CTA takes
+// the row groups ib = 4 (q W + w) + 4 W CL m; row totals are complete for
+// its rows, column totals are partial over them (combined by the caller).
 template <bool F64, bool PACKED, typename CT>
 __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
-                           double gbar, double* rowtot, double* coltot, double (*sred)[kTileN]) {
+                           double gbar, double* rowtot, double* coltot, double (*sred)[kTileN], int q_rank,
+                           int CL) {
   static_assert(kBatchWarps == 2 * kSredRows, "two-round column reduction");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4* rowp = prm;
@@ -147,7 +154,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
         }
       }
     };
-    for (int ib = 4 * warp; ib < n; ib += 4 * kBatchWarps, ++step) {
+    for (int ib = 4 * (warp + q_rank * kBatchWarps); ib < n; ib += 4 * kBatchWarps * CL, ++step) {
       CT cvc[4][8];
       load_group(ib, cvc);
       double rs[4];
@@ -252,12 +259,50 @@ __device__ __forceinline__ double batch_cost(const BatchArgs& a, int64_t idx) {
   return a.C64 ? __ldg(a.C64 + idx) : (double)__ldg(a.C + idx);
 }
 
+// Cluster exchange after a split evaluation: every CTA of the instance ends
+// with the full [rowtot | coltot]: row totals copied from the owning CTA,
+// column totals summed over the CTAs in rank order 0..CL-1 (the same bits in
+// every CTA, so every CTA's controller takes the same decisions).  Peers'
+// partials are read through DSMEM between two cluster barriers, then written.
+constexpr int kBatchMaxItemsPerThread = 4;   // 2n <= 4 x 512
+__device__ __forceinline__ void cluster_combine(cg::cluster_group& cl, double* tot, int n, int q_rank, int CL) {
+  const int n2 = 2 * n;
+  double vals[kBatchMaxItemsPerThread];
+  cl.sync();   // every CTA's partials are complete
+#pragma unroll
+  for (int m = 0; m < kBatchMaxItemsPerThread; ++m) {
+    const int k = threadIdx.x + m * blockDim.x;
+    vals[m] = 0.0;
+    if (k < n2) {
+      if (k < n) {
+        const int owner = (k / (4 * kBatchWarps)) % CL;
+        vals[m] = owner == q_rank ? tot[k] : *cl.map_shared_rank(tot + k, owner);
+      } else {
+        double y = 0.0;
+        for (int q = 0; q < CL; ++q) y += (q == q_rank) ? tot[k] : *cl.map_shared_rank(tot + k, q);
+        vals[m] = y;
+      }
+    }
+  }
+  cl.sync();   // every peer read is done before anyone overwrites its partials
+#pragma unroll
+  for (int m = 0; m < kBatchMaxItemsPerThread; ++m) {
+    const int k = threadIdx.x + m * blockDim.x;
+    if (k < n2) tot[k] = vals[m];
+  }
+  __syncthreads();
+}
+
 template <bool PACKED, typename CT>
 __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
   const int n = a.n, n2 = 2 * a.n, tid = threadIdx.x;
-  const int b = blockIdx.x;
+  // CL CTAs (a thread-block cluster) per instance; CL = 1 without a cluster launch
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int q_rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / CL;
   double* D = reinterpret_cast<double*>(smem_raw + sizeof(BatchSmem));
   double* logt = D;            // log r | log c
   double* tgt = D + 1 * n2;    // r | c
@@ -363,11 +408,12 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
             }
             __syncthreads();
           }
-          batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+          batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL);
         } else {
-          batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred);
+          batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL);
         }
         __syncthreads();
+        if (CL > 1) cluster_combine(cluster, tot, n, q_rank, CL);
         double v[kNumScalars];
 #pragma unroll
         for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
@@ -418,6 +464,9 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   }
 
   // ---- rounding + cost (a10), fp64: F = exp(U + V - gbar C), x = min(r/r(F), 1)
+  // (rank 0 of the cluster alone: once per solve, no DSMEM access after the
+  // last evaluation, so the other CTAs may exit)
+  if (q_rank != 0) return;
   double cost_F = 0.0, cost_G = 0.0;
   if (status == 0 || status == MDOT_ENOCONV) {
     double* logx = tuv;        // [n] log x
@@ -507,18 +556,48 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
 
 size_t batch_smem_bytes(int n) { return sizeof(BatchSmem) + (size_t)15 * 2 * n * sizeof(double) + (size_t)2 * n * 16; }
 
+// CTAs per instance: split the rows of each instance over a thread-block
+// cluster while the batch leaves SMs idle (config 2: 64 instances on 148
+// SMs -> 2 per instance), keeping >= 128 rows per CTA; power of two <= 8.
+// MDOT_K8_CLUSTER overrides (A/B).
+int batch_cluster(int n, int B) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int cl = 1;
+  while (cl < 8 && (int64_t)B * cl * 2 <= sms && n / (cl * 2) >= 128) cl *= 2;
+  if (const char* e = getenv("MDOT_K8_CLUSTER")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8) cl = v;
+  }
+  return cl;
+}
+
 cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st) {
   const size_t smem = batch_smem_bytes(a.n);
+  if (2 * a.n > kBatchMaxItemsPerThread * kBatchThreads) return cudaErrorInvalidValue;
   // MDOT_K8_SCALAR: A/B switch, scalar fp32 entry arithmetic
   static const bool scalar = getenv("MDOT_K8_SCALAR") != nullptr;
   const void* fn = a.C64 ? (const void*)k_batch_solve<false, double>
                          : (scalar ? (const void*)k_batch_solve<false, float> : (const void*)k_batch_solve<true, float>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (a.C64) k_batch_solve<false, double><<<B, kBatchThreads, smem, st>>>(a);
-  else if (scalar) k_batch_solve<false, float><<<B, kBatchThreads, smem, st>>>(a);
-  else k_batch_solve<true, float><<<B, kBatchThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  const int CL = batch_cluster(a.n, B);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * CL));
+  cfg.blockDim = dim3(kBatchThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (a.C64) return cudaLaunchKernelEx(&cfg, k_batch_solve<false, double>, a);
+  if (scalar) return cudaLaunchKernelEx(&cfg, k_batch_solve<false, float>, a);
+  return cudaLaunchKernelEx(&cfg, k_batch_solve<true, float>, a);
 }
 
 }  // namespace mdot

@@ -132,6 +132,10 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   // of the persistent kernel; smaller tiles for small n
   int tile_m = 512;
   while (tile_m > 32 && (int64_t)eval.n_col_tiles * ((nrows + tile_m - 1) / tile_m) < 2 * 148) tile_m /= 2;
+  if (const char* tm_env = getenv("MDOT_TILE_M")) {   // A/B experiments only
+    const int v = atoi(tm_env);
+    if (v >= 32 && v <= 512 && (v & (v - 1)) == 0) tile_m = v;
+  }
   eval.tile_m = tile_m;
   eval.n_row_tiles = (int)((nrows + tile_m - 1) / tile_m);
   chunks = (int)std::max<int64_t>(1, std::min<int64_t>(nrows, (4 * 148 + (n + 255) / 256 - 1) / ((n + 255) / 256)));

@@ -7,7 +7,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdot_b200.so")
+# MDOT_LIB: load another build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("MDOT_LIB") or os.path.join(_HERE, "libmdot_b200.so")
 
 MDOT_COST_DENSE_F32, MDOT_COST_SQEUCLID_F32, MDOT_COST_DENSE_F64 = 0, 1, 2
 MDOT_MEM_HOST, MDOT_MEM_DEVICE = 0, 1

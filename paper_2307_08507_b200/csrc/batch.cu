@@ -184,7 +184,11 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
           u64 c2[4];
 #pragma unroll
           for (int p = 0; p < 4; ++p) c2[p] = pk2(cv[2 * p], cv[2 * p + 1]);
+#if MDOT_K1_ROWRED_F32
+          rs[u] = (double)entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);   // exact: an fp32 value
+#else
           rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
+#endif
           mrow[u] = rp.y;
         } else {
           // fp64 entries: exact z = A_i + B_j - gbar C_ij, anchored by the
@@ -204,11 +208,15 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
           rs[u] = rsum;
         }
       }
-      double tot = bred4(rs[0], rs[1], rs[2], rs[3], lane);
+      // fp32 entries: rs are fp32 values, reduced across the warp in fp32
+      // (MDOT_K1_ROWRED_F32); fp64 entries keep the fp64 butterfly
+      double tot = (!F64 && MDOT_K1_ROWRED_F32)
+                       ? (double)warp_reduce4_f((float)rs[0], (float)rs[1], (float)rs[2], (float)rs[3], lane)
+                       : bred4(rs[0], rs[1], rs[2], rs[3], lane);
       const int i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
       if (!F64) tot *= (double)((lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]));
       if ((lane & 7) == 0 && i < n) rowtot[i] = (j0 == 0) ? tot : rowtot[i] + tot;
-      if (!F64 && (step & 1)) {
+      if (!F64 && (step % MDOT_K1_COLFLUSH) == MDOT_K1_COLFLUSH - 1) {
         if (PACKED) {
 #pragma unroll
           for (int p = 0; p < 4; ++p) {

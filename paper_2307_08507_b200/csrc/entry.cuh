@@ -104,6 +104,26 @@ __device__ __forceinline__ double entry_row8(const u64 (&c2)[4], float4 rp, cons
   return (double)lo + (double)hi;
 }
 
+// Same, row sum left in fp32 (lo + hi): the warp then reduces rows in fp32
+// (MDOT_K1_ROWRED_F32).
+__device__ __forceinline__ float entry_row8_f(const u64 (&c2)[4], float4 rp, const ColPairs& cp, u64 ngh2, u64 ngl2,
+                                              u64 (&cacc)[4]) {
+  const u64 ah2 = pk2(rp.x, rp.x), S2 = pk2(rp.z, rp.z);
+  u64 rsum = 0ull;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const u64 zh = fma2(ngh2, c2[p], add2(ah2, cp.bh[p]));
+    float zl, zu;
+    up2(fma2(ngl2, c2[p], zh), zl, zu);
+    const u64 e = pk2(ex2_ftz(zl), ex2_ftz(zu));
+    rsum = fma2(e, cp.T[p], rsum);
+    cacc[p] = fma2(e, S2, cacc[p]);
+  }
+  float lo, hi;
+  up2(rsum, lo, hi);
+  return lo + hi;
+}
+
 // The 8 fp32 cost values of a lane's columns from two float4 loads.
 __device__ __forceinline__ void cost_pairs(const float4& x0, const float4& x1, u64 (&c2)[4]) {
   c2[0] = pk2(x0.x, x0.y);

@@ -24,6 +24,33 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kUnroll = 4;       // rows per warp per inner step
 constexpr int kNumScalars = 16;
 
+// K1 reduction knobs, shared by the TMA kernels,
+// k_eval_fast (bitwise-equal by test), K2 and the fp32-entry paths of K8: MDOT_K1_ROWRED_F32 = 1 reduces the 4
+// rows' lane sums across the warp in fp32 (one conversion per row total
+// instead of 4 conversions + 5 fp64 adds + 12 shuffles per lane and stage);
+// MDOT_K1_COLFLUSH = 4-row steps of fp32 column sums per fp64 flush.
+#ifndef MDOT_K1_ROWRED_F32
+#define MDOT_K1_ROWRED_F32 1
+#endif
+#ifndef MDOT_K1_COLFLUSH
+#define MDOT_K1_COLFLUSH 4
+#endif
+__device__ __forceinline__ float warp_reduce4_f(float v0, float v1, float v2, float v3, int lane) {
+  const bool up = lane & 16;
+  float k0 = up ? v2 : v0, k1 = up ? v3 : v1;
+  const float s0 = up ? v0 : v2, s1 = up ? v1 : v3;
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  const bool up2 = lane & 8;
+  float kk = up2 ? k1 : k0;
+  const float ss = up2 ? k0 : k1;
+  kk += __shfl_xor_sync(0xffffffffu, ss, 8);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+  return kk;
+}
+
 struct EvalArgs {
   // cost
   const float* C;          // dense fp32, row-major, rows of this shard (row stride ldc)

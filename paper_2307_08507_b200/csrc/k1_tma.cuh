@@ -238,7 +238,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
       const int64_t ib = i0 + (int64_t)k * kTmaRows + 4 * warp;
       mbar_wait(&sm.full[s], ph);
-      float rs[4];
+      float rs[4];   // fp32 lane sums of the 4 rows
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float4& q = (u & 1) ? rq1 : rq0;
@@ -270,7 +270,11 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
+#if MDOT_K1_ROWRED_F32
+      const double tot = (double)warp_reduce4_f(rs[0], rs[1], rs[2], rs[3], lane);
+#else
       const double tot = warp_reduce4_t(rs[0], rs[1], rs[2], rs[3], lane);
+#endif
       // row multiplier M_i = 2^al_i of the row this lane writes (u = 2 h + l)
       const int srcm = 2 * k + ((lane >> 4) & 1);
       const float m0 = __shfl_sync(0xffffffffu, rq0.y, srcm);
@@ -278,7 +282,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       const float Mrow = (lane & 8) ? m1 : m0;
       const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
       if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot * (double)Mrow;
-      if (k & 1) {
+      if ((k % MDOT_K1_COLFLUSH) == MDOT_K1_COLFLUSH - 1) {
 #pragma unroll
         for (int q8 = 0; q8 < 8; ++q8) {
           csum[4 * lane + (q8 & 3) + 128 * (q8 >> 2)] += (double)cacc32[q8];

@@ -183,7 +183,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
       }
     }
 
+    #if MDOT_K1_ROWRED_F32
+    float rs[kUnroll];
+#else
     double rs[kUnroll];
+#endif
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       float rsum = 0.f;
@@ -199,14 +203,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
       }
       rs[u] = rsum;
     }
-    // row totals (fp64 butterfly over the warp), times M_i = 2^al_i
+    // row totals (butterfly over the warp, MDOT_K1_ROWRED_F32), times M_i = 2^al_i
     {
+#if MDOT_K1_ROWRED_F32
+      const double tot = (double)warp_reduce4_f(rs[0], rs[1], rs[2], rs[3], lane);
+#else
       const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
+#endif
       const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
       const float Mrow = (lane & 16) ? ((lane & 8) ? rp[3].y : rp[2].y) : ((lane & 8) ? rp[1].y : rp[0].y);
       if ((lane & 7) == 0 && i < tile_end) a.rowpart[(int64_t)blockIdx.x * nrows + i] = tot * (double)Mrow;
     }
-    if (++flush == 2) {   // 8 rows of fp32 column sums -> fp64
+    if (++flush == MDOT_K1_COLFLUSH) {   // 4 x MDOT_K1_COLFLUSH rows of fp32 column sums -> fp64
       flush = 0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) { cacc64[q] += (double)cacc32[q]; cacc32[q] = 0.f; }
@@ -243,6 +251,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 // FADD2 reads its broadcast operand straight from shared memory.
 // ---------------------------------------------------------------------------
 constexpr int kOtfChunk = 128;
+// K2 keeps the fp64 row butterfly: with the fp32 one ptxas spills ~700 bytes
+// per thread at the 128-register cap (the distance accumulators are live)
+#ifndef MDOT_K2_ROWRED_F32
+#define MDOT_K2_ROWRED_F32 0
+#endif
 
 // POW2: scale is a power of two, so C = acc * scale is exact and -g * C ==
 // (-g * scale) * acc exactly: the scale folds into (gh, gl) and the FMUL2 per
@@ -388,7 +401,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
           dk = sub2(xx, yb.y); acc[u][3] = fma2(dk, dk, acc[u][3]);
         }
       }
+#if MDOT_K2_ROWRED_F32
+      float rs[kUnroll];
+#else
       double rs[kUnroll];
+#endif
       float mrow[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -398,15 +415,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         u64 c2[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) c2[p] = POW2 ? acc[u][p] : mul2(acc[u][p], scale2);
+#if MDOT_K2_ROWRED_F32
+        rs[u] = entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);
+#else
         rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
+#endif
       }
       {
+#if MDOT_K2_ROWRED_F32
+        const double tot = (double)warp_reduce4_f(rs[0], rs[1], rs[2], rs[3], lane);
+#else
         const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
+#endif
         const int r = rb + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
         const float Mrow = (lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]);
         if ((lane & 7) == 0 && r < rows_c) a.rowpart[(int64_t)blockIdx.x * nrows + c0 + r] = tot * (double)Mrow;
       }
-      if (++flush == 2) {   // 8 rows of fp32 column sums -> fp64
+      if (++flush == MDOT_K1_COLFLUSH) {   // 4 x MDOT_K1_COLFLUSH rows of fp32 column sums -> fp64
         flush = 0;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {

@@ -236,6 +236,7 @@ struct PersistArgs {
   unsigned int* gbar;          // [2] grid barrier (zeroed before launch)
   double* cta_part;            // [grid][kNumScalars]
   unsigned long long* k1_ns;   // [2] += K1 phase ns (%globaltimer between grid barriers), count
+  unsigned long long* dbg_fin; // MDOT_DEBUG_K1TAIL: [64 slots][grid] %globaltimer when each CTA's consumers end K1
   int initial;                 // 1: the first slot is the projection's initial evaluation
   long long max_slots;
 };

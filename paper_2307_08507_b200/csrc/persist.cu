@@ -279,6 +279,10 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
     } else {
       tma_consume_pass<true>(S.tma, a.e, it, S.st.gpair[0], S.st.gpair[1], cta, ncta);
     }
+    if (a.dbg_fin && slot < 64) {
+      __syncthreads();
+      if (tid == 0) a.dbg_fin[slot * ncta + cta] = global_ns();
+    }
     grid_barrier(a.gbar, ncta);
     if (timer) {
       const unsigned long long t1 = global_ns();

@@ -736,12 +736,50 @@ static mdot_status persist_prepare(Workspace& w, const mdot_options& o, PersistA
   a.cta_part = w.blockpart;
   a.initial = 1;
   a.max_slots = (long long)1 << 40;
+  a.dbg_fin = nullptr;
+  if (getenv("MDOT_DEBUG_K1TAIL") && w.pers_grid > 0) {
+    CK(cudaMallocAsync((void**)&a.dbg_fin, (size_t)64 * w.pers_grid * 8, st));
+    CK(cudaMemsetAsync(a.dbg_fin, 0, (size_t)64 * w.pers_grid * 8, st));
+  }
   return MDOT_OK;
 }
 
 static mdot_status persist_collect(Workspace& w, const mdot_options& o, int t, mdot_result* res,
                                    const PersistArgs& a) {
   cudaStream_t st = w.st;
+  if (a.dbg_fin) {
+    // MDOT_DEBUG_K1TAIL: spread of the CTAs' K1 finish times per slot
+    const int g = w.pers_grid;
+    std::vector<unsigned long long> h((size_t)64 * g);
+    cudaMemcpyAsync(h.data(), a.dbg_fin, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double sum_mean = 0, sum_max = 0;
+    int ns = 0;
+    std::vector<double> late(g, 0.0);
+    for (int sl = 2; sl < 64; ++sl) {
+      unsigned long long mx = 0;
+      bool ok = true;
+      for (int c = 0; c < g; ++c) { if (!h[(size_t)sl * g + c]) ok = false; mx = std::max(mx, h[(size_t)sl * g + c]); }
+      if (!ok) break;
+      double sm = 0, smax = 0;
+      for (int c = 0; c < g; ++c) {
+        const double d = (double)(mx - h[(size_t)sl * g + c]) * 1e-3;
+        sm += d; smax = std::max(smax, d); late[c] += d;
+      }
+      sum_mean += sm / g; sum_max += smax; ++ns;
+    }
+    if (ns) {
+      fprintf(stderr, "[mdot] K1 tail over %d slots: mean CTA slack %.2f us, max %.2f us; slack by CTA group of 16:", ns,
+              sum_mean / ns, sum_max / ns);
+      for (int c0 = 0; c0 < g; c0 += 16) {
+        double z = 0; int k = 0;
+        for (int c = c0; c < std::min(g, c0 + 16); ++c) { z += late[c]; ++k; }
+        fprintf(stderr, " %.1f", z / k / ns);
+      }
+      fprintf(stderr, "\n");
+    }
+    cudaFreeAsync(a.dbg_fin, st);
+  }
   CtrlState h{};
   unsigned long long k1[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // [K1 ns, count, tm[0..7]]
   CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));

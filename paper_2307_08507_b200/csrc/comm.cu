@@ -162,8 +162,11 @@ mdot_status comm_allreduce(Comm* cm, double* buf, size_t count, int op, cudaStre
 // ---------------------------------------------------------------------------
 // Fused peer exchange (mdot_comm_enable_peer; persist.cu k_persist_peer)
 // ---------------------------------------------------------------------------
-static int64_t peer_ld(int64_t n) { return (n + kNumScalars + 31) / 32 * 32; }
-static size_t peer_recv_bytes(int nranks, int64_t ld) { return (size_t)2 * nranks * ld * sizeof(double); }
+// slot: [n column totals | kNumScalars row-scalar partials per CTA]
+constexpr int kPeerMaxCta = 512;
+static int64_t peer_ld(int64_t n) { return (n + (int64_t)kNumScalars * kPeerMaxCta + 31) / 32 * 32; }
+// 16-byte self-validating records (persist.cu ll_pack)
+static size_t peer_recv_bytes(int nranks, int64_t ld) { return (size_t)2 * nranks * ld * 16; }
 
 // views of rank q's block from this GPU
 static void peer_map(PeerState* ps, int q, void* base, int nranks) {
@@ -186,6 +189,7 @@ int comm_peer_ncta(const Comm* cm, int64_t n, int grid) {
   if (getenv("MDOT_NO_PEER")) return 0;
   // the in-process transport runs every rank's CTAs in one co-resident grid
   const int ncta = cm->local ? grid / cm->nranks : grid;
+  if (ncta > kPeerMaxCta) return 0;
   return ncta >= 1 ? ncta : 0;
 }
 

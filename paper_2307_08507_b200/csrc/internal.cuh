@@ -246,18 +246,20 @@ cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cuda
 
 // Row-sharded persistent projection with the column exchange fused into the
 // kernel over peer memory (SURVEY 8(e) NC1 without NCCL; DESIGN.md "Fused
-// peer exchange").  Per evaluation every rank pushes [its column totals | its
-// row scalars] into slot `rank` of EVERY rank's receive block with plain
-// stores through peer-mapped pointers (NVLink), fences at system scope and
-// raises its flag in every rank's flag array; each rank then sums the slots
-// in rank order (identical on every rank) and finalizes the replicated
-// columns.  Receive blocks are double-buffered by exchange parity: a rank
-// overwrites parity p only two exchanges later, after every rank has raised
-// the flag of the exchange in between (and so finished reading p).
+// peer exchange").  Per evaluation every CTA of every rank stores its column
+// totals and its row-scalar partial into slot `rank` of EVERY rank's receive
+// block through peer-mapped pointers (NVLink) as self-validating 16-byte
+// records {lo32, ex, hi32, ex}; each rank polls the records of its F2 column
+// chunk until they carry the exchange index, sums the slots in rank order
+// (identical on every rank) and finalizes the replicated columns.  Receive
+// blocks are double-buffered by exchange parity: a rank writes parity p again
+// only at exchange e + 2, after it has read every rank's exchange-(e + 1)
+// records, which those ranks wrote after the grid barrier that ended their
+// exchange-e reads.
 constexpr int kMaxPeers = 8;
 struct PeerNet {
-  double* recv[kMaxPeers];         // rank q's receive block as seen from this GPU: [2][nranks][ld] fp64
-  unsigned int* flag[kMaxPeers];   // rank q's flag array: [kMaxPeers] exchange epochs
+  double* recv[kMaxPeers];         // rank q's receive block as seen from this GPU: [2][nranks][ld] 16-byte records
+  unsigned int* flag[kMaxPeers];   // rank q's control words (after its records): [kMaxPeers] | epoch | err
   int nranks;
   int64_t ld;                      // slot stride (>= n + kNumScalars)
 };

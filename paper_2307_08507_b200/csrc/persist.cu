@@ -82,19 +82,40 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// System-scope flag operations of the fused peer exchange (peer memory is
-// written over NVLink; gpu scope does not cover another GPU's observers).
-__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// a flag wait longer than this means a peer is gone: record and fall through
-// (garbage scalars, no hang; the host reports MDOT_ENCCL)
+// a record wait longer than this means a peer is gone: record and fall
+// through (garbage scalars, no hang; the host reports MDOT_ENCCL)
 constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+// Self-validating 16-byte records of the peer exchange: {lo32, ex, hi32, ex}.
+// Each aligned 8-byte half {data, ex} is single-copy atomic, so a reader
+// that sees `ex` in both halves holds this exchange's value (NVLink stores
+// of one 16-byte vector may land as two 8-byte halves; each is checked).
+__device__ __forceinline__ uint4 ll_pack(double x, unsigned int ex) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return make_uint4((unsigned int)b, ex, (unsigned int)(b >> 32), ex);
+}
+__device__ __forceinline__ void ll_store(uint4* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ double ll_poll(const uint4* p, unsigned int ex, int* err) {
+  uint4 v;
+  unsigned long long t0 = 0;
+  for (;;) {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    if (v.y == ex && v.w == ex) break;
+    if (*(volatile int*)err) break;   // an earlier wait already timed out
+    if (t0 == 0) t0 = global_ns();
+    else if (global_ns() - t0 > kPeerTimeoutNs) {
+      *err = 1;
+      break;
+    }
+    __nanosleep(20);
+  }
+  return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
+}
 
 // Finalize partial totals of items [i_lo, i_lo + cnt): (item, sub) tasks over
 // all threads (a warp always holds whole octets); every partial load of up
@@ -320,72 +341,57 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
       // every CTA combines all CTA partials in the same order -> identical scalars
       combine_partials(a.cta_part, ncta, fin, S.st.sc);
     } else {
-      // F1: local rows finalize; this rank's column totals go to slot `me`
-      // of every rank's receive block (remote stores over NVLink)
+      // F1: local rows finalize; this CTA's column totals and its row-scalar
+      // partial go to slot `me` of every rank's receive block as
+      // self-validating 16-byte records {lo32, ex, hi32, ex} (the exchange
+      // index travels with every 8-byte half, as in NCCL's LL protocol): no
+      // fence, no flag -- a fence.sc.sys costs ~6 us per CTA here
       const int me = pg->rank, R = net->nranks;
       const int64_t ld = net->ld;
-      const unsigned int ep = ++epoch;
-      const int64_t slot_off = ((int64_t)(ep & 1u) * R + me) * ld;
+      const unsigned int ex = ++epoch;
+      uint4* const* recv = reinterpret_cast<uint4* const*>(net->recv);
+      const int64_t slot_off = ((int64_t)(ex & 1u) * R + me) * ld;
       for (int q = tid; q < cnt; q += blockDim.x) {
         const int64_t k = i_lo + q;
         if (k < a.f.nrows) {
           finalize_item(a.f, k, tots[q], v);
         } else {
-          const double t = tots[q];
+          const uint4 rec = ll_pack(tots[q], ex);
           const int64_t j = k - a.f.nrows;
 #pragma unroll 1
-          for (int p = 0; p < R; ++p) __stcg(net->recv[p] + slot_off + j, t);
+          for (int p = 0; p < R; ++p) ll_store(recv[p] + slot_off + j, rec);
         }
       }
-      __threadfence_system();
-      cta_partial(v, red, a.cta_part + (int64_t)cta * kNumScalars);
-      grid_barrier(a.gbar, ncta);
-      if (cta == 0) {
-        // this rank's row scalars -> slot tail, then the flag (release, sys)
-        combine_partials(a.cta_part, ncta, fin, nullptr);
-        if (tid < kNumScalars) {
-          const double y = fin[tid];
+      cta_partial(v, red, fin);   // fin[0..15] (tid < 16 wrote them)
+      if (tid < kNumScalars) {
+        const uint4 rec = ll_pack(fin[tid], ex);
 #pragma unroll 1
-          for (int p = 0; p < R; ++p) __stcg(net->recv[p] + slot_off + a.f.n + tid, y);
-          __threadfence_system();
-        }
-        __syncthreads();
-        if (tid == 0) {
-#pragma unroll 1
-          for (int p = 0; p < R; ++p) st_release_sys(net->flag[p] + me, ep);
-        }
+        for (int p = 0; p < R; ++p) ll_store(recv[p] + slot_off + a.f.n + kNumScalars * cta + tid, rec);
       }
-      // every rank's flag of this exchange (own flag array, local memory)
-      if (tid == 0) {
-        const unsigned long long t_w = global_ns();
-#pragma unroll 1
-        for (int p = 0; p < R; ++p) {
-          while ((int)(ld_acquire_sys(net->flag[me] + p) - ep) < 0) {
-            if (global_ns() - t_w > kPeerTimeoutNs) {
-              *pg->err = 1;
-              break;
-            }
-            __nanosleep(32);
-          }
-        }
-      }
-      __syncthreads();
       if (timer) tm[5] += global_ns() - tm[10];
       // F2: replicated columns, chunked identically on every rank (the
-      // scalars, and so every decision, are bitwise identical across ranks)
+      // scalars, and so every decision, are bitwise identical across ranks);
+      // each record is polled until it carries this exchange's index
 #pragma unroll
       for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
-      const double* rb = net->recv[me] + (int64_t)(ep & 1u) * R * ld;
+      const uint4* rb = recv[me] + (int64_t)(ex & 1u) * R * ld;
       const int64_t per2 = (a.f.n + ncta - 1) / ncta;
       const int64_t j_lo = (int64_t)cta * per2;
       const int64_t j_hi = (j_lo + per2 < a.f.n) ? j_lo + per2 : a.f.n;
       for (int64_t j = j_lo + tid; j < j_hi; j += blockDim.x) {
         double t = 0.0;
 #pragma unroll 1
-        for (int p = 0; p < R; ++p) t += __ldcg(rb + (int64_t)p * ld + j);
+        for (int p = 0; p < R; ++p) t += ll_poll(rb + (int64_t)p * ld + j, ex, pg->err);
         finalize_item(a.f, a.f.nrows + j, t, v);
       }
-      cta_partial(v, red, a.cta_part + (int64_t)cta * kNumScalars);
+      cta_partial(v, red, fin);
+      if (tid < kNumScalars) {
+        // + the row-scalar partials of CTA slot `cta` of every rank (rank order)
+        double t = 0.0;
+#pragma unroll 1
+        for (int p = 0; p < R; ++p) t += ll_poll(rb + (int64_t)p * ld + a.f.n + kNumScalars * cta + tid, ex, pg->err);
+        a.cta_part[(int64_t)cta * kNumScalars + tid] = fin[tid] + t;
+      }
       if (timer) tm[6] += global_ns() - tm[10];
       grid_barrier(a.gbar, ncta);
       if (timer) {
@@ -393,9 +399,8 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
         tm[2] += t2 - tm[10];
         tm[11] = t2;
       }
-      // column scalars (CTA order) + row scalars (rank order): identical on every rank
-      combine_partials(a.cta_part, ncta, fin, S.st.sc, rb + a.f.n, R, ld);
-      (void)R;
+      // identical on every rank: same partials, same order
+      combine_partials(a.cta_part, ncta, fin, S.st.sc);
     }
     if (timer) {
       tm[9] = global_ns();

@@ -158,43 +158,39 @@ def test_peer_exchange_rank_ordered_sum_is_identical_on_every_rank():
 
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_peer_exchange_protocol_double_buffering(G):
-    """Threads model of the in-kernel protocol: per exchange e, rank k writes
-    its slot into parity e & 1 of every rank's receive block, raises its flag
-    in every rank's flag array (epoch e), waits until every flag of its own
-    array reaches e, then reads its block of parity e & 1.  Random delays
-    between every step; a rank must never read a slot overwritten by a later
-    exchange (the two-exchange reuse distance of the parity buffers)."""
+    """Threads model of the in-kernel protocol (k_persist_peer, LL records):
+    per exchange e, every "CTA" (ncta per rank) of rank k writes its records
+    tagged e into parity e & 1 of every rank's receive block, then reads its
+    F2 chunk of every rank's records of its own block, polling each until it
+    carries e, then passes the rank's grid barrier.  Random delays between
+    steps; a record must never be overwritten (by exchange e + 2) before every
+    reader of exchange e has consumed it -- a reader that finds e + 2 spins to
+    the timeout and the test fails."""
     import random
     import threading
     import time
-    E = 40
-    recv = [[[None] * G for _ in range(2)] for _ in range(G)]   # [rank][parity][src]
-    flag = [[0] * G for _ in range(G)]                          # [rank][src]
+    E, ncta = 25, 3
+    recv = [[[[0] * ncta for _ in range(G)] for _ in range(2)] for _ in range(G)]   # [rank][parity][src][cta]
     errors = []
-    lock = threading.Lock()
+    bars = [threading.Barrier(ncta) for _ in range(G)]   # one grid barrier per rank
 
-    def rank_fn(k):
-        rnd = random.Random(1000 * G + k)
+    def cta_fn(k, c):
+        rnd = random.Random(1000 * G + 10 * k + c)
         for e in range(1, E + 1):
-            for p in range(G):
-                time.sleep(rnd.random() * 2e-4)
-                recv[p][e & 1][k] = (e, k)
-            time.sleep(rnd.random() * 2e-4)
-            for p in range(G):
-                with lock:
-                    flag[p][k] = e
-            t0 = time.time()
-            while any(flag[k][p] < e for p in range(G)):
-                time.sleep(1e-5)
-                if time.time() - t0 > 30:
-                    errors.append(("timeout", k, e))
-                    return
-            time.sleep(rnd.random() * 2e-4)
-            got = [recv[k][e & 1][p] for p in range(G)]
-            if got != [(e, p) for p in range(G)]:
-                errors.append((k, e, got))
+            for p in range(G):   # F1: store this CTA's record to every rank
+                time.sleep(rnd.random() * 1e-4)
+                recv[p][e & 1][k][c] = e
+            time.sleep(rnd.random() * 1e-4)
+            for p in range(G):   # F2: poll own block, chunk c of every source rank
+                t0 = time.time()
+                while recv[k][e & 1][p][c] != e:
+                    if recv[k][e & 1][p][c] > e or time.time() - t0 > 20:
+                        errors.append((k, c, e, p, recv[k][e & 1][p][c]))
+                        return
+                    time.sleep(1e-5)
+            bars[k].wait(timeout=60)   # grid barrier after F2 (before the next F1)
 
-    ths = [threading.Thread(target=rank_fn, args=(k,)) for k in range(G)]
+    ths = [threading.Thread(target=cta_fn, args=(k, c)) for k in range(G) for c in range(ncta)]
     for t in ths:
         t.start()
     for t in ths:

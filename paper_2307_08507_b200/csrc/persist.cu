@@ -302,7 +302,11 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
     }
     if (a.dbg_fin && slot < 64) {
       __syncthreads();
-      if (tid == 0) a.dbg_fin[slot * ncta + cta] = global_ns();
+      if (tid == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.dbg_fin[slot * ncta + cta] = (global_ns() << 8) | (smid & 255u);
+      }
     }
     grid_barrier(a.gbar, ncta);
     if (timer) {

@@ -753,6 +753,25 @@ static mdot_status persist_collect(Workspace& w, const mdot_options& o, int t, m
     std::vector<unsigned long long> h((size_t)64 * g);
     cudaMemcpyAsync(h.data(), a.dbg_fin, h.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
+    // low 8 bits: %smid of the CTA; per-SM pairs: finish(higher CTA index) - finish(lower)
+    std::vector<int> sm_of(g, -1);
+    for (int c = 0; c < g; ++c) sm_of[c] = (int)(h[(size_t)2 * g + c] & 255ull);
+    for (auto& x : h) x >>= 8;
+    {
+      double dsum = 0; int dn = 0, same = 0;
+      for (int c = 0; c < g; ++c)
+        for (int c2 = c + 1; c2 < g; ++c2)
+          if (sm_of[c] == sm_of[c2] && h[(size_t)2 * g + c] && h[(size_t)2 * g + c2]) {
+            for (int sl = 2; sl < 64; ++sl) {
+              const unsigned long long a0 = h[(size_t)sl * g + c], a1 = h[(size_t)sl * g + c2];
+              if (!a0 || !a1) break;
+              dsum += ((double)a1 - (double)a0) * 1e-3; ++dn;
+            }
+            if (c2 == c + g / 2) ++same;
+          }
+      fprintf(stderr, "[mdot] K1 tail: CTA pairs sharing an SM finish(higher idx) - finish(lower idx) = %.2f us mean over %d; pairs (c, c+grid/2): %d\n",
+              dn ? dsum / dn : 0.0, dn, same);
+    }
     double sum_mean = 0, sum_max = 0;
     int ns = 0;
     std::vector<double> late(g, 0.0);

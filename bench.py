@@ -259,8 +259,17 @@ def run_ours(a, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(a.warmup):
-        res = solve()
+    for w_i in range(a.warmup):
+        try:
+            res = solve()
+        except M.MdotError:
+            if comm is None or exchange is None or not exchange.startswith("fused") or w_i > 0:
+                raise
+            # the fused peer exchange failed on this box (e.g. a flag timeout):
+            # drop it on every rank and keep the NCCL path
+            M.mdot_comm_enable_peer(comm, 0, check=False)
+            exchange = "nccl allreduce in CUDA-graph slots (fused peer exchange failed)"
+            res = solve()
     barrier()
     clk = ClockSampler(local_rank)
     clk.start()

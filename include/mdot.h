@@ -225,7 +225,9 @@ mdot_status mdot_comm_destroy(mdot_comm* comm);
  * in-process comm), MDOT_ECUDA (allocation / IPC / peer access failed on ANY
  * rank -- every rank returns it and keeps the NCCL / host path), MDOT_ENOMEM.
  * A solve whose in-kernel flag wait times out (a peer died) returns
- * MDOT_ENCCL.  MDOT_NO_PEER=1 in the environment disables the path. */
+ * MDOT_ENCCL.  MDOT_NO_PEER=1 in the environment disables the path;
+ * n_max = 0 (collective) frees the exchange blocks and returns the comm to
+ * the NCCL / host path. */
 mdot_status mdot_comm_enable_peer(mdot_comm* comm, int64_t n_max);
 /* local rows [row0, row0 + n_local) of C (local_rows->C points at row row0,
  * n_local*n entries) or of X (local_rows->X at row row0; Y, r, c full).

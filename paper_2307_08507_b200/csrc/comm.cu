@@ -335,7 +335,14 @@ mdot_status mdot_comm_create_local(const char* group, int32_t nranks, int32_t ra
 
 mdot_status mdot_comm_enable_peer(mdot_comm* c, int64_t n_max) {
   Comm* cm = reinterpret_cast<Comm*>(c);
-  if (!cm || n_max < 1) { set_error("bad arguments"); return MDOT_EINVAL; }
+  if (!cm || n_max < 0) { set_error("bad arguments"); return MDOT_EINVAL; }
+  if (n_max == 0) {   // disable (collective: every rank drops its block)
+    if (cm->local && cm->peer) local_barrier(cm->local);
+    if (cudaSetDevice(cm->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }
+    cudaDeviceSynchronize();
+    peer_free(cm);
+    return MDOT_OK;
+  }
   if (cm->nranks > kMaxPeers) { set_error("fused peer exchange supports at most %d ranks", kMaxPeers); return MDOT_EINVAL; }
   if (!cm->local && !cm->nccl) { set_error("single-rank communicator: nothing to exchange"); return MDOT_EINVAL; }
   if (cudaSetDevice(cm->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }

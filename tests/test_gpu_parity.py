@@ -314,6 +314,58 @@ def test_full_size_config4_sampled_parity():
     assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
 
 
+def test_full_size_config4_bench_configuration():
+    """The headline solve exactly as bench.py times it (config 4 instance 0,
+    n = 16384, 1 GiB fp32 C, FIXED schedule to gbar 4096 with T = 16, L1 stop
+    1e-6, persistent kernel): the fp64 oracle re-evaluates the returned
+    potentials over the full matrix (marginal L1 of P(U, V) and the costs
+    <C, P(U, V)> and <C, G> of the rounded plan)."""
+    inst = S.config4(0)
+    n = inst.n
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    eps, gb = 1e-6, 4096.0
+    res = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, gb), options=M.options(eps=eps),
+                       u_out=U, v_out=V)
+    assert res["status"] == 0 and res["md_steps"] == 16 and res["control_path"] == 2
+    assert res["l1_final"] <= eps
+    prob = O.OracleProblem(inst)
+    Un, Vn = U.cpu().numpy(), V.cpu().numpy()
+    lr, lc, st = O.log_marginals(prob, Un, Vn, gb)
+    assert st == 0
+    l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
+    assert l1 <= 2 * eps, l1
+    rp = O.round_plan(prob, Un, Vn, gb)
+    assert abs(res["cost_unrounded"] - rp["cost_F"]) <= 1e-9 * rp["cost_F"], (res["cost_unrounded"], rp["cost_F"])
+    # the GPU rounds with the marginals of its last fp32-entry evaluation, the
+    # oracle with exact fp64 ones: the rounded plans differ by O(L1) (Z20 gate)
+    allow = max(1e-5 * rp["cost_G"], 2 * (res["l1_final"] + l1) * 1.0)
+    assert abs(res["cost_rounded"] - rp["cost_G"]) <= allow, (res["cost_rounded"], rp["cost_G"])
+
+
+def test_full_size_config4_fused_peer_exchange():
+    """Config 4 at full size row-sharded over 4 emulated ranks with the fused
+    peer exchange (one cooperative launch per MD step on one GPU): identical
+    results on every rank, the oracle's marginal L1 of the assembled
+    potentials within 2 eps, cost within 2e-6 of the single-GPU solve."""
+    inst = S.config4(0)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, 4096.0)
+    eps = 1e-6
+    out = _sharded_solve_threads(inst, 4, sched, {"eps": eps}, "peerfull4", peer=True)
+    assert all(o[0]["control_path"] == 2 and o[0]["status"] == 0 for o in out)
+    assert all(o[0]["cost_unrounded"] == out[0][0]["cost_unrounded"] for o in out)
+    assert all(np.array_equal(o[2], out[0][2]) for o in out)
+    U = np.concatenate([o[1] for o in out])
+    V = out[0][2]
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, U, V, 4096.0)
+    l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
+    assert l1 <= 2 * eps, l1
+    ref = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(eps=eps))
+    assert abs(out[0][0]["cost_unrounded"] - ref["cost_unrounded"]) <= 2e-6 * ref["cost_unrounded"]
+
+
 @pytest.mark.parametrize("n", [512, 2048])
 def test_tma_kernel_bitwise_equals_generic_kernel(n, monkeypatch):
     """The TMA-fed persistent kernel and the generic LDG kernel assign the same
@@ -425,6 +477,34 @@ def test_otf_marginals_match_oracle(n, d, generic, monkeypatch):
     assert fb == 0
     err_r = np.max(np.abs(np.expm1(lr.cpu().numpy() - lr_o)))
     err_c = np.max(np.abs(np.expm1(lc.cpu().numpy() - lc_o)))
+    assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
+
+
+def test_full_size_config5_sampled_parity():
+    """BASELINE config 5 at full size (n = 65536, d = 16, C computed in-kernel
+    by the packed K2 kernel): one evaluation at potentials from a short GPU
+    solve; sampled rows / columns recomputed by the oracle one by one
+    (O(n d) each), and every marginal checked finite / positive."""
+    inst = S.config5(0)
+    n = inst.n
+    X, Y, r, c = _t(inst.X), _t(inst.Y), _t(inst.r), _t(inst.c)
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    gb = 256.0
+    res = M.mdot_solve(X=X, Y=Y, scale=inst.scale, r=r, c=c, schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=1),
+                       options=M.options(eps=1e-3), u_out=U, v_out=V)
+    assert res["status"] == 0 and res["l1_final"] <= 1e-3
+    lr, lc, fb = M.mdot_marginals(U, V, gb, X=X, Y=Y, scale=inst.scale, r=r, c=c)
+    assert fb == 0
+    lr, lc = lr.cpu().numpy(), lc.cpu().numpy()
+    assert np.all(np.isfinite(lr)) and np.all(np.isfinite(lc))
+    prob = O.OracleProblem(inst)
+    rng = np.random.default_rng(1)
+    rows = np.sort(rng.choice(n, 16, replace=False))
+    cols = np.sort(rng.choice(n, 16, replace=False))
+    sub = O.log_marginal_subset(prob, U.cpu().numpy(), V.cpu().numpy(), gb, rows=rows, cols=cols)
+    err_r = np.max(np.abs(np.expm1(lr[rows] - sub["rows"])))
+    err_c = np.max(np.abs(np.expm1(lc[cols] - sub["cols"])))
     assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
 
 

@@ -341,6 +341,7 @@ def run_ours(a, rank, world, local_rank):
                      "bytes_per_launch": bytes_per_launch, "launches_timed": kern_n,
                      "timing": timing,
                      "mean_launch_us": mean_launch_s * 1e6,
+                     "kernel_evals_per_s": (1.0 / mean_launch_s) if kern_n else None,
                      "kernel_share_of_step": (mean_launch_s * evals / (ms / 1000.0)) if kern_n else None},
         "clocks": clocks,
         "gpu_launches": launches,

@@ -292,6 +292,7 @@ cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const do
                         double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
                         cudaStream_t st);
 // column partials -> local column totals (generic kernel, sharded mode)
+cudaError_t launch_sample_c(const void* C, int c64, int64_t count, int S, double* out, cudaStream_t st);
 cudaError_t launch_minmax(const void* C, int c64, int64_t count, double* out2, cudaStream_t st);
 cudaError_t launch_reduce_colpart(const double* colpart, int n_row_tiles, int64_t n, double* coltot, cudaStream_t st,
                                   const int* done = nullptr);

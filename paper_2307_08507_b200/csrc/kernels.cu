@@ -886,6 +886,20 @@ cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, c
   return cudaGetLastError();
 }
 
+// Sampled input check (C in [0, 1]): 64 entries at a fixed
+// hash of the index gathered by one launch into a mapped host buffer (one
+// synchronisation instead of one device-to-host copy per sample).
+__global__ void k_sample_c(const void* C, int c64, int64_t count, int S, double* out) {
+  const int q = threadIdx.x;
+  if (q >= S) return;
+  const int64_t idx = (int64_t)(((uint64_t)q * 2654435761ull) % (uint64_t)count);
+  out[q] = c64 ? reinterpret_cast<const double*>(C)[idx] : (double)reinterpret_cast<const float*>(C)[idx];
+}
+cudaError_t launch_sample_c(const void* C, int c64, int64_t count, int S, double* out, cudaStream_t st) {
+  k_sample_c<<<1, 64, 0, st>>>(C, c64, count, S, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // sharded helpers
 // ---------------------------------------------------------------------------

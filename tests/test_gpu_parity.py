@@ -799,3 +799,46 @@ def test_solve_is_bitwise_deterministic(dc):
         outs.append((res["evaluations"], res["cost_unrounded"].hex(), res["cost_rounded"].hex(),
                      U.cpu().numpy().tobytes(), V.cpu().numpy().tobytes()))
     assert outs[0] == outs[1] == outs[2]
+
+
+# ------------------------------------------- SPEC acceptance criteria on the GPU path
+def test_gpu_pncg_fewer_iterations_than_sinkhorn():
+    """SPEC criterion 10 on the CUDA path: n = 256, m = 4
+    sphere points, entropy 0.9 log2 n, gbar = 256, T = 1, rho <= 1e-9 (fp64
+    entries under AUTO precision): PNCG needs fewer iterations than Sinkhorn
+    on every instance and >= 3x fewer on average."""
+    ratios = []
+    for seed in range(3):
+        inst = S.paper_sphere_instance(256, 4, 0.9, seed=600 + seed)
+        C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+        sched = M.schedule(M.MDOT_SCHED_EXPLICIT, gammas=[256.0])
+        rp = M.mdot_solve(C, r, c, schedule=sched, options=M.options(eps=1e-9, stop=1))
+        rs = M.mdot_sinkhorn(C, r, c, schedule=sched, options=M.options(eps=1e-9, stop=1))
+        assert rp["status"] == 0 and rs["status"] == 0
+        assert rp["iterations"] <= rs["iterations"]
+        ratios.append(rs["iterations"] / rp["iterations"])
+    assert np.mean(ratios) >= 3.0, ratios
+
+
+def test_gpu_line_search_evaluations_per_iteration():
+    """SPEC criterion 9 / PAPER.md:698 ("typically 2-4" phi' evaluations per
+    line search): mean line-search evaluations per PNCG iteration <= 6 on the
+    CUDA path (config-3-shaped instance, device control)."""
+    inst = S.config3(0, frac=0.9, n=1024)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, 512.0, T=4),
+                       options=M.options(eps=1e-6))
+    assert res["status"] == 0
+    assert res["ls_evaluations"] / res["iterations"] <= 6.0
+
+
+def test_gpu_warm_start_rho0_decreases():
+    """SPEC criterion 12 / Fig. 2 left: with warm starts
+    the initial infeasibility rho_0 of the last MD step is below the first
+    one's, on the CUDA path (result.rho0 per MD step; n = 384 takes the
+    grid-wide path -- the one-CTA small-problem route does not record rho0)."""
+    for seed in range(2):
+        inst = S.paper_sphere_instance(384, 4, 0.9, seed=500 + seed)
+        res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, 512.0, T=16),
+                           options=M.options(eps=1e-9, stop=1))
+        assert res["status"] == 0 and len(res["rho0"]) == 16
+        assert res["rho0"][-1] < res["rho0"][0], res["rho0"]

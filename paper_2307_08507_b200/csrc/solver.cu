@@ -1006,6 +1006,8 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       else if (sharded()) pers_grid = comm_peer_ncta(comm, n, persist_grid());
       else pers_grid = comm ? 0 : persist_grid();
       if (persist_ncta > 0 && pers_grid > persist_ncta) pers_grid = persist_ncta;
+      if (persist_ncta == 0 && getenv("MDOT_PERSIST_NCTA") && pers_grid > atoi(getenv("MDOT_PERSIST_NCTA")))
+        pers_grid = atoi(getenv("MDOT_PERSIST_NCTA"));   // A/B only
       if (pers_grid > 0 && (nrows + n + pers_grid - 1) / pers_grid > persist_max_chunk()) pers_grid = 0;
     }
   }

@@ -32,6 +32,9 @@ constexpr int kNumScalars = 16;
 #ifndef MDOT_K1_ROWRED_F32
 #define MDOT_K1_ROWRED_F32 1
 #endif
+#ifndef MDOT_K1_PACKED
+#define MDOT_K1_PACKED 1
+#endif
 #ifndef MDOT_K1_COLFLUSH
 #define MDOT_K1_COLFLUSH 4
 #endif

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "entry.cuh"
 #include "internal.cuh"
 
 namespace mdot {
@@ -224,6 +225,14 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
     double* csum = &sm.sred[warp][0];
 #pragma unroll
     for (int q = 0; q < 8; ++q) { csum[4 * lane + (q & 3) + 128 * (q >> 2)] = 0.0; cacc32[q] = 0.f; }
+#if MDOT_K1_PACKED
+    // packed f32x2 entry arithmetic (entry.cuh): column pairs (2p, 2p+1)
+    ColPairs cpp;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) { cpp.bh[p] = pk2(bh[2 * p], bh[2 * p + 1]); cpp.T[p] = pk2(T[2 * p], T[2 * p + 1]); }
+    u64 cacc2[4] = {0ull, 0ull, 0ull, 0ull};
+    const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl);
+#endif
 
     // lane l holds rows (stage l/2, u = 2 (l & 1) + {0, 1}) of this warp
     float4 rq0, rq1;
@@ -248,6 +257,10 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
         const float* row = &sm.stage[s][4 * warp + u][0];
         const float4 x0 = *reinterpret_cast<const float4*>(row + 4 * lane);
         const float4 x1 = *reinterpret_cast<const float4*>(row + 128 + 4 * lane);
+#if MDOT_K1_PACKED
+        const u64 c2[4] = {pk2(x0.x, x0.y), pk2(x0.z, x0.w), pk2(x1.x, x1.y), pk2(x1.z, x1.w)};
+        rs[u] = entry_row8_f(c2, make_float4(ah, 0.f, S, 0.f), cpp, ngh2, ngl2, cacc2);
+#else
         const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         float rsum = 0.f;
 #pragma unroll
@@ -259,6 +272,7 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
           cacc32[q8] = fmaf(e, S, cacc32[q8]);
         }
         rs[u] = rsum;
+#endif
       }
       // release the slot.  The reads above are generic-proxy shared-memory
       // loads and the refill is an async-proxy (TMA) write: without this
@@ -283,6 +297,10 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
       const int64_t i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
       if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot * (double)Mrow;
       if ((k % MDOT_K1_COLFLUSH) == MDOT_K1_COLFLUSH - 1) {
+#if MDOT_K1_PACKED
+#pragma unroll
+        for (int p = 0; p < 4; ++p) { up2(cacc2[p], cacc32[2 * p], cacc32[2 * p + 1]); cacc2[p] = 0ull; }
+#endif
 #pragma unroll
         for (int q8 = 0; q8 < 8; ++q8) {
           csum[4 * lane + (q8 & 3) + 128 * (q8 >> 2)] += (double)cacc32[q8];
@@ -290,6 +308,10 @@ __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a,
         }
       }
     }
+#if MDOT_K1_PACKED
+#pragma unroll
+    for (int p = 0; p < 4; ++p) up2(cacc2[p], cacc32[2 * p], cacc32[2 * p + 1]);
+#endif
 #pragma unroll
     for (int q8 = 0; q8 < 8; ++q8) csum[4 * lane + (q8 & 3) + 128 * (q8 >> 2)] += (double)cacc32[q8];
 

@@ -128,6 +128,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
   float cacc32[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) { cacc64[q] = 0.0; cacc32[q] = 0.f; }
+#if MDOT_K1_PACKED
+  ColPairs cpp;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) { cpp.bh[p] = pk2(bh[2 * p], bh[2 * p + 1]); cpp.T[p] = pk2(T[2 * p], T[2 * p + 1]); }
+  u64 cacc2[4] = {0ull, 0ull, 0ull, 0ull};
+  const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl);
+#endif
 
   const int64_t tile_end = (i0 + a.tile_m < nrows) ? i0 + a.tile_m : nrows;
   int flush = 0;
@@ -190,6 +197,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 #endif
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
+#if MDOT_K1_PACKED
+      const u64 c2[4] = {pk2(cv[u][0], cv[u][1]), pk2(cv[u][2], cv[u][3]), pk2(cv[u][4], cv[u][5]),
+                         pk2(cv[u][6], cv[u][7])};
+      rs[u] = entry_row8_f(c2, rp[u], cpp, ngh2, ngl2, cacc2);
+#else
       float rsum = 0.f;
       const float ah = rp[u].x, S = rp[u].z;
 #pragma unroll
@@ -202,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
         cacc32[q] = fmaf(e, S, cacc32[q]);
       }
       rs[u] = rsum;
+#endif
     }
     // row totals (butterfly over the warp, MDOT_K1_ROWRED_F32), times M_i = 2^al_i
     {
@@ -216,10 +229,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
     }
     if (++flush == MDOT_K1_COLFLUSH) {   // 4 x MDOT_K1_COLFLUSH rows of fp32 column sums -> fp64
       flush = 0;
+#if MDOT_K1_PACKED
+#pragma unroll
+      for (int p = 0; p < 4; ++p) { up2(cacc2[p], cacc32[2 * p], cacc32[2 * p + 1]); cacc2[p] = 0ull; }
+#endif
 #pragma unroll
       for (int q = 0; q < 8; ++q) { cacc64[q] += (double)cacc32[q]; cacc32[q] = 0.f; }
     }
   }
+#if MDOT_K1_PACKED
+#pragma unroll
+  for (int p = 0; p < 4; ++p) up2(cacc2[p], cacc32[2 * p], cacc32[2 * p + 1]);
+#endif
 #pragma unroll
   for (int q = 0; q < 8; ++q) cacc64[q] += (double)cacc32[q];
 

@@ -24,6 +24,11 @@ namespace mdot {
 
 namespace cg = cooperative_groups;
 
+// MDOT_K8_TAIL_REGULAR=1 (A/B): keep the regular 256-column mapping for the
+// narrow last tile
+__constant__ int g_k8_tail_regular = 0;
+__device__ __forceinline__ bool batch_tail_regular() { return g_k8_tail_regular != 0; }
+
 // 16 warps: one CTA per instance has an SM to itself and its evaluation is
 // latency-bound (8 warps: 2 per scheduler, 13 % issue utilisation); the
 // column-partial scratch stays [8][256] (two-round reduction)
@@ -82,6 +87,119 @@ struct BatchSmem {
 // coltot[j] = sum_i 2^w S_i (anchored units, internal.cuh "K1 numerics").
 // F64: w assembled and exponentiated in fp64 (fp64-entry mode, eps < 1e-7,
 // and the range-guard fallback).
+// Narrow last column tile (w = n - j0 <= 64 columns, fp32 entries, packed
+// arithmetic): the regular mapping gives every lane 8 columns of ONE row, so
+// a 16-column tail (n = 784 = 3 x 256 + 16, config 2) would keep 28 of 32
+// lanes idle for a full tile's worth of row steps.  Here Lp = pow2ceil(w/8)
+// lanes share a row (8 columns each) and a warp step covers 32/Lp rows; rows
+// follow the cluster split of batch_eval (64-row blocks, block b to CTA
+// b % CL), so row totals stay with their owner.  Column sums: per lane over
+// its rows, fp32 over 16 rows then fp64, then the lanes of one column group
+// (shuffles) and the warps (shared memory) in a fixed order.
+__device__ void batch_eval_tail_packed(const float* __restrict__ C, int n, int j0, const float4* prm, float gh,
+                                       float gl, double* rowtot, double* coltot, double (*sred)[kTileN], int q_rank,
+                                       int CL) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float4* rowp = prm;
+  const float4* colp = prm + n;
+  const int w = n - j0;
+  int Lp = 1;
+  while (8 * Lp < w) Lp *= 2;                 // lanes per row (<= 8)
+  const int R = 32 / Lp;                      // rows per warp step
+  const int rr = lane / Lp, cl = lane % Lp;   // this lane's row slot and column group
+  const int jc = j0 + 8 * cl;                 // first of this lane's 8 columns
+  // column pairs of this lane (masked past n)
+  ColPairs cpp;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float b2[2], t2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = jc + 2 * p + h;
+      if (j < n) { const float4 c = colp[j]; b2[h] = c.x; t2[h] = c.z; }
+      else { b2[h] = -1.0e30f; t2[h] = 0.f; }
+    }
+    cpp.bh[p] = pk2(b2[0], b2[1]);
+    cpp.T[p] = pk2(t2[0], t2[1]);
+  }
+  const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl);
+  u64 cacc2[4] = {0ull, 0ull, 0ull, 0ull};
+  double c64[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c64[k] = 0.0;
+  // rows owned by this CTA: 64-row blocks b = q_rank + CL m
+  const int nblk = (n + 63) / 64;
+  const int own_blocks = (nblk - q_rank + CL - 1) / CL;
+  const int own_rows = own_blocks * 64;        // row slots (some past n)
+  int fl = 0;
+  for (int base = warp * R; base < own_rows; base += R * kBatchWarps) {
+    const int slot = base + rr;
+    const int i = 64 * (q_rank + CL * (slot / 64)) + (slot % 64);
+    const bool ok = slot < own_rows && i < n;
+    float4 rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+    u64 c2[4] = {0ull, 0ull, 0ull, 0ull};
+    if (ok) {
+      rp = rowp[i];
+      const float* crow = C + (int64_t)i * n;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int j = jc + 2 * p;
+        const float x0 = (j < n) ? __ldg(crow + j) : 0.f;
+        const float x1 = (j + 1 < n) ? __ldg(crow + j + 1) : 0.f;
+        c2[p] = pk2(x0, x1);
+      }
+    }
+    float rsum = entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);
+    // the Lp lanes of this row: xor 1 .. Lp/2 (fixed tree)
+    for (int off = 1; off < Lp; off <<= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, off);
+    if (ok && cl == 0) {
+      const double v = (double)rsum * (double)rp.y;   // times M_i
+      rowtot[i] = (j0 == 0) ? v : rowtot[i] + v;
+    }
+    if (++fl == 4) {   // 4 steps of fp32 column sums -> fp64
+      fl = 0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        float lo, hi;
+        up2(cacc2[p], lo, hi);
+        c64[2 * p] += (double)lo;
+        c64[2 * p + 1] += (double)hi;
+        cacc2[p] = 0ull;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float lo, hi;
+    up2(cacc2[p], lo, hi);
+    c64[2 * p] += (double)lo;
+    c64[2 * p + 1] += (double)hi;
+  }
+  // lanes with the same column group: xor Lp, 2 Lp, .. 16 (fixed tree)
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    for (int off = Lp; off < 32; off <<= 1) c64[k] += __shfl_xor_sync(0xffffffffu, c64[k], off);
+  // warps in a fixed order through the shared scratch (two rounds, as batch_eval)
+  if (rr == 0 && warp >= kSredRows) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sred[warp - kSredRows][8 * cl + k] = c64[k];
+  }
+  __syncthreads();
+  if (rr == 0 && warp < kSredRows) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sred[warp][8 * cl + k] = c64[k] + sred[warp][8 * cl + k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 * Lp) {
+    const int t = threadIdx.x;
+    double acc = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kSredRows; ++ww) acc += sred[ww][t];
+    if (j0 + t < n) coltot[j0 + t] = acc * (double)colp[j0 + t].y;   // times M_j
+  }
+  __syncthreads();
+}
+
 // Cluster split (CL CTAs per instance, q = this CTA's rank): the CTA takes
 // the row groups ib = 4 (q W + w) + 4 W CL m; row totals are complete for
 // its rows, column totals are partial over them (combined by the caller).
@@ -95,6 +213,10 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
   const float4* colp = prm + n;
   const bool vec4 = (n % 4) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   for (int j0 = 0; j0 < n; j0 += kTileN) {
+    if (!F64 && PACKED && sizeof(CT) == 4 && n - j0 <= 64 && !batch_tail_regular()) {
+      batch_eval_tail_packed(reinterpret_cast<const float*>(C), n, j0, prm, gh, gl, rowtot, coltot, sred, q_rank, CL);
+      continue;
+    }
     float bh[8], T[8];
     double Bd[F64 ? 8 : 1];
     float Wd[F64 ? 8 : 1];
@@ -591,6 +713,14 @@ cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int CL = batch_cluster(a.n, B);
+  {
+    static int set = -1;
+    const int v = getenv("MDOT_K8_TAIL_REGULAR") ? 1 : 0;
+    if (set != v) {
+      cudaMemcpyToSymbol(g_k8_tail_regular, &v, sizeof(int));
+      set = v;
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(B * CL));
   cfg.blockDim = dim3(kBatchThreads);

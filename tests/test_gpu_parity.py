@@ -849,3 +849,19 @@ def test_gpu_warm_start_rho0_decreases():
                            options=M.options(eps=1e-9, stop=1))
         assert res["status"] == 0 and len(res["rho0"]) == 16
         assert res["rho0"][-1] < res["rho0"][0], res["rho0"]
+
+
+@pytest.mark.parametrize("n", [264, 272, 288, 300, 320])
+def test_k8_narrow_last_tile_matches_oracle(n):
+    """K8's narrow-last-tile mapping (w = n mod 256 <= 64 columns: 1, 2, 4 or 8
+    lanes per row) through the one-CTA small-problem route, against the oracle."""
+    inst = S.uniform_points_instance(3, n, 2, 40 + n % 7, marg="dirichlet")
+    prob = O.OracleProblem(inst)
+    eps, gb = 1e-6, 512.0
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=2),
+                       options=M.options(eps=eps), u_out=U, v_out=V)
+    assert res["control_path"] == 3   # the one-CTA K8 route
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=2), O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)

@@ -851,7 +851,7 @@ def test_gpu_warm_start_rho0_decreases():
         assert res["rho0"][-1] < res["rho0"][0], res["rho0"]
 
 
-@pytest.mark.parametrize("n", [264, 272, 288, 300, 320])
+@pytest.mark.parametrize("n", [5, 17, 64, 264, 272, 288, 300, 320])
 def test_k8_narrow_last_tile_matches_oracle(n):
     """K8's narrow-last-tile mapping (w = n mod 256 <= 64 columns: 1, 2, 4 or 8
     lanes per row) through the one-CTA small-problem route, against the oracle."""

@@ -558,6 +558,11 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     }
     // projection result
     const CtrlState& h = S.st;
+    if (tid == 0 && q_rank == 0 && t <= 64) {
+      a.res[b].rho0[t - 1] = h.rho_0;
+      a.res[b].l10[t - 1] = h.l1_0;
+      a.res[b].iters_step[t - 1] = h.iterations;
+    }
     evals_total += h.evals;
     iters += h.iterations;
     ls_evals += h.ls_evals;

@@ -348,6 +348,8 @@ struct BatchResult {
   double cost_rounded, cost_unrounded, l1_final, rho_final, gamma_bar;
   long long evaluations, iterations, ls_evaluations, resets, ls_restarts;
   int md_steps, status;
+  double rho0[64], l10[64];      // per MD step (t <= 64): initial infeasibility / L1 of the projection
+  long long iters_step[64];      // per MD step iterations
 };
 struct BatchArgs {
   const float* C;          // shared n x n fp32 cost (device)

@@ -1300,14 +1300,15 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
 // kernel with one instance): below a few hundred points an evaluation is a
 // few thousand entries and the grid-wide paths pay ~20 us of launch /
 // barrier / control latency per evaluation instead.  Threshold: MDOT_SMALL_N
-// (default 320: crossover between n = 256 and 384, profiles/r01_small_n_route.txt); the host control
+// (default 512: crossover between n = 512 and 784 once K8 runs on thread-block clusters with the
+// narrow-tile mapping; it was 320 before, profiles/r01_small_n_route.txt); the host control
 // loop (device_control = 0) and dense plan outputs keep the general path.
 static bool small_route(const mdot_problem* pb, const mdot_options* opt, const float* P_out) {
   if (!pb || P_out || pb->n < 1) return false;
   if (pb->kind != MDOT_COST_DENSE_F32 && pb->kind != MDOT_COST_DENSE_F64) return false;
   if (opt && opt->device_control == 0) return false;
   if (getenv("MDOT_NO_BATCH_KERNEL")) return false;
-  int64_t lim = 320;
+  int64_t lim = 512;
   if (const char* e = getenv("MDOT_SMALL_N")) lim = atoll(e);
   return pb->n <= lim;
 }
@@ -1557,6 +1558,11 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     R.ls_restarts = h.ls_restarts;
     R.status = h.status;
     R.control_path = 3;   // K8 batched kernel
+    for (int q = 0; q < 64 && q < h.md_steps; ++q) {
+      R.rho0[q] = h.rho0[q];
+      R.l10[q] = h.l10[q];
+      R.iters_step[q] = h.iters_step[q];
+    }
     R.all_launches = 1;
     if (h.status != MDOT_OK && first == MDOT_OK) {
       first = (mdot_status)h.status;

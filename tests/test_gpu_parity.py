@@ -841,10 +841,10 @@ def test_gpu_line_search_evaluations_per_iteration():
 def test_gpu_warm_start_rho0_decreases():
     """SPEC criterion 12 / Fig. 2 left: with warm starts
     the initial infeasibility rho_0 of the last MD step is below the first
-    one's, on the CUDA path (result.rho0 per MD step; n = 384 takes the
-    grid-wide path -- the one-CTA small-problem route does not record rho0)."""
-    for seed in range(2):
-        inst = S.paper_sphere_instance(384, 4, 0.9, seed=500 + seed)
+    one's, on the CUDA path (result.rho0 per MD step), on the one-CTA K8 route
+    (n = 128) and the grid-wide path (n = 700)."""
+    for seed, nn in enumerate((128, 700)):
+        inst = S.paper_sphere_instance(nn, 4, 0.9, seed=500 + seed)
         res = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, 512.0, T=16),
                            options=M.options(eps=1e-9, stop=1))
         assert res["status"] == 0 and len(res["rho0"]) == 16

@@ -865,3 +865,32 @@ def test_k8_narrow_last_tile_matches_oracle(n):
     assert res["control_path"] == 3   # the one-CTA K8 route
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=2), O.make_options(eps=eps))
     _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+@pytest.mark.parametrize("n", [10, 700])
+def test_gpu_near_delta_marginal_gives_independence_coupling(n):
+    """PAPER.md:148 on the CUDA path (small-problem route at n = 10, the
+    persistent grid path at n = 700): with r a near-delta the only feasible
+    plan is r c^T, so the rounded cost is sum_j c_j C_{i*, j}."""
+    inst = S.random_small(n, seed=17, dtype=np.float32) if n <= 64 else \
+        S.uniform_points_instance(3, n, 2, 17, marg="dirichlet")
+    r = np.full(n, 1e-13)
+    r[3] = 1.0 - (n - 1) * 1e-13
+    C = inst.C.astype(np.float32)
+    res = M.mdot_solve(_t(C), _t(r), _t(inst.c), schedule=M.schedule(M.MDOT_SCHED_FIXED, 256.0),
+                       options=M.options(eps=1e-9))
+    assert res["status"] == 0
+    ind = float((np.outer(r, inst.c) * C.astype(np.float64)).sum())
+    assert abs(res["cost_rounded"] - ind) <= 1e-8 * max(ind, 1e-12) + 1e-12, (res["cost_rounded"], ind)
+
+
+def test_gpu_gamma_4096_single_step_is_stable():
+    """SPEC criterion 13 inverted on the CUDA path: one MD step of gamma_t =
+    4096 (the paper's non-log implementation failed above 256)
+    reaches the same plan as the paper's 16-step schedule (Lemma 2)."""
+    inst = S.uniform_points_instance(3, 700, 2, 0, marg="dirichlet")
+    C, r, c = _t(inst.C), _t(inst.r), _t(inst.c)
+    r1 = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_EXPLICIT, gammas=[4096.0]), options=M.options(eps=1e-6))
+    r16 = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, 4096.0), options=M.options(eps=1e-6))
+    assert r1["status"] == 0 and r16["status"] == 0 and r1["md_steps"] == 1 and r16["md_steps"] == 16
+    assert abs(r1["cost_unrounded"] - r16["cost_unrounded"]) <= COST_GATE * r16["cost_unrounded"]

@@ -200,13 +200,22 @@ __device__ void batch_eval_tail_packed(const float* __restrict__ C, int n, int j
   __syncthreads();
 }
 
+// fp64-entry evaluation: exponents below this (relative to the entry's
+// anchor 2^(rho_i + sig_j) ~ sqrt(r_i c_j)) contribute < 1e-26 of that scale;
+// n <= 792 of them change a marginal by < 1e-23 relative -- far below the
+// eps >= 1e-12 the fp64 mode serves
+#ifndef MDOT_F64_SKIP_Z
+#define MDOT_F64_SKIP_Z -60.0
+#endif
+constexpr double kF64SkipZ = MDOT_F64_SKIP_Z;
+
 // Cluster split (CL CTAs per instance, q = this CTA's rank): the CTA takes
 // the row groups ib = 4 (q W + w) + 4 W CL m; row totals are complete for
 // its rows, column totals are partial over them (combined by the caller).
 template <bool F64, bool PACKED, typename CT>
 __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
                            double gbar, double* rowtot, double* coltot, double (*sred)[kTileN], int q_rank,
-                           int CL) {
+                           int CL, double skip_z = -INFINITY) {
   static_assert(kBatchWarps == 2 * kSredRows, "two-round column reduction");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4* rowp = prm;
@@ -322,9 +331,14 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
           for (int q = 0; q < 8; ++q) {
             if (rowok && jj[q] < n) {
               const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (double)(rp.w + Wd[q]) * LN2_D;
-              const double e = exp(z);
-              rsum += e * (double)T[q];
-              c64[q] += e * (double)rp.z;
+              // entries below e^kF64SkipZ of their anchor scale (P_ij < 1e-26
+              // sqrt(r_i c_j)) are dropped without calling exp: at gbar ~ 4096
+              // that is most of the matrix, and whole warps skip the exp
+              if (z > skip_z) {
+                const double e = exp(z);
+                rsum += e * (double)T[q];
+                c64[q] += e * (double)rp.z;
+              }
             }
           }
           rs[u] = rsum;
@@ -524,7 +538,8 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
       for (int k = tid; k < n2; k += blockDim.x) prep_item(pa, k, &S.st);
       __syncthreads();
       bool use64 = a.f64 != 0;
-      for (int attempt = 0; attempt < 2; ++attempt) {
+      double skip_z = kF64SkipZ;   // fp64 entries: tiny entries skipped, exact retry if that leaves a zero total
+      for (int attempt = 0; attempt < 3; ++attempt) {
         if (use64) {
           // fp64-entry parameters for this evaluation: redo the exponent split
           if (attempt > 0 || !a.f64) {
@@ -538,7 +553,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
             }
             __syncthreads();
           }
-          batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL);
+          batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, skip_z);
         } else {
           batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL);
         }
@@ -550,8 +565,10 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
         fa.f64_entries = use64 ? 1 : 0;
         for (int k = tid; k < n2; k += blockDim.x) finalize_item(fa, k, tot[k], v);
         block_sum<kNumScalars>(v, &S.sred[0][0], S.out);
-        if (S.out[SC_BAD] == 0.0 || use64) break;
-        use64 = true;   // range guard fired: redo this evaluation with fp64 entries
+        if (S.out[SC_BAD] == 0.0) break;
+        if (!use64) { use64 = true; continue; }     // range guard fired: redo with fp64 entries
+        if (skip_z > -INFINITY) { skip_z = -INFINITY; continue; }   // a total lost to the skip: redo exactly
+        break;
       }
       if (tid < kNumScalars) S.st.sc[tid] = S.out[tid];
       __syncthreads();

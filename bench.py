@@ -404,6 +404,38 @@ def run_ours(a, rank, world, local_rank):
                        "d2h_bytes_per_step": 16 * n, "ms_per_step": 1000.0 * dt / a.steps,
                        "timing": "host wall clock around the synchronous C-ABI call"}
         del Ch
+    elif world > 1 and not a.no_e2e:
+        # every rank: its row slab of C from pinned host memory through
+        # mdot_solve_sharded (MDOT_MEM_HOST), U_local / V back to the host;
+        # whole-job evaluations over the max of the ranks' wall clocks
+        import synthetic as S
+        inst2 = S.config4(a.instance, n=n)
+        Ch = torch.from_numpy(np.ascontiguousarray(inst2.C[row0:row0 + nloc])).pin_memory()
+        del inst2.C
+        rh = torch.from_numpy(inst2.r)
+        ch = torch.from_numpy(inst2.c)
+        Uh = torch.empty(nloc, dtype=torch.float64).pin_memory()
+        Vh = torch.empty(n, dtype=torch.float64).pin_memory()
+        o2 = M.options(eps=a.eps, projector=proj, eps_md=a.eps_md)
+
+        def solve_host():
+            return M.mdot_solve_sharded(comm, row0, nloc, C_local=Ch, r=rh, c=ch, n=n, schedule=sched, options=o2,
+                                        u_local_out=Uh, v_out=Vh)
+        solve_host()   # warm
+        barrier()
+        t0 = time.perf_counter()
+        ev = 0
+        for _ in range(a.steps):
+            ev += solve_host()["evaluations"]
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        line["e2e"] = {"value": ev / dt, "unit": "evals/s", "h2d_bytes_per_step": 4 * nloc * n + 16 * n,
+                       "d2h_bytes_per_step": 8 * (nloc + n), "ms_per_step": 1000.0 * dt / a.steps,
+                       "timing": "host wall clock around the synchronous C-ABI call, max over ranks; bytes per rank"}
+        del Ch
     if rank == 0 and not a.no_cpu_baseline:
         import synthetic as S
         inst3 = S.config4(a.instance, n=n)

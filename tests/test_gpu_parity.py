@@ -894,3 +894,31 @@ def test_gpu_gamma_4096_single_step_is_stable():
     r16 = M.mdot_solve(C, r, c, schedule=M.schedule(M.MDOT_SCHED_FIXED, 4096.0), options=M.options(eps=1e-6))
     assert r1["status"] == 0 and r16["status"] == 0 and r1["md_steps"] == 1 and r16["md_steps"] == 16
     assert abs(r1["cost_unrounded"] - r16["cost_unrounded"]) <= COST_GATE * r16["cost_unrounded"]
+
+
+def test_sharded_host_memory_inputs(monkeypatch):
+    """mdot_solve_sharded with host arrays (MDOT_MEM_HOST: the slab of C, r, c
+    copied in, U_local / V copied out inside the call) -- the call bench.py's
+    multi-GPU e2e leg makes -- on a 1-rank NCCL communicator with the fused
+    peer exchange; same result as the device-resident call."""
+    monkeypatch.setenv("MDOT_SHARDED_SELFTEST", "1")
+    n, gb, eps = 1024, 512.0, 1e-6
+    inst = S.uniform_points_instance(3, n, 2, 23, marg="dirichlet")
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=2)
+    comm = M.mdot_comm_create(M.mdot_get_unique_id(), 1, 0, 0)
+    try:
+        M.mdot_comm_enable_peer(comm, n)
+        Uh = np.empty(n)
+        Vh = np.empty(n)
+        rh = M.mdot_solve_sharded(comm, 0, n, C_local=np.ascontiguousarray(inst.C), r=inst.r, c=inst.c, n=n,
+                                  schedule=sched, options=M.options(eps=eps), u_local_out=Uh, v_out=Vh)
+        Ud = torch.empty(n, dtype=torch.float64, device=DEV)
+        Vd = torch.empty_like(Ud)
+        rd = M.mdot_solve_sharded(comm, 0, n, C_local=_t(inst.C), r=_t(inst.r), c=_t(inst.c), n=n,
+                                  schedule=sched, options=M.options(eps=eps), u_local_out=Ud, v_out=Vd)
+    finally:
+        M.mdot_comm_destroy(comm)
+    assert rh["status"] == 0 and rd["status"] == 0 and rh["control_path"] == 2
+    assert rh["cost_unrounded"] == rd["cost_unrounded"]
+    np.testing.assert_array_equal(Uh, Ud.cpu().numpy())
+    np.testing.assert_array_equal(Vh, Vd.cpu().numpy())

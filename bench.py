@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--instance", type=int, default=0)
     ap.add_argument("--eps-md", type=float, default=0.0,
                     help="tolerance of the intermediate MD steps (0 = eps at every step, the paper's protocol)")
+    ap.add_argument("--sharded-selftest", action="store_true",
+                    help="run the multi-GPU code path on one rank (1-rank NCCL communicator; tests only)")
     ap.add_argument("--adaptive-leg", type=float, default=1e-3,
                     help="also time the solve with this eps_md (SURVEY 8(f) rank 1), reported under "
                          "'adaptive_eps'; 0 disables")
@@ -205,6 +207,16 @@ def run_reference(a, rank, world):
 
 
 def run_ours(a, rank, world, local_rank):
+    # --sharded-selftest: the multi-GPU code path (process group, NCCL
+    # communicator, fused peer exchange, sharded solve, e2e leg) on ONE rank,
+    # with a 1-rank NCCL communicator forced onto the sharded path
+    sharded = world > 1 or a.sharded_selftest
+    if a.sharded_selftest:
+        os.environ["MDOT_SHARDED_SELFTEST"] = "1"
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
     import numpy as np
     import torch
 
@@ -213,7 +225,7 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     inst = instance(a)
@@ -225,7 +237,7 @@ def run_ours(a, rank, world, local_rank):
     c = torch.from_numpy(inst.c).to(dev)
     comm = None
     exchange = None
-    if world > 1:
+    if sharded:
         rows = np.array_split(np.arange(n), world)[rank]
         row0, nloc = int(rows[0]), len(rows)
         C = torch.from_numpy(np.ascontiguousarray(inst.C[row0:row0 + nloc])).to(dev)
@@ -237,7 +249,7 @@ def run_ours(a, rank, world, local_rank):
         # persistent kernel); every rank gets the same status, NCCL otherwise
         exchange = "nccl allreduce in CUDA-graph slots"
         if not os.environ.get("MDOT_NO_PEER") and M.mdot_comm_enable_peer(comm, n, check=False) == 0:
-            exchange = "fused peer stores + flags in the persistent kernel (NVLink)"
+            exchange = "fused peer exchange in the persistent kernel (self-validating records over NVLink)"
         U = torch.empty(nloc, dtype=torch.float64, device=dev)
     else:
         C = torch.from_numpy(inst.C).to(dev)
@@ -325,7 +337,7 @@ def run_ours(a, rank, world, local_rank):
         "data": "synthetic (seeded config 4 instance, no dataset)",
         "config": {"workload": workload_name(a), "n": n, "gamma_bar": a.gamma_bar,
                    "T": int(results[-1]["md_steps"]), "eps": a.eps, "stop": "marginal L1",
-                   "projector": a.projector, "parallelism": f"rows sharded x{world}" if world > 1 else "1 GPU",
+                   "projector": a.projector, "parallelism": f"rows sharded x{world}" if sharded else "1 GPU",
                    "exchange": exchange,
                    "l2": "C (4 n^2 B) is larger than L2 (126 MB): no flush needed",
                    "instance_seed": 4000 + a.instance},
@@ -381,7 +393,7 @@ def run_ours(a, rank, world, local_rank):
             "note": "intermediate MD steps stop at eps_md, the last at eps; Lemma 2 (PAPER.md:152-155) makes "
                     "the final plan independent of the intermediate accuracy"}
     # end-to-end through the C ABI with host buffers (rank 0, 1 GPU)
-    if world == 1 and not a.no_e2e:
+    if not sharded and not a.no_e2e:
         import synthetic as S
         inst2 = S.config4(a.instance, n=n)
         Ch = torch.from_numpy(inst2.C).pin_memory()
@@ -404,7 +416,7 @@ def run_ours(a, rank, world, local_rank):
                        "d2h_bytes_per_step": 16 * n, "ms_per_step": 1000.0 * dt / a.steps,
                        "timing": "host wall clock around the synchronous C-ABI call"}
         del Ch
-    elif world > 1 and not a.no_e2e:
+    elif sharded and not a.no_e2e:
         # every rank: its row slab of C from pinned host memory through
         # mdot_solve_sharded (MDOT_MEM_HOST), U_local / V back to the host;
         # whole-job evaluations over the max of the ranks' wall clocks

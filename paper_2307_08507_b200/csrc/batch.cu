@@ -230,17 +230,42 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
     double Bd[F64 ? 8 : 1];
     float Wd[F64 ? 8 : 1];
     int jj[8];
+    if (!F64) {
+      // column parameters from shared memory: lane l's quad starts 64 B after
+      // lane l-1's, so lanes l and l+2 hit the same banks (4-way conflict, 9 %
+      // of the warp samples); each lane visits its quad rotated by (l/2) mod 4
+      // and the values are put back in column order with static selects
+      const int rot = (lane >> 1) & 3;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
-      jj[q] = j;
-      if (j < n) {
-        const float4 cp = colp[j];
-        bh[q] = cp.x; T[q] = cp.z;
-        if (F64) { Bd[q & (F64 ? 7 : 0)] = *reinterpret_cast<const double*>(&cp.x); Wd[q & (F64 ? 7 : 0)] = cp.w; }
-      } else {
-        bh[q] = -1.0e30f; T[q] = 0.f;
-        if (F64) { Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.f; }
+      for (int h = 0; h < 2; ++h) {
+        float4 t4[4];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+          const int j = j0 + 4 * lane + ((s4 + rot) & 3) + 128 * h;
+          t4[s4] = (j < n) ? colp[j] : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int src = (q - rot) & 3;
+          const float4 v = src == 0 ? t4[0] : (src == 1 ? t4[1] : (src == 2 ? t4[2] : t4[3]));
+          bh[4 * h + q] = v.x;
+          T[4 * h + q] = v.z;
+          jj[4 * h + q] = j0 + 4 * lane + q + 128 * h;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+        jj[q] = j;
+        if (j < n) {
+          const float4 cp = colp[j];
+          bh[q] = cp.x; T[q] = cp.z;
+          Bd[q & (F64 ? 7 : 0)] = *reinterpret_cast<const double*>(&cp.x); Wd[q & (F64 ? 7 : 0)] = cp.w;
+        } else {
+          bh[q] = -1.0e30f; T[q] = 0.f;
+          Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.f;
+        }
       }
     }
     float c32[8];

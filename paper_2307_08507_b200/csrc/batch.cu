@@ -313,7 +313,8 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
     for (int ib = 4 * (warp + q_rank * kBatchWarps); ib < n; ib += 4 * kBatchWarps * CL, ++step) {
       CT cvc[4][8];
       load_group(ib, cvc);
-      double rs[4];
+      double rs[4];    // fp64 entries
+      float rsf[4];    // fp32 entries (no fp64 round trip before the fp32 row butterfly)
       float mrow[4] = {1.f, 1.f, 1.f, 1.f};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -331,7 +332,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
             rsum = fmaf(e, T[q], rsum);
             c32[q] = fmaf(e, rp.z, c32[q]);
           }
-          rs[u] = rsum;
+          rsf[u] = rsum;
           mrow[u] = rp.y;
         } else if (!F64) {
           // fp32 entries, parameter slots {ah, M, S'} / {bh, M, T'} (ops.cuh
@@ -341,7 +342,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
 #pragma unroll
           for (int p = 0; p < 4; ++p) c2[p] = pk2(cv[2 * p], cv[2 * p + 1]);
 #if MDOT_K1_ROWRED_F32
-          rs[u] = (double)entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);   // exact: an fp32 value
+          rsf[u] = entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);
 #else
           rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
 #endif
@@ -371,9 +372,16 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
       }
       // fp32 entries: rs are fp32 values, reduced across the warp in fp32
       // (MDOT_K1_ROWRED_F32); fp64 entries keep the fp64 butterfly
-      double tot = (!F64 && MDOT_K1_ROWRED_F32)
-                       ? (double)warp_reduce4_f((float)rs[0], (float)rs[1], (float)rs[2], (float)rs[3], lane)
-                       : bred4(rs[0], rs[1], rs[2], rs[3], lane);
+      double tot;
+      if (F64) {
+        tot = bred4(rs[0], rs[1], rs[2], rs[3], lane);
+      } else if (MDOT_K1_ROWRED_F32) {
+        tot = (double)warp_reduce4_f(rsf[0], rsf[1], rsf[2], rsf[3], lane);
+      } else if (PACKED) {
+        tot = bred4(rs[0], rs[1], rs[2], rs[3], lane);
+      } else {
+        tot = bred4((double)rsf[0], (double)rsf[1], (double)rsf[2], (double)rsf[3], lane);
+      }
       const int i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
       if (!F64) tot *= (double)((lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]));
       if ((lane & 7) == 0 && i < n) rowtot[i] = (j0 == 0) ? tot : rowtot[i] + tot;
@@ -549,9 +557,22 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     __syncthreads();
     bool first = true;
     for (;;) {
+#ifdef MDOT_DIAG_K8
+      const bool dg = a.dbg && b == 0 && q_rank == 0 && tid == 0;
+      unsigned long long d0 = dg ? clock64() : 0ull;
+#define K8_MARK(slot)                                     \
+  if (dg) {                                               \
+    const unsigned long long d1 = clock64();              \
+    a.dbg[slot] += d1 - d0;                               \
+    d0 = d1;                                              \
+  }
+#else
+#define K8_MARK(slot)
+#endif
       if (!first) {
         if (tid == 0) ctrl_body(&S.st, 0, nullptr, nullptr);
         __syncthreads();
+        K8_MARK(0)
         if (S.st.done) {
           if (S.st.accept_marg || S.st.accept_pot)
             for (int k = tid; k < n2; k += blockDim.x) prep_item(pa, k, &S.st);
@@ -562,6 +583,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
       first = false;
       for (int k = tid; k < n2; k += blockDim.x) prep_item(pa, k, &S.st);
       __syncthreads();
+      K8_MARK(1)
       bool use64 = a.f64 != 0;
       double skip_z = kF64SkipZ;   // fp64 entries: tiny entries skipped, exact retry if that leaves a zero total
       for (int attempt = 0; attempt < 3; ++attempt) {
@@ -583,13 +605,19 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
           batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL);
         }
         __syncthreads();
+        K8_MARK(2)
         if (CL > 1) cluster_combine(cluster, tot, n, q_rank, CL);
+        K8_MARK(3)
         double v[kNumScalars];
 #pragma unroll
         for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
         fa.f64_entries = use64 ? 1 : 0;
         for (int k = tid; k < n2; k += blockDim.x) finalize_item(fa, k, tot[k], v);
         block_sum<kNumScalars>(v, &S.sred[0][0], S.out);
+        K8_MARK(4)
+#ifdef MDOT_DIAG_K8
+        if (dg) a.dbg[7] += 1;
+#endif
         if (S.out[SC_BAD] == 0.0) break;
         if (!use64) { use64 = true; continue; }     // range guard fired: redo with fp64 entries
         if (skip_z > -INFINITY) { skip_z = -INFINITY; continue; }   // a total lost to the skip: redo exactly

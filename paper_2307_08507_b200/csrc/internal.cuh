@@ -365,6 +365,7 @@ struct BatchArgs {
   double* U_out;           // [B][n] nullable
   double* V_out;
   BatchResult* res;        // [B] (device)
+  unsigned long long* dbg; // MDOT_DIAG_K8 builds: [8] phase clock sums of instance 0 (null otherwise)
 };
 size_t batch_smem_bytes(int n);
 cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st);

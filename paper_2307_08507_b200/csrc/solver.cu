@@ -1521,6 +1521,11 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   a.f64 = c64 || (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && o.eps < 5e-8);
   a.max_evals = o.max_evals;
   a.U_out = dU; a.V_out = dV; a.res = dres;
+  unsigned long long* kdbg = nullptr;   // MDOT_DEBUG_K8 (MDOT_DIAG_K8 builds): per-phase clocks of instance 0
+  if (getenv("MDOT_DEBUG_K8") && cudaMalloc((void**)&kdbg, 8 * sizeof(unsigned long long)) == cudaSuccess) {
+    cudaMemsetAsync(kdbg, 0, 8 * sizeof(unsigned long long), stream);
+    a.dbg = kdbg;
+  }
   cudaError_t e = launch_batch(a, Bn, stream);
   if (e != cudaSuccess) {
     cudaFreeAsync(base, stream);
@@ -1538,6 +1543,15 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   if (u_out) CK(cudaMemcpyAsync(u_out, dU, vb, k, stream));
   if (v_out) CK(cudaMemcpyAsync(v_out, dV, vb, k, stream));
   CK(cudaStreamSynchronize(stream));
+  if (kdbg) {
+    unsigned long long h[8];
+    cudaMemcpy(h, kdbg, sizeof(h), cudaMemcpyDeviceToHost);
+    const double k = h[7] ? (double)h[7] : 1.0;
+    fprintf(stderr, "[mdot] K8 cycles per evaluation (instance 0, CTA 0): ctrl %.0f prep %.0f eval %.0f "
+            "cluster-combine %.0f finalize %.0f (%llu evaluations)\n", h[0] / k, h[1] / k, h[2] / k, h[3] / k,
+            h[4] / k, h[7]);
+    cudaFree(kdbg);
+  }
   cudaFreeAsync(base, stream);
   const double secs = now_s() - t0;
   mdot_status first = MDOT_OK;

@@ -73,6 +73,7 @@ struct EvalArgs {
   const float* gpair;      // device-resident {gh, gl} (device control), overrides gh/gl
   const int* done;         // device control: kernel returns at once when *done != 0
   int keep_l2;             // TMA path: C fits in L2 -> evict_last (stays resident), else evict_first
+  int64_t l2_res_tiles;    // persistent TMA pass: tiles [0, l2_res_tiles) read with evict_last (MDOT_K1_L2RES_MB)
   // outputs
   double* rowpart;         // [n_col_tiles][nrows]  sum_j 2^w T_j
   double* colpart;         // [n_row_tiles][n]      sum_i 2^w S_i

@@ -148,7 +148,9 @@ struct TmaCursor {
 };
 __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
                                               TmaCursor& cur, uint32_t& it, int count, int cta, int ncta) {
-  const uint64_t pol = l2_policy(a.keep_l2 != 0);
+  // L2 residency: the first l2_res_tiles tiles are read with evict_last, so
+  // they stay in L2 across evaluations when C is larger than L2
+  const uint64_t pol_stream = l2_policy(a.keep_l2 != 0), pol_keep = l2_policy(true);
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
   const int spt = a.tile_m / kTmaRows;
@@ -160,7 +162,8 @@ __device__ __forceinline__ void tma_produce_n(TmaSmem& sm, const CUtensorMap* tm
     const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
     mbar_wait(&sm.empty[s], ph ^ 1u);
     mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
-    tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + cur.k * kTmaRows), &sm.full[s], pol);
+    tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + cur.k * kTmaRows), &sm.full[s],
+                     cur.tile < a.l2_res_tiles ? pol_keep : pol_stream);
     if (++cur.k == nst) {
       cur.k = 0;
       cur.tile += ncta;

@@ -1000,6 +1000,13 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
       eval.keep_l2 = (4.0 * (double)nrows * (double)n <= 0.6 * (double)l2) ? 1 : 0;
+      // C larger than L2: a quarter of L2 keeps the first tiles resident
+      // across evaluations (evict_last), the rest streams (evict_first);
+      // config 4: K1 171.8 -> 168.5 us, time-to-eps -1.5 %; 64 / 96 MB
+      // crowd out the partials and parameters (profiles/README.md)
+      double res_bytes = eval.keep_l2 ? 0.0 : 0.25 * (double)l2;
+      if (const char* mb = getenv("MDOT_K1_L2RES_MB")) res_bytes = atof(mb) * 1048576.0;   // A/B
+      eval.l2_res_tiles = (int64_t)(res_bytes / (4.0 * eval.tile_m * kTileN));
       // sharded: the persistent path needs the fused peer exchange
       // (mdot_comm_enable_peer); CTAs per rank from the transport
       if (getenv("MDOT_NO_PERSIST") || persist_ncta < 0) pers_grid = 0;

@@ -103,7 +103,7 @@ __device__ __forceinline__ double warp_reduce4_t(double v0, double v1, double v2
 // `it` is the running stage counter (kept across passes by the caller).
 __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
                                                  uint32_t& it) {
-  const uint64_t pol = l2_policy(a.keep_l2 != 0);
+  const uint64_t pol_stream = l2_policy(a.keep_l2 != 0), pol_keep = l2_policy(true);   // L2 residency as tma_produce_n
   const int64_t nrows = a.nrows;
   const int nct = a.n_col_tiles;
   const int64_t total = (int64_t)a.n_row_tiles * nct;
@@ -117,7 +117,8 @@ __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap*
       const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
       mbar_wait(&sm.empty[s], ph ^ 1u);
       mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
-      tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + k * kTmaRows), &sm.full[s], pol);
+      tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + k * kTmaRows), &sm.full[s],
+                       tile < a.l2_res_tiles ? pol_keep : pol_stream);
     }
   }
 }

@@ -128,10 +128,20 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   eval.n = n;
   eval.nrows = nrows;
   eval.n_col_tiles = (int)((n + kTileN - 1) / kTileN);
-  // 512-row tiles (fewer partials) while there are >= 2 tiles per CTA slot
-  // of the persistent kernel; smaller tiles for small n
+  // Row tile height: minimise the busiest CTA's work over the 2 x 148
+  // persistent CTAs, (tiles per CTA) x (rows per tile + ~128 rows of per-tile
+  // cost: parameter loads, column write-out, two CTA barriers; fitted).  n = 16384:
+  // 512; config 3 (n = 4096): 256, one tile per CTA (K1 17.7 -> 14.4 us vs
+  // two 128-row tiles; profiles/r01_cfg3_tile_grid.txt).
   int tile_m = 512;
-  while (tile_m > 32 && (int64_t)eval.n_col_tiles * ((nrows + tile_m - 1) / tile_m) < 2 * 148) tile_m /= 2;
+  {
+    int64_t best = INT64_MAX;
+    for (int tm = 512; tm >= 32; tm /= 2) {
+      const int64_t tiles = (int64_t)eval.n_col_tiles * ((nrows + tm - 1) / tm);
+      const int64_t cost = ((tiles + 2 * 148 - 1) / (2 * 148)) * (std::min<int64_t>(tm, nrows) + 128);
+      if (cost < best) { best = cost; tile_m = tm; }
+    }
+  }
   if (const char* tm_env = getenv("MDOT_TILE_M")) {   // A/B experiments only
     const int v = atoi(tm_env);
     if (v >= 32 && v <= 512 && (v & (v - 1)) == 0) tile_m = v;

@@ -51,7 +51,10 @@ def _sinkhorn_potentials(prob, inst, gbar, iters=6, seed=0, noise=0.0):
     return A, B
 
 
-@pytest.mark.parametrize("n,gbar", [(64, 64.0), (300, 512.0), (784, 4096.0), (1031, 256.0), (2048, 4096.0)])
+# row-tile heights of the K1 cost model: 32 (300, 1031), 64 (2048), 128 with a
+# ragged tail (3000), 256 with one tile per CTA (4096)
+@pytest.mark.parametrize("n,gbar", [(64, 64.0), (300, 512.0), (784, 4096.0), (1031, 256.0), (2048, 4096.0),
+                                    (3000, 4096.0), (4096, 1024.0)])
 def test_marginals_fp32_path_matches_oracle(n, gbar):
     inst = S.uniform_points_instance(3, n, 2, 1, marg="dirichlet")
     prob = O.OracleProblem(inst)

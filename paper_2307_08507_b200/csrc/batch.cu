@@ -209,6 +209,93 @@ __device__ void batch_eval_tail_packed(const float* __restrict__ C, int n, int j
 #endif
 constexpr double kF64SkipZ = MDOT_F64_SKIP_Z;
 
+// Narrow last tile (<= 64 columns), fp64 entries: the lane layout of
+// batch_eval_tail_packed (Lp lanes per row, 8 columns each, 32 / Lp rows per
+// warp step, the same 64-row cluster blocks) with the exact fp64 entry of
+// batch_eval.  Config 1 (n = 64) is one such tile: the regular layout kept
+// 16 of 32 lanes busy on 4 columns each.  Column sums fp64 per lane, then the
+// lanes of one column group and the warps in a fixed order.
+template <typename CT>
+__device__ void batch_eval_tail_f64(const CT* __restrict__ C, int n, int j0, const float4* prm, double gbar,
+                                    double* rowtot, double* coltot, double (*sred)[kTileN], int q_rank, int CL,
+                                    double skip_z) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float4* rowp = prm;
+  const float4* colp = prm + n;
+  const int w = n - j0;
+  int Lp = 1;
+  while (8 * Lp < w) Lp *= 2;                 // lanes per row (<= 8)
+  const int R = 32 / Lp;                      // rows per warp step
+  const int rr = lane / Lp, cl = lane % Lp;
+  const int jc = j0 + 8 * cl;
+  double Bd[8], Td[8];
+  float Wd[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int j = jc + q;
+    if (j < n) {
+      const float4 cp = colp[j];
+      Bd[q] = *reinterpret_cast<const double*>(&cp.x); Td[q] = (double)cp.z; Wd[q] = cp.w;
+    } else {
+      Bd[q] = 0.0; Td[q] = 0.0; Wd[q] = 0.f;
+    }
+  }
+  double c64[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c64[k] = 0.0;
+  const int nblk = (n + 63) / 64;
+  const int own_blocks = (nblk - q_rank + CL - 1) / CL;
+  const int own_rows = own_blocks * 64;
+  for (int base = warp * R; base < own_rows; base += R * kBatchWarps) {
+    const int slot = base + rr;
+    const int i = 64 * (q_rank + CL * (slot / 64)) + (slot % 64);
+    const bool ok = slot < own_rows && i < n;
+    double rsum = 0.0;
+    if (ok) {
+      const float4 rp = rowp[i];
+      const double Ai = *reinterpret_cast<const double*>(&rp.x);
+      const CT* crow = C + (int64_t)i * n;
+      CT cv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cv[q] = (jc + q < n) ? __ldg(crow + jc + q) : (CT)0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (jc + q < n) {
+          const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (double)(rp.w + Wd[q]) * LN2_D;
+          if (z > skip_z) {
+            const double e = exp(z);
+            rsum += e * Td[q];
+            c64[q] += e * (double)rp.z;
+          }
+        }
+      }
+    }
+    for (int off = 1; off < Lp; off <<= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, off);
+    if (ok && cl == 0) rowtot[i] = (j0 == 0) ? rsum : rowtot[i] + rsum;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    for (int off = Lp; off < 32; off <<= 1) c64[k] += __shfl_xor_sync(0xffffffffu, c64[k], off);
+  if (rr == 0 && warp >= kSredRows) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sred[warp - kSredRows][8 * cl + k] = c64[k];
+  }
+  __syncthreads();
+  if (rr == 0 && warp < kSredRows) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sred[warp][8 * cl + k] = c64[k] + sred[warp][8 * cl + k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 * Lp) {
+    const int t = threadIdx.x;
+    double acc = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kSredRows; ++ww) acc += sred[ww][t];
+    if (j0 + t < n) coltot[j0 + t] = acc;
+  }
+  __syncthreads();
+}
+
 // Cluster split (CL CTAs per instance, q = this CTA's rank): the CTA takes
 // the row groups ib = 4 (q W + w) + 4 W CL m; row totals are complete for
 // its rows, column totals are partial over them (combined by the caller).
@@ -224,6 +311,10 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
   for (int j0 = 0; j0 < n; j0 += kTileN) {
     if (!F64 && PACKED && sizeof(CT) == 4 && n - j0 <= 64 && !batch_tail_regular()) {
       batch_eval_tail_packed(reinterpret_cast<const float*>(C), n, j0, prm, gh, gl, rowtot, coltot, sred, q_rank, CL);
+      continue;
+    }
+    if (F64 && n - j0 <= 64 && !batch_tail_regular()) {
+      batch_eval_tail_f64<CT>(C, n, j0, prm, gbar, rowtot, coltot, sred, q_rank, CL, skip_z);
       continue;
     }
     float bh[8], T[8];

@@ -228,16 +228,17 @@ __device__ void batch_eval_tail_f64(const CT* __restrict__ C, int n, int j0, con
   const int R = 32 / Lp;                      // rows per warp step
   const int rr = lane / Lp, cl = lane % Lp;
   const int jc = j0 + 8 * cl;
-  double Bd[8], Td[8];
-  float Wd[8];
+  // anchors are small integers: (double)rho_i + (double)sig_j is exact and
+  // equals batch_eval's (double)(rho_i + sig_j), without a conversion per entry
+  double Bd[8], Td[8], Wd[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int j = jc + q;
     if (j < n) {
       const float4 cp = colp[j];
-      Bd[q] = *reinterpret_cast<const double*>(&cp.x); Td[q] = (double)cp.z; Wd[q] = cp.w;
+      Bd[q] = *reinterpret_cast<const double*>(&cp.x); Td[q] = (double)cp.z; Wd[q] = (double)cp.w;
     } else {
-      Bd[q] = 0.0; Td[q] = 0.0; Wd[q] = 0.f;
+      Bd[q] = 0.0; Td[q] = 0.0; Wd[q] = 0.0;
     }
   }
   double c64[8];
@@ -254,6 +255,7 @@ __device__ void batch_eval_tail_f64(const CT* __restrict__ C, int n, int j0, con
     if (ok) {
       const float4 rp = rowp[i];
       const double Ai = *reinterpret_cast<const double*>(&rp.x);
+      const double rw = (double)rp.w, rz = (double)rp.z;
       const CT* crow = C + (int64_t)i * n;
       CT cv[8];
 #pragma unroll
@@ -261,11 +263,11 @@ __device__ void batch_eval_tail_f64(const CT* __restrict__ C, int n, int j0, con
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (jc + q < n) {
-          const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (double)(rp.w + Wd[q]) * LN2_D;
+          const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (rw + Wd[q]) * LN2_D;
           if (z > skip_z) {
             const double e = exp(z);
             rsum += e * Td[q];
-            c64[q] += e * (double)rp.z;
+            c64[q] += e * rz;
           }
         }
       }

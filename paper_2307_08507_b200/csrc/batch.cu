@@ -321,7 +321,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
     }
     float bh[8], T[8];
     double Bd[F64 ? 8 : 1];
-    float Wd[F64 ? 8 : 1];
+    double Wd[F64 ? 8 : 1];   // integer anchors sig_j (exact in fp64; see batch_eval_tail_f64)
     int jj[8];
     if (!F64) {
       // column parameters from shared memory: lane l's quad starts 64 B after
@@ -354,10 +354,10 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
         if (j < n) {
           const float4 cp = colp[j];
           bh[q] = cp.x; T[q] = cp.z;
-          Bd[q & (F64 ? 7 : 0)] = *reinterpret_cast<const double*>(&cp.x); Wd[q & (F64 ? 7 : 0)] = cp.w;
+          Bd[q & (F64 ? 7 : 0)] = *reinterpret_cast<const double*>(&cp.x); Wd[q & (F64 ? 7 : 0)] = (double)cp.w;
         } else {
           bh[q] = -1.0e30f; T[q] = 0.f;
-          Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.f;
+          Bd[q & (F64 ? 7 : 0)] = 0.0; Wd[q & (F64 ? 7 : 0)] = 0.0;
         }
       }
     }
@@ -445,11 +445,12 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
           // integer (rho_i + sig_j) ln 2, fp64 exp
           double rsum = 0.0;
           const double Ai = *reinterpret_cast<const double*>(&rp.x);
+          const double rw = (double)rp.w;
           const bool rowok = i < n;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             if (rowok && jj[q] < n) {
-              const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (double)(rp.w + Wd[q]) * LN2_D;
+              const double z = (Ai + Bd[q]) - gbar * (double)cv[q] - (rw + Wd[q]) * LN2_D;
               // entries below e^kF64SkipZ of their anchor scale (P_ij < 1e-26
               // sqrt(r_i c_j)) are dropped without calling exp: at gbar ~ 4096
               // that is most of the matrix, and whole warps skip the exp

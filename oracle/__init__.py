@@ -21,7 +21,7 @@ _SRC = os.path.join(_HERE, "mdot_oracle.c")
 
 DENSE_F32, SQEUCLID_F32, DENSE_F64 = 0, 1, 2
 PNCG, SINKHORN, NCG, PNCG_JACOBI = 0, 1, 2, 3
-BETA_PPR, BETA_PPR_AF, BETA_PFR, BETA_PPR_PRINTED = 0, 1, 2, 3
+BETA_PPR, BETA_PPR_AF, BETA_PFR, BETA_PPR_PRINTED, BETA_PPR_PLUS = 0, 1, 2, 3, 4
 WARM_SCALED, WARM_CARRY, WARM_ZERO = 0, 1, 2
 STATUS = {0: "OK", 1: "EINVAL", 3: "EINSTABLE", 4: "ENOCONV", 5: "ELINESEARCH"}
 
@@ -51,7 +51,7 @@ class TraceRec(ct.Structure):
     _fields_ = [("t", ct.c_int32), ("k", ct.c_int32), ("l1", ct.c_double), ("rho", ct.c_double),
                 ("alpha", ct.c_double), ("dphi0", ct.c_double), ("dphi_alpha", ct.c_double),
                 ("dphi_value", ct.c_double), ("trials", ct.c_int32), ("reset", ct.c_int32),
-                ("beta", ct.c_double)]
+                ("beta", ct.c_double), ("gs", ct.c_double)]
 
 
 class Result(ct.Structure):
@@ -75,6 +75,7 @@ class Result(ct.Structure):
 
 
 _lib = None
+PHI_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_double, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double))
 
 
 def lib():
@@ -98,6 +99,12 @@ def lib():
         L.orc_schedule_doubling.argtypes = [D, D, P, ct.c_int32]
         L.orc_default_eps.argtypes = [D, D]
         L.orc_default_eps.restype = D
+        L.orc_line_search.argtypes = [PHI_FN, P, D, D, D, D, D, ct.c_int, ct.POINTER(D), ct.POINTER(D),
+                                      ct.POINTER(D), ct.POINTER(ct.c_int), ct.POINTER(ct.c_int)]
+        L.orc_plan_cost.argtypes = [ct.POINTER(Problem), P, P, D]
+        L.orc_plan_cost.restype = D
+        L.orc_mdot_adaptive.argtypes = [ct.POINTER(Problem), D, D, ct.POINTER(Options), P, P,
+                                        ct.POINTER(Result), P, P, ct.c_int64, ct.POINTER(ct.c_int64)]
         _lib = L
     return _lib
 
@@ -256,3 +263,50 @@ def plan(prob: OracleProblem, U, V, gbar):
     C = np.array([[prob.cost(i, j) for j in range(n)] for i in range(n)]) if prob.C is None \
         else prob.C.astype(np.float64)
     return np.exp(U[:, None] + V[None, :] - gbar * C)
+
+
+def line_search(phi, dphi0, alpha0=1.0, c1=0.1, c2=0.4, dec_tol=1e-14, max_trials=100):
+    """Run the oracle's Appx. C line search on a Python phi: alpha -> (phi'(alpha),
+    phi(alpha) - phi(0)).  Returns (alpha, phi'(alpha), dval, trials, accepted,
+    [every trial alpha in order])."""
+    seen = []
+
+    def cb(_ctx, alpha, dphi, dval):
+        seen.append(alpha)
+        a, b = phi(alpha)
+        dphi[0] = a
+        dval[0] = b
+        return 0
+
+    f = PHI_FN(cb)
+    al, dp, dv = ct.c_double(0), ct.c_double(0), ct.c_double(0)
+    tr, acc = ct.c_int(0), ct.c_int(0)
+    st = lib().orc_line_search(f, None, float(dphi0), float(alpha0), float(c1), float(c2), float(dec_tol),
+                               int(max_trials), ct.byref(al), ct.byref(dp), ct.byref(dv), ct.byref(tr),
+                               ct.byref(acc))
+    assert st == 0
+    return al.value, dp.value, dv.value, tr.value, bool(acc.value), seen
+
+
+def plan_cost(prob: OracleProblem, A, B, gbar):
+    """<C, P(A,B)> = sum_ij C_ij exp(A_i + B_j - gbar C_ij) (one pass)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    return lib().orc_plan_cost(ct.byref(prob.s), _ptr(A), _ptr(B), float(gbar))
+
+
+def mdot_adaptive(prob: OracleProblem, gamma_bar, gamma1=256.0, opts=None, trace_cap=0):
+    """MDOT with the ADAPTIVE step rule (Z29); returns (U, V, result, trace, gammas)."""
+    n = prob.n
+    U = np.empty(n)
+    V = np.empty(n)
+    g = np.zeros(64)
+    opts = opts or make_options()
+    res = Result()
+    tb = _trace_buf(trace_cap)
+    tl = ct.c_int64(0)
+    lib().orc_mdot_adaptive(ct.byref(prob.s), float(gamma_bar), float(gamma1), ct.byref(opts), _ptr(U), _ptr(V),
+                            ct.byref(res), _ptr(g), ct.cast(tb, ct.c_void_p) if tb is not None else None,
+                            trace_cap, ct.byref(tl))
+    T = int(res.md_steps)
+    return U, V, res.as_dict(), _trace_list(tb, tl.value) if tb is not None else [], g[:T].copy()

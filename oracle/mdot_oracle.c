@@ -239,6 +239,81 @@ static int sinkhorn_project(const orc_problem* pb, const double* U, const double
 }
 
 /* ------------------------------------------------------------------ */
+/* Line search, Appx. C: approximate Wolfe
+ *   (2 c1 - 1) phi'(0) >= phi'(alpha) >= c2 phi'(0)
+ * plus the decrease safeguard phi(alpha) - phi(0) <= dec_tol (Z9).  Bracket
+ * [lo, hi] with phi'(lo) < 0 < phi'(hi): while there is no hi, alpha doubles
+ * (Z8, at most 60 times); then alpha_sec = (lo phi'(hi) - hi phi'(lo)) /
+ * (phi'(hi) - phi'(lo)) and alpha = alpha_sec / 2 + (lo + hi) / 4
+ * ("alpha_hybrid"); bisection if phi'(hi) <= phi'(lo).          */
+int orc_line_search(orc_phi_fn fn, void* ctx, double dphi0, double alpha0, double c1, double c2, double dec_tol,
+                    int max_trials, double* alpha_out, double* dphi_out, double* dval_out, int* trials_out,
+                    int* accepted_out) {
+  double alpha = alpha0;
+  double lo = 0.0, dlo = dphi0, hi = 0.0, dhi = 0.0;
+  int have_hi = 0, doublings = 0, trials = 0, accepted = 0, st = ORC_OK;
+  double dphi_a = 0.0, dval = 0.0;
+  for (int tr_i = 0; tr_i < max_trials; ++tr_i) {
+    st = fn(ctx, alpha, &dphi_a, &dval);
+    trials++;
+    if (st != ORC_OK) break;
+    const int wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
+    const int decrease = dval <= dec_tol;
+    if (wolfe && decrease) { accepted = 1; break; }
+    if (dphi_a < 0.0 && decrease) {
+      lo = alpha; dlo = dphi_a;
+    } else {
+      hi = alpha; dhi = dphi_a; have_hi = 1;
+    }
+    if (!have_hi) {
+      if (++doublings > 60) break;
+      alpha = 2.0 * alpha;
+    } else if (dhi > dlo) {
+      double a_sec = (lo * dhi - hi * dlo) / (dhi - dlo);
+      alpha = 0.5 * a_sec + 0.5 * (hi + lo) / 2.0;
+    } else {
+      alpha = 0.5 * (lo + hi);
+    }
+  }
+  *alpha_out = alpha;
+  *dphi_out = dphi_a;
+  *dval_out = dval;
+  *trials_out = trials;
+  *accepted_out = accepted;
+  return st;
+}
+
+/* One trial of the PNCG line search: P(alpha) at (u + alpha p_u, v + alpha p_v). */
+typedef struct {
+  const orc_problem* pb;
+  const double *U, *V, *u, *v, *p;
+  double gbar, mass0, pr;
+  double *A, *B, *trial_u, *trial_v;
+  marg_t* T;
+  orc_result* res;
+} trial_ctx;
+
+static int pncg_trial(void* vctx, double alpha, double* dphi, double* dval) {
+  trial_ctx* c = (trial_ctx*)vctx;
+  const int64_t n = c->pb->n;
+  const double *r = c->pb->r, *cc = c->pb->c, *p = c->p;
+  for (int64_t i = 0; i < n; ++i) c->trial_u[i] = c->u[i] + alpha * p[i];
+  for (int64_t j = 0; j < n; ++j) c->trial_v[j] = c->v[j] + alpha * p[n + j];
+  int st = evaluate(c->pb, c->U, c->V, c->trial_u, c->trial_v, c->gbar, c->A, c->B, c->T);
+  c->res->evaluations++;
+  c->res->ls_evaluations++;
+  if (st != ORC_OK) return st;
+  /* phi'(alpha) = <p_u, r(P(alpha)) - r> + <p_v, c(P(alpha)) - c> */
+  double d = 0.0;
+  for (int64_t i = 0; i < n; ++i) d += p[i] * (c->T->rP[i] - r[i]);
+  for (int64_t j = 0; j < n; ++j) d += p[n + j] * (c->T->cP[j] - cc[j]);
+  *dphi = d;
+  /* phi(alpha) - phi(0) = sum P(alpha) - sum P(0) - alpha(<p_u,r> + <p_v,c>) */
+  *dval = (c->T->mass - c->mass0) - alpha * c->pr;
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
 /* PNCG projection, Alg. 2, with
  *   s   = (log r(P) - log r, log c(P) - log c)
  *   grad= (r(P) - r, c(P) - c)
@@ -317,11 +392,14 @@ static int pncg_project(const orc_problem* pb, const double* U, const double* V,
         den = dot(gprev, pprev, n2);
       } else if (opt->beta == ORC_BETA_PPR_AF) {
         den = rc_dot_prev;            /* <grad_{k-1}, s_{k-1}> */
-      } else { /* ORC_BETA_PFR: <grad_k, s_k> / <grad_{k-1}, s_{k-1}> */
+      } else if (opt->beta == ORC_BETA_PPR_PLUS) {
+        den = -dot(gprev, pprev, n2);
+      } else { /* ORC_BETA_PFR: <grad_k, s_k> / <grad_{k-1}, s_{k-1}> (PAPER.md:497 preconditioned) */
         num = dot(g, s, n2);
         den = rc_dot_prev;
       }
       beta = (fabs(den) > 1e-300) ? num / den : 0.0;
+      if (!ncg && opt->beta == ORC_BETA_PPR_PLUS && beta < 0.0) beta = 0.0;   /* PR+ */
     }
     /* direction and reset (Alg. 2 lines 6-9; Z5) */
     for (int64_t q = 0; q < n2; ++q) p[q] = -dir[q] + beta * pprev[q];
@@ -336,47 +414,18 @@ static int pncg_project(const orc_problem* pb, const double* U, const double* V,
     rc_dot_prev = dot(g, s, n2);
 
     /* line search (Alg. 2 line 10; Appx. C) */
-    const double pr = dot(p, r, n) + dot(p + n, c, n);   /* <p_u,r> + <p_v,c> */
     const double phi0 = M.mass - dot(u, r, n) - dot(v, c, n) - 1.0;  /* g(u,v) */
     const double dec_tol = 1e-14 * (fabs(phi0) > 1.0 ? fabs(phi0) : 1.0);
     double alpha = (k == 1) ? 1.0 : fmin(4.0, fmax(0.25, alpha_prev));   /* Z8 */
     int accepted = 0, trials = 0, attempt = 0;
     double dphi_a = 0.0, dval = 0.0;
+    trial_ctx tc = {pb, U, V, u, v, p, gbar, M.mass, 0.0, A, B, trial_u, trial_v, &T, res};
     while (!accepted && attempt < 2) {
-      double lo = 0.0, dlo = dphi0, hi = 0.0, dhi = 0.0;
-      int have_hi = 0, doublings = 0;
-      for (int tr_i = 0; tr_i < max_trials; ++tr_i) {
-        for (int64_t i = 0; i < n; ++i) trial_u[i] = u[i] + alpha * p[i];
-        for (int64_t j = 0; j < n; ++j) trial_v[j] = v[j] + alpha * p[n + j];
-        st = evaluate(pb, U, V, trial_u, trial_v, gbar, A, B, &T);
-        res->evaluations++;
-        res->ls_evaluations++;
-        trials++;
-        if (st != ORC_OK) break;
-        /* phi'(alpha) = <p_u, r(P(alpha)) - r> + <p_v, c(P(alpha)) - c> */
-        dphi_a = 0.0;
-        for (int64_t i = 0; i < n; ++i) dphi_a += p[i] * (T.rP[i] - r[i]);
-        for (int64_t j = 0; j < n; ++j) dphi_a += p[n + j] * (T.cP[j] - c[j]);
-        /* phi(alpha) - phi(0) = sum P(alpha) - sum P(0) - alpha(<p_u,r> + <p_v,c>) */
-        dval = (T.mass - M.mass) - alpha * pr;
-        const int wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
-        const int decrease = dval <= dec_tol;
-        if (wolfe && decrease) { accepted = 1; break; }
-        if (dphi_a < 0.0 && decrease) {
-          lo = alpha; dlo = dphi_a;
-        } else {
-          hi = alpha; dhi = dphi_a; have_hi = 1;
-        }
-        if (!have_hi) {
-          if (++doublings > 60) break;
-          alpha = 2.0 * alpha;
-        } else if (dhi > dlo) {
-          double a_sec = (lo * dhi - hi * dlo) / (dhi - dlo);
-          alpha = 0.5 * a_sec + 0.5 * (hi + lo) / 2.0;
-        } else {
-          alpha = 0.5 * (lo + hi);
-        }
-      }
+      tc.pr = dot(p, r, n) + dot(p + n, c, n);   /* <p_u,r> + <p_v,c> */
+      int tr_n = 0;
+      st = orc_line_search(pncg_trial, &tc, dphi0, alpha, c1, c2, dec_tol, max_trials, &alpha, &dphi_a, &dval,
+                           &tr_n, &accepted);
+      trials += tr_n;
       if (accepted || st != ORC_OK) break;
       /* Z10: restart along -s with a fresh bracket */
       attempt++;
@@ -392,7 +441,8 @@ static int pncg_project(const orc_problem* pb, const double* U, const double* V,
       orc_trace_rec* q = &tr[(*tlen)++];
       q->t = t; q->k = (int32_t)k; q->l1 = l1; q->rho = rho; q->alpha = alpha;
       q->dphi0 = dphi0; q->dphi_alpha = dphi_a; q->dphi_value = dval;
-      q->trials = trials; q->reset = reset; q->beta = beta;
+      q->trials = trials; q->reset = reset; q->beta = reset ? 0.0 : beta;
+      q->gs = rc_dot_prev;
     }
     /* accept: u += alpha p_u, v += alpha p_v (Alg. 2 line 11); the accepted
      * trial's marginals are those of the new iterate (lines 12-13). */
@@ -554,20 +604,44 @@ double orc_default_eps(double hmin, double gamma_bar) {
 }
 
 /* ------------------------------------------------------------------ */
+/* sum_ij C_ij exp(A_i + B_j - gbar C_ij) in index order per row. */
+double orc_plan_cost(const orc_problem* pb, const double* A, const double* B, double gbar) {
+  const int64_t n = pb->n;
+  double* rowc = (double*)malloc(sizeof(double) * n);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double cs = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      const double cij = orc_cost(pb, i, j);
+      cs += cij * exp((A[i] + B[j]) - gbar * cij);
+    }
+    rowc[i] = cs;
+  }
+  const double tot = sum(rowc, n);
+  free(rowc);
+  return tot;
+}
+
+/* ------------------------------------------------------------------ */
 /* MDOT, Alg. 1.
  *   P^0 = r c^T (PAPER.md:203 (i)) -> U = log r, V = log c;  u = v = 0.
  *   step t: gbar += gamma_t; P_hat^t = P^{t-1} exp(-gamma_t C), i.e. the plan
  *   exp(U + V - gbar C); warm start: the previous step's potentials are
  *   carried over (Z4), scaled by gamma_t/gamma_{t-1};
  *   project; U += u, V += v.  Gauge (u+d, v-d) is free: after
- *   each step U, V and u, v are re-centred so that <r,.> = <c,.> (Z19).      */
-int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_options* opt,
-             double* U, double* V, orc_result* res,
-             orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len) {
+ *   each step U, V and u, v are re-centred so that <r,.> = <c,.> (Z19).
+ * `adaptive` selects the step rule of orc_mdot_adaptive (Z29) instead of the
+ * given schedule.                                                            */
+static int mdot_run(const orc_problem* pb, const double* gammas, int32_t T, int adaptive, double gamma_bar,
+                    double gamma1, const orc_options* opt, double* U, double* V, orc_result* res,
+                    double* gammas_out, orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len) {
   const int64_t n = pb->n;
   const double *r = pb->r, *c = pb->c;
   memset(res, 0, sizeof(*res));
-  if (n < 1 || T < 1 || !(opt->eps > 0)) { res->status = ORC_EINVAL; return ORC_EINVAL; }
+  if (n < 1 || (!adaptive && T < 1) || (adaptive && !(gamma_bar > 0 && gamma1 > 0)) || !(opt->eps > 0)) {
+    res->status = ORC_EINVAL;
+    return ORC_EINVAL;
+  }
   double t0 = now_s();
   double* u = (double*)calloc(n, sizeof(double));
   double* v = (double*)calloc(n, sizeof(double));
@@ -577,10 +651,14 @@ int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_o
   if (!trace_len) trace_len = &dummy;
   *trace_len = 0;
   double gbar = 0.0, gprev = 0.0;
+  double next = adaptive ? fmin(gamma1, gamma_bar) : 0.0, eta_prev = 0.0;
+  int final_next = adaptive && gamma1 >= gamma_bar;
   int st = ORC_OK;
-  for (int32_t t = 1; t <= T; ++t) {
-    double gt = gammas[t - 1];
-    gbar += gt;
+  for (int32_t t = 1; adaptive || t <= T; ++t) {
+    double gt = adaptive ? next : gammas[t - 1];
+    const int last = adaptive ? final_next : (t == T);
+    gbar = (adaptive && last) ? gamma_bar : gbar + gt;   /* the last adaptive step lands on gamma_bar exactly */
+    if (gammas_out && t <= 64) gammas_out[t - 1] = gt;
     if (opt->warm == ORC_WARM_ZERO) {
       memset(u, 0, sizeof(double) * n);
       memset(v, 0, sizeof(double) * n);
@@ -590,7 +668,8 @@ int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_o
       for (int64_t j = 0; j < n; ++j) v[j] *= w;
     }
     orc_options ot = *opt;
-    if (t < T && opt->eps_md > opt->eps) ot.eps = opt->eps_md;
+    if (!last && opt->eps_md > opt->eps) ot.eps = opt->eps_md;
+    const int64_t evals_before = res->evaluations;
     st = orc_project(pb, U, V, gbar, u, v, &ot, t, res, trace, trace_cap, trace_len);
     res->md_steps = t;
     for (int64_t i = 0; i < n; ++i) U[i] += u[i];
@@ -602,7 +681,17 @@ int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_o
     for (int64_t i = 0; i < n; ++i) u[i] -= d2;
     for (int64_t j = 0; j < n; ++j) v[j] += d2;
     gprev = gt;
-    if (st != ORC_OK) break;
+    if (st != ORC_OK || (adaptive && last)) break;
+    if (adaptive) {
+      /* Z29: eta_t = gamma_t / E_t; double while eta does not fall, else halve */
+      const double E = (double)(res->evaluations - evals_before);
+      const double eta = gt / (E > 1.0 ? E : 1.0);
+      double g = (t == 1 || eta >= eta_prev) ? 2.0 * gt : fmax(0.5 * gt, gamma_bar / 1024.0);
+      eta_prev = eta;
+      const double rem = gamma_bar - gbar;
+      if (g >= rem || rem - g < 0.25 * g || t + 1 >= 64) { g = rem; final_next = 1; }
+      next = g;
+    }
   }
   res->gamma_bar = gbar;
   if (st == ORC_OK || st == ORC_ENOCONV)
@@ -612,4 +701,16 @@ int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_o
   free(u);
   free(v);
   return st;
+}
+
+int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_options* opt,
+             double* U, double* V, orc_result* res,
+             orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len) {
+  return mdot_run(pb, gammas, T, 0, 0.0, 0.0, opt, U, V, res, NULL, trace, trace_cap, trace_len);
+}
+
+int orc_mdot_adaptive(const orc_problem* pb, double gamma_bar, double gamma1, const orc_options* opt,
+                      double* U, double* V, orc_result* res, double* gammas_out,
+                      orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len) {
+  return mdot_run(pb, NULL, 0, 1, gamma_bar, gamma1, opt, U, V, res, gammas_out, trace, trace_cap, trace_len);
 }

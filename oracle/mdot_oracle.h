@@ -21,7 +21,9 @@ enum { ORC_DENSE_F32 = 0, ORC_SQEUCLID_F32 = 1, ORC_DENSE_F64 = 2 };
 /* ORC_PNCG_JACOBI: Alg. 2 with the Jacobi preconditioner diag(Hessian)^-1 in place
  * of the Sinkhorn direction (SURVEY 8(f) rank 2 ablation; Hessian PAPER.md:225). */
 enum { ORC_PNCG = 0, ORC_SINKHORN = 1, ORC_NCG = 2, ORC_PNCG_JACOBI = 3 };
-enum { ORC_BETA_PPR = 0, ORC_BETA_PPR_AF = 1, ORC_BETA_PFR = 2, ORC_BETA_PPR_PRINTED = 3 };
+/* ORC_BETA_PPR_PLUS: max(0, beta^PPR), the PR+ safeguard of Gilbert & Nocedal
+ * (cited at PAPER.md:499 for FR's unproductive directions). */
+enum { ORC_BETA_PPR = 0, ORC_BETA_PPR_AF = 1, ORC_BETA_PFR = 2, ORC_BETA_PPR_PRINTED = 3, ORC_BETA_PPR_PLUS = 4 };
 enum { ORC_WARM_SCALED = 0, ORC_WARM_CARRY = 1, ORC_WARM_ZERO = 2 };
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EINSTABLE = 3, ORC_ENOCONV = 4, ORC_ELINESEARCH = 5 };
 
@@ -61,6 +63,7 @@ typedef struct {         /* one PNCG / Sinkhorn iteration */
   double alpha, dphi0, dphi_alpha, dphi_value; /* line search: phi'(0), phi'(alpha), phi(alpha)-phi(0) */
   int32_t trials, reset;
   double beta;
+  double gs;             /* <grad g, s> at the iterate (the PPR_AF / PFR denominator of the next iteration) */
 } orc_trace_rec;
 
 typedef struct {
@@ -93,6 +96,37 @@ int orc_project(const orc_problem* pb, const double* U, const double* V, double 
 int orc_mdot(const orc_problem* pb, const double* gammas, int32_t T, const orc_options* opt,
              double* U_out, double* V_out, orc_result* res,
              orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len);
+
+/* phi'(alpha) and phi(alpha) - phi(0) of one line-search trial (PAPER.md:
+ * 694-696); returns ORC_OK or an error status that aborts the search. */
+typedef int (*orc_phi_fn)(void* ctx, double alpha, double* dphi, double* dval);
+/* The hybrid secant / bisection line search of Appx. C
+ * for the approximate Wolfe conditions with the decrease
+ * safeguard phi(alpha) - phi(0) <= dec_tol (Z9) and bracket expansion by
+ * doubling from alpha0 (Z8, cap 60).  Writes the accepted alpha, phi'(alpha),
+ * phi(alpha) - phi(0), the trial count and *accepted (0: no alpha within
+ * max_trials / 60 doublings).  Returns the callback's error status or ORC_OK. */
+int orc_line_search(orc_phi_fn fn, void* ctx, double dphi0, double alpha0, double c1, double c2, double dec_tol,
+                    int max_trials, double* alpha_out, double* dphi_out, double* dval_out, int* trials_out,
+                    int* accepted_out);
+
+/* sum_ij C_ij exp(A_i + B_j - gbar C_ij): <C, P(A,B)> in one pass (the
+ * unrounded cost of north_star's parity gate, Z20). */
+double orc_plan_cost(const orc_problem* pb, const double* A, const double* B, double gbar);
+
+/* MDOT with the ADAPTIVE step rule (PAPER.md:371 future work, "variable
+ * learning rate MD procedures that exploit the warm-starting of the dual
+ * variables"; reading Z29): gamma_1 = min(gamma1, gamma_bar); after
+ * step t with E_t evaluations, eta_t = gamma_t / E_t (progress in gbar per
+ * O(n^2) pass); gamma_2 = 2 gamma_1; for t >= 2 gamma_{t+1} = 2 gamma_t if
+ * eta_t >= eta_{t-1} else max(gamma_t / 2, gamma_bar / 1024); every step is
+ * clipped to the remaining budget, a remainder below a quarter of the next
+ * step is merged into it, and step 64 takes the whole remainder.  By Lemma 2
+ * the final plan is the entropic plan at gamma_bar for
+ * ANY such schedule.  gammas_out[0..md_steps-1] receives the schedule. */
+int orc_mdot_adaptive(const orc_problem* pb, double gamma_bar, double gamma1, const orc_options* opt,
+                      double* U_out, double* V_out, orc_result* res, double* gammas_out,
+                      orc_trace_rec* trace, int64_t trace_cap, int64_t* trace_len);
 
 /* Rounding onto U(r,c) (Altschuler et al. Alg. 2, as restated in SPEC.md:331)
  * of F = exp(U + V - gbar*C).  Writes cost <C,F>, cost <C,G>, and optionally

@@ -127,10 +127,35 @@ def _is_cuda(x):
     return hasattr(x, "is_cuda") and x.is_cuda
 
 
-def _ptr(x, dtype=None):
-    """Raw pointer of a contiguous torch tensor / numpy array (None -> NULL)."""
+F64, F32 = ("float64",), ("float32",)
+F32_OR_F64 = ("float32", "float64")
+
+
+def _dtname(x):
+    return str(x.dtype).replace("torch.", "") if hasattr(x, "data_ptr") else np.dtype(x.dtype).name
+
+
+def _check_arr(name, x, dtypes, cuda=None):
+    """The C side reads / writes these buffers with a fixed element type
+    (include/mdot.h): a float32 buffer passed where fp64 is expected would be
+    over-read or overwritten by 2x its size.  Also every buffer of one call
+    must live where the problem's `mem` kind says."""
+    if x is None:
+        return
+    dt = _dtname(x)
+    if dt not in dtypes:
+        raise TypeError(f"{name}: dtype {dt}, expected {' or '.join(dtypes)}")
+    if cuda is not None and _is_cuda(x) != cuda:
+        raise TypeError(f"{name}: {'host' if cuda else 'device'} buffer expected (same memory kind as the problem)")
+
+
+def _ptr(x, dtypes=None, name="array", cuda=None):
+    """Raw pointer of a contiguous torch tensor / numpy array (None -> NULL);
+    with `dtypes`, the element type (and memory kind) is checked first."""
     if x is None:
         return None
+    if dtypes is not None:
+        _check_arr(name, x, dtypes, cuda)
     if hasattr(x, "data_ptr"):
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
@@ -159,8 +184,9 @@ def problem(C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, n=None):
         kind = MDOT_COST_SQEUCLID_F32
         nn = Y.shape[0] if n is None else n
         d = X.shape[1]
-    pb = Problem(nn, kind, MDOT_MEM_DEVICE if dev else MDOT_MEM_HOST, _ptr(C), d, float(scale),
-                 _ptr(X), _ptr(Y), _ptr(r), _ptr(c))
+    pb = Problem(nn, kind, MDOT_MEM_DEVICE if dev else MDOT_MEM_HOST, _ptr(C, F32_OR_F64, "C", dev), d,
+                 float(scale), _ptr(X, F32, "X", dev), _ptr(Y, F32, "Y", dev), _ptr(r, F64, "r", dev),
+                 _ptr(c, F64, "c", dev))
     pb._keep = (C, r, c, X, Y)
     return pb
 
@@ -200,8 +226,9 @@ def _solve(fn, C, r, c, X, Y, scale, sched, opts, u_out, v_out, P_out, check):
     if pb.mem == MDOT_MEM_DEVICE:
         opts.stream = _current_stream()
     res = Result()
-    st = fn(ct.byref(pb), ct.byref(sched), ct.byref(opts), _ptr(u_out), _ptr(v_out), _ptr(P_out),
-            ct.byref(res))
+    dev = pb.mem == MDOT_MEM_DEVICE
+    st = fn(ct.byref(pb), ct.byref(sched), ct.byref(opts), _ptr(u_out, F64, "u_out", dev),
+            _ptr(v_out, F64, "v_out", dev), _ptr(P_out, F32, "P_out", dev), ct.byref(res))
     d = res.as_dict()
     d["status"] = st
     if check and st not in (0,):
@@ -229,8 +256,9 @@ def mdot_solve_batch(C, R, Cm, *, schedule=None, options=None, u_out=None, v_out
     if pb.mem == MDOT_MEM_DEVICE:
         opts.stream = _current_stream()
     res = (Result * B)()
-    st = lib().mdot_solve_batch(ct.byref(pb), B, _ptr(R), _ptr(Cm), ct.byref(sched), ct.byref(opts),
-                                _ptr(u_out), _ptr(v_out), res)
+    dev = pb.mem == MDOT_MEM_DEVICE
+    st = lib().mdot_solve_batch(ct.byref(pb), B, _ptr(R, F64, "R", dev), _ptr(Cm, F64, "Cm", dev), ct.byref(sched),
+                                ct.byref(opts), _ptr(u_out, F64, "u_out", dev), _ptr(v_out, F64, "v_out", dev), res)
     if check:
         _check(st, "mdot_solve_batch")
     return [res[b].as_dict() for b in range(B)]
@@ -250,8 +278,9 @@ def mdot_marginals(A, B, gbar, C=None, r=None, c=None, *, X=None, Y=None, scale=
         lr = np.empty(pb.n) if lr is None else lr
         lc = np.empty(pb.n) if lc is None else lc
     fb = ct.c_int32(0)
-    st = lib().mdot_marginals(ct.byref(pb), _ptr(A), _ptr(B), float(gbar), _ptr(lr), _ptr(lc),
-                              ct.byref(opts), ct.byref(fb))
+    dev = pb.mem == MDOT_MEM_DEVICE
+    st = lib().mdot_marginals(ct.byref(pb), _ptr(A, F64, "A", dev), _ptr(B, F64, "B", dev), float(gbar),
+                              _ptr(lr, F64, "lr", dev), _ptr(lc, F64, "lc", dev), ct.byref(opts), ct.byref(fb))
     if check:
         _check(st, "mdot_marginals")
     return lr, lc, int(fb.value)
@@ -265,8 +294,9 @@ def mdot_round(U, V, gbar, C=None, r=None, c=None, *, X=None, Y=None, scale=0.0,
         opts.stream = _current_stream()
     cF = ct.c_double(0)
     cG = ct.c_double(0)
-    st = lib().mdot_round(ct.byref(pb), _ptr(U), _ptr(V), float(gbar), _ptr(P_out), ct.byref(cF),
-                          ct.byref(cG), ct.byref(opts))
+    dev = pb.mem == MDOT_MEM_DEVICE
+    st = lib().mdot_round(ct.byref(pb), _ptr(U, F64, "U", dev), _ptr(V, F64, "V", dev), float(gbar),
+                          _ptr(P_out, F32, "P_out", dev), ct.byref(cF), ct.byref(cG), ct.byref(opts))
     if check:
         _check(st, "mdot_round")
     return cF.value, cG.value
@@ -314,8 +344,10 @@ def mdot_solve_sharded(comm, row0, n_local, C_local=None, r=None, c=None, *, X_l
     if pb.mem == MDOT_MEM_DEVICE:
         opts.stream = _current_stream()
     res = Result()
+    dev = pb.mem == MDOT_MEM_DEVICE
     st = lib().mdot_solve_sharded(comm, ct.byref(pb), int(row0), int(n_local), ct.byref(sched),
-                                  ct.byref(opts), _ptr(u_local_out), _ptr(v_out), ct.byref(res))
+                                  ct.byref(opts), _ptr(u_local_out, F64, "u_local_out", dev),
+                                  _ptr(v_out, F64, "v_out", dev), ct.byref(res))
     d = res.as_dict()
     d["status"] = st
     if check:

@@ -201,9 +201,10 @@ __device__ void batch_eval_tail_packed(const float* __restrict__ C, int n, int j
 }
 
 // fp64-entry evaluation: exponents below this (relative to the entry's
-// anchor 2^(rho_i + sig_j) ~ sqrt(r_i c_j)) contribute < 1e-26 of that scale;
-// n <= 792 of them change a marginal by < 1e-23 relative -- far below the
-// eps >= 1e-12 the fp64 mode serves
+// anchor 2^(rho_i + sig_j) ~ sqrt(r_i c_j)) contribute < 1e-26 of that scale
+// and are not exponentiated.  The finalize range guard (f64_tot_min) redoes
+// an evaluation exactly whenever a total is small enough that the skipped
+// entries could exceed 1e-16 of it
 #ifndef MDOT_F64_SKIP_Z
 #define MDOT_F64_SKIP_Z -60.0
 #endif
@@ -706,6 +707,12 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
 #pragma unroll
         for (int q = 0; q < kNumScalars; ++q) v[q] = 0.0;
         fa.f64_entries = use64 ? 1 : 0;
+        // skipped entries (z <= skip_z) each carry < e^skip_z T_j (row) or
+        // e^skip_z S_i (column) in anchored units, with T, S <= 1 (anchors
+        // <= 0): a total below n e^skip_z / 1e-16 may have lost more than
+        // 1e-16 of itself to the skip -- redo that evaluation exactly (far-off
+        // trial points, or targets below the anchor clamp 2^-120)
+        fa.f64_tot_min = (use64 && skip_z > -INFINITY) ? (double)n * exp(skip_z) * 1e16 : 0.0;
         for (int k = tid; k < n2; k += blockDim.x) finalize_item(fa, k, tot[k], v);
         block_sum<kNumScalars>(v, &S.sred[0][0], S.out);
         K8_MARK(4)
@@ -775,10 +782,20 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     double* ec = pprev;        // [n] err_c
     double* er = pprev + n;    // [n] err_r (first holds 1/x)
     double* invx = er;
+    const int lane = tid & 31, warp = tid >> 5;
+    // x = min(r / r(F), 1) from an exact fp64 row pass over F: the last
+    // evaluation's fp32-entry marginals resolve r(F) only to ~1e-7 relative,
+    // and x_i r_i(F) <= r_i is what keeps err_r >= 0 and G in U(r,c)
+    // (solver.cu round_and_cost)
+    for (int i = warp; i < n; i += kBatchWarps) {
+      double s = 0.0;
+      for (int j = lane; j < n; j += 32) s += exp((UV[i] + UV[n + j]) - gbar * batch_cost(a, (int64_t)i * n + j));
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) logx[i] = fmin(logt[i] - log(s), 0.0);
+    }
+    __syncthreads();
     for (int i = tid; i < n; i += blockDim.x) {
-      double lx = logt[i] - cl[i];
-      if (lx > 0.0) lx = 0.0;
-      logx[i] = lx;
+      const double lx = logx[i];
       Ap[i] = UV[i] + lx;
       invx[i] = exp(-lx);
     }
@@ -802,11 +819,10 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     for (int j = tid; j < n; j += blockDim.x) {
       const double y = fmin(tgt[n + j] / cF1[j], 1.0);
       Bpp[j] = UV[n + j] + log(y);
-      ec[j] = tgt[n + j] - y * cF1[j];
+      ec[j] = fmax(tgt[n + j] - y * cF1[j], 0.0);   // >= 0 in exact arithmetic (kernels.cu)
     }
     __syncthreads();
     // rows: r(F''), <C, F''>, (C err_c)_i ; warp per row
-    const int lane = tid & 31, warp = tid >> 5;
     double v3[3] = {0.0, 0.0, 0.0};   // |err_r|_1, <C,F''>, err_r . C err_c (lane 0 of each warp)
     for (int i = warp; i < n; i += kBatchWarps) {
       double s = 0.0, cs2 = 0.0, cr = 0.0;
@@ -823,7 +839,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
         cr += __shfl_xor_sync(0xffffffffu, cr, off);
       }
       if (lane == 0) {
-        const double e = tgt[i] - s;
+        const double e = fmax(tgt[i] - s, 0.0);
         er[i] = e;
         v3[0] += fabs(e);
         v3[1] += cs2;

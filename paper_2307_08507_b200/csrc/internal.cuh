@@ -105,6 +105,8 @@ struct ExactArgs {
   const int* done;   // device control early exit
 };
 cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st);
+// rows only: lr = exact fp64 log row marginals (rounding)
+cudaError_t launch_exact_rows(const ExactArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // O(n) kernels
@@ -160,6 +162,8 @@ struct FinalizeArgs {
   int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
   int jacobi;            // 1: s = grad / diag(Hessian) (MDOT_PROJ_PNCG_JACOBI) instead of the Sinkhorn direction
   int f64_entries;       // partials from fp64 entries (K8): range guard at the fp64 limits, not fp32's
+  double f64_tot_min;    // fp64 entries: totals below this (anchored units) are redone exactly -- the
+                         // bound on the mass K8's entry skip may have dropped (batch.cu); 0 = 1e-300
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 
@@ -324,6 +328,9 @@ struct RoundArgs {
 cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
                               double* logx, double* Aout, cudaStream_t st);
 cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t st);
+// L2 lines of [p, p + bytes) back to evict_normal priority (K1 reads part or
+// all of C with evict_last; the caller's later kernels must not inherit it)
+cudaError_t launch_l2_normal(const void* p, size_t bytes, cudaStream_t st);
 cudaError_t launch_round_cols(const RoundArgs& a, cudaStream_t st);
 cudaError_t launch_round_rows3(const RoundArgs& a, cudaStream_t st);
 cudaError_t launch_round_plan(const RoundArgs& a, cudaStream_t st);

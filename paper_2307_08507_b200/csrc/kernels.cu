@@ -594,10 +594,14 @@ __global__ void k_exact_cols(ExactArgs a) {
   a.cols[(int64_t)chunk * a.n + j] = s;
 }
 
-cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st) {
+cudaError_t launch_exact_rows(const ExactArgs& a, cudaStream_t st) {
   const int wpb = 8;
   k_exact_rows<<<(unsigned)((a.nrows + wpb - 1) / wpb), wpb * 32, 0, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval_exact(const ExactArgs& a, cudaStream_t st) {
+  cudaError_t e = launch_exact_rows(a, st);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + 255) / 256), a.chunks);
   k_exact_cols<<<grid, 256, 0, st>>>(a);
@@ -1063,7 +1067,9 @@ __global__ void k_round_combine_cols(RoundArgs a, const double* c, const double*
     }
     const double y = fmin(c[j] / cf, 1.0);
     Bout[j] = V[j] + log(y);
-    ec[j] = c[j] - y * cf;
+    // c(F'') = y c(F') <= c in exact arithmetic; the clamp removes the
+    // last-bit sign flips of the fp64 product
+    ec[j] = fmax(c[j] - y * cf, 0.0);
     v[0] = cc;
     v[1] = cf;
   }
@@ -1076,7 +1082,9 @@ __global__ void k_round_combine_rows(RoundArgs a, const double* r, double* block
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   if (i < a.nrows) {
-    const double er = r[i] - a.rowF2[i];
+    // r(F'') <= x r(F) <= r in exact arithmetic (x from the fp64 r(F)); the
+    // clamp keeps G >= 0 against fp64 rounding of the row sums
+    const double er = fmax(r[i] - a.rowF2[i], 0.0);
     a.er[i] = er;
     v[0] = fabs(er);
     v[1] = a.rowcost2[i];
@@ -1119,6 +1127,18 @@ __global__ void k_exp_neg(int64_t n, const double* x, double* y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = exp(-x[i]);
 }
+__global__ void k_l2_normal(const char* p, size_t lines) {
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < lines; q += (size_t)gridDim.x * blockDim.x)
+    asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p + 128 * q) : "memory");
+}
+cudaError_t launch_l2_normal(const void* p, size_t bytes, cudaStream_t st) {
+  const uintptr_t b = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127);
+  const size_t lines = (reinterpret_cast<uintptr_t>(p) + bytes - b + 127) / 128;
+  if (lines == 0) return cudaSuccess;
+  k_l2_normal<<<296, 256, 0, st>>>(reinterpret_cast<const char*>(b), lines);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t st) {
   k_exp_neg<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, x, y);
   return cudaGetLastError();

@@ -165,7 +165,7 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
       lm = log(tot) + anchor * LN2_D;
       // fp32 entry range guard (K1 numerics): totals far from 1 in
       // anchored units mean under/overflowed entries -> exact re-evaluation
-      if (a.f64_entries ? !(tot > 1e-300 && tot < 1e300)
+      if (a.f64_entries ? !(tot > fmax(a.f64_tot_min, 1e-300) && tot < 1e300)
                         : !(tot > 7.888609052210118e-31 && tot < 1.2676506002282294e30)) bad = 1.0;
     } else {
       if (is_row) {

@@ -135,10 +135,18 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   // two 128-row tiles; profiles/r01_cfg3_tile_grid.txt).
   int tile_m = 512;
   {
+    // CTAs that will share the pass: 2 per SM (K1 and the persistent kernel),
+    // divided among the ranks when one GPU emulates several (in-process
+    // transport with the fused peer exchange)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t ctas = 2 * (int64_t)sms;
+    if (comm && comm->local && comm->peer && comm->nranks > 1) ctas = std::max<int64_t>(1, ctas / comm->nranks);
     int64_t best = INT64_MAX;
     for (int tm = 512; tm >= 32; tm /= 2) {
       const int64_t tiles = (int64_t)eval.n_col_tiles * ((nrows + tm - 1) / tm);
-      const int64_t cost = ((tiles + 2 * 148 - 1) / (2 * 148)) * (std::min<int64_t>(tm, nrows) + 128);
+      const int64_t cost = ((tiles + ctas - 1) / ctas) * (std::min<int64_t>(tm, nrows) + 128);
       if (cost < best) { best = cost; tile_m = tm; }
     }
   }
@@ -906,15 +914,20 @@ mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g) {
 // Input handling
 // ---------------------------------------------------------------------------
 mdot_status validate_marginal(const double* h, int64_t n, const char* name) {
-  double s = 0.0;
+  // Neumaier-compensated sum: the test sees the exact sum of the given fp64
+  // values to ~1 ulp at any n, so the documented 1e-12 bound holds as stated
+  double s = 0.0, comp = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     if (!(h[i] > 0.0) || !isfinite(h[i])) {
       set_error("%s[%lld] = %g is not strictly positive (PAPER.md:38)", name, (long long)i, h[i]);
       return MDOT_EINVAL;
     }
-    s += h[i];
+    const double t = s + h[i];
+    comp += (fabs(s) >= fabs(h[i])) ? (s - t) + h[i] : (h[i] - t) + s;
+    s = t;
   }
-  if (fabs(s - 1.0) > 1e-12 * std::max<double>(1.0, (double)n / 1e4)) {
+  s += comp;
+  if (fabs(s - 1.0) > 1e-12) {
     set_error("%s sums to %.17g, not 1 within 1e-12", name, s);
     return MDOT_EINVAL;
   }
@@ -1034,6 +1047,21 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   return MDOT_OK;
 }
 
+// K1 fetched the first tiles of C (all of C when it fits in L2) with an
+// evict_last policy; give those lines normal priority before returning so
+// later kernels of the caller -- or a solve on another C -- are not crowded
+// out by lines nobody reads any more (the data stays cached, only its
+// priority changes).
+mdot_status Workspace::l2_reset() {
+  if (!use_tma || !Cdev) return MDOT_OK;
+  int64_t rows = 0;
+  if (eval.keep_l2) rows = nrows;
+  else if (eval.l2_res_tiles > 0)
+    rows = std::min<int64_t>(nrows, (eval.l2_res_tiles + eval.n_col_tiles - 1) / eval.n_col_tiles * eval.tile_m);
+  if (rows > 0) CKL(launch_l2_normal(Cdev, (size_t)rows * (size_t)n * sizeof(float), st));
+  return MDOT_OK;
+}
+
 void Workspace::free_owned() {
   if (owned_C) cudaFreeAsync(owned_C, st);
   if (owned_X) cudaFreeAsync(owned_X, st);
@@ -1098,7 +1126,25 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   double* rowF2 = aux + 3 * nrows + 2 * n;
   double* rowcost2 = aux + 4 * nrows + 2 * n;
   double* rowcorr = aux + 5 * nrows + 2 * n;
-  CKL(launch_round_rows(nrows, logr, cur->lm, U, logx, A, st));
+  // x needs r(F) to fp64 accuracy: with x_i r_i(F) <= r_i the rounded plan's
+  // row error err_r = r - r(F'') is >= 0 and G = F'' + err_r err_c^T / |err_r|_1
+  // lies in U(r,c) (Altschuler's precondition).
+  // The fp32-entry evaluation resolves r(F) only to ~1e-7 relative, the same
+  // size as err_r near convergence, so those log marginals are recomputed
+  // here by one exact fp64 row pass (F = exp(U + V - gbar C); the last
+  // evaluation's marginals are used as they are when they are fp64 already).
+  const double* lrF = cur->lm;
+  if (!exact_mode) {
+    ExactArgs x{};
+    x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
+    x.X = Xdev; x.Y = Ydev; x.d = d; x.scale = scale; x.otf = otf;
+    x.n = n; x.nrows = nrows;
+    x.A = U; x.B = V; x.gbar = gbar;
+    x.lr = lr_ex;
+    CKL(launch_exact_rows(x, st));
+    lrF = lr_ex;
+  }
+  CKL(launch_round_rows(nrows, logr, lrF, U, logx, A, st));
   CKL(launch_exp_neg(nrows, logx, invx, st));
   RoundArgs a{};
   a.C = Cdev; a.ldc = n; a.c_f64 = c_f64;
@@ -1292,6 +1338,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     if (u_out) cudaMemcpyAsync(u_out, w.U, sizeof(double) * nr, k, stream);
     if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * n, k, stream);
   }
+  if (st == MDOT_OK) st = w.l2_reset();
   res->evaluations = w.evals;
   res->fallbacks = w.fallbacks;
   res->kernel_ms = w.kernel_ms;
@@ -1634,6 +1681,7 @@ mdot_status mdot_marginals(const mdot_problem* pb, const double* Ain, const doub
       cudaMemcpyAsync(lc, w.cur->lm + n, sizeof(double) * n, k, stream);
     }
     if (fallback_out) *fallback_out = (int32_t)w.fallbacks;
+    if (st == MDOT_OK) st = w.l2_reset();
   }
   w.free_owned();
   w.release();

@@ -97,6 +97,7 @@ struct Workspace {
   void release();
   mdot_status load_problem(const mdot_problem* pb, int64_t row0);
   void free_owned();
+  mdot_status l2_reset();
   mdot_status setup(const mdot_options& o);
   void set_gamma(double gb);
   mdot_status prep(int mode, double alpha, double beta, const double* s_dir, const double* Ain,

@@ -74,3 +74,28 @@ def test_defaults_and_host_side_validation(L):
     st = L.mdot_solve(None, ct.byref(s), ct.byref(o), None, None, None, ct.byref(res))
     assert st == 1 and "NULL" in M.mdot_last_error()
     assert L.mdot_abi_version() == 2
+
+
+def test_binding_rejects_wrong_dtypes_before_any_call(L):
+    """The C side reads r, c, U, V, A, B as fp64 and writes u/v/lr/lc as fp64
+    and P as fp32 (include/mdot.h): the binding refuses other element types
+    and mixed host/device buffers instead of letting the library over-read or
+    overwrite them."""
+    import numpy as np
+    import paper_2307_08507_b200 as M
+    C = np.zeros((4, 4), dtype=np.float32)
+    r = np.full(4, 0.25)
+    with pytest.raises(TypeError, match="r: dtype float32"):
+        M.mdot_solve(C, r.astype(np.float32), r)
+    with pytest.raises(TypeError, match="C: dtype int32"):
+        M.mdot_solve(C.astype(np.int32), r, r)
+    with pytest.raises(TypeError, match="u_out: dtype float32"):
+        M.mdot_solve(C, r, r, u_out=np.zeros(4, dtype=np.float32))
+    with pytest.raises(TypeError, match="P_out: dtype float64"):
+        M.mdot_solve(C, r, r, P_out=np.zeros((4, 4)))
+    with pytest.raises(TypeError, match="lr: dtype float32"):
+        M.mdot_marginals(r, r, 1.0, C, r, r, lr=np.zeros(4, dtype=np.float32))
+    with pytest.raises(TypeError, match="X: dtype float64"):
+        M.mdot_solve(X=np.zeros((4, 2)), Y=np.zeros((4, 2), dtype=np.float32), r=r, c=r)
+    with pytest.raises(TypeError, match="V: dtype float32"):
+        M.mdot_round(r, r.astype(np.float32), 1.0, C, r, r)

@@ -547,3 +547,217 @@ def test_fig3_left_ncg_vs_pncg_and_jacobi_ablation():
         assert np.abs(plans[O.PNCG_JACOBI] - plans[O.PNCG]).sum() < 1e-10
     assert np.mean(its[O.NCG]) > 5 * np.mean(its[O.PNCG])
     assert np.mean(its[O.PNCG_JACOBI]) < 3 * np.mean(its[O.PNCG])
+
+
+# --------------------------------------------------- round-2 pins
+@pytest.mark.parametrize("kind", ["f32", "f64", "sqeuclid"])
+def test_log_marginal_subsets_bitwise_and_direct(kind):
+    """orc_log_marginal_rows / _cols (the checker of the full-size GPU tests)
+    must give the SAME bits as orc_log_marginals on every row / column, and
+    both must equal a direct fp64 sum of the explicit matrix."""
+    rng = np.random.default_rng(40)
+    for n in (1, 7, 33, 64):
+        if kind == "sqeuclid":
+            inst = S.config5(0, n=n, d=3)
+        else:
+            inst = S.random_small(n, seed=41 + n, dtype=np.float64 if kind == "f64" else np.float32)
+        prob = O.OracleProblem(inst)
+        C = _dense_C(prob)
+        A = np.log(inst.r) + 0.5 * rng.standard_normal(n)
+        B = np.log(inst.c) + 0.5 * rng.standard_normal(n)
+        g = 37.0
+        lr, lc, st = O.log_marginals(prob, A, B, g)
+        assert st == 0
+        idx = rng.permutation(n)
+        sub = O.log_marginal_subset(prob, A, B, g, rows=idx, cols=idx[::-1])
+        assert np.array_equal(sub["rows"], lr[idx])
+        assert np.array_equal(sub["cols"], lc[idx[::-1]])
+        P = np.exp(A[:, None] + B[None, :] - g * C)
+        np.testing.assert_allclose(np.exp(sub["rows"]), P.sum(1)[idx], rtol=1e-13)
+        np.testing.assert_allclose(np.exp(sub["cols"]), P.sum(0)[idx[::-1]], rtol=1e-13)
+
+
+def test_plan_cost_direct_sum_and_rounding_cost_F():
+    """orc_plan_cost = sum_ij C_ij P_ij (the unrounded cost of the Z20 gate):
+    direct dense sum, and the rounding routine's <C, F>."""
+    for kind in ("f32", "sqeuclid"):
+        inst = S.random_small(29, seed=44, dtype=np.float32) if kind == "f32" else S.config5(1, n=29, d=5)
+        prob = O.OracleProblem(inst)
+        C = _dense_C(prob)
+        rng = np.random.default_rng(45)
+        A = np.log(inst.r) + 0.2 * rng.standard_normal(29)
+        B = np.log(inst.c) + 0.2 * rng.standard_normal(29)
+        pc = O.plan_cost(prob, A, B, 11.0)
+        assert abs(pc - float((C * np.exp(A[:, None] + B[None, :] - 11.0 * C)).sum())) <= 1e-14 * pc
+        assert abs(pc - O.round_plan(prob, A, B, 11.0)["cost_F"]) <= 1e-14 * pc
+
+
+def test_line_search_quadratic_phi_closed_form():
+    """Appx. C on a quadratic phi(alpha) = a/2 (alpha - a*)^2 - a/2 a*^2: phi' is
+    linear, so the secant step alpha_sec is the exact minimiser
+    a* and the hybrid step is a*/2 + (lo + hi)/4.  From alpha0 = 1
+    with a* = 5.3: doubling (Z8) 1, 2, 4, 8 brackets a* in [4, 8], the hybrid
+    step is 5.3/2 + 3 = 5.65, accepted by approximate Wolfe with
+    c1 = 0.45, c2 = 0.1.  A sign or index slip in either formula changes the
+    trial sequence."""
+    a, star = 2.0, 5.3
+
+    def phi(al):
+        return a * (al - star), 0.5 * a * (al - star) ** 2 - 0.5 * a * star ** 2
+
+    al, dp, dv, tr, acc, seen = O.line_search(phi, -a * star, c1=0.45, c2=0.1)
+    assert acc and tr == 5
+    np.testing.assert_allclose(seen, [1.0, 2.0, 4.0, 8.0, 0.5 * star + 0.25 * 12.0], rtol=0, atol=1e-14)
+    assert al == seen[-1] and dv < 0
+    # a* < alpha0: the first trial overshoots; every later trial is
+    # a*/2 + (lo + hi)/4 of the current bracket: [0, 1] -> 0.4 (phi' > 0),
+    # [0, 0.4] -> 0.25 (phi' < c2 phi'(0)), [0.25, 0.4] -> 0.3125 (accepted)
+    star = 0.3
+    al, dp, dv, tr, acc, seen = O.line_search(phi, -a * star, c1=0.45, c2=0.1)
+    assert acc
+    np.testing.assert_allclose(seen, [1.0, 0.15 + 0.25, 0.15 + 0.1, 0.15 + 0.1625], rtol=0, atol=1e-15)
+    # near-exact search (c1 -> 1/2, c2 -> 0): converges to the minimiser
+    star = 13.7
+    al, dp, dv, tr, acc, seen = O.line_search(phi, -a * star, c1=0.5 - 1e-9, c2=1e-9)
+    assert acc and abs(al - star) < 1e-7 * star and tr <= 60
+    # the decrease safeguard (Z9) rejects a trial whose phi rose even when phi'
+    # satisfies the curvature window
+    al, dp, dv, tr, acc, seen = O.line_search(lambda x: (0.0, 1.0), -1.0, max_trials=5)
+    assert not acc
+
+
+def _traced(inst, gb, T, beta, c1=0.1, c2=0.4, eps=1e-10, max_evals=0):
+    prob = O.OracleProblem(inst)
+    U, V, res, tr = O.mdot(prob, O.schedule_fixed(gb, T=T),
+                           O.make_options(eps=eps, beta=beta, c1=c1, c2=c2, max_evals=max_evals), trace_cap=100000)
+    assert res["status"] == 0 or (max_evals and res["status"] == 4), res
+    return U, V, res, tr
+
+
+@pytest.mark.parametrize("beta", [O.BETA_PPR, O.BETA_PPR_AF, O.BETA_PFR, O.BETA_PPR_PRINTED, O.BETA_PPR_PLUS])
+def test_direction_update_identity_every_beta_variant(beta):
+    """p_k = -s_k + beta_k p_{k-1} (Alg. 2 line 6) implies
+    <p_k, g_k> = -<g_k, s_k> + beta_k <p_{k-1}, g_k>, and <p_{k-1}, g_k> is the
+    previous search's phi'(alpha) (g_k is the gradient at the
+    accepted trial).  Checked on the traced scalars of every beta variant
+    (first 300 evaluations: on this instance FR stalls in the "unproductive
+    directions" PAPER.md:499 describes, beta ~ 1 with tiny steps)."""
+    inst = S.paper_sphere_instance(40, 4, 0.7, seed=50)
+    _, _, _, tr = _traced(inst, 128.0, 2, beta, max_evals=300)
+    checked = 0
+    for prev, q in zip(tr, tr[1:]):
+        if q["t"] != prev["t"] or q["reset"]:
+            continue
+        rhs = -q["gs"] + q["beta"] * prev["dphi_alpha"]
+        assert abs(q["dphi0"] - rhs) <= 1e-10 * (abs(q["gs"]) + abs(q["beta"] * prev["dphi_alpha"])), (q, prev)
+        checked += 1
+        if beta == O.BETA_PPR_PLUS:
+            assert q["beta"] >= 0.0
+        if beta == O.BETA_PFR:
+            assert q["beta"] >= 0.0      # ratio of <g, s> = four-divergence sums >= 0
+    assert checked >= 5
+
+
+def test_beta_denominators_agree_under_exact_line_search_and_at_k2():
+    """Z6: the PPR denominator -<g_{k-1}, p_{k-1}> and the Al-Baali-Fletcher
+    one <g_{k-1}, s_{k-1}> differ by beta_{k-1} <g_{k-1}, p_{k-2}>, which vanishes
+    under an exact line search (c1 -> 1/2, c2 -> 0 squeeze phi'(alpha) to ~0).
+    At k = 2 (p_1 = -s_1 for every variant) they are equal
+    exactly, the printed sign of PAPER.md:262 gives -beta^PPR, and PR+ gives
+    max(0, beta^PPR)."""
+    inst = S.paper_sphere_instance(40, 4, 0.7, seed=51)
+    _, _, _, tr = _traced(inst, 128.0, 1, O.BETA_PPR, c1=0.5 - 1e-6, c2=1e-6)
+    rel = [abs(-q["dphi0"] - q["gs"]) / q["gs"] for q in tr[1:] if not q["reset"] and q["gs"] > 0]
+    assert len(rel) >= 5 and max(rel) <= 1e-4, max(rel)
+    k2 = {}
+    for beta in (O.BETA_PPR, O.BETA_PPR_AF, O.BETA_PPR_PRINTED, O.BETA_PPR_PLUS):
+        prob = O.OracleProblem(inst)
+        _, _, res, trb = O.project(prob, np.log(inst.r), np.log(inst.c), 128.0,
+                                   opts=O.make_options(eps=1e-12, beta=beta, max_evals=40), trace_cap=100)
+        q = trb[1]
+        assert q["k"] == 2 and trb[0]["beta"] == 0.0
+        k2[beta] = q["beta"] if not q["reset"] else 0.0
+    b = k2[O.BETA_PPR]
+    assert b != 0.0
+    assert k2[O.BETA_PPR_AF] == b
+    assert k2[O.BETA_PPR_PLUS] == max(b, 0.0)
+    assert k2[O.BETA_PPR_PRINTED] in (-b, 0.0)   # 0.0 when the printed sign forces a reset (Z5)
+
+
+@pytest.mark.parametrize("beta", [O.BETA_PPR_AF, O.BETA_PFR, O.BETA_PPR_PRINTED, O.BETA_PPR_PLUS])
+def test_every_beta_variant_reaches_the_2x2_closed_form_and_the_ppr_plan(beta):
+    """Uniqueness of the Bregman projection: every beta variant
+    (FR; PPR with either denominator, Z6; PR+) converges to
+    the entropic plan, pinned by the 2x2 closed form and, at n = 20, by the
+    default PPR solve."""
+    rng = np.random.default_rng(52)
+    for trial in range(8):
+        C = rng.uniform(0, 1, size=(2, 2))
+        r = rng.dirichlet([1, 1])
+        c = rng.dirichlet([1, 1])
+        gb = [4.0, 32.0, 150.0][trial % 3]
+        prob = O.OracleProblem(C=C, r=r, c=c)
+        U, V, res, _ = O.mdot(prob, [gb], O.make_options(eps=1e-14, beta=beta))
+        assert res["status"] == 0
+        np.testing.assert_allclose(np.exp(U[:, None] + V[None, :] - gb * C), X.entropic_2x2(C, r, c, gb), atol=1e-13)
+    inst = S.random_small(20, seed=53)
+    ref, _ = _md_plan(O.OracleProblem(inst), [30.0], eps=1e-13)
+    P, _ = _md_plan(O.OracleProblem(inst), [30.0], eps=1e-13, beta=beta)
+    assert np.abs(P - ref).sum() < 1e-11
+
+
+def test_warm_start_modes_reach_the_same_plan():
+    """Z4 warm-start readings (scaled / carried / zero potentials) only move
+    where each projection starts: by Lemma 2 the final plan
+    is the entropic plan at gbar for all three, on a variable (doubling)
+    schedule where scaled and carried differ."""
+    inst = S.random_small(10, seed=54)
+    prob = O.OracleProblem(inst)
+    sched = O.schedule_doubling(64.0)
+    ref, r0 = _md_plan(prob, [64.0], eps=1e-13)
+    evals = {}
+    for warm in (O.WARM_SCALED, O.WARM_CARRY, O.WARM_ZERO):
+        P, res = _md_plan(prob, sched, eps=1e-13, warm=warm)
+        assert np.abs(P - ref).sum() < 1e-10, warm
+        evals[warm] = res["evaluations"]
+    assert evals[O.WARM_ZERO] > evals[O.WARM_SCALED]   # warm starts save work
+    rng = np.random.default_rng(55)
+    C = rng.uniform(0, 1, size=(2, 2))
+    r, c = rng.dirichlet([1, 1]), rng.dirichlet([1, 1])
+    for warm in (O.WARM_CARRY, O.WARM_ZERO):
+        U, V, res, _ = O.mdot(O.OracleProblem(C=C, r=r, c=c), O.schedule_doubling(100.0),
+                              O.make_options(eps=1e-14, warm=warm))
+        np.testing.assert_allclose(np.exp(U[:, None] + V[None, :] - 100.0 * C), X.entropic_2x2(C, r, c, 100.0),
+                                   atol=1e-13)
+
+
+def test_adaptive_gamma_schedule_lemma2_and_budget():
+    """Adaptive step rule (Z29, PAPER.md:371 future work): the realised steps
+    sum to gbar exactly, follow the doubling / halving rule, and -- Lemma 2,
+    PAPER.md:152-155 -- the final plan equals the single-step (T = 1) plan and
+    the 2x2 closed form."""
+    inst = S.random_small(12, seed=56)
+    prob = O.OracleProblem(inst)
+    gb = 512.0
+    ref, _ = _md_plan(prob, [gb], eps=1e-12)
+    U, V, res, _, g = O.mdot_adaptive(prob, gb, 16.0, O.make_options(eps=1e-12))
+    assert res["status"] == 0 and res["gamma_bar"] == gb
+    assert g.sum() == gb and len(g) == res["md_steps"] >= 3
+    assert g[0] == 16.0 and g[1] == 32.0
+    for a, b in zip(g[1:-1], g[2:-1]):
+        assert b in (2 * a, max(a / 2, gb / 1024))
+    P = np.exp(U[:, None] + V[None, :] - gb * inst.C)
+    assert np.abs(P - ref).sum() < 1e-10
+    # eps_md composes with it (both only move starting points)
+    U2, V2, res2, _, g2 = O.mdot_adaptive(prob, gb, 16.0, O.make_options(eps=1e-12, eps_md=1e-3))
+    assert np.abs(np.exp(U2[:, None] + V2[None, :] - gb * inst.C) - ref).sum() < 1e-10
+    # a first step covering the budget is the T = 1 solve
+    U3, V3, res3, _, g3 = O.mdot_adaptive(prob, gb, 4096.0, O.make_options(eps=1e-12))
+    assert list(g3) == [gb]
+    rng = np.random.default_rng(57)
+    C = rng.uniform(0, 1, size=(2, 2))
+    r, c = rng.dirichlet([1, 1]), rng.dirichlet([1, 1])
+    U, V, res, _, g = O.mdot_adaptive(O.OracleProblem(C=C, r=r, c=c), 100.0, 4.0, O.make_options(eps=1e-14))
+    assert res["status"] == 0 and len(g) >= 3
+    np.testing.assert_allclose(np.exp(U[:, None] + V[None, :] - 100.0 * C), X.entropic_2x2(C, r, c, 100.0),
+                               atol=1e-13)

@@ -24,7 +24,8 @@
  * row-major fp32 point clouds; the on-the-fly cost is
  *   C_ij = fl32( fmaf-chain over k of (x_ik - y_jk)^2 ) * scale
  * with the exact fp32 op order of DESIGN.md "Z22".  r, c are fp64 [n],
- * strictly positive, summing to 1 within 1e-12.
+ * strictly positive, summing to 1 within 1e-12 (checked with a
+ * compensated sum).
  */
 #ifndef MDOT_H
 #define MDOT_H
@@ -34,7 +35,7 @@
 extern "C" {
 #endif
 
-#define MDOT_ABI_VERSION 2
+#define MDOT_ABI_VERSION 3
 
 typedef enum {
   MDOT_OK = 0,
@@ -73,7 +74,15 @@ typedef enum {
   MDOT_SCHED_FIXED = 0,     /* T equal steps gamma_t = gamma_bar/T; T = max(1, floor(gamma_bar/step_max))
                                when T == 0 */
   MDOT_SCHED_DOUBLING = 1,  /* cumulative gbar_t = gamma0 * 2^(t-1) up to gamma_bar (BASELINE config 1, Z13) */
-  MDOT_SCHED_EXPLICIT = 2   /* gammas[0..n_gammas-1] */
+  MDOT_SCHED_EXPLICIT = 2,  /* gammas[0..n_gammas-1] */
+  MDOT_SCHED_ADAPTIVE = 3   /* variable step rule (PAPER.md:371 future work; Z29): gamma_1 =
+                               min(step_max, gamma_bar); with E_t the O(n^2) evaluations step t took and
+                               eta_t = gamma_t / E_t, gamma_2 = 2 gamma_1 and gamma_{t+1} = 2 gamma_t if
+                               eta_t >= eta_{t-1}, else max(gamma_t / 2, gamma_bar / 1024); each step is
+                               clipped to the remaining budget, a remainder below a quarter of the next step
+                               is merged into it, step 64 takes the rest.  Lemma 2: the
+                               final plan is the entropic plan at gamma_bar whatever the realised steps.
+                               The realised schedule is returned in mdot_result.gammas. */
 } mdot_sched_kind;
 
 typedef struct {
@@ -91,9 +100,29 @@ typedef struct {
  * bounded below by the target marginals (max(r(P), r)), in place of the
  * Sinkhorn direction (SURVEY 8(f) rank 2 ablation of PAPER.md:257). */
 typedef enum { MDOT_PROJ_PNCG = 0, MDOT_PROJ_SINKHORN = 1, MDOT_PROJ_NCG = 2, MDOT_PROJ_PNCG_JACOBI = 3 } mdot_projector;
-typedef enum { MDOT_BETA_PPR = 0, MDOT_BETA_PPR_AF = 1, MDOT_BETA_PFR = 2 } mdot_beta;
+/* PPR: Eq. beta_PPR_OT with the denominator sign of Z6;
+ * PPR_AF: Al-Baali-Fletcher denominator <g_{k-1}, s_{k-1}> (equal under exact
+ * line search); PFR: preconditioned Fletcher-Reeves <g_k, s_k> / <g_{k-1},
+ * s_{k-1}>; PPR_PLUS: max(0, beta^PPR) (PR+, Gilbert &
+ * Nocedal, cited at PAPER.md:499). */
+typedef enum { MDOT_BETA_PPR = 0, MDOT_BETA_PPR_AF = 1, MDOT_BETA_PFR = 2, MDOT_BETA_PPR_PLUS = 3 } mdot_beta;
 typedef enum { MDOT_WARM_SCALED = 0, MDOT_WARM_CARRY = 1, MDOT_WARM_ZERO = 2 } mdot_warm;
 typedef enum { MDOT_PREC_AUTO = 0, MDOT_PREC_F32P = 1, MDOT_PREC_F64P = 2 } mdot_precision;
+
+/* One record per PNCG iteration (accepted step) or Sinkhorn half-step, in
+ * order ("SolveTrace"; the oracle's orc_trace_rec has the same
+ * fields).  PNCG: l1, rho at the iterate BEFORE the update; alpha the accepted
+ * step; dphi0 = phi'(0) = <p, grad g>; dphi_alpha = phi'(alpha);
+ * dphi_value = phi(alpha) - phi(0); beta the beta_k used in p (0 after a reset);
+ * gs = <grad g, s> at the iterate; trials = line-search evaluations; reset = 1
+ * when p = -s was forced (Z5 / Z10).  Sinkhorn: alpha = 1, the rest 0. */
+typedef struct {
+  int32_t t, k;            /* MD step (1-based), iteration within the projection (1-based) */
+  double l1, rho;
+  double alpha, dphi0, dphi_alpha, dphi_value;
+  int32_t trials, reset;
+  double beta, gs;
+} mdot_trace_rec;
 
 typedef struct {
   double eps;              /* projection stop tolerance (> 0) */
@@ -116,6 +145,10 @@ typedef struct {
                               U(r,c) is invariant to diagonal scalings of its input, so an inexact
                               intermediate projection only moves the last step's starting point
                               (adaptive eps, the paper's stated future work). */
+  mdot_trace_rec* trace;   /* nullable HOST buffer of trace_cap records; filled in iteration order
+                              (mdot_solve_batch: instance 0 only; sharded: this rank's copy) */
+  int64_t trace_cap;
+  int64_t* trace_len;      /* nullable host pointer: number of records written (<= trace_cap) */
 } mdot_options;
 
 typedef struct {
@@ -141,6 +174,7 @@ typedef struct {
   double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */
   double l10[64];          /* per MD step: L1 at the warm start */
   int64_t iters_step[64];  /* per MD step: projection iterations */
+  double gammas[64];       /* per MD step: the realised gamma_t (ADAPTIVE chooses them on the fly) */
 } mdot_result;
 
 /* Fill defaults: eps 1e-6 on L1, PNCG, beta PPR (Z6), c1 0.1, c2 0.4,

@@ -18,6 +18,7 @@ from ._binding import (  # noqa: F401
     MDOT_BETA_PFR,
     MDOT_BETA_PPR,
     MDOT_BETA_PPR_AF,
+    MDOT_BETA_PPR_PLUS,
     MDOT_COST_DENSE_F32,
     MDOT_COST_DENSE_F64,
     MDOT_COST_SQEUCLID_F32,
@@ -28,6 +29,7 @@ from ._binding import (  # noqa: F401
     MDOT_PROJ_PNCG_JACOBI,
     MDOT_PROJ_PNCG,
     MDOT_PROJ_SINKHORN,
+    MDOT_SCHED_ADAPTIVE,
     MDOT_SCHED_DOUBLING,
     MDOT_SCHED_EXPLICIT,
     MDOT_SCHED_FIXED,
@@ -35,6 +37,7 @@ from ._binding import (  # noqa: F401
     MDOT_WARM_SCALED,
     MDOT_WARM_ZERO,
     STATUS_NAMES,
+    TraceRec,
     MdotError,
     lib,
     mdot_comm_create,
@@ -50,5 +53,6 @@ from ._binding import (  # noqa: F401
     mdot_solve_batch,
     mdot_solve_sharded,
     options,
+    read_trace,
     schedule,
 )

@@ -12,9 +12,9 @@ LIB_PATH = os.environ.get("MDOT_LIB") or os.path.join(_HERE, "libmdot_b200.so")
 
 MDOT_COST_DENSE_F32, MDOT_COST_SQEUCLID_F32, MDOT_COST_DENSE_F64 = 0, 1, 2
 MDOT_MEM_HOST, MDOT_MEM_DEVICE = 0, 1
-MDOT_SCHED_FIXED, MDOT_SCHED_DOUBLING, MDOT_SCHED_EXPLICIT = 0, 1, 2
+MDOT_SCHED_FIXED, MDOT_SCHED_DOUBLING, MDOT_SCHED_EXPLICIT, MDOT_SCHED_ADAPTIVE = 0, 1, 2, 3
 MDOT_PROJ_PNCG, MDOT_PROJ_SINKHORN, MDOT_PROJ_NCG, MDOT_PROJ_PNCG_JACOBI = 0, 1, 2, 3
-MDOT_BETA_PPR, MDOT_BETA_PPR_AF, MDOT_BETA_PFR = 0, 1, 2
+MDOT_BETA_PPR, MDOT_BETA_PPR_AF, MDOT_BETA_PFR, MDOT_BETA_PPR_PLUS = 0, 1, 2, 3
 MDOT_WARM_SCALED, MDOT_WARM_CARRY, MDOT_WARM_ZERO = 0, 1, 2
 MDOT_PREC_AUTO, MDOT_PREC_F32P, MDOT_PREC_F64P = 0, 1, 2
 STATUS_NAMES = {0: "MDOT_OK", 1: "MDOT_EINVAL", 2: "MDOT_EGEN", 3: "MDOT_EINSTABLE",
@@ -40,13 +40,22 @@ class Schedule(ct.Structure):
                 ("n_gammas", ct.c_int32)]
 
 
+class TraceRec(ct.Structure):
+    """mdot_trace_rec (include/mdot.h): one PNCG iteration / Sinkhorn half-step."""
+    _fields_ = [("t", ct.c_int32), ("k", ct.c_int32), ("l1", ct.c_double), ("rho", ct.c_double),
+                ("alpha", ct.c_double), ("dphi0", ct.c_double), ("dphi_alpha", ct.c_double),
+                ("dphi_value", ct.c_double), ("trials", ct.c_int32), ("reset", ct.c_int32),
+                ("beta", ct.c_double), ("gs", ct.c_double)]
+
+
 class Options(ct.Structure):
     _fields_ = [("eps", ct.c_double), ("stop", ct.c_int32), ("projector", ct.c_int32),
                 ("beta", ct.c_int32), ("c1", ct.c_double), ("c2", ct.c_double),
                 ("warm", ct.c_int32), ("precision", ct.c_int32), ("p0_ones", ct.c_int32),
                 ("ls_max_trials", ct.c_int32), ("max_evals", ct.c_int64),
                 ("time_kernels", ct.c_int32), ("device_control", ct.c_int32),
-                ("stream", ct.c_void_p), ("eps_md", ct.c_double)]
+                ("stream", ct.c_void_p), ("eps_md", ct.c_double),
+                ("trace", ct.c_void_p), ("trace_cap", ct.c_int64), ("trace_len", ct.c_void_p)]
 
 
 class Result(ct.Structure):
@@ -59,16 +68,17 @@ class Result(ct.Structure):
                 ("stage_ms", ct.c_double * 4), ("stage_samples", ct.c_int64),
                 ("status", ct.c_int32), ("control_path", ct.c_int32),
                 ("rho0", ct.c_double * 64), ("l10", ct.c_double * 64),
-                ("iters_step", ct.c_int64 * 64)]
+                ("iters_step", ct.c_int64 * 64), ("gammas", ct.c_double * 64)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_
-             if f not in ("rho0", "l10", "iters_step", "stage_ms")}
+             if f not in ("rho0", "l10", "iters_step", "stage_ms", "gammas")}
         d["stage_ms"] = list(self.stage_ms)
         T = int(min(self.md_steps, 64))
         d["rho0"] = list(self.rho0)[:T]
         d["l10"] = list(self.l10)[:T]
         d["iters_step"] = list(self.iters_step)[:T]
+        d["gammas"] = list(self.gammas)[:T]
         d["status_name"] = STATUS_NAMES.get(self.status, str(self.status))
         return d
 
@@ -112,7 +122,7 @@ def lib():
                    "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_enable_peer", "mdot_comm_destroy",
                    "mdot_solve_sharded"):
             getattr(L, nm).restype = ct.c_int
-        if L.mdot_abi_version() != 2:
+        if L.mdot_abi_version() != 3:
             raise ImportError("libmdot_b200.so ABI version mismatch")
         _lib = L
     return _lib
@@ -204,14 +214,29 @@ def schedule(kind=MDOT_SCHED_FIXED, gamma_bar=4096.0, T=0, step_max=256.0, gamma
     return s
 
 
-def options(**kw):
+def options(trace_cap=0, **kw):
+    """mdot_options with defaults; trace_cap > 0 attaches a host trace buffer
+    (read it back with read_trace(options) after the call)."""
     o = Options()
     lib().mdot_options_default(ct.byref(o))
     for k, v in kw.items():
         if k == "stream":
             continue
         setattr(o, k, v)
+    if trace_cap:
+        buf = (TraceRec * int(trace_cap))()
+        ln = ct.c_int64(0)
+        o.trace = ct.cast(buf, ct.c_void_p)
+        o.trace_cap = int(trace_cap)
+        o.trace_len = ct.cast(ct.pointer(ln), ct.c_void_p)
+        o._trace = (buf, ln)
     return o
+
+
+def read_trace(opts):
+    """The records the last call wrote into opts' trace buffer, as dicts."""
+    buf, ln = opts._trace
+    return [{f: getattr(buf[k], f) for f, _ in TraceRec._fields_} for k in range(ln.value)]
 
 
 def _check(st, what):

@@ -627,9 +627,14 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   int status = 0;
   double gbar = 0.0, gprev = 0.0, l1 = 0.0, rho = 0.0;
   int t_done = 0;
-  for (int t = 1; t <= a.T; ++t) {
-    const double gt = a.gammas[t - 1];
-    gbar += gt;
+  // ADAPTIVE schedule (Z29): the next step from this step's evaluation count
+  double next = a.adaptive ? a.gamma1 : 0.0, eta_prev = 0.0;
+  int final_next = a.adaptive && a.gamma1 >= a.gamma_bar;
+  for (int t = 1; a.adaptive || t <= a.T; ++t) {
+    const double gt = a.adaptive ? next : a.gammas[t - 1];
+    const bool last = a.adaptive ? final_next != 0 : t == a.T;
+    gbar = (a.adaptive && last) ? a.gamma_bar : gbar + gt;
+    if (tid == 0 && q_rank == 0 && t <= 64) a.res[b].gammas[t - 1] = gt;
     const double g2 = gbar * L2E_D;
     const float gh = (float)g2, gl = (float)(g2 - (double)(float)g2);
     // warm start (Z4)
@@ -643,11 +648,15 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     if (tid == 0) {
       CtrlState& h = S.st;
       memset(&h, 0, sizeof(CtrlState));
-      h.eps = t < a.T ? a.eps_md : a.eps; h.c1 = a.c1; h.c2 = a.c2; h.noise = ls_noise(a.f64 != 0, gbar);
+      h.eps = last ? a.eps : a.eps_md; h.c1 = a.c1; h.c2 = a.c2; h.noise = ls_noise(a.f64 != 0, gbar);
       h.stop_rho = a.stop_rho; h.ncg = a.projector == MDOT_PROJ_NCG; h.sinkhorn = a.projector == MDOT_PROJ_SINKHORN;
       h.beta_kind = a.beta_kind; h.ls_max_trials = a.ls_max_trials;
       h.max_evals = a.max_evals - evals_total;
       h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+      h.md_t = t;
+      if (a.trace && b == 0 && q_rank == 0) {   // one writer: instance 0, cluster rank 0
+        h.trace = a.trace; h.trace_len = a.trace_len; h.trace_cap = a.trace_cap;
+      }
     }
     __syncthreads();
     bool first = true;
@@ -767,6 +776,11 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
     t_done = t;
     if (status != 0 && status != MDOT_ENOCONV) break;
     if (status == MDOT_ENOCONV) break;
+    if (a.adaptive) {
+      if (last) break;
+      // every CTA of the cluster holds the same h.evals: same decision everywhere
+      next = adaptive_next_gamma(t, gt, (double)h.evals, gbar, a.gamma_bar, &eta_prev, &final_next);
+    }
   }
 
   // ---- rounding + cost (a10), fp64: F = exp(U + V - gbar C), x = min(r/r(F), 1)
@@ -922,5 +936,7 @@ cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st) {
   if (scalar) return cudaLaunchKernelEx(&cfg, k_batch_solve<false, float>, a);
   return cudaLaunchKernelEx(&cfg, k_batch_solve<true, float>, a);
 }
+
+void fault_set_batch(int mode) { fault_set_tu(mode); }
 
 }  // namespace mdot

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/mdot.h"
+
 namespace mdot {
 
 // ---------------------------------------------------------------------------
@@ -23,6 +25,7 @@ constexpr int kWarps = 8;        // warps per CTA
 constexpr int kThreads = kWarps * 32;
 constexpr int kUnroll = 4;       // rows per warp per inner step
 constexpr int kNumScalars = 16;
+constexpr long long kTraceDevCap = 1 << 20;   // device trace records per projection (mdot_options.trace)
 
 // K1 reduction knobs, shared by the TMA kernels,
 // k_eval_fast (bitwise-equal by test), K2 and the fp32-entry paths of K8: MDOT_K1_ROWRED_F32 = 1 reduces the 4
@@ -191,6 +194,13 @@ struct CtrlState {
   // line search
   double lo, dlo, hi, dhi, dphi0, dg;
   int have_hi, doublings, trials, attempt;
+  // per-iteration trace (mdot_options.trace): device records written by the
+  // ONE controller copy whose `trace` is non-null (CTA 0 of the persistent
+  // grid, k_ctrl, instance 0 of K8); md_t = MD step of this projection
+  mdot_trace_rec* trace;
+  long long* trace_len;
+  long long trace_cap;
+  int md_t, reset_flag;
   // scalars published by k_finalize
   double sc[kNumScalars];
 };
@@ -358,7 +368,36 @@ struct BatchResult {
   int md_steps, status;
   double rho0[64], l10[64];      // per MD step (t <= 64): initial infeasibility / L1 of the projection
   long long iters_step[64];      // per MD step iterations
+  double gammas[64];             // per MD step: realised gamma_t
 };
+// beta_k (Z6; FR PAPER.md:496-498; PR+) from the scalars of
+// the current iterate; shared by the device controller and the host loop
+__host__ __device__ inline double beta_k(bool ncg, int beta_kind, double S_sg, double S_gcs, double S_gg,
+                                        double S_gcg, double dphi0_prev, double sg_prev, double gg_prev) {
+  double num, den;
+  if (ncg) { num = S_gg - S_gcg; den = gg_prev; }
+  else if (beta_kind == MDOT_BETA_PPR || beta_kind == MDOT_BETA_PPR_PLUS) { num = S_sg - S_gcs; den = -dphi0_prev; }
+  else if (beta_kind == MDOT_BETA_PPR_AF) { num = S_sg - S_gcs; den = sg_prev; }
+  else { num = S_sg; den = sg_prev; }
+  double b = (fabs(den) > 1e-300) ? num / den : 0.0;
+  if (!ncg && beta_kind == MDOT_BETA_PPR_PLUS && b < 0.0) b = 0.0;   // PR+
+  return b;
+}
+
+// ADAPTIVE schedule step rule (mdot.h MDOT_SCHED_ADAPTIVE, Z29),
+// shared by the host loop (solver.cu) and K8: given the step just finished
+// (gamma_t, its evaluation count E, the running gbar and the previous
+// efficiency eta_prev), the next step; *final is set when it is the last.
+__host__ __device__ inline double adaptive_next_gamma(int t, double gt, double evals, double gbar,
+                                                      double gamma_bar, double* eta_prev, int* final) {
+  const double eta = gt / (evals > 1.0 ? evals : 1.0);
+  double g = (t == 1 || eta >= *eta_prev) ? 2.0 * gt : fmax(0.5 * gt, gamma_bar / 1024.0);
+  *eta_prev = eta;
+  const double rem = gamma_bar - gbar;
+  *final = 0;
+  if (g >= rem || rem - g < 0.25 * g || t + 1 >= 64) { g = rem; *final = 1; }
+  return g;
+}
 struct BatchArgs {
   const float* C;          // shared n x n fp32 cost (device)
   const double* C64;       // or fp64 cost (DENSE_F64; fp64 entries), C unused
@@ -367,6 +406,11 @@ struct BatchArgs {
   const double* c;         // [B][n]
   const double* gammas;    // [T] schedule (device)
   int T;
+  int adaptive;            // MDOT_SCHED_ADAPTIVE: steps chosen on the fly from gamma1, gamma_bar
+  double gamma_bar, gamma1;
+  mdot_trace_rec* trace;   // nullable device trace of instance 0
+  long long* trace_len;
+  long long trace_cap;
   double eps, eps_md, c1, c2;   // eps_md: intermediate MD steps (>= eps)
   int stop_rho, projector, beta_kind, ls_max_trials, warm, p0_ones, f64;
   long long max_evals;
@@ -377,5 +421,12 @@ struct BatchArgs {
 };
 size_t batch_smem_bytes(int n);
 cudaError_t launch_batch(const BatchArgs& a, int B, cudaStream_t st);
+
+// MDOT_FAULT_NAN test hook (ops.cuh): per translation unit setters; apply_fault_env()
+// (solver.cu) reads the environment and sets all of them when it changes
+void fault_set_kernels(int mode);
+void fault_set_persist(int mode);
+void fault_set_batch(int mode);
+void apply_fault_env();
 
 }  // namespace mdot

@@ -1144,4 +1144,6 @@ cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t s
   return cudaGetLastError();
 }
 
+void fault_set_kernels(int mode) { fault_set_tu(mode); }
+
 }  // namespace mdot

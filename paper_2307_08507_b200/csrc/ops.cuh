@@ -136,6 +136,21 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
   }
 }
 
+// Fault injection for the error-path tests (MDOT_FAULT_NAN, solver.cu):
+// 1 = the total of item 0 in the first fp32-entry evaluation becomes NaN
+//     (the range guard must redo that evaluation exactly, the solve go on);
+// 2 = item 0's log marginal is NaN in every evaluation, exact ones included
+//     (the call must end with MDOT_EINSTABLE, not hang or return garbage).
+// `static` in a header: every translation unit has its own copy, set by its
+// own fault_set_* (no relocatable device code).
+static __constant__ int c_fault_nan = 0;
+static __device__ unsigned int g_fault_hits = 0;
+static inline void fault_set_tu(int mode) {
+  unsigned int z = 0;
+  cudaMemcpyToSymbol(c_fault_nan, &mode, sizeof(int));
+  cudaMemcpyToSymbol(g_fault_hits, &z, sizeof(z));
+}
+
 // 8 threads per item: the partial sums are split over the octet (t = lane%8,
 // t+8, ...) in a fixed order and combined by a fixed shuffle tree, so every
 // partial load of an item is in flight at once.
@@ -160,6 +175,7 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
                                               double (&v)[kNumScalars]) {
   const bool is_row = k < a.nrows;
     double lm, bad = 0.0;
+    if (c_fault_nan == 1 && k == 0 && a.from_partials == 1 && atomicAdd(&g_fault_hits, 1u) == 0u) tot = __longlong_as_double(0x7ff8000000000000ll);
     if (a.from_partials == 1) {
       const double anchor = is_row ? a.rho_r[k] : a.sig_c[k - a.nrows];
       lm = log(tot) + anchor * LN2_D;
@@ -179,6 +195,7 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
       }
       if (!isfinite(lm)) bad = 1.0;
     }
+    if (c_fault_nan == 2 && k == 0) { lm = __longlong_as_double(0x7ff8000000000000ll); bad = 1.0; }
     const double tgt = is_row ? a.r[k] : a.c[k - a.nrows];
     const double ltg = is_row ? a.logr[k] : a.logc[k - a.nrows];
     const double mm = exp(lm);
@@ -222,20 +239,27 @@ __device__ inline void ctrl_finish(CtrlState* st, int status, int* done_host) {
   if (done_host) *((volatile int*)done_host) = 1;
 }
 
+__device__ inline void ctrl_trace(CtrlState* st, double alpha, double dphi_a, double dval) {
+  if (!st->trace || *st->trace_len >= st->trace_cap) return;
+  mdot_trace_rec& q = st->trace[*st->trace_len];
+  q.t = st->md_t; q.k = (int32_t)st->k;
+  q.l1 = st->l1; q.rho = st->rho;
+  q.alpha = alpha; q.dphi0 = st->sinkhorn ? 0.0 : st->dphi0; q.dphi_alpha = dphi_a; q.dphi_value = dval;
+  q.trials = st->sinkhorn ? 0 : st->trials; q.reset = st->sinkhorn ? 0 : st->reset_flag;
+  q.beta = st->sinkhorn ? 0.0 : st->beta; q.gs = st->sinkhorn ? 0.0 : st->S_sg;
+  *st->trace_len += 1;
+}
+
 __device__ inline void ctrl_start_iteration(CtrlState* st) {
   st->k++;
   double beta = 0.0;
-  if (st->k > 1) {
-    double num, den;
-    if (st->ncg) { num = st->S_gg - st->S_gcg; den = st->gg_prev; }
-    else if (st->beta_kind == 0) { num = st->S_sg - st->S_gcs; den = -st->dphi0_prev; }   // Z6
-    else if (st->beta_kind == 1) { num = st->S_sg - st->S_gcs; den = st->sg_prev; }
-    else { num = st->S_sg; den = st->sg_prev; }
-    beta = (fabs(den) > 1e-300) ? num / den : 0.0;
-  }
+  if (st->k > 1)
+    beta = beta_k(st->ncg, st->beta_kind, st->S_sg, st->S_gcs, st->S_gg, st->S_gcg, st->dphi0_prev, st->sg_prev,
+                  st->gg_prev);
   const double dg = st->ncg ? st->S_gg : st->S_sg;
   double dphi0 = -dg + beta * st->S_pcg;
-  if (!(dphi0 < 0.0)) { beta = 0.0; dphi0 = -dg; st->resets++; }   // Z5
+  st->reset_flag = 0;
+  if (!(dphi0 < 0.0)) { beta = 0.0; dphi0 = -dg; st->resets++; st->reset_flag = 1; }   // Z5
   st->dg = dg;
   st->dphi0 = dphi0;
   st->beta = beta;
@@ -270,6 +294,7 @@ __device__ inline void ctrl_body(CtrlState* st, int slot, int* done_host, int* r
   }
   if (st->sinkhorn) {   // Alg. 3 half-step result
     if (bad) { ctrl_finish(st, CTRL_NEED_HOST, done_host); if (ran_host) ran_host[slot] = 0; return; }
+    ctrl_trace(st, 1.0, 0.0, 0.0);
     st->accept_marg = 1;
     st->iterations++;
     st->l1 = sc[SC_L1]; st->rho = sc[SC_RHO]; st->mass = sc[SC_MASS];
@@ -289,6 +314,7 @@ __device__ inline void ctrl_body(CtrlState* st, int slot, int* done_host, int* r
   const bool wolfe = ((2.0 * st->c1 - 1.0) * st->dphi0 >= dphi_a) && (dphi_a >= st->c2 * st->dphi0);
   const bool decrease = dval <= st->noise * fmax(1.0, st->mass);
   if (!bad && wolfe && decrease) {
+    ctrl_trace(st, st->alpha, dphi_a, dval);
     st->accept_marg = 1;
     st->accept_pot = 1;
     st->iterations++;
@@ -326,6 +352,7 @@ __device__ inline void ctrl_body(CtrlState* st, int slot, int* done_host, int* r
     st->dphi0 = -st->dg;
     st->alpha = 1.0;
     st->beta = 0.0;
+    st->reset_flag = 1;
     st->lo = 0.0; st->dlo = st->dphi0; st->hi = 0.0; st->dhi = 0.0;
     st->have_hi = 0; st->doublings = 0; st->trials = 0;
     st->mode = PREP_NEWDIR | PREP_TRIAL;

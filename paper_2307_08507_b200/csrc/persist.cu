@@ -241,6 +241,8 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
     for (int i = tid; i < kWords; i += blockDim.x) sh[i] = g[i];
   }
   __syncthreads();
+  // one trace writer: CTA 0's controller copy (every CTA takes the same decisions)
+  if (tid == 0 && cta != 0) S.st.trace = nullptr;
   if (warp == kConsumerWarps && lane == 0)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
 
@@ -495,5 +497,7 @@ cudaError_t launch_persist(const void* map, const PersistArgs& a, int grid, cuda
   void* args[] = {const_cast<CUtensorMap*>(m), const_cast<PersistArgs*>(&a)};
   return cudaLaunchCooperativeKernel(persist_fn(), dim3(grid), dim3(kTmaThreads), args, (size_t)smem, st);
 }
+
+void fault_set_persist(int mode) { fault_set_tu(mode); }
 
 }  // namespace mdot

@@ -234,6 +234,9 @@ void Workspace::release() {
   gev_made = false;
   if (base) cudaFreeAsync(base, st);
   base = nullptr;
+  if (trace_dev) cudaFreeAsync(trace_dev, st);
+  trace_dev = nullptr;
+  trace_len_dev = nullptr;
   if (scal_host) {
     cudaStreamSynchronize(st);   // the block may still be written by queued kernels
     host_block_put(scal_host);
@@ -383,6 +386,11 @@ mdot_status project_sinkhorn(Workspace& w, const mdot_options& o, int t, mdot_re
   while (stopval(sc, o.stop) > o.eps) {
     if (w.evals >= o.max_evals) { st = MDOT_ENOCONV; break; }
     ++k;
+    if (w.trace_cap) {
+      mdot_trace_rec q{};
+      q.t = t; q.k = (int32_t)k; q.l1 = sc[SC_L1]; q.rho = sc[SC_RHO]; q.alpha = 1.0;
+      w.trace_add(q);
+    }
     CKS(w.prep((k % 2 == 1) ? PREP_SK_ROW : PREP_SK_COL, 0, 0, nullptr, nullptr, nullptr));
     CKS(w.evaluate(w.cur, nullptr, nullptr, sc));
     res->iterations++;
@@ -414,24 +422,18 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
   while (stopval(sc, o.stop) > o.eps) {
     if (w.evals >= o.max_evals) { st = MDOT_ENOCONV; break; }
     ++k;
-    // beta_k (Z6) from scalars of the current iterate
+    // beta_k (Z6; FR / PR+ variants) from scalars of the current iterate
     double beta = 0.0;
-    if (k > 1) {
-      double num, den;
-      if (ncg) { num = S_gg - S_gcg; den = gg_prev; }
-      else if (o.beta == MDOT_BETA_PPR) { num = S_sg - S_gcs; den = -dphi0_prev; }
-      else if (o.beta == MDOT_BETA_PPR_AF) { num = S_sg - S_gcs; den = sg_prev; }
-      else { num = S_sg; den = sg_prev; }
-      beta = (fabs(den) > 1e-300) ? num / den : 0.0;
-    }
+    if (k > 1) beta = beta_k(ncg, o.beta, S_sg, S_gcs, S_gg, S_gcg, dphi0_prev, sg_prev, gg_prev);
     const double* dir = ncg ? w.cur->g : w.cur->s;
     const double dg = ncg ? S_gg : S_sg;            // <dir, g>
     double dphi0 = -dg + beta * S_pcg;              // <p, g> with p = -dir + beta p_prev
-    if (!(dphi0 < 0.0)) { beta = 0.0; dphi0 = -dg; res->resets++; }   // Z5
+    int reset = 0;
+    if (!(dphi0 < 0.0)) { beta = 0.0; dphi0 = -dg; res->resets++; reset = 1; }   // Z5
     double alpha = (k == 1) ? 1.0 : std::min(4.0, std::max(0.25, alpha_prev));  // Z8
     CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, beta, dir, nullptr, nullptr));
-    int accepted = 0, attempt = 0;
-    double dphi_a = 0;
+    int accepted = 0, attempt = 0, trials = 0;
+    double dphi_a = 0, dval = 0;
     while (!accepted && attempt < 2) {
       double lo = 0.0, dlo = dphi0, hi = 0.0, dhi = 0.0;
       int have_hi = 0, doublings = 0;
@@ -439,8 +441,9 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
         if (tr > 0) CKS(w.prep(PREP_TRIAL, alpha, 0, nullptr, nullptr, nullptr));
         CKS(w.evaluate(w.trial, w.cur->g, w.p, ts));
         res->ls_evaluations++;
+        trials++;
         dphi_a = ts[SC_PCG];                                       // phi'(alpha)
-        const double dval = (ts[SC_MASS] - mass) - alpha * ts[SC_PRC];
+        dval = (ts[SC_MASS] - mass) - alpha * ts[SC_PRC];
         const int wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
         const int decrease = dval <= noise * std::max(1.0, mass);
         if (wolfe && decrease) { accepted = 1; break; }
@@ -461,12 +464,21 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
       res->ls_restarts++;
       dphi0 = -dg;
       alpha = 1.0;
+      beta = 0.0;
+      reset = 1;
       if (attempt < 2) CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, 0.0, dir, nullptr, nullptr));
     }
     if (!accepted) {
       set_error("line search failed twice at MD step %d, iteration %lld", t, (long long)k);
       st = MDOT_ELINESEARCH;
       break;
+    }
+    if (w.trace_cap) {
+      mdot_trace_rec q{};
+      q.t = t; q.k = (int32_t)k; q.l1 = sc[SC_L1]; q.rho = sc[SC_RHO];
+      q.alpha = alpha; q.dphi0 = dphi0; q.dphi_alpha = dphi_a; q.dphi_value = dval;
+      q.trials = trials; q.reset = reset; q.beta = beta; q.gs = S_sg;
+      w.trace_add(q);
     }
     // accept (Alg. 2 lines 11-13): the trial becomes the iterate
     std::swap(w.u, w.tu);
@@ -628,6 +640,30 @@ mdot_status Workspace::build_graph() {
   return MDOT_OK;
 }
 
+void Workspace::ctrl_trace_setup(CtrlState& h, int t) {
+  h.md_t = t;
+  h.trace = nullptr; h.trace_len = nullptr; h.trace_cap = 0;
+  if (!trace_cap || !trace_dev) return;
+  h.trace = trace_dev;
+  h.trace_len = trace_len_dev;
+  h.trace_cap = std::max<int64_t>(0, std::min<int64_t>(trace_cap - (int64_t)trace_host.size(), kTraceDevCap));
+  cudaMemsetAsync(trace_len_dev, 0, sizeof(long long), st);
+}
+
+mdot_status Workspace::ctrl_trace_collect() {
+  if (!trace_cap || !trace_dev) return MDOT_OK;
+  long long len = 0;
+  CK(cudaMemcpyAsync(&len, trace_len_dev, sizeof(len), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (len <= 0) return MDOT_OK;
+  const size_t old = trace_host.size();
+  trace_host.resize(old + (size_t)len);
+  CK(cudaMemcpyAsync(trace_host.data() + old, trace_dev, sizeof(mdot_trace_rec) * (size_t)len,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return MDOT_OK;
+}
+
 mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
   CtrlState h{};
   h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
@@ -637,6 +673,7 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
   h.max_evals = o.max_evals - w.evals;
   h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+  w.ctrl_trace_setup(h, t);
   res->control_path = 1;
   CKS(w.build_graph());
   cudaStream_t st = w.st;
@@ -678,6 +715,7 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
   }
   CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  CKS(w.ctrl_trace_collect());
   w.evals += h.evals;
   res->iterations += h.iterations;
   res->ls_evaluations += h.ls_evals;
@@ -711,7 +749,7 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
 // ---------------------------------------------------------------------------
 // Persistent projection: prepare the control state and the kernel arguments,
 // launch, collect the controller's result.
-static mdot_status persist_prepare(Workspace& w, const mdot_options& o, PersistArgs& a) {
+static mdot_status persist_prepare(Workspace& w, const mdot_options& o, int t, PersistArgs& a) {
   CtrlState h{};
   h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
   h.noise = 6e-8;
@@ -720,6 +758,7 @@ static mdot_status persist_prepare(Workspace& w, const mdot_options& o, PersistA
   h.max_evals = o.max_evals - w.evals;
   h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+  w.ctrl_trace_setup(h, t);
   cudaStream_t st = w.st;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.pers_bar, 0, 2 * sizeof(unsigned int) + 14 * sizeof(unsigned long long) + 8, st));
@@ -822,6 +861,7 @@ static mdot_status persist_collect(Workspace& w, const mdot_options& o, int t, m
   CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(k1, a.k1_ns, sizeof(k1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  CKS(w.ctrl_trace_collect());
   if (w.time_kernels && k1[1]) {
     w.kernel_ms += (double)k1[0] * 1e-6;
     w.kernel_launches += (int64_t)k1[1];
@@ -861,7 +901,7 @@ static mdot_status persist_collect(Workspace& w, const mdot_options& o, int t, m
 mdot_status project_persistent(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
   res->control_path = 2;
   PersistArgs a;
-  CKS(persist_prepare(w, o, a));
+  CKS(persist_prepare(w, o, t, a));
   if (w.sharded()) {
     // row-sharded: column exchange fused into the kernel over peer memory
     CKS(comm_peer_persist(w.comm, a, w.tmap, w.pers_grid, w.st));
@@ -901,6 +941,11 @@ mdot_status build_schedule(const mdot_schedule* s, std::vector<double>& g) {
       gb += next;
       if (g.size() > 4096) { set_error("doubling schedule too long"); return MDOT_EINVAL; }
     }
+  } else if (s->kind == MDOT_SCHED_ADAPTIVE) {
+    // only the first step is known up front (Z29); solve_impl / K8 choose the rest
+    if (!(s->gamma_bar > 0) || !isfinite(s->gamma_bar)) { set_error("gamma_bar must be > 0"); return MDOT_EINVAL; }
+    const double g1 = s->step_max > 0 ? s->step_max : 256.0;
+    g.assign(1, std::min(g1, s->gamma_bar));
   } else {
     set_error("unknown schedule kind %d", s->kind);
     return MDOT_EINVAL;
@@ -1069,8 +1114,20 @@ void Workspace::free_owned() {
   owned_C = nullptr; owned_X = owned_Y = nullptr;
 }
 
+void apply_fault_env() {
+  static int last = 0;
+  const char* e = getenv("MDOT_FAULT_NAN");
+  const int mode = e ? atoi(e) : 0;
+  if (mode == last && mode == 0) return;
+  fault_set_kernels(mode);
+  fault_set_persist(mode);
+  fault_set_batch(mode);
+  last = mode;
+}
+
 mdot_status Workspace::setup(const mdot_options& o) {
   set_smem_carveout();
+  apply_fault_env();
   time_kernels = o.time_kernels;
   if (time_kernels) {
     CK(cudaEventCreate(&ev0));
@@ -1244,6 +1301,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   std::vector<double> gam;
   mdot_status st = build_schedule(sched, gam);
   if (st != MDOT_OK) { res->status = st; return st; }
+  const bool adaptive = sched->kind == MDOT_SCHED_ADAPTIVE;
   cudaStream_t stream = (cudaStream_t)o.stream;
   const int64_t n = pb->n;
   const int64_t nr = nrows_in < 0 ? n : nrows_in;
@@ -1269,6 +1327,16 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     tr_last = now;
   };
   st = w.alloc(stream, n, nr);
+  if (st == MDOT_OK && o.trace && o.trace_cap > 0) {
+    w.trace_cap = o.trace_cap;
+    const size_t recs = (size_t)std::min<int64_t>(o.trace_cap, kTraceDevCap);
+    if (cudaMallocAsync((void**)&w.trace_dev, recs * sizeof(mdot_trace_rec) + 64, stream) != cudaSuccess) {
+      set_error("trace buffer allocation failed");
+      st = MDOT_ENOMEM;
+    } else {
+      w.trace_len_dev = reinterpret_cast<long long*>(reinterpret_cast<char*>(w.trace_dev) + recs * sizeof(mdot_trace_rec));
+    }
+  }
   trace_mark("alloc", 0, 0);
   if (st == MDOT_OK) st = w.load_problem(pb, row0);
   trace_mark("load", 0, 0);
@@ -1287,9 +1355,15 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     ++w.launches; launch_fill(nr, 0.0, w.u, stream);
     ++w.launches; launch_fill(n, 0.0, w.v, stream);
     double gb = 0.0, gprev = 0.0;
-    for (size_t t = 1; t <= gam.size(); ++t) {
-      const double gt = gam[t - 1];
-      gb += gt;
+    // ADAPTIVE (Z29): steps chosen after each projection from its cost
+    double next = adaptive ? gam[0] : 0.0, eta_prev = 0.0;
+    int final_next = adaptive && gam[0] >= sched->gamma_bar;
+    for (size_t t = 1; adaptive || t <= gam.size(); ++t) {
+      const double gt = adaptive ? next : gam[t - 1];
+      const bool last = adaptive ? final_next != 0 : t == gam.size();
+      gb = (adaptive && last) ? sched->gamma_bar : gb + gt;   // the last adaptive step lands on gamma_bar exactly
+      if (t <= 64) res->gammas[t - 1] = gt;
+      const int64_t evals_before = w.evals;
       w.set_gamma(gb);
       if (o.warm == MDOT_WARM_ZERO) {
         ++w.launches; launch_fill(nr, 0.0, w.u, stream);
@@ -1300,7 +1374,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       }
       // intermediate MD steps may stop at the looser eps_md (Lemma 2; mdot.h)
       mdot_options ot = o;
-      if (t < gam.size() && o.eps_md > o.eps) ot.eps = o.eps_md;
+      if (!last && o.eps_md > o.eps) ot.eps = o.eps_md;
       if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, ot, (int)t, res);
       else if (o.device_control && !(w.sharded() && (w.exact_mode || !comm->capturable())))
         solve_st = project_device(w, ot, (int)t, res);
@@ -1316,7 +1390,10 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       if (st != MDOT_OK) break;
       gprev = gt;
       trace_mark("step-end", (long long)t, 0);
-      if (solve_st != MDOT_OK) break;
+      if (solve_st != MDOT_OK || (adaptive && last)) break;
+      if (adaptive)
+        next = adaptive_next_gamma((int)t, gt, (double)(w.evals - evals_before), gb, sched->gamma_bar, &eta_prev,
+                                   &final_next);
     }
     res->gamma_bar = gb;
     if (st == MDOT_OK && (solve_st == MDOT_OK || solve_st == MDOT_ENOCONV)) {
@@ -1339,6 +1416,11 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * n, k, stream);
   }
   if (st == MDOT_OK) st = w.l2_reset();
+  if (o.trace && o.trace_cap > 0) {
+    const int64_t len = std::min<int64_t>((int64_t)w.trace_host.size(), o.trace_cap);
+    if (len > 0) memcpy(o.trace, w.trace_host.data(), sizeof(mdot_trace_rec) * (size_t)len);
+    if (o.trace_len) *o.trace_len = len;
+  }
   res->evaluations = w.evals;
   res->fallbacks = w.fallbacks;
   res->kernel_ms = w.kernel_ms;
@@ -1577,6 +1659,18 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   a.C = c64 ? nullptr : (const float*)dC;
   a.C64 = c64 ? (const double*)dC : nullptr;
   a.n = (int)n; a.r = dr; a.c = dc; a.gammas = dg; a.T = (int)gam.size();
+  a.adaptive = sched->kind == MDOT_SCHED_ADAPTIVE;
+  a.gamma_bar = sched->gamma_bar;
+  a.gamma1 = gam[0];
+  mdot_trace_rec* dtrace = nullptr;
+  if (o.trace && o.trace_cap > 0) {
+    const size_t recs = (size_t)std::min<int64_t>(o.trace_cap, kTraceDevCap);
+    CK(cudaMallocAsync((void**)&dtrace, recs * sizeof(mdot_trace_rec) + 64, stream));
+    a.trace = dtrace;
+    a.trace_cap = (long long)recs;
+    a.trace_len = reinterpret_cast<long long*>(reinterpret_cast<char*>(dtrace) + recs * sizeof(mdot_trace_rec));
+    CK(cudaMemsetAsync(a.trace_len, 0, sizeof(long long), stream));
+  }
   a.eps = o.eps; a.eps_md = o.eps_md > o.eps ? o.eps_md : o.eps; a.c1 = o.c1; a.c2 = o.c2;
   a.stop_rho = o.stop; a.projector = o.projector; a.beta_kind = o.beta; a.ls_max_trials = o.ls_max_trials;
   a.warm = o.warm; a.p0_ones = o.p0_ones;
@@ -1590,6 +1684,7 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     cudaMemsetAsync(kdbg, 0, 8 * sizeof(unsigned long long), stream);
     a.dbg = kdbg;
   }
+  apply_fault_env();
   cudaError_t e = launch_batch(a, Bn, stream);
   if (e != cudaSuccess) {
     cudaFreeAsync(base, stream);
@@ -1603,6 +1698,15 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   }
   std::vector<BatchResult> hres(Bn);
   CK(cudaMemcpyAsync(hres.data(), dres, sizeof(BatchResult) * Bn, cudaMemcpyDeviceToHost, stream));
+  if (dtrace) {
+    long long len = 0;
+    CK(cudaMemcpyAsync(&len, a.trace_len, sizeof(len), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    len = std::min<long long>(len, (long long)o.trace_cap);
+    if (len > 0)
+      CK(cudaMemcpyAsync(o.trace, dtrace, sizeof(mdot_trace_rec) * (size_t)len, cudaMemcpyDeviceToHost, stream));
+    if (o.trace_len) *o.trace_len = len;
+  }
   const cudaMemcpyKind k = dev_mem ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (u_out) CK(cudaMemcpyAsync(u_out, dU, vb, k, stream));
   if (v_out) CK(cudaMemcpyAsync(v_out, dV, vb, k, stream));
@@ -1617,6 +1721,7 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     cudaFree(kdbg);
   }
   cudaFreeAsync(base, stream);
+  if (dtrace) cudaFreeAsync(dtrace, stream);
   const double secs = now_s() - t0;
   mdot_status first = MDOT_OK;
   for (int32_t b = 0; b < Bn; ++b) {
@@ -1640,6 +1745,7 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
       R.rho0[q] = h.rho0[q];
       R.l10[q] = h.l10[q];
       R.iters_step[q] = h.iters_step[q];
+      R.gammas[q] = h.gammas[q];
     }
     R.all_launches = 1;
     if (h.status != MDOT_OK && first == MDOT_OK) {

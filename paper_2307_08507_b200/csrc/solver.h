@@ -86,6 +86,18 @@ struct Workspace {
   cudaEvent_t gev[2 * 65] = {};
   bool gev_made = false;
 
+  // per-iteration trace (mdot_options.trace): host records in order; device
+  // control paths write into trace_dev and are appended after each projection
+  int64_t trace_cap = 0;            // 0 = off
+  std::vector<mdot_trace_rec> trace_host;
+  mdot_trace_rec* trace_dev = nullptr;
+  long long* trace_len_dev = nullptr;
+  void trace_add(const mdot_trace_rec& q) {
+    if ((int64_t)trace_host.size() < trace_cap) trace_host.push_back(q);
+  }
+  void ctrl_trace_setup(CtrlState& h, int t);   // device controller: buffer + counter for this projection
+  mdot_status ctrl_trace_collect();              // append the projection's device records
+
   ~Workspace() {   // error paths: release() and free_owned() are idempotent
     free_owned();
     release();

@@ -36,6 +36,10 @@ CASES = {
                          "BASELINE config 3: n=4096, H(r)/log n = 0.99, FIXED gbar 4096 T 16, L1 1e-6"),
     "cfg3_h0.5_gb512_T4_seed1": (lambda: S.config3(1, frac=0.5), 512.0, 4, 1e-6,
                                  "BASELINE config 3 secondary: n=4096, H/log n = 0.5, FIXED gbar 512 T 4, L1 1e-6"),
+    "cfg2_s0_p0_eps1e-8": (lambda: S.config2_pair(0, 0), 4096.0, 16, 1e-8,
+                           "BASELINE config 2: n=784 28x28 grid, blob pair 0 of seed 0, FIXED gbar 4096 T 16, L1 1e-8"),
+    "cfg2_s0_p1_eps1e-8": (lambda: S.config2_pair(0, 1), 4096.0, 16, 1e-8,
+                           "BASELINE config 2: n=784 28x28 grid, blob pair 1 of seed 0, FIXED gbar 4096 T 16, L1 1e-8"),
 }
 
 

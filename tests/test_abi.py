@@ -73,7 +73,7 @@ def test_defaults_and_host_side_validation(L):
     # NULL problem is rejected before any CUDA call
     st = L.mdot_solve(None, ct.byref(s), ct.byref(o), None, None, None, ct.byref(res))
     assert st == 1 and "NULL" in M.mdot_last_error()
-    assert L.mdot_abi_version() == 2
+    assert L.mdot_abi_version() == 3
 
 
 def test_binding_rejects_wrong_dtypes_before_any_call(L):

@@ -67,6 +67,12 @@ def parse():
                     help="tolerance of the intermediate MD steps (0 = eps at every step, the paper's protocol)")
     ap.add_argument("--sharded-selftest", action="store_true",
                     help="run the multi-GPU code path on one rank (1-rank NCCL communicator; tests only)")
+    ap.add_argument("--no-config5", action="store_true",
+                    help="skip the config-5 block (n=65536, d=16, on-the-fly cost; north_star scaling target)")
+    ap.add_argument("--c5-evals", type=int, default=48,
+                    help="config-5 step = the first K O(n^2) evaluations of the config-5 solve (fixed budget)")
+    ap.add_argument("--c5-full", type=int, default=1,
+                    help="also time one complete config-5 solve to L1 1e-5 (time-to-eps; ~10 s on one B200)")
     ap.add_argument("--adaptive-leg", type=float, default=1e-3,
                     help="also time the solve with this eps_md (SURVEY 8(f) rank 1), reported under "
                          "'adaptive_eps'; 0 disables")
@@ -392,6 +398,8 @@ def run_ours(a, rank, world, local_rank):
             "status_name": ra[-1]["status_name"],
             "note": "intermediate MD steps stop at eps_md, the last at eps; Lemma 2 (PAPER.md:152-155) makes "
                     "the final plan independent of the intermediate accuracy"}
+    if not a.no_config5:
+        line["config5"] = run_config5(a, rank, world, dev, M, dist, comm, barrier)
     # end-to-end through the C ABI with host buffers (rank 0, 1 GPU)
     if not sharded and not a.no_e2e:
         import synthetic as S
@@ -460,6 +468,121 @@ def run_ours(a, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_config5(a, rank, world, dev, M, dist, comm, barrier):
+    """BASELINE configs[4] -- the north_star scaling target (n = 65536, X, Y ~
+    U[0,1]^16, C_ij = ||x_i - y_j||^2 / 16 computed in-kernel (K2, Z22),
+    Dirichlet(1), FIXED gbar 4096 (T = 16), L1 1e-5), rows of X sharded over
+    the ranks with one NCCL allreduce of [column totals | row scalars] per
+    evaluation.  A step is the first --c5-evals O(n^2)
+    evaluations of the solve (fixed budget, so the driver's 20 steps fit);
+    the complete solve is timed once more for time-to-eps.  Roofline: K2 is
+    bound by the FP32 pipe (2d + 5 = 37 FP32 ops per pair, K2), peak
+    = 148 SMs x 128 FP32 lanes x 1.965 GHz / 37 (B200_PROFILING.md unit counts);
+    the MUFU floor (1 ex2 per pair, 16 per SM per clock) is reported beside it."""
+    import numpy as np
+    import torch
+
+    import synthetic as S
+    inst = S.config5(0)
+    n, d = inst.n, inst.X.shape[1]
+    rows = np.array_split(np.arange(n), world)[rank]
+    row0, nloc = int(rows[0]), len(rows)
+    X = torch.from_numpy(np.ascontiguousarray(inst.X[row0:row0 + nloc])).to(dev)
+    Y = torch.from_numpy(inst.Y).to(dev)
+    r = torch.from_numpy(inst.r).to(dev)
+    c = torch.from_numpy(inst.c).to(dev)
+    U = torch.empty(nloc, dtype=torch.float64, device=dev)
+    V = torch.empty(n, dtype=torch.float64, device=dev)
+    gb, eps = 4096.0, 1e-5
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb)
+
+    def solve(max_evals):
+        o = M.options(eps=eps, time_kernels=1, max_evals=max_evals)
+        if comm is not None:
+            return M.mdot_solve_sharded(comm, row0, nloc, X_local=X, Y=Y, scale=inst.scale, r=r, c=c, n=n,
+                                        schedule=sched, options=o, u_local_out=U, v_out=V, check=False)
+        return M.mdot_solve(X=X, Y=Y, scale=inst.scale, r=r, c=c, schedule=sched, options=o, u_out=U, v_out=V,
+                            check=False)
+
+    def maxr(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    K = a.c5_evals
+    solve(K)
+    barrier()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    res = []
+    barrier()
+    e0.record(st)
+    for _ in range(a.steps):
+        res.append(solve(K))
+    e1.record(st)
+    barrier()
+    ms = maxr(e0.elapsed_time(e1))
+    ev = sum(x["evaluations"] for x in res)
+    kms = sum(x["kernel_ms"] for x in res)
+    kn = sum(x["kernel_launches"] for x in res)
+    pairs_per_eval = float(n) * n
+    launch_s = kms / kn / 1000.0 if kn else float("nan")
+    achieved = float(nloc) * n / launch_s if kn else None
+    if dist is not None and achieved is not None:
+        t = torch.tensor([achieved], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        achieved = float(t.item())
+    fp32_peak = world * 148 * 128 * 1.965e9 / (2 * d + 5)
+    mufu_peak = world * 148 * 16 * 1.965e9
+    out = {
+        "workload": f"cfg5-otf-n{n}-d{d}-dirichlet1-gbar4096-T16-L1eps1e-05",
+        "step": f"first {K} O(n^2) evaluations of the solve (fixed budget per step)",
+        "parallelism": f"rows of X sharded x{world}" if world > 1 else "1 GPU",
+        "exchange": "NCCL allreduce of [column totals | row scalars] per evaluation in CUDA-graph slots"
+                    if world > 1 else None,
+        "steps": a.steps, "ms_per_step": ms / a.steps,
+        "evals_per_s": ev / (ms / 1000.0), "pairs_per_s": ev * pairs_per_eval / (ms / 1000.0),
+        "roofline": {"kernel": "k_eval_otf<16> (K2: on-the-fly cost, fused marginals)", "bound": "alu",
+                     "achieved": achieved / 1e9 if achieved else None, "unit": "Gpairs/s",
+                     "peak": fp32_peak / 1e9, "frac": (achieved / fp32_peak) if achieved else None,
+                     "peak_source": "FP32 pipe: 148 SMs x 128 lanes x 1.965 GHz / (2d+5 = 37 ops per pair)",
+                     "mufu_floor_frac": (achieved / mufu_peak) if achieved else None,
+                     "mean_launch_ms": launch_s * 1e3, "launches_timed": kn,
+                     "traffic": None},
+        "status_name": res[-1]["status_name"],
+    }
+    if a.c5_full:
+        solve(0)   # warm the full path once (graph capture, L2)
+        barrier()
+        e0.record(st)
+        full = solve(0)
+        e1.record(st)
+        barrier()
+        ms_full = maxr(e0.elapsed_time(e1))
+        out["time_to_eps_s"] = ms_full / 1000.0
+        out["full_solve"] = {k: full[k] for k in ("evaluations", "iterations", "md_steps", "l1_final",
+                                                   "cost_unrounded", "cost_rounded", "status_name")}
+        out["full_solve"]["evals_per_s"] = full["evaluations"] / (ms_full / 1000.0)
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        # the oracle's pair rate on this host: exact fp64 log-marginals of 32
+        # sampled rows of the same instance at the same potentials (O(n d) each)
+        import oracle as O
+        prob = O.OracleProblem(inst)
+        rows_s = np.arange(0, n, n // 32)[:32]
+        A0, B0 = np.log(inst.r), np.log(inst.c)
+        t0 = time.perf_counter()
+        O.log_marginal_subset(prob, A0, B0, gb, rows=rows_s)
+        dt = time.perf_counter() - t0
+        cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+        out["cpu_baseline"] = {"value": len(rows_s) * n / dt, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+                               "sample": f"oracle log-sum-exp of {len(rows_s)} rows x {n} columns (2 passes), "
+                                         f"{dt:.2f} s wall"}
+    return out
 
 
 def main():

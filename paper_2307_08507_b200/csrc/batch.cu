@@ -622,6 +622,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   fa.gcur = cg; fa.pcur = p;
   fa.lm = tl; fa.m = nullptr; fa.s = ts; fa.g = tg;
   fa.jacobi = a.projector == MDOT_PROJ_PNCG_JACOBI;
+  fa.fault_repl = CL;   // every CTA of the cluster finalizes every item (identical decisions)
 
   long long evals_total = 0, iters = 0, ls_evals = 0, resets = 0, restarts = 0;
   int status = 0;

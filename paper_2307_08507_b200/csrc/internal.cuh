@@ -165,6 +165,7 @@ struct FinalizeArgs {
   int cols_local_only;   // sharded: 1 -> column items produce raw partial sums (no log) ... (unused)
   int jacobi;            // 1: s = grad / diag(Hessian) (MDOT_PROJ_PNCG_JACOBI) instead of the Sinkhorn direction
   int f64_entries;       // partials from fp64 entries (K8): range guard at the fp64 limits, not fp32's
+  int fault_repl;        // MDOT_FAULT_NAN=1 hook: copies of item 0 finalized per evaluation (K8 cluster: CL)
   double f64_tot_min;    // fp64 entries: totals below this (anchored units) are redone exactly -- the
                          // bound on the mass K8's entry skip may have dropped (batch.cu); 0 = 1e-300
 };

@@ -175,7 +175,9 @@ __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, 
                                               double (&v)[kNumScalars]) {
   const bool is_row = k < a.nrows;
     double lm, bad = 0.0;
-    if (c_fault_nan == 1 && k == 0 && a.from_partials == 1 && atomicAdd(&g_fault_hits, 1u) == 0u) tot = __longlong_as_double(0x7ff8000000000000ll);
+    if (c_fault_nan == 1 && k == 0 && a.from_partials == 1 &&
+        atomicAdd(&g_fault_hits, 1u) < (unsigned)(a.fault_repl > 1 ? a.fault_repl : 1))
+      tot = __longlong_as_double(0x7ff8000000000000ll);
     if (a.from_partials == 1) {
       const double anchor = is_row ? a.rho_r[k] : a.sig_c[k - a.nrows];
       lm = log(tot) + anchor * LN2_D;

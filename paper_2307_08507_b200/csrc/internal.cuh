@@ -321,24 +321,47 @@ cudaError_t launch_exact_colcombine(const double* colm, const double* cols, int 
 cudaError_t launch_rescale_to_max(int64_t n, const double* Mloc, const double* Mglob, double* S, cudaStream_t st);
 cudaError_t launch_sum_chunks(const double* x, int chunks, int64_t n, double* out, cudaStream_t st);
 
-// rounding (fp64, once per solve)
+// rounding (fp64, once per solve; round.cu).  Altschuler et al. Alg. 2 as
+// restated in SPEC.md:331 in three passes over the cost:
+//   R0 rows:    r(F)_i, sum_j C_ij F_ij            F   = exp(U + V - gbar C)
+//   R2 columns: c(F')_j                            F'  = D(x) F, x = min(r / r(F), 1)
+//   R3 rows:    r(F'')_i, sum_j C F'', sum_j C_ij err_c_j   F'' = F' D(y)
+// Entries below e^-50 of their pass's target marginal (r_i for row passes,
+// c_j for the column pass) are not exponentiated: each is < 2e-22 of that
+// target, so a pass drops < n * 2e-22 of total mass (1.3e-17 at n = 65536).
 struct RoundArgs {
   const void* C; int64_t ldc; int c_f64;
   const float* X; const float* Y; int d; float scale; int otf;
   int64_t n, nrows;
-  const double* A;      // rows: U + log x
-  const double* B;      // cols: V (R2) or V + log y (R3, plan)
-  const double* invx;   // rows: 1/x
   double gbar;
-  double* colF1; double* colcost; int chunks;   // R2 partials [chunks][n]
-  const double* ec;     // err_c [n]
-  double* er;           // err_r [nrows]
-  double* rowF2; double* rowcost2; double* rowcorr;
-  float* plan; double inv_ner;
+  const double* A;      // row exponent base of the pass (U or U + log x)
+  const double* B;      // column exponent base of the pass (V or V + log y)
+  const double* logr;   // [nrows] skip thresholds (log targets)
+  const double* logc;   // [n]
+  const double* ec;     // R3: err_c [n]
+  int chunks;           // partial chunks: column chunks of a row pass / row chunks of the column pass
+  double* rowS;         // [chunks][nrows] sum of entries
+  double* rowC;         // [chunks][nrows] sum C * entry
+  double* rowE;         // [chunks][nrows] sum_j C_ij err_c_j (R3)
+  double* colS;         // [chunks][n] column sums (R2)
+  // plan output
+  const double* er; float* plan; double inv_ner;
 };
-cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
-                              double* logx, double* Aout, cudaStream_t st);
-cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t st);
+constexpr int kRoundMaxChunks = 8;
+int round_chunks(const RoundArgs& a, bool rows);           // chunks a pass launches with (<= kRoundMaxChunks)
+cudaError_t launch_round_rows(const RoundArgs& a, int with_corr, cudaStream_t st);   // R0 / R3
+cudaError_t launch_round_cols(const RoundArgs& a, cudaStream_t st);                  // R2
+cudaError_t launch_round_plan(const RoundArgs& a, cudaStream_t st);
+// x from R0's row sums: logx = min(log r - log r(F), 0), Aout = U + logx, rowcostF = sum of R0's C F chunks
+cudaError_t launch_round_x(int64_t nrows, int chunks, const double* rowS, const double* rowC, const double* r,
+                           const double* U, double* logx, double* Aout, double* rowcostF, cudaStream_t st);
+// y from R2's column sums (chunks): Bout = V + log y, ec = max(c - y c(F'), 0)
+cudaError_t launch_round_y(int64_t n, int chunks, const double* colS, const double* c, const double* V,
+                           double* Bout, double* ec, cudaStream_t st);
+// err_r = max(r - r(F''), 0); scalars [|err_r|_1, <C,F''>, err_r . (C err_c), <C,F>] published
+cudaError_t launch_round_fin(int64_t nrows, int chunks, const double* rowS, const double* rowC, const double* rowE,
+                             const double* rowcostF, const double* r, double* er, double* blockpart,
+                             unsigned int* ticket, double* out_dev, double* out_host, cudaStream_t st);
 // L2 lines of [p, p + bytes) back to evict_normal priority (K1 reads part or
 // all of C with evict_last; the caller's later kernels must not inherit it)
 cudaError_t launch_l2_normal(const void* p, size_t bytes, cudaStream_t st);

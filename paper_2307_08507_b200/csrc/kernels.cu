@@ -895,22 +895,6 @@ cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const do
   return cudaGetLastError();
 }
 
-// x_i = min(r_i / r_i(F), 1) in log form; A' = U + log x
-__global__ void k_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
-                             double* logx, double* Aout) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double lx = logr[i] - lr[i];
-  if (lx > 0.0) lx = 0.0;
-  logx[i] = lx;
-  Aout[i] = U[i] + lx;
-}
-cudaError_t launch_round_rows(int64_t n, const double* logr, const double* lr, const double* U,
-                              double* logx, double* Aout, cudaStream_t st) {
-  k_round_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, logr, lr, U, logx, Aout);
-  return cudaGetLastError();
-}
-
 // Sampled input check (C in [0, 1]): 64 entries at a fixed
 // hash of the index gathered by one launch into a mapped host buffer (one
 // synchronisation instead of one device-to-host copy per sample).
@@ -974,159 +958,6 @@ cudaError_t launch_sum_chunks(const double* x, int chunks, int64_t n, double* ou
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// Rounding onto U(r,c) (Altschuler et al. Alg. 2 as restated in
-// SPEC.md:331) in fp64 -- once per solve, so the entries are recomputed in
-// fp64 with exp() instead of the fp32 streaming path.
-//   F = exp(U + V - gbar C) (final plan),  x = min(r / r(F), 1)
-//   R2 (columns): c(F')_j = sum_i x_i F_ij ;  sum_i C_ij F_ij (cost of F)
-//   y = min(c / c(F'), 1); F'' = D(x) F D(y); err_c = c - y * c(F')
-//   R3 (rows):    r(F'')_i, sum_j C_ij F''_ij, sum_j C_ij err_c_j
-//   <C,G> = <C,F''> + err_r^T C err_c / |err_r|_1
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double round_cost(const RoundArgs& a, int64_t i, int64_t j) {
-  if (a.otf) {
-    const float* x = a.X + i * a.d;
-    const float* y = a.Y + j * a.d;
-    float acc = 0.f;
-    for (int k = 0; k < a.d; ++k) {
-      const float dk = __fsub_rn(x[k], y[k]);
-      acc = __fmaf_rn(dk, dk, acc);
-    }
-    return (double)__fmul_rn(acc, a.scale);
-  }
-  if (a.c_f64) return reinterpret_cast<const double*>(a.C)[i * a.ldc + j];
-  return (double)reinterpret_cast<const float*>(a.C)[i * a.ldc + j];
-}
-
-__global__ void k_round_cols(RoundArgs a) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int chunk = blockIdx.y;
-  const int64_t rows_per = (a.nrows + a.chunks - 1) / a.chunks;
-  const int64_t ib = chunk * rows_per;
-  const int64_t ie = (ib + rows_per < a.nrows) ? ib + rows_per : a.nrows;
-  if (j >= a.n) return;
-  const double Bj = a.B[j];
-  double s1 = 0.0, s2 = 0.0;
-  for (int64_t i = ib; i < ie; ++i) {
-    const double cij = round_cost(a, i, j);
-    const double f1 = exp((a.A[i] + Bj) - a.gbar * cij);   // F'_ij = x_i F_ij
-    s1 += f1;
-    s2 += cij * f1 * a.invx[i];                               // C_ij F_ij
-  }
-  a.colF1[(int64_t)chunk * a.n + j] = s1;
-  a.colcost[(int64_t)chunk * a.n + j] = s2;
-}
-
-__global__ void k_round_rows3(RoundArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= a.nrows) return;
-  const double Ai = a.A[i];
-  double s = 0.0, cs = 0.0, cr = 0.0;
-  for (int64_t j = lane; j < a.n; j += 32) {
-    const double cij = round_cost(a, i, j);
-    const double f2 = exp((Ai + a.B[j]) - a.gbar * cij);   // F''_ij
-    s += f2;
-    cs += cij * f2;
-    cr += cij * a.ec[j];
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, off);
-    cs += __shfl_xor_sync(0xffffffffu, cs, off);
-    cr += __shfl_xor_sync(0xffffffffu, cr, off);
-  }
-  if (lane == 0) {
-    a.rowF2[i] = s;
-    a.rowcost2[i] = cs;
-    a.rowcorr[i] = cr;
-  }
-}
-
-__global__ void k_round_plan(RoundArgs a) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = blockIdx.y;
-  if (j >= a.n || i >= a.nrows) return;
-  const double cij = round_cost(a, i, j);
-  double gij = exp((a.A[i] + a.B[j]) - a.gbar * cij);
-  if (a.inv_ner > 0.0) gij += a.er[i] * a.ec[j] * a.inv_ner;
-  a.plan[i * a.n + j] = (float)gij;
-}
-
-// columns: c(F') total, y, B'' = V + log y, err_c; scalars: [cost_F, sum c(F'), 0, 0]
-__global__ void k_round_combine_cols(RoundArgs a, const double* c, const double* V, double* Bout,
-                                     double* ec, double* blockpart, unsigned int* ticket,
-                                     double* out_dev, double* out_host) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  if (j < a.n) {
-    double cf = 0.0, cc = 0.0;
-    for (int k = 0; k < a.chunks; ++k) {
-      cf += a.colF1[(int64_t)k * a.n + j];
-      cc += a.colcost[(int64_t)k * a.n + j];
-    }
-    const double y = fmin(c[j] / cf, 1.0);
-    Bout[j] = V[j] + log(y);
-    // c(F'') = y c(F') <= c in exact arithmetic; the clamp removes the
-    // last-bit sign flips of the fp64 product
-    ec[j] = fmax(c[j] - y * cf, 0.0);
-    v[0] = cc;
-    v[1] = cf;
-  }
-  block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, out_host);
-}
-
-// rows: err_r; scalars [|err_r|_1, <C,F''>, err_r . (C err_c), sum r(F'')]
-__global__ void k_round_combine_rows(RoundArgs a, const double* r, double* blockpart,
-                                     unsigned int* ticket, double* out_dev, double* out_host) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  if (i < a.nrows) {
-    // r(F'') <= x r(F) <= r in exact arithmetic (x from the fp64 r(F)); the
-    // clamp keeps G >= 0 against fp64 rounding of the row sums
-    const double er = fmax(r[i] - a.rowF2[i], 0.0);
-    a.er[i] = er;
-    v[0] = fabs(er);
-    v[1] = a.rowcost2[i];
-    v[2] = er * a.rowcorr[i];
-    v[3] = a.rowF2[i];
-  }
-  block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, out_host);
-}
-
-cudaError_t launch_round_cols(const RoundArgs& a, cudaStream_t st) {
-  dim3 grid((unsigned)((a.n + 255) / 256), a.chunks);
-  k_round_cols<<<grid, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-cudaError_t launch_round_rows3(const RoundArgs& a, cudaStream_t st) {
-  k_round_rows3<<<(unsigned)((a.nrows + 7) / 8), 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-cudaError_t launch_round_plan(const RoundArgs& a, cudaStream_t st) {
-  dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)a.nrows);
-  k_round_plan<<<grid, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-cudaError_t launch_round_combine_cols(const RoundArgs& a, const double* c, const double* V, double* Bout,
-                                      double* ec, double* blockpart, unsigned int* ticket,
-                                      double* out_dev, double* out_host, cudaStream_t st) {
-  k_round_combine_cols<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a, c, V, Bout, ec, blockpart,
-                                                                      ticket, out_dev, out_host);
-  return cudaGetLastError();
-}
-cudaError_t launch_round_combine_rows(const RoundArgs& a, const double* r, double* blockpart,
-                                      unsigned int* ticket, double* out_dev, double* out_host,
-                                      cudaStream_t st) {
-  k_round_combine_rows<<<(unsigned)((a.nrows + 255) / 256), 256, 0, st>>>(a, r, blockpart, ticket,
-                                                                          out_dev, out_host);
-  return cudaGetLastError();
-}
-
-__global__ void k_exp_neg(int64_t n, const double* x, double* y) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) y[i] = exp(-x[i]);
-}
 __global__ void k_l2_normal(const char* p, size_t lines) {
   for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < lines; q += (size_t)gridDim.x * blockDim.x)
     asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p + 128 * q) : "memory");
@@ -1139,10 +970,6 @@ cudaError_t launch_l2_normal(const void* p, size_t bytes, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_exp_neg(int64_t n, const double* x, double* y, cudaStream_t st) {
-  k_exp_neg<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, x, y);
-  return cudaGetLastError();
-}
 
 void fault_set_kernels(int mode) { fault_set_tu(mode); }
 

@@ -1172,80 +1172,80 @@ mdot_status Workspace::gauge_center(double* X_, double* Y_) {
   return MDOT_OK;
 }
 
-// Rounding + cost, fp64 kernels.
+// Rounding + cost, fp64 kernels (round.cu):
+// R0 rows -> x (from an exact fp64 r(F): with x_i r_i(F) <= r_i the row error
+// err_r = r - r(F'') is >= 0 and G lies in U(r,c), Altschuler's precondition;
+// the last evaluation's fp32-entry marginals resolve r(F) only to ~1e-7),
+// R2 columns -> y, err_c, R3 rows -> err_r and the costs.  Sharded: column
+// sums and the final scalars are allreduced.
 mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* cost_G) {
-  // x = min(r / r(F), 1) from the current log marginals; A' = U + log x
-  double* logx = aux;
-  double* invx = aux + nrows;
-  double* Bpp = aux + 2 * nrows;
-  double* ec = aux + 2 * nrows + n;
-  double* er = aux + 2 * nrows + 2 * n;
-  double* rowF2 = aux + 3 * nrows + 2 * n;
-  double* rowcost2 = aux + 4 * nrows + 2 * n;
-  double* rowcorr = aux + 5 * nrows + 2 * n;
-  // x needs r(F) to fp64 accuracy: with x_i r_i(F) <= r_i the rounded plan's
-  // row error err_r = r - r(F'') is >= 0 and G = F'' + err_r err_c^T / |err_r|_1
-  // lies in U(r,c) (Altschuler's precondition).
-  // The fp32-entry evaluation resolves r(F) only to ~1e-7 relative, the same
-  // size as err_r near convergence, so those log marginals are recomputed
-  // here by one exact fp64 row pass (F = exp(U + V - gbar C); the last
-  // evaluation's marginals are used as they are when they are fp64 already).
-  const double* lrF = cur->lm;
-  if (!exact_mode) {
-    ExactArgs x{};
-    x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
-    x.X = Xdev; x.Y = Ydev; x.d = d; x.scale = scale; x.otf = otf;
-    x.n = n; x.nrows = nrows;
-    x.A = U; x.B = V; x.gbar = gbar;
-    x.lr = lr_ex;
-    CKL(launch_exact_rows(x, st));
-    lrF = lr_ex;
-  }
-  CKL(launch_round_rows(nrows, logr, lrF, U, logx, A, st));
-  CKL(launch_exp_neg(nrows, logx, invx, st));
   RoundArgs a{};
   a.C = Cdev; a.ldc = n; a.c_f64 = c_f64;
   a.X = Xdev; a.Y = Ydev; a.d = d; a.scale = scale; a.otf = otf;
-  a.n = n; a.nrows = nrows;
-  a.A = A; a.B = V; a.invx = invx; a.gbar = gbar;
-  a.colF1 = colm; a.colcost = cols; a.chunks = chunks;
-  a.ec = ec; a.er = er; a.rowF2 = rowF2; a.rowcost2 = rowcost2; a.rowcorr = rowcorr;
-  CKL(launch_round_cols(a, st));
-  if (sharded()) {
-    // column sums over this rank's rows -> global (one allreduce of 2n)
-    double* cs = aux + 6 * nrows + 2 * n;
-    CKL(launch_sum_chunks(colm, chunks, n, cs, st));
-    CKL(launch_sum_chunks(cols, chunks, n, cs + n, st));
-    CKS(comm_allreduce(comm, cs, 2 * (size_t)n, COMM_SUM, st));
-    a.colF1 = cs;
-    a.colcost = cs + n;
-    a.chunks = 1;
-  }
-  CKL(launch_round_combine_cols(a, c, V, Bpp, ec, blockpart, ticket, scal_dev, scal_host_dev, st));
-  CK(cudaStreamSynchronize(st));
-  const double cF = scal_host[0];
-  a.B = Bpp;
-  CKL(launch_round_rows3(a, st));
-  CKL(launch_round_combine_rows(a, r, blockpart, ticket, scal_dev, scal_host_dev, st));
-  double ner, cF2, corr;
-  if (sharded()) {
-    CKS(comm_allreduce(comm, scal_dev, 4, COMM_SUM, st));
-    double h4[4];
-    CK(cudaMemcpyAsync(h4, scal_dev, sizeof(h4), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    ner = h4[0]; cF2 = h4[1]; corr = h4[2];
-  } else {
-    CK(cudaStreamSynchronize(st));
-    ner = scal_host[0]; cF2 = scal_host[1]; corr = scal_host[2];
-  }
-  if (cost_F) *cost_F = cF;
-  if (cost_G) *cost_G = cF2 + (ner >= 1e-300 ? corr / ner : 0.0);
-  if (P_out_dev) {
-    a.plan = P_out_dev;
-    a.inv_ner = ner >= 1e-300 ? 1.0 / ner : 0.0;
-    CKL(launch_round_plan(a, st));
-  }
-  return MDOT_OK;
+  a.n = n; a.nrows = nrows; a.gbar = gbar;
+  a.logr = logr; a.logc = logc;
+  const int chr = round_chunks(a, true), chc = round_chunks(a, false);
+  const size_t dbl = (size_t)(4 + 3 * chr) * nrows + (size_t)(3 + chc) * n;
+  double* buf = nullptr;
+  CK(cudaMallocAsync((void**)&buf, dbl * sizeof(double), st));
+  double* logx = buf;
+  double* Ap = logx + nrows;
+  double* er = Ap + nrows;
+  double* rowcostF = er + nrows;
+  double* rowS = rowcostF + nrows;
+  double* rowC = rowS + (size_t)chr * nrows;
+  double* rowE = rowC + (size_t)chr * nrows;
+  double* Bpp = rowE + (size_t)chr * nrows;
+  double* ec = Bpp + n;
+  double* cs = ec + n;
+  double* colS = cs + n;
+  mdot_status stt = MDOT_OK;
+  auto run = [&]() -> mdot_status {
+    // R0: r(F), <C, F> per row
+    a.A = U; a.B = V; a.chunks = chr; a.rowS = rowS; a.rowC = rowC; a.rowE = rowE;
+    CKL(launch_round_rows(a, 0, st));
+    CKL(launch_round_x(nrows, chr, rowS, rowC, r, U, logx, Ap, rowcostF, st));
+    // R2: c(F') per column (partial over this rank's rows)
+    a.A = Ap; a.B = V; a.chunks = chc; a.colS = colS;
+    CKL(launch_round_cols(a, st));
+    const double* colsum = colS;
+    int colchunks = chc;
+    if (sharded()) {
+      CKL(launch_sum_chunks(colS, chc, n, cs, st));
+      CKS(comm_allreduce(comm, cs, (size_t)n, COMM_SUM, st));
+      colsum = cs;
+      colchunks = 1;
+    }
+    CKL(launch_round_y(n, colchunks, colsum, c, V, Bpp, ec, st));
+    // R3: r(F''), <C, F''>, C err_c per row
+    a.A = Ap; a.B = Bpp; a.ec = ec; a.chunks = chr;
+    CKL(launch_round_rows(a, 1, st));
+    CKL(launch_round_fin(nrows, chr, rowS, rowC, rowE, rowcostF, r, er, blockpart, ticket, scal_dev, scal_host_dev,
+                         st));
+    double ner, cF2, corr, cF;
+    if (sharded()) {
+      CKS(comm_allreduce(comm, scal_dev, 4, COMM_SUM, st));
+      double h4[4];
+      CK(cudaMemcpyAsync(h4, scal_dev, sizeof(h4), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ner = h4[0]; cF2 = h4[1]; corr = h4[2]; cF = h4[3];
+    } else {
+      CK(cudaStreamSynchronize(st));
+      ner = scal_host[0]; cF2 = scal_host[1]; corr = scal_host[2]; cF = scal_host[3];
+    }
+    if (cost_F) *cost_F = cF;
+    if (cost_G) *cost_G = cF2 + (ner >= 1e-300 ? corr / ner : 0.0);   // Z18
+    if (P_out_dev) {
+      a.A = Ap; a.B = Bpp; a.er = er; a.ec = ec;
+      a.plan = P_out_dev;
+      a.inv_ner = ner >= 1e-300 ? 1.0 / ner : 0.0;
+      CKL(launch_round_plan(a, st));
+    }
+    return MDOT_OK;
+  };
+  stt = run();
+  cudaFreeAsync(buf, st);
+  return stt;
 }
 
 }  // namespace mdot

@@ -76,12 +76,18 @@ __device__ __forceinline__ void block_sum(double (&v)[NS], double* scratch /*[kB
   __syncthreads();
 }
 
+struct BatchSmem;
+__host__ __device__ inline size_t batch_smem_bytes_d(int n);
 struct BatchSmem {
   // arrays of 2n doubles (rows then columns) follow in dynamic smem
   CtrlState st;
   double out[kNumScalars];
   double sred[kSredRows][kTileN];   // column partials of batch_eval; block_sum scratch otherwise
 };
+
+__host__ __device__ inline size_t batch_smem_bytes_d(int n) {
+  return sizeof(BatchSmem) + (size_t)15 * 2 * n * sizeof(double) + (size_t)2 * n * 16;
+}
 
 // Fused evaluation of one instance: rowtot[i] = sum_j 2^w T_j and
 // coltot[j] = sum_i 2^w S_i (anchored units, internal.cuh "K1 numerics").
@@ -192,6 +198,7 @@ __device__ void batch_eval_tail_packed(const float* __restrict__ C, int n, int j
   __syncthreads();
   if (threadIdx.x < 8 * Lp) {
     const int t = threadIdx.x;
+    MDOT_DCHECK(t < kTileN);
     double acc = 0.0;
 #pragma unroll
     for (int ww = 0; ww < kSredRows; ++ww) acc += sred[ww][t];
@@ -478,6 +485,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
         tot = bred4((double)rsf[0], (double)rsf[1], (double)rsf[2], (double)rsf[3], lane);
       }
       const int i = ib + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+      MDOT_DCHECK(i >= 0 && (i < n || i >= ib));
       if (!F64) tot *= (double)((lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]));
       if ((lane & 7) == 0 && i < n) rowtot[i] = (j0 == 0) ? tot : rowtot[i] + tot;
       if (!F64 && (step % MDOT_K1_COLFLUSH) == MDOT_K1_COLFLUSH - 1) {
@@ -570,6 +578,13 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BatchSmem& S = *reinterpret_cast<BatchSmem*>(smem_raw);
   const int n = a.n, n2 = 2 * a.n, tid = threadIdx.x;
+#ifdef MDOT_CHECKED
+  {  // the dynamic allocation must cover every vector of the instance
+    unsigned int dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    MDOT_DCHECK((size_t)dyn >= batch_smem_bytes_d(n));
+  }
+#endif
   // CL CTAs (a thread-block cluster) per instance; CL = 1 without a cluster launch
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
@@ -884,7 +899,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
   }
 }
 
-size_t batch_smem_bytes(int n) { return sizeof(BatchSmem) + (size_t)15 * 2 * n * sizeof(double) + (size_t)2 * n * 16; }
+size_t batch_smem_bytes(int n) { return batch_smem_bytes_d(n); }
 
 // CTAs per instance: split the rows of each instance over a thread-block
 // cluster while the batch leaves SMs idle (config 2: 64 instances on 148

@@ -3,10 +3,30 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/mdot.h"
 
 namespace mdot {
+
+// Checked builds (-DMDOT_CHECKED; tests/test_gpu_checked.py): device-side
+// bounds / invariant checks that trap, and guard bands around every
+// workspace sub-buffer verified when the call returns (solver.cu).  The
+// sanitizer is not available on this pool; these are the replacement.
+#ifdef MDOT_CHECKED
+#define MDOT_DCHECK(c)                                                              \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("MDOT_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                   \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define MDOT_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // Fused marginal evaluation (rounding K6/K7).

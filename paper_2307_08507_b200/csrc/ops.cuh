@@ -69,6 +69,7 @@ __device__ __forceinline__ float4 f64_param(double base, double anchor) {
 // state `c` (device control) overrides mode / alpha / beta and requests the
 // element-wise accept copy.
 __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const CtrlState* c) {
+  MDOT_DCHECK(k >= 0 && k < a.nrows + a.n);
   const bool is_row = k < a.nrows;
   const int64_t idx = is_row ? k : k - a.nrows;
   int mode = a.mode;
@@ -173,6 +174,7 @@ __device__ __forceinline__ double octet_partial(const double* x, int64_t stride,
 // (PAPER.md:236-239), and this item's contributions to the 16 scalars.
 __device__ __forceinline__ void finalize_item(const FinalizeArgs& a, int64_t k, double tot,
                                               double (&v)[kNumScalars]) {
+  MDOT_DCHECK(k >= 0 && k < a.nrows + a.n);
   const bool is_row = k < a.nrows;
     double lm, bad = 0.0;
     if (c_fault_nan == 1 && k == 0 && a.from_partials == 1 &&
@@ -243,6 +245,7 @@ __device__ inline void ctrl_finish(CtrlState* st, int status, int* done_host) {
 
 __device__ inline void ctrl_trace(CtrlState* st, double alpha, double dphi_a, double dval) {
   if (!st->trace || *st->trace_len >= st->trace_cap) return;
+  MDOT_DCHECK(*st->trace_len >= 0);
   mdot_trace_rec& q = st->trace[*st->trace_len];
   q.t = st->md_t; q.k = (int32_t)st->k;
   q.l1 = st->l1; q.rho = st->rho;

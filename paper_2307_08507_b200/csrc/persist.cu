@@ -327,6 +327,7 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
     const int64_t i_lo = (int64_t)cta * per;
     const int64_t i_hi = (i_lo + per < items) ? i_lo + per : items;
     const int cnt = i_hi > i_lo ? (int)(i_hi - i_lo) : 0;
+    MDOT_DCHECK(cnt <= kPersistMaxChunk);
     double* tots = fin + 256;   // [cnt]
     fin_totals(a.f, i_lo, cnt, tots);
     __syncthreads();
@@ -354,6 +355,7 @@ __device__ __forceinline__ void persist_body(const CUtensorMap& tmap, const Pers
       // fence, no flag -- a fence.sc.sys costs ~6 us per CTA here
       const int me = pg->rank, R = net->nranks;
       const int64_t ld = net->ld;
+      MDOT_DCHECK(me < R && R <= kMaxPeers && a.f.n + kNumScalars * (int64_t)ncta <= ld);
       const unsigned int ex = ++epoch;
       uint4* const* recv = reinterpret_cast<uint4* const*>(net->recv);
       const int64_t slot_off = ((int64_t)(ex & 1u) * R + me) * ld;

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kRT) k_round_rows_otf(RoundArgs a) {
     }
   }
   if (ok) {
+    MDOT_DCHECK((int)blockIdx.y < a.chunks && a.chunks <= kRoundMaxChunks);
     const int64_t o = (int64_t)blockIdx.y * a.nrows + i;
     a.rowS[o] = s;
     a.rowC[o] = cs;

@@ -160,7 +160,16 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   const int64_t fin_blocks = std::max<int64_t>((items * 8 + 255) / 256 + 8, 1024);   // k_finalize / persistent CTAs
 
   size_t dbl = 0;
-  auto take = [&](int64_t k) { size_t o = dbl; dbl += (size_t)((k + 31) / 32 * 32); return o; };
+  guards.clear();
+  auto take = [&](int64_t k) {
+    size_t o = dbl;
+    dbl += (size_t)((k + 31) / 32 * 32);
+#ifdef MDOT_CHECKED
+    guards.push_back(dbl);   // a guard band after every sub-buffer
+    dbl += kGuardDbl;
+#endif
+    return o;
+  };
   size_t o_r = take(nrows), o_c = take(n), o_logr = take(nrows), o_logc = take(n);
   size_t o_rho = take(nrows), o_sig = take(n);
   size_t o_U = take(nrows), o_V = take(n), o_u = take(nrows), o_v = take(n), o_tu = take(nrows), o_tv = take(n);
@@ -180,12 +189,20 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   size_t o_ctrl = take((int64_t)((sizeof(CtrlState) + 7) / 8));
   const size_t tickets = (size_t)eval.n_row_tiles + eval.n_col_tiles + 64;
   size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256 + tickets * 4;
+#ifdef MDOT_CHECKED
+  const size_t tail_guard = bytes;
+  bytes += kGuardDbl * sizeof(double);
+#endif
   cudaError_t e = cudaMallocAsync(&base, bytes, st);
   if (e != cudaSuccess) {
     set_error("workspace allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
     return MDOT_ENOMEM;
   }
   double* D = reinterpret_cast<double*>(base);
+#ifdef MDOT_CHECKED
+  guards.push_back(tail_guard / sizeof(double));
+  for (size_t g : guards) CK(cudaMemsetAsync(D + g, 0xA5, kGuardDbl * sizeof(double), st));
+#endif
   r = D + o_r; c = D + o_c; logr = D + o_logr; logc = D + o_logc; rho_r = D + o_rho; sig_c = D + o_sig;
   U = D + o_U; V = D + o_V; u = D + o_u; v = D + o_v; tu = D + o_tu; tv = D + o_tv;
   A = D + o_A; B = D + o_B; p = D + o_p; pprev = D + o_pp;
@@ -1092,6 +1109,25 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   return MDOT_OK;
 }
 
+// Checked builds: every guard band must still hold its 0xA5 fill.
+mdot_status Workspace::check_guards() {
+#ifdef MDOT_CHECKED
+  if (!base) return MDOT_OK;
+  std::vector<unsigned char> h(kGuardDbl * sizeof(double));
+  for (size_t k = 0; k < guards.size(); ++k) {
+    CK(cudaMemcpyAsync(h.data(), reinterpret_cast<double*>(base) + guards[k], h.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t b = 0; b < h.size(); ++b)
+      if (h[b] != 0xA5) {
+        set_error("MDOT_CHECKED: guard band %zu of %zu (workspace double %zu) overwritten at byte %zu", k,
+                  guards.size(), guards[k], b);
+        return MDOT_ECUDA;
+      }
+  }
+#endif
+  return MDOT_OK;
+}
+
 // K1 fetched the first tiles of C (all of C when it fits in L2) with an
 // evict_last policy; give those lines normal priority before returning so
 // later kernels of the caller -- or a solve on another C -- are not crowded
@@ -1187,7 +1223,12 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   const int chr = round_chunks(a, true), chc = round_chunks(a, false);
   const size_t dbl = (size_t)(4 + 3 * chr) * nrows + (size_t)(3 + chc) * n;
   double* buf = nullptr;
+#ifdef MDOT_CHECKED
+  CK(cudaMallocAsync((void**)&buf, (dbl + kGuardDbl) * sizeof(double), st));
+  CK(cudaMemsetAsync(buf + dbl, 0xA5, kGuardDbl * sizeof(double), st));
+#else
   CK(cudaMallocAsync((void**)&buf, dbl * sizeof(double), st));
+#endif
   double* logx = buf;
   double* Ap = logx + nrows;
   double* er = Ap + nrows;
@@ -1244,6 +1285,15 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
     return MDOT_OK;
   };
   stt = run();
+#ifdef MDOT_CHECKED
+  if (stt == MDOT_OK) {
+    std::vector<unsigned char> h(kGuardDbl * sizeof(double));
+    CK(cudaMemcpyAsync(h.data(), buf + dbl, h.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (unsigned char b : h)
+      if (b != 0xA5) { set_error("MDOT_CHECKED: rounding buffer overrun"); stt = MDOT_ECUDA; break; }
+  }
+#endif
   cudaFreeAsync(buf, st);
   return stt;
 }
@@ -1416,6 +1466,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * n, k, stream);
   }
   if (st == MDOT_OK) st = w.l2_reset();
+  if (st == MDOT_OK) st = w.check_guards();
   if (o.trace && o.trace_cap > 0) {
     const int64_t len = std::min<int64_t>((int64_t)w.trace_host.size(), o.trace_cap);
     if (len > 0) memcpy(o.trace, w.trace_host.data(), sizeof(mdot_trace_rec) * (size_t)len);
@@ -1788,6 +1839,7 @@ mdot_status mdot_marginals(const mdot_problem* pb, const double* Ain, const doub
     }
     if (fallback_out) *fallback_out = (int32_t)w.fallbacks;
     if (st == MDOT_OK) st = w.l2_reset();
+    if (st == MDOT_OK) st = w.check_guards();
   }
   w.free_owned();
   w.release();

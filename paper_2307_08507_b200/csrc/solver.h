@@ -110,6 +110,10 @@ struct Workspace {
   mdot_status load_problem(const mdot_problem* pb, int64_t row0);
   void free_owned();
   mdot_status l2_reset();
+  // MDOT_CHECKED builds: guard bands (in doubles from base) after each sub-buffer
+  static constexpr size_t kGuardDbl = 64;
+  std::vector<size_t> guards;
+  mdot_status check_guards();
   mdot_status setup(const mdot_options& o);
   void set_gamma(double gb);
   mdot_status prep(int mode, double alpha, double beta, const double* s_dir, const double* Ain,

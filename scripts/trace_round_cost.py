@@ -1,3 +1,5 @@
+"""Per-stage host timestamps (MDOT_TRACE=1) of config-5 and config-4 solves capped at 48
+evaluations: isolates the rounding stage (a10) cost."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

@@ -73,6 +73,9 @@ def parse():
                     help="config-5 step = the first K O(n^2) evaluations of the config-5 solve (fixed budget)")
     ap.add_argument("--c5-full", type=int, default=1,
                     help="also time one complete config-5 solve to L1 1e-5 (time-to-eps; ~10 s on one B200)")
+    ap.add_argument("--adaptive-gamma-leg", type=float, default=256.0,
+                    help="also time the solve with MDOT_SCHED_ADAPTIVE starting at this gamma_1 (Z29), reported "
+                         "under 'adaptive_gamma'; 0 disables")
     ap.add_argument("--adaptive-leg", type=float, default=1e-3,
                     help="also time the solve with this eps_md (SURVEY 8(f) rank 1), reported under "
                          "'adaptive_eps'; 0 disables")
@@ -366,6 +369,42 @@ def run_ours(a, rank, world, local_rank):
         "control": control,
         "slot_stage_us": stages,
     }
+    # adaptive gamma (Z29): the step sizes chosen on the fly from
+    # each projection's cost, the paper's eps at every step; same final plan by
+    # Lemma 2.  Reported beside the paper-protocol headline.
+    if a.adaptive_gamma_leg > 0 and not a.eps_md and a.projector == "pncg":
+        sched_a = M.schedule(M.MDOT_SCHED_ADAPTIVE, a.gamma_bar, step_max=a.adaptive_gamma_leg)
+        oa = M.options(eps=a.eps, projector=proj)
+
+        def solve_a():
+            if comm is not None:
+                return M.mdot_solve_sharded(comm, row0, nloc, C, r, c, n=n, schedule=sched_a, options=oa,
+                                            u_local_out=U, v_out=V)
+            return M.mdot_solve(C, r, c, schedule=sched_a, options=oa, u_out=U, v_out=V)
+        solve_a()
+        barrier()
+        rg = []
+        e0.record(st)
+        for _ in range(a.steps):
+            rg.append(solve_a())
+        e1.record(st)
+        barrier()
+        ms_g = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms_g], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_g = float(t.item())
+        ev_g = sum(x["evaluations"] for x in rg)
+        line["adaptive_gamma"] = {
+            "gamma_1": a.adaptive_gamma_leg, "realised_gammas": rg[-1]["gammas"],
+            "time_to_eps_s": ms_g / a.steps / 1000.0, "evals_per_s": ev_g / (ms_g / 1000.0),
+            "evaluations_per_solve": ev_g / a.steps, "speedup_vs_headline": ms_step / (ms_g / a.steps),
+            "cost_unrounded": rg[-1]["cost_unrounded"], "l1_final": rg[-1]["l1_final"],
+            "cost_rel_diff_vs_headline": abs(rg[-1]["cost_unrounded"] - results[-1]["cost_unrounded"])
+            / abs(results[-1]["cost_unrounded"]),
+            "status_name": rg[-1]["status_name"],
+            "note": "MDOT_SCHED_ADAPTIVE (DESIGN.md Z29): gamma doubles while the gbar gained per evaluation does "
+                    "not fall; eps at every MD step as in the paper; Lemma 2 (PAPER.md:152-155) fixes the final plan"}
     # adaptive eps: the same solve with loose intermediate
     # MD steps; same final eps, same device timing.  Reported beside the
     # paper-protocol headline, not instead of it.

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(256) k_round_rows_dense(RoundArgs a) {
   };
   if (!a.c_f64 && (a.n & 3) == 0 && (a.ldc & 3) == 0) {
     const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.C) + i * a.ldc);
+#pragma unroll 4
     for (int64_t q = lane; q < a.n / 4; q += 32) {
       const float4 c4 = __ldg(row + q);
       one((double)c4.x, 4 * q);
@@ -113,10 +114,13 @@ __global__ void __launch_bounds__(256) k_round_cols_dense(RoundArgs a) {
   if (j >= a.n) return;
   const double Bj = a.B[j], thr = a.logc[j] - kRoundSkip, g = a.gbar;
   double s = 0.0;
+  // 8 rows' loads in flight per thread (the loop is otherwise one dependent
+  // L2/HBM round trip per row: 0.9 TB/s on config 4)
+#pragma unroll 8
   for (int64_t i = ib; i < ie; ++i) {
-    const double cij = a.c_f64 ? reinterpret_cast<const double*>(a.C)[i * a.ldc + j]
-                               : (double)reinterpret_cast<const float*>(a.C)[i * a.ldc + j];
-    const double z = (a.A[i] + Bj) - g * cij;
+    const double cij = a.c_f64 ? __ldg(reinterpret_cast<const double*>(a.C) + i * a.ldc + j)
+                               : (double)__ldg(reinterpret_cast<const float*>(a.C) + i * a.ldc + j);
+    const double z = (__ldg(a.A + i) + Bj) - g * cij;
     if (z > thr) s += exp(z);
   }
   a.colS[(int64_t)chunk * a.n + j] = s;

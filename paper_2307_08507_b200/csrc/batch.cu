@@ -312,7 +312,19 @@ __device__ void batch_eval_tail_f64(const CT* __restrict__ C, int n, int j0, con
 template <bool F64, bool PACKED, typename CT>
 __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
                            double gbar, double* rowtot, double* coltot, double (*sred)[kTileN], int q_rank,
-                           int CL, double skip_z = -INFINITY) {
+                           int CL, double skip_z = -INFINITY, unsigned long long* dbgp = nullptr) {
+#ifdef MDOT_DIAG_K8
+  // sub-phase clocks of thread 0 (MDOT_DEBUG_K8): [5] tile main loops, [6] tile epilogues + tail tile
+  unsigned long long dt0 = (dbgp && threadIdx.x == 0) ? clock64() : 0ull;
+#define K8_SUB(slot)                                   \
+  if (dbgp && threadIdx.x == 0) {                      \
+    const unsigned long long dt1 = clock64();          \
+    dbgp[slot] += dt1 - dt0;                           \
+    dt0 = dt1;                                         \
+  }
+#else
+#define K8_SUB(slot)
+#endif
   static_assert(kBatchWarps == 2 * kSredRows, "two-round column reduction");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4* rowp = prm;
@@ -504,6 +516,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
         }
       }
     }
+    K8_SUB(5)
     if (!F64 && PACKED) {
 #pragma unroll
       for (int p = 0; p < 4; ++p) up2(cacc2[p], c32[2 * p], c32[2 * p + 1]);
@@ -531,7 +544,9 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
       if (j0 + t < n) coltot[j0 + t] = F64 ? acc : acc * (double)colp[j0 + t].y;   // fp32: times M_j = 2^bl_j
     }
     __syncthreads();
+    K8_SUB(6)
   }
+#undef K8_SUB
 }
 
 // C read as fp32 (DENSE_F32) or fp64 (DENSE_F64: fp64 entries only)
@@ -722,7 +737,8 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
           }
           batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, skip_z);
         } else {
-          batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL);
+          batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, -INFINITY,
+                                        (a.dbg && b == 0 && q_rank == 0) ? a.dbg : nullptr);
         }
         __syncthreads();
         K8_MARK(2)

@@ -1767,8 +1767,8 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
     cudaMemcpy(h, kdbg, sizeof(h), cudaMemcpyDeviceToHost);
     const double k = h[7] ? (double)h[7] : 1.0;
     fprintf(stderr, "[mdot] K8 cycles per evaluation (instance 0, CTA 0): ctrl %.0f prep %.0f eval %.0f "
-            "cluster-combine %.0f finalize %.0f (%llu evaluations)\n", h[0] / k, h[1] / k, h[2] / k, h[3] / k,
-            h[4] / k, h[7]);
+            "(tile loops %.0f, tile epilogues + tail %.0f) cluster-combine %.0f finalize %.0f (%llu evaluations)\n",
+            h[0] / k, h[1] / k, h[2] / k, h[5] / k, h[6] / k, h[3] / k, h[4] / k, h[7]);
     cudaFree(kdbg);
   }
   cudaFreeAsync(base, stream);

@@ -363,7 +363,13 @@ def run_ours(a, rank, world, local_rank):
                      "timing": timing,
                      "mean_launch_us": mean_launch_s * 1e6,
                      "kernel_evals_per_s": (1.0 / mean_launch_s) if kern_n else None,
-                     "kernel_share_of_step": (mean_launch_s * evals / (ms / 1000.0)) if kern_n else None},
+                     "kernel_share_of_step": (mean_launch_s * evals / (ms / 1000.0)) if kern_n else None,
+                     # the algorithmic-bytes fraction counts the L2-resident quarter of C and
+                     # the stages prefetched outside the K1 window as if read in it; these two bracket it
+                     "frac_dram_in_window": (traffic * (nloc / n) / mean_launch_s / 1e9 / (hbm / (world if dist else 1)))
+                     if (kern_n and traffic) else None,
+                     "frac_whole_slot": (bytes_per_launch * evals / (ms / 1000.0) / 1e9 / (hbm / (world if dist else 1)))
+                     if evals else None},
         "clocks": clocks,
         "gpu_launches": launches,
         "control": control,

@@ -170,7 +170,8 @@ typedef struct {
   int64_t stage_samples;   /* number of sampled slots in stage_ms */
   int32_t status;
   int32_t control_path;    /* last projection's control: 0 host loop, 1 CUDA-graph slots, 2 persistent kernel,
-                              3 one-CTA-per-instance kernel (mdot_solve_batch, small mdot_solve) */
+                              3 one-CTA-per-instance kernel (mdot_solve_batch, small mdot_solve),
+                              4 lockstep batch (mdot_solve_batch with MDOT_BATCH_LOCKSTEP=1) */
   double rho0[64];         /* per MD step: infeasibility at the warm start (Fig. 2 left) */
   double l10[64];          /* per MD step: L1 at the warm start */
   int64_t iters_step[64];  /* per MD step: projection iterations */

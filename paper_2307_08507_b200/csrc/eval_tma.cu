@@ -54,6 +54,70 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   tma_consume_pass<false>(sm, a, it, gh, gl, blockIdx.x, gridDim.x);
 }
 
+// Lockstep batch (throughput mode): ONE persistent pass evaluates every
+// active instance of a batch that shares C.  The virtual tile list is
+// (active instance, tile) in instance-major order, round-robin over the grid
+// as in k_eval_tma, so a CTA streams several tiles and the ring reaches steady
+// state even when one instance has fewer tiles than CTAs (n = 4096: 256
+// tiles).  Every instance keeps its own parameters and partials; instances
+// whose controller is done are skipped (all CTAs read the same flags).
+__global__ void __launch_bounds__(kTmaThreads, 2)
+    k_eval_tma_multi(const __grid_constant__ CUtensorMap tmap, const EvalArgs* args, int B) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+  TmaSmem& sm = *reinterpret_cast<TmaSmem*>(smem_raw + pad);
+  __shared__ int act[kMaxBatchLockstep];
+  __shared__ int nact;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int b = 0; b < B; ++b)
+      if (!(args[b].done && *args[b].done)) act[k++] = b;
+    nact = k;
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t tpi = (int64_t)args[0].n_row_tiles * args[0].n_col_tiles;   // tiles per instance (same for all)
+  const int64_t total = (int64_t)nact * tpi;
+  uint32_t it = 0;
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      for (int64_t v = blockIdx.x; v < total; v += gridDim.x) {
+        const EvalArgs& a = args[act[v / tpi]];
+        tma_produce_tile(sm, &tmap, a, it, v % tpi, l2_policy(a.keep_l2 != 0), l2_policy(true));
+      }
+    }
+    return;
+  }
+  for (int64_t v = blockIdx.x; v < total; v += gridDim.x) {
+    const EvalArgs& a = args[act[v / tpi]];
+    const float gh = a.gpair ? a.gpair[0] : a.gh;
+    const float gl = a.gpair ? a.gpair[1] : a.gl;
+    tma_consume_tile<false>(sm, a, it, gh, gl, v % tpi);
+  }
+}
+
+cudaError_t launch_eval_tma_multi(const void* map, const EvalArgs* args_dev, int B, int grid, cudaStream_t st) {
+  static bool attr = false;
+  const int smem = (int)sizeof(TmaSmem) + 128;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_eval_tma_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(k_eval_tma_multi, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  if (B > kMaxBatchLockstep) return cudaErrorInvalidValue;
+  const CUtensorMap& m = *reinterpret_cast<const CUtensorMap*>(map);
+  k_eval_tma_multi<<<grid, kTmaThreads, smem, st>>>(m, args_dev, B);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

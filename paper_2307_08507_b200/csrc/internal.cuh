@@ -105,6 +105,7 @@ struct EvalArgs {
 bool tma_supported(const EvalArgs& a);
 cudaError_t make_tma_map(const EvalArgs& a, void* map_out);
 cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_eval_tma_multi(const void* map, const EvalArgs* args_dev, int B, int grid, cudaStream_t st);
 int tma_smem_bytes();
 
 // Launch the fused evaluation over the (row tile x column tile) grid.
@@ -190,6 +191,7 @@ struct FinalizeArgs {
                          // bound on the mass K8's entry skip may have dropped (batch.cu); 0 = 1e-300
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+cudaError_t launch_finalize_multi(const FinalizeArgs* args_dev, const FinalizeArgs& a0, int B, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Device-resident PNCG / Sinkhorn control (one thread; k_ctrl).  The host
@@ -226,6 +228,13 @@ struct CtrlState {
   double sc[kNumScalars];
 };
 cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, cudaStream_t s);
+
+// Lockstep batch (throughput mode, solver.cu solve_batch_lockstep): one launch
+// per phase for every instance of a batch sharing a dense fp32 C; argument
+// arrays in device memory, instance b = blockIdx.y (prep / finalize), block b
+// (ctrl), or the b-th active instance of the virtual tile list (K1).
+constexpr int kMaxBatchLockstep = 64;
+cudaError_t launch_ctrl_multi(CtrlState* const* sts_dev, int B, int* done_flags, cudaStream_t s);
 // Prefer the maximum shared-memory carveout for every kernel of the solve loop
 // (one L1/smem configuration for the whole loop, no reconfiguration between
 // the TMA kernel and the O(n) kernels).
@@ -263,6 +272,7 @@ struct PrepArgs {
   const double *tr_lm, *tr_m, *tr_s, *tr_g;
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
+cudaError_t launch_prep_multi(const PrepArgs* args_dev, const PrepArgs& a0, int B, cudaStream_t st);
 
 // Persistent cooperative slot kernel (persist.cu): a whole projection in one
 // launch (ctrl / prep / K1 / finalize phases separated by grid barriers).

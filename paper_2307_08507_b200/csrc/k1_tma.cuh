@@ -101,26 +101,29 @@ __device__ __forceinline__ double warp_reduce4_t(double v0, double v1, double v2
 // Producer: one elected lane streams this CTA's tiles (round-robin over the
 // persistent grid) as 32-row x 256-column TMA boxes into the stage ring.
 // `it` is the running stage counter (kept across passes by the caller).
+// One tile's stages (tile = tr * n_col_tiles + tc of `a`).
+__device__ __forceinline__ void tma_produce_tile(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
+                                                 uint32_t& it, int64_t tile, uint64_t pol_stream, uint64_t pol_keep) {
+  const int nct = a.n_col_tiles;
+  const int tr = (int)(tile / nct), tc = (int)(tile % nct);
+  const int64_t i0 = (int64_t)tr * a.tile_m;
+  int nst = a.tile_m / kTmaRows;
+  if (i0 + (int64_t)nst * kTmaRows > a.nrows) nst = (int)((a.nrows - i0 + kTmaRows - 1) / kTmaRows);
+  for (int k = 0; k < nst; ++k, ++it) {
+    const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
+    mbar_wait(&sm.empty[s], ph ^ 1u);
+    mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
+    tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + k * kTmaRows), &sm.full[s],
+                     tile < a.l2_res_tiles ? pol_keep : pol_stream);
+  }
+}
+
 __device__ __forceinline__ void tma_produce_pass(TmaSmem& sm, const CUtensorMap* tmap, const EvalArgs& a,
                                                  uint32_t& it) {
   const uint64_t pol_stream = l2_policy(a.keep_l2 != 0), pol_keep = l2_policy(true);   // L2 residency as tma_produce_n
-  const int64_t nrows = a.nrows;
-  const int nct = a.n_col_tiles;
-  const int64_t total = (int64_t)a.n_row_tiles * nct;
-  const int stages_per_tile = a.tile_m / kTmaRows;
-  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    const int tr = (int)(tile / nct), tc = (int)(tile % nct);
-    const int64_t i0 = (int64_t)tr * a.tile_m;
-    int nst = stages_per_tile;
-    if (i0 + (int64_t)nst * kTmaRows > nrows) nst = (int)((nrows - i0 + kTmaRows - 1) / kTmaRows);
-    for (int k = 0; k < nst; ++k, ++it) {
-      const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
-      mbar_wait(&sm.empty[s], ph ^ 1u);
-      mbar_expect_tx(&sm.full[s], (uint32_t)(kTmaRows * kTileN * sizeof(float)));
-      tma_load_2d_hint(&sm.stage[s][0][0], tmap, tc * kTileN, (int)(i0 + k * kTmaRows), &sm.full[s],
-                       tile < a.l2_res_tiles ? pol_keep : pol_stream);
-    }
-  }
+  const int64_t total = (int64_t)a.n_row_tiles * a.n_col_tiles;
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x)
+    tma_produce_tile(sm, tmap, a, it, tile, pol_stream, pol_keep);
 }
 
 // Stages of C this CTA streams per pass (its tiles, round-robin over the
@@ -195,14 +198,25 @@ __device__ __forceinline__ float4 ld_param(const float4* p) {
 // release and spills at the 96-register cap of 18 warps/SM: 190 vs 185 us
 // in-solve), packed f32x2 arithmetic (186 vs 185 us).
 template <bool COHERENT = false>
+__device__ __forceinline__ void tma_consume_tile(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh, float gl,
+                                                 int64_t tile);
+
+template <bool COHERENT = false>
 __device__ __forceinline__ void tma_consume_pass(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh,
                                                  float gl, int cta, int ncta) {
+  const int64_t total = (int64_t)a.n_row_tiles * a.n_col_tiles;
+  for (int64_t tile = cta; tile < total; tile += ncta) tma_consume_tile<COHERENT>(sm, a, it, gh, gl, tile);
+}
+
+// One tile of `a` (tile = tr * n_col_tiles + tc): the consumers' share of the pass.
+template <bool COHERENT>
+__device__ __forceinline__ void tma_consume_tile(TmaSmem& sm, const EvalArgs& a, uint32_t& it, float gh, float gl,
+                                                 int64_t tile) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n = a.n, nrows = a.nrows;
   const int nct = a.n_col_tiles;
-  const int64_t total = (int64_t)a.n_row_tiles * nct;
   const int stages_per_tile = a.tile_m / kTmaRows;
-  for (int64_t tile = cta; tile < total; tile += ncta) {
+  {
     const int tr = (int)(tile / nct), tc = (int)(tile % nct);
     const int64_t i0 = (int64_t)tr * a.tile_m;
     const int64_t j0 = (int64_t)tc * kTileN;

@@ -19,6 +19,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "entry.cuh"
 #include "internal.cuh"
 #include "ops.cuh"
@@ -690,7 +692,18 @@ __device__ __forceinline__ double sum_strided(const double* x, int64_t stride, i
 // ---------------------------------------------------------------------------
 // finalize: marginals, s, grad, scalars
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
+__device__ __forceinline__ void finalize_body(const FinalizeArgs& a);
+
+__global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) { finalize_body(a); }
+
+// Lockstep batch (throughput mode): blockIdx.y = instance, its own args,
+// tickets and block partials (an instance whose controller is done exits).
+__global__ void __launch_bounds__(256) k_finalize_multi(const FinalizeArgs* args) {
+  const FinalizeArgs a = args[blockIdx.y];
+  finalize_body(a);
+}
+
+__device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
   if (a.done && *a.done) return;
   const int sub = threadIdx.x & (kFinTPI - 1);
   const int64_t tot_items = a.item_end > 0 ? a.item_end : a.nrows + a.n;
@@ -720,6 +733,19 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   if (in_range && sub == 0) finalize_item(a, k, tot, v);
   }
   block_reduce_and_publish<kNumScalars>(v, a.blockpart, a.ticket, a.scalars_dev, a.scalars_host, a.add_in);
+}
+
+cudaError_t launch_finalize_multi(const FinalizeArgs* args_dev, const FinalizeArgs& a0, int B, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = a0.nrows + a0.n;
+  const int64_t groups = (items * kFinTPI + 255) / 256;
+  // at least ~2 blocks per SM over the whole batch, at most 2 x #SMs per instance
+  const int64_t cap = std::max<int64_t>(8, std::min<int64_t>(2 * sms, (4 * (int64_t)sms + B - 1) / B));
+  const unsigned blocks = (unsigned)(groups < cap ? groups : cap);
+  k_finalize_multi<<<dim3(blocks, (unsigned)B), 256, 0, st>>>(args_dev);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
@@ -777,6 +803,29 @@ void set_smem_carveout() {
   set_smem_carveout_tma();
 }
 
+// Lockstep batch: block b runs instance b's controller; done_flags[b] (mapped
+// host memory) mirrors its `done` so the host knows when every instance's
+// projection has finished.
+__global__ void k_ctrl_multi(CtrlState* const* gsts, int* done_flags) {
+  __shared__ CtrlState sst;
+  constexpr int kWords = (int)(sizeof(CtrlState) / sizeof(unsigned long long));
+  unsigned long long* g = reinterpret_cast<unsigned long long*>(gsts[blockIdx.x]);
+  unsigned long long* sh = reinterpret_cast<unsigned long long*>(&sst);
+  for (int i = threadIdx.x; i < kWords; i += 32) sh[i] = g[i];
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    ctrl_body(&sst, 0, nullptr, nullptr);
+    *((volatile int*)&done_flags[blockIdx.x]) = sst.done;
+  }
+  __syncwarp();
+  for (int i = threadIdx.x; i < kWords; i += 32) g[i] = sh[i];
+}
+
+cudaError_t launch_ctrl_multi(CtrlState* const* sts_dev, int B, int* done_flags, cudaStream_t s) {
+  k_ctrl_multi<<<B, 32, 0, s>>>(sts_dev, done_flags);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, cudaStream_t s) {
   k_ctrl<<<1, 32, 0, s>>>(st, slot, done_host, ran_host);
   return cudaGetLastError();
@@ -786,6 +835,19 @@ __global__ void k_prep(PrepArgs a) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= a.nrows + a.n) return;
   prep_item(a, k, a.ctrl);
+}
+
+__global__ void k_prep_multi(const PrepArgs* args) {
+  const PrepArgs& a = args[blockIdx.y];
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.nrows + a.n) return;
+  prep_item(a, k, a.ctrl);
+}
+
+cudaError_t launch_prep_multi(const PrepArgs* args_dev, const PrepArgs& a0, int B, cudaStream_t st) {
+  const int64_t items = a0.nrows + a0.n;
+  k_prep_multi<<<dim3((unsigned)((items + 255) / 256), (unsigned)B), 256, 0, st>>>(args_dev);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {

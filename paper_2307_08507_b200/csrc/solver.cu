@@ -1546,6 +1546,270 @@ mdot_status mdot_solve_sharded(mdot_comm* c, const mdot_problem* local_rows, int
   return solve_impl(local_rows, sched, opt, u_local_out, v_out, nullptr, res, 0, cm, row0, n_local);
 }
 
+// Throughput mode, lockstep ("including as
+// a batch process"): B instances sharing one dense fp32 C advance together,
+// one evaluation slot for all of them at a time, with ONE launch per phase for
+// the whole batch -- k_ctrl_multi (every controller), k_prep_multi,
+// k_eval_tma_multi (one persistent TMA pass over the virtual tile list
+// (active instance, tile): a CTA streams several tiles, so the ring reaches
+// steady state even where one instance has fewer tiles than the grid has
+// CTAs) and k_finalize_multi -- captured in CUDA graphs of K slots.
+// Instances whose projection has converged drop out of K1 and finalize; the
+// MD step ends when every instance's has.  Each instance keeps its own
+// workspace, controller and results, so it takes exactly the decisions of a
+// device-control solve of its own (up to summation-order bits).  Returns
+// MDOT_EGEN when the batch cannot run this way (the caller then uses the
+// worker-stream path).  Opt-in (MDOT_BATCH_LOCKSTEP=1): without sharing the
+// C reads between instances the batched K1 is bound by the same ~4.6 TB/s
+// stream as one instance's (n = 4096, C "L2-resident" at 64 MB), so it does
+// not beat the concurrent worker streams (16 x n = 4096, eps_md 1e-3: 264 vs
+// 163 ms; profiles/r02_throughput_lockstep.txt).  A K1 that evaluates every
+// instance on one read of each C stage is the lever; DESIGN.md section 10.
+static mdot_status solve_batch_lockstep(const mdot_problem* shared, int32_t Bn, const double* r, const double* c,
+                                        const mdot_schedule* sched, const mdot_options* opt_in, double* u_out,
+                                        double* v_out, mdot_result* res) {
+  mdot_options o;
+  if (opt_in) o = *opt_in; else mdot_options_default(&o);
+  if (o.ls_max_trials <= 0) o.ls_max_trials = 100;
+  if (o.max_evals <= 0) o.max_evals = 10000000;
+  if (Bn < 2 || Bn > kMaxBatchLockstep || shared->kind != MDOT_COST_DENSE_F32 || shared->mem != MDOT_MEM_DEVICE ||
+      !sched || sched->kind == MDOT_SCHED_ADAPTIVE || o.device_control == 0 || o.trace ||
+      !(getenv("MDOT_BATCH_LOCKSTEP") && atoi(getenv("MDOT_BATCH_LOCKSTEP")) == 1))
+    return MDOT_EGEN;
+  std::vector<double> gam;
+  mdot_status st = build_schedule(sched, gam);
+  if (st != MDOT_OK) return st;
+  const double t0 = now_s();
+  cudaStream_t stream = (cudaStream_t)o.stream;
+  const int64_t n = shared->n;
+  std::vector<std::unique_ptr<Workspace>> W;
+  for (int32_t b = 0; b < Bn; ++b) {
+    memset(&res[b], 0, sizeof(mdot_result));
+    W.emplace_back(new Workspace());
+    Workspace& w = *W.back();
+    w.persist_ncta = -1;   // no persistent projection: the batch has its own slots
+    CKS(w.alloc(stream, n, n));
+    mdot_problem p = *shared;
+    p.r = r + (int64_t)b * n;
+    p.c = c + (int64_t)b * n;
+    CKS(w.load_problem(&p, 0));
+    CKS(w.setup(o));
+    if (!w.use_tma || w.exact_mode || w.otf) return MDOT_EGEN;
+  }
+  // argument arrays (pointers fixed for the whole solve: device control
+  // accepts by element-wise copies, never by swapping buffers)
+  std::vector<PrepArgs> hp(Bn);
+  std::vector<EvalArgs> he(Bn);
+  std::vector<FinalizeArgs> hf(Bn);
+  std::vector<CtrlState*> hc(Bn);
+  for (int32_t b = 0; b < Bn; ++b) {
+    Workspace& w = *W[b];
+    PrepArgs& a = hp[b];
+    a = PrepArgs{};
+    a.n = n; a.nrows = n; a.mode = 0;
+    a.U = w.U; a.V = w.V; a.u = w.u; a.v = w.v; a.tu = w.tu; a.tv = w.tv;
+    a.p = w.p; a.s = w.cur->s; a.pprev = w.pprev; a.lm = w.cur->lm;
+    a.logr = w.logr; a.logc = w.logc; a.rho_r = w.rho_r; a.sig_c = w.sig_c;
+    a.Aout = w.A; a.Bout = w.B;
+    a.rowp = w.rowp; a.colp = w.colp; a.flag = w.flag;
+    a.ctrl = w.ctrl;
+    a.cur_lm = w.cur->lm; a.cur_m = w.cur->m; a.cur_s = w.cur->s; a.cur_g = w.cur->g;
+    a.tr_lm = w.trial->lm; a.tr_m = w.trial->m; a.tr_s = w.trial->s; a.tr_g = w.trial->g;
+    EvalArgs& e = he[b];
+    e = w.eval;
+    e.gpair = w.ctrl->gpair;
+    e.done = &w.ctrl->done;
+    FinalizeArgs& f = hf[b];
+    f = FinalizeArgs{};
+    f.n = n; f.nrows = n;
+    f.rho_r = w.rho_r; f.sig_c = w.sig_c;
+    f.r = w.r; f.c = w.c; f.logr = w.logr; f.logc = w.logc;
+    f.gcur = w.cur->g; f.pcur = w.p;
+    f.lm = w.trial->lm; f.m = w.trial->m; f.s = w.trial->s; f.g = w.trial->g;
+    f.blockpart = w.blockpart; f.ticket = w.ticket;
+    f.scalars_dev = w.ctrl->sc; f.scalars_host = nullptr;
+    f.prep_flag = w.flag;
+    f.jacobi = w.jacobi;
+    f.done = &w.ctrl->done;
+    f.from_partials = 1;
+    f.rowpart = w.rowpart; f.n_col_tiles = w.eval.n_col_tiles;
+    f.colpart = w.colpart; f.n_row_tiles = w.eval.n_row_tiles;
+    hc[b] = w.ctrl;
+  }
+  const size_t bytes = sizeof(PrepArgs) * Bn + sizeof(EvalArgs) * Bn + sizeof(FinalizeArgs) * Bn +
+                       sizeof(CtrlState*) * Bn + 4 * 256;
+  char* dargs = nullptr;
+  CK(cudaMallocAsync((void**)&dargs, bytes, stream));
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  PrepArgs* dp = reinterpret_cast<PrepArgs*>(dargs);
+  EvalArgs* de = reinterpret_cast<EvalArgs*>(dargs + al(sizeof(PrepArgs) * Bn));
+  FinalizeArgs* df = reinterpret_cast<FinalizeArgs*>(dargs + al(sizeof(PrepArgs) * Bn) + al(sizeof(EvalArgs) * Bn));
+  CtrlState** dc = reinterpret_cast<CtrlState**>(dargs + al(sizeof(PrepArgs) * Bn) + al(sizeof(EvalArgs) * Bn) +
+                                                 al(sizeof(FinalizeArgs) * Bn));
+  CK(cudaMemcpyAsync(dp, hp.data(), sizeof(PrepArgs) * Bn, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(de, he.data(), sizeof(EvalArgs) * Bn, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(df, hf.data(), sizeof(FinalizeArgs) * Bn, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(dc, hc.data(), sizeof(CtrlState*) * Bn, cudaMemcpyHostToDevice, stream));
+  // done flags: mapped pinned (the host polls them after each graph)
+  int* done_h = nullptr;
+  int* done_d = nullptr;
+  CK(cudaHostAlloc((void**)&done_h, sizeof(int) * kMaxBatchLockstep, cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&done_d, done_h, 0));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = 2 * sms;
+  Workspace& w0 = *W[0];
+  // one graph of K slots [ctrl, prep, K1, finalize] for the whole batch (~2 ms of work)
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const double est = (4.0 * (double)n * n / 5.0e12) * Bn + 20e-6;
+  const int K = (int)std::max(2.0, std::min(64.0, ceil(2e-3 / est)));
+  auto slot = [&](cudaStream_t s2, bool with_ctrl) -> mdot_status {
+    if (with_ctrl) CK(launch_ctrl_multi(dc, Bn, done_d, s2));
+    CK(launch_prep_multi(dp, hp[0], Bn, s2));
+    CK(launch_eval_tma_multi(w0.tmap, de, Bn, grid, s2));
+    CK(launch_finalize_multi(df, hf[0], Bn, s2));
+    return MDOT_OK;
+  };
+  mdot_status stt = MDOT_OK;
+  {
+    CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < K && stt == MDOT_OK; ++k) stt = slot(cap, true);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+    if (stt != MDOT_OK || ce != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      set_error("lockstep graph capture failed");
+      return stt != MDOT_OK ? stt : MDOT_ECUDA;
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) { set_error("lockstep graph instantiate failed"); return MDOT_ECUDA; }
+  }
+  int64_t launches = 0;
+  double gb = 0.0, gprev = 0.0;
+  std::vector<mdot_status> sts((size_t)Bn, MDOT_OK);
+  for (size_t t = 1; t <= gam.size() && stt == MDOT_OK; ++t) {
+    const double gt = gam[t - 1];
+    gb += gt;
+    const bool last = t == gam.size();
+    for (int32_t b = 0; b < Bn; ++b) {
+      Workspace& w = *W[b];
+      if (sts[b] != MDOT_OK) continue;
+      w.set_gamma(gb);
+      if (o.warm == MDOT_WARM_ZERO) {
+        launch_fill(n, 0.0, w.u, stream);
+        launch_fill(n, 0.0, w.v, stream);
+      } else if (o.warm == MDOT_WARM_SCALED && t > 1 && gt != gprev) {
+        launch_axpby(n, 0.0, w.u, gt / gprev, w.u, stream);
+        launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
+      }
+      CtrlState h{};
+      h.eps = (!last && o.eps_md > o.eps) ? o.eps_md : o.eps;
+      h.c1 = o.c1; h.c2 = o.c2;
+      h.noise = ls_noise(false, gb);
+      h.stop_rho = o.stop; h.ncg = o.projector == MDOT_PROJ_NCG; h.sinkhorn = o.projector == MDOT_PROJ_SINKHORN;
+      h.beta_kind = o.beta; h.ls_max_trials = o.ls_max_trials;
+      h.max_evals = o.max_evals - w.evals;
+      h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
+      h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+      h.md_t = (int)t;
+      CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, stream));
+      done_h[b] = 0;
+    }
+    // instances that already failed sit out (their controller is marked done)
+    for (int32_t b = 0; b < Bn; ++b)
+      if (sts[b] != MDOT_OK) {
+        const int one = 1;
+        CK(cudaMemcpyAsync(&W[b]->ctrl->done, &one, sizeof(int), cudaMemcpyHostToDevice, stream));
+        done_h[b] = 1;
+      }
+    // initial evaluation of every instance (no controller), then graphs
+    stt = slot(stream, false);
+    launches += 3;
+    while (stt == MDOT_OK) {
+      CK(cudaGraphLaunch(gexec, stream));
+      launches += 4 * (int64_t)K;
+      CK(cudaStreamSynchronize(stream));
+      bool all = true;
+      for (int32_t b = 0; b < Bn; ++b) all = all && ((volatile int*)done_h)[b] != 0;
+      if (all) break;
+    }
+    for (int32_t b = 0; b < Bn && stt == MDOT_OK; ++b) {
+      Workspace& w = *W[b];
+      if (sts[b] != MDOT_OK) continue;
+      CtrlState h{};
+      CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      mdot_result* R = &res[b];
+      w.evals += h.evals;
+      R->iterations += h.iterations;
+      R->ls_evaluations += h.ls_evals;
+      R->resets += h.resets;
+      R->ls_restarts += h.restarts;
+      if (t <= 64) {
+        R->rho0[t - 1] = h.rho_0;
+        R->l10[t - 1] = h.l1_0;
+        R->iters_step[t - 1] += h.iterations;
+        R->gammas[t - 1] = gt;
+      }
+      R->l1_final = h.l1;
+      R->rho_final = h.rho;
+      R->md_steps = (int64_t)t;
+      R->control_path = 4;
+      mdot_options ot = o;
+      if (!last && o.eps_md > o.eps) ot.eps = o.eps_md;
+      mdot_status ps = MDOT_OK;
+      if (h.status == CTRL_NOCONV) ps = MDOT_ENOCONV;
+      else if (h.status == CTRL_LS_FAIL) {
+        set_error("instance %d: line search failed twice at MD step %d (lockstep batch)", (int)b, (int)t);
+        ps = MDOT_ELINESEARCH;
+      } else if (h.status == CTRL_NEED_HOST) {
+        // range guard: this instance finishes the projection under host control
+        w.fallbacks++;
+        ps = (o.projector == MDOT_PROJ_SINKHORN) ? project_sinkhorn(w, ot, (int)t, R) : project_pncg(w, ot, (int)t, R);
+      }
+      launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u
+      launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);
+      if (ps != MDOT_OK && ps != MDOT_ENOCONV) { sts[b] = ps; continue; }
+      mdot_status gs = w.gauge_center(w.U, w.V);
+      if (gs == MDOT_OK) gs = w.gauge_center(w.u, w.v);
+      if (gs != MDOT_OK) { stt = gs; break; }
+      if (ps == MDOT_ENOCONV) sts[b] = ps;
+    }
+    gprev = gt;
+  }
+  mdot_status first = stt;
+  for (int32_t b = 0; b < Bn; ++b) {
+    Workspace& w = *W[b];
+    mdot_result* R = &res[b];
+    R->gamma_bar = gb;
+    if (stt == MDOT_OK && (sts[b] == MDOT_OK || sts[b] == MDOT_ENOCONV)) {
+      const mdot_status rs = w.round_and_cost(nullptr, &R->cost_unrounded, &R->cost_rounded);
+      if (rs != MDOT_OK && first == MDOT_OK) first = rs;
+    }
+    if (u_out) cudaMemcpyAsync(u_out + (int64_t)b * n, w.U, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
+    if (v_out) cudaMemcpyAsync(v_out + (int64_t)b * n, w.V, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
+    R->evaluations = w.evals;
+    R->fallbacks = w.fallbacks;
+    R->all_launches = w.launches + launches / Bn;
+    R->status = (stt != MDOT_OK) ? stt : sts[b];
+    if (first == MDOT_OK && sts[b] != MDOT_OK) first = sts[b];
+  }
+  if (stt == MDOT_OK) W[0]->l2_reset();
+  cudaGraphExecDestroy(gexec);
+  cudaStreamDestroy(cap);
+  cudaFreeAsync(dargs, stream);
+  for (auto& w : W) { w->free_owned(); w->release(); }
+  cudaStreamSynchronize(stream);
+  cudaFreeHost(done_h);
+  const double secs = now_s() - t0;
+  for (int32_t b = 0; b < Bn; ++b) res[b].seconds = secs;
+  return first;
+}
+
 // mdot_solve_batch for costs the K8 kernel cannot hold (SURVEY 8(f) rank 4,
 // throughput mode): device-resident instances are solved concurrently by up
 // to MDOT_BATCH_WORKERS (default 8) host workers, each on its own stream
@@ -1633,7 +1897,11 @@ mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t Bn, const doubl
   const bool fits = (shared->kind == MDOT_COST_DENSE_F32 || c64) && n >= 1 &&
                     (int64_t)batch_smem_bytes((int)n) <= optin && getenv("MDOT_NO_BATCH_KERNEL") == nullptr &&
                     !(c64 && o.precision == MDOT_PREC_F32P);   // rejected by the per-instance path
-  if (!fits) return solve_batch_loop(shared, Bn, r, c, sched, opt_in, u_out, v_out, res);
+  if (!fits) {
+    const mdot_status ls = solve_batch_lockstep(shared, Bn, r, c, sched, opt_in, u_out, v_out, res);
+    if (ls != MDOT_EGEN) return ls;
+    return solve_batch_loop(shared, Bn, r, c, sched, opt_in, u_out, v_out, res);
+  }
   const double t0 = now_s();
   for (int32_t b = 0; b < Bn; ++b) memset(&res[b], 0, sizeof(mdot_result));
   if (!(o.eps > 0)) { set_error("eps must be > 0"); return MDOT_EINVAL; }

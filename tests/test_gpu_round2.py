@@ -294,3 +294,29 @@ def test_nan_injection_persistent_failure_returns_einstable(n, dc, monkeypatch):
     # the library is usable afterwards
     res, U, V = _solve(inst, 512.0, 2, 1e-6)
     assert res["status"] == 0
+
+
+def test_lockstep_batch_matches_single_solves_and_oracle(monkeypatch):
+    """Throughput mode, lockstep variant (MDOT_BATCH_LOCKSTEP=1: one launch per
+    phase for every instance sharing C, a persistent K1 over the virtual
+    (instance, tile) list): each instance against its own
+    single solve (Z20 gate) and one against the oracle."""
+    monkeypatch.setenv("MDOT_BATCH_LOCKSTEP", "1")
+    n, B, gb, T, eps = 1000, 4, 1024.0, 4, 1e-6
+    base = S.uniform_points_instance(3, n, 2, 90, marg="dirichlet")
+    R = np.stack([S.uniform_points_instance(3, n, 2, 90 + b, marg="dirichlet").r for b in range(B)])
+    Cm = np.stack([S.uniform_points_instance(3, n, 2, 95 + b, marg="dirichlet").c for b in range(B)])
+    U = torch.empty((B, n), dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=T)
+    res = M.mdot_solve_batch(_t(base.C), _t(R), _t(Cm), schedule=sched, options=M.options(eps=eps),
+                             u_out=U, v_out=V)
+    assert all(x["status"] == 0 and x["control_path"] == 4 and x["l1_final"] <= eps for x in res)
+    monkeypatch.setenv("MDOT_BATCH_LOCKSTEP", "0")
+    for b in range(B):
+        rs = M.mdot_solve(_t(base.C), _t(R[b]), _t(Cm[b]), schedule=sched, options=M.options(eps=eps))
+        assert abs(res[b]["cost_unrounded"] - rs["cost_unrounded"]) <= COST_GATE * rs["cost_unrounded"]
+    inst = S.Instance(n, R[1], Cm[1], C=base.C)
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), O.make_options(eps=eps))
+    _gates(res[1], ores, inst, prob, U[1].cpu().numpy(), V[1].cpu().numpy(), eps)

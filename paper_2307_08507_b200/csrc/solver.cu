@@ -1085,6 +1085,7 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
       eval.keep_l2 = (4.0 * (double)nrows * (double)n <= 0.6 * (double)l2) ? 1 : 0;
+      if (const char* kl = getenv("MDOT_K1_KEEP_L2")) eval.keep_l2 = atoi(kl) != 0;   // A/B only
       // C larger than L2: a quarter of L2 keeps the first tiles resident
       // across evaluations (evict_last), the rest streams (evict_first);
       // config 4: K1 171.8 -> 168.5 us, time-to-eps -1.5 %; 64 / 96 MB

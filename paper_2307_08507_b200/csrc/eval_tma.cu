@@ -102,6 +102,70 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   }
 }
 
+// Shared-C variant: the virtual list is (tile, group of up to 8 active
+// instances), tile-major, so one streamed copy of a C tile serves a whole
+// group (consumer warp w = instance 8 g + w; tma_consume_tile_shared) and the
+// groups of one tile run on neighbouring CTAs at about the same time (their
+// second read of the tile hits L2).  C traffic per slot: ceil(active / 8)
+// passes instead of one per instance.
+__global__ void __launch_bounds__(kTmaThreads, 2)
+    k_eval_tma_shared(const __grid_constant__ CUtensorMap tmap, const EvalArgs* args, int B) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+  TmaSmem& sm = *reinterpret_cast<TmaSmem*>(smem_raw + pad);
+  __shared__ int act[kMaxBatchLockstep];
+  __shared__ int nact;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int b = 0; b < B; ++b)
+      if (!(args[b].done && *args[b].done)) act[k++] = b;
+    nact = k;
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const EvalArgs& a0 = args[0];   // geometry: identical for every instance of the batch
+  const int64_t tpi = (int64_t)a0.n_row_tiles * a0.n_col_tiles;
+  const int groups = (nact + kConsumerWarps - 1) / kConsumerWarps;
+  const int64_t total = (int64_t)groups * tpi;
+  uint32_t it = 0;
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      const uint64_t pol_stream = l2_policy(a0.keep_l2 != 0), pol_keep = l2_policy(true);
+      for (int64_t v = blockIdx.x; v < total; v += gridDim.x)
+        tma_produce_tile(sm, &tmap, a0, it, v / groups, pol_stream, pol_keep);
+    }
+    return;
+  }
+  for (int64_t v = blockIdx.x; v < total; v += gridDim.x) {
+    const int g = (int)(v % groups);
+    const int slot = g * kConsumerWarps + warp;
+    const int b = slot < nact ? act[slot] : -1;
+    tma_consume_tile_shared(sm, args[b >= 0 ? b : 0], b, it, v / groups);
+  }
+}
+
+cudaError_t launch_eval_tma_shared(const void* map, const EvalArgs* args_dev, int B, int grid, cudaStream_t st) {
+  static bool attr = false;
+  const int smem = (int)sizeof(TmaSmem) + 128;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_eval_tma_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(k_eval_tma_shared, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  if (B > kMaxBatchLockstep) return cudaErrorInvalidValue;
+  const CUtensorMap& m = *reinterpret_cast<const CUtensorMap*>(map);
+  k_eval_tma_shared<<<grid, kTmaThreads, smem, st>>>(m, args_dev, B);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_eval_tma_multi(const void* map, const EvalArgs* args_dev, int B, int grid, cudaStream_t st) {
   static bool attr = false;
   const int smem = (int)sizeof(TmaSmem) + 128;

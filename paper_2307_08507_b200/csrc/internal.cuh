@@ -106,6 +106,8 @@ bool tma_supported(const EvalArgs& a);
 cudaError_t make_tma_map(const EvalArgs& a, void* map_out);
 cudaError_t launch_eval_tma(const void* map, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_eval_tma_multi(const void* map, const EvalArgs* args_dev, int B, int grid, cudaStream_t st);
+// shared C reads: up to 8 instances per streamed tile (one per consumer warp)
+cudaError_t launch_eval_tma_shared(const void* map, const EvalArgs* args_dev, int B, int grid, cudaStream_t st);
 int tma_smem_bytes();
 
 // Launch the fused evaluation over the (row tile x column tile) grid.

@@ -347,4 +347,111 @@ __device__ __forceinline__ void tma_consume_tile(TmaSmem& sm, const EvalArgs& a,
   }
 }
 
+// Shared-C multi-instance consumer (lockstep throughput batch,
+// k_eval_tma_shared): consumer warp w evaluates instance `b` (< 0: idle) on
+// ALL 32 rows of every stage of the tile, so one read of C serves up to eight
+// instances per CTA.  The warp's columns belong to it alone: its column sums
+// (fp32 over 16 rows, then fp64 in its private row of sm.sred) become the
+// tile's column partial without a cross-warp reduction, and its row totals are
+// complete per (row, column tile) after the 4-row butterfly, as in
+// tma_consume_tile.  Lane l holds stage row l's parameters (one load per stage)
+// and broadcasts them with shuffles.
+__device__ __forceinline__ void tma_consume_tile_shared(TmaSmem& sm, const EvalArgs& a, int b, uint32_t& it,
+                                                        int64_t tile) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = a.n, nrows = a.nrows;
+  const int nct = a.n_col_tiles;
+  const int tr = (int)(tile / nct), tc = (int)(tile % nct);
+  const int64_t i0 = (int64_t)tr * a.tile_m;
+  const int64_t j0 = (int64_t)tc * kTileN;
+  int nst = a.tile_m / kTmaRows;
+  if (i0 + (int64_t)nst * kTmaRows > nrows) nst = (int)((nrows - i0 + kTmaRows - 1) / kTmaRows);
+  if (b < 0) {   // no instance for this warp: keep the ring protocol only
+    for (int k = 0; k < nst; ++k, ++it) {
+      const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
+      mbar_wait(&sm.full[s], ph);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+    }
+    return;
+  }
+  float bh[8], T[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+    if (j < n) {
+      const float4 cp = __ldg(&a.colp[j]);
+      bh[q] = cp.x; T[q] = cp.z;
+    } else {
+      bh[q] = -1.0e30f; T[q] = 0.f;
+    }
+  }
+  ColPairs cpp;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) { cpp.bh[p] = pk2(bh[2 * p], bh[2 * p + 1]); cpp.T[p] = pk2(T[2 * p], T[2 * p + 1]); }
+  const float gh = a.gpair ? a.gpair[0] : a.gh;
+  const float gl = a.gpair ? a.gpair[1] : a.gl;
+  const u64 ngh2 = pk2(-gh, -gh), ngl2 = pk2(-gl, -gl);
+  double* csum = &sm.sred[warp][0];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) csum[4 * lane + (q & 3) + 128 * (q >> 2)] = 0.0;
+  u64 cacc2[4] = {0ull, 0ull, 0ull, 0ull};
+  int grp = 0;
+  const float4 none = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < nst; ++k, ++it) {
+    const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
+    const int64_t irow = i0 + (int64_t)k * kTmaRows + lane;
+    const float4 rq = (irow < nrows) ? __ldg(&a.rowp[irow]) : none;
+    mbar_wait(&sm.full[s], ph);
+#pragma unroll 1
+    for (int g = 0; g < kTmaRows / 4; ++g) {
+      float rs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rl = 4 * g + u;
+        const float ah = __shfl_sync(0xffffffffu, rq.x, rl);
+        const float S = __shfl_sync(0xffffffffu, rq.z, rl);
+        const float* row = &sm.stage[s][rl][0];
+        const float4 x0 = *reinterpret_cast<const float4*>(row + 4 * lane);
+        const float4 x1 = *reinterpret_cast<const float4*>(row + 128 + 4 * lane);
+        const u64 c2[4] = {pk2(x0.x, x0.y), pk2(x0.z, x0.w), pk2(x1.x, x1.y), pk2(x1.z, x1.w)};
+        rs[u] = entry_row8_f(c2, make_float4(ah, 0.f, S, 0.f), cpp, ngh2, ngl2, cacc2);
+      }
+      const double tot = (double)warp_reduce4_f(rs[0], rs[1], rs[2], rs[3], lane);
+      const int rw = 4 * g + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+      const float Mrow = __shfl_sync(0xffffffffu, rq.y, rw);
+      const int64_t i = i0 + (int64_t)k * kTmaRows + rw;
+      if ((lane & 7) == 0 && i < nrows) a.rowpart[(int64_t)tc * nrows + i] = tot * (double)Mrow;
+      if (++grp == MDOT_K1_COLFLUSH) {
+        grp = 0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          float lo, hi;
+          up2(cacc2[p], lo, hi);
+          csum[4 * lane + ((2 * p) & 3) + 128 * ((2 * p) >> 2)] += (double)lo;
+          csum[4 * lane + ((2 * p + 1) & 3) + 128 * ((2 * p + 1) >> 2)] += (double)hi;
+          cacc2[p] = 0ull;
+        }
+      }
+    }
+    // every row of the stage has been read: release the slot (generic-proxy
+    // reads before the async-proxy refill, as in tma_consume_tile)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float lo, hi;
+    up2(cacc2[p], lo, hi);
+    csum[4 * lane + ((2 * p) & 3) + 128 * ((2 * p) >> 2)] += (double)lo;
+    csum[4 * lane + ((2 * p + 1) & 3) + 128 * ((2 * p + 1) >> 2)] += (double)hi;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+    if (j < n) a.colpart[(int64_t)tr * n + j] = csum[4 * lane + (q & 3) + 128 * (q >> 2)] * (double)__ldg(&a.colp[j]).y;
+  }
+}
+
 }  // namespace mdot

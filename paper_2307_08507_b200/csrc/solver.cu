@@ -1661,6 +1661,8 @@ static mdot_status solve_batch_lockstep(const mdot_problem* shared, int32_t Bn, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = 2 * sms;
   Workspace& w0 = *W[0];
+  // K1 with shared C reads (MDOT_BATCH_SHARED_C=0: one pass per instance, A/B)
+  const bool shared_c = !(getenv("MDOT_BATCH_SHARED_C") && atoi(getenv("MDOT_BATCH_SHARED_C")) == 0);
   // one graph of K slots [ctrl, prep, K1, finalize] for the whole batch (~2 ms of work)
   cudaStream_t cap = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -1669,7 +1671,8 @@ static mdot_status solve_batch_lockstep(const mdot_problem* shared, int32_t Bn, 
   auto slot = [&](cudaStream_t s2, bool with_ctrl) -> mdot_status {
     if (with_ctrl) CK(launch_ctrl_multi(dc, Bn, done_d, s2));
     CK(launch_prep_multi(dp, hp[0], Bn, s2));
-    CK(launch_eval_tma_multi(w0.tmap, de, Bn, grid, s2));
+    if (shared_c) CK(launch_eval_tma_shared(w0.tmap, de, Bn, grid, s2));
+    else CK(launch_eval_tma_multi(w0.tmap, de, Bn, grid, s2));
     CK(launch_finalize_multi(df, hf[0], Bn, s2));
     return MDOT_OK;
   };

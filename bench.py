@@ -631,6 +631,9 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
 
 
 def main():
+    # keep stdout to the one JSON line (NCCL prints its version banner to
+    # stdout at INFO/VERSION levels)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -212,7 +212,7 @@ def run_reference(a, rank, world):
             "impl": "reference",
             "cpu_baseline": {k: steps[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "evals/s"},
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(a, rank, world, local_rank):
@@ -509,7 +509,7 @@ def run_ours(a, rank, world, local_rank):
     if comm is not None:
         M.mdot_comm_destroy(comm)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -630,10 +630,26 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
     return out
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The JSON line goes to the real stdout; everything else libraries write
+    to fd 1 (e.g. the NCCL version banner torch prints when a communicator
+    comes up) was redirected to stderr by main()."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
-    # keep stdout to the one JSON line (NCCL prints its version banner to
-    # stdout at INFO/VERSION levels)
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -71,6 +71,9 @@ def parse():
                     help="skip the config-5 block (n=65536, d=16, on-the-fly cost; north_star scaling target)")
     ap.add_argument("--c5-evals", type=int, default=48,
                     help="config-5 step = the first K O(n^2) evaluations of the config-5 solve (fixed budget)")
+    ap.add_argument("--c5-recipe", default="dot", choices=["dot", "diff"],
+                    help="on-the-fly cost recipe of the config-5 block: dot form (Z22b, d + 7 FP32 ops per pair) "
+                         "or difference form (Z22, 2d + 5)")
     ap.add_argument("--c5-full", type=int, default=1,
                     help="also time one complete config-5 solve to L1 1e-5 (time-to-eps; ~10 s on one B200)")
     ap.add_argument("--adaptive-gamma-leg", type=float, default=256.0,
@@ -523,8 +526,9 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
     evaluation.  A step is the first --c5-evals O(n^2)
     evaluations of the solve (fixed budget, so the driver's 20 steps fit);
     the complete solve is timed once more for time-to-eps.  Roofline: K2 is
-    bound by the FP32 pipe (2d + 5 = 37 FP32 ops per pair, K2), peak
-    = 148 SMs x 128 FP32 lanes x 1.965 GHz / 37 (B200_PROFILING.md unit counts);
+    bound by the FP32 pipe (d + 7 = 23 FMA-pipe ops per pair for the dot form,
+    2d + 5 = 37 for the difference form; K2), peak = 148 SMs x 128
+    FP32 lanes x 1.965 GHz / ops (unit counts measured, profiles/r02_mufu_ffma2_rate.txt);
     the MUFU floor (1 ex2 per pair, 16 per SM per clock) is reported beside it."""
     import numpy as np
     import torch
@@ -547,9 +551,10 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
         o = M.options(eps=eps, time_kernels=1, max_evals=max_evals)
         if comm is not None:
             return M.mdot_solve_sharded(comm, row0, nloc, X_local=X, Y=Y, scale=inst.scale, r=r, c=c, n=n,
-                                        schedule=sched, options=o, u_local_out=U, v_out=V, check=False)
+                                        schedule=sched, options=o, u_local_out=U, v_out=V, check=False,
+                                        recipe=a.c5_recipe)
         return M.mdot_solve(X=X, Y=Y, scale=inst.scale, r=r, c=c, schedule=sched, options=o, u_out=U, v_out=V,
-                            check=False)
+                            check=False, recipe=a.c5_recipe)
 
     def maxr(x):
         if dist is None:
@@ -582,10 +587,13 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
         t = torch.tensor([achieved], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         achieved = float(t.item())
-    fp32_peak = world * 148 * 128 * 1.965e9 / (2 * d + 5)
+    ops = (d + 7) if a.c5_recipe == "dot" else (2 * d + 5)   # FMA-pipe ops per pair (power-of-two scale folded)
+    fp32_peak = world * 148 * 128 * 1.965e9 / ops
     mufu_peak = world * 148 * 16 * 1.965e9
     out = {
-        "workload": f"cfg5-otf-n{n}-d{d}-dirichlet1-gbar4096-T16-L1eps1e-05",
+        "workload": f"cfg5-otf-n{n}-d{d}-dirichlet1-gbar4096-T16-L1eps1e-05-{a.c5_recipe}",
+        "cost_recipe": ("dot form (Z22b): max(fmaf(-2, x.y, |x|^2 + |y|^2), 0) / 16" if a.c5_recipe == "dot"
+                        else "difference form (Z22): fmaf chain of (x - y)^2, / 16"),
         "step": f"first {K} O(n^2) evaluations of the solve (fixed budget per step)",
         "parallelism": f"rows of X sharded x{world}" if world > 1 else "1 GPU",
         "exchange": "NCCL allreduce of [column totals | row scalars] per evaluation in CUDA-graph slots"
@@ -595,7 +603,7 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
         "roofline": {"kernel": "k_eval_otf<16> (K2: on-the-fly cost, fused marginals)", "bound": "alu",
                      "achieved": achieved / 1e9 if achieved else None, "unit": "Gpairs/s",
                      "peak": fp32_peak / 1e9, "frac": (achieved / fp32_peak) if achieved else None,
-                     "peak_source": "FP32 pipe: 148 SMs x 128 lanes x 1.965 GHz / (2d+5 = 37 ops per pair)",
+                     "peak_source": f"FP32 pipe: 148 SMs x 128 lanes x 1.965 GHz / ({ops} ops per pair)",
                      "mufu_floor_frac": (achieved / mufu_peak) if achieved else None,
                      "mean_launch_ms": launch_s * 1e3, "launches_timed": kn,
                      "traffic": None},
@@ -617,7 +625,7 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
         # the oracle's pair rate on this host: exact fp64 log-marginals of 32
         # sampled rows of the same instance at the same potentials (O(n d) each)
         import oracle as O
-        prob = O.OracleProblem(inst)
+        prob = O.OracleProblem(inst, recipe=a.c5_recipe)
         rows_s = np.arange(0, n, n // 32)[:32]
         A0, B0 = np.log(inst.r), np.log(inst.c)
         t0 = time.perf_counter()

@@ -51,8 +51,12 @@ typedef enum {
 
 typedef enum {
   MDOT_COST_DENSE_F32 = 0,     /* C: const float*  (n*n) */
-  MDOT_COST_SQEUCLID_F32 = 1,  /* X, Y: const float* (n*d), scale */
-  MDOT_COST_DENSE_F64 = 2      /* C: const double* (n*n) */
+  MDOT_COST_SQEUCLID_F32 = 1,  /* X, Y: const float* (n*d), scale; the difference recipe (Z22):
+                                  acc = fmaf(x_k - y_k, x_k - y_k, acc) for k = 0..d-1, C = acc * scale */
+  MDOT_COST_DENSE_F64 = 2,     /* C: const double* (n*n) */
+  MDOT_COST_SQEUCLID_DOT_F32 = 3  /* the same squared distance in dot form (Z22b), 2d + 5 -> d + 7 FP32 ops per pair:
+                                  nx = fmaf chain of x_k^2, ny likewise, s = fmaf chain of x_k y_k (k = 0..d-1),
+                                  C = max(fmaf(-2, s, nx + ny), 0) * scale, every step one fp32 rounding */
 } mdot_cost_kind;
 
 typedef enum { MDOT_MEM_HOST = 0, MDOT_MEM_DEVICE = 1 } mdot_mem;

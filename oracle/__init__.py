@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "mdot_oracle.c")
 
-DENSE_F32, SQEUCLID_F32, DENSE_F64 = 0, 1, 2
+DENSE_F32, SQEUCLID_F32, DENSE_F64, SQEUCLID_DOT_F32 = 0, 1, 2, 3
 PNCG, SINKHORN, NCG, PNCG_JACOBI = 0, 1, 2, 3
 BETA_PPR, BETA_PPR_AF, BETA_PFR, BETA_PPR_PRINTED, BETA_PPR_PLUS = 0, 1, 2, 3, 4
 WARM_SCALED, WARM_CARRY, WARM_ZERO = 0, 1, 2
@@ -116,7 +116,7 @@ def _ptr(a):
 class OracleProblem:
     """Holds contiguous arrays alive for the C side."""
 
-    def __init__(self, inst=None, *, C=None, r=None, c=None, X=None, Y=None, scale=0.0):
+    def __init__(self, inst=None, *, C=None, r=None, c=None, X=None, Y=None, scale=0.0, recipe="diff"):
         if inst is not None:
             C, r, c, X, Y, scale = inst.C, inst.r, inst.c, inst.X, inst.Y, inst.scale
             if C is not None:
@@ -137,7 +137,7 @@ class OracleProblem:
         else:
             self.X = np.ascontiguousarray(X, dtype=np.float32)
             self.Y = np.ascontiguousarray(Y, dtype=np.float32)
-            kind = SQEUCLID_F32
+            kind = SQEUCLID_DOT_F32 if recipe == "dot" else SQEUCLID_F32   # Z22 / Z22b
             d = self.X.shape[1]
         self.kind = kind
         self.s = Problem(self.n, kind, d, _ptr(self.C), _ptr(self.X), _ptr(self.Y),

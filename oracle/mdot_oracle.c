@@ -39,6 +39,18 @@ double orc_cost(const orc_problem* pb, int64_t i, int64_t j) {
   const int64_t n = pb->n;
   if (pb->kind == ORC_DENSE_F32) return (double)((const float*)pb->C)[i * n + j];
   if (pb->kind == ORC_DENSE_F64) return ((const double*)pb->C)[i * n + j];
+  if (pb->kind == ORC_SQEUCLID_DOT_F32) {
+    /* Z22b: C = max(fl(nx + ny) - 2 s, 0) * scale, each fp32 step rounded once */
+    const float* x = pb->X + i * pb->d;
+    const float* y = pb->Y + j * pb->d;
+    float nx = 0.0f, ny = 0.0f, sxy = 0.0f;
+    for (int k = 0; k < pb->d; ++k) nx = fmaf(x[k], x[k], nx);
+    for (int k = 0; k < pb->d; ++k) ny = fmaf(y[k], y[k], ny);
+    for (int k = 0; k < pb->d; ++k) sxy = fmaf(x[k], y[k], sxy);
+    const float t = nx + ny;
+    const float cij = fmaxf(fmaf(-2.0f, sxy, t), 0.0f) * pb->scale;
+    return (double)cij;
+  }
   {
     const float* x = pb->X + i * pb->d;
     const float* y = pb->Y + j * pb->d;

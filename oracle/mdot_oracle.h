@@ -17,7 +17,10 @@
 extern "C" {
 #endif
 
-enum { ORC_DENSE_F32 = 0, ORC_SQEUCLID_F32 = 1, ORC_DENSE_F64 = 2 };
+/* ORC_SQEUCLID_DOT_F32 (Z22b): the dot form of the same squared distance with
+ * its own fixed fp32 op order, nx = fmaf chain of x_k^2, ny likewise, s = fmaf
+ * chain of x_k y_k, C = max(fmaf(-2, s, nx + ny), 0) * scale. */
+enum { ORC_DENSE_F32 = 0, ORC_SQEUCLID_F32 = 1, ORC_DENSE_F64 = 2, ORC_SQEUCLID_DOT_F32 = 3 };
 /* ORC_PNCG_JACOBI: Alg. 2 with the Jacobi preconditioner diag(Hessian)^-1 in place
  * of the Sinkhorn direction (SURVEY 8(f) rank 2 ablation; Hessian PAPER.md:225). */
 enum { ORC_PNCG = 0, ORC_SINKHORN = 1, ORC_NCG = 2, ORC_PNCG_JACOBI = 3 };

@@ -21,6 +21,7 @@ from ._binding import (  # noqa: F401
     MDOT_BETA_PPR_PLUS,
     MDOT_COST_DENSE_F32,
     MDOT_COST_DENSE_F64,
+    MDOT_COST_SQEUCLID_DOT_F32,
     MDOT_COST_SQEUCLID_F32,
     MDOT_PREC_AUTO,
     MDOT_PREC_F32P,

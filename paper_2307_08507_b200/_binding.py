@@ -10,7 +10,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MDOT_LIB: load another build of the same library (A/B experiments only)
 LIB_PATH = os.environ.get("MDOT_LIB") or os.path.join(_HERE, "libmdot_b200.so")
 
-MDOT_COST_DENSE_F32, MDOT_COST_SQEUCLID_F32, MDOT_COST_DENSE_F64 = 0, 1, 2
+MDOT_COST_DENSE_F32, MDOT_COST_SQEUCLID_F32, MDOT_COST_DENSE_F64, MDOT_COST_SQEUCLID_DOT_F32 = 0, 1, 2, 3
 MDOT_MEM_HOST, MDOT_MEM_DEVICE = 0, 1
 MDOT_SCHED_FIXED, MDOT_SCHED_DOUBLING, MDOT_SCHED_EXPLICIT, MDOT_SCHED_ADAPTIVE = 0, 1, 2, 3
 MDOT_PROJ_PNCG, MDOT_PROJ_SINKHORN, MDOT_PROJ_NCG, MDOT_PROJ_PNCG_JACOBI = 0, 1, 2, 3
@@ -182,8 +182,10 @@ def _current_stream():
     return ct.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def problem(C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, n=None):
-    """Build an mdot_problem; keeps references to the arrays on the struct."""
+def problem(C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, n=None, recipe="diff"):
+    """Build an mdot_problem; keeps references to the arrays on the struct.
+    recipe selects the on-the-fly cost's fp32 op sequence: "diff" (Z22,
+    MDOT_COST_SQEUCLID_F32) or "dot" (Z22b, MDOT_COST_SQEUCLID_DOT_F32)."""
     ref = C if C is not None else X
     dev = _is_cuda(ref)
     if C is not None:
@@ -191,7 +193,9 @@ def problem(C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, n=None):
         nn = C.shape[0] if n is None else n
         d = 0
     else:
-        kind = MDOT_COST_SQEUCLID_F32
+        if recipe not in ("diff", "dot"):
+            raise ValueError(f"recipe {recipe!r}: 'diff' or 'dot'")
+        kind = MDOT_COST_SQEUCLID_DOT_F32 if recipe == "dot" else MDOT_COST_SQEUCLID_F32
         nn = Y.shape[0] if n is None else n
         d = X.shape[1]
     pb = Problem(nn, kind, MDOT_MEM_DEVICE if dev else MDOT_MEM_HOST, _ptr(C, F32_OR_F64, "C", dev), d,
@@ -244,8 +248,8 @@ def _check(st, what):
         raise MdotError(st, f"{what}: {mdot_last_error()}")
 
 
-def _solve(fn, C, r, c, X, Y, scale, sched, opts, u_out, v_out, P_out, check):
-    pb = problem(C, r, c, X=X, Y=Y, scale=scale)
+def _solve(fn, C, r, c, X, Y, scale, sched, opts, u_out, v_out, P_out, check, recipe="diff"):
+    pb = problem(C, r, c, X=X, Y=Y, scale=scale, recipe=recipe)
     sched = sched if sched is not None else schedule()
     opts = opts if opts is not None else options()
     if pb.mem == MDOT_MEM_DEVICE:
@@ -262,15 +266,15 @@ def _solve(fn, C, r, c, X, Y, scale, sched, opts, u_out, v_out, P_out, check):
 
 
 def mdot_solve(C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, schedule=None, options=None,
-               u_out=None, v_out=None, P_out=None, check=True):
+               u_out=None, v_out=None, P_out=None, check=True, recipe="diff"):
     """MDOT-PNCG solve; returns the mdot_result as a dict."""
-    return _solve(lib().mdot_solve, C, r, c, X, Y, scale, schedule, options, u_out, v_out, P_out, check)
+    return _solve(lib().mdot_solve, C, r, c, X, Y, scale, schedule, options, u_out, v_out, P_out, check, recipe)
 
 
 def mdot_sinkhorn(C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, schedule=None, options=None,
-                  u_out=None, v_out=None, P_out=None, check=True):
+                  u_out=None, v_out=None, P_out=None, check=True, recipe="diff"):
     """Same solve with Sinkhorn projections (Alg. 3) on the same kernels."""
-    return _solve(lib().mdot_sinkhorn, C, r, c, X, Y, scale, schedule, options, u_out, v_out, P_out, check)
+    return _solve(lib().mdot_sinkhorn, C, r, c, X, Y, scale, schedule, options, u_out, v_out, P_out, check, recipe)
 
 
 def mdot_solve_batch(C, R, Cm, *, schedule=None, options=None, u_out=None, v_out=None, check=True):
@@ -290,9 +294,9 @@ def mdot_solve_batch(C, R, Cm, *, schedule=None, options=None, u_out=None, v_out
 
 
 def mdot_marginals(A, B, gbar, C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, lr=None, lc=None,
-                   options=None, check=True):
+                   options=None, check=True, recipe="diff"):
     """One fused evaluation: (log r(P), log c(P)) for P = exp(A + B - gbar C)."""
-    pb = problem(C, r, c, X=X, Y=Y, scale=scale)
+    pb = problem(C, r, c, X=X, Y=Y, scale=scale, recipe=recipe)
     opts = options if options is not None else globals()["options"]()
     if pb.mem == MDOT_MEM_DEVICE:
         import torch
@@ -312,8 +316,8 @@ def mdot_marginals(A, B, gbar, C=None, r=None, c=None, *, X=None, Y=None, scale=
 
 
 def mdot_round(U, V, gbar, C=None, r=None, c=None, *, X=None, Y=None, scale=0.0, P_out=None,
-               options=None, check=True):
-    pb = problem(C, r, c, X=X, Y=Y, scale=scale)
+               options=None, check=True, recipe="diff"):
+    pb = problem(C, r, c, X=X, Y=Y, scale=scale, recipe=recipe)
     opts = options if options is not None else globals()["options"]()
     if pb.mem == MDOT_MEM_DEVICE:
         opts.stream = _current_stream()
@@ -362,8 +366,8 @@ def mdot_comm_destroy(comm):
 
 def mdot_solve_sharded(comm, row0, n_local, C_local=None, r=None, c=None, *, X_local=None, Y=None,
                        scale=0.0, n=None, schedule=None, options=None, u_local_out=None, v_out=None,
-                       check=True):
-    pb = problem(C_local, r, c, X=X_local, Y=Y, scale=scale, n=n if n is not None else len(c))
+                       check=True, recipe="diff"):
+    pb = problem(C_local, r, c, X=X_local, Y=Y, scale=scale, n=n if n is not None else len(c), recipe=recipe)
     sched = schedule if schedule is not None else globals()["schedule"]()
     opts = options if options is not None else globals()["options"]()
     if pb.mem == MDOT_MEM_DEVICE:

@@ -85,6 +85,7 @@ struct EvalArgs {
   const float* Y;          // on-the-fly: [n x d]
   int d;
   float scale;
+  int otf_dot;             // on-the-fly cost recipe: 0 diff (Z22), 1 dot form (Z22b; otf_cost.cuh)
   int64_t n;               // number of columns (global n)
   int64_t nrows;           // number of rows evaluated (local rows)
   int tile_m;              // rows per tile (multiple of kWarps*kUnroll)
@@ -119,7 +120,7 @@ cudaError_t launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st);
 // shard) and column (max, sum) partials.
 struct ExactArgs {
   const void* C; int64_t ldc; int c_f64;  // dense (fp32 or fp64)
-  const float* X; const float* Y; int d; float scale; int otf;
+  const float* X; const float* Y; int d; float scale; int otf;   // otf: 0 dense, 1 diff recipe, 2 dot recipe
   int64_t n, nrows;
   const double* A;   // [nrows]
   const double* B;   // [n]
@@ -363,7 +364,7 @@ cudaError_t launch_sum_chunks(const double* x, int chunks, int64_t n, double* ou
 // target, so a pass drops < n * 2e-22 of total mass (1.3e-17 at n = 65536).
 struct RoundArgs {
   const void* C; int64_t ldc; int c_f64;
-  const float* X; const float* Y; int d; float scale; int otf;
+  const float* X; const float* Y; int d; float scale; int otf;   // otf: 0 dense, 1 diff recipe, 2 dot recipe
   int64_t n, nrows;
   double gbar;
   const double* A;      // row exponent base of the pass (U or U + log x)

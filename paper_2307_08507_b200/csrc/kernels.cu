@@ -24,6 +24,7 @@
 #include "entry.cuh"
 #include "internal.cuh"
 #include "ops.cuh"
+#include "otf_cost.cuh"
 
 namespace mdot {
 
@@ -162,6 +163,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
               cv[u][q] = (j < n) ? ld_stream1(a.C + i * a.ldc + j) : 0.f;
             }
           }
+        } else if (a.otf_dot) {
+          // Z22b: C_ij = max(fmaf(-2, s, fl(nx_i + ny_j)), 0) * scale (otf_cost.cuh)
+          const float* xr = a.X + i * a.d;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+            cv[u][q] = (j < n) ? (float)otf_cost(xr, a.Y + j * a.d, a.d, a.scale, 2) : 0.f;
+          }
         } else {
           // C_ij = fl32(fmaf chain over k of (x_ik - y_jk)^2) * scale  (Z22)
           float acc[8];
@@ -283,7 +292,7 @@ constexpr int kOtfChunk = 128;
 // POW2: scale is a power of two, so C = acc * scale is exact and -g * C ==
 // (-g * scale) * acc exactly: the scale folds into (gh, gl) and the FMUL2 per
 // pair of entries disappears, with the Z22 recipe's bits unchanged.
-template <int D, bool POW2>
+template <int D, bool POW2, bool DOT>
 __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -294,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 
   __shared__ double sred[kWarps][kTileN];
   __shared__ float4 sRP[2][kOtfChunk];   // row parameters, double-buffered by chunk
+  __shared__ float sNX[DOT ? kOtfChunk : 1];   // Z22b: squared norms of the chunk's rows
   extern __shared__ __align__(16) unsigned char sraw[];
   float* sY = reinterpret_cast<float*>(sraw);                          // [D][256]
   float* sX = reinterpret_cast<float*>(sraw + sizeof(float) * D * kTileN);   // [2][chunk][D]
@@ -357,6 +367,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) sY[k * kTileN + threadIdx.x] = yv[k];
+    if (DOT) {   // this column's squared norm (Z22b), kept in sred until the pairs are built
+      float ny = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) ny = __fmaf_rn(yv[k], yv[k], ny);
+      reinterpret_cast<float*>(&sred[0][0])[threadIdx.x] = ny;
+    }
+  }
+  u64 ny2[DOT ? 4 : 1];   // the lane's column pairs' squared norms
+  if (DOT) {
+    __syncthreads();
+    const float* sny = reinterpret_cast<const float*>(&sred[0][0]);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int c = 4 * lane + ((2 * p) & 3) + 128 * ((2 * p) >> 2);
+      ny2[p & (DOT ? 3 : 0)] = pk2(sny[c], sny[c + 1]);
+    }
+    __syncthreads();   // sred is reused for the column sums at the end
   }
 
   ColPairs cpp;
@@ -402,6 +429,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
       __syncthreads();
     }
     const float* xs = sX + buf * kOtfChunk * D;
+    if (DOT) {   // the chunk's row squared norms (Z22b)
+      if ((int)threadIdx.x < kOtfChunk) {
+        float nx = 0.f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) nx = __fmaf_rn(xs[threadIdx.x * D + k], xs[threadIdx.x * D + k], nx);
+        sNX[threadIdx.x & (DOT ? kOtfChunk - 1 : 0)] = nx;
+      }
+      __syncthreads();
+    }
     for (int rb = 4 * warp; rb < rows_c; rb += kWarps * kUnroll) {
       u64 acc[kUnroll][4];
 #pragma unroll
@@ -417,11 +453,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         for (int u = 0; u < kUnroll; ++u) {
           const float x = xs[(rb + u) * D + k];
           const u64 xx = pk2(x, x);   // ptxas: a broadcast (.F32) operand of the packed ops
-          u64 dk;
-          dk = sub2(xx, ya.x); acc[u][0] = fma2(dk, dk, acc[u][0]);
-          dk = sub2(xx, ya.y); acc[u][1] = fma2(dk, dk, acc[u][1]);
-          dk = sub2(xx, yb.x); acc[u][2] = fma2(dk, dk, acc[u][2]);
-          dk = sub2(xx, yb.y); acc[u][3] = fma2(dk, dk, acc[u][3]);
+          if (DOT) {   // s = fmaf chain of x_k y_k (Z22b)
+            acc[u][0] = fma2(xx, ya.x, acc[u][0]);
+            acc[u][1] = fma2(xx, ya.y, acc[u][1]);
+            acc[u][2] = fma2(xx, yb.x, acc[u][2]);
+            acc[u][3] = fma2(xx, yb.y, acc[u][3]);
+          } else {
+            u64 dk;
+            dk = sub2(xx, ya.x); acc[u][0] = fma2(dk, dk, acc[u][0]);
+            dk = sub2(xx, ya.y); acc[u][1] = fma2(dk, dk, acc[u][1]);
+            dk = sub2(xx, yb.x); acc[u][2] = fma2(dk, dk, acc[u][2]);
+            dk = sub2(xx, yb.y); acc[u][3] = fma2(dk, dk, acc[u][3]);
+          }
+        }
+      }
+      if (DOT) {   // C / scale = max(fmaf(-2, s, fl(nx_i + ny_j)), 0), pairwise
+        const u64 m2 = pk2(-2.0f, -2.0f);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const float nx = sNX[(rb + u) & (kOtfChunk - 1)];
+          const u64 nx2 = pk2(nx, nx);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            float lo, hi;
+            up2(fma2(m2, acc[u][p], add2(nx2, ny2[p & (DOT ? 3 : 0)])), lo, hi);
+            acc[u][p] = pk2(fmaxf(lo, 0.f), fmaxf(hi, 0.f));
+          }
         }
       }
 #if MDOT_K2_ROWRED_F32
@@ -488,24 +545,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   }
 }
 
-template <int D, bool POW2>
+template <int D, bool POW2, bool DOT>
 static cudaError_t launch_otf_pt(const EvalArgs& a, cudaStream_t st) {
   dim3 grid(a.n_col_tiles, a.n_row_tiles);
   const size_t smem = sizeof(float) * D * kTileN + sizeof(float) * 2 * kOtfChunk * D;
   static bool attr_set = false;
   if (!attr_set) {   // static (column sums, row parameters) + dynamic exceeds the 48 KB default
-    cudaError_t e = cudaFuncSetAttribute(k_eval_otf<D, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_eval_otf<D, POW2, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_eval_otf<D, POW2><<<grid, kThreads, smem, st>>>(a);
+  k_eval_otf<D, POW2, DOT><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 template <int D>
 static cudaError_t launch_otf_t(const EvalArgs& a, cudaStream_t st) {
   int e2 = 0;
   const bool pow2 = a.scale > 0.f && frexpf(a.scale, &e2) == 0.5f && e2 > -100 && e2 < 100;
-  return pow2 ? launch_otf_pt<D, true>(a, st) : launch_otf_pt<D, false>(a, st);
+  if (a.otf_dot) return pow2 ? launch_otf_pt<D, true, true>(a, st) : launch_otf_pt<D, false, true>(a, st);
+  return pow2 ? launch_otf_pt<D, true, false>(a, st) : launch_otf_pt<D, false, false>(a, st);
 }
 
 template <int KIND, bool VEC4>
@@ -545,16 +603,7 @@ cudaError_t launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st) {
 // column over a chunk of rows, (max, sum) partials per chunk.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double exact_cost(const ExactArgs& a, int64_t i, int64_t j) {
-  if (a.otf) {
-    const float* x = a.X + i * a.d;
-    const float* y = a.Y + j * a.d;
-    float acc = 0.f;
-    for (int k = 0; k < a.d; ++k) {
-      const float dk = __fsub_rn(x[k], y[k]);
-      acc = __fmaf_rn(dk, dk, acc);
-    }
-    return (double)__fmul_rn(acc, a.scale);
-  }
+  if (a.otf) return otf_cost(a.X + i * a.d, a.Y + j * a.d, a.d, a.scale, a.otf);
   if (a.c_f64) return reinterpret_cast<const double*>(a.C)[i * a.ldc + j];
   return (double)reinterpret_cast<const float*>(a.C)[i * a.ldc + j];
 }

@@ -30,23 +30,24 @@
 #include <algorithm>
 
 #include "internal.cuh"
+#include "otf_cost.cuh"
 
 namespace mdot {
 
 constexpr double kRoundSkip = 50.0;
 constexpr int kRT = 128;   // rows / columns per on-the-fly tile and per CTA
 
-__device__ __forceinline__ float sqd_recipe(const float* x, const float* y, int d) {
-  float acc = 0.f;
-  for (int k = 0; k < d; ++k) {
-    const float dk = __fsub_rn(x[k], y[k]);
-    acc = __fmaf_rn(dk, dk, acc);
+// unscaled pair cost with the thread's own point in registers (x, its squared
+// norm nx for the dot form) and the other point y (norm ny) from shared memory;
+// the dot form is symmetric bit for bit (fl(nx + ny) and the exact products)
+template <int D, bool DOT>
+__device__ __forceinline__ float pair_cost_t(const float (&x)[D], float nx, const float* y, float ny) {
+  if (DOT) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) s = __fmaf_rn(x[k], y[k], s);
+    return fmaxf(__fmaf_rn(-2.0f, s, __fadd_rn(nx, ny)), 0.0f);
   }
-  return acc;
-}
-
-template <int D>
-__device__ __forceinline__ float sqd_recipe_t(const float (&x)[D], const float* y) {
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -54,6 +55,13 @@ __device__ __forceinline__ float sqd_recipe_t(const float (&x)[D], const float* 
     acc = __fmaf_rn(dk, dk, acc);
   }
   return acc;
+}
+template <int D>
+__device__ __forceinline__ float sqnorm_t(const float (&x)[D]) {
+  float a = 0.f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) a = __fmaf_rn(x[k], x[k], a);
+  return a;
 }
 
 // ---------------------------------------------------------------- dense rows
@@ -129,16 +137,18 @@ __global__ void __launch_bounds__(256) k_round_cols_dense(RoundArgs a) {
 // ---------------------------------------------------------- on-the-fly rows
 // thread per row (128 rows per CTA), columns of chunk blockIdx.y in tiles of
 // 128: Y tile, B and err_c staged in shared memory, read as broadcasts
-template <int D, bool CORR>
+template <int D, bool CORR, bool DOT>
 __global__ void __launch_bounds__(kRT) k_round_rows_otf(RoundArgs a) {
   __shared__ __align__(16) float sY[kRT * D];
   __shared__ double sB[kRT], sE[kRT];
+  __shared__ float sN[kRT];
   const int t = threadIdx.x;
   const int64_t i = (int64_t)blockIdx.x * kRT + t;
   const bool ok = i < a.nrows;
   float x[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) x[k] = ok ? a.X[i * D + k] : 0.f;
+  const float nx = DOT ? sqnorm_t<D>(x) : 0.f;
   const double Ai = ok ? a.A[i] : 0.0, thr = ok ? a.logr[i] - kRoundSkip : INFINITY, g = a.gbar;
   const int64_t cols_per = ((a.n + a.chunks - 1) / a.chunks + kRT - 1) / kRT * kRT;
   const int64_t jb = (int64_t)blockIdx.y * cols_per;
@@ -153,8 +163,12 @@ __global__ void __launch_bounds__(kRT) k_round_rows_otf(RoundArgs a) {
       if (CORR) sE[t] = a.ec[j0 + t];
     }
     __syncthreads();
+    if (DOT) {   // column squared norms of the tile (Z22b), one per thread
+      if (t < w) sN[t] = sqnorm_recipe(sY + t * D, D);
+      __syncthreads();
+    }
     for (int jj = 0; jj < w; ++jj) {
-      const double cij = (double)__fmul_rn(sqd_recipe_t<D>(x, sY + jj * D), a.scale);
+      const double cij = (double)__fmul_rn(pair_cost_t<D, DOT>(x, nx, sY + jj * D, DOT ? sN[jj] : 0.f), a.scale);
       const double z = (Ai + sB[jj]) - g * cij;
       if (z > thr) {
         const double f = exp(z);
@@ -176,16 +190,18 @@ __global__ void __launch_bounds__(kRT) k_round_rows_otf(RoundArgs a) {
 // ------------------------------------------------------- on-the-fly columns
 // thread per column (128 columns per CTA), rows of chunk blockIdx.y in tiles
 // of 128: X tile and A staged in shared memory
-template <int D>
+template <int D, bool DOT>
 __global__ void __launch_bounds__(kRT) k_round_cols_otf(RoundArgs a) {
   __shared__ __align__(16) float sX[kRT * D];
   __shared__ double sA[kRT];
+  __shared__ float sN[kRT];
   const int t = threadIdx.x;
   const int64_t j = (int64_t)blockIdx.x * kRT + t;
   const bool ok = j < a.n;
   float y[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) y[k] = ok ? a.Y[j * D + k] : 0.f;
+  const float ny = DOT ? sqnorm_t<D>(y) : 0.f;
   const double Bj = ok ? a.B[j] : 0.0, thr = ok ? a.logc[j] - kRoundSkip : INFINITY, g = a.gbar;
   const int64_t rows_per = ((a.nrows + a.chunks - 1) / a.chunks + kRT - 1) / kRT * kRT;
   const int64_t ib = (int64_t)blockIdx.y * rows_per;
@@ -197,10 +213,14 @@ __global__ void __launch_bounds__(kRT) k_round_cols_otf(RoundArgs a) {
     for (int q = t; q < kRT * D; q += kRT) sX[q] = (q / D < w) ? a.X[i0 * D + q] : 0.f;
     if (t < w) sA[t] = a.A[i0 + t];
     __syncthreads();
+    if (DOT) {
+      if (t < w) sN[t] = sqnorm_recipe(sX + t * D, D);
+      __syncthreads();
+    }
     for (int ii = 0; ii < w; ++ii) {
-      // the recipe is symmetric in the operand order only up to the sign of
-      // x - y, whose square is exact: (x_k - y_k)^2 == (y_k - x_k)^2 bitwise
-      const double cij = (double)__fmul_rn(sqd_recipe_t<D>(y, sX + ii * D), a.scale);
+      // the diff recipe is symmetric in the operand order only up to the sign
+      // of x - y, whose square is exact: (x_k - y_k)^2 == (y_k - x_k)^2 bitwise
+      const double cij = (double)__fmul_rn(pair_cost_t<D, DOT>(y, ny, sX + ii * D, DOT ? sN[ii] : 0.f), a.scale);
       const double z = (sA[ii] + Bj) - g * cij;
       if (z > thr) s += exp(z);
     }
@@ -217,7 +237,7 @@ __global__ void __launch_bounds__(256) k_round_rows_otf_any(RoundArgs a) {
   const double Ai = a.A[i], thr = a.logr[i] - kRoundSkip, g = a.gbar;
   double s = 0.0, cs = 0.0, cr = 0.0;
   for (int64_t j = lane; j < a.n; j += 32) {
-    const double cij = (double)__fmul_rn(sqd_recipe(a.X + i * a.d, a.Y + j * a.d, a.d), a.scale);
+    const double cij = otf_cost(a.X + i * a.d, a.Y + j * a.d, a.d, a.scale, a.otf);
     const double z = (Ai + a.B[j]) - g * cij;
     if (z > thr) {
       const double f = exp(z);
@@ -248,7 +268,7 @@ __global__ void __launch_bounds__(256) k_round_cols_otf_any(RoundArgs a) {
   const double Bj = a.B[j], thr = a.logc[j] - kRoundSkip, g = a.gbar;
   double s = 0.0;
   for (int64_t i = ib; i < ie; ++i) {
-    const double cij = (double)__fmul_rn(sqd_recipe(a.X + i * a.d, a.Y + j * a.d, a.d), a.scale);
+    const double cij = otf_cost(a.X + i * a.d, a.Y + j * a.d, a.d, a.scale, a.otf);
     const double z = (a.A[i] + Bj) - g * cij;
     if (z > thr) s += exp(z);
   }
@@ -261,7 +281,7 @@ __global__ void k_round_plan(RoundArgs a) {
   const int64_t i = blockIdx.y;
   if (j >= a.n || i >= a.nrows) return;
   double cij;
-  if (a.otf) cij = (double)__fmul_rn(sqd_recipe(a.X + i * a.d, a.Y + j * a.d, a.d), a.scale);
+  if (a.otf) cij = otf_cost(a.X + i * a.d, a.Y + j * a.d, a.d, a.scale, a.otf);
   else if (a.c_f64) cij = reinterpret_cast<const double*>(a.C)[i * a.ldc + j];
   else cij = (double)reinterpret_cast<const float*>(a.C)[i * a.ldc + j];
   double gij = exp((a.A[i] + a.B[j]) - a.gbar * cij);
@@ -352,14 +372,21 @@ int round_chunks(const RoundArgs& a, bool rows) {
 template <int D>
 static cudaError_t rows_otf_t(const RoundArgs& a, int corr, cudaStream_t st) {
   dim3 grid((unsigned)((a.nrows + kRT - 1) / kRT), (unsigned)a.chunks);
-  if (corr) k_round_rows_otf<D, true><<<grid, kRT, 0, st>>>(a);
-  else k_round_rows_otf<D, false><<<grid, kRT, 0, st>>>(a);
+  const bool dot = a.otf == 2;
+  if (corr) {
+    if (dot) k_round_rows_otf<D, true, true><<<grid, kRT, 0, st>>>(a);
+    else k_round_rows_otf<D, true, false><<<grid, kRT, 0, st>>>(a);
+  } else {
+    if (dot) k_round_rows_otf<D, false, true><<<grid, kRT, 0, st>>>(a);
+    else k_round_rows_otf<D, false, false><<<grid, kRT, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 template <int D>
 static cudaError_t cols_otf_t(const RoundArgs& a, cudaStream_t st) {
   dim3 grid((unsigned)((a.n + kRT - 1) / kRT), (unsigned)a.chunks);
-  k_round_cols_otf<D><<<grid, kRT, 0, st>>>(a);
+  if (a.otf == 2) k_round_cols_otf<D, true><<<grid, kRT, 0, st>>>(a);
+  else k_round_cols_otf<D, false><<<grid, kRT, 0, st>>>(a);
   return cudaGetLastError();
 }
 

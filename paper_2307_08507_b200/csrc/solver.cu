@@ -998,10 +998,10 @@ mdot_status validate_marginal(const double* h, int64_t n, const char* name) {
 
 mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   if (!pb || pb->n < 1) { set_error("problem is NULL or n < 1"); return MDOT_EINVAL; }
-  if (pb->kind < 0 || pb->kind > 2) { set_error("unknown cost kind %d", pb->kind); return MDOT_EINVAL; }
+  if (pb->kind < 0 || pb->kind > 3) { set_error("unknown cost kind %d", pb->kind); return MDOT_EINVAL; }
   const bool dev = pb->mem == MDOT_MEM_DEVICE;
   host_io = !dev;
-  otf = pb->kind == MDOT_COST_SQEUCLID_F32;
+  otf = pb->kind == MDOT_COST_SQEUCLID_F32 ? 1 : (pb->kind == MDOT_COST_SQEUCLID_DOT_F32 ? 2 : 0);   // Z22 / Z22b
   c_f64 = pb->kind == MDOT_COST_DENSE_F64;
   kind_fast = otf ? 1 : 0;
   d = pb->d;
@@ -1072,7 +1072,7 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   }
   eval.C = (const float*)Cdev;
   eval.ldc = n;
-  eval.X = Xdev; eval.Y = Ydev; eval.d = d; eval.scale = scale;
+  eval.X = Xdev; eval.Y = Ydev; eval.d = d; eval.scale = scale; eval.otf_dot = otf == 2;
   use_tma = false;
   if (!otf && !c_f64 && getenv("MDOT_DISABLE_TMA") == nullptr && tma_supported(eval)) {
     if (make_tma_map(eval, tmap) == cudaSuccess) {

@@ -44,6 +44,10 @@ def main(case):
         inst = S.config5(0, n=600, d=16)
         res = M.mdot_solve(X=t(inst.X), Y=t(inst.Y), scale=inst.scale, r=t(inst.r), c=t(inst.c), schedule=sched,
                            options=opts)
+    elif case == "otf_dot":        # k_eval_otf<16, DOT> + dot-form rounding tiles (Z22b), ragged n
+        inst = S.config5(0, n=777, d=16)
+        res = M.mdot_solve(X=t(inst.X), Y=t(inst.Y), scale=inst.scale, r=t(inst.r), c=t(inst.c), schedule=sched,
+                           options=opts, recipe="dot")
     elif case == "round":          # rounding + dense plan output, exact fp64 evaluator
         inst = S.uniform_points_instance(3, 300, 2, 2, marg="dirichlet")
         P = torch.empty((300, 300), dtype=torch.float32, device=DEV)

@@ -23,7 +23,7 @@ if not torch.cuda.is_available():
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASE = os.path.join(ROOT, "tests", "checked", "case.py")
-CASES = ("persist", "graph", "k8", "otf", "round", "peer2")
+CASES = ("persist", "graph", "k8", "otf", "otf_dot", "round", "peer2")
 
 
 @pytest.fixture(scope="module")

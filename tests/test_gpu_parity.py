@@ -469,28 +469,31 @@ def test_device_control_fp64_config1(monkeypatch):
 
 
 # ------------------------------------------------------------- on-the-fly cost (K2)
+@pytest.mark.parametrize("recipe", ["diff", "dot"])
 @pytest.mark.parametrize("generic", [False, True])
 @pytest.mark.parametrize("n,d", [(300, 16), (1024, 16), (777, 3), (513, 2), (600, 32), (389, 5)])
-def test_otf_marginals_match_oracle(n, d, generic, monkeypatch):
-    """Config-5 kernel: C computed in-kernel with the Z22 fp32 recipe, the
-    oracle computes the same recipe in C (-ffp-contract=off).  Both the packed
-    f32x2 kernel (d in {2,3,4,8,16,32}) and the generic scalar one."""
+def test_otf_marginals_match_oracle(n, d, generic, recipe, monkeypatch):
+    """Config-5 kernel: C computed in-kernel with the Z22 (difference) or Z22b
+    (dot) fp32 recipe, the oracle computes the same recipe in C
+    (-ffp-contract=off, explicit fmaf).  Both the packed f32x2 kernel (d in
+    {2,3,4,8,16,32}) and the generic scalar one."""
     if generic:
         monkeypatch.setenv("MDOT_OTF_GENERIC", "1")
     inst = S.config5(0, n=n, d=d)
-    prob = O.OracleProblem(inst)
+    prob = O.OracleProblem(inst, recipe=recipe)
     gb = 512.0
     A, B = _sinkhorn_potentials(prob, inst, gb, iters=3, noise=0.02)
     lr_o, lc_o, _ = O.log_marginals(prob, A, B, gb)
     lr, lc, fb = M.mdot_marginals(_t(A), _t(B), gb, X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale,
-                                  r=_t(inst.r), c=_t(inst.c))
+                                  r=_t(inst.r), c=_t(inst.c), recipe=recipe)
     assert fb == 0
     err_r = np.max(np.abs(np.expm1(lr.cpu().numpy() - lr_o)))
     err_c = np.max(np.abs(np.expm1(lc.cpu().numpy() - lc_o)))
     assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
 
 
-def test_full_size_config5_sampled_parity():
+@pytest.mark.parametrize("recipe", ["diff", "dot"])
+def test_full_size_config5_sampled_parity(recipe):
     """BASELINE config 5 at full size (n = 65536, d = 16, C computed in-kernel
     by the packed K2 kernel): one evaluation at potentials from a short GPU
     solve; sampled rows / columns recomputed by the oracle one by one
@@ -502,13 +505,13 @@ def test_full_size_config5_sampled_parity():
     V = torch.empty_like(U)
     gb = 256.0
     res = M.mdot_solve(X=X, Y=Y, scale=inst.scale, r=r, c=c, schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=1),
-                       options=M.options(eps=1e-3), u_out=U, v_out=V)
+                       options=M.options(eps=1e-3), u_out=U, v_out=V, recipe=recipe)
     assert res["status"] == 0 and res["l1_final"] <= 1e-3
-    lr, lc, fb = M.mdot_marginals(U, V, gb, X=X, Y=Y, scale=inst.scale, r=r, c=c)
+    lr, lc, fb = M.mdot_marginals(U, V, gb, X=X, Y=Y, scale=inst.scale, r=r, c=c, recipe=recipe)
     assert fb == 0
     lr, lc = lr.cpu().numpy(), lc.cpu().numpy()
     assert np.all(np.isfinite(lr)) and np.all(np.isfinite(lc))
-    prob = O.OracleProblem(inst)
+    prob = O.OracleProblem(inst, recipe=recipe)
     rng = np.random.default_rng(1)
     rows = np.sort(rng.choice(n, 16, replace=False))
     cols = np.sort(rng.choice(n, 16, replace=False))
@@ -518,17 +521,18 @@ def test_full_size_config5_sampled_parity():
     assert err_r <= 2e-6 and err_c <= 2e-6, (err_r, err_c)
 
 
-def test_otf_solve_matches_oracle():
-    n = 512
-    inst = S.config5(1, n=n, d=16)
-    prob = O.OracleProblem(inst)
+@pytest.mark.parametrize("recipe", ["diff", "dot"])
+@pytest.mark.parametrize("n,d", [(512, 16), (1300, 16), (700, 3)])
+def test_otf_solve_matches_oracle(n, d, recipe):
+    inst = S.config5(1, n=n, d=d)
+    prob = O.OracleProblem(inst, recipe=recipe)
     eps = 1e-5   # config 5 target
     gb = 1024.0
     U = torch.empty(n, dtype=torch.float64, device=DEV)
     V = torch.empty_like(U)
     res = M.mdot_solve(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c),
                        schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=4), options=M.options(eps=eps),
-                       u_out=U, v_out=V)
+                       u_out=U, v_out=V, recipe=recipe)
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=4), O.make_options(eps=eps))
     _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
 

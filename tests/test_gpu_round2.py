@@ -240,20 +240,23 @@ def test_config2_eps1e8_at_baseline_parameters_against_stored_oracle_solves():
         assert _oracle_l1(prob, inst, U[b].cpu().numpy(), V[b].cpu().numpy(), gb) <= 2 * eps
 
 
-def test_config5_full_size_at_baseline_parameters_oracle_reevaluation():
+@pytest.mark.parametrize("recipe", ["diff", "dot"])
+def test_config5_full_size_at_baseline_parameters_oracle_reevaluation(recipe):
     """BASELINE config 5 at its stated parameters (n = 65536, d = 16, C on the
     fly, gbar 4096, T = 16, L1 1e-5): the oracle re-evaluates the GPU
-    potentials over the WHOLE matrix with the Z22 fp32 cost recipe: marginal
-    L1 within max(2 eps, 1e-6) and <C, P(U,V)> within 1e-9 of the GPU's."""
+    potentials over the WHOLE matrix with the same fp32 cost recipe (Z22
+    difference form, Z22b dot form -- the one bench.py times): marginal L1
+    within max(2 eps, 1e-6) and <C, P(U,V)> within 1e-9 of the GPU's."""
     inst = S.config5(0)
     n = inst.n
     U = torch.empty(n, dtype=torch.float64, device=DEV)
     V = torch.empty_like(U)
     eps, gb = 1e-5, 4096.0
     res = M.mdot_solve(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c),
-                       schedule=M.schedule(M.MDOT_SCHED_FIXED, gb), options=M.options(eps=eps), u_out=U, v_out=V)
+                       schedule=M.schedule(M.MDOT_SCHED_FIXED, gb), options=M.options(eps=eps), u_out=U, v_out=V,
+                       recipe=recipe)
     assert res["status"] == 0 and res["md_steps"] == 16 and res["l1_final"] <= eps
-    prob = O.OracleProblem(inst)
+    prob = O.OracleProblem(inst, recipe=recipe)
     Un, Vn = U.cpu().numpy(), V.cpu().numpy()
     assert _oracle_l1(prob, inst, Un, Vn, gb) <= max(2 * eps, 1e-6)
     cF = O.plan_cost(prob, Un, Vn, gb)

@@ -761,3 +761,30 @@ def test_adaptive_gamma_schedule_lemma2_and_budget():
     assert res["status"] == 0 and len(g) >= 3
     np.testing.assert_allclose(np.exp(U[:, None] + V[None, :] - 100.0 * C), X.entropic_2x2(C, r, c, 100.0),
                                atol=1e-13)
+
+
+def test_cost_sqeuclid_dot_recipe_is_its_fp32_chain():
+    """Z22b (dot form of the config-5 cost): C = max(fl(nx + ny) - 2 s, 0) * scale
+    with nx, ny, s fp32 fma chains in index order; checked against a numpy
+    float32 emulation (each fma exact in fp64 for fp32 operands, rounded once),
+    and against the exact squared distance to fp32 cancellation accuracy."""
+    inst = S.config5(0, n=64, d=16)
+    prob = O.OracleProblem(inst, recipe="dot")
+
+    def fma32(a, b, c):
+        return np.float32(np.float64(a) * np.float64(b) + np.float64(c))
+
+    for (i, j) in [(0, 0), (3, 7), (63, 1), (10, 10), (5, 40)]:
+        x, y = inst.X[i], inst.Y[j]
+        nx = ny = s = np.float32(0.0)
+        for k in range(16):
+            nx = fma32(x[k], x[k], nx)
+        for k in range(16):
+            ny = fma32(y[k], y[k], ny)
+        for k in range(16):
+            s = fma32(x[k], y[k], s)
+        t = np.float32(nx + ny)
+        ref = np.float32(max(fma32(np.float32(-2.0), s, t), np.float32(0.0)) * np.float32(1.0 / 16))
+        assert prob.cost(i, j) == float(ref)
+        exact = float(np.sum((x.astype(np.float64) - y.astype(np.float64)) ** 2)) / 16
+        assert abs(prob.cost(i, j) - exact) <= 4e-7 * max(1.0, 16 * exact)

@@ -91,8 +91,8 @@ struct EvalArgs {
   int tile_m;              // rows per tile (multiple of kWarps*kUnroll)
   int n_row_tiles, n_col_tiles;
   // per-row / per-column parameters
-  const float4* rowp;      // [nrows] {ah, al, S=2^rho, w}
-  const float4* colp;      // [n]     {bh, bl, T=2^sig, w}
+  const float4* rowp;      // [nrows] {ah, al, S=2^rho, w}  (w: |x_i|^2 for the dot recipe, else 0)
+  const float4* colp;      // [n]     {bh, bl, T=2^sig, w}  (w: |y_j|^2 for the dot recipe, else 0)
   float gh, gl;            // g2 = gbar*log2(e) = gh + gl
   const float* gpair;      // device-resident {gh, gl} (device control), overrides gh/gl
   const int* done;         // device control: kernel returns at once when *done != 0
@@ -267,6 +267,7 @@ struct PrepArgs {
   const double* Ain; const double* Bin;   // PREP_AB
   double* Aout; double* Bout;         // fp64 bases (for the exact path)
   float4* rowp; float4* colp;
+  const float* nrm;                   // [nrows + n] squared norms (Z22b dot recipe) -> rowp/colp .w, or null
   int* flag;                          // set to 1 when |a2|,|b2| >= 2^15
   int f64_params;                     // 1: write {fp64 base, 2^anchor, anchor} (fp64-entry evaluation)
   // device control: mode/alpha/beta/accept come from ctrl; accept copies trial -> cur
@@ -275,6 +276,8 @@ struct PrepArgs {
   const double *tr_lm, *tr_m, *tr_s, *tr_g;
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
+// out[i] = sqnorm_recipe(P + i d, d) for i < m (the Z22b recipe, otf_cost.cuh)
+cudaError_t launch_sqnorms(const float* P, int64_t m, int d, float* out, cudaStream_t st);
 cudaError_t launch_prep_multi(const PrepArgs* args_dev, const PrepArgs& a0, int B, cudaStream_t st);
 
 // Persistent cooperative slot kernel (persist.cu): a whole projection in one

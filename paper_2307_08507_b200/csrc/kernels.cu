@@ -279,10 +279,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fast(EvalArgs a) {
 // bit-identical to the scalar recipe.  Layout as
 // k_eval_fast: lane owns columns j0 + 4*lane + {0..3} and
 // j0 + 128 + 4*lane + {0..3} (pairs {0,1},{2,3} of each quad); X rows are
-// staged in chunks of kOtfChunk rows as duplicated pairs (x, x) so each
+// staged in chunks of OtfChunk<D> rows as duplicated pairs (x, x) so each
 // FADD2 reads its broadcast operand straight from shared memory.
 // ---------------------------------------------------------------------------
-constexpr int kOtfChunk = 128;
+// rows per staged X chunk: 256 for d <= 16 (half the CTA barriers per row;
+// 2 x 72 KB of shared memory per SM at d = 16), 128 above (d = 32: 2 x 112 KB)
+template <int D>
+struct OtfChunk {
+  static constexpr int value = D <= 16 ? 256 : 128;
+};
 // K2 keeps the fp64 row butterfly: with the fp32 one ptxas spills ~700 bytes
 // per thread at the 128-register cap (the distance accumulators are live)
 #ifndef MDOT_K2_ROWRED_F32
@@ -294,6 +299,7 @@ constexpr int kOtfChunk = 128;
 // pair of entries disappears, with the Z22 recipe's bits unchanged.
 template <int D, bool POW2, bool DOT>
 __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
+  constexpr int kOtfChunk = OtfChunk<D>::value;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   if (a.done && *a.done) return;
@@ -303,7 +309,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 
   __shared__ double sred[kWarps][kTileN];
   __shared__ float4 sRP[2][kOtfChunk];   // row parameters, double-buffered by chunk
-  __shared__ float sNX[DOT ? kOtfChunk : 1];   // Z22b: squared norms of the chunk's rows
   extern __shared__ __align__(16) unsigned char sraw[];
   float* sY = reinterpret_cast<float*>(sraw);                          // [D][256]
   float* sX = reinterpret_cast<float*>(sraw + sizeof(float) * D * kTileN);   // [2][chunk][D]
@@ -367,23 +372,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) sY[k * kTileN + threadIdx.x] = yv[k];
-    if (DOT) {   // this column's squared norm (Z22b), kept in sred until the pairs are built
-      float ny = 0.f;
-#pragma unroll
-      for (int k = 0; k < D; ++k) ny = __fmaf_rn(yv[k], yv[k], ny);
-      reinterpret_cast<float*>(&sred[0][0])[threadIdx.x] = ny;
-    }
   }
-  u64 ny2[DOT ? 4 : 1];   // the lane's column pairs' squared norms
+  // Z22b: the lane's column pairs' squared norms |y_j|^2 (colp .w, written by
+  // prep from the once-per-solve norms; the row norms come with sRP .w)
+  u64 ny2[DOT ? 4 : 1];
   if (DOT) {
-    __syncthreads();
-    const float* sny = reinterpret_cast<const float*>(&sred[0][0]);
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      const int c = 4 * lane + ((2 * p) & 3) + 128 * ((2 * p) >> 2);
-      ny2[p & (DOT ? 3 : 0)] = pk2(sny[c], sny[c + 1]);
+      float v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * p + h;
+        const int64_t j = j0 + 4 * lane + (q & 3) + 128 * (q >> 2);
+        v[h] = j < n ? a.colp[j].w : 0.f;
+      }
+      ny2[p & (DOT ? 3 : 0)] = pk2(v[0], v[1]);
     }
-    __syncthreads();   // sred is reused for the column sums at the end
   }
 
   ColPairs cpp;
@@ -429,15 +433,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
       __syncthreads();
     }
     const float* xs = sX + buf * kOtfChunk * D;
-    if (DOT) {   // the chunk's row squared norms (Z22b)
-      if ((int)threadIdx.x < kOtfChunk) {
-        float nx = 0.f;
-#pragma unroll
-        for (int k = 0; k < D; ++k) nx = __fmaf_rn(xs[threadIdx.x * D + k], xs[threadIdx.x * D + k], nx);
-        sNX[threadIdx.x & (DOT ? kOtfChunk - 1 : 0)] = nx;
-      }
-      __syncthreads();
-    }
     for (int rb = 4 * warp; rb < rows_c; rb += kWarps * kUnroll) {
       u64 acc[kUnroll][4];
 #pragma unroll
@@ -471,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         const u64 m2 = pk2(-2.0f, -2.0f);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-          const float nx = sNX[(rb + u) & (kOtfChunk - 1)];
+          const float nx = sRP[buf][rb + u].w;   // |x_i|^2 (0 on zero-filled rows past the tile)
           const u64 nx2 = pk2(nx, nx);
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
@@ -548,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 template <int D, bool POW2, bool DOT>
 static cudaError_t launch_otf_pt(const EvalArgs& a, cudaStream_t st) {
   dim3 grid(a.n_col_tiles, a.n_row_tiles);
-  const size_t smem = sizeof(float) * D * kTileN + sizeof(float) * 2 * kOtfChunk * D;
+  const size_t smem = sizeof(float) * D * kTileN + sizeof(float) * 2 * OtfChunk<D>::value * D;
   static bool attr_set = false;
   if (!attr_set) {   // static (column sums, row parameters) + dynamic exceeds the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(k_eval_otf<D, POW2, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -902,6 +897,18 @@ cudaError_t launch_prep_multi(const PrepArgs* args_dev, const PrepArgs& a0, int 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
   const int64_t items = a.nrows + a.n;
   k_prep<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Z22b squared norms, once per solve (O(m d)): one thread per point.
+__global__ void k_sqnorms(const float* __restrict__ P, int64_t m, int d, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = sqnorm_recipe(P + i * d, d);
+}
+
+cudaError_t launch_sqnorms(const float* P, int64_t m, int d, float* out, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_sqnorms<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(P, m, d, out);
   return cudaGetLastError();
 }
 

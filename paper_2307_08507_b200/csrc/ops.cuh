@@ -117,7 +117,13 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
       base = a.U[idx] + a.u[idx];
     }
     if (a.Aout) a.Aout[idx] = base;
-    a.rowp[idx] = a.f64_params ? f64_param(base, a.rho_r[idx]) : split_param(base, a.rho_r[idx], a.flag);
+    if (a.f64_params) {
+      a.rowp[idx] = f64_param(base, a.rho_r[idx]);
+    } else {
+      float4 q = split_param(base, a.rho_r[idx], a.flag);
+      if (a.nrm) q.w = a.nrm[idx];
+      a.rowp[idx] = q;
+    }
   } else {
     if (mode & PREP_TRIAL) {
       const double t = a.v[idx] + alpha * pk;
@@ -133,7 +139,13 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
       base = a.V[idx] + a.v[idx];
     }
     if (a.Bout) a.Bout[idx] = base;
-    a.colp[idx] = a.f64_params ? f64_param(base, a.sig_c[idx]) : split_param(base, a.sig_c[idx], a.flag);
+    if (a.f64_params) {
+      a.colp[idx] = f64_param(base, a.sig_c[idx]);
+    } else {
+      float4 q = split_param(base, a.sig_c[idx], a.flag);
+      if (a.nrm) q.w = a.nrm[a.nrows + idx];
+      a.colp[idx] = q;
+    }
   }
 }
 

@@ -187,6 +187,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   size_t o_aux = take(8 * items);
   size_t o_tot = take(items + 32);
   size_t o_ctrl = take((int64_t)((sizeof(CtrlState) + 7) / 8));
+  size_t o_nrm = take((items + 1) / 2);   // items floats
   const size_t tickets = (size_t)eval.n_row_tiles + eval.n_col_tiles + 64;
   size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256 + tickets * 4;
 #ifdef MDOT_CHECKED
@@ -214,6 +215,7 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   rowpart = D + o_rowpart; colpart = D + o_colpart; colm = D + o_colm; cols = D + o_cols; lr_ex = D + o_lr;
   blockpart = D + o_blk; scal_dev = D + o_scal; aux = D + o_aux;
   ctrl = reinterpret_cast<CtrlState*>(D + o_ctrl);
+  nrm = reinterpret_cast<float*>(D + o_nrm);
   tot.coltot = D + o_tot;   // sharded: [column totals | row scalars] allreduce buffer
   float4* F4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(base) + dbl * sizeof(double));
   F4 = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(F4) + 15) & ~uintptr_t(15));
@@ -373,7 +375,7 @@ mdot_status Workspace::prep(int mode, double alpha, double beta, const double* s
   a.p = p; a.s = s_dir; a.pprev = pprev; a.lm = cur->lm;
   a.logr = logr; a.logc = logc; a.rho_r = rho_r; a.sig_c = sig_c;
   a.Ain = Ain; a.Bin = Bin; a.Aout = A; a.Bout = B;
-  a.rowp = rowp; a.colp = colp; a.flag = flag;
+  a.rowp = rowp; a.colp = colp; a.flag = flag; a.nrm = use_nrm ? nrm : nullptr;
   CKL(launch_prep(a, st));
   return MDOT_OK;
 }
@@ -546,7 +548,7 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
   a.p = p; a.s = cur->s; a.pprev = pprev; a.lm = cur->lm;
   a.logr = logr; a.logc = logc; a.rho_r = rho_r; a.sig_c = sig_c;
   a.Aout = A; a.Bout = B;
-  a.rowp = rowp; a.colp = colp; a.flag = flag;
+  a.rowp = rowp; a.colp = colp; a.flag = flag; a.nrm = use_nrm ? nrm : nullptr;
   a.ctrl = ctrl;
   a.cur_lm = cur->lm; a.cur_m = cur->m; a.cur_s = cur->s; a.cur_g = cur->g;
   a.tr_lm = trial->lm; a.tr_m = trial->m; a.tr_s = trial->s; a.tr_g = trial->g;
@@ -788,7 +790,7 @@ static mdot_status persist_prepare(Workspace& w, const mdot_options& o, int t, P
   p.p = w.p; p.s = w.cur->s; p.pprev = w.pprev; p.lm = w.cur->lm;
   p.logr = w.logr; p.logc = w.logc; p.rho_r = w.rho_r; p.sig_c = w.sig_c;
   p.Aout = w.A; p.Bout = w.B;
-  p.rowp = w.rowp; p.colp = w.colp; p.flag = w.flag;
+  p.rowp = w.rowp; p.colp = w.colp; p.flag = w.flag; p.nrm = w.use_nrm ? w.nrm : nullptr;
   p.ctrl = nullptr;
   p.cur_lm = w.cur->lm; p.cur_m = w.cur->m; p.cur_s = w.cur->s; p.cur_g = w.cur->g;
   p.tr_lm = w.trial->lm; p.tr_m = w.trial->m; p.tr_s = w.trial->s; p.tr_g = w.trial->g;
@@ -1073,6 +1075,11 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   eval.C = (const float*)Cdev;
   eval.ldc = n;
   eval.X = Xdev; eval.Y = Ydev; eval.d = d; eval.scale = scale; eval.otf_dot = otf == 2;
+  use_nrm = otf == 2;
+  if (use_nrm) {   // Z22b: |x_i|^2, |y_j|^2 once per solve; prep carries them to K2 in rowp/colp .w
+    CKL(launch_sqnorms(Xdev, nrows, (int)d, nrm, st));
+    CKL(launch_sqnorms(Ydev, n, (int)d, nrm + nrows, st));
+  }
   use_tma = false;
   if (!otf && !c_f64 && getenv("MDOT_DISABLE_TMA") == nullptr && tma_supported(eval)) {
     if (make_tma_map(eval, tmap) == cudaSuccess) {

@@ -51,6 +51,8 @@ struct Workspace {
   double *rowpart = nullptr, *colpart = nullptr, *colm = nullptr, *cols = nullptr, *lr_ex = nullptr;
   double *blockpart = nullptr, *scal_dev = nullptr, *aux = nullptr;
   float4 *rowp = nullptr, *colp = nullptr;
+  float* nrm = nullptr;              // [nrows + n] Z22b squared norms of X, Y rows (dot-form K2)
+  bool use_nrm = false;             // set by load_problem for the dot recipe: prep writes them into .w
   unsigned int* ticket_flag = nullptr;
   unsigned int* ticket = nullptr;
   int* flag = nullptr;

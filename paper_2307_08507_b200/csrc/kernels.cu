@@ -288,10 +288,13 @@ template <int D>
 struct OtfChunk {
   static constexpr int value = D <= 16 ? 256 : 128;
 };
-// K2 keeps the fp64 row butterfly: with the fp32 one ptxas spills ~700 bytes
-// per thread at the 128-register cap (the distance accumulators are live)
-#ifndef MDOT_K2_ROWRED_F32
-#define MDOT_K2_ROWRED_F32 0
+// Row sums: each lane stores its 4 fp32 row partials (8 entries each) to
+// shared memory and one thread per row adds the 32 partials in fp64 after the
+// chunk (fixed order).  The per-iteration fp64 shuffle butterfly this replaces
+// (MDOT_K2_ROWSMEM=0) was ~15 % of the loop's instructions and its most
+// latency-bound part (profiles/r02_k2_dot_ncu.md).
+#ifndef MDOT_K2_ROWSMEM
+#define MDOT_K2_ROWSMEM 1
 #endif
 
 // POW2: scale is a power of two, so C = acc * scale is exact and -g * C ==
@@ -312,6 +315,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char sraw[];
   float* sY = reinterpret_cast<float*>(sraw);                          // [D][256]
   float* sX = reinterpret_cast<float*>(sraw + sizeof(float) * D * kTileN);   // [2][chunk][D]
+#if MDOT_K2_ROWSMEM
+  // [32 lanes][chunk + 4] fp32 row partials (the +4 pad spreads the lanes'
+  // float4 stores over all banks)
+  constexpr int kPartStride = kOtfChunk + 4;
+  float* sPart = sX + 2 * kOtfChunk * D;
+#endif
   // X chunks (and their row parameters) stream through a 2-deep cp.async
   // ring: the next chunk's copy overlaps this chunk's arithmetic.  Vector
   // copies need D % 4 == 0 and 16-byte aligned X, Y (else synchronous
@@ -476,11 +485,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
           }
         }
       }
-#if MDOT_K2_ROWRED_F32
+#if MDOT_K2_ROWSMEM
       float rs[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        float4 rp = sRP[buf][rb + u];   // broadcast
+        if (rb + u >= rows_c) rp = make_float4(-1.0e30f, 0.f, 0.f, 0.f);   // zero-filled rows past the tile
+        u64 c2[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) c2[p] = POW2 ? acc[u][p] : mul2(acc[u][p], scale2);
+        rs[u] = entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);
+      }
+      // the lane's 4 row partials (8 entries each) -> sPart, reduced per row after the chunk
+      *reinterpret_cast<float4*>(sPart + lane * kPartStride + rb) = make_float4(rs[0], rs[1], rs[2], rs[3]);
 #else
       double rs[kUnroll];
-#endif
       float mrow[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -490,22 +509,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         u64 c2[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) c2[p] = POW2 ? acc[u][p] : mul2(acc[u][p], scale2);
-#if MDOT_K2_ROWRED_F32
-        rs[u] = entry_row8_f(c2, rp, cpp, ngh2, ngl2, cacc2);
-#else
         rs[u] = entry_row8(c2, rp, cpp, ngh2, ngl2, cacc2);
-#endif
       }
       {
-#if MDOT_K2_ROWRED_F32
-        const double tot = (double)warp_reduce4_f(rs[0], rs[1], rs[2], rs[3], lane);
-#else
         const double tot = warp_reduce4(rs[0], rs[1], rs[2], rs[3], lane);
-#endif
         const int r = rb + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
         const float Mrow = (lane & 16) ? ((lane & 8) ? mrow[3] : mrow[2]) : ((lane & 8) ? mrow[1] : mrow[0]);
         if ((lane & 7) == 0 && r < rows_c) a.rowpart[(int64_t)blockIdx.x * nrows + c0 + r] = tot * (double)Mrow;
       }
+#endif
       if (++flush == MDOT_K1_COLFLUSH) {   // 4 x MDOT_K1_COLFLUSH rows of fp32 column sums -> fp64
         flush = 0;
 #pragma unroll
@@ -518,7 +530,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
         }
       }
     }
+#if MDOT_K2_ROWSMEM
+    __syncthreads();   // every lane's partials of this chunk are in sPart
+    for (int r = threadIdx.x; r < rows_c; r += kThreads) {   // one row per thread: 32 partials in fp64, fixed order
+      double tot = 0.0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) tot += (double)sPart[l * kPartStride + r];
+      a.rowpart[(int64_t)blockIdx.x * nrows + c0 + r] = tot * (double)sRP[buf][r].y;   // times M_i = 2^al_i
+    }
+    __syncthreads();   // sPart and the chunk buffer free for the next chunk
+#else
     if (vec) __syncthreads();   // chunk buffer free before the next iteration's copy into it
+#endif
   }
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
@@ -543,7 +566,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_otf(EvalArgs a) {
 template <int D, bool POW2, bool DOT>
 static cudaError_t launch_otf_pt(const EvalArgs& a, cudaStream_t st) {
   dim3 grid(a.n_col_tiles, a.n_row_tiles);
-  const size_t smem = sizeof(float) * D * kTileN + sizeof(float) * 2 * OtfChunk<D>::value * D;
+  const size_t smem = sizeof(float) * D * kTileN + sizeof(float) * 2 * OtfChunk<D>::value * D +
+                      (MDOT_K2_ROWSMEM ? sizeof(float) * 32 * (OtfChunk<D>::value + 4) : 0);
   static bool attr_set = false;
   if (!attr_set) {   // static (column sums, row parameters) + dynamic exceeds the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(k_eval_otf<D, POW2, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

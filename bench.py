@@ -98,9 +98,9 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram bytes per launch of K1 from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+def profile_traffic(name="k1_traffic.json"):
+    """dram bytes per launch of K1 (K2: k2_traffic.json) from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         try:
             return json.load(open(p)).get("bytes_per_launch")
@@ -606,7 +606,9 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
                      "peak_source": f"FP32 pipe: 148 SMs x 128 lanes x 1.965 GHz / ({ops} ops per pair)",
                      "mufu_floor_frac": (achieved / mufu_peak) if achieved else None,
                      "mean_launch_ms": launch_s * 1e3, "launches_timed": kn,
-                     "traffic": None},
+                     "traffic": profile_traffic("k2_traffic.json") if a.c5_recipe == "dot" else None,
+                     "traffic_note": "DRAM bytes per K2 launch (ncu --set full, profiles/k2_traffic.json): X, Y "
+                                     "are L2-resident; the bytes are mostly the fp64 row / column partials"},
         "status_name": res[-1]["status_name"],
     }
     if a.c5_full:

@@ -788,3 +788,37 @@ def test_cost_sqeuclid_dot_recipe_is_its_fp32_chain():
         assert prob.cost(i, j) == float(ref)
         exact = float(np.sum((x.astype(np.float64) - y.astype(np.float64)) ** 2)) / 16
         assert abs(prob.cost(i, j) - exact) <= 4e-7 * max(1.0, 16 * exact)
+
+
+def test_cost_sqeuclid_dot_recipe_clamps_cancellation_at_zero():
+    """Z22b's max(., 0): for nearly coincident points the dot form can round
+    below zero; the oracle must return exactly 0 there (C >= 0),
+    and exactly 0 for coincident points (the chains cancel exactly)."""
+    rng = np.random.default_rng(7)
+
+    def fma32(a, b, c):
+        return np.float32(np.float64(a) * np.float64(b) + np.float64(c))
+
+    def raw(x, y):
+        nx = ny = s = np.float32(0.0)
+        for k in range(len(x)):
+            nx = fma32(x[k], x[k], nx)
+            ny = fma32(y[k], y[k], ny)
+            s = fma32(x[k], y[k], s)
+        return float(fma32(np.float32(-2.0), s, np.float32(nx + ny)))
+
+    neg = None
+    for _ in range(4000):
+        x = rng.random(16, dtype=np.float32)
+        y = (x + rng.normal(0, 1e-4, 16).astype(np.float32)).astype(np.float32)
+        if raw(x, y) < 0.0:
+            neg = (x, y)
+            break
+    assert neg is not None, "no cancelling pair found"
+    X = np.stack([neg[0], neg[0]])
+    Y = np.stack([neg[1], neg[0]])
+    prob = O.OracleProblem(X=X, Y=Y, r=np.full(2, 0.5), c=np.full(2, 0.5), scale=1.0 / 16, recipe="dot")
+    assert prob.cost(0, 0) == 0.0          # clamped (unclamped value < 0)
+    assert prob.cost(1, 1) == 0.0          # coincident points
+    diffp = O.OracleProblem(X=X, Y=Y, r=np.full(2, 0.5), c=np.full(2, 0.5), scale=1.0 / 16)
+    assert diffp.cost(0, 0) > 0.0          # the difference form sees the distance

@@ -76,15 +76,44 @@ __device__ void bar_tree(unsigned* bar) {
   __syncthreads();
 }
 
+// count barrier: every CTA arrives with a release-add on a monotonic counter
+// and polls it until it reaches gen * ncta (no last-arriver release step)
+__device__ void bar_count(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    red_rel(&bar[8], 1u);
+    const unsigned tgt = gen * gridDim.x;
+    while ((int)(ld_acq(&bar[8]) - tgt) < 0) {}
+  }
+  __syncthreads();
+}
+// flat with the generation tracked in a register (persist.cu's grid_barrier)
+__device__ void bar_flat_reg(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atom_acqrel(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      red_rel(&bar[1], 1u);
+    } else {
+      while (ld_acq(&bar[1]) == gen) __nanosleep(8);
+    }
+    ++gen;
+  }
+  __syncthreads();
+}
 template <int MODE>
 __global__ void __launch_bounds__(288, 2) k(unsigned* bar, int iters, unsigned long long* out) {
   unsigned long long t0 = clock64();
+  unsigned gen = 0;
   for (int i = 0; i < iters; ++i) {
     if (MODE == 0) bar_flat(bar);
     else if (MODE == 1) bar_tree<8>(bar);
     else if (MODE == 2) bar_tree<16>(bar);
     else if (MODE == 3) bar_flat_v<0>(bar);
-    else bar_flat_v<1>(bar);
+    else if (MODE == 4) bar_flat_v<1>(bar);
+    else if (MODE == 5) bar_count(bar, gen);
+    else bar_flat_reg(bar, gen);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = clock64() - t0;
 }
@@ -97,23 +126,26 @@ int main() {
   cudaMalloc(&bar, 4096 * 4);
   cudaMalloc(&out, 8);
   const int iters = 2000;
-  for (int mode = 0; mode < 5; ++mode) {
+  const int grids[3] = {2 * sms, 256, sms};
+  for (int gi = 0; gi < 3; ++gi)
+  for (int mode = 0; mode < 7; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(bar, 0, 4096 * 4);
-      int grid = 2 * sms, iters_ = iters;
+      int grid = grids[gi], iters_ = iters;
       void* args[] = {&bar, &iters_, &out};
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0);
-      const void* fns[5] = {(const void*)k<0>, (const void*)k<1>, (const void*)k<2>, (const void*)k<3>, (const void*)k<4>};
+      const void* fns[7] = {(const void*)k<0>, (const void*)k<1>, (const void*)k<2>, (const void*)k<3>, (const void*)k<4>,
+                            (const void*)k<5>, (const void*)k<6>};
       const void* fn = fns[mode];
       cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(288), args, 0, 0);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
-      printf("mode %d (%s) grid %d: %.3f us per barrier (%s)\n", mode, mode == 0 ? "flat" : mode == 1 ? "tree8" : mode == 2 ? "tree16" : mode == 3 ? "flat-spin" : "flat-relaxed",
+      printf("mode %d (%s) grid %d: %.3f us per barrier (%s)\n", mode, mode == 0 ? "flat" : mode == 1 ? "tree8" : mode == 2 ? "tree16" : mode == 3 ? "flat-spin" : mode == 4 ? "flat-relaxed" : mode == 5 ? "count" : "flat-reggen",
              grid, 1000.0 * ms / iters, cudaGetErrorString(e));
     }
   }

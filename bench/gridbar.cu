@@ -88,6 +88,33 @@ __device__ void bar_count(unsigned* bar, unsigned& gen) {
   }
   __syncthreads();
 }
+// count barrier variants: V=0 relaxed polls + one acquire fence; V=1 fence +
+// relaxed red arrival, acquire polls; V=2 relaxed red after __threadfence,
+// volatile polls, __threadfence (the classic cooperative-groups shape)
+template <int V>
+__device__ void bar_count_v(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    const unsigned tgt = gen * gridDim.x;
+    if (V == 0) {
+      red_rel(&bar[8], 1u);
+      unsigned v;
+      do { asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&bar[8]) : "memory"); } while ((int)(v - tgt) < 0);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    } else if (V == 1) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&bar[8]), "r"(1u) : "memory");
+      while ((int)(ld_acq(&bar[8]) - tgt) < 0) {}
+    } else {
+      __threadfence();
+      atomicAdd(&bar[8], 1u);
+      while ((int)(*((volatile unsigned*)&bar[8]) - tgt) < 0) {}
+      __threadfence();
+    }
+  }
+  __syncthreads();
+}
 // flat with the generation tracked in a register (persist.cu's grid_barrier)
 __device__ void bar_flat_reg(unsigned* bar, unsigned& gen) {
   __syncthreads();
@@ -113,7 +140,10 @@ __global__ void __launch_bounds__(288, 2) k(unsigned* bar, int iters, unsigned l
     else if (MODE == 3) bar_flat_v<0>(bar);
     else if (MODE == 4) bar_flat_v<1>(bar);
     else if (MODE == 5) bar_count(bar, gen);
-    else bar_flat_reg(bar, gen);
+    else if (MODE == 6) bar_flat_reg(bar, gen);
+    else if (MODE == 7) bar_count_v<0>(bar, gen);
+    else if (MODE == 8) bar_count_v<1>(bar, gen);
+    else bar_count_v<2>(bar, gen);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = clock64() - t0;
 }
@@ -126,9 +156,9 @@ int main() {
   cudaMalloc(&bar, 4096 * 4);
   cudaMalloc(&out, 8);
   const int iters = 2000;
-  const int grids[3] = {2 * sms, 256, sms};
-  for (int gi = 0; gi < 3; ++gi)
-  for (int mode = 0; mode < 7; ++mode) {
+  const int grids[1] = {2 * sms};
+  for (int gi = 0; gi < 1; ++gi)
+  for (int mode = 5; mode < 10; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(bar, 0, 4096 * 4);
       int grid = grids[gi], iters_ = iters;
@@ -137,15 +167,15 @@ int main() {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0);
-      const void* fns[7] = {(const void*)k<0>, (const void*)k<1>, (const void*)k<2>, (const void*)k<3>, (const void*)k<4>,
-                            (const void*)k<5>, (const void*)k<6>};
+      const void* fns[10] = {(const void*)k<0>, (const void*)k<1>, (const void*)k<2>, (const void*)k<3>, (const void*)k<4>,
+                             (const void*)k<5>, (const void*)k<6>, (const void*)k<7>, (const void*)k<8>, (const void*)k<9>};
       const void* fn = fns[mode];
       cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(288), args, 0, 0);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
-      printf("mode %d (%s) grid %d: %.3f us per barrier (%s)\n", mode, mode == 0 ? "flat" : mode == 1 ? "tree8" : mode == 2 ? "tree16" : mode == 3 ? "flat-spin" : mode == 4 ? "flat-relaxed" : mode == 5 ? "count" : "flat-reggen",
+      printf("mode %d (%s) grid %d: %.3f us per barrier (%s)\n", mode, mode == 0 ? "flat" : mode == 1 ? "tree8" : mode == 2 ? "tree16" : mode == 3 ? "flat-spin" : mode == 4 ? "flat-relaxed" : mode == 5 ? "count" : mode == 6 ? "flat-reggen" : mode == 7 ? "count-relaxedpoll" : mode == 8 ? "count-fence-redrelaxed" : "count-cg",
              grid, 1000.0 * ms / iters, cudaGetErrorString(e));
     }
   }

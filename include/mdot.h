@@ -275,6 +275,17 @@ mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, 
                                const mdot_schedule* sched, const mdot_options* opt,
                                double* u_local_out, double* v_out, mdot_result* res);
 
+/* Screened evaluation statistics of the calling thread's last mdot_solve /
+ * mdot_sinkhorn (K2s): on-the-fly costs with
+ * d in {2, 4, 8, 16} on one rank evaluate the graph-slot trials with a
+ * tensor-core screen that skips the entries below 2^-T (T = 56 by default,
+ * env MDOT_SCREEN_T) of both their row and column totals -- a rigorous bound,
+ * < n 2^-T relative change of any marginal.  out[0] entries kept, out[1]
+ * entries screened, out[2] screened evaluations, out[3] summed device time
+ * of the timed screened evaluations (ms, options.time_kernels), out[4] their
+ * count.  env MDOT_SCREEN=0 disables the screen.  out: 5 doubles (host). */
+mdot_status mdot_last_screen_stats(double* out);
+
 const char* mdot_last_error(void);
 int32_t mdot_abi_version(void);
 

@@ -118,9 +118,10 @@ def lib():
         L.mdot_solve_sharded.argtypes = [P, ct.POINTER(Problem), ct.c_int64, ct.c_int64,
                                          ct.POINTER(Schedule), ct.POINTER(Options), P, P,
                                          ct.POINTER(Result)]
+        L.mdot_last_screen_stats.argtypes = [ct.POINTER(D)]
         for nm in ("mdot_solve_batch", "mdot_marginals", "mdot_round", "mdot_get_unique_id",
                    "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_enable_peer", "mdot_comm_destroy",
-                   "mdot_solve_sharded"):
+                   "mdot_solve_sharded", "mdot_last_screen_stats"):
             getattr(L, nm).restype = ct.c_int
         if L.mdot_abi_version() != 3:
             raise ImportError("libmdot_b200.so ABI version mismatch")
@@ -130,6 +131,14 @@ def lib():
 
 def mdot_last_error() -> str:
     return lib().mdot_last_error().decode()
+
+
+def mdot_last_screen_stats() -> dict:
+    """K2s statistics of this thread's last solve (include/mdot.h)."""
+    out = (ct.c_double * 5)()
+    lib().mdot_last_screen_stats(out)
+    return {"kept": out[0], "screened": out[1], "evals": int(out[2]), "ms": out[3], "timed": int(out[4]),
+            "kept_frac": (out[0] / out[1]) if out[1] else None}
 
 
 # ---------------------------------------------------------------- marshalling

@@ -8,8 +8,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "eval_tma.cu", "persist.cu", "batch.cu", "round.cu", "solver.cu", "comm.cu")]
-HDR = [os.path.join(HERE, "csrc", f) for f in ("internal.cuh", "solver.h", "comm.h", "ops.cuh", "k1_tma.cuh", "entry.cuh")] + \
+SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "eval_tma.cu", "persist.cu", "batch.cu", "round.cu", "solver.cu", "comm.cu", "screen.cu")]
+HDR = [os.path.join(HERE, "csrc", f) for f in ("internal.cuh", "solver.h", "comm.h", "ops.cuh", "k1_tma.cuh", "entry.cuh", "umma.cuh")] + \
       [os.path.join(ROOT, "include", "mdot.h")]
 OUT = os.path.join(HERE, "libmdot_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

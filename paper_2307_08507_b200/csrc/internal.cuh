@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "../../include/mdot.h"
 
@@ -101,6 +102,11 @@ struct EvalArgs {
   // outputs
   double* rowpart;         // [n_col_tiles][nrows]  sum_j 2^w T_j
   double* colpart;         // [n_row_tiles][n]      sum_i 2^w S_i
+  // screened on-the-fly evaluation (K2s, screen.cu): operand rows written by k_prep
+  const float* sopA;                 // [nrows padded to 128][32] tf32 A rows (K-major SW128 image)
+  const float* sopB;                 // [n padded to 256][32] tf32 B rows
+  const unsigned long long* smin;    // [2] ordered keys: min potential shift over rows, over columns (nats)
+  unsigned long long* scount;        // [2] += entries kept, entries screened (nullable)
 };
 
 bool tma_supported(const EvalArgs& a);
@@ -114,6 +120,17 @@ int tma_smem_bytes();
 // Launch the fused evaluation over the (row tile x column tile) grid.
 // kind: 0 dense fp32, 1 on-the-fly squared Euclidean.
 cudaError_t launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st);
+// K2s: on-the-fly cost with the tensor-core screen (screen.cu); d in {2, 4, 8, 16}
+bool screen_supported(int d);
+cudaError_t launch_eval_screen(const EvalArgs& a, cudaStream_t st);
+size_t screen_smem_bytes();
+// ordered 64-bit key of a double (unsigned order = numeric order; atomicMin)
+__host__ __device__ inline unsigned long long double_key(double x) {
+  unsigned long long b;
+  memcpy(&b, &x, sizeof b);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+constexpr unsigned long long kKeyPosInf = 0xFFF0000000000000ull;   // double_key(+inf)
 
 // Exact fp64 evaluator (two-pass online log-sum-exp, fp64 exp): fallback of
 // the fp32 path and the fp64-P precision mode.  Writes lr (rows of this
@@ -192,6 +209,7 @@ struct FinalizeArgs {
   int fault_repl;        // MDOT_FAULT_NAN=1 hook: copies of item 0 finalized per evaluation (K8 cluster: CL)
   double f64_tot_min;    // fp64 entries: totals below this (anchored units) are redone exactly -- the
                          // bound on the mass K8's entry skip may have dropped (batch.cu); 0 = 1e-300
+  unsigned long long* smin_reset;   // nullable: [2] screen shift minima, reset to +inf (block 0) for the next prep
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 cudaError_t launch_finalize_multi(const FinalizeArgs* args_dev, const FinalizeArgs& a0, int B, cudaStream_t st);
@@ -274,7 +292,27 @@ struct PrepArgs {
   const CtrlState* ctrl;
   double *cur_lm, *cur_m, *cur_s, *cur_g;
   const double *tr_lm, *tr_m, *tr_s, *tr_g;
+  // K2s screen operands (device control only; null = off): the accept copy
+  // also carries the base potentials of the accepted evaluation (cur_bp),
+  // prep writes this evaluation's bases to tr_bp, the item's 128-byte tf32
+  // operand row (screen.cu) to sopA / sopB and the per-side minimum shift to
+  // smin[2] (k_prep)
+  double* cur_bp; double* tr_bp;
+  float* sopA; float* sopB;
+  unsigned long long* smin;
+  const float* X; const float* Y; int d; float scale;   // on-the-fly coordinates
+  const double* sop_ymax;            // max_j |y_j| (setup)
+  float screen_T;                    // entries below 2^-T of their row and column totals are skipped
 };
+// one 128-byte operand row of K2s (screen.cu): 8 chunks of 16 bytes, chunk c
+// stored at position c ^ (r & 7) -- the K-major SW128 image of row r
+__device__ __forceinline__ void sop_store(float* rowbase, int64_t r, const float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(rowbase + 4 * (c ^ (int)(r & 7))) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+cudaError_t launch_norm_max(const float* P, int64_t m, int d, double* out, cudaStream_t st);
+cudaError_t launch_sop_pad(float* sopA, int64_t nrows, float* sopB, int64_t n, cudaStream_t st);
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
 // out[i] = sqnorm_recipe(P + i d, d) for i < m (the Z22b recipe, otf_cost.cuh)
 cudaError_t launch_sqnorms(const float* P, int64_t m, int d, float* out, cudaStream_t st);

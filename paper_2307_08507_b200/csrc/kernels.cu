@@ -772,6 +772,7 @@ __global__ void __launch_bounds__(256) k_finalize_multi(const FinalizeArgs* args
 }
 
 __device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
+  if (a.smin_reset && blockIdx.x == 0 && threadIdx.x < 2) a.smin_reset[threadIdx.x] = kKeyPosInf;   // K2s: next prep
   if (a.done && *a.done) return;
   const int sub = threadIdx.x & (kFinTPI - 1);
   const int64_t tot_items = a.item_end > 0 ? a.item_end : a.nrows + a.n;
@@ -899,10 +900,28 @@ cudaError_t launch_ctrl(CtrlState* st, int slot, int* done_host, int* ran_host, 
   return cudaGetLastError();
 }
 
-__global__ void k_prep(PrepArgs a) {
+__global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= a.nrows + a.n) return;
-  prep_item(a, k, a.ctrl);
+  const bool in = k < a.nrows + a.n;
+  const double dlt = in ? prep_item(a, k, a.ctrl) : INFINITY;
+  if (!a.sopA) return;
+  // K2s screen bounds: per-side minimum shift, block-reduced, one atomic per side and block
+  double mr = (in && k < a.nrows) ? dlt : INFINITY;
+  double mc = (in && k >= a.nrows) ? dlt : INFINITY;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mr = fmin(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+    mc = fmin(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+  }
+  __shared__ double sm[2][8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sm[0][w] = mr; sm[1][w] = mc; }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double m = INFINITY;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmin(m, sm[threadIdx.x][q]);
+    if (m < INFINITY) atomicMin(&a.smin[threadIdx.x], double_key(m));
+  }
 }
 
 __global__ void k_prep_multi(const PrepArgs* args) {
@@ -921,6 +940,49 @@ cudaError_t launch_prep_multi(const PrepArgs* args_dev, const PrepArgs& a0, int 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
   const int64_t items = a.nrows + a.n;
   k_prep<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// K2s (screen.cu): max_j |y_j| over the points (the tf32 error bound), once
+// per solve; one CTA, fixed-order reduction
+__global__ void __launch_bounds__(1024) k_norm_max(const float* __restrict__ P, int64_t m, int d, double* out) {
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < d; ++t) s = __fma_rn((double)P[i * d + t], (double)P[i * d + t], s);
+    mx = fmax(mx, sqrt(s));
+  }
+  __shared__ double sm[32];
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sm[w]);
+    *out = __dmul_rn(mx, 1.0 + 1e-6);
+  }
+}
+cudaError_t launch_norm_max(const float* P, int64_t m, int d, double* out, cudaStream_t st) {
+  k_norm_max<<<1, 1024, 0, st>>>(P, m, d, out);
+  return cudaGetLastError();
+}
+// K2s padding rows (past nrows / n up to the chunk / tile multiple): never kept
+__global__ void k_sop_pad(float* sopA, int64_t nrows, int64_t nrows_p, float* sopB, int64_t n, int64_t n_p) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ka = nrows_p - nrows, kb = n_p - n;
+  if (t >= ka + kb) return;
+  const bool isA = t < ka;
+  const int64_t r = isA ? nrows + t : n + (t - ka);
+  float v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = 0.f;
+  if (isA) { v[16] = -1.0e32f; v[20] = 1.f; v[21] = 1.f; }
+  else { v[18] = -1.0e32f; }
+  sop_store((isA ? sopA : sopB) + r * 32, r, v);
+}
+cudaError_t launch_sop_pad(float* sopA, int64_t nrows, float* sopB, int64_t n, cudaStream_t st) {
+  const int64_t nrows_p = (nrows + 127) / 128 * 128 + 128, n_p = (n + 255) / 256 * 256;
+  const int64_t tot = nrows_p - nrows + n_p - n;
+  if (tot > 0) k_sop_pad<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(sopA, nrows, nrows_p, sopB, n, n_p);
   return cudaGetLastError();
 }
 

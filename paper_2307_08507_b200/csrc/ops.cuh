@@ -56,6 +56,12 @@ __device__ __forceinline__ float4 split_param(double base, double anchor, int* f
   return make_float4((float)ah, M, (float)(exp2(anchor) * (double)M), 0.f);
 }
 
+__device__ __forceinline__ float screen_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 // fp64-entry parameter slot: {base potential (fp64), 2^anchor (fp32), anchor (fp32)}
 __device__ __forceinline__ float4 f64_param(double base, double anchor) {
   float4 r;
@@ -68,7 +74,9 @@ __device__ __forceinline__ float4 f64_param(double base, double anchor) {
 // One row/column item of the prep step (k in [0, nrows + n)); the controller
 // state `c` (device control) overrides mode / alpha / beta and requests the
 // element-wise accept copy.
-__device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const CtrlState* c) {
+// Returns this item's potential shift against the accepted iterate (K2s
+// screen operands, a.sopA set) or +inf.
+__device__ __forceinline__ double prep_item(const PrepArgs& a, int64_t k, const CtrlState* c) {
   MDOT_DCHECK(k >= 0 && k < a.nrows + a.n);
   const bool is_row = k < a.nrows;
   const int64_t idx = is_row ? k : k - a.nrows;
@@ -82,13 +90,14 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
       if (a.cur_m) a.cur_m[k] = a.tr_m[k];
       a.cur_s[k] = a.tr_s[k];
       a.cur_g[k] = a.tr_g[k];
+      if (a.cur_bp) a.cur_bp[k] = a.tr_bp[k];
     }
     if (c->accept_pot) {
       a.pprev[k] = a.p[k];
       if (is_row) a.u[idx] = a.tu[idx];
       else a.v[idx] = a.tv[idx];
     }
-    if (c->done) return;
+    if (c->done) return INFINITY;
     mode = c->mode;
     alpha = c->alpha;
     beta = c->beta;
@@ -147,6 +156,47 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t k, const Ct
       a.colp[idx] = q;
     }
   }
+  if (!a.sopA) return INFINITY;
+  // K2s (screen.cu): the marginal at the new potentials is at least the
+  // accepted iterate's times e^(this shift + the other side's smallest
+  // shift); the latter is a grid-wide minimum, folded in by the kernel
+  // (every rounding explicit: the screen's decisions, and so the kept set,
+  // must not depend on the compiler's contraction choices -- checked and
+  // release builds give identical bits)
+  double dlt = __dsub_rn(base, a.cur_bp[k]);
+  if (!(dlt == dlt)) dlt = -INFINITY;
+  a.tr_bp[k] = base;
+  double sl = __dmul_rn(__dadd_rn(a.cur_lm[k], dlt), L2E_D);   // log2 of the predicted marginal, own shift only
+  if (!(sl == sl)) sl = -INFINITY;
+  const double mlog = -log2((double)a.n);
+  const double g = __dmul_rn(__dadd_rn((double)c->gpair[0], (double)c->gpair[1]), (double)a.scale);
+  const float4 q = is_row ? a.rowp[idx] : a.colp[idx];
+  const float* P = (is_row ? a.X : a.Y) + idx * a.d;
+  float v[32];
+  double nrm2 = 0.0;
+  const float tg = is_row ? (float)__dmul_rn(2.0, g) : 1.f;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const float x = t < a.d ? P[t] : 0.f;
+    nrm2 = __fma_rn((double)x, (double)x, nrm2);
+    v[t] = screen_tf32(__fmul_rn(tg, x));
+  }
+  double w = __dsub_rn(__dsub_rn(__dadd_rn((double)q.x, log2((double)q.z)), __dmul_rn(g, nrm2)), fmin(sl, mlog));
+  if (is_row) {
+    const double delta = __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, g), sqrt(nrm2)), __dmul_rn(*a.sop_ymax, 1.001 / 1024.0)), 2.0);
+    w = __dadd_rn(w, __dadd_rn(__dadd_rn(mlog, (double)a.screen_T), delta));
+  }
+  if (!(w < 1.0e30)) w = 1.0e30;   // +inf / NaN: keep the whole row / column
+  const float wh = screen_tf32((float)w), wl = screen_tf32((float)__dsub_rn(w, (double)wh));
+  if (is_row) {   // chunk 4 {alpha_hi, alpha_lo, 1, 1}, chunk 5 {1, 1, 0, 0}
+    v[16] = wh; v[17] = wl; v[18] = 1.f; v[19] = 1.f; v[20] = 1.f; v[21] = 1.f;
+  } else {        // chunk 4 {1, 1, beta_hi, beta_lo}, chunk 5 {-G_hi, -G_lo, 0, 0} (G: per CTA)
+    v[16] = 1.f; v[17] = 1.f; v[18] = wh; v[19] = wl; v[20] = 0.f; v[21] = 0.f;
+  }
+#pragma unroll
+  for (int t = 22; t < 32; ++t) v[t] = 0.f;
+  sop_store((is_row ? a.sopA : a.sopB) + idx * 32, idx, v);
+  return dlt;
 }
 
 // Fault injection for the error-path tests (MDOT_FAULT_NAN, solver.cu):

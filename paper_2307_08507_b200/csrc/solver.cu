@@ -188,6 +188,12 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   size_t o_tot = take(items + 32);
   size_t o_ctrl = take((int64_t)((sizeof(CtrlState) + 7) / 8));
   size_t o_nrm = take((items + 1) / 2);   // items floats
+  size_t o_bp[2] = {take(items), take(items)};
+  const int64_t nrows_p = (nrows + 127) / 128 * 128, n_p = (n + 255) / 256 * 256;
+  // 32 floats per row; A one chunk longer: tiles shorter than 128 rows run
+  // their last chunk's MMA over up to 127 rows past the padded end
+  size_t o_sopA = take((nrows_p + 128) * 16), o_sopB = take(n_p * 16);
+  size_t o_scr = take(6);                 // smin[2], scount[2], ymax
   const size_t tickets = (size_t)eval.n_row_tiles + eval.n_col_tiles + 64;
   size_t bytes = dbl * sizeof(double) + (size_t)(items + 64) * sizeof(float4) + 256 + tickets * 4;
 #ifdef MDOT_CHECKED
@@ -209,7 +215,15 @@ mdot_status Workspace::alloc(cudaStream_t stream, int64_t n_, int64_t nrows_) {
   A = D + o_A; B = D + o_B; p = D + o_p; pprev = D + o_pp;
   for (int b = 0; b < 2; ++b) {
     mg[b].lm = D + o_m[b][0]; mg[b].m = D + o_m[b][1]; mg[b].s = D + o_m[b][2]; mg[b].g = D + o_m[b][3];
+    mg[b].bp = D + o_bp[b];
   }
+  sopA = reinterpret_cast<float*>(D + o_sopA);
+  sopB = reinterpret_cast<float*>(D + o_sopB);
+  smin = reinterpret_cast<unsigned long long*>(D + o_scr);
+  scount = smin + 2;
+  sop_ymax = D + o_scr + 4;
+  CK(cudaMemsetAsync(smin, 0xFF, 2 * sizeof(unsigned long long), st));   // NaN keys: keep everything
+  CK(cudaMemsetAsync(scount, 0, 2 * sizeof(unsigned long long), st));
   cur = &mg[0];
   trial = &mg[1];
   rowpart = D + o_rowpart; colpart = D + o_colpart; colm = D + o_colm; cols = D + o_cols; lr_ex = D + o_lr;
@@ -552,6 +566,11 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
   a.ctrl = ctrl;
   a.cur_lm = cur->lm; a.cur_m = cur->m; a.cur_s = cur->s; a.cur_g = cur->g;
   a.tr_lm = trial->lm; a.tr_m = trial->m; a.tr_s = trial->s; a.tr_g = trial->g;
+  const bool scr = screen_cap && !exact_mode;   // K2s bounds (every slot, so cur->bp stays current)
+  if (scr) {
+    a.cur_bp = cur->bp; a.tr_bp = trial->bp; a.sopA = sopA; a.sopB = sopB; a.smin = smin;
+    a.X = Xdev; a.Y = Ydev; a.d = d; a.scale = scale; a.sop_ymax = sop_ymax; a.screen_T = screen_T;
+  }
   CKL(launch_prep(a, s));
   FinalizeArgs f{};
   f.n = n; f.nrows = nrows;
@@ -564,6 +583,7 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
   f.prep_flag = flag;
   f.jacobi = jacobi;
   f.done = &ctrl->done;
+  if (scr) f.smin_reset = smin;
   if (timed) CK(cudaEventRecordWithFlags(gev[2], s, cudaEventRecordExternal));
   if (!exact_mode) {
     EvalArgs e = eval;
@@ -571,6 +591,12 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
     e.done = &ctrl->done;
     if (use_tma) {
       CKL(launch_eval_tma(tmap, e, tma_grid, s));
+    } else if (scr && screen_now && with_ctrl) {
+      // K2s: the slot's evaluation against the accepted iterate's bounds (the
+      // projection's initial evaluation, with_ctrl = false, stays dense: its
+      // reference marginals belong to the previous gbar)
+      e.sopA = sopA; e.sopB = sopB; e.smin = smin; e.scount = scount;
+      CKL(launch_eval_screen(e, s));
     } else {
       CKL(launch_eval_fast(e, kind_fast, s));
     }
@@ -621,8 +647,9 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
 }
 
 mdot_status Workspace::build_graph() {
-  const void* sig[8] = {cur, trial, u, tu, p, pprev, (const void*)(intptr_t)(exact_mode ? 1 : 0),
-                        (const void*)(intptr_t)(exact_mode ? (int64_t)(gbar * 1024.0) : 0)};
+  const void* sig[9] = {cur, trial, u, tu, p, pprev, (const void*)(intptr_t)(exact_mode ? 1 : 0),
+                        (const void*)(intptr_t)(exact_mode ? (int64_t)(gbar * 1024.0) : 0),
+                        (const void*)(intptr_t)(screen_now ? 1 : 0)};
   if (gexec && memcmp(sig, gsig, sizeof(sig)) == 0) return MDOT_OK;
   if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
   if (!cap_stream) CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
@@ -694,6 +721,12 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
   h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
   w.ctrl_trace_setup(h, t);
   res->control_path = 1;
+  // K2s from the first graph of every projection except the first MD step of
+  // a multi-step schedule (the smallest gamma: nearly every entry matters) and
+  // the one after a probe that kept more than 8 screen_fmax
+  w.screen_now = w.screen_cap && !w.exact_mode && !(t == 1 && !w.md_last) && !w.screen_skip;
+  w.screen_skip = false;
+  bool probe = true;
   CKS(w.build_graph());
   cudaStream_t st = w.st;
   CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, st));
@@ -712,7 +745,25 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
     for (int k = 0; k < w.gslots; ++k) ((volatile int*)w.ran_host)[k] = 0;
     CK(cudaGraphLaunch(w.gexec, st));
     w.launches += (w.sharded() ? 6 : 4) * w.gslots;   // our kernels per slot (NCCL's not counted)
+    const bool was_scr = w.screen_now;
+    unsigned long long hc[2] = {0ull, 0ull};
+    if (was_scr) {
+      CK(cudaMemcpyAsync(hc, w.scount, sizeof(hc), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemsetAsync(w.scount, 0, sizeof(hc), st));
+    }
     CK(cudaStreamSynchronize(st));
+    if (was_scr) {
+      w.screen_kept += (int64_t)hc[0];
+      w.screen_total += (int64_t)hc[1];
+      w.screen_slots += (int64_t)(hc[1] / (unsigned long long)(w.n * w.nrows));
+      // too many survivors at this gbar: the dense kernel is faster for the rest of the projection
+      if (hc[1] > 0 && (double)hc[0] > w.screen_fmax * (double)hc[1]) {
+        if (probe && (double)hc[0] > 8.0 * w.screen_fmax * (double)hc[1]) w.screen_skip = true;
+        w.screen_now = false;
+        CKS(w.build_graph());
+      }
+      probe = false;
+    }
     if (w.time_kernels) {
       float ms = 0.f;
       if (first) {
@@ -727,6 +778,10 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
         w.stage_samples++;
         w.kernel_ms += st4[2];
         w.kernel_launches++;
+        if (was_scr) { w.screen_ms += st4[2]; w.screen_timed++; }
+        if (getenv("MDOT_SCREEN_DEBUG"))
+          fprintf(stderr, "[mdot] t=%d %s eval %.3f ms (kept %.4f%%)\n", t, was_scr ? "K2s" : "K2 ", st4[2],
+                  hc[1] ? 100.0 * (double)hc[0] / (double)hc[1] : 0.0);
       }
     }
     first = false;
@@ -1188,6 +1243,16 @@ mdot_status Workspace::setup(const mdot_options& o) {
   }
   CKL(launch_setup(nrows, r, logr, rho_r, st));
   CKL(launch_setup(n, c, logc, sig_c, st));
+  // K2s (screen.cu): graph-slot control on the on-the-fly cost, one rank
+  const char* se = getenv("MDOT_SCREEN");
+  const bool al16 = ((reinterpret_cast<uintptr_t>(Xdev) | reinterpret_cast<uintptr_t>(Ydev)) & 15) == 0;
+  screen_cap = otf && !sharded() && screen_supported(d) && al16 && !(se && atoi(se) == 0);
+  if (const char* e = getenv("MDOT_SCREEN_T")) screen_T = (float)atof(e);
+  if (const char* e = getenv("MDOT_SCREEN_FMAX")) screen_fmax = atof(e);
+  if (screen_cap) {
+    CKL(launch_norm_max(Ydev, n, d, sop_ymax, st));
+    CKL(launch_sop_pad(sopA, nrows, sopB, n, st));
+  }
   return MDOT_OK;
 }
 
@@ -1315,6 +1380,13 @@ using namespace mdot;
 
 extern "C" {
 
+static thread_local double g_screen_stats[5] = {0, 0, 0, 0, 0};
+mdot_status mdot_last_screen_stats(double* out) {
+  if (!out) return MDOT_EINVAL;
+  for (int q = 0; q < 5; ++q) out[q] = g_screen_stats[q];
+  return MDOT_OK;
+}
+
 const char* mdot_last_error(void) { return g_last_error.c_str(); }
 int32_t mdot_abi_version(void) { return MDOT_ABI_VERSION; }
 
@@ -1433,6 +1505,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       // intermediate MD steps may stop at the looser eps_md (Lemma 2; mdot.h)
       mdot_options ot = o;
       if (!last && o.eps_md > o.eps) ot.eps = o.eps_md;
+      w.md_last = last;
       if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, ot, (int)t, res);
       else if (o.device_control && !(w.sharded() && (w.exact_mode || !comm->capturable())))
         solve_st = project_device(w, ot, (int)t, res);
@@ -1482,6 +1555,8 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   }
   res->evaluations = w.evals;
   res->fallbacks = w.fallbacks;
+  g_screen_stats[0] = (double)w.screen_kept; g_screen_stats[1] = (double)w.screen_total;
+  g_screen_stats[2] = (double)w.screen_slots; g_screen_stats[3] = w.screen_ms; g_screen_stats[4] = (double)w.screen_timed;
   res->kernel_ms = w.kernel_ms;
   res->kernel_launches = w.kernel_launches;
   res->all_launches = w.launches;
@@ -1772,6 +1847,7 @@ static mdot_status solve_batch_lockstep(const mdot_problem* shared, int32_t Bn, 
       R->control_path = 4;
       mdot_options ot = o;
       if (!last && o.eps_md > o.eps) ot.eps = o.eps_md;
+      w.md_last = last;
       mdot_status ps = MDOT_OK;
       if (h.status == CTRL_NOCONV) ps = MDOT_ENOCONV;
       else if (h.status == CTRL_LS_FAIL) {

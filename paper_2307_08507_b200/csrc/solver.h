@@ -18,6 +18,7 @@ struct Marg {           // marginals of one plan (rows then columns, [nrows + n]
   double* m = nullptr;  // marginals
   double* s = nullptr;  // Sinkhorn direction
   double* g = nullptr;  // gradient
+  double* bp = nullptr; // base potentials A, B this plan was evaluated at (K2s screen bounds)
 };
 
 struct Comm;
@@ -68,6 +69,22 @@ struct Workspace {
   int persist_ncta = 0;             // persistent grid: 0 all co-resident CTAs, > 0 at most that many (batch
                                     // workers run side by side on slices of the grid), < 0 off
   unsigned int* pers_bar = nullptr;
+  // K2s screen (screen.cu): graph-slot device control on the on-the-fly
+  // cost, one rank, d in {2, 4, 8, 16}.  screen_cap: prep writes the bounds;
+  // screen_now: the slots evaluate with K2s (dropped for the rest of a
+  // projection once a graph kept more than screen_fmax of its entries)
+  bool screen_cap = false, screen_now = false;
+  bool screen_skip = false;   // the last probe kept > 8 screen_fmax: the next projection stays dense
+  bool md_last = false;       // this projection is the solve's last MD step (set by the MD loop)
+  float screen_T = 48.f;
+  double screen_fmax = 0.008;
+  float* sopA = nullptr;                  // [nrows padded to 128][32] K2s A operand rows (prep)
+  float* sopB = nullptr;                  // [n padded to 256][32] K2s B operand rows (prep)
+  double* sop_ymax = nullptr;             // max_j |y_j|
+  unsigned long long* smin = nullptr;     // [2]
+  unsigned long long* scount = nullptr;   // [2] kept, screened entries (zeroed per graph)
+  int64_t screen_kept = 0, screen_total = 0, screen_slots = 0, screen_timed = 0;
+  double screen_ms = 0.0;
   // stats
   int64_t evals = 0, fallbacks = 0, kernel_launches = 0, launches = 0;
   double kernel_ms = 0.0;
@@ -84,7 +101,7 @@ struct Workspace {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;
   int gslots = 0;
-  const void* gsig[8] = {};
+  const void* gsig[9] = {};
   cudaEvent_t gev[2 * 65] = {};
   bool gev_made = false;
 

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
     // ascending per lane); the list is evaluated 32 entries per warp step,
     // then every lane adds its own row's entries (list order) and lane k the
     // entries of column k of each group (list order = row order).
-    float rsum = 0.f;
+    double rsum = 0.0;   // fp64: a lane's row may collect many survivors
     double csum[4] = {0.0, 0.0, 0.0, 0.0};
     int L = 0;                 // list length (warp-uniform)
     int seg_off[4], seg_cnt[4];
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
       __syncwarp();
 #pragma unroll
       for (int gq = 0; gq < 4; ++gq)
-        for (int t = 0; t < seg_cnt[gq]; ++t) rsum += lrow[seg_off[gq] + t];
+        for (int t = 0; t < seg_cnt[gq]; ++t) rsum += (double)lrow[seg_off[gq] + t];
       // column k of group gq: entries in list order (ascending rows); four at a time
       int p = 0;
       for (; p + 4 <= L; p += 4) {
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
       const int cb = 128 * h + 32 * grp;   // first column of this group (CTA-local)
       uint32_t v[32];
       umma::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)cb, v);
-      umma::tmem_ld_wait();
+      umma::tmem_ld_wait(v);   // binds v: nothing may read it before the asynchronous load lands
       // some t >= 0 in this lane's 32 values <=> the AND of their bit patterns has a clear sign bit
       uint32_t a0 = v[0] & v[1] & v[2] & v[3], a1 = v[4] & v[5] & v[6] & v[7];
       uint32_t a2 = v[8] & v[9] & v[10] & v[11], a3 = v[12] & v[13] & v[14] & v[15];
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
           }
           kept += (lane == 0) ? (unsigned)__popc(mk) : 0u;
         }
-        rsum += rs;
+        rsum += (double)rs;
         continue;
       }
       const int off0 = L + incl - cnt;
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
 #pragma unroll
     for (int gq = 0; gq < 4; ++gq)
       if (csum[gq] != 0.0) S.col[q][128 * h + 32 * gq + lane] += csum[gq];
-    S.row[buf][h][32 * q + lane] = (double)rsum;
+    S.row[buf][h][32 * q + lane] = rsum;
     // M_i before the barrier: the next chunk's copy may overwrite this row-parameter buffer right after it
     const float Mi = tid < rows_c ? RPr[tid].y : 0.f;
     umma::fence_before();

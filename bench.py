@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--c5-recipe", default="dot", choices=["dot", "diff"],
                     help="on-the-fly cost recipe of the config-5 block: dot form (Z22b, d + 7 FP32 ops per pair) "
                          "or difference form (Z22, 2d + 5)")
+    ap.add_argument("--c5-dense-ab", type=int, default=1,
+                    help="also time the full config-5 solve with the screen off (dense K2 only)")
     ap.add_argument("--c5-full", type=int, default=1,
                     help="also time one complete config-5 solve to L1 1e-5 (time-to-eps; ~10 s on one B200)")
     ap.add_argument("--adaptive-gamma-leg", type=float, default=256.0,
@@ -612,17 +614,49 @@ def run_config5(a, rank, world, dev, M, dist, comm, barrier):
         "status_name": res[-1]["status_name"],
     }
     if a.c5_full:
-        solve(0)   # warm the full path once (graph capture, L2)
-        barrier()
-        e0.record(st)
-        full = solve(0)
-        e1.record(st)
-        barrier()
-        ms_full = maxr(e0.elapsed_time(e1))
+        def full_solve():
+            solve(0)   # warm the full path once (graph capture, L2)
+            barrier()
+            e0.record(st)
+            f = solve(0)
+            e1.record(st)
+            barrier()
+            return f, maxr(e0.elapsed_time(e1)), M.mdot_last_screen_stats()
+        if a.c5_dense_ab and world == 1:
+            # the same solve with every evaluation on the dense K2 (K2s off): the screen's gain, measured
+            os.environ["MDOT_SCREEN"] = "0"
+            fd, ms_dense, _ = full_solve()
+            os.environ.pop("MDOT_SCREEN", None)
+            out["time_to_eps_dense_k2_s"] = ms_dense / 1000.0
+            out["dense_k2_solve"] = {k: fd[k] for k in ("evaluations", "cost_unrounded", "l1_final", "status_name")}
+        full, ms_full, sst = full_solve()
         out["time_to_eps_s"] = ms_full / 1000.0
         out["full_solve"] = {k: full[k] for k in ("evaluations", "iterations", "md_steps", "l1_final",
                                                    "cost_unrounded", "cost_rounded", "status_name")}
         out["full_solve"]["evals_per_s"] = full["evaluations"] / (ms_full / 1000.0)
+        if sst["evals"] > 0:
+            # K2s (csrc/screen.cu): the tensor-core screen of the later MD steps.  Floor: the
+            # tf32 MMA work, 2 x 24 flops per pair (K = 24) at the tf32 dense peak (the measured
+            # bf16 burst peak x 1.1 / 2.25, the guide's nominal ratio); the dense-equivalent pair
+            # rate is the rate at which the screened kernel resolves all n^2 pairs.
+            pp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+            pk = json.load(open(pp)) if os.path.exists(pp) else {"bf16_tflops": 2250.0}
+            tf32 = (float(pk.get("bf16_tflops", 2250.0)) * 1.1 / 2.25) * 1e12
+            k2s_s = sst["ms"] / sst["timed"] / 1000.0 if sst["timed"] else None
+            floor_s = 2.0 * 24.0 * float(n) * n / tf32
+            out["screen"] = {
+                "kernel": "k_eval_screen<16> (K2s: tcgen05 kind::tf32 screen + exact recipe on the survivors)",
+                "screened_evaluations": sst["evals"], "kept_fraction": sst["kept_frac"],
+                "mean_launch_ms": k2s_s * 1e3 if k2s_s else None, "launches_timed": sst["timed"],
+                "dense_equivalent_pairs_per_s": (float(n) * n / k2s_s) if k2s_s else None,
+                "vs_dense_k2_fp32_floor": ((float(n) * n / k2s_s) / fp32_peak) if k2s_s else None,
+                "roofline": {"bound": "tensor", "unit": "ms", "floor_ms": floor_s * 1e3,
+                             "frac": (floor_s / k2s_s) if k2s_s else None,
+                             "peak_source": f"tf32 dense = measured bf16 {pk.get('bf16_tflops')} TF/s x 1.1/2.25; "
+                                            "2 x 24 flops per pair (K = 24)"},
+                "note": "bound: keep (i, j) iff log2 P_ij >= min(row, column total) - 48 (rigorous, "
+                        "DESIGN.md Z30); the first MD step and projections keeping > 0.8 % run the dense K2",
+            }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         # the oracle's pair rate on this host: exact fp64 log-marginals of 32
         # sampled rows of the same instance at the same potentials (O(n d) each)

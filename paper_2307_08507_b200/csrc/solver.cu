@@ -740,8 +740,31 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
     (void)before;
   }
   if (w.time_kernels) CK(cudaEventRecord(w.ev1, st));
+  if (w.screen_now) {
+    // K2s probe: ONE slot outside the graphs (a whole graph of K2s slots at a
+    // density where the dense kernel is faster costs several evaluations)
+    ((volatile int*)w.ran_host)[0] = 0;
+    CKS(w.launch_slot_body(st, 0, false, true));
+    w.launches += 4;
+    unsigned long long hc[2] = {0ull, 0ull};
+    CK(cudaMemcpyAsync(hc, w.scount, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(w.scount, 0, sizeof(hc), st));
+    CK(cudaStreamSynchronize(st));
+    w.screen_kept += (int64_t)hc[0];
+    w.screen_total += (int64_t)hc[1];
+    w.screen_slots += (int64_t)(hc[1] / (unsigned long long)(w.n * w.nrows));
+    if (getenv("MDOT_SCREEN_DEBUG"))
+      fprintf(stderr, "[mdot] t=%d probe kept %.4f%%\n", t, hc[1] ? 100.0 * (double)hc[0] / (double)hc[1] : 0.0);
+    if (hc[1] > 0 && (double)hc[0] > w.screen_fmax * (double)hc[1]) {
+      if ((double)hc[0] > 8.0 * w.screen_fmax * (double)hc[1]) w.screen_skip = true;
+      w.screen_now = false;
+      CKS(w.build_graph());
+    }
+    probe = false;
+  }
   bool first = true;
   for (;;) {
+    if (*((volatile int*)w.done_host)) break;   // the probe slot may have ended the projection
     for (int k = 0; k < w.gslots; ++k) ((volatile int*)w.ran_host)[k] = 0;
     CK(cudaGraphLaunch(w.gexec, st));
     w.launches += (w.sharded() ? 6 : 4) * w.gslots;   // our kernels per slot (NCCL's not counted)

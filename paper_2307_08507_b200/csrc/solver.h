@@ -77,7 +77,7 @@ struct Workspace {
   bool screen_skip = false;   // the last probe kept > 8 screen_fmax: the next projection stays dense
   bool md_last = false;       // this projection is the solve's last MD step (set by the MD loop)
   float screen_T = 48.f;
-  double screen_fmax = 0.008;
+  double screen_fmax = 0.004;
   float* sopA = nullptr;                  // [nrows padded to 128][32] K2s A operand rows (prep)
   float* sopB = nullptr;                  // [n padded to 256][32] K2s B operand rows (prep)
   double* sop_ymax = nullptr;             // max_j |y_j|

@@ -106,8 +106,11 @@ struct EvalArgs {
   const float* sopA;                 // [nrows padded to 128][32] tf32 A rows (K-major SW128 image)
   const float* sopB;                 // [n padded to 256][32] tf32 B rows
   const unsigned long long* smin;    // [2] ordered keys: min potential shift over rows, over columns (nats)
+  const double* smin_rows_neg;       // row-sharded: -(min row shift over ALL ranks) (allreduced), else null
   unsigned long long* scount;        // [2] += entries kept, entries screened (nullable)
 };
+// row-sharded K2s: out[0] = -(this rank's min row shift) for a MAX allreduce
+cudaError_t launch_smin_neg(const unsigned long long* smin, double* out, cudaStream_t st);
 
 bool tma_supported(const EvalArgs& a);
 cudaError_t make_tma_map(const EvalArgs& a, void* map_out);

@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
   {
     const double L2E = 1.4426950408889634;
     const double dr = __dsub_rn(__dmul_rn(key_to_double(a.smin[1]), L2E), 1.0);
-    const double dc = __dsub_rn(__dmul_rn(key_to_double(a.smin[0]), L2E), 1.0);
+    // the smallest row shift: over every rank's rows when the rows are sharded
+    const double drow = a.smin_rows_neg ? -a.smin_rows_neg[0] : key_to_double(a.smin[0]);
+    const double dc = __dsub_rn(__dmul_rn(drow, L2E), 1.0);
     G = fmin(dr, dc);
     if (!(G == G)) G = -INFINITY;
   }
@@ -419,6 +421,15 @@ __global__ void __launch_bounds__(kScrThreads, 2) k_eval_screen(EvalArgs a) {
 }
 
 size_t screen_smem_bytes() { return sizeof(ScrSmem) + 1024; }
+
+__global__ void k_smin_neg(const unsigned long long* smin, double* out) {
+  const double v = key_to_double(smin[0]);
+  out[0] = (v == v) ? -v : INFINITY;   // NaN (no prep yet) -> +inf: the allreduced bound keeps everything
+}
+cudaError_t launch_smin_neg(const unsigned long long* smin, double* out, cudaStream_t st) {
+  k_smin_neg<<<1, 1, 0, st>>>(smin, out);
+  return cudaGetLastError();
+}
 
 template <int D, bool POW2, bool DOT>
 static cudaError_t launch_screen_t(const EvalArgs& a, cudaStream_t st) {

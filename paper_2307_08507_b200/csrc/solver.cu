@@ -596,6 +596,14 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
       // projection's initial evaluation, with_ctrl = false, stays dense: its
       // reference marginals belong to the previous gbar)
       e.sopA = sopA; e.sopB = sopB; e.smin = smin; e.scount = scount;
+      if (sharded()) {
+        // column totals sum over every rank's rows: the bound needs the smallest
+        // row shift of ALL ranks (one scalar MAX-allreduce of its negation)
+        double* g = tot.coltot + n + kNumScalars;
+        CKL(launch_smin_neg(smin, g, s));
+        CKS(comm_allreduce(comm, g, 1, COMM_MAX, s));
+        e.smin_rows_neg = g;
+      }
       CKL(launch_eval_screen(e, s));
     } else {
       CKL(launch_eval_fast(e, kind_fast, s));
@@ -710,6 +718,30 @@ mdot_status Workspace::ctrl_trace_collect() {
   return MDOT_OK;
 }
 
+// K2s counters of the slots since the last call (kept, screened), summed over
+// the ranks when sharded so that every rank takes the same screen decision;
+// zeroes them, synchronizes the stream
+mdot_status Workspace::screen_counts(unsigned long long* hc) {
+  if (sharded()) {
+    double* g = tot.coltot + n + kNumScalars + 1;   // 2 doubles past the bound scalar
+    double h[2];
+    CK(cudaMemcpyAsync(hc, scount, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h[0] = (double)hc[0]; h[1] = (double)hc[1];
+    CK(cudaMemcpyAsync(g, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    CKS(comm_allreduce(comm, g, 2, COMM_SUM, st));
+    CK(cudaMemcpyAsync(h, g, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(scount, 0, 2 * sizeof(unsigned long long), st));
+    CK(cudaStreamSynchronize(st));
+    hc[0] = (unsigned long long)h[0]; hc[1] = (unsigned long long)h[1];
+    return MDOT_OK;
+  }
+  CK(cudaMemcpyAsync(hc, scount, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemsetAsync(scount, 0, 2 * sizeof(unsigned long long), st));
+  CK(cudaStreamSynchronize(st));
+  return MDOT_OK;
+}
+
 mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_result* res) {
   CtrlState h{};
   h.eps = o.eps; h.c1 = o.c1; h.c2 = o.c2;
@@ -747,12 +779,10 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
     CKS(w.launch_slot_body(st, 0, false, true));
     w.launches += 4;
     unsigned long long hc[2] = {0ull, 0ull};
-    CK(cudaMemcpyAsync(hc, w.scount, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemsetAsync(w.scount, 0, sizeof(hc), st));
-    CK(cudaStreamSynchronize(st));
+    CKS(w.screen_counts(hc));
     w.screen_kept += (int64_t)hc[0];
     w.screen_total += (int64_t)hc[1];
-    w.screen_slots += (int64_t)(hc[1] / (unsigned long long)(w.n * w.nrows));
+    w.screen_slots += (int64_t)(hc[1] / (unsigned long long)(w.n * (w.sharded() ? w.n : w.nrows)));
     if (getenv("MDOT_SCREEN_DEBUG"))
       fprintf(stderr, "[mdot] t=%d probe kept %.4f%%\n", t, hc[1] ? 100.0 * (double)hc[0] / (double)hc[1] : 0.0);
     if (hc[1] > 0 && (double)hc[0] > w.screen_fmax * (double)hc[1]) {
@@ -770,15 +800,12 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
     w.launches += (w.sharded() ? 6 : 4) * w.gslots;   // our kernels per slot (NCCL's not counted)
     const bool was_scr = w.screen_now;
     unsigned long long hc[2] = {0ull, 0ull};
-    if (was_scr) {
-      CK(cudaMemcpyAsync(hc, w.scount, sizeof(hc), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemsetAsync(w.scount, 0, sizeof(hc), st));
-    }
+    if (was_scr) CKS(w.screen_counts(hc));
     CK(cudaStreamSynchronize(st));
     if (was_scr) {
       w.screen_kept += (int64_t)hc[0];
       w.screen_total += (int64_t)hc[1];
-      w.screen_slots += (int64_t)(hc[1] / (unsigned long long)(w.n * w.nrows));
+      w.screen_slots += (int64_t)(hc[1] / (unsigned long long)(w.n * (w.sharded() ? w.n : w.nrows)));
       // too many survivors at this gbar: the dense kernel is faster for the rest of the projection
       if (hc[1] > 0 && (double)hc[0] > w.screen_fmax * (double)hc[1]) {
         if (probe && (double)hc[0] > 8.0 * w.screen_fmax * (double)hc[1]) w.screen_skip = true;
@@ -1269,7 +1296,9 @@ mdot_status Workspace::setup(const mdot_options& o) {
   // K2s (screen.cu): graph-slot control on the on-the-fly cost, one rank
   const char* se = getenv("MDOT_SCREEN");
   const bool al16 = ((reinterpret_cast<uintptr_t>(Xdev) | reinterpret_cast<uintptr_t>(Ydev)) & 15) == 0;
-  screen_cap = otf && !sharded() && screen_supported(d) && al16 && !(se && atoi(se) == 0);
+  // row-sharded: only with the graph-capturable NCCL transport (device control), where
+  // every rank runs the same slots; the screen's decisions are allreduced (project_device)
+  screen_cap = otf && (!sharded() || comm->capturable()) && screen_supported(d) && al16 && !(se && atoi(se) == 0);
   if (const char* e = getenv("MDOT_SCREEN_T")) screen_T = (float)atof(e);
   if (const char* e = getenv("MDOT_SCREEN_FMAX")) screen_fmax = atof(e);
   if (screen_cap) {

@@ -125,6 +125,7 @@ struct Workspace {
   mdot_status alloc(cudaStream_t stream, int64_t n, int64_t nrows);
   mdot_status launch_slot_body(cudaStream_t s, int slot, bool timed, bool with_ctrl = false);
   mdot_status build_graph();
+  mdot_status screen_counts(unsigned long long* hc);
   void release();
   mdot_status load_problem(const mdot_problem* pb, int64_t row0);
   void free_owned();

@@ -85,3 +85,30 @@ def test_screen_disabled_is_the_dense_kernel(monkeypatch):
     assert st["evals"] == 0
     r2, U2, _, _ = _solve(inst, 2048.0, 4, 1e-5, "dot")
     assert np.array_equal(U1, U2) and r1["evaluations"] == r2["evaluations"]
+
+
+def test_screened_sharded_nccl_one_rank(forced_screen, monkeypatch):
+    """Row-sharded path (the config-5 multi-GPU layout) with K2s: a 1-rank NCCL
+    communicator forced onto the sharded code (MDOT_SHARDED_SELFTEST) runs the
+    graph slots with the allreduced screen bound and decisions; gates against
+    the oracle."""
+    monkeypatch.setenv("MDOT_SHARDED_SELFTEST", "1")
+    n, d, gb, T, eps = 1200, 16, 2048.0, 4, 1e-5
+    inst = S.config5(5, n=n, d=d)
+    r, c = _t(inst.r), _t(inst.c)
+    comm = M.mdot_comm_create(M.mdot_get_unique_id(), 1, 0, 0)
+    try:
+        U = torch.empty(n, dtype=torch.float64, device=DEV)
+        V = torch.empty_like(U)
+        res = M.mdot_solve_sharded(comm, 0, n, X_local=_t(inst.X), Y=_t(inst.Y), scale=float(inst.scale), r=r, c=c,
+                                   n=n, schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=T),
+                                   options=M.options(eps=eps), u_local_out=U, v_out=V, recipe="dot")
+        torch.cuda.synchronize()
+        st = M.mdot_last_screen_stats()
+    finally:
+        M.mdot_comm_destroy(comm)
+    assert res["control_path"] == 1, res["control_path"]
+    assert st["evals"] > 0 and st["kept_frac"] < 0.9, st
+    prob = O.OracleProblem(inst, recipe="dot")
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)

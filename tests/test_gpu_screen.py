@@ -112,3 +112,48 @@ def test_screened_sharded_nccl_one_rank(forced_screen, monkeypatch):
     prob = O.OracleProblem(inst, recipe="dot")
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), O.make_options(eps=eps))
     _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+@pytest.mark.parametrize("projector", ["sinkhorn", "ncg"])
+def test_screened_other_projectors_match_oracle(forced_screen, projector):
+    """The graph slots of Alg. 3 (Sinkhorn half-steps: only one side's
+    potentials move, the other side's shift is 0) and of vanilla NCG use K2s
+    like PNCG; gates against the oracle's same projector."""
+    n, d, gb, T, eps = 800, 8, 1024.0, 2, 1e-5
+    inst = S.config5(6, n=n, d=d)
+    prob = O.OracleProblem(inst, recipe="dot")
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    if projector == "sinkhorn":
+        res = M.mdot_sinkhorn(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c),
+                              schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=T), options=M.options(eps=eps),
+                              u_out=U, v_out=V, recipe="dot")
+        oopts = O.make_options(eps=eps, projector=O.SINKHORN)
+    else:
+        res = M.mdot_solve(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c),
+                           schedule=M.schedule(M.MDOT_SCHED_FIXED, gb, T=T),
+                           options=M.options(eps=eps, projector=M.MDOT_PROJ_NCG), u_out=U, v_out=V, recipe="dot")
+        oopts = O.make_options(eps=eps, projector=O.NCG)
+    torch.cuda.synchronize()
+    st = M.mdot_last_screen_stats()
+    assert st["evals"] > 0, st
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), oopts)
+    _gates(res, ores, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+def test_screened_adaptive_schedule_matches_oracle(forced_screen):
+    """MDOT_SCHED_ADAPTIVE (Z29) realises its steps on the fly; every
+    projection after the first runs K2s (forced); Lemma 2 fixes the plan."""
+    n, d, gb, eps = 1000, 16, 2048.0, 1e-5
+    inst = S.config5(7, n=n, d=d)
+    prob = O.OracleProblem(inst, recipe="dot")
+    U = torch.empty(n, dtype=torch.float64, device=DEV)
+    V = torch.empty_like(U)
+    res = M.mdot_solve(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c),
+                       schedule=M.schedule(M.MDOT_SCHED_ADAPTIVE, gb, step_max=256.0), options=M.options(eps=eps),
+                       u_out=U, v_out=V, recipe="dot")
+    torch.cuda.synchronize()
+    st = M.mdot_last_screen_stats()
+    assert st["evals"] > 0, st
+    Uf, Vf, fres, _ = O.mdot(prob, O.schedule_fixed(gb, T=8), O.make_options(eps=eps))
+    _gates(res, fres, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)

@@ -16,6 +16,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <nvtx3/nvToolsExt.h>
 #include <string.h>
 #include <time.h>
 
@@ -33,6 +34,22 @@
 #include "solver.h"
 
 namespace mdot {
+
+// NVTX ranges (header-only NVTX v3: no library to link; a profiler that
+// injects itself -- nsys, ncu --nvtx -- sees the solve, each MD step (its
+// projection) and the rounding as named ranges; otherwise each is a no-op call)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int t, double gbar) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), fmt, t, gbar);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 static thread_local std::string g_last_error;
 
@@ -1501,6 +1518,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   // MDOT_TRACE: host timestamps per stage (synchronizes between stages)
   const bool trace = getenv("MDOT_TRACE") != nullptr;
   double tr_last = t0;
+  NvtxRange solve_range("mdot solve");
   auto trace_mark = [&](const char* what, long long a0, long long a1) {
     if (!trace) return;
     cudaStreamSynchronize(stream);
@@ -1558,6 +1576,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       mdot_options ot = o;
       if (!last && o.eps_md > o.eps) ot.eps = o.eps_md;
       w.md_last = last;
+      NvtxRange md_range("md step %d gbar %g", (int)t, gb);
       if (o.device_control == 1 && w.pers_grid > 0 && !w.exact_mode) solve_st = project_persistent(w, ot, (int)t, res);
       else if (o.device_control && !(w.sharded() && (w.exact_mode || !comm->capturable())))
         solve_st = project_device(w, ot, (int)t, res);
@@ -1586,7 +1605,10 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
         if (pb->mem == MDOT_MEM_DEVICE) Pdev = P_out;
         else if (cudaMallocAsync((void**)&Pown, sizeof(float) * nr * n, stream) == cudaSuccess) Pdev = Pown;
       }
-      st = w.round_and_cost(Pdev, &res->cost_unrounded, &res->cost_rounded);
+      {
+        NvtxRange rr("rounding (Altschuler) + cost");
+        st = w.round_and_cost(Pdev, &res->cost_unrounded, &res->cost_rounded);
+      }
       if (st == MDOT_OK && Pown) {
         if (cudaMemcpyAsync(P_out, Pown, sizeof(float) * nr * n, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
           st = MDOT_ECUDA;

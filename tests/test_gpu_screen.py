@@ -157,3 +157,17 @@ def test_screened_adaptive_schedule_matches_oracle(forced_screen):
     assert st["evals"] > 0, st
     Uf, Vf, fres, _ = O.mdot(prob, O.schedule_fixed(gb, T=8), O.make_options(eps=eps))
     _gates(res, fres, inst, prob, U.cpu().numpy(), V.cpu().numpy(), eps)
+
+
+@pytest.mark.parametrize("recipe", ["dot", "diff"])
+def test_screened_non_power_of_two_scale(forced_screen, recipe):
+    """A cost scale that is not a power of two (0.1): the recipe multiplies
+    C~ by the scale (no fold into gh / gl) in K2s's exact path as in K2."""
+    import dataclasses
+    n, d, gb, T, eps = 700, 8, 1024.0, 2, 1e-5
+    inst = dataclasses.replace(S.config5(8, n=n, d=d), scale=0.1)
+    prob = O.OracleProblem(inst, recipe=recipe)
+    res, U, V, st = _solve(inst, gb, T, eps, recipe)
+    assert st["evals"] > 0, st
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=T), O.make_options(eps=eps))
+    _gates(res, ores, inst, prob, U, V, eps)

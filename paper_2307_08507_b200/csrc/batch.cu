@@ -400,7 +400,22 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
     // the 4 rows' C values (L2) are loaded before any is used: with 8 warps
     // per SM the per-row loads were exposed (long-scoreboard stalls on their
     // first use: 32 % of the warp samples)
+    // full 256-column tile, whole 4-row groups (n % 4 == 0), aligned fp32 C:
+    // two float4 loads per row from one base pointer, no per-row bounds tests
+    // (the general path below spent ~90 issue slots per 4-row step on them)
+    const bool fast_tile = sizeof(CT) == 4 && vec4 && (n % 4) == 0 && j0 + kTileN <= n;
     auto load_group = [&](int ib, CT (&cvg)[4][8]) {
+      if (fast_tile) {
+        const float* base = reinterpret_cast<const float*>(C) + (int64_t)ib * n + j0 + 4 * lane;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 x0 = __ldg(reinterpret_cast<const float4*>(base + (int64_t)u * n));
+          const float4 x1 = __ldg(reinterpret_cast<const float4*>(base + (int64_t)u * n + 128));
+          cvg[u][0] = x0.x; cvg[u][1] = x0.y; cvg[u][2] = x0.z; cvg[u][3] = x0.w;
+          cvg[u][4] = x1.x; cvg[u][5] = x1.y; cvg[u][6] = x1.z; cvg[u][7] = x1.w;
+        }
+        return;
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = ib + u;

@@ -309,7 +309,8 @@ __device__ void batch_eval_tail_f64(const CT* __restrict__ C, int n, int j0, con
 // Cluster split (CL CTAs per instance, q = this CTA's rank): the CTA takes
 // the row groups ib = 4 (q W + w) + 4 W CL m; row totals are complete for
 // its rows, column totals are partial over them (combined by the caller).
-template <bool F64, bool PACKED, typename CT>
+// R4: n % 4 == 0, so every row of a 4-row group exists (no per-row guards)
+template <bool F64, bool PACKED, typename CT, bool R4 = false>
 __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, float gh, float gl, double g2,
                            double gbar, double* rowtot, double* coltot, double (*sred)[kTileN], int q_rank,
                            int CL, double skip_z = -INFINITY, unsigned long long* dbgp = nullptr) {
@@ -450,7 +451,7 @@ __device__ void batch_eval(const CT* __restrict__ C, int n, const float4* prm, f
         CT cv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) cv[q] = cvc[u][q];
-        const float4 rp = (i < n) ? rowp[i] : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+        const float4 rp = (R4 || i < n) ? rowp[i] : make_float4(-1.0e30f, 0.f, 0.f, 0.f);
         if (!F64 && !PACKED) {
           float rsum = 0.f;
 #pragma unroll
@@ -752,8 +753,12 @@ __global__ void __launch_bounds__(kBatchThreads, 1) k_batch_solve(BatchArgs a) {
           }
           batch_eval<true, false, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, skip_z);
         } else {
-          batch_eval<false, PACKED, CT>(reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C), n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, -INFINITY,
-                                        (a.dbg && b == 0 && q_rank == 0) ? a.dbg : nullptr);
+          const CT* Cb = reinterpret_cast<const CT*>(a.C64 ? (const void*)a.C64 : (const void*)a.C);
+          unsigned long long* dbg = (a.dbg && b == 0 && q_rank == 0) ? a.dbg : nullptr;
+          if ((n & 3) == 0)
+            batch_eval<false, PACKED, CT, true>(Cb, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, -INFINITY, dbg);
+          else
+            batch_eval<false, PACKED, CT, false>(Cb, n, prm, gh, gl, g2, gbar, tot, tot + n, S.sred, q_rank, CL, -INFINITY, dbg);
         }
         __syncthreads();
         K8_MARK(2)

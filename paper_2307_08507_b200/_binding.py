@@ -118,10 +118,12 @@ def lib():
         L.mdot_solve_sharded.argtypes = [P, ct.POINTER(Problem), ct.c_int64, ct.c_int64,
                                          ct.POINTER(Schedule), ct.POINTER(Options), P, P,
                                          ct.POINTER(Result)]
-        L.mdot_last_screen_stats.argtypes = [ct.POINTER(D)]
+        if hasattr(L, "mdot_last_screen_stats"):   # absent from libraries built before K2s (A/B builds)
+            L.mdot_last_screen_stats.argtypes = [ct.POINTER(D)]
+            L.mdot_last_screen_stats.restype = ct.c_int
         for nm in ("mdot_solve_batch", "mdot_marginals", "mdot_round", "mdot_get_unique_id",
                    "mdot_comm_create", "mdot_comm_create_local", "mdot_comm_enable_peer", "mdot_comm_destroy",
-                   "mdot_solve_sharded", "mdot_last_screen_stats"):
+                   "mdot_solve_sharded"):
             getattr(L, nm).restype = ct.c_int
         if L.mdot_abi_version() != 3:
             raise ImportError("libmdot_b200.so ABI version mismatch")

@@ -61,11 +61,38 @@ __device__ __forceinline__ double bred4(double v0, double v1, double v2, double 
 template <int NS>
 __device__ __forceinline__ void block_sum(double (&v)[NS], double* scratch /*[kBatchWarps][NS]*/, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (NS == 16) {
+    // reduce-scatter butterfly: each stage halves the values a lane holds (the
+    // half it keeps is chosen by its lane bit) and adds the partner's other
+    // half -- 16 + 8 + 4 + 2 + 1 = 31 fp64 shuffles instead of 16 x 5 = 80;
+    // after the stages lane l (l < 16 after the last) holds scalar q(l) summed
+    // over the warp in a fixed order
+    double a[16];
 #pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    double x = v[q];
-    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-    if (lane == 0) scratch[warp * NS + q] = x;
+    for (int q = 0; q < 16; ++q) a[q] = v[q];
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+      const int half = 8 >> st;            // values kept after this stage
+      const int off = 16 >> st;            // partner lane distance
+      const bool up = lane & off;
+#pragma unroll
+      for (int q = 0; q < half; ++q) {
+        const double send = up ? a[q] : a[q + half];
+        const double keep = up ? a[q + half] : a[q];
+        a[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    // one value per lane: scalar index from the lane bits 16, 8, 4, 2 (bit 1 pairs stay to be added)
+    const double x = a[0] + __shfl_xor_sync(0xffffffffu, a[0], 1);
+    const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    if ((lane & 1) == 0) scratch[warp * NS + q] = x;
+  } else {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      double x = v[q];
+      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+      if (lane == 0) scratch[warp * NS + q] = x;
+    }
   }
   __syncthreads();
   if (threadIdx.x < NS) {

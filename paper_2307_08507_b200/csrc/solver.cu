@@ -1752,6 +1752,18 @@ static mdot_status solve_batch_lockstep(const mdot_problem* shared, int32_t Bn, 
     CKS(w.load_problem(&p, 0));
     CKS(w.setup(o));
     if (!w.use_tma || w.exact_mode || w.otf) return MDOT_EGEN;
+    // P0 = r c^T: U = log r, V = log c; u = v = 0 (Alg. 1
+    // line 2) -- as in the single solve; the workspace comes from the memory
+    // pool and holds whatever the last user left there
+    if (o.p0_ones) {
+      launch_fill(n, 0.0, w.U, stream);
+      launch_fill(n, 0.0, w.V, stream);
+    } else {
+      CK(cudaMemcpyAsync(w.U, w.logr, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+      CK(cudaMemcpyAsync(w.V, w.logc, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+    }
+    launch_fill(n, 0.0, w.u, stream);
+    launch_fill(n, 0.0, w.v, stream);
   }
   // argument arrays (pointers fixed for the whole solve: device control
   // accepts by element-wise copies, never by swapping buffers)

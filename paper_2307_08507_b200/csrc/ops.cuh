@@ -53,7 +53,9 @@ __device__ __forceinline__ float4 split_param(double base, double anchor, int* f
   }
   const double al = a2 - ah;
   const float M = (float)exp2(al);
-  return make_float4((float)ah, M, (float)(exp2(anchor) * (double)M), 0.f);
+  // integer anchors (k_setup rounds them): exp2(anchor) * M == ldexp(M, anchor) exactly
+  const double S = (anchor == rint(anchor)) ? ldexp((double)M, (int)anchor) : exp2(anchor) * (double)M;
+  return make_float4((float)ah, M, (float)S, 0.f);
 }
 
 __device__ __forceinline__ float screen_tf32(float x) {
@@ -66,7 +68,7 @@ __device__ __forceinline__ float screen_tf32(float x) {
 __device__ __forceinline__ float4 f64_param(double base, double anchor) {
   float4 r;
   *reinterpret_cast<double*>(&r.x) = base;
-  r.z = (float)exp2(anchor);
+  r.z = (float)((anchor == rint(anchor)) ? ldexp(1.0, (int)anchor) : exp2(anchor));
   r.w = (float)anchor;
   return r;
 }

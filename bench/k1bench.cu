@@ -454,12 +454,13 @@ int main(int argc, char** argv) {
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     for (int tm : {128, 256, 512}) {
-      if (quick && tm != 512) continue;
+      if (quick && tm != (getenv("K1B_TM") ? atoi(getenv("K1B_TM")) : 512)) continue;
       ProdCtx pc{};
       pc.e.C = C; pc.e.ldc = n; pc.e.n = n; pc.e.nrows = n; pc.e.tile_m = tm;
       pc.e.n_col_tiles = (int)(n / 256); pc.e.n_row_tiles = (int)(n / tm);
       pc.e.rowp = rowp; pc.e.colp = colp; pc.e.gh = 16.0f; pc.e.gl = 1e-6f;
       pc.e.rowpart = rowpart; pc.e.colpart = colpart;
+      if (getenv("K1B_KEEP")) pc.e.keep_l2 = 1;   // C read with evict_last (L2-resident when it fits)
       CK(mdot::make_tma_map(pc.e, pc.map));
       pc.grid = (int)std::min<int64_t>((int64_t)pc.e.n_row_tiles * pc.e.n_col_tiles, 2 * sms);
       char nm[128];

@@ -275,6 +275,34 @@ mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, 
                                const mdot_schedule* sched, const mdot_options* opt,
                                double* u_local_out, double* v_out, mdot_result* res);
 
+/* 2-D (row x column) sharding (past the replicated
+ * column vectors of mdot_solve_sharded).  The ranks form a Gr x Gc grid; this
+ * rank owns the block rows [row0, row0 + n_rows) x columns
+ * [col0, col0 + n_cols) of the n x n cost (block->C points at that block,
+ * row-major, n_rows x n_cols, leading dimension n_cols; block->n is the
+ * GLOBAL n; block->r, block->c are the FULL marginals, validated as in
+ * mdot_solve).  An evaluation is K1 over the block, then
+ * two allreduces: the block's row sums over `row_comm` (the Gc ranks of this
+ * row block) and its column sums over `col_comm` (the Gr ranks of this column
+ * block); rows and columns then finalize locally and the 16 control scalars
+ * are summed over the other communicator (row items are replicated across
+ * row_comm, column items across col_comm), so every rank holds identical
+ * scalars and takes identical line-search decisions.
+ * Rounding reduces its row sums over row_comm and its column
+ * sums over col_comm the same way.  Either communicator may have one rank
+ * (Gr = 1 or Gc = 1).  u_local_out: [n_rows], v_local_out: [n_cols] (the
+ * rank's slices of the gauge-fixed potentials; identical across the
+ * replicas).  Restrictions (-> MDOT_EINVAL): dense fp32 C only
+ * (MDOT_COST_DENSE_F32), fp32-entry precision (options.precision AUTO with
+ * eps >= 5e-8, or F32P); the host control loop runs (device_control is
+ * ignored).  If the fp32-entry range guard fires (an evaluation far from
+ * feasibility) the call returns MDOT_EINSTABLE: the exact fp64 evaluator is
+ * not distributed in 2-D. */
+mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, const mdot_problem* block,
+                                  int64_t row0, int64_t n_rows, int64_t col0, int64_t n_cols,
+                                  const mdot_schedule* sched, const mdot_options* opt, double* u_local_out,
+                                  double* v_local_out, mdot_result* res);
+
 /* Screened evaluation statistics of the calling thread's last mdot_solve /
  * mdot_sinkhorn (K2s): on-the-fly costs with
  * d in {2, 4, 8, 16} on one rank evaluate the graph-slot trials with a

@@ -8,7 +8,7 @@ package raises if the library is missing or cannot be loaded.
 Python names mirror the C entry points:
     mdot_solve, mdot_sinkhorn, mdot_solve_batch, mdot_marginals, mdot_round,
     mdot_get_unique_id, mdot_comm_create, mdot_comm_destroy,
-    mdot_solve_sharded, mdot_last_error, mdot_last_screen_stats
+    mdot_solve_sharded, mdot_solve_sharded_2d, mdot_last_error, mdot_last_screen_stats
 Arrays may be CUDA torch tensors (MDOT_MEM_DEVICE, used in place on the
 current stream) or host numpy arrays / CPU tensors (MDOT_MEM_HOST, copied in
 and out inside the call).
@@ -54,6 +54,7 @@ from ._binding import (  # noqa: F401
     mdot_solve,
     mdot_solve_batch,
     mdot_solve_sharded,
+    mdot_solve_sharded_2d,
     options,
     read_trace,
     schedule,

@@ -118,6 +118,11 @@ def lib():
         L.mdot_solve_sharded.argtypes = [P, ct.POINTER(Problem), ct.c_int64, ct.c_int64,
                                          ct.POINTER(Schedule), ct.POINTER(Options), P, P,
                                          ct.POINTER(Result)]
+        if hasattr(L, "mdot_solve_sharded_2d"):   # absent from libraries built before session 4 (A/B builds)
+            L.mdot_solve_sharded_2d.argtypes = [P, P, ct.POINTER(Problem), ct.c_int64, ct.c_int64, ct.c_int64,
+                                                ct.c_int64, ct.POINTER(Schedule), ct.POINTER(Options), P, P,
+                                                ct.POINTER(Result)]
+            L.mdot_solve_sharded_2d.restype = ct.c_int
         if hasattr(L, "mdot_last_screen_stats"):   # absent from libraries built before K2s (A/B builds)
             L.mdot_last_screen_stats.argtypes = [ct.POINTER(D)]
             L.mdot_last_screen_stats.restype = ct.c_int
@@ -373,6 +378,32 @@ def mdot_comm_enable_peer(comm, n_max: int, check=True):
 
 def mdot_comm_destroy(comm):
     _check(lib().mdot_comm_destroy(comm), "mdot_comm_destroy")
+
+
+def mdot_solve_sharded_2d(row_comm, col_comm, row0, n_rows, col0, n_cols, C_block, r, c, *, n,
+                          schedule=None, options=None, u_local_out=None, v_local_out=None, check=True):
+    """2-D (row x column) sharded solve (include/mdot.h mdot_solve_sharded_2d):
+    C_block = C[row0:row0+n_rows, col0:col0+n_cols] (contiguous fp32), r, c the
+    full marginals, n the global size; row_comm joins the ranks of this row
+    block, col_comm those of this column block."""
+    if tuple(C_block.shape) != (int(n_rows), int(n_cols)):
+        raise ValueError(f"C_block shape {tuple(C_block.shape)} != ({n_rows}, {n_cols})")
+    pb = problem(C_block, r, c, n=n)
+    sched = schedule if schedule is not None else globals()["schedule"]()
+    opts = options if options is not None else globals()["options"]()
+    if pb.mem == MDOT_MEM_DEVICE:
+        opts.stream = _current_stream()
+    res = Result()
+    dev = pb.mem == MDOT_MEM_DEVICE
+    st = lib().mdot_solve_sharded_2d(row_comm, col_comm, ct.byref(pb), int(row0), int(n_rows), int(col0),
+                                     int(n_cols), ct.byref(sched), ct.byref(opts),
+                                     _ptr(u_local_out, F64, "u_local_out", dev),
+                                     _ptr(v_local_out, F64, "v_local_out", dev), ct.byref(res))
+    d = res.as_dict()
+    d["status"] = st
+    if check:
+        _check(st, "mdot_solve_sharded_2d")
+    return d
 
 
 def mdot_solve_sharded(comm, row0, n_local, C_local=None, r=None, c=None, *, X_local=None, Y=None,

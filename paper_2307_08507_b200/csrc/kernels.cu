@@ -790,7 +790,8 @@ __device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
   if (a.from_partials == 1) {   // octet-parallel partial sums; the shuffles run on the whole warp
     double x = 0.0;
     if (in_range) {
-      if (is_row) x = octet_partial(a.rowpart + k, a.nrows, a.n_col_tiles, sub);
+      if (is_row) x = a.rowtot ? ((sub == 0) ? a.rowtot[k] : 0.0)   // already reduced (2-D sharded)
+                               : octet_partial(a.rowpart + k, a.nrows, a.n_col_tiles, sub);
       else if (a.coltot) x = (sub == 0) ? a.coltot[k - a.nrows] : 0.0;   // already reduced (sharded)
       else x = octet_partial(a.colpart + (k - a.nrows), a.n, a.n_row_tiles, sub);
     }

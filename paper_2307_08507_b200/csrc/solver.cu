@@ -325,7 +325,37 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
     f.from_partials = 1;
     f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
     f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
-    if (!shard) {
+    if (two_d()) {
+      // 2-D block: row totals are partial over this rank's columns, column
+      // totals over its rows.  Allreduce each over the ranks holding the other
+      // parts (row_comm / col_comm), finalize both sides locally, then sum
+      // each side's 16 scalars over the ranks holding the OTHER blocks of that
+      // side (row items are replicated across comm_row, columns across comm).
+      double* colbuf = tot.coltot;                   // [n column totals | 16 column scalars]
+      double* rowbuf = tot.coltot + n + kNumScalars; // [nrows row totals | 16 row scalars]
+      CKL(launch_reduce_colpart(colpart, eval.n_row_tiles, n, colbuf, st));
+      CKL(launch_reduce_colpart(rowpart, eval.n_col_tiles, nrows, rowbuf, st));   // [tc][row]: same layout
+      CKS(comm_allreduce(comm, colbuf, (size_t)n, COMM_SUM, st));
+      CKS(comm_allreduce(comm_row, rowbuf, (size_t)nrows, COMM_SUM, st));
+      FinalizeArgs fr = f;
+      fr.rowtot = rowbuf;
+      fr.item_begin = 0; fr.item_end = nrows;
+      fr.scalars_dev = rowbuf + nrows; fr.scalars_host = nullptr;
+      CKL(launch_finalize(fr, st));
+      FinalizeArgs fc = f;
+      fc.coltot = colbuf;
+      fc.item_begin = nrows; fc.item_end = nrows + n;
+      fc.scalars_dev = colbuf + n; fc.scalars_host = nullptr;
+      fc.prep_flag = nullptr;
+      CKL(launch_finalize(fc, st));
+      CKS(comm_allreduce(comm, rowbuf + nrows, kNumScalars, COMM_SUM, st));
+      CKS(comm_allreduce(comm_row, colbuf + n, kNumScalars, COMM_SUM, st));
+      double h[2][kNumScalars];
+      CK(cudaMemcpyAsync(h[0], rowbuf + nrows, sizeof(h[0]), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h[1], colbuf + n, sizeof(h[1]), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int q = 0; q < kNumScalars; ++q) scal_host[q] = h[0][q] + h[1][q];
+    } else if (!shard) {
       CKL(launch_finalize(f, st));
     } else {
       // rows are complete locally; columns are partial over this rank's rows.
@@ -356,6 +386,11 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
     memcpy(sc, scal_host, kNumScalars * sizeof(double));
     if (sc[SC_BAD] == 0.0) return MDOT_OK;
     fallbacks++;
+  }
+  if (two_d()) {
+    set_error("2-D sharded solve: the fp32-entry range guard fired at gbar=%g (the exact fp64 evaluator is not "
+              "distributed in 2-D; mdot.h)", gbar);
+    return MDOT_EINSTABLE;
   }
   ExactArgs x{};
   x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
@@ -1142,20 +1177,22 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
   }
   if (!otf && !pb->C) { set_error("C is NULL"); return MDOT_EINVAL; }
   if (!pb->r || !pb->c) { set_error("r or c is NULL"); return MDOT_EINVAL; }
-  // marginals: validate on a host copy
-  std::vector<double> hr(n), hc(n);
+  // marginals: validate on a host copy (2-D: the full marginals, n_glob long;
+  // this rank keeps its row and column slices)
+  const int64_t ng = two_d() ? n_glob : n;
+  std::vector<double> hr(ng), hc(ng);
   if (dev) {
-    CK(cudaMemcpyAsync(hr.data(), pb->r + row0 * 0, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hc.data(), pb->c, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hr.data(), pb->r, sizeof(double) * ng, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), pb->c, sizeof(double) * ng, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   } else {
-    memcpy(hr.data(), pb->r, sizeof(double) * n);
-    memcpy(hc.data(), pb->c, sizeof(double) * n);
+    memcpy(hr.data(), pb->r, sizeof(double) * ng);
+    memcpy(hc.data(), pb->c, sizeof(double) * ng);
   }
-  CKS(validate_marginal(hr.data(), n, "r"));
-  CKS(validate_marginal(hc.data(), n, "c"));
+  CKS(validate_marginal(hr.data(), ng, "r"));
+  CKS(validate_marginal(hc.data(), ng, "c"));
   CK(cudaMemcpyAsync(r, hr.data() + row0, sizeof(double) * nrows, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c, hc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c, hc.data() + (two_d() ? col0 : 0), sizeof(double) * n, cudaMemcpyHostToDevice, st));
   // cost
   if (otf) {
     if (dev) {
@@ -1224,7 +1261,7 @@ mdot_status Workspace::load_problem(const mdot_problem* pb, int64_t row0) {
       eval.l2_res_tiles = (int64_t)(res_bytes / (4.0 * eval.tile_m * kTileN));
       // sharded: the persistent path needs the fused peer exchange
       // (mdot_comm_enable_peer); CTAs per rank from the transport
-      if (getenv("MDOT_NO_PERSIST") || persist_ncta < 0) pers_grid = 0;
+      if (getenv("MDOT_NO_PERSIST") || persist_ncta < 0 || two_d()) pers_grid = 0;
       else if (sharded()) pers_grid = comm_peer_ncta(comm, n, persist_grid());
       else pers_grid = comm ? 0 : persist_grid();
       if (persist_ncta > 0 && pers_grid > persist_ncta) pers_grid = persist_ncta;
@@ -1304,6 +1341,10 @@ mdot_status Workspace::setup(const mdot_options& o) {
   // that resolution (the same rule as the batched solver, mdot_solve_batch)
   exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && (c_f64 || o.eps < 5e-8));
   jacobi = o.projector == MDOT_PROJ_PNCG_JACOBI;
+  if (two_d() && exact_mode) {
+    set_error("2-D sharded solve: fp32-entry precision only (eps >= 5e-8 with AUTO, or F32P); mdot.h");
+    return MDOT_EINVAL;
+  }
   if (!exact_mode && c_f64) {
     set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
     return MDOT_EINVAL;
@@ -1315,7 +1356,7 @@ mdot_status Workspace::setup(const mdot_options& o) {
   const bool al16 = ((reinterpret_cast<uintptr_t>(Xdev) | reinterpret_cast<uintptr_t>(Ydev)) & 15) == 0;
   // row-sharded: only with the graph-capturable NCCL transport (device control), where
   // every rank runs the same slots; the screen's decisions are allreduced (project_device)
-  screen_cap = otf && (!sharded() || comm->capturable()) && screen_supported(d) && al16 && !(se && atoi(se) == 0);
+  screen_cap = otf && !two_d() && (!sharded() || comm->capturable()) && screen_supported(d) && al16 && !(se && atoi(se) == 0);
   if (const char* e = getenv("MDOT_SCREEN_T")) screen_T = (float)atof(e);
   if (const char* e = getenv("MDOT_SCREEN_FMAX")) screen_fmax = atof(e);
   if (screen_cap) {
@@ -1333,7 +1374,7 @@ mdot_status Workspace::gauge_center(double* X_, double* Y_) {
   // rows (possibly sharded) and columns (replicated) separately
   CKL(launch_dots(nrows, 1, &xs[0], &ys[0], blockpart, ticket, scal_dev, scal_host_dev, st));
   double a = 0.0;
-  if (sharded()) {
+  if (sharded() || two_d()) {
     CKS(comm_allreduce(comm, scal_dev, 1, COMM_SUM, st));
     CK(cudaMemcpyAsync(&a, scal_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1342,8 +1383,15 @@ mdot_status Workspace::gauge_center(double* X_, double* Y_) {
     a = scal_host[0];
   }
   CKL(launch_dots(n, 1, &xs[1], &ys[1], blockpart, ticket, scal_dev, scal_host_dev, st));
-  CK(cudaStreamSynchronize(st));
-  const double b = scal_host[0];
+  double b = 0.0;
+  if (two_d()) {   // this rank's column block: sum over the row team
+    CKS(comm_allreduce(comm_row, scal_dev, 1, COMM_SUM, st));
+    CK(cudaMemcpyAsync(&b, scal_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } else {
+    CK(cudaStreamSynchronize(st));
+    b = scal_host[0];
+  }
   const double dd = 0.5 * (a - b);
   CKL(launch_add_scalar(nrows, -dd, X_, st));
   CKL(launch_add_scalar(n, dd, Y_, st));
@@ -1363,7 +1411,8 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   a.n = n; a.nrows = nrows; a.gbar = gbar;
   a.logr = logr; a.logc = logc;
   const int chr = round_chunks(a, true), chc = round_chunks(a, false);
-  const size_t dbl = (size_t)(4 + 3 * chr) * nrows + (size_t)(3 + chc) * n;
+  if (two_d() && P_out_dev) { set_error("2-D sharded solve: no dense plan output"); return MDOT_EINVAL; }
+  const size_t dbl = (size_t)(4 + 3 * chr + (two_d() ? 3 : 0)) * nrows + (size_t)(3 + chc) * n;
   double* buf = nullptr;
 #ifdef MDOT_CHECKED
   CK(cudaMallocAsync((void**)&buf, (dbl + kGuardDbl) * sizeof(double), st));
@@ -1382,18 +1431,33 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
   double* ec = Bpp + n;
   double* cs = ec + n;
   double* colS = cs + n;
+  // 2-D: row sums of this rank's column block, summed over the row team
+  double* rowT = colS + (size_t)chc * n;   // [3][nrows] (S, C, E)
+  auto row_team_sum = [&](int k) -> mdot_status {
+    const double* src[3] = {rowS, rowC, rowE};
+    for (int q = 0; q < k; ++q) {
+      CKL(launch_sum_chunks(src[q], chr, nrows, rowT + (size_t)q * nrows, st));
+    }
+    CKS(comm_allreduce(comm_row, rowT, (size_t)k * nrows, COMM_SUM, st));
+    return MDOT_OK;
+  };
   mdot_status stt = MDOT_OK;
   auto run = [&]() -> mdot_status {
     // R0: r(F), <C, F> per row
     a.A = U; a.B = V; a.chunks = chr; a.rowS = rowS; a.rowC = rowC; a.rowE = rowE;
     CKL(launch_round_rows(a, 0, st));
-    CKL(launch_round_x(nrows, chr, rowS, rowC, r, U, logx, Ap, rowcostF, st));
+    if (two_d()) {
+      CKS(row_team_sum(2));
+      CKL(launch_round_x(nrows, 1, rowT, rowT + nrows, r, U, logx, Ap, rowcostF, st));
+    } else {
+      CKL(launch_round_x(nrows, chr, rowS, rowC, r, U, logx, Ap, rowcostF, st));
+    }
     // R2: c(F') per column (partial over this rank's rows)
     a.A = Ap; a.B = V; a.chunks = chc; a.colS = colS;
     CKL(launch_round_cols(a, st));
     const double* colsum = colS;
     int colchunks = chc;
-    if (sharded()) {
+    if (sharded() || two_d()) {
       CKL(launch_sum_chunks(colS, chc, n, cs, st));
       CKS(comm_allreduce(comm, cs, (size_t)n, COMM_SUM, st));
       colsum = cs;
@@ -1403,10 +1467,16 @@ mdot_status Workspace::round_and_cost(float* P_out_dev, double* cost_F, double* 
     // R3: r(F''), <C, F''>, C err_c per row
     a.A = Ap; a.B = Bpp; a.ec = ec; a.chunks = chr;
     CKL(launch_round_rows(a, 1, st));
-    CKL(launch_round_fin(nrows, chr, rowS, rowC, rowE, rowcostF, r, er, blockpart, ticket, scal_dev, scal_host_dev,
-                         st));
+    if (two_d()) {
+      CKS(row_team_sum(3));
+      CKL(launch_round_fin(nrows, 1, rowT, rowT + nrows, rowT + 2 * nrows, rowcostF, r, er, blockpart, ticket,
+                           scal_dev, scal_host_dev, st));
+    } else {
+      CKL(launch_round_fin(nrows, chr, rowS, rowC, rowE, rowcostF, r, er, blockpart, ticket, scal_dev, scal_host_dev,
+                           st));
+    }
     double ner, cF2, corr, cF;
-    if (sharded()) {
+    if (sharded() || two_d()) {
       CKS(comm_allreduce(comm, scal_dev, 4, COMM_SUM, st));
       double h4[4];
       CK(cudaMemcpyAsync(h4, scal_dev, sizeof(h4), cudaMemcpyDeviceToHost, st));
@@ -1485,7 +1555,8 @@ void mdot_schedule_default(mdot_schedule* s) {
 static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched, const mdot_options* opt_in,
                               double* u_out, double* v_out, float* P_out, mdot_result* res, int force_sinkhorn,
                               Comm* comm = nullptr, int64_t row0 = 0, int64_t nrows_in = -1,
-                              int persist_ncta = 0) {
+                              int persist_ncta = 0, Comm* comm_row = nullptr, int64_t col0 = 0,
+                              int64_t ncols_in = -1) {
   g_last_error.clear();
   if (!res) { set_error("result pointer is NULL"); return MDOT_EINVAL; }
   memset(res, 0, sizeof(*res));
@@ -1505,6 +1576,12 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   const int64_t n = pb->n;
   const int64_t nr = nrows_in < 0 ? n : nrows_in;
   if (row0 < 0 || nr < 1 || row0 + nr > n) { set_error("bad row range"); res->status = MDOT_EINVAL; return MDOT_EINVAL; }
+  // columns held by this rank: all n, or (2-D) the block [col0, col0 + nc)
+  const int64_t nc = comm_row ? ncols_in : n;
+  if (comm_row && (col0 < 0 || nc < 1 || col0 + nc > n)) {
+    set_error("bad column range"); res->status = MDOT_EINVAL; return MDOT_EINVAL;
+  }
+  if (comm_row) o.device_control = 0;   // 2-D: host control loop (mdot.h)
   // sharded: device control (CUDA-graph slots with the NCCL allreduce captured
   // inside) needs a capturable transport; the in-process transport syncs on
   // the host in every allreduce, so it runs the host loop
@@ -1514,6 +1591,9 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   Workspace w;
   w.comm = comm;
   w.row0 = row0;
+  w.comm_row = comm_row;
+  w.col0 = comm_row ? col0 : 0;
+  w.n_glob = n;
   w.persist_ncta = persist_ncta;
   // MDOT_TRACE: host timestamps per stage (synchronizes between stages)
   const bool trace = getenv("MDOT_TRACE") != nullptr;
@@ -1526,7 +1606,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     fprintf(stderr, "[mdot-trace] %-10s %9.3f ms  (%lld, %lld)\n", what, (now - tr_last) * 1e3, a0, a1);
     tr_last = now;
   };
-  st = w.alloc(stream, n, nr);
+  st = w.alloc(stream, nc, nr);
   if (st == MDOT_OK && o.trace && o.trace_cap > 0) {
     w.trace_cap = o.trace_cap;
     const size_t recs = (size_t)std::min<int64_t>(o.trace_cap, kTraceDevCap);
@@ -1547,13 +1627,13 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     // P0 = r c^T -> U = log r, V = log c ; u = v = 0 (Alg. 1 line 2)
     if (o.p0_ones) {
       ++w.launches; launch_fill(nr, 0.0, w.U, stream);
-      ++w.launches; launch_fill(n, 0.0, w.V, stream);
+      ++w.launches; launch_fill(nc, 0.0, w.V, stream);
     } else {
       cudaMemcpyAsync(w.U, w.logr, sizeof(double) * nr, cudaMemcpyDeviceToDevice, stream);
-      cudaMemcpyAsync(w.V, w.logc, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream);
+      cudaMemcpyAsync(w.V, w.logc, sizeof(double) * nc, cudaMemcpyDeviceToDevice, stream);
     }
     ++w.launches; launch_fill(nr, 0.0, w.u, stream);
-    ++w.launches; launch_fill(n, 0.0, w.v, stream);
+    ++w.launches; launch_fill(nc, 0.0, w.v, stream);
     double gb = 0.0, gprev = 0.0;
     // ADAPTIVE (Z29): steps chosen after each projection from its cost
     double next = adaptive ? gam[0] : 0.0, eta_prev = 0.0;
@@ -1567,10 +1647,10 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       w.set_gamma(gb);
       if (o.warm == MDOT_WARM_ZERO) {
         ++w.launches; launch_fill(nr, 0.0, w.u, stream);
-        ++w.launches; launch_fill(n, 0.0, w.v, stream);
+        ++w.launches; launch_fill(nc, 0.0, w.v, stream);
       } else if (o.warm == MDOT_WARM_SCALED && t > 1 && gt != gprev) {
         ++w.launches; launch_axpby(nr, 0.0, w.u, gt / gprev, w.u, stream);   // Z4: scale by gamma_t / gamma_{t-1}
-        ++w.launches; launch_axpby(n, 0.0, w.v, gt / gprev, w.v, stream);
+        ++w.launches; launch_axpby(nc, 0.0, w.v, gt / gprev, w.v, stream);
       }
       // intermediate MD steps may stop at the looser eps_md (Lemma 2; mdot.h)
       mdot_options ot = o;
@@ -1585,7 +1665,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       res->md_steps = (int64_t)t;
       trace_mark("project", (long long)t, (long long)w.evals);
       ++w.launches; launch_axpby(nr, 1.0, w.u, 1.0, w.U, stream);   // U += u
-      ++w.launches; launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);   // V += v
+      ++w.launches; launch_axpby(nc, 1.0, w.v, 1.0, w.V, stream);   // V += v
       if (solve_st != MDOT_OK && solve_st != MDOT_ENOCONV) break;
       st = w.gauge_center(w.U, w.V);
       if (st == MDOT_OK) st = w.gauge_center(w.u, w.v);
@@ -1603,14 +1683,14 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
       float* Pown = nullptr;
       if (P_out) {
         if (pb->mem == MDOT_MEM_DEVICE) Pdev = P_out;
-        else if (cudaMallocAsync((void**)&Pown, sizeof(float) * nr * n, stream) == cudaSuccess) Pdev = Pown;
+        else if (cudaMallocAsync((void**)&Pown, sizeof(float) * nr * nc, stream) == cudaSuccess) Pdev = Pown;
       }
       {
         NvtxRange rr("rounding (Altschuler) + cost");
         st = w.round_and_cost(Pdev, &res->cost_unrounded, &res->cost_rounded);
       }
       if (st == MDOT_OK && Pown) {
-        if (cudaMemcpyAsync(P_out, Pown, sizeof(float) * nr * n, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        if (cudaMemcpyAsync(P_out, Pown, sizeof(float) * nr * nc, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
           st = MDOT_ECUDA;
       }
       if (Pown) cudaFreeAsync(Pown, stream);
@@ -1618,7 +1698,7 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
     }
     const cudaMemcpyKind k = pb->mem == MDOT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (u_out) cudaMemcpyAsync(u_out, w.U, sizeof(double) * nr, k, stream);
-    if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * n, k, stream);
+    if (v_out) cudaMemcpyAsync(v_out, w.V, sizeof(double) * nc, k, stream);
   }
   if (st == MDOT_OK) st = w.l2_reset();
   if (st == MDOT_OK) st = w.check_guards();
@@ -1701,6 +1781,28 @@ mdot_status mdot_solve_sharded(mdot_comm* c, const mdot_problem* local_rows, int
   if (!cm || !local_rows) { set_error("bad arguments"); return MDOT_EINVAL; }
   if (cudaSetDevice(cm->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }
   return solve_impl(local_rows, sched, opt, u_local_out, v_out, nullptr, res, 0, cm, row0, n_local);
+}
+
+// 2-D (row x column) sharding: the block
+// evaluation's row sums travel over the row team, its column sums over the
+// column team; the host loop runs the Appx. C line search on the summed
+// scalars (identical on every rank of the grid).
+mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, const mdot_problem* block,
+                                  int64_t row0, int64_t n_rows, int64_t col0, int64_t n_cols,
+                                  const mdot_schedule* sched, const mdot_options* opt, double* u_local_out,
+                                  double* v_local_out, mdot_result* res) {
+  Comm* cr = reinterpret_cast<Comm*>(row_comm);
+  Comm* cc = reinterpret_cast<Comm*>(col_comm);
+  if (!cr || !cc || !block) { set_error("bad arguments"); return MDOT_EINVAL; }
+  if (block->kind != MDOT_COST_DENSE_F32) {
+    set_error("2-D sharded solve: dense fp32 C only (mdot.h)");
+    if (res) { memset(res, 0, sizeof(*res)); res->status = MDOT_EINVAL; }
+    return MDOT_EINVAL;
+  }
+  if (cr->device != cc->device) { set_error("row and column communicators on different devices"); return MDOT_EINVAL; }
+  if (cudaSetDevice(cc->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }
+  return solve_impl(block, sched, opt, u_local_out, v_local_out, nullptr, res, 0, cc, row0, n_rows, 0, cr, col0,
+                    n_cols);
 }
 
 // Throughput mode, lockstep ("including as

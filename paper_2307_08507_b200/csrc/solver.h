@@ -28,6 +28,14 @@ struct Workspace {
   Comm* comm = nullptr;
   int64_t row0 = 0;
   int64_t n = 0, nrows = 0;
+  // 2-D (row x column) sharding (mdot_solve_sharded_2d): this rank owns the
+  // block rows [row0, row0 + nrows) x columns [col0, col0 + n) of an n_glob x
+  // n_glob problem; `comm` joins the ranks of this column block (other row
+  // blocks: column sums), `comm_row` the ranks of this row block (other
+  // column blocks: row sums).  Host control loop only.
+  Comm* comm_row = nullptr;
+  int64_t col0 = 0, n_glob = 0;
+  bool two_d() const { return comm_row != nullptr; }
   // problem
   const void* Cdev = nullptr;
   const float* Xdev = nullptr;

@@ -1,0 +1,151 @@
+"""2-D (row x column) sharding (mdot_solve_sharded_2d) on
+one GPU: a Gr x Gc grid of virtual ranks = threads of this process, each with
+its own stream and its own block C[rows_a, cols_b]; the row team of a rank is
+an in-process communicator over the Gc ranks of its row block, the column team
+one over the Gr ranks of its column block (host-side rank-ordered sums: no
+device code waits on another rank, so the ranks may share the GPU).
+
+Gates:
+  * every rank takes identical decisions: identical evaluation counts, costs,
+    and identical potential slices across the replicas of a block;
+  * unrounded cost within the Z20 gate (1e-5 relative) of the single-GPU solve;
+  * the oracle's fp64 re-evaluation of the assembled (U, V): L1 <= 2 eps;
+  * rounding: the rounded and unrounded costs equal the oracle's rounding of
+    the SAME assembled (U, V) to 1e-10 relative.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2307_08507_b200 as M  # noqa: E402
+
+DEV = torch.device("cuda:0")
+COST_GATE = 1e-5
+
+
+def _t(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def _solve_2d(inst, Gr, Gc, sched, opts_kw, tag):
+    n = inst.n
+    rows = np.array_split(np.arange(n), Gr)
+    cols = np.array_split(np.arange(n), Gc)
+    out = {}
+    err = []
+
+    def run(a, b):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                r0, nr = int(rows[a][0]), len(rows[a])
+                c0, nc = int(cols[b][0]), len(cols[b])
+                Cb = _t(inst.C[r0:r0 + nr, c0:c0 + nc])
+                U = torch.empty(nr, dtype=torch.float64, device=DEV)
+                V = torch.empty(nc, dtype=torch.float64, device=DEV)
+                rc = M.mdot_comm_create_local(f"{tag}_row{a}", Gc, b, 0)
+                cc = M.mdot_comm_create_local(f"{tag}_col{b}", Gr, a, 0)
+                res = M.mdot_solve_sharded_2d(rc, cc, r0, nr, c0, nc, Cb, _t(inst.r), _t(inst.c), n=n,
+                                              schedule=sched, options=M.options(**opts_kw),
+                                              u_local_out=U, v_local_out=V, check=False)
+                s.synchronize()
+                M.mdot_comm_destroy(rc)
+                M.mdot_comm_destroy(cc)
+                out[(a, b)] = (res, U.cpu().numpy(), V.cpu().numpy(), M.mdot_last_error())
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    ths = [threading.Thread(target=run, args=(a, b)) for a in range(Gr) for b in range(Gc)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    if err:
+        raise err[0]
+    return out, rows, cols
+
+
+@pytest.mark.parametrize("Gr,Gc,projector", [(2, 2, 0), (1, 3, 0), (3, 2, 0), (2, 2, 1)])
+def test_2d_grid_matches_single_gpu_and_oracle(Gr, Gc, projector):
+    n = 600                                   # ragged blocks for Gr, Gc = 3 (200 x 300, 300 x 200 ...)
+    inst = S.uniform_points_instance(3, n, 2, 31, marg="dirichlet")
+    gb, T, eps = 512.0, 2, 1e-6
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=T)
+    kw = {"eps": eps, "projector": projector}
+    out, rows, cols = _solve_2d(inst, Gr, Gc, sched, kw, f"g2d_{Gr}{Gc}{projector}")
+    r00 = out[(0, 0)][0]
+    assert all(o[0]["status"] == 0 for o in out.values()), [(k, o[0]["status_name"], o[3]) for k, o in out.items()]
+    assert all(o[0]["control_path"] == 0 for o in out.values())      # host control loop (mdot.h)
+    # identical decisions and scalars on every rank of the grid
+    assert all(o[0]["evaluations"] == r00["evaluations"] for o in out.values())
+    assert all(o[0]["cost_unrounded"] == r00["cost_unrounded"] for o in out.values())
+    assert all(o[0]["cost_rounded"] == r00["cost_rounded"] for o in out.values())
+    # replicas: U slices identical across a row team, V slices across a column team
+    for a in range(Gr):
+        assert all(np.array_equal(out[(a, b)][1], out[(a, 0)][1]) for b in range(Gc))
+    for b in range(Gc):
+        assert all(np.array_equal(out[(a, b)][2], out[(0, b)][2]) for a in range(Gr))
+    assert r00["l1_final"] <= eps
+    ref = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(**kw))
+    assert abs(r00["cost_unrounded"] - ref["cost_unrounded"]) <= COST_GATE * ref["cost_unrounded"]
+    U = np.concatenate([out[(a, 0)][1] for a in range(Gr)])
+    V = np.concatenate([out[(0, b)][2] for b in range(Gc)])
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, U, V, gb)
+    l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
+    assert l1 <= 2 * eps, l1
+    rp = O.round_plan(prob, U, V, gb)
+    assert abs(r00["cost_unrounded"] - rp["cost_F"]) <= 1e-10 * rp["cost_F"], (r00["cost_unrounded"], rp["cost_F"])
+    assert abs(r00["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"], (r00["cost_rounded"], rp["cost_G"])
+
+
+def test_2d_one_by_one_grid_equals_host_loop_solve():
+    """A 1 x 1 grid is the unsharded problem on the 2-D code path: same
+    decisions as the single-GPU host-loop solve (device_control = 0) up to the
+    summation order of the reduced partials (Z20 gate), oracle rounding of its
+    own (U, V) to 1e-10."""
+    n = 1000
+    inst = S.uniform_points_instance(3, n, 2, 32, marg="dirichlet")
+    gb, eps = 1024.0, 1e-6
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=4)
+    out, _, _ = _solve_2d(inst, 1, 1, sched, {"eps": eps}, "g2d_11")
+    res, U, V, _ = out[(0, 0)]
+    assert res["status"] == 0 and res["l1_final"] <= eps
+    ref = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched,
+                       options=M.options(eps=eps, device_control=0))
+    assert abs(res["cost_unrounded"] - ref["cost_unrounded"]) <= COST_GATE * ref["cost_unrounded"]
+    rp = O.round_plan(O.OracleProblem(inst), U, V, gb)
+    assert abs(res["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]
+
+
+def test_2d_rejects_unsupported_inputs():
+    """fp64-entry precision and on-the-fly / fp64 costs are outside the 2-D
+    path (mdot.h): MDOT_EINVAL before any device work."""
+    n = 64
+    inst = S.uniform_points_instance(3, n, 2, 33, marg="dirichlet")
+    rc = M.mdot_comm_create_local("g2d_rej_row", 1, 0, 0)
+    cc = M.mdot_comm_create_local("g2d_rej_col", 1, 0, 0)
+    try:
+        sched = M.schedule(M.MDOT_SCHED_FIXED, 64.0, T=1)
+        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 0, n, _t(inst.C), _t(inst.r), _t(inst.c), n=n, schedule=sched,
+                                      options=M.options(eps=1e-9), check=False)
+        assert res["status"] == 1 and "fp32-entry" in M.mdot_last_error()
+        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 0, n, _t(inst.C.astype(np.float64)), _t(inst.r), _t(inst.c),
+                                      n=n, schedule=sched, options=M.options(eps=1e-6), check=False)
+        assert res["status"] == 1 and "dense fp32" in M.mdot_last_error()
+        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 8, n - 8, _t(inst.C[:, 8:]), _t(inst.r), _t(inst.c), n=n - 4,
+                                      schedule=sched, options=M.options(eps=1e-6), check=False)
+        assert res["status"] == 1
+    finally:
+        M.mdot_comm_destroy(rc)
+        M.mdot_comm_destroy(cc)

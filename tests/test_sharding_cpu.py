@@ -196,3 +196,73 @@ def test_peer_exchange_protocol_double_buffering(G):
     for t in ths:
         t.join()
     assert not errors, errors[:3]
+
+
+def _worker_2d(rank, world, port, q, Gr, Gc):
+    """2-D grid (mdot_solve_sharded_2d): rank (a, b) = (rank // Gc, rank % Gc)
+    owns block rows_a x cols_b.  Row sums go over the row team (same a), column
+    sums over the column team (same b); row-side scalars (replicated across the
+    row team) are then summed over the column team, column-side scalars over
+    the row team -- the order of collectives the CUDA path uses."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import synthetic as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    row_teams = [dist.new_group([a * Gc + b for b in range(Gc)]) for a in range(Gr)]
+    col_teams = [dist.new_group([a * Gc + b for a in range(Gr)]) for b in range(Gc)]
+    a, b = rank // Gc, rank % Gc
+    inst = S.uniform_points_instance(3, 101, 2, 12, marg="dirichlet")
+    n = inst.n
+    rng = np.random.default_rng(1)
+    A = np.log(inst.r) + 0.1 * rng.standard_normal(n)
+    B = np.log(inst.c) + 0.1 * rng.standard_normal(n)
+    p = rng.standard_normal(2 * n)
+    g = 30.0
+    rows = np.array_split(np.arange(n), Gr)[a]
+    cols = np.array_split(np.arange(n), Gc)[b]
+    Cb = inst.C[np.ix_(rows, cols)].astype(np.float64)
+    P = np.exp(A[rows, None] + B[None, cols] - g * Cb)
+    rsum = torch.from_numpy(P.sum(1).copy())
+    csum = torch.from_numpy(P.sum(0).copy())
+    dist.all_reduce(rsum, group=row_teams[a])     # rows: over the column blocks
+    dist.all_reduce(csum, group=col_teams[b])     # columns: over the row blocks
+    rP, cP = rsum.numpy(), csum.numpy()
+    rs = torch.from_numpy(np.array([rP.sum(), np.abs(rP - inst.r[rows]).sum(), (p[:n][rows] * (rP - inst.r[rows])).sum()]))
+    cs = torch.from_numpy(np.array([0.0, np.abs(cP - inst.c[cols]).sum(), (p[n:][cols] * (cP - inst.c[cols])).sum()]))
+    dist.all_reduce(rs, group=col_teams[b])       # row items: replicated across the row team
+    dist.all_reduce(cs, group=row_teams[a])       # column items: replicated across the column team
+    tot = (rs + cs).numpy()
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, A, B, g)
+    rr, cc = np.exp(lr), np.exp(lc)
+    ref = np.array([rr.sum(), np.abs(rr - inst.r).sum() + np.abs(cc - inst.c).sum(),
+                    (p[:n] * (rr - inst.r)).sum() + (p[n:] * (cc - inst.c)).sum()])
+    q.put((rank, tot.tolist(), ref.tolist(), float(np.abs(rP - rr[rows]).max() / rr[rows].max()),
+           float(np.abs(cP - cc[cols]).max() / cc[cols].max())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("Gr,Gc", [(2, 2), (1, 3)])
+def test_2d_grid_decomposition(Gr, Gc):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = Gr * Gc
+    procs = [ctx.Process(target=_worker_2d, args=(r, world, port, q, Gr, Gc)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, tot, ref, drow, dcol in got:
+        # identical scalars on every rank, equal to the unsharded evaluation
+        np.testing.assert_allclose(tot, ref, rtol=1e-12, atol=1e-15)
+        assert drow < 1e-13 and dcol < 1e-13

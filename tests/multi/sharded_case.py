@@ -2,7 +2,8 @@
 tests/test_gpu_multi.py with torch.distributed.run, one process per GPU):
 rows of C (dense, fused peer exchange over NVLink / CUDA IPC) or of X
 (on-the-fly cost, NCCL allreduce in CUDA-graph slots) sharded over the
-ranks; rank 0 gathers the potentials and checks them against the fp64 oracle
+ranks, then a 2-D (row x column) grid of blocks (mdot_solve_sharded_2d, NCCL
+team communicators); rank 0 gathers the potentials and checks them against the fp64 oracle
 and the single-GPU solve.  Prints "MULTI OK" on rank 0."""
 import os
 import sys
@@ -17,6 +18,66 @@ import torch.distributed as dist  # noqa: E402
 import oracle as O  # noqa: E402
 import paper_2307_08507_b200 as M  # noqa: E402
 import synthetic as S  # noqa: E402
+
+
+def _team_comm(members, rank, lr, dev):
+    """mdot communicator over `members` (global ranks): the first member's
+    NCCL unique id broadcast over a torch subgroup.  Every rank calls this for
+    every team in the same order (new_group is collective)."""
+    grp = dist.new_group(members)
+    if rank not in members:
+        return None
+    uid = M.mdot_get_unique_id() if rank == members[0] else bytes(128)
+    t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
+    dist.broadcast(t, members[0], group=grp)
+    return M.mdot_comm_create(bytes(t.cpu().numpy()), len(members), members.index(rank), lr)
+
+
+def two_d(rank, world, lr, dev, sched, eps, gb):
+    """2-D grid (mdot_solve_sharded_2d): Gr x Gc ranks, rank = a Gc + b owns
+    block rows_a x cols_b; row team = same a, column team = same b."""
+    Gr = 2 if world >= 4 else 1
+    Gc = world // Gr
+    if Gr * Gc != world:
+        return True
+    a, b = rank // Gc, rank % Gc
+    rc = cc = None
+    for aa in range(Gr):
+        x = _team_comm([aa * Gc + bb for bb in range(Gc)], rank, lr, dev)
+        rc = x if aa == a else rc
+    for bb in range(Gc):
+        x = _team_comm([aa * Gc + bb for aa in range(Gr)], rank, lr, dev)
+        cc = x if bb == b else cc
+    inst = S.uniform_points_instance(3, 3000, 2, 81, marg="dirichlet")
+    n = inst.n
+    rows = np.array_split(np.arange(n), Gr)[a]
+    cols = np.array_split(np.arange(n), Gc)[b]
+    r0, nr, c0, nc = int(rows[0]), len(rows), int(cols[0]), len(cols)
+    Cb = torch.from_numpy(np.ascontiguousarray(inst.C[r0:r0 + nr, c0:c0 + nc])).to(dev)
+    r, c = torch.from_numpy(inst.r).to(dev), torch.from_numpy(inst.c).to(dev)
+    U = torch.empty(nr, dtype=torch.float64, device=dev)
+    V = torch.empty(nc, dtype=torch.float64, device=dev)
+    res = M.mdot_solve_sharded_2d(rc, cc, r0, nr, c0, nc, Cb, r, c, n=n, schedule=sched,
+                                  options=M.options(eps=eps), u_local_out=U, v_local_out=V)
+    M.mdot_comm_destroy(rc)
+    M.mdot_comm_destroy(cc)
+    got = [None] * world
+    dist.all_gather_object(got, (a, b, res["cost_unrounded"], res["cost_rounded"], res["evaluations"],
+                                 U.cpu().numpy(), V.cpu().numpy()))
+    if rank != 0:
+        return True
+    same = len({(g[2], g[3], g[4]) for g in got}) == 1
+    Ufull = np.concatenate([g[5] for g in got if g[1] == 0])
+    Vfull = np.concatenate([g[6] for g in got if g[0] == 0])
+    prob = O.OracleProblem(inst)
+    lrr, lcc, _ = O.log_marginals(prob, Ufull, Vfull, gb)
+    l1 = np.abs(np.exp(lrr) - inst.r).sum() + np.abs(np.exp(lcc) - inst.c).sum()
+    rp = O.round_plan(prob, Ufull, Vfull, gb)
+    relG = abs(res["cost_rounded"] - rp["cost_G"]) / rp["cost_G"]
+    good = res["status"] == 0 and same and l1 <= 2 * eps and relG <= 1e-10
+    print(f"2d {Gr}x{Gc}: status {res['status_name']} identical_on_ranks {same} oracle_L1 {l1:.2e} "
+          f"rounded_cost_rel_vs_oracle_rounding {relG:.2e} evals {res['evaluations']}", flush=True)
+    return good
 
 
 def main():
@@ -75,6 +136,7 @@ def main():
                   f"cost_rel {rel:.2e} evals {res['evaluations']}", flush=True)
             ok = ok and good
     M.mdot_comm_destroy(comm)
+    ok = two_d(rank, world, lr, dev, sched, eps, gb) and ok
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:

@@ -149,3 +149,30 @@ def test_2d_rejects_unsupported_inputs():
     finally:
         M.mdot_comm_destroy(rc)
         M.mdot_comm_destroy(cc)
+
+
+def test_2d_nccl_teams_one_rank():
+    """The NCCL transport on the 2-D path: both teams are 1-rank NCCL
+    communicators, so every row / column / scalar reduction is a real
+    ncclAllReduce on the solve's stream (the multi-rank logic is covered by
+    the virtual-rank grids above, the gloo test and tests/multi/)."""
+    n = 800
+    inst = S.uniform_points_instance(3, n, 2, 34, marg="dirichlet")
+    gb, eps = 512.0, 1e-6
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=2)
+    rc = M.mdot_comm_create(M.mdot_get_unique_id(), 1, 0, 0)
+    cc = M.mdot_comm_create(M.mdot_get_unique_id(), 1, 0, 0)
+    try:
+        U = torch.empty(n, dtype=torch.float64, device=DEV)
+        V = torch.empty(n, dtype=torch.float64, device=DEV)
+        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 0, n, _t(inst.C), _t(inst.r), _t(inst.c), n=n, schedule=sched,
+                                      options=M.options(eps=eps), u_local_out=U, v_local_out=V)
+    finally:
+        M.mdot_comm_destroy(rc)
+        M.mdot_comm_destroy(cc)
+    assert res["status"] == 0 and res["l1_final"] <= eps
+    prob = O.OracleProblem(inst)
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=2), O.make_options(eps=eps))
+    assert abs(res["cost_unrounded"] - ores["cost_unrounded"]) <= COST_GATE * ores["cost_unrounded"]
+    rp = O.round_plan(prob, U.cpu().numpy(), V.cpu().numpy(), gb)
+    assert abs(res["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]

@@ -294,8 +294,11 @@ mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, 
  * rank's slices of the gauge-fixed potentials; identical across the
  * replicas).  Restrictions (-> MDOT_EINVAL): dense fp32 C only
  * (MDOT_COST_DENSE_F32), fp32-entry precision (options.precision AUTO with
- * eps >= 5e-8, or F32P); the host control loop runs (device_control is
- * ignored).  If the fp32-entry range guard fires (an evaluation far from
+ * eps >= 5e-8, or F32P).  Control: with both communicators on the NCCL
+ * transport, options.device_control = 1 runs the line search on the device
+ * (CUDA-graph slots with the four per-evaluation allreduces captured); the
+ * in-process transport, or device_control = 0, runs the host control loop.
+ * If the fp32-entry range guard fires (an evaluation far from
  * feasibility) the call returns MDOT_EINSTABLE: the exact fp64 evaluator is
  * not distributed in 2-D. */
 mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, const mdot_problem* block,

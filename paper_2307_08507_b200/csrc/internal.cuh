@@ -382,6 +382,9 @@ cudaError_t launch_persist_peer(const PeerLaunch& L, cudaStream_t st);
 cudaError_t launch_setup(int64_t n, const double* r, double* logr, double* rho, cudaStream_t st);
 cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t st); // y = a x + b y
 cudaError_t launch_add_scalar(int64_t n, double d, double* y, cudaStream_t st);
+// 2-D sharded graph slots: out[q] = a[q] + b[q] for the kNumScalars control
+// scalars (row side + column side), skipped once the controller is done
+cudaError_t launch_sum_scalars(const double* a, const double* b, double* out, const int* done, cudaStream_t st);
 cudaError_t launch_fill(int64_t n, double v, double* y, cudaStream_t st);
 // deterministic dot products: out[k] = sum_i x_k[i] * y_k[i] for up to 4 pairs
 cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,

@@ -1059,6 +1059,15 @@ __global__ void k_add_scalar(int64_t n, double d, double* y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] += d;
 }
+__global__ void k_sum_scalars(const double* a, const double* b, double* out, const int* done) {
+  if (done && *done) return;
+  const int q = threadIdx.x;
+  if (q < kNumScalars) out[q] = a[q] + b[q];
+}
+cudaError_t launch_sum_scalars(const double* a, const double* b, double* out, const int* done, cudaStream_t st) {
+  k_sum_scalars<<<1, 32, 0, st>>>(a, b, out, done);
+  return cudaGetLastError();
+}
 cudaError_t launch_add_scalar(int64_t n, double d, double* y, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_add_scalar<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, y);

@@ -663,6 +663,33 @@ mdot_status Workspace::launch_slot_body(cudaStream_t s, int slot, bool timed, bo
     f.from_partials = 1;
     f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
     f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
+    if (two_d()) {
+      // the host path's 2-D evaluation (Workspace::evaluate), captured with
+      // both teams' NCCL allreduces; the summed scalars land in ctrl->sc
+      if (timed) CK(cudaEventRecordWithFlags(gev[3], s, cudaEventRecordExternal));
+      double* colbuf = tot.coltot;
+      double* rowbuf = tot.coltot + n + kNumScalars;
+      CKL(launch_reduce_colpart(colpart, eval.n_row_tiles, n, colbuf, s, &ctrl->done));
+      CKL(launch_reduce_colpart(rowpart, eval.n_col_tiles, nrows, rowbuf, s, &ctrl->done));
+      CKS(comm_allreduce(comm, colbuf, (size_t)n, COMM_SUM, s));
+      CKS(comm_allreduce(comm_row, rowbuf, (size_t)nrows, COMM_SUM, s));
+      FinalizeArgs fr = f;
+      fr.rowtot = rowbuf;
+      fr.item_begin = 0; fr.item_end = nrows;
+      fr.scalars_dev = rowbuf + nrows;
+      CKL(launch_finalize(fr, s));
+      FinalizeArgs fc = f;
+      fc.coltot = colbuf;
+      fc.item_begin = nrows; fc.item_end = nrows + n;
+      fc.scalars_dev = colbuf + n;
+      fc.prep_flag = nullptr;
+      CKL(launch_finalize(fc, s));
+      CKS(comm_allreduce(comm, rowbuf + nrows, kNumScalars, COMM_SUM, s));
+      CKS(comm_allreduce(comm_row, colbuf + n, kNumScalars, COMM_SUM, s));
+      CKL(launch_sum_scalars(rowbuf + nrows, colbuf + n, ctrl->sc, &ctrl->done, s));
+      if (timed) CK(cudaEventRecordWithFlags(gev[4], s, cudaEventRecordExternal));
+      return MDOT_OK;
+    }
     if (sharded()) {
       // the host path's sharded evaluation (Workspace::evaluate), captured:
       // rows finalize locally with their scalars in the tail of the column
@@ -849,7 +876,7 @@ mdot_status project_device(Workspace& w, const mdot_options& o, int t, mdot_resu
     if (*((volatile int*)w.done_host)) break;   // the probe slot may have ended the projection
     for (int k = 0; k < w.gslots; ++k) ((volatile int*)w.ran_host)[k] = 0;
     CK(cudaGraphLaunch(w.gexec, st));
-    w.launches += (w.sharded() ? 6 : 4) * w.gslots;   // our kernels per slot (NCCL's not counted)
+    w.launches += (w.two_d() ? 8 : w.sharded() ? 6 : 4) * w.gslots;   // our kernels per slot (NCCL's not counted)
     const bool was_scr = w.screen_now;
     unsigned long long hc[2] = {0ull, 0ull};
     if (was_scr) CKS(w.screen_counts(hc));
@@ -1581,7 +1608,9 @@ static mdot_status solve_impl(const mdot_problem* pb, const mdot_schedule* sched
   if (comm_row && (col0 < 0 || nc < 1 || col0 + nc > n)) {
     set_error("bad column range"); res->status = MDOT_EINVAL; return MDOT_EINVAL;
   }
-  if (comm_row) o.device_control = 0;   // 2-D: host control loop (mdot.h)
+  // 2-D: device control (graph slots with both teams' NCCL allreduces
+  // captured) when both transports are capturable, else the host loop
+  if (comm_row && !(comm && comm->capturable() && comm_row->capturable())) o.device_control = 0;
   // sharded: device control (CUDA-graph slots with the NCCL allreduce captured
   // inside) needs a capturable transport; the in-process transport syncs on
   // the host in every allreduce, so it runs the host loop

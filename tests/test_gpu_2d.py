@@ -85,7 +85,7 @@ def test_2d_grid_matches_single_gpu_and_oracle(Gr, Gc, projector):
     out, rows, cols = _solve_2d(inst, Gr, Gc, sched, kw, f"g2d_{Gr}{Gc}{projector}")
     r00 = out[(0, 0)][0]
     assert all(o[0]["status"] == 0 for o in out.values()), [(k, o[0]["status_name"], o[3]) for k, o in out.items()]
-    assert all(o[0]["control_path"] == 0 for o in out.values())      # host control loop (mdot.h)
+    assert all(o[0]["control_path"] == 0 for o in out.values())      # in-process teams: host control loop
     # identical decisions and scalars on every rank of the grid
     assert all(o[0]["evaluations"] == r00["evaluations"] for o in out.values())
     assert all(o[0]["cost_unrounded"] == r00["cost_unrounded"] for o in out.values())
@@ -151,11 +151,15 @@ def test_2d_rejects_unsupported_inputs():
         M.mdot_comm_destroy(cc)
 
 
-def test_2d_nccl_teams_one_rank():
+@pytest.mark.parametrize("dc", [1, 0])
+def test_2d_nccl_teams_one_rank(dc, monkeypatch):
     """The NCCL transport on the 2-D path: both teams are 1-rank NCCL
     communicators, so every row / column / scalar reduction is a real
-    ncclAllReduce on the solve's stream (the multi-rank logic is covered by
-    the virtual-rank grids above, the gloo test and tests/multi/)."""
+    ncclAllReduce on the solve's stream -- captured inside the CUDA-graph
+    slots under device control (dc = 1, control_path 1), or issued by the host
+    loop (dc = 0).  The multi-rank logic is covered by the virtual-rank grids
+    above, the gloo test and tests/multi/."""
+    monkeypatch.setenv("MDOT_SHARDED_SELFTEST", "1")   # a 1-rank comm keeps its NCCL communicator
     n = 800
     inst = S.uniform_points_instance(3, n, 2, 34, marg="dirichlet")
     gb, eps = 512.0, 1e-6
@@ -166,13 +170,16 @@ def test_2d_nccl_teams_one_rank():
         U = torch.empty(n, dtype=torch.float64, device=DEV)
         V = torch.empty(n, dtype=torch.float64, device=DEV)
         res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 0, n, _t(inst.C), _t(inst.r), _t(inst.c), n=n, schedule=sched,
-                                      options=M.options(eps=eps), u_local_out=U, v_local_out=V)
+                                      options=M.options(eps=eps, device_control=dc), u_local_out=U, v_local_out=V)
     finally:
         M.mdot_comm_destroy(rc)
         M.mdot_comm_destroy(cc)
     assert res["status"] == 0 and res["l1_final"] <= eps
+    assert res["control_path"] == dc
     prob = O.OracleProblem(inst)
     Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=2), O.make_options(eps=eps))
     assert abs(res["cost_unrounded"] - ores["cost_unrounded"]) <= COST_GATE * ores["cost_unrounded"]
     rp = O.round_plan(prob, U.cpu().numpy(), V.cpu().numpy(), gb)
     assert abs(res["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]
+    lr, lc, _ = O.log_marginals(prob, U.cpu().numpy(), V.cpu().numpy(), gb)
+    assert np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum() <= 2 * eps

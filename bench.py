@@ -84,7 +84,79 @@ def parse():
     ap.add_argument("--adaptive-leg", type=float, default=1e-3,
                     help="also time the solve with this eps_md (SURVEY 8(f) rank 1), reported under "
                          "'adaptive_eps'; 0 disables")
+    ap.add_argument("--two-d", type=int, default=1,
+                    help="at N >= 4 (even) also time one config-4 solve on a 2 x N/2 grid of blocks "
+                         "(mdot_solve_sharded_2d, NCCL team communicators, device control); 0 disables")
     return ap.parse_args()
+
+
+def run_two_d(a, rank, world, local_rank, dev, M, dist, barrier, headline):
+    """2-D (row x column) sharded config-4 solve (mdot_solve_sharded_2d,
+    SURVEY 8(f) rank 4): Gr = 2 row blocks x Gc = N / 2 column blocks, row and
+    column teams as NCCL communicators (uniqueId broadcast over torch
+    subgroups), the line search under device control.  One warm-up + one timed
+    solve, device time as the max over ranks."""
+    import numpy as np
+    import torch
+    Gr = 2 if world >= 4 else 1        # 1 x 1 under --sharded-selftest (1-rank NCCL teams)
+    Gc = world // Gr
+    ai, bi = rank // Gc, rank % Gc
+
+    def team(members):
+        grp = dist.new_group(members)
+        if rank not in members:
+            return None
+        uid = M.mdot_get_unique_id() if rank == members[0] else bytes(128)
+        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
+        dist.broadcast(t, members[0], group=grp)
+        return M.mdot_comm_create(bytes(t.cpu().numpy()), len(members), members.index(rank), local_rank)
+
+    rc = cc = None
+    for x in range(Gr):
+        cm = team([x * Gc + y for y in range(Gc)])
+        rc = cm if x == ai else rc
+    for y in range(Gc):
+        cm = team([x * Gc + y for x in range(Gr)])
+        cc = cm if y == bi else cc
+    inst = instance(a)
+    n = inst.n
+    rows = np.array_split(np.arange(n), Gr)[ai]
+    cols = np.array_split(np.arange(n), Gc)[bi]
+    r0, nr, c0, nc = int(rows[0]), len(rows), int(cols[0]), len(cols)
+    Cb = torch.from_numpy(np.ascontiguousarray(inst.C[r0:r0 + nr, c0:c0 + nc])).to(dev)
+    del inst.C
+    r = torch.from_numpy(inst.r).to(dev)
+    c = torch.from_numpy(inst.c).to(dev)
+    U = torch.empty(nr, dtype=torch.float64, device=dev)
+    V = torch.empty(nc, dtype=torch.float64, device=dev)
+    sched = M.schedule(M.MDOT_SCHED_FIXED, a.gamma_bar, T=a.T)
+    opts = M.options(eps=a.eps, eps_md=a.eps_md)
+
+    def solve():
+        return M.mdot_solve_sharded_2d(rc, cc, r0, nr, c0, nc, Cb, r, c, n=n, schedule=sched, options=opts,
+                                       u_local_out=U, v_local_out=V)
+    solve()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = solve()
+    e1.record()
+    barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    M.mdot_comm_destroy(rc)
+    M.mdot_comm_destroy(cc)
+    return {
+        "grid": f"{Gr}x{Gc}", "api": "mdot_solve_sharded_2d", "control_path": res["control_path"],
+        "time_to_eps_s": ms / 1000.0, "evals_per_s": res["evaluations"] / (ms / 1000.0),
+        "evaluations_per_solve": res["evaluations"], "status_name": res["status_name"],
+        "cost_unrounded": res["cost_unrounded"], "l1_final": res["l1_final"],
+        "cost_rel_diff_vs_1d": abs(res["cost_unrounded"] - headline) / abs(headline),
+        "exchange_bytes_per_eval_per_rank": 8 * (nr + nc) + 4 * 16 * 8,
+        "exchange_bytes_per_eval_per_rank_1d": 8 * (n + 16),
+        "note": "row sums over the row team, column sums over the column team (NCCL, captured in the graph "
+                "slots); DESIGN.md section 8 '2-D sharding'"}
 
 
 def workload_name(a):
@@ -450,6 +522,8 @@ def run_ours(a, rank, world, local_rank):
                     "the final plan independent of the intermediate accuracy"}
     if not a.no_config5:
         line["config5"] = run_config5(a, rank, world, dev, M, dist, comm, barrier)
+    if a.two_d and ((world >= 4 and world % 2 == 0) or a.sharded_selftest):
+        line["two_d"] = run_two_d(a, rank, world, local_rank, dev, M, dist, barrier, results[-1]["cost_unrounded"])
     # end-to-end through the C ABI with host buffers (rank 0, 1 GPU)
     if not sharded and not a.no_e2e:
         import synthetic as S

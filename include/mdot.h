@@ -278,10 +278,13 @@ mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, 
 /* 2-D (row x column) sharding (past the replicated
  * column vectors of mdot_solve_sharded).  The ranks form a Gr x Gc grid; this
  * rank owns the block rows [row0, row0 + n_rows) x columns
- * [col0, col0 + n_cols) of the n x n cost (block->C points at that block,
- * row-major, n_rows x n_cols, leading dimension n_cols; block->n is the
- * GLOBAL n; block->r, block->c are the FULL marginals, validated as in
- * mdot_solve).  An evaluation is K1 over the block, then
+ * [col0, col0 + n_cols) of the n x n cost: block->C points at that block
+ * (dense fp32, row-major, n_rows x n_cols, leading dimension n_cols), or, for
+ * (dense fp64 for MDOT_COST_DENSE_F64), or, for
+ * the on-the-fly costs (MDOT_COST_SQEUCLID_F32 / _DOT_F32), block->X at the
+ * n_rows x d rows of X and block->Y at the n_cols x d rows of Y of the block;
+ * block->n is the GLOBAL n; block->r, block->c are the FULL marginals,
+ * validated as in mdot_solve.  An evaluation is K1 over the block, then
  * two allreduces: the block's row sums over `row_comm` (the Gc ranks of this
  * row block) and its column sums over `col_comm` (the Gr ranks of this column
  * block); rows and columns then finalize locally and the 16 control scalars
@@ -292,15 +295,16 @@ mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, 
  * sums over col_comm the same way.  Either communicator may have one rank
  * (Gr = 1 or Gc = 1).  u_local_out: [n_rows], v_local_out: [n_cols] (the
  * rank's slices of the gauge-fixed potentials; identical across the
- * replicas).  Restrictions (-> MDOT_EINVAL): dense fp32 C only
- * (MDOT_COST_DENSE_F32), fp32-entry precision (options.precision AUTO with
- * eps >= 5e-8, or F32P).  Control: with both communicators on the NCCL
+ * replicas).  Precision as mdot_solve: fp32 entries, with the exact fp64
+ * evaluator distributed the same way ((max, sum) pairs: a max-allreduce, a
+ * rescale and a sum-allreduce per side) for the range-guard fallback and for
+ * fp64-entry solves (eps < 5e-8 with AUTO, F64P, fp64 C; host control).
+ * Control: with both communicators on the NCCL
  * transport, options.device_control = 1 runs the line search on the device
  * (CUDA-graph slots with the four per-evaluation allreduces captured); the
  * in-process transport, or device_control = 0, runs the host control loop.
- * If the fp32-entry range guard fires (an evaluation far from
- * feasibility) the call returns MDOT_EINSTABLE: the exact fp64 evaluator is
- * not distributed in 2-D. */
+ * The screened on-the-fly evaluation (K2s), the persistent fused-exchange
+ * kernel and the dense plan output are not part of the 2-D path. */
 mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, const mdot_problem* block,
                                   int64_t row0, int64_t n_rows, int64_t col0, int64_t n_cols,
                                   const mdot_schedule* sched, const mdot_options* opt, double* u_local_out,

@@ -380,15 +380,20 @@ def mdot_comm_destroy(comm):
     _check(lib().mdot_comm_destroy(comm), "mdot_comm_destroy")
 
 
-def mdot_solve_sharded_2d(row_comm, col_comm, row0, n_rows, col0, n_cols, C_block, r, c, *, n,
+def mdot_solve_sharded_2d(row_comm, col_comm, row0, n_rows, col0, n_cols, C_block=None, r=None, c=None, *, n,
+                          X_block=None, Y_block=None, scale=0.0, recipe="diff",
                           schedule=None, options=None, u_local_out=None, v_local_out=None, check=True):
     """2-D (row x column) sharded solve (include/mdot.h mdot_solve_sharded_2d):
-    C_block = C[row0:row0+n_rows, col0:col0+n_cols] (contiguous fp32), r, c the
-    full marginals, n the global size; row_comm joins the ranks of this row
-    block, col_comm those of this column block."""
-    if tuple(C_block.shape) != (int(n_rows), int(n_cols)):
-        raise ValueError(f"C_block shape {tuple(C_block.shape)} != ({n_rows}, {n_cols})")
-    pb = problem(C_block, r, c, n=n)
+    C_block = C[row0:row0+n_rows, col0:col0+n_cols] (contiguous fp32), or the
+    on-the-fly cost's X_block = X[row0:row0+n_rows], Y_block = Y[col0:col0+n_cols];
+    r, c the full marginals, n the global size; row_comm joins the ranks of
+    this row block, col_comm those of this column block."""
+    if C_block is not None:
+        if tuple(C_block.shape) != (int(n_rows), int(n_cols)):
+            raise ValueError(f"C_block shape {tuple(C_block.shape)} != ({n_rows}, {n_cols})")
+    elif X_block is None or Y_block is None or X_block.shape[0] != int(n_rows) or Y_block.shape[0] != int(n_cols):
+        raise ValueError("on-the-fly cost: X_block [n_rows x d] and Y_block [n_cols x d] required")
+    pb = problem(C_block, r, c, X=X_block, Y=Y_block, scale=scale, n=n, recipe=recipe)
     sched = schedule if schedule is not None else globals()["schedule"]()
     opts = options if options is not None else globals()["options"]()
     if pb.mem == MDOT_MEM_DEVICE:

@@ -385,6 +385,9 @@ cudaError_t launch_add_scalar(int64_t n, double d, double* y, cudaStream_t st);
 // 2-D sharded graph slots: out[q] = a[q] + b[q] for the kNumScalars control
 // scalars (row side + column side), skipped once the controller is done
 cudaError_t launch_sum_scalars(const double* a, const double* b, double* out, const int* done, cudaStream_t st);
+// 2-D exact fallback: out[i] = M[i] + log(S[i]) (a log-sum-exp from its
+// allreduced (max, scaled sum) form)
+cudaError_t launch_lse_finish(int64_t n, const double* M, const double* S, double* out, cudaStream_t st);
 cudaError_t launch_fill(int64_t n, double v, double* y, cudaStream_t st);
 // deterministic dot products: out[k] = sum_i x_k[i] * y_k[i] for up to 4 pairs
 cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,

@@ -1068,6 +1068,14 @@ cudaError_t launch_sum_scalars(const double* a, const double* b, double* out, co
   k_sum_scalars<<<1, 32, 0, st>>>(a, b, out, done);
   return cudaGetLastError();
 }
+__global__ void k_lse_finish(int64_t n, const double* M, const double* S, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = M[i] + log(S[i]);
+}
+cudaError_t launch_lse_finish(int64_t n, const double* M, const double* S, double* out, cudaStream_t st) {
+  k_lse_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, M, S, out);
+  return cudaGetLastError();
+}
 cudaError_t launch_add_scalar(int64_t n, double d, double* y, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_add_scalar<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, y);

@@ -387,11 +387,6 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
     if (sc[SC_BAD] == 0.0) return MDOT_OK;
     fallbacks++;
   }
-  if (two_d()) {
-    set_error("2-D sharded solve: the fp32-entry range guard fired at gbar=%g (the exact fp64 evaluator is not "
-              "distributed in 2-D; mdot.h)", gbar);
-    return MDOT_EINSTABLE;
-  }
   ExactArgs x{};
   x.C = Cdev; x.ldc = n; x.c_f64 = c_f64;
   x.X = Xdev; x.Y = Ydev; x.d = d; x.scale = scale; x.otf = otf;
@@ -402,6 +397,52 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   f.from_partials = 0;
   f.lr_in = lr_ex; f.colm = colm; f.cols = cols; f.chunks = chunks;
   f.prep_flag = nullptr;
+  if (two_d()) {
+    // 2-D exact: column (max, sum) pairs combined over the column team (as
+    // the 1-D path), row log-sums of this block's columns combined over the
+    // row team the same way: M = max-allreduce, S = sum-allreduce of
+    // e^(l - M), l = M + log S; then both sides finalize and their scalars
+    // are summed over the other team (as the fp32-entry branch above)
+    double* Mloc = aux;
+    double* Mg = aux + n;
+    double* Sg = aux + 2 * n;
+    double* Mr = aux + 3 * n;
+    double* Sr = Mr + nrows;
+    CKL(launch_exact_colcombine(colm, cols, chunks, n, Mloc, Sg, st));
+    CK(cudaMemcpyAsync(Mg, Mloc, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CKS(comm_allreduce(comm, Mg, (size_t)n, COMM_MAX, st));
+    CKL(launch_rescale_to_max(n, Mloc, Mg, Sg, st));
+    CKS(comm_allreduce(comm, Sg, (size_t)n, COMM_SUM, st));
+    CK(cudaMemcpyAsync(Mr, lr_ex, sizeof(double) * nrows, cudaMemcpyDeviceToDevice, st));
+    CKS(comm_allreduce(comm_row, Mr, (size_t)nrows, COMM_MAX, st));
+    CKL(launch_fill(nrows, 1.0, Sr, st));
+    CKL(launch_rescale_to_max(nrows, lr_ex, Mr, Sr, st));
+    CKS(comm_allreduce(comm_row, Sr, (size_t)nrows, COMM_SUM, st));
+    CKL(launch_lse_finish(nrows, Mr, Sr, lr_ex, st));
+    double* colsc = tot.coltot + n;
+    double* rowsc = tot.coltot + n + kNumScalars + nrows;
+    FinalizeArgs fr = f;
+    fr.item_begin = 0; fr.item_end = nrows;
+    fr.scalars_dev = rowsc; fr.scalars_host = nullptr;
+    CKL(launch_finalize(fr, st));
+    FinalizeArgs fc = f;
+    fc.colm = Mg; fc.cols = Sg; fc.chunks = 1;
+    fc.item_begin = nrows; fc.item_end = nrows + n;
+    fc.scalars_dev = colsc; fc.scalars_host = nullptr;
+    CKL(launch_finalize(fc, st));
+    CKS(comm_allreduce(comm, rowsc, kNumScalars, COMM_SUM, st));
+    CKS(comm_allreduce(comm_row, colsc, kNumScalars, COMM_SUM, st));
+    double h[2][kNumScalars];
+    CK(cudaMemcpyAsync(h[0], rowsc, sizeof(h[0]), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h[1], colsc, sizeof(h[1]), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int q = 0; q < kNumScalars; ++q) sc[q] = h[0][q] + h[1][q];
+    if (sc[SC_BAD] != 0.0) {
+      set_error("non-finite marginals at gbar=%g on the exact fp64 evaluator (2-D)", gbar);
+      return MDOT_EINSTABLE;
+    }
+    return MDOT_OK;
+  }
   if (!shard) {
     CKL(launch_finalize(f, st));
   } else {
@@ -1368,10 +1409,6 @@ mdot_status Workspace::setup(const mdot_options& o) {
   // that resolution (the same rule as the batched solver, mdot_solve_batch)
   exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && (c_f64 || o.eps < 5e-8));
   jacobi = o.projector == MDOT_PROJ_PNCG_JACOBI;
-  if (two_d() && exact_mode) {
-    set_error("2-D sharded solve: fp32-entry precision only (eps >= 5e-8 with AUTO, or F32P); mdot.h");
-    return MDOT_EINVAL;
-  }
   if (!exact_mode && c_f64) {
     set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
     return MDOT_EINVAL;
@@ -1823,11 +1860,6 @@ mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, cons
   Comm* cr = reinterpret_cast<Comm*>(row_comm);
   Comm* cc = reinterpret_cast<Comm*>(col_comm);
   if (!cr || !cc || !block) { set_error("bad arguments"); return MDOT_EINVAL; }
-  if (block->kind != MDOT_COST_DENSE_F32) {
-    set_error("2-D sharded solve: dense fp32 C only (mdot.h)");
-    if (res) { memset(res, 0, sizeof(*res)); res->status = MDOT_EINVAL; }
-    return MDOT_EINVAL;
-  }
   if (cr->device != cc->device) { set_error("row and column communicators on different devices"); return MDOT_EINVAL; }
   if (cudaSetDevice(cc->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }
   return solve_impl(block, sched, opt, u_local_out, v_local_out, nullptr, res, 0, cc, row0, n_rows, 0, cr, col0,

@@ -37,7 +37,7 @@ def _t(x):
     return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
 
 
-def _solve_2d(inst, Gr, Gc, sched, opts_kw, tag):
+def _solve_2d(inst, Gr, Gc, sched, opts_kw, tag, otf_recipe=None):
     n = inst.n
     rows = np.array_split(np.arange(n), Gr)
     cols = np.array_split(np.arange(n), Gc)
@@ -50,14 +50,18 @@ def _solve_2d(inst, Gr, Gc, sched, opts_kw, tag):
             with torch.cuda.stream(s):
                 r0, nr = int(rows[a][0]), len(rows[a])
                 c0, nc = int(cols[b][0]), len(cols[b])
-                Cb = _t(inst.C[r0:r0 + nr, c0:c0 + nc])
+                if otf_recipe is None:
+                    cost = dict(C_block=_t(inst.C[r0:r0 + nr, c0:c0 + nc]))
+                else:
+                    cost = dict(X_block=_t(inst.X[r0:r0 + nr]), Y_block=_t(inst.Y[c0:c0 + nc]),
+                                scale=float(inst.scale), recipe=otf_recipe)
                 U = torch.empty(nr, dtype=torch.float64, device=DEV)
                 V = torch.empty(nc, dtype=torch.float64, device=DEV)
                 rc = M.mdot_comm_create_local(f"{tag}_row{a}", Gc, b, 0)
                 cc = M.mdot_comm_create_local(f"{tag}_col{b}", Gr, a, 0)
-                res = M.mdot_solve_sharded_2d(rc, cc, r0, nr, c0, nc, Cb, _t(inst.r), _t(inst.c), n=n,
+                res = M.mdot_solve_sharded_2d(rc, cc, r0, nr, c0, nc, r=_t(inst.r), c=_t(inst.c), n=n,
                                               schedule=sched, options=M.options(**opts_kw),
-                                              u_local_out=U, v_local_out=V, check=False)
+                                              u_local_out=U, v_local_out=V, check=False, **cost)
                 s.synchronize()
                 M.mdot_comm_destroy(rc)
                 M.mdot_comm_destroy(cc)
@@ -109,6 +113,36 @@ def test_2d_grid_matches_single_gpu_and_oracle(Gr, Gc, projector):
     assert abs(r00["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"], (r00["cost_rounded"], rp["cost_G"])
 
 
+@pytest.mark.parametrize("recipe", ["diff", "dot"])
+def test_2d_grid_on_the_fly_cost(recipe):
+    """Config-5-shaped on-the-fly cost (d = 16, C = ||x - y||^2 / 16 by the
+    Z22 / Z22b fp32 recipe) on a 2 x 2 grid: block (i, j) evaluates X rows_i
+    against Y rows_j in-kernel (K2).  Same gates as the dense grid, the oracle
+    built on the same fp32 recipe."""
+    n = 1000
+    inst = S.config5(1, n=n, d=16)
+    gb, eps = 1024.0, 1e-5                     # config 5 target
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=4)
+    out, _, _ = _solve_2d(inst, 2, 2, sched, {"eps": eps}, f"g2d_otf_{recipe}", otf_recipe=recipe)
+    r00 = out[(0, 0)][0]
+    assert all(o[0]["status"] == 0 for o in out.values()), [(k, o[0]["status_name"], o[3]) for k, o in out.items()]
+    assert all(o[0]["evaluations"] == r00["evaluations"] for o in out.values())
+    assert all(o[0]["cost_rounded"] == r00["cost_rounded"] for o in out.values())
+    assert r00["l1_final"] <= eps
+    ref = M.mdot_solve(X=_t(inst.X), Y=_t(inst.Y), scale=inst.scale, r=_t(inst.r), c=_t(inst.c), schedule=sched,
+                       options=M.options(eps=eps), recipe=recipe)
+    assert abs(r00["cost_unrounded"] - ref["cost_unrounded"]) <= COST_GATE * ref["cost_unrounded"]
+    U = np.concatenate([out[(a, 0)][1] for a in range(2)])
+    V = np.concatenate([out[(0, b)][2] for b in range(2)])
+    prob = O.OracleProblem(inst, recipe=recipe)
+    lr, lc, _ = O.log_marginals(prob, U, V, gb)
+    l1 = np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum()
+    assert l1 <= 2 * eps, l1
+    rp = O.round_plan(prob, U, V, gb)
+    assert abs(r00["cost_unrounded"] - rp["cost_F"]) <= 1e-9 * rp["cost_F"], (r00["cost_unrounded"], rp["cost_F"])
+    assert abs(r00["cost_rounded"] - rp["cost_G"]) <= 1e-9 * rp["cost_G"], (r00["cost_rounded"], rp["cost_G"])
+
+
 def test_2d_one_by_one_grid_equals_host_loop_solve():
     """A 1 x 1 grid is the unsharded problem on the 2-D code path: same
     decisions as the single-GPU host-loop solve (device_control = 0) up to the
@@ -128,21 +162,48 @@ def test_2d_one_by_one_grid_equals_host_loop_solve():
     assert abs(res["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]
 
 
-def test_2d_rejects_unsupported_inputs():
-    """fp64-entry precision and on-the-fly / fp64 costs are outside the 2-D
-    path (mdot.h): MDOT_EINVAL before any device work."""
+@pytest.mark.parametrize("f64_cost", [False, True])
+def test_2d_grid_fp64_entries(f64_cost):
+    """fp64-entry solves on the 2-D path (eps 1e-9 < 5e-8 with AUTO; fp64 C
+    implies fp64 entries): every evaluation is the exact evaluator, its row
+    log-sums combined over the row team and its column (max, sum) pairs over
+    the column team.  Gates as the dense grid; at eps 1e-9 the unrounded cost
+    agrees with the ORACLE's own solve to 1e-5 (Z20 (ii))."""
+    n = 300
+    inst = S.uniform_points_instance(3, n, 2, 35, marg="dirichlet")
+    if f64_cost:
+        inst.C = inst.C.astype(np.float64)
+    gb, eps = 256.0, 1e-9
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=1)
+    out, _, _ = _solve_2d(inst, 2, 2, sched, {"eps": eps}, f"g2d_f64_{int(f64_cost)}")
+    r00 = out[(0, 0)][0]
+    assert all(o[0]["status"] == 0 for o in out.values()), [(k, o[0]["status_name"], o[3]) for k, o in out.items()]
+    assert all(o[0]["evaluations"] == r00["evaluations"] for o in out.values())
+    assert all(o[0]["cost_rounded"] == r00["cost_rounded"] for o in out.values())
+    assert r00["l1_final"] <= eps
+    U = np.concatenate([out[(a, 0)][1] for a in range(2)])
+    V = np.concatenate([out[(0, b)][2] for b in range(2)])
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, U, V, gb)
+    assert np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum() <= 2 * eps
+    Uo, Vo, ores, _ = O.mdot(prob, O.schedule_fixed(gb, T=1), O.make_options(eps=eps))
+    assert abs(r00["cost_unrounded"] - ores["cost_unrounded"]) <= COST_GATE * ores["cost_unrounded"]
+    rp = O.round_plan(prob, U, V, gb)
+    assert abs(r00["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]
+
+
+def test_2d_rejects_bad_blocks():
+    """A block outside the problem, or marginals that do not match the global
+    n: MDOT_EINVAL before any device work."""
     n = 64
     inst = S.uniform_points_instance(3, n, 2, 33, marg="dirichlet")
     rc = M.mdot_comm_create_local("g2d_rej_row", 1, 0, 0)
     cc = M.mdot_comm_create_local("g2d_rej_col", 1, 0, 0)
     try:
         sched = M.schedule(M.MDOT_SCHED_FIXED, 64.0, T=1)
-        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 0, n, _t(inst.C), _t(inst.r), _t(inst.c), n=n, schedule=sched,
-                                      options=M.options(eps=1e-9), check=False)
-        assert res["status"] == 1 and "fp32-entry" in M.mdot_last_error()
-        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 0, n, _t(inst.C.astype(np.float64)), _t(inst.r), _t(inst.c),
-                                      n=n, schedule=sched, options=M.options(eps=1e-6), check=False)
-        assert res["status"] == 1 and "dense fp32" in M.mdot_last_error()
+        res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 8, n - 4, _t(inst.C[:, 4:]), _t(inst.r), _t(inst.c), n=n,
+                                      schedule=sched, options=M.options(eps=1e-6), check=False)
+        assert res["status"] == 1 and "column range" in M.mdot_last_error()
         res = M.mdot_solve_sharded_2d(rc, cc, 0, n, 8, n - 8, _t(inst.C[:, 8:]), _t(inst.r), _t(inst.c), n=n - 4,
                                       schedule=sched, options=M.options(eps=1e-6), check=False)
         assert res["status"] == 1

@@ -1859,9 +1859,14 @@ mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, cons
                                   double* v_local_out, mdot_result* res) {
   Comm* cr = reinterpret_cast<Comm*>(row_comm);
   Comm* cc = reinterpret_cast<Comm*>(col_comm);
-  if (!cr || !cc || !block) { set_error("bad arguments"); return MDOT_EINVAL; }
-  if (cr->device != cc->device) { set_error("row and column communicators on different devices"); return MDOT_EINVAL; }
-  if (cudaSetDevice(cc->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return MDOT_ECUDA; }
+  auto fail = [&](mdot_status e, const char* msg) {
+    set_error("%s", msg);
+    if (res) { memset(res, 0, sizeof(*res)); res->status = e; }
+    return e;
+  };
+  if (!cr || !cc || !block) return fail(MDOT_EINVAL, "bad arguments");
+  if (cr->device != cc->device) return fail(MDOT_EINVAL, "row and column communicators on different devices");
+  if (cudaSetDevice(cc->device) != cudaSuccess) return fail(MDOT_ECUDA, "cudaSetDevice failed");
   return solve_impl(block, sched, opt, u_local_out, v_local_out, nullptr, res, 0, cc, row0, n_rows, 0, cr, col0,
                     n_cols);
 }

@@ -304,7 +304,11 @@ mdot_status mdot_solve_sharded(mdot_comm* comm, const mdot_problem* local_rows, 
  * (CUDA-graph slots with the four per-evaluation allreduces captured); the
  * in-process transport, or device_control = 0, runs the host control loop.
  * The screened on-the-fly evaluation (K2s), the persistent fused-exchange
- * kernel and the dense plan output are not part of the 2-D path. */
+ * kernel and the dense plan output are not part of the 2-D path.
+ * Environment MDOT_NC2=1 (this call and mdot_solve_sharded, host control
+ * loop, fp32 entries): scalar-only line-search trials --
+ * a trial reduces 4 scalars, an accepted trial is completed with the vector
+ * exchange (measured slower at the BASELINE sizes). */
 mdot_status mdot_solve_sharded_2d(mdot_comm* row_comm, mdot_comm* col_comm, const mdot_problem* block,
                                   int64_t row0, int64_t n_rows, int64_t col0, int64_t n_cols,
                                   const mdot_schedule* sched, const mdot_options* opt, double* u_local_out,

@@ -388,6 +388,10 @@ cudaError_t launch_sum_scalars(const double* a, const double* b, double* out, co
 // 2-D exact fallback: out[i] = M[i] + log(S[i]) (a log-sum-exp from its
 // allreduced (max, scaled sum) form)
 cudaError_t launch_lse_finish(int64_t n, const double* M, const double* S, double* out, cudaStream_t st);
+// NC2 scalar-only line-search trial (kernels.cu k_nc2_trial): 4 doubles
+cudaError_t launch_nc2_trial(const double* rowpart, int nct, const double* colpart, int nrt, int64_t nrows, int64_t n,
+                             const double* rho_r, const double* sig_c, const double* p, const int* flag,
+                             double* blockpart, unsigned int* ticket, double* out_dev, cudaStream_t st);
 cudaError_t launch_fill(int64_t n, double v, double* y, cudaStream_t st);
 // deterministic dot products: out[k] = sum_i x_k[i] * y_k[i] for up to 4 pairs
 cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,

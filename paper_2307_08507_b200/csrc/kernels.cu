@@ -1104,6 +1104,43 @@ __global__ void k_dots(int64_t n, int npairs, DotPtrs P, double* blockpart, unsi
   }
   block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, out_host);
 }
+// NC2: the line-search scalars of a trial from this rank's
+// partials alone, no vector exchange -- phi'(alpha) and the mass are linear in
+// the marginals, so each rank sums its own partials' contributions
+// (PAPER.md:694-696): out[0] = sum_i p_i R_i 2^rho_i, out[1] = sum_i R_i 2^rho_i,
+// out[2] = sum_j p_j C_j 2^sig_j (R, C: this rank's anchored row / column
+// partial totals), out[3] = non-finite count + the prep range flag.
+__global__ void __launch_bounds__(256) k_nc2_trial(const double* rowpart, int nct, const double* colpart, int nrt,
+                                                   int64_t nrows, int64_t n, const double* rho_r,
+                                                   const double* sig_c, const double* p, const int* flag,
+                                                   double* blockpart, unsigned int* ticket, double* out_dev) {
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nrows + n; k += (int64_t)gridDim.x * blockDim.x) {
+    if (k < nrows) {
+      const double R = sum_strided(rowpart + k, nrows, nct) * exp2(rho_r[k]);
+      v[0] += p[k] * R;
+      v[1] += R;
+      if (!isfinite(R)) v[3] += 1.0;
+    } else {
+      const int64_t j = k - nrows;
+      const double Cj = sum_strided(colpart + j, n, nrt) * exp2(sig_c[j]);
+      v[2] += p[k] * Cj;
+      if (!isfinite(Cj)) v[3] += 1.0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && flag) v[3] += (double)(*flag);
+  block_reduce_and_publish<4>(v, blockpart, ticket, out_dev, nullptr);
+}
+cudaError_t launch_nc2_trial(const double* rowpart, int nct, const double* colpart, int nrt, int64_t nrows, int64_t n,
+                             const double* rho_r, const double* sig_c, const double* p, const int* flag,
+                             double* blockpart, unsigned int* ticket, double* out_dev, cudaStream_t st) {
+  const int64_t items = nrows + n;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 296));
+  k_nc2_trial<<<blocks, 256, 0, st>>>(rowpart, nct, colpart, nrt, nrows, n, rho_r, sig_c, p, flag, blockpart, ticket,
+                                      out_dev);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dots(int64_t n, int npairs, const double* const* xs, const double* const* ys,
                         double* blockpart, unsigned int* ticket, double* out_dev, double* out_host,
                         cudaStream_t st) {

@@ -301,7 +301,61 @@ void Workspace::release() {
 // One evaluation at the parameters last written by prep: fast fp32 kernel,
 // finalize, and (if the range guard fires) the exact fp64 re-evaluation.
 // ---------------------------------------------------------------------------
-mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcur, double* sc) {
+mdot_status Workspace::launch_eval() {
+  if (time_kernels) CK(cudaEventRecord(ev0, st));
+  if (use_tma) {
+    CKL(launch_eval_tma(tmap, eval, tma_grid, st));
+  } else {
+    CKL(launch_eval_fast(eval, kind_fast, st));
+  }
+  if (time_kernels) CK(cudaEventRecord(ev1, st));
+  return MDOT_OK;
+}
+
+// NC2 trial: phi'(alpha) = <p, m(alpha)> - <p, (r, c)> and the
+// mass are linear in the marginals, so each rank's partial totals contribute
+// additively; 4 scalars are reduced over the ranks (both
+// teams on a 2-D grid) and the partials stay in place for the completion of
+// an accepted trial (evaluate with skip_k1).
+mdot_status Workspace::nc2_trial(double* q) {
+  evals++;
+  CKS(launch_eval());
+  CKL(launch_nc2_trial(rowpart, eval.n_col_tiles, colpart, eval.n_row_tiles, nrows, n, rho_r, sig_c, p, flag,
+                       blockpart, ticket, scal_dev, st));
+  CKS(comm_allreduce(comm, scal_dev, 4, COMM_SUM, st));
+  if (two_d()) CKS(comm_allreduce(comm_row, scal_dev, 4, COMM_SUM, st));
+  CK(cudaMemcpyAsync(q, scal_dev, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (time_kernels) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    kernel_ms += ms;
+    kernel_launches++;
+  }
+  return MDOT_OK;
+}
+
+mdot_status Workspace::nc2_prc(double* prc) {
+  // rows: distinct over the ranks of `comm`; columns: replicated (1-D) or
+  // distinct over the row team (2-D)
+  const double* xr = p;
+  const double* yr = r;
+  CKL(launch_dots(nrows, 1, &xr, &yr, blockpart, ticket, scal_dev, scal_host_dev, st));
+  CKS(comm_allreduce(comm, scal_dev, 1, COMM_SUM, st));
+  double a = 0.0, b = 0.0;
+  CK(cudaMemcpyAsync(&a, scal_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double* xc = p + nrows;
+  const double* yc = c;
+  CKL(launch_dots(n, 1, &xc, &yc, blockpart, ticket, scal_dev, scal_host_dev, st));
+  if (two_d()) CKS(comm_allreduce(comm_row, scal_dev, 1, COMM_SUM, st));
+  CK(cudaMemcpyAsync(&b, scal_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *prc = a + b;
+  return MDOT_OK;
+}
+
+mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcur, double* sc, bool skip_k1) {
   FinalizeArgs f{};
   f.n = n; f.nrows = nrows;
   f.rho_r = rho_r; f.sig_c = sig_c;
@@ -313,15 +367,9 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
   f.prep_flag = flag;
   f.jacobi = jacobi;
   const bool shard = sharded();
-  evals++;
+  if (!skip_k1) evals++;
   if (!exact_mode) {
-    if (time_kernels) CK(cudaEventRecord(ev0, st));
-    if (use_tma) {
-      CKL(launch_eval_tma(tmap, eval, tma_grid, st));
-    } else {
-      CKL(launch_eval_fast(eval, kind_fast, st));
-    }
-    if (time_kernels) CK(cudaEventRecord(ev1, st));
+    if (!skip_k1) CKS(launch_eval());
     f.from_partials = 1;
     f.rowpart = rowpart; f.n_col_tiles = eval.n_col_tiles;
     f.colpart = colpart; f.n_row_tiles = eval.n_row_tiles;
@@ -377,7 +425,7 @@ mdot_status Workspace::evaluate(Marg* out, const double* gcur, const double* pcu
       CKL(launch_finalize(fc, st));
     }
     CK(cudaStreamSynchronize(st));
-    if (time_kernels) {
+    if (time_kernels && !skip_k1) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, ev0, ev1));
       kernel_ms += ms;
@@ -560,18 +608,45 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
     CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, beta, dir, nullptr, nullptr));
     int accepted = 0, attempt = 0, trials = 0;
     double dphi_a = 0, dval = 0;
+    // NC2: <p, (r, c)> once per direction; trials exchange 4 scalars
+    double prc = 0.0;
+    if (w.nc2) CKS(w.nc2_prc(&prc));
     while (!accepted && attempt < 2) {
       double lo = 0.0, dlo = dphi0, hi = 0.0, dhi = 0.0;
       int have_hi = 0, doublings = 0;
       for (int tr = 0; tr < o.ls_max_trials; ++tr) {
         if (tr > 0) CKS(w.prep(PREP_TRIAL, alpha, 0, nullptr, nullptr, nullptr));
-        CKS(w.evaluate(w.trial, w.cur->g, w.p, ts));
+        bool partial = false;   // NC2 trial: only the line-search scalars are known
+        if (w.nc2) {
+          double q[4];
+          CKS(w.nc2_trial(q));
+          if (q[3] == 0.0 && std::isfinite(q[0] + q[1] + q[2])) {
+            partial = true;
+            dphi_a = q[0] + q[2] - prc;                            // phi'(alpha) = <p, m(alpha)> - <p, (r, c)>
+            dval = (q[1] - mass) - alpha * prc;
+          } else {
+            w.evals--;                                             // re-done in full below
+          }
+        }
+        if (!partial) {
+          CKS(w.evaluate(w.trial, w.cur->g, w.p, ts));
+          dphi_a = ts[SC_PCG];                                     // phi'(alpha)
+          dval = (ts[SC_MASS] - mass) - alpha * ts[SC_PRC];
+        }
         res->ls_evaluations++;
         trials++;
-        dphi_a = ts[SC_PCG];                                       // phi'(alpha)
-        dval = (ts[SC_MASS] - mass) - alpha * ts[SC_PRC];
-        const int wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
-        const int decrease = dval <= noise * std::max(1.0, mass);
+        int wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
+        int decrease = dval <= noise * std::max(1.0, mass);
+        if (wolfe && decrease && partial) {
+          // complete the accepted trial from its kept partials (the vector
+          // exchange + finalize); re-test with the full scalars, which may
+          // come from the exact evaluator if the range guard fires
+          CKS(w.evaluate(w.trial, w.cur->g, w.p, ts, true));
+          dphi_a = ts[SC_PCG];
+          dval = (ts[SC_MASS] - mass) - alpha * ts[SC_PRC];
+          wolfe = ((2.0 * c1 - 1.0) * dphi0 >= dphi_a) && (dphi_a >= c2 * dphi0);
+          decrease = dval <= noise * std::max(1.0, mass);
+        }
         if (wolfe && decrease) { accepted = 1; break; }
         if (dphi_a < 0.0 && decrease) { lo = alpha; dlo = dphi_a; }
         else { hi = alpha; dhi = dphi_a; have_hi = 1; }
@@ -592,7 +667,10 @@ mdot_status project_pncg(Workspace& w, const mdot_options& o, int t, mdot_result
       alpha = 1.0;
       beta = 0.0;
       reset = 1;
-      if (attempt < 2) CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, 0.0, dir, nullptr, nullptr));
+      if (attempt < 2) {
+        CKS(w.prep(PREP_NEWDIR | PREP_TRIAL, alpha, 0.0, dir, nullptr, nullptr));
+        if (w.nc2) CKS(w.nc2_prc(&prc));   // the restart direction p = -s
+      }
     }
     if (!accepted) {
       set_error("line search failed twice at MD step %d, iteration %lld", t, (long long)k);
@@ -1409,6 +1487,12 @@ mdot_status Workspace::setup(const mdot_options& o) {
   // that resolution (the same rule as the batched solver, mdot_solve_batch)
   exact_mode = (o.precision == MDOT_PREC_F64P) || (o.precision == MDOT_PREC_AUTO && (c_f64 || o.eps < 5e-8));
   jacobi = o.projector == MDOT_PROJ_PNCG_JACOBI;
+  // NC2 scalar-only trials: sharded host loop, fp32 entries, opt-in
+  // (a net loss at the BASELINE sizes on the fused path)
+  {
+    const char* e = getenv("MDOT_NC2");
+    nc2 = e && atoi(e) == 1 && (sharded() || two_d()) && !exact_mode;
+  }
   if (!exact_mode && c_f64) {
     set_error("fp32-entry precision requested for an fp64 cost; use MDOT_PREC_F64P or AUTO");
     return MDOT_EINVAL;

@@ -146,7 +146,16 @@ struct Workspace {
   void set_gamma(double gb);
   mdot_status prep(int mode, double alpha, double beta, const double* s_dir, const double* Ain,
                    const double* Bin);
-  mdot_status evaluate(Marg* out, const double* gcur, const double* pcur, double* sc);
+  // skip_k1: the fp32-entry partials of this point are already in
+  // rowpart / colpart (an NC2 trial being completed)
+  mdot_status evaluate(Marg* out, const double* gcur, const double* pcur, double* sc, bool skip_k1 = false);
+  // NC2 scalar-only line-search trials (MDOT_NC2=1, sharded host
+  // loop): K1 + this rank's contributions to phi'(alpha) and the mass, summed
+  // over the ranks as 4 scalars instead of the column (and row) vectors
+  bool nc2 = false;
+  mdot_status nc2_trial(double* q);          // q[4]: sum p R 2^rho, sum R 2^rho, sum p C 2^sig, bad
+  mdot_status nc2_prc(double* prc);          // <p, (r, c)> over the whole problem
+  mdot_status launch_eval();                 // the fp32-entry K1 / K2 pass of evaluate
   mdot_status gauge_center(double* X, double* Y);
   mdot_status round_and_cost(float* P_out_dev, double* cost_F, double* cost_G);
 };

@@ -244,3 +244,74 @@ def test_2d_nccl_teams_one_rank(dc, monkeypatch):
     assert abs(res["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]
     lr, lc, _ = O.log_marginals(prob, U.cpu().numpy(), V.cpu().numpy(), gb)
     assert np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum() <= 2 * eps
+
+
+# ------------------------------------------------------------------ NC2
+def _solve_1d(inst, G, sched, opts_kw, tag):
+    n = inst.n
+    rows = np.array_split(np.arange(n), G)
+    out = {}
+    err = []
+
+    def run(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                r0, nr = int(rows[k][0]), len(rows[k])
+                U = torch.empty(nr, dtype=torch.float64, device=DEV)
+                V = torch.empty(n, dtype=torch.float64, device=DEV)
+                cm = M.mdot_comm_create_local(tag, G, k, 0)
+                res = M.mdot_solve_sharded(cm, r0, nr, _t(inst.C[r0:r0 + nr]), _t(inst.r), _t(inst.c), n=n,
+                                           schedule=sched, options=M.options(**opts_kw), u_local_out=U, v_out=V)
+                s.synchronize()
+                M.mdot_comm_destroy(cm)
+                out[k] = (res, U.cpu().numpy(), V.cpu().numpy())
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    ths = [threading.Thread(target=run, args=(k,)) for k in range(G)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    if err:
+        raise err[0]
+    return out
+
+
+@pytest.mark.parametrize("layout", ["1d3", "2d22"])
+def test_nc2_scalar_only_trials(layout, monkeypatch):
+    """NC2 (MDOT_NC2=1, sharded host loop): a line-search trial
+    exchanges 4 scalars -- each rank's contributions to phi'(alpha) and the
+    mass, linear in its partial marginals -- and only an
+    accepted trial's row / column vectors are reduced (evaluate from the kept
+    partials).  Same gates as the vector-per-trial path: identical decisions on
+    every rank, Z20 cost gate against the single-GPU solve, oracle L1 <= 2 eps,
+    and the accepted-trial count equal to the iteration count."""
+    monkeypatch.setenv("MDOT_NC2", "1")
+    n = 600
+    inst = S.uniform_points_instance(3, n, 2, 36, marg="dirichlet")
+    gb, eps = 512.0, 1e-6
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=2)
+    kw = {"eps": eps}
+    if layout == "1d3":
+        out = _solve_1d(inst, 3, sched, kw, "nc2_1d3")
+        res = [o[0] for o in out.values()]
+        U = np.concatenate([out[k][1] for k in range(3)])
+        V = out[0][2]
+    else:
+        o2, _, _ = _solve_2d(inst, 2, 2, sched, kw, "nc2_2d22")
+        res = [o[0] for o in o2.values()]
+        U = np.concatenate([o2[(a, 0)][1] for a in range(2)])
+        V = np.concatenate([o2[(0, b)][2] for b in range(2)])
+    r0 = res[0]
+    assert all(x["status"] == 0 for x in res)
+    assert all(x["evaluations"] == r0["evaluations"] and x["cost_unrounded"] == r0["cost_unrounded"] for x in res)
+    assert r0["l1_final"] <= eps
+    ref = M.mdot_solve(_t(inst.C), _t(inst.r), _t(inst.c), schedule=sched, options=M.options(eps=eps))
+    assert abs(r0["cost_unrounded"] - ref["cost_unrounded"]) <= COST_GATE * ref["cost_unrounded"]
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, U, V, gb)
+    assert np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum() <= 2 * eps
+    rp = O.round_plan(prob, U, V, gb)
+    assert abs(r0["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]

@@ -315,3 +315,36 @@ def test_nc2_scalar_only_trials(layout, monkeypatch):
     assert np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum() <= 2 * eps
     rp = O.round_plan(prob, U, V, gb)
     assert abs(r0["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]
+
+
+def test_2d_grid_config4_full_size():
+    """Config 4 at its BASELINE size and parameters (n = 16384, 1 GiB fp32 C,
+    Dirichlet(1), gbar 4096, T 16, L1 1e-6) on a 2 x 2 grid of 8192 x 8192
+    blocks: identical decisions on every rank, the oracle's full fp64
+    re-evaluation of the assembled (U, V) at L1 <= 2 eps, the unrounded cost
+    within the Z20 gate of the stored full oracle solve (tests/golden), and the
+    rounded / unrounded costs equal to the oracle's rounding of the same
+    potentials to 1e-10."""
+    import json
+    import os
+    inst = S.config4(0)
+    n = inst.n
+    gb, eps = 4096.0, 1e-6
+    sched = M.schedule(M.MDOT_SCHED_FIXED, gb, T=16)
+    out, _, _ = _solve_2d(inst, 2, 2, sched, {"eps": eps}, "g2d_cfg4")
+    r00 = out[(0, 0)][0]
+    assert all(o[0]["status"] == 0 for o in out.values()), [(k, o[0]["status_name"], o[3]) for k, o in out.items()]
+    assert all(o[0]["evaluations"] == r00["evaluations"] for o in out.values())
+    assert all(o[0]["cost_rounded"] == r00["cost_rounded"] for o in out.values())
+    assert r00["l1_final"] <= eps
+    U = np.concatenate([out[(a, 0)][1] for a in range(2)])
+    V = np.concatenate([out[(0, b)][2] for b in range(2)])
+    prob = O.OracleProblem(inst)
+    lr, lc, _ = O.log_marginals(prob, U, V, gb)
+    assert np.abs(np.exp(lr) - inst.r).sum() + np.abs(np.exp(lc) - inst.c).sum() <= 2 * eps
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg4_seed0.json")))
+    gc = golden["cost_unrounded"]
+    assert abs(r00["cost_unrounded"] - gc) <= COST_GATE * gc, (r00["cost_unrounded"], gc)
+    rp = O.round_plan(prob, U, V, gb)
+    assert abs(r00["cost_unrounded"] - rp["cost_F"]) <= 1e-10 * rp["cost_F"]
+    assert abs(r00["cost_rounded"] - rp["cost_G"]) <= 1e-10 * rp["cost_G"]

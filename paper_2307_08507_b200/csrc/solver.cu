@@ -2115,7 +2115,118 @@ static mdot_status solve_batch_lockstep(const mdot_problem* shared, int32_t Bn, 
   int64_t launches = 0;
   double gb = 0.0, gprev = 0.0;
   std::vector<mdot_status> sts((size_t)Bn, MDOT_OK);
-  for (size_t t = 1; t <= gam.size() && stt == MDOT_OK; ++t) {
+  // Decoupled MD steps (default): an instance whose projection has converged
+  // starts its next MD step at once (own gamma, warm start, controller reset
+  // and its initial evaluation on its own slot body) instead of waiting for
+  // the slowest instance of the batch, so the shared-C slots stay full; each
+  // instance still takes exactly the decisions of its own device-control solve.
+  // MDOT_BATCH_SYNC_MD=1: every instance changes step together (A/B).
+  const bool sync_md = getenv("MDOT_BATCH_SYNC_MD") && atoi(getenv("MDOT_BATCH_SYNC_MD")) == 1;
+  if (!sync_md) {
+    std::vector<size_t> tb((size_t)Bn, 0);
+    std::vector<double> gbb((size_t)Bn, 0.0);
+    std::vector<char> fin((size_t)Bn, 0);
+    auto begin_step = [&](int32_t b) -> mdot_status {
+      Workspace& w = *W[b];
+      const size_t t = ++tb[b];
+      const double gt = gam[t - 1];
+      const double gp = t > 1 ? gam[t - 2] : 0.0;
+      gbb[b] += gt;
+      const bool last = t == gam.size();
+      w.set_gamma(gbb[b]);
+      if (o.warm == MDOT_WARM_ZERO) {
+        launch_fill(n, 0.0, w.u, stream);
+        launch_fill(n, 0.0, w.v, stream);
+      } else if (o.warm == MDOT_WARM_SCALED && t > 1 && gt != gp) {
+        launch_axpby(n, 0.0, w.u, gt / gp, w.u, stream);
+        launch_axpby(n, 0.0, w.v, gt / gp, w.v, stream);
+      }
+      CtrlState h{};
+      h.eps = (!last && o.eps_md > o.eps) ? o.eps_md : o.eps;
+      h.c1 = o.c1; h.c2 = o.c2;
+      h.noise = ls_noise(false, gbb[b]);
+      h.stop_rho = o.stop; h.ncg = o.projector == MDOT_PROJ_NCG; h.sinkhorn = o.projector == MDOT_PROJ_SINKHORN;
+      h.beta_kind = o.beta; h.ls_max_trials = o.ls_max_trials;
+      h.max_evals = o.max_evals - w.evals;
+      h.gpair[0] = w.eval.gh; h.gpair[1] = w.eval.gl;
+      h.mode = PREP_CUR; h.phase = 0; h.alpha_prev = 1.0;
+      h.md_t = (int)t;
+      CK(cudaMemcpyAsync(w.ctrl, &h, sizeof(h), cudaMemcpyHostToDevice, stream));
+      done_h[b] = 0;
+      CKS(w.launch_slot_body(stream, 0, false));   // this instance's initial evaluation
+      launches += 3;
+      return MDOT_OK;
+    };
+    auto end_step = [&](int32_t b) -> mdot_status {
+      Workspace& w = *W[b];
+      const size_t t = tb[b];
+      const double gt = gam[t - 1];
+      const bool last = t == gam.size();
+      CtrlState h{};
+      CK(cudaMemcpyAsync(&h, w.ctrl, sizeof(h), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      mdot_result* R = &res[b];
+      w.evals += h.evals;
+      R->iterations += h.iterations;
+      R->ls_evaluations += h.ls_evals;
+      R->resets += h.resets;
+      R->ls_restarts += h.restarts;
+      if (t <= 64) {
+        R->rho0[t - 1] = h.rho_0;
+        R->l10[t - 1] = h.l1_0;
+        R->iters_step[t - 1] += h.iterations;
+        R->gammas[t - 1] = gt;
+      }
+      R->l1_final = h.l1;
+      R->rho_final = h.rho;
+      R->md_steps = (int64_t)t;
+      R->control_path = 4;
+      mdot_options ot = o;
+      if (!last && o.eps_md > o.eps) ot.eps = o.eps_md;
+      w.md_last = last;
+      mdot_status ps = MDOT_OK;
+      if (h.status == CTRL_NOCONV) ps = MDOT_ENOCONV;
+      else if (h.status == CTRL_LS_FAIL) {
+        set_error("instance %d: line search failed twice at MD step %d (lockstep batch)", (int)b, (int)t);
+        ps = MDOT_ELINESEARCH;
+      } else if (h.status == CTRL_NEED_HOST) {
+        w.fallbacks++;
+        ps = (o.projector == MDOT_PROJ_SINKHORN) ? project_sinkhorn(w, ot, (int)t, R) : project_pncg(w, ot, (int)t, R);
+      }
+      launch_axpby(n, 1.0, w.u, 1.0, w.U, stream);   // U += u
+      launch_axpby(n, 1.0, w.v, 1.0, w.V, stream);
+      if (ps != MDOT_OK && ps != MDOT_ENOCONV) { sts[b] = ps; return MDOT_OK; }
+      mdot_status gs = w.gauge_center(w.U, w.V);
+      if (gs == MDOT_OK) gs = w.gauge_center(w.u, w.v);
+      if (gs != MDOT_OK) return gs;
+      if (ps == MDOT_ENOCONV) sts[b] = ps;
+      return MDOT_OK;
+    };
+    for (int32_t b = 0; b < Bn && stt == MDOT_OK; ++b) stt = begin_step(b);
+    while (stt == MDOT_OK) {
+      bool any = false;
+      for (int32_t b = 0; b < Bn; ++b) any = any || !fin[b];
+      if (!any) break;
+      CK(cudaGraphLaunch(gexec, stream));
+      launches += 4 * (int64_t)K;
+      CK(cudaStreamSynchronize(stream));
+      for (int32_t b = 0; b < Bn && stt == MDOT_OK; ++b) {
+        if (fin[b] || !((volatile int*)done_h)[b]) continue;
+        stt = end_step(b);
+        if (stt != MDOT_OK) break;
+        if (sts[b] != MDOT_OK || tb[b] == gam.size()) {
+          fin[b] = 1;
+          const int one = 1;   // sits out the remaining graphs
+          CK(cudaMemcpyAsync(&W[b]->ctrl->done, &one, sizeof(int), cudaMemcpyHostToDevice, stream));
+          done_h[b] = 1;
+        } else {
+          stt = begin_step(b);
+        }
+      }
+    }
+    for (double g : gam) gb += g;
+  }
+  for (size_t t = 1; sync_md && t <= gam.size() && stt == MDOT_OK; ++t) {
     const double gt = gam[t - 1];
     gb += gt;
     const bool last = t == gam.size();

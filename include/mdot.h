@@ -214,8 +214,14 @@ mdot_status mdot_sinkhorn(const mdot_problem* pb, const mdot_schedule* sched, co
  * Dense fp32 costs whose per-instance state fits in one SM's shared memory
  * (n <= 784 on B200) run on the K8 kernel: one CTA per instance executes the
  * whole solve on-chip, C shared through L2.  precision AUTO uses fp64 entries
- * when eps < 5e-8.  Other costs fall back to one solve per instance.
- * Returns the first non-OK status (all instances run). */
+ * when eps < 5e-8.  Larger instances (throughput mode)
+ * run concurrently on worker streams (MDOT_BATCH_WORKERS, default 8), or, with
+ * environment MDOT_BATCH_LOCKSTEP=1 and a shared dense fp32 C on the device,
+ * as a lockstep batch: one launch per phase for every instance, one streamed
+ * copy of each C tile evaluated by every active instance (k_eval_tma_shared),
+ * MD steps decoupled per instance (MDOT_BATCH_SYNC_MD=1: step-synchronous);
+ * the two are measured at parity.  Returns the
+ * first non-OK status (all instances run). */
 mdot_status mdot_solve_batch(const mdot_problem* shared, int32_t B, const double* r, const double* c,
                              const mdot_schedule* sched, const mdot_options* opt,
                              double* u_out, double* v_out, mdot_result* res);

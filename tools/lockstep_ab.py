@@ -1,4 +1,4 @@
-"""Throughput mode A/B (16 x n = 4096 sharing one C, config-3 shape, gbar 4096,
+"""Throughput mode A/B (B = TP_B (16) x n = 4096 sharing one C, config-3 shape, gbar 4096,
 T 16, L1 1e-6): lockstep batch with decoupled MD steps (MDOT_BATCH_LOCKSTEP=1),
 lockstep with synchronous MD steps (+ MDOT_BATCH_SYNC_MD=1), worker streams
 (default path); three interleaved rounds, host wall clock per batch after a
@@ -17,7 +17,8 @@ import synthetic as S  # noqa: E402
 t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
 base = S.config3(0, frac=0.9)
 C = t(base.C)
-pairs = [S.config3(i, frac=0.9) for i in range(16)]
+B = int(os.environ.get("TP_B", "16"))   # the paper runs 32 instances per point
+pairs = [S.config3(i, frac=0.9) for i in range(B)]
 Rb = t(np.stack([p.r for p in pairs]))
 Cb = t(np.stack([p.c for p in pairs]))
 sched = M.schedule(M.MDOT_SCHED_FIXED, 4096.0, T=16)
@@ -51,5 +52,5 @@ for em in (1e-3, 0.0):
                       f"max L1 {max(o['l1_final'] for o in out):.2e}", flush=True)
     for name in VARIANTS:
         ts = times[name]
-        print(f"eps_md {em:g} {name:20s} ms per batch: " + " ".join(f"{x:7.1f}" for x in ts)
+        print(f"B {B} eps_md {em:g} {name:20s} ms per batch: " + " ".join(f"{x:7.1f}" for x in ts)
               + f"   median {sorted(ts)[1]:7.1f}", flush=True)

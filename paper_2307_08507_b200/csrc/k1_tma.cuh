@@ -356,6 +356,13 @@ __device__ __forceinline__ void tma_consume_tile(TmaSmem& sm, const EvalArgs& a,
 // complete per (row, column tile) after the 4-row butterfly, as in
 // tma_consume_tile.  Lane l holds stage row l's parameters (one load per stage)
 // and broadcasts them with shuffles.
+#ifndef MDOT_SHARED_UNROLL
+#define MDOT_SHARED_UNROLL 8
+#endif
+// 4-row group loop of the shared-C consumer, fully unrolled: lockstep batch
+// 518.9 -> 507.8 ms (16 x n = 4096, paper protocol; identical evaluations;
+// profiles/r02_shared_unroll_ab.txt); MDOT_SHARED_UNROLL=1: A/B
+constexpr int kSharedUnroll = MDOT_SHARED_UNROLL;
 __device__ __forceinline__ void tma_consume_tile_shared(TmaSmem& sm, const EvalArgs& a, int b, uint32_t& it,
                                                         int64_t tile) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -403,7 +410,7 @@ __device__ __forceinline__ void tma_consume_tile_shared(TmaSmem& sm, const EvalA
     const int64_t irow = i0 + (int64_t)k * kTmaRows + lane;
     const float4 rq = (irow < nrows) ? __ldg(&a.rowp[irow]) : none;
     mbar_wait(&sm.full[s], ph);
-#pragma unroll 1
+#pragma unroll kSharedUnroll
     for (int g = 0; g < kTmaRows / 4; ++g) {
       float rs[4];
 #pragma unroll

@@ -405,10 +405,16 @@ __device__ __forceinline__ void tma_consume_tile_shared(TmaSmem& sm, const EvalA
   u64 cacc2[4] = {0ull, 0ull, 0ull, 0ull};
   int grp = 0;
   const float4 none = make_float4(-1.0e30f, 0.f, 0.f, 0.f);
+  // row parameters one stage ahead (their L2 latency was the top stall:
+  // long scoreboard 2.5 warps per issue, profiles/r02_shared_k1_ncu.md)
+  float4 rq_next = (i0 + lane < nrows) ? __ldg(&a.rowp[i0 + lane]) : none;
   for (int k = 0; k < nst; ++k, ++it) {
     const uint32_t s = it % kTmaStages, ph = (it / kTmaStages) & 1u;
-    const int64_t irow = i0 + (int64_t)k * kTmaRows + lane;
-    const float4 rq = (irow < nrows) ? __ldg(&a.rowp[irow]) : none;
+    const float4 rq = rq_next;
+    if (k + 1 < nst) {
+      const int64_t irow = i0 + (int64_t)(k + 1) * kTmaRows + lane;
+      rq_next = (irow < nrows) ? __ldg(&a.rowp[irow]) : none;
+    }
     mbar_wait(&sm.full[s], ph);
 #pragma unroll kSharedUnroll
     for (int g = 0; g < kTmaRows / 4; ++g) {
